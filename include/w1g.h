@@ -1,0 +1,153 @@
+/*
+ * w1g.h -- C ABI of libw1g.so, the B200 (sm_100a) sparsify front-end of
+ * PDoptFlow (arXiv 2110.14734).
+ *
+ * The reference (w1flow, /root/reference/pkg/src/w1flow) has no FFI layer:
+ * its "operator API" is the set of module-level Python stage functions that
+ * approx_w1 calls in order (pipeline.py:105-130).  Each entry point below
+ * replaces one of them; the ctypes stub that binds them is
+ * paper_2110_14734_b200/_lib.py.
+ *
+ * Conventions
+ *  - every call returns W1G_OK (0) or a negative W1G_E* code; a message is
+ *    kept per host thread (w1g_last_error);
+ *  - one context = one device + one CUDA stream + device-resident stage
+ *    state; a context is not thread-safe, use one host thread per context;
+ *  - data-dependent outputs are two-phase: a stage call returns sizes, a
+ *    w1g_fetch_* call copies into caller-owned host arrays of those sizes;
+ *  - host arrays are C-contiguous: points (n,2) float64 as x0,y0,x1,y1,...;
+ *    indices, masses, supplies int64; costs float64 (the reference dtypes).
+ */
+#ifndef W1G_H
+#define W1G_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define W1G_OK 0
+#define W1G_EINVAL (-1)     /* bad argument (maps to ValueError) */
+#define W1G_ECUDA (-2)      /* CUDA runtime failure (RuntimeError) */
+#define W1G_EOVERFLOW (-3)  /* lattice pitch too small, condensation.py:75-76 (ValueError) */
+#define W1G_EDUPLICATE (-4) /* split tree duplicate points, spanner.py:134-135 (ValueError) */
+#define W1G_ECOUNT (-5)     /* WSPD write pass != counted offsets, spanner.py:259-260 (AssertionError) */
+#define W1G_ENETWORK (-6)   /* build_network validation, network.py:56-68 (NetworkError) */
+#define W1G_ENOMEM (-7)     /* device allocation failed (MemoryError) */
+#define W1G_ESTATE (-8)     /* stage called before its inputs exist (RuntimeError) */
+
+/* node-set slots held by a context */
+#define W1G_NODES0 0 /* output of zero_condense */
+#define W1G_NODES 1  /* output of delta_condense (or nodes0 when delta == 0) */
+
+typedef struct w1g_ctx w1g_ctx;
+
+/* per-stage result of the fused front end (pipeline.py:98-132) */
+typedef struct {
+    int64_t n_points0;      /* K0: nodes after zero_condense */
+    int64_t n_points;       /* K: nodes after delta_condense */
+    int64_t n_tree_nodes;   /* 2K-1 */
+    int64_t n_pairs;        /* WSPD pairs P */
+    int64_t n_arcs;         /* network arcs M (after dedup) */
+    int64_t node_count;     /* K + 2 */
+    double lower_bound;     /* RWMD L = max(L_A, L_B) */
+    double lower_bound_a;   /* L_A */
+    double lower_bound_b;   /* L_B */
+    double epsilon_condense;/* pipeline.py:67-69 */
+    double delta;           /* lattice pitch parameter used (0 = no condensation) */
+    int32_t short_circuit;  /* empty input or a_mass == b_mass (pipeline.py:106-109) */
+    int32_t tree_depth;     /* split tree levels */
+    int32_t n_levels_wspd;  /* WSPD frontier levels */
+    int32_t pad;
+    float stage_ms[8];      /* device time per stage: zc, rwmd, dc, tree, wspd, emit, csr, total */
+} w1g_front_end_info;
+
+int w1g_version(void);
+/* number of CUDA kernels this library has launched (process-wide) */
+uint64_t w1g_launch_count(void);
+/* measurement hook: time `reps` launches of the FP32 all-pairs RWMD tile
+ * kernel (A->B then B->A, culling as configured) on the context's nodes0 with
+ * CUDA events on the context stream; returns the mean device time per launch
+ * and the directed (source, target) evaluations one launch covers */
+int w1g_profile_rwmd_tile(w1g_ctx *ctx, int reps, float *ms_per_launch, int64_t *evals_per_launch);
+int w1g_device_count(int *count);
+const char *w1g_last_error(void);
+
+int w1g_ctx_create(int device, w1g_ctx **out);
+int w1g_ctx_destroy(w1g_ctx *ctx);
+/* the CUDA stream the context launches on (cudaStream_t), for event timing */
+void *w1g_ctx_stream(w1g_ctx *ctx);
+int w1g_synchronize(w1g_ctx *ctx);
+
+/* replaces diagram.zero_condense, diagram.py:190-208 -> slot W1G_NODES0 */
+int w1g_zero_condense(w1g_ctx *ctx, const double *a, int64_t na, const double *b, int64_t nb,
+                      int64_t *k0, int32_t *balanced);
+/* device-resident variant: a/b already in device memory (bench "value" leg) */
+int w1g_zero_condense_device(w1g_ctx *ctx, const double *d_a, int64_t na, const double *d_b,
+                             int64_t nb, int64_t *k0, int32_t *balanced);
+/* upload an arbitrary SuppliedNodes (diagram.py:150-187) into a slot */
+int w1g_load_nodes(w1g_ctx *ctx, int slot, const double *points, const int64_t *a_mass,
+                   const int64_t *b_mass, int64_t k, int64_t abar_supply, int64_t bbar_supply);
+int w1g_nodes_size(w1g_ctx *ctx, int slot, int64_t *k);
+int w1g_fetch_nodes(w1g_ctx *ctx, int slot, double *points, int64_t *a_mass, int64_t *b_mass);
+
+/* replaces lower_bound.rwmd, lower_bound.py:61-75, on slot W1G_NODES0 */
+int w1g_rwmd(w1g_ctx *ctx, double *L, double *LA, double *LB);
+/* per-source best distance min(nn, diag) for one side (0 = A, 1 = B), node order */
+int w1g_fetch_rwmd_best(w1g_ctx *ctx, int side, double *best, int64_t *n);
+/* tile culling in the FP32 all-pairs pass: 1 (default) or 0 (full brute force) */
+int w1g_set_rwmd_culling(w1g_ctx *ctx, int enabled);
+
+/* replaces condensation.delta_condense, condensation.py:105-124: NODES0 -> NODES.
+ * pitch = k*delta, half_width = (1-k)*delta/2 as computed by the caller
+ * (condensation.py:73,121); delta == 0 copies NODES0 to NODES. */
+int w1g_delta_condense(w1g_ctx *ctx, double delta, double pitch, double half_width,
+                       uint64_t seed, int64_t *k);
+
+/* replaces spanner.build_split_tree, spanner.py:96-159, over a slot's points */
+int w1g_split_tree(w1g_ctx *ctx, int slot, int64_t *n_nodes, int32_t *depth);
+int w1g_fetch_tree(w1g_ctx *ctx, int64_t *left, int64_t *right, double *bbox, int64_t *rep,
+                   int64_t *size);
+/* upload a SplitTree (spanner.py:37-64) for a standalone build_wspd */
+int w1g_load_tree(w1g_ctx *ctx, const double *points, int64_t n_points, const int64_t *left,
+                  const int64_t *right, const double *bbox, const int64_t *rep, int64_t n_nodes);
+
+/* replaces spanner.build_wspd / count_pairs / write_pairs, spanner.py:263-307.
+ * reference_order = 1 sorts pairs into the reference layout (owner ascending,
+ * DFS pop order); 0 leaves them in frontier order (the fused path). */
+int w1g_wspd(w1g_ctx *ctx, double s, int reference_order, int64_t *n_pairs);
+int w1g_fetch_pairs(w1g_ctx *ctx, int64_t *node_pairs, int64_t *indices);
+/* pairs per internal node, internal nodes in id order (count_pairs output) */
+int w1g_fetch_pair_counts(w1g_ctx *ctx, int64_t *counts, int64_t *n_internal);
+/* upload WSPairList.indices and .points (spanner.py:67-81) for a standalone emit_arcs */
+int w1g_load_pairs(w1g_ctx *ctx, const int64_t *indices, int64_t n_pairs, const double *points,
+                   int64_t n_points);
+
+/* replaces spanner.emit_arcs, spanner.py:310-337, over slot W1G_NODES */
+int w1g_emit_arcs(w1g_ctx *ctx, int64_t *n_arcs);
+int w1g_fetch_arcs(w1g_ctx *ctx, int64_t *tails, int64_t *heads, double *costs);
+int w1g_load_arcs(w1g_ctx *ctx, const int64_t *tails, const int64_t *heads, const double *costs,
+                  int64_t m);
+
+/* replaces network.build_network, network.py:44-85, over the context's arcs */
+int w1g_build_network(w1g_ctx *ctx, const int64_t *supplies, int64_t n, int64_t *n_arcs);
+/* replaces network.assemble, network.py:88-93 (supplies from slot W1G_NODES) */
+int w1g_assemble(w1g_ctx *ctx, int64_t *node_count, int64_t *n_arcs);
+int w1g_fetch_network(w1g_ctx *ctx, int64_t *supplies, int64_t *tails, int64_t *heads,
+                      double *costs, int64_t *row_offsets);
+
+/* fused front end: pipeline.py:105-130 (zero_condense .. assemble).
+ * delta_mode 0: delta from the RWMD bound as the reference (pipeline.py:116-122);
+ * delta_mode 1: the given delta (the fixed-delta chain of test_acceptance.py:224-237). */
+int w1g_front_end(w1g_ctx *ctx, const double *a, int64_t na, const double *b, int64_t nb,
+                  double s, int use_condensation, int delta_mode, double delta, double k,
+                  uint64_t seed, w1g_front_end_info *info);
+int w1g_front_end_device(w1g_ctx *ctx, const double *d_a, int64_t na, const double *d_b,
+                         int64_t nb, double s, int use_condensation, int delta_mode,
+                         double delta, double k, uint64_t seed, w1g_front_end_info *info);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* W1G_H */

@@ -1,0 +1,630 @@
+// capi.cu -- the extern "C" boundary of libw1g.so (include/w1g.h) plus the
+// context, buffer, flag and error plumbing shared by the stage translation
+// units.  Each entry point cites the reference function it replaces.
+#include <cstdarg>
+#include <cstring>
+
+#include "common.cuh"
+
+namespace w1g {
+
+static thread_local char g_err[1024] = "";
+unsigned long long g_launches = 0;
+
+void set_error(const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof g_err, fmt, ap);
+    va_end(ap);
+}
+
+int cuda_fail(cudaError_t e, const char *what, const char *file, int line) {
+    set_error("CUDA error %s (%s) in %s at %s:%d", cudaGetErrorName(e), cudaGetErrorString(e), what,
+              file, line);
+    if (e == cudaErrorMemoryAllocation) return W1G_ENOMEM;
+    return W1G_ECUDA;
+}
+
+int ensure_bytes(DevBuf &b, size_t bytes) {
+    if (bytes <= b.cap) return W1G_OK;
+    size_t want = bytes + bytes / 4 + 4096;
+    if (b.p) {
+        cudaError_t e = cudaFree(b.p);
+        b.p = nullptr;
+        b.cap = 0;
+        if (e != cudaSuccess) return cuda_fail(e, "cudaFree", __FILE__, __LINE__);
+    }
+    cudaError_t e = cudaMalloc(&b.p, want);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        b.p = nullptr;
+        set_error("device allocation of %zu bytes failed: %s", want, cudaGetErrorString(e));
+        return W1G_ENOMEM;
+    }
+    b.cap = want;
+    return W1G_OK;
+}
+
+void free_buf(DevBuf &b) {
+    if (b.p) cudaFree(b.p);
+    b.p = nullptr;
+    b.cap = 0;
+}
+
+int flags_reset(Ctx &c) {
+    W1G_CUDA(cudaMemsetAsync(c.flags.p, 0, sizeof(int64_t) * F_NSLOTS, c.stream));
+    return W1G_OK;
+}
+
+int flags_fetch(Ctx &c, int first, int count) {
+    W1G_CUDA(cudaMemcpyAsync(c.h_pinned + first, dflags(c) + first, sizeof(int64_t) * count,
+                             cudaMemcpyDeviceToHost, c.stream));
+    W1G_CUDA(cudaStreamSynchronize(c.stream));
+    return W1G_OK;
+}
+
+int stage_ensure(Ctx &c, size_t bytes) {
+    if (bytes <= c.h_stage_cap) return W1G_OK;
+    if (c.h_stage) {
+        W1G_CUDA(cudaStreamSynchronize(c.stream));
+        cudaFreeHost(c.h_stage);
+        c.h_stage = nullptr;
+        c.h_stage_cap = 0;
+    }
+    size_t want = bytes + bytes / 4 + 65536;
+    W1G_CUDA(cudaHostAlloc(&c.h_stage, want, cudaHostAllocDefault));
+    c.h_stage_cap = want;
+    return W1G_OK;
+}
+
+int scan_prepare(Ctx &c, int64_t n, ScanArgs *a, int64_t *n_tiles) {
+    int64_t tiles = (n + SCAN_TILE - 1) / SCAN_TILE;
+    if (tiles < 1) tiles = 1;
+    unsigned long long *st;
+    W1G_TRY(ensure(c.scan_state, (size_t)tiles + 8, &st));
+    W1G_CUDA(cudaMemsetAsync(st, 0, sizeof(unsigned long long) * (tiles + 8), c.stream));
+    a->status = st + 8;
+    a->ticket = reinterpret_cast<unsigned int *>(st);
+    *n_tiles = tiles;
+    return W1G_OK;
+}
+
+static int upload(Ctx &c, DevBuf &dst, const void *src, size_t bytes) {
+    void *d;
+    W1G_TRY(ensure(dst, bytes, reinterpret_cast<char **>(&d)));
+    if (bytes) W1G_CUDA(cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, c.stream));
+    return W1G_OK;
+}
+
+static int download(Ctx &c, void *dst, const void *src, size_t bytes) {
+    if (!dst || !bytes) return W1G_OK;
+    W1G_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c.stream));
+    return W1G_OK;
+}
+
+static void invalidate_from_nodes(Ctx &c) {
+    c.tree_valid = false;
+    c.pairs_valid = false;
+    c.arcs_valid = false;
+    c.net_valid = false;
+}
+
+}  // namespace w1g
+
+using namespace w1g;
+
+#define CTX_CHECK(ctx)                                   \
+    do {                                                 \
+        if (!(ctx)) {                                    \
+            set_error("null context");                   \
+            return W1G_EINVAL;                           \
+        }                                                \
+        cudaError_t _e = cudaSetDevice((ctx)->device);   \
+        if (_e != cudaSuccess) return cuda_fail(_e, "cudaSetDevice", __FILE__, __LINE__); \
+    } while (0)
+
+extern "C" {
+
+int w1g_version(void) { return 10000; }
+
+uint64_t w1g_launch_count(void) { return __atomic_load_n(&g_launches, __ATOMIC_RELAXED); }
+
+int w1g_profile_rwmd_tile(w1g_ctx *c, int reps, float *ms_per_launch, int64_t *evals_per_launch) {
+    CTX_CHECK(c);
+    if (!c->nodes[0].valid) {
+        set_error("profile_rwmd_tile: no nodes0");
+        return W1G_ESTATE;
+    }
+    return rwmd_tile_profile(*c, reps, ms_per_launch, evals_per_launch);
+}
+
+const char *w1g_last_error(void) { return g_err; }
+
+int w1g_device_count(int *count) {
+    W1G_CUDA(cudaGetDeviceCount(count));
+    return W1G_OK;
+}
+
+int w1g_ctx_create(int device, w1g_ctx **out) {
+    if (!out) return W1G_EINVAL;
+    *out = nullptr;
+    W1G_CUDA(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    W1G_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10 || prop.minor != 0) {
+        set_error("libw1g targets sm_100a (B200); device %d is sm_%d%d", device, prop.major, prop.minor);
+        return W1G_ECUDA;
+    }
+    w1g_ctx *c = new w1g_ctx();
+    c->device = device;
+    c->sm_count = prop.multiProcessorCount;
+    W1G_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    int64_t *f;
+    W1G_TRY(ensure(c->flags, F_NSLOTS, &f));
+    W1G_CUDA(cudaHostAlloc(&c->h_pinned, sizeof(int64_t) * F_NSLOTS, cudaHostAllocDefault));
+    for (auto &e : c->ev) W1G_CUDA(cudaEventCreate(&e));
+    *out = c;
+    return W1G_OK;
+}
+
+int w1g_ctx_destroy(w1g_ctx *c) {
+    if (!c) return W1G_OK;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    DevBuf *bufs[] = {&c->in_pts, &c->best[0], &c->best[1], &c->tree_pts, &c->t_left, &c->t_right,
+                      &c->t_rep, &c->t_size, &c->t_bbox, &c->t_geom, &c->t_lr, &c->t_rep32,
+                      &c->pair_uv, &c->pair_w, &c->pair_path, &c->pair_idx, &c->pair_counts,
+                      &c->arc_t, &c->arc_h, &c->arc_c, &c->net_sup, &c->net_t, &c->net_h,
+                      &c->net_c, &c->net_ro, &c->scan_state, &c->flags};
+    for (DevBuf *b : bufs) free_buf(*b);
+    for (auto &ns : c->nodes) {
+        free_buf(ns.pts);
+        free_buf(ns.am);
+        free_buf(ns.bm);
+    }
+    for (auto &b : c->scr) free_buf(b);
+    for (auto &b : c->sort_scr) free_buf(b);
+    if (c->h_pinned) cudaFreeHost(c->h_pinned);
+    if (c->h_stage) cudaFreeHost(c->h_stage);
+    for (auto &e : c->ev)
+        if (e) cudaEventDestroy(e);
+    cudaStreamDestroy(c->stream);
+    delete c;
+    return W1G_OK;
+}
+
+void *w1g_ctx_stream(w1g_ctx *c) { return c ? (void *)c->stream : nullptr; }
+
+int w1g_synchronize(w1g_ctx *c) {
+    CTX_CHECK(c);
+    W1G_CUDA(cudaStreamSynchronize(c->stream));
+    return W1G_OK;
+}
+
+// ---------------------------------------------------------------- nodes
+
+int w1g_zero_condense_device(w1g_ctx *c, const double *d_a, int64_t na, const double *d_b,
+                             int64_t nb, int64_t *k0, int32_t *balanced) {
+    CTX_CHECK(c);
+    if (na < 0 || nb < 0 || na + nb >= (1ll << 31)) {
+        set_error("zero_condense: bad sizes na=%lld nb=%lld", (long long)na, (long long)nb);
+        return W1G_EINVAL;
+    }
+    invalidate_from_nodes(*c);
+    c->nodes[1].valid = false;
+    return zc_run(*c, reinterpret_cast<const double2 *>(d_a), na,
+                  reinterpret_cast<const double2 *>(d_b), nb, k0, balanced);
+}
+
+int w1g_zero_condense(w1g_ctx *c, const double *a, int64_t na, const double *b, int64_t nb,
+                      int64_t *k0, int32_t *balanced) {
+    CTX_CHECK(c);
+    if (na < 0 || nb < 0) return W1G_EINVAL;
+    double2 *d;
+    W1G_TRY(ensure(c->in_pts, (size_t)(na + nb), &d));
+    if (na) W1G_CUDA(cudaMemcpyAsync(d, a, sizeof(double2) * na, cudaMemcpyHostToDevice, c->stream));
+    if (nb) W1G_CUDA(cudaMemcpyAsync(d + na, b, sizeof(double2) * nb, cudaMemcpyHostToDevice, c->stream));
+    return w1g_zero_condense_device(c, reinterpret_cast<double *>(d), na,
+                                    reinterpret_cast<double *>(d + na), nb, k0, balanced);
+}
+
+int w1g_load_nodes(w1g_ctx *c, int slot, const double *points, const int64_t *am,
+                   const int64_t *bm, int64_t k, int64_t abar, int64_t bbar) {
+    CTX_CHECK(c);
+    if (slot < 0 || slot > 1 || k < 0 || k >= (1ll << 31)) return W1G_EINVAL;
+    NodeSet &ns = c->nodes[slot];
+    W1G_TRY(upload(*c, ns.pts, points, sizeof(double2) * k));
+    W1G_TRY(upload(*c, ns.am, am, sizeof(int64_t) * k));
+    W1G_TRY(upload(*c, ns.bm, bm, sizeof(int64_t) * k));
+    ns.k = k;
+    ns.valid = true;
+    ns.abar = abar;
+    ns.bbar = bbar;
+    invalidate_from_nodes(*c);
+    if (slot == 0) c->nodes[1].valid = false;
+    return W1G_OK;
+}
+
+int w1g_nodes_size(w1g_ctx *c, int slot, int64_t *k) {
+    CTX_CHECK(c);
+    if (slot < 0 || slot > 1 || !c->nodes[slot].valid) {
+        set_error("node slot %d is empty", slot);
+        return W1G_ESTATE;
+    }
+    *k = c->nodes[slot].k;
+    return W1G_OK;
+}
+
+int w1g_fetch_nodes(w1g_ctx *c, int slot, double *points, int64_t *am, int64_t *bm) {
+    CTX_CHECK(c);
+    if (slot < 0 || slot > 1 || !c->nodes[slot].valid) {
+        set_error("node slot %d is empty", slot);
+        return W1G_ESTATE;
+    }
+    NodeSet &ns = c->nodes[slot];
+    W1G_TRY(download(*c, points, ns.pts.p, sizeof(double2) * ns.k));
+    W1G_TRY(download(*c, am, ns.am.p, sizeof(int64_t) * ns.k));
+    W1G_TRY(download(*c, bm, ns.bm.p, sizeof(int64_t) * ns.k));
+    W1G_CUDA(cudaStreamSynchronize(c->stream));
+    return W1G_OK;
+}
+
+// ---------------------------------------------------------------- rwmd
+
+int w1g_rwmd(w1g_ctx *c, double *L, double *LA, double *LB) {
+    CTX_CHECK(c);
+    if (!c->nodes[0].valid) {
+        set_error("rwmd: no nodes0 (call zero_condense or load_nodes first)");
+        return W1G_ESTATE;
+    }
+    double l, la, lb;
+    W1G_TRY(rwmd_run(*c, &l, &la, &lb));
+    if (L) *L = l;
+    if (LA) *LA = la;
+    if (LB) *LB = lb;
+    return W1G_OK;
+}
+
+int w1g_fetch_rwmd_best(w1g_ctx *c, int side, double *best, int64_t *n) {
+    CTX_CHECK(c);
+    if (side < 0 || side > 1) return W1G_EINVAL;
+    *n = c->n_best[side];
+    if (best) {
+        W1G_TRY(download(*c, best, c->best[side].p, sizeof(double) * c->n_best[side]));
+        W1G_CUDA(cudaStreamSynchronize(c->stream));
+    }
+    return W1G_OK;
+}
+
+int w1g_set_rwmd_culling(w1g_ctx *c, int enabled) {
+    if (!c) return W1G_EINVAL;
+    c->culling = enabled ? 1 : 0;
+    return W1G_OK;
+}
+
+// ---------------------------------------------------------------- delta condense
+
+int w1g_delta_condense(w1g_ctx *c, double delta, double pitch, double half_width, uint64_t seed,
+                       int64_t *k) {
+    CTX_CHECK(c);
+    if (!c->nodes[0].valid) {
+        set_error("delta_condense: no nodes0");
+        return W1G_ESTATE;
+    }
+    if (!(delta >= 0.0)) {
+        set_error("delta must be nonnegative");
+        return W1G_EINVAL;
+    }
+    invalidate_from_nodes(*c);
+    return dc_run(*c, delta, pitch, half_width, seed, k);
+}
+
+// ---------------------------------------------------------------- split tree
+
+int w1g_split_tree(w1g_ctx *c, int slot, int64_t *n_nodes, int32_t *depth) {
+    CTX_CHECK(c);
+    if (slot < 0 || slot > 1 || !c->nodes[slot].valid) {
+        set_error("split_tree: node slot %d is empty", slot);
+        return W1G_ESTATE;
+    }
+    c->pairs_valid = false;
+    c->arcs_valid = false;
+    c->net_valid = false;
+    NodeSet &ns = c->nodes[slot];
+    return tree_run(*c, ptr<double2>(ns.pts), ns.k, n_nodes, depth);
+}
+
+int w1g_fetch_tree(w1g_ctx *c, int64_t *left, int64_t *right, double *bbox, int64_t *rep,
+                   int64_t *size) {
+    CTX_CHECK(c);
+    if (!c->tree_valid) {
+        set_error("no split tree");
+        return W1G_ESTATE;
+    }
+    const size_t nn = (size_t)c->tree_n_nodes;
+    W1G_TRY(download(*c, left, c->t_left.p, sizeof(int64_t) * nn));
+    W1G_TRY(download(*c, right, c->t_right.p, sizeof(int64_t) * nn));
+    W1G_TRY(download(*c, bbox, c->t_bbox.p, sizeof(double) * 4 * nn));
+    W1G_TRY(download(*c, rep, c->t_rep.p, sizeof(int64_t) * nn));
+    W1G_TRY(download(*c, size, c->t_size.p, sizeof(int64_t) * nn));
+    W1G_CUDA(cudaStreamSynchronize(c->stream));
+    return W1G_OK;
+}
+
+int w1g_load_tree(w1g_ctx *c, const double *points, int64_t n_points, const int64_t *left,
+                  const int64_t *right, const double *bbox, const int64_t *rep, int64_t n_nodes) {
+    CTX_CHECK(c);
+    if (n_points < 0 || n_nodes < 0 || n_nodes >= (1ll << 31)) return W1G_EINVAL;
+    c->pairs_valid = false;
+    c->arcs_valid = false;
+    c->net_valid = false;
+    W1G_TRY(upload(*c, c->tree_pts, points, sizeof(double2) * n_points));
+    W1G_TRY(upload(*c, c->t_left, left, sizeof(int64_t) * n_nodes));
+    W1G_TRY(upload(*c, c->t_right, right, sizeof(int64_t) * n_nodes));
+    W1G_TRY(upload(*c, c->t_bbox, bbox, sizeof(double) * 4 * n_nodes));
+    W1G_TRY(upload(*c, c->t_rep, rep, sizeof(int64_t) * n_nodes));
+    int64_t *sz;
+    W1G_TRY(ensure(c->t_size, (size_t)n_nodes, &sz));
+    c->tree_n_points = n_points;
+    c->tree_n_nodes = n_nodes;
+    c->tree_depth = 0;
+    c->pair_pts = ptr<double2>(c->tree_pts);
+    W1G_TRY(tree_geom(*c));
+    c->tree_valid = true;
+    return W1G_OK;
+}
+
+// ---------------------------------------------------------------- WSPD
+
+int w1g_wspd(w1g_ctx *c, double s, int reference_order, int64_t *n_pairs) {
+    CTX_CHECK(c);
+    if (!(s > 0.0)) {
+        set_error("s must be positive");
+        return W1G_EINVAL;
+    }
+    if (!c->tree_valid) {
+        set_error("wspd: no split tree");
+        return W1G_ESTATE;
+    }
+    c->arcs_valid = false;
+    c->net_valid = false;
+    return wspd_run(*c, s, reference_order, n_pairs);
+}
+
+int w1g_fetch_pairs(w1g_ctx *c, int64_t *node_pairs, int64_t *indices) {
+    CTX_CHECK(c);
+    if (!c->pairs_valid) {
+        set_error("no WSPD pairs");
+        return W1G_ESTATE;
+    }
+    const size_t P = (size_t)c->n_pairs;
+    if (node_pairs) {
+        if (!c->pairs_have_nodes) {
+            set_error("pairs were loaded from indices only");
+            return W1G_ESTATE;
+        }
+        // int2 (u, v) -> int64 (P, 2)
+        W1G_TRY(stage_ensure(*c, sizeof(int2) * P));
+        W1G_TRY(download(*c, c->h_stage, c->pair_uv.p, sizeof(int2) * P));
+        W1G_CUDA(cudaStreamSynchronize(c->stream));
+        const int2 *uv = static_cast<const int2 *>(c->h_stage);
+        for (size_t i = 0; i < P; i++) {
+            node_pairs[2 * i] = uv[i].x;
+            node_pairs[2 * i + 1] = uv[i].y;
+        }
+    }
+    if (indices) {
+        W1G_TRY(download(*c, indices, c->pair_idx.p, sizeof(int64_t) * 2 * P));
+        W1G_CUDA(cudaStreamSynchronize(c->stream));
+    }
+    return W1G_OK;
+}
+
+int w1g_fetch_pair_counts(w1g_ctx *c, int64_t *counts, int64_t *n_internal) {
+    CTX_CHECK(c);
+    if (!c->pairs_valid || !c->pairs_have_nodes) {
+        set_error("no WSPD pairs");
+        return W1G_ESTATE;
+    }
+    const int64_t ni = c->tree_n_nodes > 0 ? (c->tree_n_nodes - 1) / 2 : 0;
+    *n_internal = ni;
+    if (counts) {
+        W1G_TRY(download(*c, counts, c->pair_counts.p, sizeof(int64_t) * ni));
+        W1G_CUDA(cudaStreamSynchronize(c->stream));
+    }
+    return W1G_OK;
+}
+
+int w1g_load_pairs(w1g_ctx *c, const int64_t *indices, int64_t n_pairs, const double *points,
+                   int64_t n_points) {
+    CTX_CHECK(c);
+    if (n_pairs < 0 || n_points < 0) return W1G_EINVAL;
+    W1G_TRY(upload(*c, c->pair_idx, indices, sizeof(int64_t) * 2 * n_pairs));
+    W1G_TRY(upload(*c, c->tree_pts, points, sizeof(double2) * n_points));
+    c->pair_pts = ptr<double2>(c->tree_pts);
+    c->n_pairs = n_pairs;
+    c->pairs_valid = true;
+    c->pairs_have_nodes = false;
+    c->arcs_valid = false;
+    c->net_valid = false;
+    return W1G_OK;
+}
+
+// ---------------------------------------------------------------- arcs / network
+
+int w1g_emit_arcs(w1g_ctx *c, int64_t *n_arcs) {
+    CTX_CHECK(c);
+    if (!c->pairs_valid || !c->nodes[1].valid) {
+        set_error("emit_arcs: needs pairs and nodes");
+        return W1G_ESTATE;
+    }
+    c->net_valid = false;
+    return emit_run(*c, n_arcs);
+}
+
+int w1g_fetch_arcs(w1g_ctx *c, int64_t *tails, int64_t *heads, double *costs) {
+    CTX_CHECK(c);
+    if (!c->arcs_valid) {
+        set_error("no arcs");
+        return W1G_ESTATE;
+    }
+    const size_t m = (size_t)c->n_arcs;
+    W1G_TRY(download(*c, tails, c->arc_t.p, sizeof(int64_t) * m));
+    W1G_TRY(download(*c, heads, c->arc_h.p, sizeof(int64_t) * m));
+    W1G_TRY(download(*c, costs, c->arc_c.p, sizeof(double) * m));
+    W1G_CUDA(cudaStreamSynchronize(c->stream));
+    return W1G_OK;
+}
+
+int w1g_load_arcs(w1g_ctx *c, const int64_t *tails, const int64_t *heads, const double *costs,
+                  int64_t m) {
+    CTX_CHECK(c);
+    if (m < 0 || m >= (1ll << 32)) return W1G_EINVAL;
+    W1G_TRY(upload(*c, c->arc_t, tails, sizeof(int64_t) * m));
+    W1G_TRY(upload(*c, c->arc_h, heads, sizeof(int64_t) * m));
+    W1G_TRY(upload(*c, c->arc_c, costs, sizeof(double) * m));
+    c->n_arcs = m;
+    c->arcs_valid = true;
+    c->net_valid = false;
+    return W1G_OK;
+}
+
+int w1g_build_network(w1g_ctx *c, const int64_t *supplies, int64_t n, int64_t *n_arcs) {
+    CTX_CHECK(c);
+    if (!c->arcs_valid) {
+        set_error("build_network: no arcs");
+        return W1G_ESTATE;
+    }
+    if (n < 0 || n >= (1ll << 31)) return W1G_EINVAL;
+    int64_t *d;
+    W1G_TRY(ensure(c->net_sup, (size_t)n, &d));
+    if (n) W1G_CUDA(cudaMemcpyAsync(d, supplies, sizeof(int64_t) * n, cudaMemcpyHostToDevice, c->stream));
+    return net_run(*c, d, n, n_arcs);
+}
+
+int w1g_assemble(w1g_ctx *c, int64_t *node_count, int64_t *n_arcs) {
+    CTX_CHECK(c);
+    if (!c->arcs_valid || !c->nodes[1].valid) {
+        set_error("assemble: needs arcs and nodes");
+        return W1G_ESTATE;
+    }
+    int64_t *d, n;
+    W1G_TRY(assemble_supplies(*c, &d, &n));
+    *node_count = n;
+    return net_run(*c, d, n, n_arcs);
+}
+
+int w1g_fetch_network(w1g_ctx *c, int64_t *supplies, int64_t *tails, int64_t *heads, double *costs,
+                      int64_t *row_offsets) {
+    CTX_CHECK(c);
+    if (!c->net_valid) {
+        set_error("no network");
+        return W1G_ESTATE;
+    }
+    const size_t n = (size_t)c->net_n, m = (size_t)c->net_m;
+    W1G_TRY(download(*c, supplies, c->net_sup.p, sizeof(int64_t) * n));
+    W1G_TRY(download(*c, tails, c->net_t.p, sizeof(int64_t) * m));
+    W1G_TRY(download(*c, heads, c->net_h.p, sizeof(int64_t) * m));
+    W1G_TRY(download(*c, costs, c->net_c.p, sizeof(double) * m));
+    W1G_TRY(download(*c, row_offsets, c->net_ro.p, sizeof(int64_t) * (n + 1)));
+    W1G_CUDA(cudaStreamSynchronize(c->stream));
+    return W1G_OK;
+}
+
+// ---------------------------------------------------------------- fused front end
+
+static const double SQRT2 = 1.4142135623730951;  // math.sqrt(2.0)
+
+int w1g_front_end_device(w1g_ctx *c, const double *d_a, int64_t na, const double *d_b, int64_t nb,
+                         double s, int use_condensation, int delta_mode, double delta, double k,
+                         uint64_t seed, w1g_front_end_info *info) {
+    CTX_CHECK(c);
+    if (!info) return W1G_EINVAL;
+    memset(info, 0, sizeof *info);
+    if (!(s > 0.0)) {
+        set_error("s must be positive");
+        return W1G_EINVAL;
+    }
+    if (!(k >= 0.5 && k < 1.0)) {
+        set_error("k must lie in [0.5, 1)");
+        return W1G_EINVAL;
+    }
+    cudaEvent_t *ev = c->ev;
+    W1G_CUDA(cudaEventRecord(ev[0], c->stream));
+    int64_t k0;
+    int32_t balanced;
+    W1G_TRY(w1g_zero_condense_device(c, d_a, na, d_b, nb, &k0, &balanced));
+    W1G_CUDA(cudaEventRecord(ev[1], c->stream));
+    info->n_points0 = k0;
+    if (k0 == 0 || balanced) {
+        // pipeline.py:106-109: empty inputs or identical multisets -> 0.0
+        info->short_circuit = 1;
+        W1G_CUDA(cudaStreamSynchronize(c->stream));
+        return W1G_OK;
+    }
+    double L, LA, LB;
+    W1G_TRY(rwmd_run(*c, &L, &LA, &LB));
+    W1G_CUDA(cudaEventRecord(ev[2], c->stream));
+    info->lower_bound = L;
+    info->lower_bound_a = LA;
+    info->lower_bound_b = LB;
+    // pipeline.py:67-69, condensation.py:47-59 (same IEEE operation order as the Python)
+    const double eps_c = s >= 12 ? 8.0 / (s - 4.0) : 1.0;
+    info->epsilon_condense = eps_c;
+    double d = 0.0;
+    if (use_condensation && L > 0.0) {
+        if (delta_mode == 0) {
+            const double n_points = (double)(na + nb);
+            d = 2.0 * eps_c * L / (SQRT2 * n_points);
+        } else {
+            d = delta;
+        }
+    }
+    info->delta = d;
+    int64_t kk;
+    const double pitch = k * d;
+    const double half_width = (1.0 - k) * d / 2.0;
+    W1G_TRY(dc_run(*c, d > 0.0 ? d : 0.0, pitch, half_width, seed, &kk));
+    W1G_CUDA(cudaEventRecord(ev[3], c->stream));
+    info->n_points = kk;
+    int64_t nn;
+    int32_t depth;
+    W1G_TRY(tree_run(*c, ptr<double2>(c->nodes[1].pts), kk, &nn, &depth));
+    W1G_CUDA(cudaEventRecord(ev[4], c->stream));
+    info->n_tree_nodes = nn;
+    info->tree_depth = depth;
+    int64_t P;
+    W1G_TRY(wspd_run(*c, s, 0, &P));
+    W1G_CUDA(cudaEventRecord(ev[5], c->stream));
+    info->n_pairs = P;
+    info->n_levels_wspd = c->wspd_levels;
+    int64_t M;
+    W1G_TRY(emit_run(*c, &M));
+    W1G_CUDA(cudaEventRecord(ev[6], c->stream));
+    int64_t *dsup, nsup, mm;
+    W1G_TRY(assemble_supplies(*c, &dsup, &nsup));
+    W1G_TRY(net_run(*c, dsup, nsup, &mm));
+    W1G_CUDA(cudaEventRecord(ev[7], c->stream));
+    W1G_CUDA(cudaEventSynchronize(ev[7]));
+    info->n_arcs = mm;
+    info->node_count = nsup;
+    for (int i = 0; i < 7; i++) W1G_CUDA(cudaEventElapsedTime(&info->stage_ms[i], ev[i], ev[i + 1]));
+    W1G_CUDA(cudaEventElapsedTime(&info->stage_ms[7], ev[0], ev[7]));
+    return W1G_OK;
+}
+
+int w1g_front_end(w1g_ctx *c, const double *a, int64_t na, const double *b, int64_t nb, double s,
+                  int use_condensation, int delta_mode, double delta, double k, uint64_t seed,
+                  w1g_front_end_info *info) {
+    CTX_CHECK(c);
+    if (na < 0 || nb < 0) return W1G_EINVAL;
+    double2 *d;
+    W1G_TRY(ensure(c->in_pts, (size_t)(na + nb), &d));
+    if (na) W1G_CUDA(cudaMemcpyAsync(d, a, sizeof(double2) * na, cudaMemcpyHostToDevice, c->stream));
+    if (nb) W1G_CUDA(cudaMemcpyAsync(d + na, b, sizeof(double2) * nb, cudaMemcpyHostToDevice, c->stream));
+    return w1g_front_end_device(c, reinterpret_cast<double *>(d), na,
+                                reinterpret_cast<double *>(d + na), nb, s, use_condensation,
+                                delta_mode, delta, k, seed, info);
+}
+
+}  // extern "C"

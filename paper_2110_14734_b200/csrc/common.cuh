@@ -1,0 +1,325 @@
+// common.cuh -- shared infrastructure of libw1g.so (sm_100a only).
+//
+// Context / device-buffer plumbing, error reporting, the exact-IEEE fp64
+// helpers every reference-parity kernel uses, a single-pass decoupled
+// look-back scan and the LSD radix sort interface.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <string>
+
+#include "../../include/w1g.h"
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ != 1000)
+#error "libw1g is built for sm_100a only"
+#endif
+
+namespace w1g {
+
+// ------------------------------------------------------------------ errors
+void set_error(const char *fmt, ...);
+int cuda_fail(cudaError_t e, const char *what, const char *file, int line);
+
+#define W1G_CUDA(call)                                                      \
+    do {                                                                    \
+        cudaError_t _e = (call);                                            \
+        if (_e != cudaSuccess) return ::w1g::cuda_fail(_e, #call, __FILE__, __LINE__); \
+    } while (0)
+// every kernel launch is followed by W1G_CHECK_LAUNCH(), which also counts it
+extern unsigned long long g_launches;
+#define W1G_CHECK_LAUNCH()                                  \
+    do {                                                    \
+        __atomic_fetch_add(&::w1g::g_launches, 1ull, __ATOMIC_RELAXED); \
+        W1G_CUDA(cudaGetLastError());                       \
+    } while (0)
+#define W1G_TRY(expr)                \
+    do {                             \
+        int _rc = (expr);            \
+        if (_rc != W1G_OK) return _rc; \
+    } while (0)
+
+// ------------------------------------------------------------------ buffers
+struct DevBuf {
+    void *p = nullptr;
+    size_t cap = 0;
+};
+// grow-only device buffer (geometric); contents are NOT preserved on growth
+int ensure_bytes(DevBuf &b, size_t bytes);
+template <class T>
+inline int ensure(DevBuf &b, size_t n, T **out) {
+    int rc = ensure_bytes(b, n * sizeof(T) + 16);
+    *out = static_cast<T *>(b.p);
+    return rc;
+}
+template <class T>
+inline T *ptr(DevBuf &b) { return static_cast<T *>(b.p); }
+void free_buf(DevBuf &b);
+
+struct NodeSet {
+    int64_t k = 0;
+    bool valid = false;
+    DevBuf pts;  // (k) double2 (x, y), node order
+    DevBuf am;   // (k) int64 a_mass
+    DevBuf bm;   // (k) int64 b_mass
+    int64_t abar = 0, bbar = 0;
+};
+
+// per-node geometry used by the WSPD predicate (spanner.py:176-194), computed
+// once per node with the reference's exact operation sequence
+struct NodeGeom {
+    double cx, cy;  // 0.5*(xmin+xmax), 0.5*(ymin+ymax)
+    double r;       // 0.5*sqrt(w*w+h*h)
+    double dsq;     // w*w+h*h
+};
+
+enum { SCR_N = 24 };
+
+struct Ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int sm_count = 148;
+
+    DevBuf in_pts;  // (na+nb) double2
+    NodeSet nodes[2];
+
+    // rwmd
+    int culling = 1;
+    DevBuf best[2];
+    int64_t n_best[2] = {0, 0};
+    int64_t rw_members[2] = {0, 0};  // A- and B-member counts of the last rwmd_run
+
+    // split tree (over `tree_pts`, a copy of the slot's points)
+    bool tree_valid = false;
+    int64_t tree_n_points = 0, tree_n_nodes = 0;
+    int32_t tree_depth = 0;
+    DevBuf tree_pts;                                // double2
+    DevBuf t_left, t_right, t_rep, t_size, t_bbox;  // int64 x4, double x4 (reference layout)
+    DevBuf t_geom;                                  // NodeGeom per node
+    DevBuf t_lr;                                    // int2 (left, right) per node, -1 leaf
+    DevBuf t_rep32;                                 // int32 rep
+    const double2 *pair_pts = nullptr;              // points the pairs' reps index
+
+    // WSPD
+    bool pairs_valid = false;
+    int64_t n_pairs = 0;
+    int32_t wspd_levels = 0;
+    DevBuf pair_uv;    // int2 (u, v) tree node ids
+    DevBuf pair_w;     // int32 owner internal node
+    DevBuf pair_path;  // uint64 left-aligned DFS path bits (1 = right child)
+    DevBuf pair_idx;   // int64 (P,2) representative point indices
+    DevBuf pair_counts;
+    bool pairs_have_nodes = false;
+
+    // arcs (emit_arcs output, reference order)
+    bool arcs_valid = false;
+    int64_t n_arcs = 0;
+    DevBuf arc_t, arc_h, arc_c;
+
+    // network (CSR)
+    bool net_valid = false;
+    int64_t net_n = 0, net_m = 0;
+    DevBuf net_sup, net_t, net_h, net_c, net_ro;
+
+    // scratch
+    DevBuf scr[SCR_N];
+    DevBuf sort_scr[8];
+    DevBuf scan_state;
+    DevBuf flags;  // small device flag block (int64 x 64)
+    int64_t *h_pinned = nullptr;  // pinned host mirror of `flags`
+    void *h_stage = nullptr;      // pinned staging buffer for H2D / D2H
+    size_t h_stage_cap = 0;
+
+    cudaEvent_t ev[16] = {};
+};
+
+// device flag block layout (int64 slots)
+enum FlagSlot {
+    F_K0 = 0,
+    F_UNBALANCED = 1,
+    F_OVERFLOW = 2,
+    F_DUP = 3,
+    F_ACTIVE = 4,
+    F_PAIRS = 5,
+    F_FRONT = 6,
+    F_PAIR_OVF = 7,
+    F_FRONT_OVF = 8,
+    F_NET_ERR = 9,
+    F_TOTAL = 10,
+    F_PATH_OVF = 11,
+    F_MISC0 = 12,
+    F_MISC1 = 13,
+    F_MISC2 = 14,
+    F_MISC3 = 15,
+    F_CELL_MIN = 16,  // 4 slots: min cx, max cx, min cy, max cy
+    F_BBOX = 24,      // 4 doubles (as bits)
+    F_SCAL = 32,      // 8 doubles of scalar results
+    F_NSLOTS = 64
+};
+
+int flags_reset(Ctx &c);
+int flags_fetch(Ctx &c, int first, int count);  // D2H into h_pinned + stream sync
+inline int64_t *dflags(Ctx &c) { return ptr<int64_t>(c.flags); }
+
+// pinned staging (host) buffer
+int stage_ensure(Ctx &c, size_t bytes);
+
+// ------------------------------------------------------------------ exact fp64
+// Every reference-parity fp64 expression is written with the _rn intrinsics so
+// that no FMA contraction can occur regardless of compiler flags.
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+__device__ __forceinline__ double dsqrt(double a) { return __dsqrt_rn(a); }
+
+// IEEE-754 total order key for non-NaN doubles, with -0.0 folded onto +0.0
+// (np.unique / np.lexsort compare floats, so -0.0 == +0.0).
+__device__ __forceinline__ uint64_t dkey(double v) {
+    if (v == 0.0) v = 0.0;
+    uint64_t b = (uint64_t)__double_as_longlong(v);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+// signed int64 -> order-preserving uint64
+__device__ __forceinline__ uint64_t ikey(int64_t v) { return (uint64_t)v ^ 0x8000000000000000ull; }
+
+// ------------------------------------------------------------------ scan
+// Exclusive prefix sum of int64 values produced by a functor, one pass with
+// decoupled look-back.  out may be null (only the total is wanted).
+struct ScanArgs {
+    unsigned long long *status;  // tiles
+    unsigned int *ticket;
+};
+constexpr int SCAN_BLOCK = 256;
+constexpr int SCAN_IPT = 8;
+constexpr int SCAN_TILE = SCAN_BLOCK * SCAN_IPT;
+
+int scan_prepare(Ctx &c, int64_t n, ScanArgs *a, int64_t *n_tiles);
+
+template <class F>
+__global__ void __launch_bounds__(SCAN_BLOCK) k_scan_i64(F f, int64_t n, int64_t *out,
+                                                        int64_t *total, ScanArgs a) {
+    __shared__ unsigned int s_tile;
+    __shared__ int64_t s_warp[SCAN_BLOCK / 32];
+    __shared__ int64_t s_prefix;
+    if (threadIdx.x == 0) s_tile = atomicAdd(a.ticket, 1u);
+    __syncthreads();
+    const int64_t tile = s_tile;
+    const int64_t base = tile * SCAN_TILE + (int64_t)threadIdx.x * SCAN_IPT;
+    int64_t v[SCAN_IPT];
+    int64_t tsum = 0;
+#pragma unroll
+    for (int i = 0; i < SCAN_IPT; i++) {
+        int64_t idx = base + i;
+        v[i] = idx < n ? (int64_t)f(idx) : 0;
+        tsum += v[i];
+    }
+    // block exclusive scan of tsum
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int64_t x = tsum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_warp[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+        int64_t w = lane < SCAN_BLOCK / 32 ? s_warp[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int64_t y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += y;
+        }
+        if (lane < SCAN_BLOCK / 32) s_warp[lane] = w;  // inclusive warp totals
+    }
+    __syncthreads();
+    const int64_t warp_excl = wid ? s_warp[wid - 1] : 0;
+    const int64_t excl = warp_excl + x - tsum;
+    const int64_t agg = s_warp[SCAN_BLOCK / 32 - 1];
+    if (threadIdx.x == 0) {
+        constexpr unsigned long long FA = 1ull << 62, FP = 2ull << 62, MASK = (1ull << 62) - 1;
+        if (tile == 0) {
+            atomicExch(&a.status[0], FP | (unsigned long long)agg);
+            s_prefix = 0;
+        } else {
+            atomicExch(&a.status[tile], FA | (unsigned long long)agg);
+            int64_t prefix = 0;
+            int64_t j = tile - 1;
+            while (true) {
+                unsigned long long st = *((volatile unsigned long long *)&a.status[j]);
+                if ((st >> 62) == 0) continue;
+                __threadfence();
+                prefix += (int64_t)(st & MASK);
+                if ((st >> 62) == 2) break;
+                j--;
+            }
+            __threadfence();
+            atomicExch(&a.status[tile], FP | (unsigned long long)(prefix + agg));
+            s_prefix = prefix;
+        }
+    }
+    __syncthreads();
+    if (out) {
+        int64_t run = s_prefix + excl;
+#pragma unroll
+        for (int i = 0; i < SCAN_IPT; i++) {
+            int64_t idx = base + i;
+            if (idx < n) out[idx] = run;
+            run += v[i];
+        }
+    }
+    if (total && threadIdx.x == 0 && tile == (n > 0 ? (n - 1) / SCAN_TILE : 0)) *total = s_prefix + agg;
+}
+
+template <class F>
+int scan_i64(Ctx &c, F f, int64_t n, int64_t *out, int64_t *total) {
+    ScanArgs a;
+    int64_t tiles;
+    W1G_TRY(scan_prepare(c, n, &a, &tiles));
+    k_scan_i64<F><<<(unsigned)tiles, SCAN_BLOCK, 0, c.stream>>>(f, n, out, total, a);
+    W1G_CHECK_LAUNCH();
+    return W1G_OK;
+}
+
+// ------------------------------------------------------------------ radix sort
+// Stable LSD radix sort, 8-bit digits, ascending by a key of `words` uint64
+// words (keys[words-1] most significant), carrying a uint32 payload.  The
+// key words and the payload are permuted in place (ping-pong internally).
+// Digits whose value is the same for every key are skipped (one D2H of the
+// digit histogram per sort).  bits_hint limits the digits considered in the
+// most-significant word (64 = all).
+int radix_sort(Ctx &c, uint64_t **keys, int words, uint32_t *vals, int64_t n, int top_bits = 64);
+
+// ------------------------------------------------------------------ misc
+inline unsigned grid_for(int64_t n, int block, unsigned cap = 0x7fffffffu) {
+    int64_t g = (n + block - 1) / block;
+    if (g < 1) g = 1;
+    if (g > (int64_t)cap) g = cap;
+    return (unsigned)g;
+}
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+// stage launchers (one translation unit each)
+int zc_run(Ctx &c, const double2 *d_a, int64_t na, const double2 *d_b, int64_t nb, int64_t *k0,
+           int32_t *balanced);
+int rwmd_run(Ctx &c, double *L, double *LA, double *LB);
+int rwmd_tile_profile(Ctx &c, int reps, float *ms, int64_t *evals);
+int dc_run(Ctx &c, double delta, double pitch, double half_width, uint64_t seed, int64_t *k);
+int tree_run(Ctx &c, const double2 *d_pts, int64_t n, int64_t *n_nodes, int32_t *depth);
+int tree_geom(Ctx &c);
+int wspd_run(Ctx &c, double s, int reference_order, int64_t *n_pairs);
+int emit_run(Ctx &c, int64_t *n_arcs);
+int net_run(Ctx &c, const int64_t *d_supplies, int64_t n, int64_t *n_arcs);
+int assemble_supplies(Ctx &c, int64_t **d_sup, int64_t *n);
+
+}  // namespace w1g
+
+struct w1g_ctx : public w1g::Ctx {};

@@ -1,0 +1,301 @@
+// condense.cu -- node sparsification on device.
+//
+//  zero_condense  (diagram.py:190-208): order-preserving 128-bit (x, y) keys,
+//      stable radix sort, run-length unique, per-side multiplicities.
+//  delta_condense (condensation.py:62-124): exact fp64 snap with the
+//      reference's round-half-away (sign(t)*floor(|t|+0.5)), signed-int64
+//      cell keys packed into one word when the cell range allows, stable
+//      radix sort, reduce-by-key of masses, splitmix64 per-cell offsets and
+//      coords = fl(fl(cell*pitch) + offset).
+#include "common.cuh"
+
+namespace w1g {
+
+namespace {
+
+__device__ __forceinline__ double2 pick(const double2 *a, int64_t na, const double2 *b, int64_t i) {
+    return i < na ? a[i] : b[i - na];
+}
+
+__global__ void k_zc_keys(const double2 *a, int64_t na, const double2 *b, int64_t n, uint64_t *hi,
+                          uint64_t *lo, uint32_t *vals) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        double2 p = pick(a, na, b, i);
+        hi[i] = dkey(p.x);
+        lo[i] = dkey(p.y);
+        vals[i] = (uint32_t)i;
+    }
+}
+
+struct ZcFlag {
+    const double2 *a, *b;
+    int64_t na;
+    const uint32_t *v;
+    __device__ int64_t operator()(int64_t i) const {
+        if (i == 0) return 1;
+        double2 p = pick(a, na, b, v[i]), q = pick(a, na, b, v[i - 1]);
+        return (p.x == q.x && p.y == q.y) ? 0 : 1;
+    }
+};
+
+__global__ void k_zc_emit(ZcFlag f, int64_t n, const int64_t *excl, double2 *pts, int64_t *am,
+                          int64_t *bm) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t fl = f(i);
+        int64_t rid = excl[i] + fl - 1;
+        uint32_t src = f.v[i];
+        if (fl) pts[rid] = pick(f.a, f.na, f.b, src);  // first of the run (lowest input index)
+        if ((int64_t)src < f.na)
+            atomicAdd((unsigned long long *)&am[rid], 1ull);
+        else
+            atomicAdd((unsigned long long *)&bm[rid], 1ull);
+    }
+}
+
+__global__ void k_unbalanced(const int64_t *am, const int64_t *bm, const int64_t *kp, int64_t *flag) {
+    const int64_t k = *kp;
+    int any = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < k;
+         i += (int64_t)gridDim.x * blockDim.x)
+        any |= am[i] != bm[i];
+    if (__syncthreads_or(any) && threadIdx.x == 0) atomicOr((unsigned long long *)flag, 1ull);
+}
+
+// ------------------------------------------------------------ delta condense
+
+__device__ __forceinline__ double round_half_away(double t) {
+    // condensation.py:62-63: np.sign(t) * np.floor(np.abs(t) + 0.5)
+    double sg = t > 0.0 ? 1.0 : (t < 0.0 ? -1.0 : t);
+    return dmul(sg, floor(dadd(fabs(t), 0.5)));
+}
+
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+    // condensation.py:85-89
+    x = x + 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+
+__global__ void k_init_ranges(int64_t *f) {
+    f[F_CELL_MIN + 0] = INT64_MAX;
+    f[F_CELL_MIN + 1] = INT64_MIN;
+    f[F_CELL_MIN + 2] = INT64_MAX;
+    f[F_CELL_MIN + 3] = INT64_MIN;
+}
+
+__global__ void k_dc_snap(const double2 *pts, int64_t k, double pitch, longlong2 *cells, int64_t *f) {
+    int64_t mnx = INT64_MAX, mxx = INT64_MIN, mny = INT64_MAX, mxy = INT64_MIN;
+    int ovf = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < k;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        double2 p = pts[i];
+        // snap_points, condensation.py:73-77
+        double cx = round_half_away(ddiv(p.x, pitch));
+        double cy = round_half_away(ddiv(p.y, pitch));
+        if (!(fabs(cx) < 4611686018427387904.0) || !(fabs(cy) < 4611686018427387904.0)) {
+            ovf = 1;
+            cx = 0.0;
+            cy = 0.0;
+        }
+        long long ix = __double2ll_rz(cx), iy = __double2ll_rz(cy);
+        cells[i] = make_longlong2(ix, iy);
+        mnx = min(mnx, (int64_t)ix);
+        mxx = max(mxx, (int64_t)ix);
+        mny = min(mny, (int64_t)iy);
+        mxy = max(mxy, (int64_t)iy);
+    }
+    if (ovf) atomicOr((unsigned long long *)&f[F_OVERFLOW], 1ull);
+    // warp reduce then one atomic per warp
+    for (int o = 16; o; o >>= 1) {
+        mnx = min(mnx, (int64_t)__shfl_xor_sync(0xffffffffu, (long long)mnx, o));
+        mxx = max(mxx, (int64_t)__shfl_xor_sync(0xffffffffu, (long long)mxx, o));
+        mny = min(mny, (int64_t)__shfl_xor_sync(0xffffffffu, (long long)mny, o));
+        mxy = max(mxy, (int64_t)__shfl_xor_sync(0xffffffffu, (long long)mxy, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin((long long *)&f[F_CELL_MIN + 0], (long long)mnx);
+        atomicMax((long long *)&f[F_CELL_MIN + 1], (long long)mxx);
+        atomicMin((long long *)&f[F_CELL_MIN + 2], (long long)mny);
+        atomicMax((long long *)&f[F_CELL_MIN + 3], (long long)mxy);
+    }
+}
+
+__global__ void k_dc_keys(const longlong2 *cells, int64_t k, int packed, int64_t mnx, int64_t mny,
+                          int by, uint64_t *k0, uint64_t *k1, uint32_t *vals) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < k;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        longlong2 c = cells[i];
+        if (packed) {
+            k0[i] = (by >= 64 ? 0ull : ((uint64_t)(c.x - mnx) << by)) | (uint64_t)(c.y - mny);
+        } else {
+            k0[i] = ikey(c.y);  // least significant word first
+            k1[i] = ikey(c.x);
+        }
+        vals[i] = (uint32_t)i;
+    }
+}
+
+struct DcFlag {
+    const longlong2 *cells;
+    const uint32_t *v;
+    __device__ int64_t operator()(int64_t i) const {
+        if (i == 0) return 1;
+        longlong2 p = cells[v[i]], q = cells[v[i - 1]];
+        return (p.x == q.x && p.y == q.y) ? 0 : 1;
+    }
+};
+
+__global__ void k_dc_emit(DcFlag f, int64_t k, const int64_t *excl, const int64_t *am_in,
+                          const int64_t *bm_in, double pitch, double half_width, uint64_t base,
+                          double2 *pts, int64_t *am, int64_t *bm) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < k;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t fl = f(i);
+        int64_t rid = excl[i] + fl - 1;
+        uint32_t src = f.v[i];
+        if (fl) {
+            longlong2 c = f.cells[src];
+            // _lattice_offsets, condensation.py:92-102
+            uint64_t h1 = splitmix64(base ^ (uint64_t)c.x);
+            uint64_t h2 = splitmix64(h1 ^ (uint64_t)c.y);
+            uint64_t h3 = splitmix64(h2);
+            double u1 = dmul(__ull2double_rn(h2 >> 11), 0x1p-53);
+            double u2 = dmul(__ull2double_rn(h3 >> 11), 0x1p-53);
+            double o1 = dmul(half_width, dsub(dmul(2.0, u1), 1.0));
+            double o2 = dmul(half_width, dsub(dmul(2.0, u2), 1.0));
+            // condensation.py:123: cells.astype(f64) * (k*delta) + offsets
+            pts[rid] = make_double2(dadd(dmul(__ll2double_rn(c.x), pitch), o1),
+                                    dadd(dmul(__ll2double_rn(c.y), pitch), o2));
+        }
+        if (am_in[src]) atomicAdd((unsigned long long *)&am[rid], (unsigned long long)am_in[src]);
+        if (bm_in[src]) atomicAdd((unsigned long long *)&bm[rid], (unsigned long long)bm_in[src]);
+    }
+}
+
+inline unsigned gs(const Ctx &c, int64_t n) { return grid_for(n, 256, 8u * c.sm_count); }
+
+}  // namespace
+
+int zc_run(Ctx &c, const double2 *d_a, int64_t na, const double2 *d_b, int64_t nb, int64_t *k0,
+           int32_t *balanced) {
+    const int64_t n = na + nb;
+    NodeSet &ns = c.nodes[0];
+    ns.abar = -na;
+    ns.bbar = nb;
+    ns.valid = true;
+    c.nodes[1].valid = false;
+    if (n == 0) {
+        ns.k = 0;
+        *k0 = 0;
+        *balanced = 1;
+        return W1G_OK;
+    }
+    uint64_t *hi, *lo;
+    uint32_t *vals;
+    int64_t *excl;
+    W1G_TRY(ensure(c.scr[0], n, &hi));
+    W1G_TRY(ensure(c.scr[1], n, &lo));
+    W1G_TRY(ensure(c.scr[2], n, &vals));
+    W1G_TRY(ensure(c.scr[3], n, &excl));
+    double2 *pts;
+    int64_t *am, *bm;
+    W1G_TRY(ensure(ns.pts, n, &pts));
+    W1G_TRY(ensure(ns.am, n, &am));
+    W1G_TRY(ensure(ns.bm, n, &bm));
+    W1G_TRY(flags_reset(c));
+    k_zc_keys<<<gs(c, n), 256, 0, c.stream>>>(d_a, na, d_b, n, hi, lo, vals);
+    W1G_CHECK_LAUNCH();
+    uint64_t *keys[2] = {lo, hi};
+    W1G_TRY(radix_sort(c, keys, 2, vals, n));
+    ZcFlag f{d_a, d_b, na, vals};
+    W1G_TRY(scan_i64(c, f, n, excl, dflags(c) + F_K0));
+    W1G_CUDA(cudaMemsetAsync(am, 0, sizeof(int64_t) * n, c.stream));
+    W1G_CUDA(cudaMemsetAsync(bm, 0, sizeof(int64_t) * n, c.stream));
+    k_zc_emit<<<gs(c, n), 256, 0, c.stream>>>(f, n, excl, pts, am, bm);
+    W1G_CHECK_LAUNCH();
+    k_unbalanced<<<gs(c, n), 256, 0, c.stream>>>(am, bm, dflags(c) + F_K0, dflags(c) + F_UNBALANCED);
+    W1G_CHECK_LAUNCH();
+    W1G_TRY(flags_fetch(c, F_K0, 2));
+    ns.k = c.h_pinned[F_K0];
+    *k0 = ns.k;
+    *balanced = c.h_pinned[F_UNBALANCED] ? 0 : 1;
+    return W1G_OK;
+}
+
+int dc_run(Ctx &c, double delta, double pitch, double half_width, uint64_t seed, int64_t *kout) {
+    NodeSet &src = c.nodes[0], &dst = c.nodes[1];
+    const int64_t k = src.k;
+    dst.abar = src.abar;
+    dst.bbar = src.bbar;
+    if (delta == 0.0 || k == 0) {
+        // condensation.py:111-112: identity
+        double2 *p;
+        int64_t *a, *b;
+        W1G_TRY(ensure(dst.pts, k, &p));
+        W1G_TRY(ensure(dst.am, k, &a));
+        W1G_TRY(ensure(dst.bm, k, &b));
+        if (k) {
+            W1G_CUDA(cudaMemcpyAsync(p, src.pts.p, sizeof(double2) * k, cudaMemcpyDeviceToDevice, c.stream));
+            W1G_CUDA(cudaMemcpyAsync(a, src.am.p, sizeof(int64_t) * k, cudaMemcpyDeviceToDevice, c.stream));
+            W1G_CUDA(cudaMemcpyAsync(b, src.bm.p, sizeof(int64_t) * k, cudaMemcpyDeviceToDevice, c.stream));
+        }
+        dst.k = k;
+        dst.valid = true;
+        *kout = k;
+        return W1G_OK;
+    }
+    longlong2 *cells;
+    uint64_t *k0, *k1;
+    uint32_t *vals;
+    int64_t *excl;
+    W1G_TRY(ensure(c.scr[4], k, &cells));
+    W1G_TRY(ensure(c.scr[0], k, &k0));
+    W1G_TRY(ensure(c.scr[1], k, &k1));
+    W1G_TRY(ensure(c.scr[2], k, &vals));
+    W1G_TRY(ensure(c.scr[3], k, &excl));
+    W1G_TRY(flags_reset(c));
+    k_init_ranges<<<1, 1, 0, c.stream>>>(dflags(c));
+    k_dc_snap<<<gs(c, k), 256, 0, c.stream>>>(ptr<double2>(src.pts), k, pitch, cells, dflags(c));
+    W1G_CHECK_LAUNCH();
+    W1G_TRY(flags_fetch(c, 0, F_CELL_MIN + 4));
+    if (c.h_pinned[F_OVERFLOW]) {
+        set_error("lattice pitch too small for the coordinate range");
+        return W1G_EOVERFLOW;
+    }
+    const int64_t mnx = c.h_pinned[F_CELL_MIN + 0], mxx = c.h_pinned[F_CELL_MIN + 1];
+    const int64_t mny = c.h_pinned[F_CELL_MIN + 2], mxy = c.h_pinned[F_CELL_MIN + 3];
+    const uint64_t sx = (uint64_t)(mxx - mnx), sy = (uint64_t)(mxy - mny);
+    const int bx = sx ? 64 - __builtin_clzll(sx) : 0, by = sy ? 64 - __builtin_clzll(sy) : 0;
+    const int packed = (bx + by) <= 64;
+    k_dc_keys<<<gs(c, k), 256, 0, c.stream>>>(cells, k, packed, mnx, mny, by, k0, k1, vals);
+    W1G_CHECK_LAUNCH();
+    uint64_t *keys[2] = {k0, k1};
+    W1G_TRY(radix_sort(c, keys, packed ? 1 : 2, vals, k, packed ? (bx + by > 0 ? bx + by : 1) : 64));
+    DcFlag f{cells, vals};
+    W1G_TRY(scan_i64(c, f, k, excl, dflags(c) + F_TOTAL));
+    double2 *pts;
+    int64_t *am, *bm;
+    W1G_TRY(ensure(dst.pts, k, &pts));
+    W1G_TRY(ensure(dst.am, k, &am));
+    W1G_TRY(ensure(dst.bm, k, &bm));
+    W1G_CUDA(cudaMemsetAsync(am, 0, sizeof(int64_t) * k, c.stream));
+    W1G_CUDA(cudaMemsetAsync(bm, 0, sizeof(int64_t) * k, c.stream));
+    // base = splitmix64(seed & 0xFFFF_FFFF_FFFF_FFFF), condensation.py:96 (host, same arithmetic)
+    uint64_t x = seed + 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    const uint64_t base = x ^ (x >> 31);
+    k_dc_emit<<<gs(c, k), 256, 0, c.stream>>>(f, k, excl, ptr<int64_t>(src.am), ptr<int64_t>(src.bm),
+                                              pitch, half_width, base, pts, am, bm);
+    W1G_CHECK_LAUNCH();
+    W1G_TRY(flags_fetch(c, F_TOTAL, 1));
+    dst.k = c.h_pinned[F_TOTAL];
+    dst.valid = true;
+    *kout = dst.k;
+    return W1G_OK;
+}
+
+}  // namespace w1g

@@ -1,0 +1,149 @@
+"""Persistence diagrams and 0-condensation (reference: w1flow/diagram.py).
+
+`zero_condense` runs on the B200 (condense.cu: 128-bit key radix sort,
+run-length unique, per-side multiplicities); the dataclasses and validation
+mirror the reference so objects flow unchanged into the rest of the API.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+from typing import Iterable, Iterator, NamedTuple
+
+import numpy as np
+
+from . import _lib
+
+SQRT2 = math.sqrt(2.0)
+
+
+class DiagramFormatError(ValueError):
+    """Invalid diagram content (diagram.py:20-21)."""
+
+
+class PDPoint(NamedTuple):
+    birth: float
+    death: float
+
+
+def diagonal_distance(p: PDPoint) -> float:
+    """(death - birth)/sqrt(2), diagram.py:35-37 (scalar helper)."""
+    return (p.death - p.birth) / SQRT2
+
+
+def diagonal_projection(p: PDPoint) -> tuple[float, float]:
+    """((b+d)/2, (b+d)/2), diagram.py:29-32 (scalar helper)."""
+    m = 0.5 * (p.birth + p.death)
+    return (m, m)
+
+
+class PersistenceDiagram:
+    """Finite multiset of (birth, death) points with death > birth (diagram.py:57-95)."""
+
+    __slots__ = ("points",)
+
+    def __init__(self, points: Iterable | np.ndarray = ()):
+        pts = np.asarray(points, dtype=np.float64)
+        if pts.size == 0:
+            pts = np.empty((0, 2), dtype=np.float64)
+        if pts.ndim != 2 or pts.shape[1] != 2:
+            raise DiagramFormatError("expected an (n, 2) array of (birth, death) pairs")
+        if not np.all(np.isfinite(pts)):
+            raise DiagramFormatError("non-finite coordinate in diagram")
+        if np.any(pts[:, 1] <= pts[:, 0]):
+            raise DiagramFormatError("every point must satisfy death > birth")
+        self.points = pts
+
+    def __len__(self) -> int:
+        return self.points.shape[0]
+
+    def __iter__(self) -> Iterator[PDPoint]:
+        for b, d in self.points:
+            yield PDPoint(float(b), float(d))
+
+    def __eq__(self, other) -> bool:
+        if not isinstance(other, PersistenceDiagram):
+            return NotImplemented
+        if len(self) != len(other):
+            return False
+        a = self.points[np.lexsort((self.points[:, 1], self.points[:, 0]))]
+        b = other.points[np.lexsort((other.points[:, 1], other.points[:, 0]))]
+        return bool(np.array_equal(a, b))
+
+    def __repr__(self) -> str:
+        return f"PersistenceDiagram({len(self)} points)"
+
+
+def points_of(d) -> np.ndarray:
+    """(n, 2) float64 C-contiguous points of a diagram-like object."""
+    pts = d.points if hasattr(d, "points") else d
+    return _lib.as_points(pts)
+
+
+@dataclass(frozen=True)
+class SuppliedNodes:
+    """Deduplicated planar nodes with per-side integer masses (diagram.py:150-187)."""
+
+    points: np.ndarray  # (k, 2) float64, pairwise distinct
+    a_mass: np.ndarray  # (k,) int64
+    b_mass: np.ndarray  # (k,) int64
+    abar_supply: int
+    bbar_supply: int
+
+    @property
+    def supply(self) -> np.ndarray:
+        return self.a_mass - self.b_mass
+
+    @property
+    def a_member(self) -> np.ndarray:
+        return self.a_mass > 0
+
+    @property
+    def b_member(self) -> np.ndarray:
+        return self.b_mass > 0
+
+    def n_points(self) -> int:
+        return int(self.a_mass.sum() + self.b_mass.sum())
+
+    def total_balance(self) -> int:
+        return int(self.supply.sum()) + self.abar_supply + self.bbar_supply
+
+
+def _empty_nodes(abar: int = 0, bbar: int = 0) -> SuppliedNodes:
+    z = np.zeros(0, dtype=np.int64)
+    return SuppliedNodes(np.empty((0, 2), dtype=np.float64), z, z.copy(), abar, bbar)
+
+
+def fetch_nodes(ctx, slot: int, abar: int, bbar: int) -> SuppliedNodes:
+    k = ctypes.c_int64(0)
+    ctx.call("w1g_nodes_size", slot, ctypes.byref(k))
+    k = int(k.value)
+    pts = np.empty((k, 2), dtype=np.float64)
+    am = np.empty(k, dtype=np.int64)
+    bm = np.empty(k, dtype=np.int64)
+    if k:
+        ctx.call("w1g_fetch_nodes", slot, _lib.f64p(pts), _lib.i64p(am), _lib.i64p(bm))
+    return SuppliedNodes(pts, am, bm, abar, bbar)
+
+
+def load_nodes(ctx, slot: int, nodes: SuppliedNodes) -> None:
+    pts = _lib.as_points(nodes.points)
+    am = _lib.as_i64(nodes.a_mass)
+    bm = _lib.as_i64(nodes.b_mass)
+    ctx.call("w1g_load_nodes", slot, _lib.f64p(pts), _lib.i64p(am), _lib.i64p(bm), pts.shape[0],
+             int(nodes.abar_supply), int(nodes.bbar_supply))
+
+
+def zero_condense(a, b, device: int | None = None) -> SuppliedNodes:
+    """Merge coincident points of both diagrams (diagram.py:190-208), on device."""
+    ap, bp = points_of(a), points_of(b)
+    na, nb = ap.shape[0], bp.shape[0]
+    if na + nb == 0:
+        return _empty_nodes()
+    ctx = _lib.context(device)
+    k0 = ctypes.c_int64(0)
+    bal = ctypes.c_int32(0)
+    ctx.call("w1g_zero_condense", _lib.f64p(ap), na, _lib.f64p(bp), nb, ctypes.byref(k0), ctypes.byref(bal))
+    return fetch_nodes(ctx, _lib.NODES0, -na, nb)

@@ -1,0 +1,217 @@
+"""Top-level approximate W1 (reference: w1flow/pipeline.py:28-142).
+
+`approx_w1` is the reference's entry point with the sparsify front end
+(pipeline.py:105-130: zero_condense -> rwmd -> compute_delta ->
+delta_condense -> build_split_tree -> build_wspd -> emit_arcs -> assemble)
+fused into one device-resident call (w1g_front_end), followed by the
+reference's own host network simplex.  Additions required by the north
+star: an optional fixed `delta` in ApproxParams, `sparsify` (front end
+only) and `pairwise_w1` (batched matrix, pairs sharded over devices).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+from concurrent.futures import ThreadPoolExecutor
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib, solver
+from .diagram import points_of
+from .network import TransshipmentNetwork, fetch_network
+
+GUARANTEE_MIN_S = 2.0
+
+
+@dataclass(frozen=True)
+class ApproxParams:
+    """Knobs for one approximate distance computation (pipeline.py:28-50).
+
+    `delta` (new): None derives the lattice pitch from the RWMD bound as the
+    reference does (pipeline.py:116-122); a float fixes it.  `k` is the
+    lattice fraction of CondensationParams (condensation.py:42)."""
+
+    s: float
+    use_condensation: bool = True
+    seed: int = 0
+    best_effort: bool = False
+    block_size: int | None = None
+    stop_c: float = 4.0
+    stop_b: float = 1e5
+    threads: int = 1
+    delta: float | None = None
+    k: float = 0.99
+
+    def __post_init__(self):
+        if self.s <= 0:
+            raise ValueError("s must be positive")
+        if self.s <= GUARANTEE_MIN_S and not self.best_effort:
+            raise ValueError(
+                "s <= 2 has no approximation guarantee; pass best_effort=True to acknowledge"
+            )
+        if self.threads < 1:
+            raise ValueError("threads must be >= 1")
+        if self.delta is not None and self.delta < 0:
+            raise ValueError("delta must be nonnegative")
+        if not (0.5 <= self.k < 1.0):
+            raise ValueError("k must lie in [0.5, 1)")
+
+
+@dataclass
+class ApproxDiagnostics:
+    """pipeline.py:53-64, plus device-side detail of the front end."""
+
+    n_nodes: int = 0
+    n_arcs: int = 0
+    lower_bound: float = 0.0
+    epsilon_condense: float = 0.0
+    delta: float = 0.0
+    node_drop_pct: float = 0.0
+    pivots: int = 0
+    blocks_searched: int = 0
+    status: str = solver.OPTIMAL
+    short_circuit: bool = False
+    # additions
+    n_pairs: int = 0
+    tree_depth: int = 0
+    stage_ms: dict = field(default_factory=dict)
+
+
+def condensation_epsilon(s: float) -> float:
+    """pipeline.py:67-69."""
+    return 8.0 / (s - 4.0) if s >= 12 else 1.0
+
+
+def total_error_factor(s: float) -> float:
+    """pipeline.py:72-76."""
+    if s <= 4:
+        raise ValueError("the error expression requires s > 4")
+    return (1.0 + 4.0 / s + 4.0 / (s - 2.0)) * (1.0 + 8.0 / (s - 4.0)) - 1.0
+
+
+def s_from_error(eps_target: float) -> int:
+    """pipeline.py:79-95."""
+    if eps_target <= 0:
+        raise ValueError("target error must be positive")
+    lo = 12
+    if total_error_factor(lo) <= eps_target:
+        return lo
+    hi = lo
+    while total_error_factor(hi) > eps_target:
+        hi *= 2
+    while hi - lo > 1:
+        mid = (lo + hi) // 2
+        if total_error_factor(mid) <= eps_target:
+            hi = mid
+        else:
+            lo = mid
+    return hi
+
+
+def _front_end(ctx, ap: np.ndarray, bp: np.ndarray, params: ApproxParams) -> _lib.FrontEndInfo:
+    info = _lib.FrontEndInfo()
+    fixed = params.delta is not None
+    ctx.call("w1g_front_end", _lib.f64p(ap), ap.shape[0], _lib.f64p(bp), bp.shape[0], float(params.s),
+             1 if params.use_condensation else 0, 1 if fixed else 0,
+             float(params.delta) if fixed else 0.0, float(params.k),
+             ctypes.c_uint64(int(params.seed) & 0xFFFFFFFFFFFFFFFF), ctypes.byref(info))
+    return info
+
+
+def _diagnostics(info: _lib.FrontEndInfo) -> ApproxDiagnostics:
+    d = ApproxDiagnostics()
+    if info.short_circuit:
+        d.short_circuit = True
+        return d
+    d.lower_bound = info.lower_bound
+    d.epsilon_condense = info.epsilon_condense
+    d.delta = info.delta
+    d.node_drop_pct = 100.0 * (1.0 - info.n_points / info.n_points0)
+    d.n_nodes = int(info.node_count)
+    d.n_arcs = int(info.n_arcs)
+    d.n_pairs = int(info.n_pairs)
+    d.tree_depth = int(info.tree_depth)
+    d.stage_ms = {name: float(info.stage_ms[i]) for i, name in enumerate(_lib.STAGES)}
+    return d
+
+
+def sparsify(a, b, params: ApproxParams, device: int | None = None
+             ) -> tuple[TransshipmentNetwork | None, ApproxDiagnostics]:
+    """The sparsify front end alone (pipeline.py:105-130): the network that
+    approx_w1 hands to the solver, or None when the distance short-circuits."""
+    ap, bp = points_of(a), points_of(b)
+    ctx = _lib.context(device)
+    info = _front_end(ctx, ap, bp, params)
+    diag = _diagnostics(info)
+    if info.short_circuit:
+        return None, diag
+    return fetch_network(ctx, int(info.node_count), int(info.n_arcs)), diag
+
+
+def solve_network(network: TransshipmentNetwork, params: ApproxParams, diag: ApproxDiagnostics) -> float:
+    """Run the reference's host simplex on a device-built network (pipeline.py:133-142)."""
+    result = solver.solve(network, block_size=params.block_size, stop_c=params.stop_c, stop_b=params.stop_b)
+    diag.pivots = result.pivots
+    diag.blocks_searched = result.blocks_searched
+    diag.status = result.status
+    return result.objective
+
+
+def approx_w1(a, b, params: ApproxParams, device: int | None = None) -> tuple[float, ApproxDiagnostics]:
+    """Approximate W1(a, b) with sparsity parameter params.s (pipeline.py:98-142)."""
+    network, diag = sparsify(a, b, params, device)
+    if network is None:
+        return 0.0, diag
+    return solve_network(network, params, diag), diag
+
+
+def _devices(devices):
+    if devices is None:
+        n = _lib.device_count()
+        return list(range(max(n, 1)))
+    return list(devices)
+
+
+def pair_shard(n_diagrams: int, rank: int, world: int) -> list[tuple[int, int]]:
+    """Static round-robin of the unordered pairs i<j over `world` workers."""
+    pairs = [(i, j) for i in range(n_diagrams) for j in range(i + 1, n_diagrams)]
+    return pairs[rank::world]
+
+
+def pairwise_w1(diagrams, params: ApproxParams, devices=None, solver_threads: int | None = None,
+                pairs: list[tuple[int, int]] | None = None) -> np.ndarray:
+    """Symmetric matrix of approx_w1(D[i], D[j]) for i < j, mirrored to (j, i).
+
+    Pairs are sharded round-robin over `devices` (one host thread and one
+    context per device, no collective); each device's networks go to a pool
+    of `solver_threads` host threads running the reference solver (numba,
+    GIL released).  `pairs` restricts the work to a subset (other entries NaN).
+    """
+    pts = [points_of(d) for d in diagrams]
+    n = len(pts)
+    devs = _devices(devices)
+    todo = pairs if pairs is not None else [(i, j) for i in range(n) for j in range(i + 1, n)]
+    out = np.full((n, n), np.nan)
+    np.fill_diagonal(out, 0.0)
+    if solver_threads is None:
+        solver_threads = max(1, (os.cpu_count() or 1) - len(devs))
+    pool = ThreadPoolExecutor(max_workers=solver_threads)
+    futures = []
+
+    def device_worker(dev: int, mine: list[tuple[int, int]]):
+        for i, j in mine:
+            net, diag = sparsify(pts[i], pts[j], params, device=dev)
+            if net is None:
+                out[i, j] = out[j, i] = 0.0
+                continue
+            futures.append((i, j, pool.submit(solve_network, net, params, diag)))
+
+    with ThreadPoolExecutor(max_workers=len(devs)) as dpool:
+        list(dpool.map(lambda k: device_worker(devs[k], todo[k::len(devs)]), range(len(devs))))
+    for i, j, f in futures:
+        out[i, j] = out[j, i] = f.result()
+    pool.shutdown()
+    return out
