@@ -71,6 +71,9 @@ uint64_t w1g_launch_count(void);
  * CUDA events on the context stream; returns the mean device time per launch
  * and the directed (source, target) evaluations one launch covers */
 int w1g_profile_rwmd_tile(w1g_ctx *ctx, int reps, float *ms_per_launch, int64_t *evals_per_launch);
+/* test hook: stable device radix sort of host keys (`words` arrays of n
+ * uint64, word 0 least significant); writes the sorting permutation */
+int w1g_debug_radix_sort(w1g_ctx *ctx, const uint64_t *keys, int words, int64_t n, uint32_t *perm);
 int w1g_device_count(int *count);
 const char *w1g_last_error(void);
 

@@ -72,6 +72,7 @@ _PROTOS = [
     ("w1g_version", ctypes.c_int, []),
     ("w1g_launch_count", ctypes.c_uint64, []),
     ("w1g_profile_rwmd_tile", ctypes.c_int, [_vp, ctypes.c_int, ctypes.POINTER(ctypes.c_float), _I64P]),
+    ("w1g_debug_radix_sort", ctypes.c_int, [_vp, _vp, ctypes.c_int, _i64, _vp]),
     ("w1g_device_count", ctypes.c_int, [_I32P]),
     ("w1g_last_error", ctypes.c_char_p, []),
     ("w1g_ctx_create", ctypes.c_int, [ctypes.c_int, ctypes.POINTER(_vp)]),

@@ -126,6 +126,7 @@ struct Ctx {
     // scratch
     DevBuf scr[SCR_N];
     DevBuf sort_scr[8];
+    unsigned sort_epoch = 0;  // onesweep status-word epoch (sort.cu)
     DevBuf scan_state;
     DevBuf flags;  // small device flag block (int64 x 64)
     int64_t *h_pinned = nullptr;  // pinned host mirror of `flags`
@@ -200,7 +201,10 @@ int scan_prepare(Ctx &c, int64_t n, ScanArgs *a, int64_t *n_tiles);
 
 template <class F>
 __global__ void __launch_bounds__(SCAN_BLOCK) k_scan_i64(F f, int64_t n, int64_t *out,
-                                                        int64_t *total, ScanArgs a) {
+                                                        int64_t *total, ScanArgs a,
+                                                        const int32_t *live) {
+    // `live` (optional): a device counter; when it is 0 the whole scan is a no-op
+    if (live && *live == 0) return;
     __shared__ unsigned int s_tile;
     __shared__ int64_t s_warp[SCAN_BLOCK / 32];
     __shared__ int64_t s_prefix;
@@ -239,26 +243,39 @@ __global__ void __launch_bounds__(SCAN_BLOCK) k_scan_i64(F f, int64_t n, int64_t
     const int64_t warp_excl = wid ? s_warp[wid - 1] : 0;
     const int64_t excl = warp_excl + x - tsum;
     const int64_t agg = s_warp[SCAN_BLOCK / 32 - 1];
-    if (threadIdx.x == 0) {
+    if (wid == 0) {
+        // warp-parallel decoupled look-back: 32 predecessors per memory round trip
         constexpr unsigned long long FA = 1ull << 62, FP = 2ull << 62, MASK = (1ull << 62) - 1;
         if (tile == 0) {
-            atomicExch(&a.status[0], FP | (unsigned long long)agg);
-            s_prefix = 0;
+            if (lane == 0) {
+                atomicExch(&a.status[0], FP | (unsigned long long)agg);
+                s_prefix = 0;
+            }
         } else {
-            atomicExch(&a.status[tile], FA | (unsigned long long)agg);
+            if (lane == 0) atomicExch(&a.status[tile], FA | (unsigned long long)agg);
             int64_t prefix = 0;
             int64_t j = tile - 1;
             while (true) {
-                unsigned long long st = *((volatile unsigned long long *)&a.status[j]);
-                if ((st >> 62) == 0) continue;
-                __threadfence();
-                prefix += (int64_t)(st & MASK);
-                if ((st >> 62) == 2) break;
-                j--;
+                const int64_t idx = j - lane;
+                const unsigned long long st =
+                    idx >= 0 ? *((volatile unsigned long long *)&a.status[idx]) : FP;  // before tile 0: prefix 0
+                const unsigned kind = (unsigned)(st >> 62);
+                const unsigned inc = __ballot_sync(0xffffffffu, kind == 2);
+                const unsigned unpub = __ballot_sync(0xffffffffu, kind == 0);
+                const int first = inc ? __ffs(inc) - 1 : 31;
+                const unsigned need = (2u << first) - 1u;  // lanes 0..first
+                if (unpub & need) continue;                // someone in range not published: re-poll
+                int64_t v = lane <= first ? (int64_t)(st & MASK) : 0;
+#pragma unroll
+                for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                prefix += v;
+                if (inc) break;
+                j -= 32;
             }
-            __threadfence();
-            atomicExch(&a.status[tile], FP | (unsigned long long)(prefix + agg));
-            s_prefix = prefix;
+            if (lane == 0) {
+                atomicExch(&a.status[tile], FP | (unsigned long long)(prefix + agg));
+                s_prefix = prefix;
+            }
         }
     }
     __syncthreads();
@@ -275,11 +292,11 @@ __global__ void __launch_bounds__(SCAN_BLOCK) k_scan_i64(F f, int64_t n, int64_t
 }
 
 template <class F>
-int scan_i64(Ctx &c, F f, int64_t n, int64_t *out, int64_t *total) {
+int scan_i64(Ctx &c, F f, int64_t n, int64_t *out, int64_t *total, const int32_t *live = nullptr) {
     ScanArgs a;
     int64_t tiles;
     W1G_TRY(scan_prepare(c, n, &a, &tiles));
-    k_scan_i64<F><<<(unsigned)tiles, SCAN_BLOCK, 0, c.stream>>>(f, n, out, total, a);
+    k_scan_i64<F><<<(unsigned)tiles, SCAN_BLOCK, 0, c.stream>>>(f, n, out, total, a, live);
     W1G_CHECK_LAUNCH();
     return W1G_OK;
 }

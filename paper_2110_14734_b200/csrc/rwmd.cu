@@ -5,26 +5,33 @@
 // value per source is best = min(sqrt(min_j fl(fl(dx^2)+fl(dy^2))), diag)
 // (cKDTree distance, np.minimum) and L_X = np.sum(mass * best) in node order.
 //
-//  1. FP32 all-pairs tile pass (rwmd_tile.cu) gives every source an
-//     approximate squared NN distance with a rigorous error bound;
-//  2. an exact fp64 pass scans only the targets inside that bound (uniform
-//     cell grid over the targets, counting-sorted on device) and computes
-//     the reference's exact IEEE distance, then mass * best;
-//  3. numpy's pairwise summation tree (loops_utils.h.src pairwise_sum) is
-//     rebuilt level by level on device and evaluated leaf-first, so L_X is
+//  1. members of each side are put in Morton order (radix sort of 32-bit
+//     codes), so CTAs of sources and tiles of targets are spatially compact;
+//  2. the FP32 all-pairs tile pass (rwmd_tile.cu) gives every source a
+//     squared-distance estimate with a rigorous error bound -> a radius that
+//     provably contains the exact nearest target;
+//  3. an exact fp64 pass per source block keeps only the 64-target Morton
+//     tiles within that radius (box test) and evaluates the reference's IEEE
+//     distance on them, then mass * best in node order;
+//  4. numpy's pairwise summation tree (pairwise_sum.cu) makes L_X
 //     bit-identical to np.sum.
 #include <cmath>
+#include <cstring>
 
 #include "common.cuh"
 
 namespace w1g {
 
-int rwmd_f32_min(Ctx &c, const float2 *q, int64_t nq, const float2 *t, int64_t nt, unsigned *mout,
-                 int culling);
+int rwmd_f32_min(Ctx &c, const double2 *q, int64_t nq, const double2 *t, int64_t nt, double scale,
+                 unsigned *mout, float *qn_out, double4 *tbox, int culling);
+int pairwise_sum(Ctx &c, const double *d_v, int64_t n, double *d_out, DevBuf &nodes_buf,
+                 DevBuf &val_buf, DevBuf &lev_buf);
 
 static const double SQRT2 = 1.4142135623730951;  // math.sqrt(2.0), diagram.py:17
 
 namespace {
+
+constexpr int RT = 64;  // targets per refine tile
 
 struct MemberFlag {
     const int64_t *mass;
@@ -35,6 +42,14 @@ __global__ void k_compact(const int64_t *mass, int64_t k, const int64_t *excl, i
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < k;
          i += (int64_t)gridDim.x * blockDim.x)
         if (mass[i] > 0) out[excl[i]] = (int32_t)i;
+}
+
+__global__ void k_bbox_init(int64_t *f) {
+    unsigned long long *u = (unsigned long long *)f;
+    u[F_BBOX + 0] = ~0ull;
+    u[F_BBOX + 1] = 0;
+    u[F_BBOX + 2] = ~0ull;
+    u[F_BBOX + 3] = 0;
 }
 
 __global__ void k_bbox(const double2 *pts, int64_t k, int64_t *f) {
@@ -63,252 +78,187 @@ __global__ void k_bbox(const double2 *pts, int64_t k, int64_t *f) {
     }
 }
 
-__global__ void k_bbox_init(int64_t *f) {
-    unsigned long long *u = (unsigned long long *)f;
-    u[F_BBOX + 0] = ~0ull;
-    u[F_BBOX + 1] = 0;
-    u[F_BBOX + 2] = ~0ull;
-    u[F_BBOX + 3] = 0;
+__device__ __forceinline__ uint32_t spread16(uint32_t v) {
+    v &= 0xffff;
+    v = (v | (v << 8)) & 0x00ff00ff;
+    v = (v | (v << 4)) & 0x0f0f0f0f;
+    v = (v | (v << 2)) & 0x33333333;
+    v = (v | (v << 1)) & 0x55555555;
+    return v;
 }
 
-__global__ void k_to_f32(const double2 *pts, const int32_t *idx, int64_t n, double cx, double cy,
-                         double scale, float2 *out) {
+// Morton code on a 65536^2 grid over the node bbox; payload = member position
+__global__ void k_morton(const double2 *pts, const int32_t *members, int64_t n, double x0, double y0,
+                         double inv, uint64_t *key, uint32_t *val) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
-        double2 p = pts[idx[i]];
-        out[i] = make_float2((float)((p.x - cx) * scale), (float)((p.y - cy) * scale));
+        const double2 p = pts[members[i]];
+        double fx = (p.x - x0) * inv, fy = (p.y - y0) * inv;
+        fx = fx < 0 ? 0 : (fx > 65535.0 ? 65535.0 : fx);
+        fy = fy < 0 ? 0 : (fy > 65535.0 ? 65535.0 : fy);
+        key[i] = (uint64_t)(spread16((uint32_t)fx) | (spread16((uint32_t)fy) << 1));
+        val[i] = (uint32_t)i;
     }
 }
 
-struct Grid {
-    double x0, y0, inv_c;
-    int gx, gy;
-};
-
-__device__ __forceinline__ int cell_coord(double v, double v0, double inv_c, int g) {
-    double f = floor((v - v0) * inv_c);
-    if (!(f >= 0.0)) f = 0.0;
-    if (f > (double)(g - 1)) f = (double)(g - 1);
-    return (int)f;
-}
-
-__global__ void k_cell_count(const double2 *pts, const int32_t *idx, int64_t n, Grid g,
-                             int32_t *cell, int64_t *counts) {
+__global__ void k_gather_members(const double2 *pts, const int32_t *members, const uint32_t *perm,
+                                  int64_t n, double2 *out, int32_t *pos) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
-        double2 p = pts[idx[i]];
-        int c = cell_coord(p.y, g.y0, g.inv_c, g.gy) * g.gx + cell_coord(p.x, g.x0, g.inv_c, g.gx);
-        cell[i] = c;
-        atomicAdd((unsigned long long *)&counts[c], 1ull);
+        const uint32_t m = perm[i];
+        out[i] = pts[members[m]];
+        pos[i] = (int32_t)m;
     }
 }
 
-struct CountVal {
-    const int64_t *counts;
-    __device__ int64_t operator()(int64_t i) const { return counts[i]; }
-};
-
-__global__ void k_cell_fill(const double2 *pts, const int32_t *idx, int64_t n, const int32_t *cell,
-                            int64_t *cursor, double2 *sorted) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        int64_t pos = (int64_t)atomicAdd((unsigned long long *)&cursor[cell[i]], 1ull);
-        sorted[pos] = pts[idx[i]];
+__global__ void k_boxes64(const double2 *t, int64_t nt, double4 *box) {
+    const int lane = threadIdx.x & 31;
+    const int64_t ntile = (nt + RT - 1) / RT;
+    for (int64_t tile = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; tile < ntile;
+         tile += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        double x0 = INFINITY, y0 = INFINITY, x1 = -INFINITY, y1 = -INFINITY;
+        const int64_t te = min(nt, (tile + 1) * RT);
+        for (int64_t j = tile * RT + lane; j < te; j += 32) {
+            const double2 p = t[j];
+            x0 = fmin(x0, p.x);
+            y0 = fmin(y0, p.y);
+            x1 = fmax(x1, p.x);
+            y1 = fmax(y1, p.y);
+        }
+        for (int o = 16; o; o >>= 1) {
+            x0 = fmin(x0, __shfl_xor_sync(0xffffffffu, x0, o));
+            y0 = fmin(y0, __shfl_xor_sync(0xffffffffu, y0, o));
+            x1 = fmax(x1, __shfl_xor_sync(0xffffffffu, x1, o));
+            y1 = fmax(y1, __shfl_xor_sync(0xffffffffu, y1, o));
+        }
+        if (lane == 0) box[tile] = make_double4(x0, y0, x1, y1);
     }
 }
 
-// exact fp64 refinement + mass * best (lower_bound.py:51-58)
-__global__ void __launch_bounds__(128) k_refine(const double2 *pts, const int32_t *src_idx,
-                                                const int64_t *mass, int64_t ns, const unsigned *mf32,
-                                                int has_targets, double unscale, Grid g,
-                                                const int64_t *cell_start, const double2 *tsorted,
-                                                double *best_out, double *terms) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ns;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t node = src_idx[i];
-        const double2 q = pts[node];
-        const double diag = ddiv(fabs(dsub(q.y, q.x)), SQRT2);  // diagram.py:47
-        double best = diag;
-        if (has_targets) {
-            // FP32 bound: |d_f32 - d| <= 2^-21 (1 + d) in scaled units; use 2^-19
-            const double df = sqrt((double)__uint_as_float(mf32[i]));
-            const double lo = (df - 0x1p-19) * (1.0 - 0x1p-19) * unscale;
-            if (!(lo > diag * (1.0 + 1e-12))) {
-                const double R = (df + 0x1p-19) * (1.0 + 0x1p-19) * unscale * (1.0 + 1e-12);
-                const int cx0 = cell_coord(q.x - R, g.x0, g.inv_c, g.gx) - 1;
-                const int cx1 = cell_coord(q.x + R, g.x0, g.inv_c, g.gx) + 1;
-                const int cy0 = cell_coord(q.y - R, g.y0, g.inv_c, g.gy) - 1;
-                const int cy1 = cell_coord(q.y + R, g.y0, g.inv_c, g.gy) + 1;
-                double m2 = INFINITY;
-                for (int cy = max(cy0, 0); cy <= min(cy1, g.gy - 1); cy++) {
-                    const int64_t rs = cell_start[(int64_t)cy * g.gx + max(cx0, 0)];
-                    const int64_t re = cell_start[(int64_t)cy * g.gx + min(cx1, g.gx - 1) + 1];
-                    for (int64_t p = rs; p < re; p++) {
-                        const double2 t = tsorted[p];
-                        const double dx = dsub(q.x, t.x), dy = dsub(q.y, t.y);
+__device__ __forceinline__ double box_gap(double4 b, double4 a) {
+    const double gx = fmax(0.0, fmax(b.x - a.z, a.x - b.z));
+    const double gy = fmax(0.0, fmax(b.y - a.w, a.y - b.w));
+    return sqrt(gx * gx + gy * gy);
+}
+
+// Rigorous upper bound (scaled units) on the distance from a source to the
+// target that produced its FP32 estimate `est` in the local frame of
+// rwmd_tile.cu, where |x| = qn is the source's local radius.  With
+// u = 2^-24 and D~ the distance of the rounded local coordinates:
+//   |est - D~^2| <= 5u (2|x| + D~)^2          (expanded form, FFMA/FFMA2)
+//   |D - D~|     <= u (2|x| + D~)              (one rounding per coordinate)
+// so with c = 2^-20 >= 5u:  D~ <= (sqrt(est) + 2 sqrt(c) |x|) / (1 - sqrt(c)).
+__device__ __forceinline__ double upper_bound(float est, float qn) {
+    const double x = (double)qn * (1.0 + 0x1p-20) + 0x1p-60;
+    const double dt = (sqrt(fmax((double)est, 0.0)) + 0x1p-9 * x) / (1.0 - 0x1p-10);
+    return dt * (1.0 + 0x1p-20) + 0x1p-20 * x + 0x1p-40;
+}
+
+constexpr int RF_BLOCK = 128;
+constexpr int RF_CAND = 2048;
+
+// exact fp64 refinement + mass * best (lower_bound.py:51-58); one source per
+// thread, sources in Morton order, target tiles kept by a box test
+__global__ void __launch_bounds__(RF_BLOCK) k_refine(const double2 *__restrict__ q, const int32_t *__restrict__ qpos,
+                                                     const int32_t *__restrict__ members,
+                                                     const int64_t *__restrict__ mass, int64_t nq,
+                                                     const unsigned *__restrict__ mf32,
+                                                     const float *__restrict__ qn, double unscale,
+                                                     const double2 *__restrict__ t, int64_t nt,
+                                                     const double4 *__restrict__ tbox,
+                                                     double *__restrict__ best_out, double *__restrict__ terms) {
+    __shared__ int32_t s_cand[RF_CAND];
+    __shared__ int s_nc;
+    __shared__ double s_r[RF_BLOCK / 32];
+    __shared__ double4 s_box[RF_BLOCK / 32];
+    __shared__ double4 s_qb;
+    __shared__ double s_rmax;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int64_t i = (int64_t)blockIdx.x * RF_BLOCK + tid;
+    const bool valid = i < nq;
+    double2 p = make_double2(0, 0);
+    double diag = 0.0, r = -1.0;
+    if (valid) {
+        p = q[i];
+        diag = ddiv(fabs(dsub(p.y, p.x)), SQRT2);  // diagram.py:47
+        if (nt > 0) {
+            const double U = upper_bound(__uint_as_float(mf32[i]), qn[i]) * unscale * (1.0 + 1e-9);
+            r = fmin(U, diag * (1.0 + 1e-12));
+            r += 0x1p-50 * (fabs(p.x) + fabs(p.y) + r) + 1e-300;
+        }
+    }
+    double m2 = INFINITY;
+    if (nt > 0) {
+        // block bbox and radius
+        double4 b = valid ? make_double4(p.x, p.y, p.x, p.y) : make_double4(INFINITY, INFINITY, -INFINITY, -INFINITY);
+        double rm = r;
+        for (int o = 16; o; o >>= 1) {
+            b.x = fmin(b.x, __shfl_xor_sync(0xffffffffu, b.x, o));
+            b.y = fmin(b.y, __shfl_xor_sync(0xffffffffu, b.y, o));
+            b.z = fmax(b.z, __shfl_xor_sync(0xffffffffu, b.z, o));
+            b.w = fmax(b.w, __shfl_xor_sync(0xffffffffu, b.w, o));
+            rm = fmax(rm, __shfl_xor_sync(0xffffffffu, rm, o));
+        }
+        if (lane == 0) {
+            s_box[wid] = b;
+            s_r[wid] = rm;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            double4 bb = s_box[0];
+            double rr = s_r[0];
+            for (int w = 1; w < RF_BLOCK / 32; w++) {
+                bb.x = fmin(bb.x, s_box[w].x);
+                bb.y = fmin(bb.y, s_box[w].y);
+                bb.z = fmax(bb.z, s_box[w].z);
+                bb.w = fmax(bb.w, s_box[w].w);
+                rr = fmax(rr, s_r[w]);
+            }
+            s_qb = bb;
+            s_rmax = rr * (1.0 + 1e-9);
+        }
+        __syncthreads();
+        const double4 qb = s_qb;
+        const double rmax = s_rmax;
+        const double4 pb = make_double4(p.x, p.y, p.x, p.y);
+        const int64_t ntile = (nt + RT - 1) / RT;
+        for (int64_t t0 = 0; t0 < ntile; t0 += RF_CAND) {
+            if (tid == 0) s_nc = 0;
+            __syncthreads();
+            const int64_t t1 = min(ntile, t0 + RF_CAND);
+            for (int64_t k = t0 + tid; k < t1; k += RF_BLOCK)
+                if (box_gap(tbox[k], qb) <= rmax) s_cand[atomicAdd(&s_nc, 1)] = (int32_t)k;
+            __syncthreads();
+            const int nc = s_nc;
+            if (valid && r >= 0.0) {
+                for (int c = 0; c < nc; c++) {
+                    const int64_t k = s_cand[c];
+                    if (box_gap(tbox[k], pb) > r * (1.0 + 1e-9)) continue;
+                    const int64_t te = min(nt, (k + 1) * RT);
+                    for (int64_t j = k * RT; j < te; j++) {
+                        const double2 tt = t[j];
+                        const double dx = dsub(p.x, tt.x), dy = dsub(p.y, tt.y);
                         const double d2 = dadd(dmul(dx, dx), dmul(dy, dy));
                         m2 = d2 < m2 ? d2 : m2;
                     }
                 }
-                const double nnd = dsqrt(m2);
-                best = nnd < diag ? nnd : diag;  // np.minimum(nnd, diag)
-            }
-        }
-        best_out[i] = best;
-        terms[i] = dmul(__ll2double_rn(mass[node]), best);  // float64(src_mass) * best
-    }
-}
-
-// ---------------------------------------------------------------- numpy pairwise sum
-struct PwNode {
-    int64_t start, len;
-    int32_t child;  // index of the left child (right = child + 1); -1 for a leaf
-    int32_t pad;
-};
-constexpr int PW_MAX_LEVELS = 64;
-
-__global__ void __launch_bounds__(1024) k_pw_build(int64_t n, PwNode *nodes, int32_t *levels,
-                                                   int32_t *n_levels) {
-    __shared__ int32_t s_warp[32];
-    __shared__ int32_t s_base;
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    if (threadIdx.x == 0) {
-        nodes[0].start = 0;
-        nodes[0].len = n;
-        levels[0] = 0;
-        levels[1] = 1;
-    }
-    __syncthreads();
-    int lo = 0, hi = 1, L = 0;
-    while (lo < hi && L < PW_MAX_LEVELS - 2) {
-        if (threadIdx.x == 0) s_base = 0;
-        __syncthreads();
-        for (int chunk = lo; chunk < hi; chunk += 1024) {
-            const int i = chunk + threadIdx.x;
-            const bool valid = i < hi;
-            const bool internal = valid && nodes[i].len > 128;
-            int cnt = internal ? 2 : 0;
-            int x = cnt;
-            for (int o = 1; o < 32; o <<= 1) {
-                int y = __shfl_up_sync(0xffffffffu, x, o);
-                if (lane >= o) x += y;
-            }
-            if (lane == 31) s_warp[wid] = x;
-            __syncthreads();
-            if (wid == 0) {
-                int w = s_warp[lane];
-                for (int o = 1; o < 32; o <<= 1) {
-                    int y = __shfl_up_sync(0xffffffffu, w, o);
-                    if (lane >= o) w += y;
-                }
-                s_warp[lane] = w;
             }
             __syncthreads();
-            const int off = s_base + (wid ? s_warp[wid - 1] : 0) + x - cnt;
-            if (valid) {
-                if (internal) {
-                    const int64_t len = nodes[i].len, st = nodes[i].start;
-                    int64_t n2 = len / 2;
-                    n2 -= n2 % 8;
-                    const int child = hi + off;
-                    nodes[child].start = st;
-                    nodes[child].len = n2;
-                    nodes[child + 1].start = st + n2;
-                    nodes[child + 1].len = len - n2;
-                    nodes[i].child = child;
-                } else {
-                    nodes[i].child = -1;
-                }
-            }
-            __syncthreads();
-            if (threadIdx.x == 0) s_base += s_warp[31];
-            __syncthreads();
-        }
-        const int nb = s_base;
-        lo = hi;
-        hi = hi + nb;
-        L++;
-        if (threadIdx.x == 0) levels[L + 1] = hi;
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) *n_levels = L;
-}
-
-// one warp per leaf: numpy's 8-accumulator block (n <= 128) or sequential (n < 8)
-__global__ void k_pw_leaves(const double *v, const PwNode *nodes, const int32_t *levels,
-                            const int32_t *n_levels, double *val) {
-    const int total = levels[*n_levels];
-    const int lane = threadIdx.x & 31;
-    for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < total;
-         i += (gridDim.x * blockDim.x) >> 5) {
-        const PwNode nd = nodes[i];
-        if (nd.child >= 0) continue;
-        const double *a = v + nd.start;
-        const int64_t len = nd.len;
-        if (len < 8) {
-            if (lane == 0) {
-                double res = 0.0;
-                for (int64_t j = 0; j < len; j++) res = dadd(res, a[j]);
-                val[i] = res;
-            }
-            continue;
-        }
-        double r = 0.0;
-        if (lane < 8) {
-            r = a[lane];
-            for (int64_t j = 8; j < len - (len % 8); j += 8) r = dadd(r, a[j + lane]);
-        }
-        double r0 = __shfl_sync(0xffffffffu, r, 0), r1 = __shfl_sync(0xffffffffu, r, 1);
-        double r2 = __shfl_sync(0xffffffffu, r, 2), r3 = __shfl_sync(0xffffffffu, r, 3);
-        double r4 = __shfl_sync(0xffffffffu, r, 4), r5 = __shfl_sync(0xffffffffu, r, 5);
-        double r6 = __shfl_sync(0xffffffffu, r, 6), r7 = __shfl_sync(0xffffffffu, r, 7);
-        if (lane == 0) {
-            double res = dadd(dadd(dadd(r0, r1), dadd(r2, r3)), dadd(dadd(r4, r5), dadd(r6, r7)));
-            for (int64_t j = len - (len % 8); j < len; j++) res = dadd(res, a[j]);
-            val[i] = res;
         }
     }
-}
-
-__global__ void __launch_bounds__(1024) k_pw_combine(const PwNode *nodes, const int32_t *levels,
-                                                     const int32_t *n_levels, double *val,
-                                                     double *out) {
-    const int L = *n_levels;
-    for (int l = L - 1; l >= 0; l--) {
-        for (int i = levels[l] + threadIdx.x; i < levels[l + 1]; i += blockDim.x) {
-            const int ch = nodes[i].child;
-            if (ch >= 0) val[i] = dadd(val[ch], val[ch + 1]);
+    if (valid) {
+        double best = diag;
+        if (nt > 0) {
+            const double nnd = dsqrt(m2);
+            best = nnd < diag ? nnd : diag;  // np.minimum(nnd, diag)
         }
-        __syncthreads();
+        const int32_t pos = qpos[i];
+        best_out[pos] = best;
+        terms[pos] = dmul(__ll2double_rn(mass[members[pos]]), best);  // float64(src_mass) * best
     }
-    if (threadIdx.x == 0) *out = val[0];
 }
 
 }  // namespace
-
-// np.sum of a contiguous float64 vector on device -> *d_out (device)
-int pairwise_sum(Ctx &c, const double *d_v, int64_t n, double *d_out, DevBuf &nodes_buf,
-                 DevBuf &val_buf, DevBuf &lev_buf) {
-    if (n == 0) {
-        W1G_CUDA(cudaMemsetAsync(d_out, 0, sizeof(double), c.stream));
-        return W1G_OK;
-    }
-    const int64_t cap = n / 32 + 64;
-    PwNode *nodes;
-    double *val;
-    int32_t *lev;
-    W1G_TRY(ensure(nodes_buf, (size_t)cap, &nodes));
-    W1G_TRY(ensure(val_buf, (size_t)cap, &val));
-    W1G_TRY(ensure(lev_buf, PW_MAX_LEVELS + 2, &lev));
-    k_pw_build<<<1, 1024, 0, c.stream>>>(n, nodes, lev, lev + PW_MAX_LEVELS);
-    W1G_CHECK_LAUNCH();
-    const unsigned warps = (unsigned)(n / 64 + 2);
-    k_pw_leaves<<<grid_for(warps * 32, 256, 4u * c.sm_count), 256, 0, c.stream>>>(d_v, nodes, lev, lev + PW_MAX_LEVELS, val);
-    W1G_CHECK_LAUNCH();
-    k_pw_combine<<<1, 1024, 0, c.stream>>>(nodes, lev, lev + PW_MAX_LEVELS, val, d_out);
-    W1G_CHECK_LAUNCH();
-    return W1G_OK;
-}
 
 static inline double key_to_double(uint64_t k) {
     uint64_t b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
@@ -317,61 +267,96 @@ static inline double key_to_double(uint64_t k) {
     return d;
 }
 
-int rwmd_run(Ctx &c, double *L, double *LA, double *LB) {
+// shared preparation: members, bbox frame, Morton order (per side)
+struct RwmdFrame {
+    int64_t nm[2];
+    double scale, unscale;
+    int32_t *members[2];
+    double2 *mpts[2];  // member points in Morton order
+    int32_t *mpos[2];  // member position (node order) of each Morton slot
+};
+
+static int rwmd_prepare(Ctx &c, RwmdFrame &F) {
     NodeSet &ns = c.nodes[0];
     const int64_t k = ns.k;
     const double2 *pts = ptr<double2>(ns.pts);
     const int64_t *mass[2] = {ptr<int64_t>(ns.am), ptr<int64_t>(ns.bm)};
-    if (k == 0) {
-        *L = *LA = *LB = 0.0;
-        c.n_best[0] = c.n_best[1] = 0;
-        return W1G_OK;
-    }
     int64_t *excl;
-    int32_t *members[2];
     W1G_TRY(ensure(c.scr[3], k, &excl));
-    W1G_TRY(ensure(c.scr[5], k, &members[0]));
-    W1G_TRY(ensure(c.scr[6], k, &members[1]));
+    W1G_TRY(ensure(c.scr[5], k, &F.members[0]));
+    W1G_TRY(ensure(c.scr[6], k, &F.members[1]));
     W1G_TRY(flags_reset(c));
     const unsigned g = grid_for(k, 256, 8u * c.sm_count);
     for (int s = 0; s < 2; s++) {
         W1G_TRY(scan_i64(c, MemberFlag{mass[s]}, k, excl, dflags(c) + F_MISC0 + s));
-        k_compact<<<g, 256, 0, c.stream>>>(mass[s], k, excl, members[s]);
+        k_compact<<<g, 256, 0, c.stream>>>(mass[s], k, excl, F.members[s]);
         W1G_CHECK_LAUNCH();
     }
     k_bbox_init<<<1, 1, 0, c.stream>>>(dflags(c));
     k_bbox<<<g, 256, 0, c.stream>>>(pts, k, dflags(c));
     W1G_CHECK_LAUNCH();
     W1G_TRY(flags_fetch(c, 0, F_BBOX + 4));
-    const int64_t nm[2] = {c.h_pinned[F_MISC0], c.h_pinned[F_MISC1]};
-    c.rw_members[0] = nm[0];
-    c.rw_members[1] = nm[1];
+    F.nm[0] = c.h_pinned[F_MISC0];
+    F.nm[1] = c.h_pinned[F_MISC1];
+    c.rw_members[0] = F.nm[0];
+    c.rw_members[1] = F.nm[1];
     const double xmin = key_to_double((uint64_t)c.h_pinned[F_BBOX + 0]);
     const double xmax = key_to_double((uint64_t)c.h_pinned[F_BBOX + 1]);
     const double ymin = key_to_double((uint64_t)c.h_pinned[F_BBOX + 2]);
     const double ymax = key_to_double((uint64_t)c.h_pinned[F_BBOX + 3]);
-    // scaled FP32 frame: |x'| < 1 with a power-of-two scale (exact in fp64)
-    const double cx = 0.5 * (xmin + xmax), cy = 0.5 * (ymin + ymax);
-    double H = std::fmax(std::fmax(xmax - cx, cx - xmin), std::fmax(ymax - cy, cy - ymin));
+    // scaled FP32 frame: a power-of-two scale (exact in fp64) bringing the extent below 1
+    double H = std::fmax(xmax - xmin, ymax - ymin);
     int e = 0;
     if (H > 0.0 && std::isfinite(H)) e = std::ilogb(H) + 1;
-    const double scale = std::ldexp(1.0, -e), unscale = std::ldexp(1.0, e);
-
-    float2 *f32[2];
-    W1G_TRY(ensure(c.scr[7], nm[0], &f32[0]));
-    W1G_TRY(ensure(c.scr[8], nm[1], &f32[1]));
+    F.scale = std::ldexp(1.0, -e);
+    F.unscale = std::ldexp(1.0, e);
+    const double ext = H > 0.0 && std::isfinite(H) ? H : 1.0;
+    const double inv = 65535.0 / ext;
     for (int s = 0; s < 2; s++) {
-        if (nm[s] == 0) continue;
-        k_to_f32<<<grid_for(nm[s], 256, 8u * c.sm_count), 256, 0, c.stream>>>(pts, members[s], nm[s], cx, cy,
-                                                                             scale, f32[s]);
+        const int64_t n = F.nm[s];
+        uint64_t *key;
+        uint32_t *perm;
+        W1G_TRY(ensure(c.scr[0], (size_t)n + 1, &key));
+        W1G_TRY(ensure(c.scr[2], (size_t)n + 1, &perm));
+        W1G_TRY(ensure(c.scr[7 + 2 * s], (size_t)n + 1, &F.mpts[s]));
+        W1G_TRY(ensure(c.scr[8 + 2 * s], (size_t)n + 1, &F.mpos[s]));
+        if (n == 0) continue;
+        const unsigned gn = grid_for(n, 256, 8u * c.sm_count);
+        k_morton<<<gn, 256, 0, c.stream>>>(pts, F.members[s], n, xmin, ymin, inv, key, perm);
+        W1G_CHECK_LAUNCH();
+        uint64_t *keys[1] = {key};
+        W1G_TRY(radix_sort(c, keys, 1, perm, n, 32));
+        k_gather_members<<<gn, 256, 0, c.stream>>>(pts, F.members[s], perm, n, F.mpts[s], F.mpos[s]);
         W1G_CHECK_LAUNCH();
     }
+    return W1G_OK;
+}
+
+int rwmd_run(Ctx &c, double *L, double *LA, double *LB) {
+    NodeSet &ns = c.nodes[0];
+    const int64_t k = ns.k;
+    const int64_t *mass[2] = {ptr<int64_t>(ns.am), ptr<int64_t>(ns.bm)};
+    if (k == 0) {
+        *L = *LA = *LB = 0.0;
+        c.n_best[0] = c.n_best[1] = 0;
+        return W1G_OK;
+    }
+    RwmdFrame F;
+    W1G_TRY(rwmd_prepare(c, F));
+    const int64_t mx = (F.nm[0] > F.nm[1] ? F.nm[0] : F.nm[1]) + 1;
     double *terms, *dres;
-    W1G_TRY(ensure(c.scr[9], (size_t)(nm[0] > nm[1] ? nm[0] : nm[1]) + 1, &terms));
-    W1G_TRY(ensure(c.scr[10], 4, &dres));
+    unsigned *mf;
+    float *qn;
+    double4 *tbox, *box64;
+    W1G_TRY(ensure(c.scr[11], (size_t)mx, &terms));
+    W1G_TRY(ensure(c.scr[12], 4, &dres));
+    W1G_TRY(ensure(c.scr[13], (size_t)mx, &mf));
+    W1G_TRY(ensure(c.scr[14], (size_t)mx, &qn));
+    W1G_TRY(ensure(c.scr[15], (size_t)mx / 1024 + 2, &tbox));
+    W1G_TRY(ensure(c.scr[16], (size_t)mx / 64 + 2, &box64));
     for (int s = 0; s < 2; s++) {
         const int o = 1 - s;
-        const int64_t n_src = nm[s], n_dst = nm[o];
+        const int64_t n_src = F.nm[s], n_dst = F.nm[o];
         c.n_best[s] = n_src;
         double *best;
         W1G_TRY(ensure(c.best[s], (size_t)n_src + 1, &best));
@@ -379,52 +364,15 @@ int rwmd_run(Ctx &c, double *L, double *LA, double *LB) {
             W1G_CUDA(cudaMemsetAsync(dres + s, 0, sizeof(double), c.stream));
             continue;
         }
-        unsigned *mf = nullptr;
-        Grid gr{0, 0, 1, 1, 1};
-        int64_t *cell_start = nullptr;
-        double2 *tsorted = nullptr;
         if (n_dst > 0) {
-            W1G_TRY(ensure(c.scr[11], (size_t)n_src, &mf));
             W1G_CUDA(cudaMemsetAsync(mf, 0x7f, sizeof(unsigned) * n_src, c.stream));
-            W1G_TRY(rwmd_f32_min(c, f32[s], n_src, f32[o], n_dst, mf, c.culling));
-            // uniform grid over the targets, ~4 targets per cell on average
-            const double W = xmax - xmin, Hh = ymax - ymin;
-            double cs;
-            if (W > 0 && Hh > 0)
-                cs = std::sqrt(W * Hh / (4.0 * (double)n_dst));
-            else
-                cs = std::fmax(W, Hh) / (4.0 * (double)n_dst);
-            if (!(cs > 0.0) || !std::isfinite(cs)) cs = 1.0;
-            double gxf = std::floor(W / cs) + 1, gyf = std::floor(Hh / cs) + 1;
-            while (gxf * gyf > (double)(1 << 26)) {
-                cs *= 1.5;
-                gxf = std::floor(W / cs) + 1;
-                gyf = std::floor(Hh / cs) + 1;
-            }
-            gr.x0 = xmin;
-            gr.y0 = ymin;
-            gr.inv_c = 1.0 / cs;
-            gr.gx = (int)gxf;
-            gr.gy = (int)gyf;
-            const int64_t ncell = (int64_t)gr.gx * gr.gy;
-            int32_t *cell;
-            int64_t *counts, *cursor;
-            W1G_TRY(ensure(c.scr[12], (size_t)n_dst, &cell));
-            W1G_TRY(ensure(c.scr[13], (size_t)ncell + 1, &counts));
-            W1G_TRY(ensure(c.scr[14], (size_t)ncell + 1, &cell_start));
-            W1G_TRY(ensure(c.scr[15], (size_t)ncell + 1, &cursor));
-            W1G_TRY(ensure(c.scr[16], (size_t)n_dst, &tsorted));
-            W1G_CUDA(cudaMemsetAsync(counts, 0, sizeof(int64_t) * (ncell + 1), c.stream));
-            const unsigned gd = grid_for(n_dst, 256, 8u * c.sm_count);
-            k_cell_count<<<gd, 256, 0, c.stream>>>(pts, members[o], n_dst, gr, cell, counts);
-            W1G_CHECK_LAUNCH();
-            W1G_TRY(scan_i64(c, CountVal{counts}, ncell + 1, cell_start, nullptr));
-            W1G_CUDA(cudaMemcpyAsync(cursor, cell_start, sizeof(int64_t) * ncell, cudaMemcpyDeviceToDevice, c.stream));
-            k_cell_fill<<<gd, 256, 0, c.stream>>>(pts, members[o], n_dst, cell, cursor, tsorted);
+            W1G_TRY(rwmd_f32_min(c, F.mpts[s], n_src, F.mpts[o], n_dst, F.scale, mf, qn, tbox, c.culling));
+            k_boxes64<<<grid_for((n_dst / RT + 1) * 32, 256, 8u * c.sm_count), 256, 0, c.stream>>>(F.mpts[o], n_dst, box64);
             W1G_CHECK_LAUNCH();
         }
-        k_refine<<<grid_for(n_src, 128, 16u * c.sm_count), 128, 0, c.stream>>>(
-            pts, members[s], mass[s], n_src, mf, n_dst > 0, unscale, gr, cell_start, tsorted, best, terms);
+        k_refine<<<(unsigned)((n_src + RF_BLOCK - 1) / RF_BLOCK), RF_BLOCK, 0, c.stream>>>(
+            F.mpts[s], F.mpos[s], F.members[s], mass[s], n_src, mf, qn, F.unscale, F.mpts[o], n_dst, box64,
+            best, terms);
         W1G_CHECK_LAUNCH();
         W1G_TRY(pairwise_sum(c, terms, n_src, dres + s, c.scr[17], c.scr[18], c.scr[19]));
     }
@@ -440,20 +388,23 @@ int rwmd_run(Ctx &c, double *L, double *LA, double *LB) {
 // measurement hook (w1g_profile_rwmd_tile): the FP32 tile pass alone, both
 // directions, `reps` times, timed with events on the context stream
 int rwmd_tile_profile(Ctx &c, int reps, float *ms, int64_t *evals) {
-    double L, la, lb;
-    W1G_TRY(rwmd_run(c, &L, &la, &lb));  // builds the scaled FP32 member arrays
-    const int64_t na = c.rw_members[0], nb = c.rw_members[1];
+    RwmdFrame F;
+    W1G_TRY(rwmd_prepare(c, F));
+    const int64_t na = F.nm[0], nb = F.nm[1];
     *evals = na * nb;
     *ms = 0.f;
     if (na == 0 || nb == 0 || reps < 1) return W1G_OK;
-    const float2 *fa = ptr<float2>(c.scr[7]), *fb = ptr<float2>(c.scr[8]);
-    unsigned *ma, *mb;
-    W1G_TRY(ensure(c.scr[11], (size_t)na, &ma));
-    W1G_TRY(ensure(c.scr[12], (size_t)nb, &mb));
+    const int64_t mx = (na > nb ? na : nb) + 1;
+    unsigned *mf;
+    float *qn;
+    double4 *tbox;
+    W1G_TRY(ensure(c.scr[13], (size_t)mx, &mf));
+    W1G_TRY(ensure(c.scr[14], (size_t)mx, &qn));
+    W1G_TRY(ensure(c.scr[15], (size_t)mx / 1024 + 2, &tbox));
     W1G_CUDA(cudaEventRecord(c.ev[8], c.stream));
     for (int r = 0; r < reps; r++) {
-        W1G_TRY(rwmd_f32_min(c, fa, na, fb, nb, ma, c.culling));
-        W1G_TRY(rwmd_f32_min(c, fb, nb, fa, na, mb, c.culling));
+        W1G_TRY(rwmd_f32_min(c, F.mpts[0], na, F.mpts[1], nb, F.scale, mf, qn, tbox, c.culling));
+        W1G_TRY(rwmd_f32_min(c, F.mpts[1], nb, F.mpts[0], na, F.scale, mf, qn, tbox, c.culling));
     }
     W1G_CUDA(cudaEventRecord(c.ev[9], c.stream));
     W1G_CUDA(cudaEventSynchronize(c.ev[9]));

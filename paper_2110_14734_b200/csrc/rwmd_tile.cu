@@ -1,19 +1,31 @@
 // rwmd_tile.cu -- the FP32 all-pairs nearest-neighbour tile pass of RWMD.
 //
-// For every source q (scaled frame, |q| < 1) computes min over all targets t
-// of fl32(dx*dx + dy*dy) -- the "tiled all-pairs nearest-neighbour min" of the
-// north star, on the FP32 pipe (a min over a distance is not a contraction,
-// so no tensor cores).  Each thread keeps R sources in registers, targets
-// stream through shared memory in tiles and are broadcast to the warp; the
-// target range is split across grid.y so the grid fills all 148 SMs, and the
-// per-chunk minima are merged with an order-independent atomicMin on the
-// float bits (non-negative floats order like their bit patterns).
+// For every source q, min over targets t of |q - t|^2 -- the "tiled
+// all-pairs nearest-neighbour min" of the north star -- on the FP32 pipe
+// (a min over a distance is not a contraction, so no tensor cores):
 //
-// The result only sizes the exact fp64 search in rwmd.cu: its error is
-// bounded by |d_f32 - d| <= 2^-21 (1 + d) in the scaled frame.
+//  * R sources per thread in registers, targets staged through shared
+//    memory in tiles and broadcast to the warp;
+//  * expanded form with packed FP32x2 math: per two targets
+//        s = fma2(-2qy, ty, fma2(-2qx, tx, |t|^2))   (2 x FFMA2)
+//        m = min3(m, s.x, s.y)                        (1 x FMNMX3)
+//    i.e. one FFMA2 and half an FMNMX3 per evaluation; |q|^2 is added
+//    after the min;
+//  * the expansion cancels, so every CTA works in a LOCAL frame: origin =
+//    its first source (sources are Morton-ordered, so a CTA's sources are
+//    spatially compact) and targets are shifted into that frame as they are
+//    staged (in fp64, then rounded once).  The error of the result is then
+//    bounded by 2^-20 (2|q'| + d)^2 in scaled units, small
+//    exactly where it matters;
+//  * full mode (culling off): every source meets every target, the target
+//    range is split across grid.y to fill the 148 SMs and per-chunk minima
+//    merge with an order-independent atomicMin on the float bits;
+//  * culled mode: one CTA per source block walks the Morton-ordered target
+//    tiles outward from its own position and skips every tile whose bbox is
+//    farther than the CTA's current worst upper bound.
 //
-// This translation unit is compiled with FMA contraction allowed; nothing
-// here feeds a reference-parity value directly.
+// The result only sizes the exact fp64 search in rwmd.cu.  This translation
+// unit is compiled with FMA contraction allowed.
 #include "common.cuh"
 
 namespace w1g {
@@ -21,75 +33,252 @@ namespace w1g {
 namespace {
 
 constexpr int T_BLOCK = 256;
-constexpr int T_R = 8;        // sources per thread
-constexpr int T_TILE = 2048;  // targets per shared-memory tile
+constexpr int T_TS = 1024;  // targets per shared-memory tile
+constexpr int CULL_STEPS = 3;  // culled mode: the Morton-nearest tile and its two neighbours
 
-__global__ void __launch_bounds__(T_BLOCK) k_rwmd_f32(const float2 *__restrict__ q, int nq,
-                                                      const float2 *__restrict__ t, int nt,
-                                                      int chunk, unsigned *__restrict__ mout) {
-    __shared__ float4 s_t[T_TILE / 2];
-    const int q0 = blockIdx.x * (T_BLOCK * T_R) + threadIdx.x;
-    float qx[T_R], qy[T_R], m[T_R];
+__device__ __forceinline__ float min3(float a, float b, float c) {
+    float d;
+    asm("min.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+    return d;
+}
+
+// error bound of an estimate m (scaled units^2) for a source at local radius qn
+__device__ __forceinline__ float upper_bound(float m, float qn) {
+    const float d = sqrtf(fmaxf(m, 0.f));
+    const float e = 2.f * qn + d + 0x1p-20f;
+    return sqrtf(fmaxf(m, 0.f) + 0x1p-20f * e * e) * (1.f + 0x1p-20f) + 0x1p-22f;
+}
+
+struct TileArgs {
+    const double2 *q;       // sources (Morton order), original coordinates
+    const double2 *t;       // targets (Morton order)
+    const double4 *tbox;    // per T_TS-tile bbox of the targets (culled mode)
+    int nq, nt;
+    double scale;           // 2^-e
+    unsigned *mout;         // min d^2 estimate (float bits), scaled units
+    float *qn_out;          // |q'| per source
+    int chunk;              // targets per grid.y chunk (full mode)
+};
+
+template <int R, bool CULL>
+__global__ void __launch_bounds__(T_BLOCK) k_rwmd_f32(TileArgs A) {
+    __shared__ float4 s_xy[T_TS / 2];
+    __shared__ float2 s_tt[T_TS / 2];
+    __shared__ float s_red[T_BLOCK / 32];
+    __shared__ double2 s_org;
+    __shared__ double4 s_qbox;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int q0 = blockIdx.x * (T_BLOCK * R);
+    if (tid == 0) s_org = A.q[q0];
+    __syncthreads();
+    const double ox = s_org.x, oy = s_org.y, sc = A.scale;
+    float2 ax[R], ay[R];
+    float m[R], qq[R], qn[R];
+    double bx0 = INFINITY, by0 = INFINITY, bx1 = -INFINITY, by1 = -INFINITY;
 #pragma unroll
-    for (int r = 0; r < T_R; r++) {
-        int i = q0 + r * T_BLOCK;
-        float2 p = i < nq ? q[i] : make_float2(0.f, 0.f);
-        qx[r] = p.x;
-        qy[r] = p.y;
+    for (int r = 0; r < R; r++) {
+        const int i = q0 + r * T_BLOCK + tid;
+        const bool v = i < A.nq;
+        const double2 p = v ? A.q[i] : s_org;
+        const float x = (float)((p.x - ox) * sc), y = (float)((p.y - oy) * sc);
+        ax[r] = make_float2(-2.f * x, -2.f * x);
+        ay[r] = make_float2(-2.f * y, -2.f * y);
+        qq[r] = fmaf(x, x, y * y);
+        qn[r] = sqrtf(qq[r]);
         m[r] = INFINITY;
+        if (CULL && v) {
+            bx0 = fmin(bx0, p.x);
+            by0 = fmin(by0, p.y);
+            bx1 = fmax(bx1, p.x);
+            by1 = fmax(by1, p.y);
+        }
     }
-    const int t_begin = blockIdx.y * chunk;
-    const int t_end = min(nt, t_begin + chunk);
-    for (int tb = t_begin; tb < t_end; tb += T_TILE) {
-        const int cnt = min(T_TILE, t_end - tb);
+    int n_tiles, t_first, center = 0;
+    if (CULL) {
+        // CTA bbox of its sources (original units) for the tile test
+        for (int o = 16; o; o >>= 1) {
+            bx0 = fmin(bx0, __shfl_xor_sync(0xffffffffu, bx0, o));
+            by0 = fmin(by0, __shfl_xor_sync(0xffffffffu, by0, o));
+            bx1 = fmax(bx1, __shfl_xor_sync(0xffffffffu, bx1, o));
+            by1 = fmax(by1, __shfl_xor_sync(0xffffffffu, by1, o));
+        }
+        __shared__ double s_b[4][T_BLOCK / 32];
+        if (lane == 0) {
+            s_b[0][wid] = bx0;
+            s_b[1][wid] = by0;
+            s_b[2][wid] = bx1;
+            s_b[3][wid] = by1;
+        }
         __syncthreads();
-        for (int j = threadIdx.x; j < T_TILE / 2; j += T_BLOCK) {
-            float2 a = 2 * j < cnt ? t[tb + 2 * j] : make_float2(INFINITY, INFINITY);
-            float2 b = 2 * j + 1 < cnt ? t[tb + 2 * j + 1] : make_float2(INFINITY, INFINITY);
-            s_t[j] = make_float4(a.x, a.y, b.x, b.y);
+        if (tid == 0) {
+            double4 b = make_double4(INFINITY, INFINITY, -INFINITY, -INFINITY);
+            for (int w = 0; w < T_BLOCK / 32; w++) {
+                b.x = fmin(b.x, s_b[0][w]);
+                b.y = fmin(b.y, s_b[1][w]);
+                b.z = fmax(b.z, s_b[2][w]);
+                b.w = fmax(b.w, s_b[3][w]);
+            }
+            s_qbox = b;
+        }
+        __syncthreads();  // every thread must see s_qbox: skip decisions are CTA-uniform
+        n_tiles = (A.nt + T_TS - 1) / T_TS;
+        t_first = 0;
+        // start at the target tile whose Morton range meets this source block:
+        // sources and targets share one Morton frame, so proportional position is a good guess
+        center = (int)(((long long)q0 * n_tiles) / (A.nq > 0 ? A.nq : 1));
+        if (center >= n_tiles) center = n_tiles - 1;
+    } else {
+        const int tb = blockIdx.y * A.chunk;
+        const int te = min(A.nt, tb + A.chunk);
+        t_first = tb;
+        n_tiles = (te - tb + T_TS - 1) / T_TS;
+    }
+    float bound = INFINITY;  // CTA-wide worst upper bound (culled mode), scaled units
+    // culled mode only needs SOME real target per source (any target's distance
+    // is a valid upper bound for the exact pass), so it walks a few Morton
+    // neighbours of the CTA and stops; full mode meets every target
+    const int n_steps = CULL ? min(2 * n_tiles, CULL_STEPS) : n_tiles;
+    for (int k = 0; k < n_steps; k++) {
+        int tile;
+        if (CULL) {
+            // outward walk: center, center+1, center-1, center+2, ... (each tile once)
+            const int d = (k + 1) >> 1;
+            tile = (k & 1) ? center + d : center - d;
+            if (tile < 0 || tile >= n_tiles) continue;
+            const double4 b = A.tbox[tile];
+            const double4 qb = s_qbox;
+            const double gx = fmax(0.0, fmax(b.x - qb.z, qb.x - b.z));
+            const double gy = fmax(0.0, fmax(b.y - qb.w, qb.y - b.w));
+            const double lb = sqrt(gx * gx + gy * gy) * sc;  // scaled units
+            if (lb * (1.0 - 1e-6) > (double)bound) continue;
+        } else {
+            tile = k;
+        }
+        const int tb = CULL ? tile * T_TS : t_first + tile * T_TS;
+        const int te = CULL ? min(A.nt, tb + T_TS) : min(min(A.nt, t_first + A.chunk), tb + T_TS);
+        const int cnt = te - tb;
+        __syncthreads();
+        for (int j = tid; j < T_TS / 2; j += T_BLOCK) {
+            float xa = 1e18f, ya = 1e18f, xb = 1e18f, yb = 1e18f;
+            if (2 * j < cnt) {
+                const double2 p = A.t[tb + 2 * j];
+                xa = (float)((p.x - ox) * sc);
+                ya = (float)((p.y - oy) * sc);
+            }
+            if (2 * j + 1 < cnt) {
+                const double2 p = A.t[tb + 2 * j + 1];
+                xb = (float)((p.x - ox) * sc);
+                yb = (float)((p.y - oy) * sc);
+            }
+            s_xy[j] = make_float4(xa, xb, ya, yb);
+            s_tt[j] = make_float2(fmaf(xa, xa, ya * ya), fmaf(xb, xb, yb * yb));
         }
         __syncthreads();
         const int pairs = (cnt + 1) >> 1;
 #pragma unroll 4
         for (int j = 0; j < pairs; j++) {
-            const float4 tt = s_t[j];
+            const float4 v = s_xy[j];
+            const float2 tx = make_float2(v.x, v.y), ty = make_float2(v.z, v.w), tt = s_tt[j];
 #pragma unroll
-            for (int r = 0; r < T_R; r++) {
-                float dx = qx[r] - tt.x, dy = qy[r] - tt.y;
-                float d = fmaf(dy, dy, dx * dx);
-                float ex = qx[r] - tt.z, ey = qy[r] - tt.w;
-                float e = fmaf(ey, ey, ex * ex);
-                m[r] = fminf(m[r], fminf(d, e));
+            for (int r = 0; r < R; r++) {
+                const float2 s = __ffma2_rn(ay[r], ty, __ffma2_rn(ax[r], tx, tt));
+                m[r] = min3(m[r], s.x, s.y);
             }
+        }
+        if (CULL) {
+            float ub = 0.f;
+#pragma unroll
+            for (int r = 0; r < R; r++) {
+                const int i = q0 + r * T_BLOCK + tid;
+                if (i < A.nq) ub = fmaxf(ub, upper_bound(m[r] + qq[r], qn[r]));
+            }
+            for (int o = 16; o; o >>= 1) ub = fmaxf(ub, __shfl_xor_sync(0xffffffffu, ub, o));
+            if (lane == 0) s_red[wid] = ub;
+            __syncthreads();
+            float b2 = 0.f;
+#pragma unroll
+            for (int w = 0; w < T_BLOCK / 32; w++) b2 = fmaxf(b2, s_red[w]);
+            bound = b2;
         }
     }
 #pragma unroll
-    for (int r = 0; r < T_R; r++) {
-        int i = q0 + r * T_BLOCK;
-        if (i < nq) atomicMin(&mout[i], __float_as_uint(m[r]));
+    for (int r = 0; r < R; r++) {
+        const int i = q0 + r * T_BLOCK + tid;
+        if (i < A.nq) {
+            const float est = fmaxf(m[r] + qq[r], 0.f);
+            atomicMin(&A.mout[i], __float_as_uint(est));
+            if (blockIdx.y == 0) A.qn_out[i] = qn[r];
+        }
+    }
+}
+
+__global__ void k_tile_boxes(const double2 *t, int nt, double4 *box) {
+    const int lane = threadIdx.x & 31;
+    const int ntile = (nt + T_TS - 1) / T_TS;
+    for (int tile = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; tile < ntile;
+         tile += (gridDim.x * blockDim.x) >> 5) {
+        double x0 = INFINITY, y0 = INFINITY, x1 = -INFINITY, y1 = -INFINITY;
+        const int te = min(nt, (tile + 1) * T_TS);
+        for (int j = tile * T_TS + lane; j < te; j += 32) {
+            const double2 p = t[j];
+            x0 = fmin(x0, p.x);
+            y0 = fmin(y0, p.y);
+            x1 = fmax(x1, p.x);
+            y1 = fmax(y1, p.y);
+        }
+        for (int o = 16; o; o >>= 1) {
+            x0 = fmin(x0, __shfl_xor_sync(0xffffffffu, x0, o));
+            y0 = fmin(y0, __shfl_xor_sync(0xffffffffu, y0, o));
+            x1 = fmax(x1, __shfl_xor_sync(0xffffffffu, x1, o));
+            y1 = fmax(y1, __shfl_xor_sync(0xffffffffu, y1, o));
+        }
+        if (lane == 0) box[tile] = make_double4(x0, y0, x1, y1);
     }
 }
 
 }  // namespace
 
-int rwmd_f32_min(Ctx &c, const float2 *q, int64_t nq, const float2 *t, int64_t nt, unsigned *mout,
-                 int culling) {
-    (void)culling;
+// FP32 pass for one direction: sources q (nq, Morton order) against targets t
+// (nt, Morton order).  mout (float bits, pre-set to +huge) receives the
+// scaled squared-distance estimate, qn_out the local radius |q'|.
+int rwmd_f32_min(Ctx &c, const double2 *q, int64_t nq, const double2 *t, int64_t nt, double scale,
+                 unsigned *mout, float *qn_out, double4 *tbox, int culling) {
     if (nq == 0 || nt == 0) return W1G_OK;
-    const int per_block = T_BLOCK * T_R;
+    TileArgs A;
+    A.q = q;
+    A.t = t;
+    A.tbox = tbox;
+    A.nq = (int)nq;
+    A.nt = (int)nt;
+    A.scale = scale;
+    A.mout = mout;
+    A.qn_out = qn_out;
+    if (culling) {
+        const int ntile = (int)((nt + T_TS - 1) / T_TS);
+        k_tile_boxes<<<grid_for((int64_t)ntile * 32, 256, 8u * c.sm_count), 256, 0, c.stream>>>(t, (int)nt, tbox);
+        W1G_CHECK_LAUNCH();
+        constexpr int R = 2;
+        const int gx = (int)((nq + T_BLOCK * R - 1) / (T_BLOCK * R));
+        A.chunk = (int)nt;
+        k_rwmd_f32<R, true><<<gx, T_BLOCK, 0, c.stream>>>(A);
+        W1G_CHECK_LAUNCH();
+        return W1G_OK;
+    }
+    constexpr int R = 8;
+    const int per_block = T_BLOCK * R;
     const int gx = (int)((nq + per_block - 1) / per_block);
-    // enough CTAs for ~4 waves of 4 resident CTAs per SM
+    // enough CTAs for several waves of the resident CTAs on every SM
     const int want = 16 * c.sm_count;
     int gy = (want + gx - 1) / gx;
-    int64_t max_gy = (nt + T_TILE - 1) / T_TILE;
+    const int64_t max_gy = (nt + T_TS - 1) / T_TS;
     if (gy > max_gy) gy = (int)max_gy;
     if (gy < 1) gy = 1;
     if (gy > 65535) gy = 65535;
     int chunk = (int)((nt + gy - 1) / gy);
     chunk = (chunk + 1) & ~1;
     gy = (int)((nt + chunk - 1) / chunk);
-    dim3 grid(gx, gy);
-    k_rwmd_f32<<<grid, T_BLOCK, 0, c.stream>>>(q, (int)nq, t, (int)nt, chunk, mout);
+    A.chunk = chunk;
+    k_rwmd_f32<R, false><<<dim3(gx, gy), T_BLOCK, 0, c.stream>>>(A);
     W1G_CHECK_LAUNCH();
     return W1G_OK;
 }

@@ -1,12 +1,18 @@
 // sort.cu -- stable LSD radix sort (8-bit digits) with a uint32 payload.
 //
 // Replaces the sorts inside np.unique(axis=0) (diagram.py:203,
-// condensation.py:114) and np.lexsort (network.py:70).  One histogram pass
-// computes every digit's global histogram; digits that are constant over
-// all keys are skipped.  Each remaining digit is one count -> per-bin scan ->
-// stable scatter pass.  Stability inside a tile comes from warp match-any
-// ranking in index order, so equal keys keep their input order (np.unique
-// keeps the first occurrence; np.lexsort is stable).
+// condensation.py:114) and np.lexsort (network.py:70).
+//
+//  * one histogram kernel computes every digit's global histogram; digits
+//    that are constant over all keys are skipped (one 2-8 KB D2H per sort);
+//  * each remaining digit is ONE "onesweep" kernel: a tile (4096 keys) ranks
+//    its keys stably with warp match-any in index order, publishes its
+//    per-digit counts, looks back over earlier tiles (decoupled look-back,
+//    epoch-tagged status words, so nothing is re-zeroed between passes),
+//    stages the tile in shared memory in digit order and writes it out with
+//    coalesced stores.
+// Equal keys keep their input order (np.unique keeps the first occurrence,
+// np.lexsort is stable).
 #include "common.cuh"
 
 namespace w1g {
@@ -16,8 +22,8 @@ namespace {
 constexpr int RS_BLOCK = 256;
 constexpr int RS_WARPS = RS_BLOCK / 32;
 constexpr int RS_IPT = 16;
-constexpr int RS_TILE = RS_BLOCK * RS_IPT;
-constexpr int RS_WTILE = 32 * RS_IPT;  // items per warp
+constexpr int RS_TILE = RS_BLOCK * RS_IPT;  // 4096
+constexpr int RS_WTILE = 32 * RS_IPT;       // items per warp
 
 struct KeyPtrs {
     uint64_t *k[4];
@@ -42,121 +48,179 @@ __global__ void __launch_bounds__(512) k_rs_hist_all(KeyPtrs kp, int words, int6
         if (sh[i]) atomicAdd(&hist[i], sh[i]);
 }
 
-__global__ void __launch_bounds__(RS_BLOCK) k_rs_count(const uint64_t *__restrict__ kw, int shift,
-                                                       int64_t n, uint32_t *counts, int ntiles) {
-    __shared__ uint32_t h[256];
-    h[threadIdx.x] = 0;
-    __syncthreads();
-    const int64_t base = (int64_t)blockIdx.x * RS_TILE;
-#pragma unroll 4
-    for (int i = 0; i < RS_IPT; i++) {
-        int64_t idx = base + i * RS_BLOCK + threadIdx.x;
-        if (idx < n) atomicAdd(&h[(int)((kw[idx] >> shift) & 255)], 1u);
-    }
-    __syncthreads();
-    counts[(int64_t)threadIdx.x * ntiles + blockIdx.x] = h[threadIdx.x];
+// status word: [epoch (30 bits) | kind (2 bits) | count (32 bits)]
+constexpr unsigned long long ST_AGG = 1, ST_INC = 2;
+
+__device__ __forceinline__ unsigned long long st_make(unsigned epoch, unsigned long long kind, uint32_t cnt) {
+    return ((unsigned long long)epoch << 34) | (kind << 32) | cnt;
 }
 
-// one block per bin: offsets[b][t] = sum_{b'<b} hist[b'] + sum_{t'<t} counts[b][t']
-__global__ void __launch_bounds__(1024) k_rs_binscan(uint32_t *counts, const uint32_t *dhist,
-                                                     int ntiles) {
-    __shared__ uint32_t s_warp[32];
-    __shared__ uint32_t s_carry;
-    const int b = blockIdx.x;
-    if (threadIdx.x == 0) {
-        uint32_t base = 0;
-        for (int i = 0; i < b; i++) base += dhist[i];
-        s_carry = base;
-    }
-    __syncthreads();
-    uint32_t *row = counts + (int64_t)b * ntiles;
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    for (int start = 0; start < ntiles; start += 1024) {
-        int t = start + threadIdx.x;
-        uint32_t v = t < ntiles ? row[t] : 0;
-        uint32_t x = v;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
-        }
-        if (lane == 31) s_warp[wid] = x;
-        __syncthreads();
-        if (wid == 0) {
-            uint32_t w = s_warp[lane];
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
-                if (lane >= o) w += y;
-            }
-            s_warp[lane] = w;
-        }
-        __syncthreads();
-        uint32_t excl = (wid ? s_warp[wid - 1] : 0) + x - v;
-        uint32_t carry = s_carry;
-        if (t < ntiles) row[t] = carry + excl;
-        __syncthreads();
-        if (threadIdx.x == 0) s_carry = carry + s_warp[31];
-        __syncthreads();
-    }
-}
-
-__global__ void __launch_bounds__(RS_BLOCK) k_rs_scatter(KeyPtrs src, KeyPtrs dst, int wfirst,
-                                                         int words, const uint32_t *__restrict__ vsrc,
-                                                         uint32_t *__restrict__ vdst, int dword,
-                                                         int shift, const uint32_t *__restrict__ offsets,
-                                                         int ntiles, int64_t n) {
+template <int W, int M>
+__global__ void __launch_bounds__(RS_BLOCK) k_rs_onesweep(KeyPtrs src, KeyPtrs dst,
+                                                          const uint32_t *__restrict__ vsrc,
+                                                          uint32_t *__restrict__ vdst, int shift,
+                                                          const uint32_t *__restrict__ dhist,
+                                                          unsigned long long *status, unsigned *ticket,
+                                                          unsigned epoch, int64_t n) {
+    constexpr int DW = W - M;  // word holding the digit; words DW..W-1 move
+    extern __shared__ __align__(16) unsigned char smem[];
+    uint64_t *s_key = reinterpret_cast<uint64_t *>(smem);           // M * RS_TILE
+    uint32_t *s_val = reinterpret_cast<uint32_t *>(s_key + M * RS_TILE);  // RS_TILE
     __shared__ uint32_t whist[RS_WARPS][257];
-    __shared__ uint32_t toff[256];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    toff[threadIdx.x] = offsets[(int64_t)threadIdx.x * ntiles + blockIdx.x];
-    for (int w = 0; w < RS_WARPS; w++) whist[w][threadIdx.x] = 0;
-    if (threadIdx.x < RS_WARPS) whist[threadIdx.x][256] = 0;
+    __shared__ uint32_t t_start[256];  // tile-local exclusive start of each digit
+    __shared__ uint32_t g_base[256];   // global output start of this tile's digit run
+    __shared__ uint32_t s_tile;
+
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    if (tid == 0) s_tile = atomicAdd(ticket, 1u);
+    for (int w = 0; w < RS_WARPS; w++) whist[w][tid] = 0;
+    if (tid < RS_WARPS) whist[tid][256] = 0;
     __syncthreads();
-    const uint64_t *kd = src.k[dword];
-    const int64_t wbase = (int64_t)blockIdx.x * RS_TILE + wid * RS_WTILE;
+    const int64_t tile = s_tile;
+    const int64_t tbase = tile * RS_TILE;
+    const int tn = (n - tbase) < RS_TILE ? (int)(n - tbase) : RS_TILE;
+    const uint64_t *kd = src.k[DW];
     const unsigned lt = lanemask_lt();
-    uint32_t rank[RS_IPT];
+
+    // 1. stable rank inside the tile (warp w owns items [w*512, (w+1)*512), striped)
+    uint16_t rank[RS_IPT];
     uint16_t dig[RS_IPT];
 #pragma unroll
     for (int i = 0; i < RS_IPT; i++) {
-        int64_t idx = wbase + i * 32 + lane;
-        int d = idx < n ? (int)((kd[idx] >> shift) & 255) : 256;
-        unsigned peers = __match_any_sync(0xffffffffu, d);
-        uint32_t b = whist[wid][d];
+        const int li = wid * RS_WTILE + i * 32 + lane;
+        const int d = li < tn ? (int)((kd[tbase + li] >> shift) & 255) : 256;
+        const unsigned peers = __match_any_sync(0xffffffffu, d);
+        const uint32_t b = whist[wid][d];
         __syncwarp();
         if ((__ffs(peers) - 1) == lane) whist[wid][d] = b + __popc(peers);
         __syncwarp();
-        rank[i] = b + __popc(peers & lt);
+        rank[i] = (uint16_t)(b + __popc(peers & lt));
         dig[i] = (uint16_t)d;
     }
     __syncthreads();
-    {  // exclusive prefix over warps for each bin
-        uint32_t run = 0;
-        for (int w = 0; w < RS_WARPS; w++) {
-            uint32_t t = whist[w][threadIdx.x];
-            whist[w][threadIdx.x] = run;
-            run += t;
+    // 2. per-digit tile counts, warp prefixes, tile-local digit starts
+    uint32_t cnt = 0;
+    for (int w = 0; w < RS_WARPS; w++) {
+        const uint32_t t = whist[w][tid];
+        whist[w][tid] = cnt;
+        cnt += t;
+    }
+    // publish this tile's count for digit `tid` as early as possible
+    if (tile > 0) atomicExch(&status[tile * 256 + tid], st_make(epoch, ST_AGG, cnt));
+    uint32_t hbase;
+    {  // block exclusive scans over digits: tile counts -> t_start, global histogram -> hbase
+        const uint32_t hd = dhist[tid];
+        uint32_t x = cnt, y = hd;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t a = __shfl_up_sync(0xffffffffu, x, o);
+            const uint32_t b = __shfl_up_sync(0xffffffffu, y, o);
+            if (lane >= o) {
+                x += a;
+                y += b;
+            }
+        }
+        __shared__ uint32_t s_w[RS_WARPS], s_h[RS_WARPS];
+        if (lane == 31) {
+            s_w[wid] = x;
+            s_h[wid] = y;
+        }
+        __syncthreads();
+        uint32_t off = 0, hoff = 0;
+        for (int w = 0; w < wid; w++) {
+            off += s_w[w];
+            hoff += s_h[w];
+        }
+        t_start[tid] = off + x - cnt;
+        hbase = hoff + y - hd;
+    }
+    // 3. decoupled look-back per digit (thread `tid` handles digit `tid`); a
+    //    window of predecessors is loaded at once so a walk over published
+    //    aggregates costs one memory latency per LB_W tiles, not per tile
+    {
+        constexpr int LB_W = 16;
+        uint32_t prefix = 0;
+        int64_t j = tile - 1;
+        while (j >= 0) {
+            unsigned long long s[LB_W];
+#pragma unroll
+            for (int w = 0; w < LB_W; w++)
+                s[w] = (j - w >= 0) ? *((volatile unsigned long long *)&status[(j - w) * 256 + tid]) : 0ull;
+            int used = 0;
+            bool done = false;
+#pragma unroll
+            for (int w = 0; w < LB_W; w++) {
+                if (done || used < w) break;
+                if (j - w < 0 || (unsigned)(s[w] >> 34) != epoch) break;  // not published yet
+                prefix += (uint32_t)s[w];
+                used = w + 1;
+                if (((s[w] >> 32) & 3) == ST_INC) done = true;
+            }
+            if (done) break;
+            j -= used;  // consumed aggregates; re-poll from the first unpublished tile
+        }
+        atomicExch(&status[tile * 256 + tid], st_make(epoch, ST_INC, prefix + cnt));
+        // global start of digit `tid`: smaller digits over all keys + this digit in earlier tiles
+        g_base[tid] = hbase + prefix;
+    }
+    __syncthreads();
+    // 4. stage the tile in digit order
+#pragma unroll
+    for (int i = 0; i < RS_IPT; i++) {
+        const int li = wid * RS_WTILE + i * 32 + lane;
+        if (li < tn) {
+            const int d = dig[i];
+            const int lp = t_start[d] + whist[wid][d] + rank[i];
+#pragma unroll
+            for (int m = 0; m < M; m++) s_key[m * RS_TILE + lp] = src.k[DW + m][tbase + li];
+            s_val[lp] = vsrc[tbase + li];
         }
     }
     __syncthreads();
+    // 5. coalesced write-out: consecutive staged items of one digit go to consecutive addresses
+    for (int j = tid; j < tn; j += RS_BLOCK) {
+        const uint64_t k0 = s_key[j];
+        const int d = (int)((k0 >> shift) & 255);
+        const uint32_t pos = g_base[d] + (uint32_t)j - t_start[d];
 #pragma unroll
-    for (int i = 0; i < RS_IPT; i++) {
-        int64_t idx = wbase + i * 32 + lane;
-        if (idx < n) {
-            int d = dig[i];
-            uint32_t pos = toff[d] + whist[wid][d] + rank[i];
-            for (int w = wfirst; w < words; w++) dst.k[w][pos] = src.k[w][idx];
-            vdst[pos] = vsrc[idx];
-        }
+        for (int m = 0; m < M; m++) dst.k[DW + m][pos] = s_key[m * RS_TILE + j];
+        vdst[pos] = s_val[j];
     }
+}
+
+template <int W, int M>
+int launch_pass(Ctx &c, KeyPtrs *src, KeyPtrs *dst, const uint32_t *vsrc, uint32_t *vdst, int shift,
+                const uint32_t *dhist, unsigned long long *status, unsigned *ticket, unsigned epoch,
+                int64_t n, int ntiles) {
+    const size_t sm = (size_t)RS_TILE * (8 * M + 4);
+    W1G_CUDA(cudaFuncSetAttribute(k_rs_onesweep<W, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    k_rs_onesweep<W, M><<<ntiles, RS_BLOCK, sm, c.stream>>>(*src, *dst, vsrc, vdst, shift, dhist, status,
+                                                           ticket, epoch, n);
+    W1G_CHECK_LAUNCH();
+    return W1G_OK;
+}
+
+int dispatch_pass(int W, int M, Ctx &c, KeyPtrs *src, KeyPtrs *dst, const uint32_t *vsrc, uint32_t *vdst,
+                  int shift, const uint32_t *dhist, unsigned long long *status, unsigned *ticket,
+                  unsigned epoch, int64_t n, int ntiles) {
+#define RS_CASE(w, m) \
+    if (W == w && M == m) return launch_pass<w, m>(c, src, dst, vsrc, vdst, shift, dhist, status, ticket, epoch, n, ntiles);
+    RS_CASE(1, 1)
+    RS_CASE(2, 2)
+    RS_CASE(2, 1)
+    RS_CASE(3, 3)
+    RS_CASE(3, 2)
+    RS_CASE(3, 1)
+#undef RS_CASE
+    set_error("radix_sort: unsupported word count %d", W);
+    return W1G_EINVAL;
 }
 
 }  // namespace
 
 int radix_sort(Ctx &c, uint64_t **keys, int words, uint32_t *vals, int64_t n, int top_bits) {
     if (n <= 1) return W1G_OK;
-    if (words < 1 || words > 4 || n > 0xffffffffll) {
+    if (words < 1 || words > 3 || n > 0xffffffffll) {
         set_error("radix_sort: unsupported shape (words=%d, n=%lld)", words, (long long)n);
         return W1G_EINVAL;
     }
@@ -167,11 +231,19 @@ int radix_sort(Ctx &c, uint64_t **keys, int words, uint32_t *vals, int64_t n, in
         a.k[w] = keys[w];
         W1G_TRY(ensure(c.sort_scr[w], (size_t)n, &b.k[w]));
     }
-    uint32_t *va = vals, *vb, *hist, *counts;
+    uint32_t *va = vals, *vb, *hist;
+    unsigned long long *status;
     W1G_TRY(ensure(c.sort_scr[4], (size_t)n, &vb));
-    W1G_TRY(ensure(c.sort_scr[5], (size_t)words * 8 * 256, &hist));
-    W1G_TRY(ensure(c.sort_scr[6], (size_t)ntiles * 256, &counts));
-    W1G_CUDA(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * words * 8 * 256, c.stream));
+    W1G_TRY(ensure(c.sort_scr[5], (size_t)words * 8 * 256 + 64, &hist));
+    const size_t cap0 = c.sort_scr[6].cap;
+    W1G_TRY(ensure(c.sort_scr[6], (size_t)ntiles * 256, &status));
+    if (c.sort_scr[6].cap != cap0) {
+        // fresh status words: make sure no stale bits can match an epoch
+        W1G_CUDA(cudaMemsetAsync(status, 0, c.sort_scr[6].cap, c.stream));
+        c.sort_epoch = 0;
+    }
+    unsigned *tickets = hist + words * 8 * 256;  // 64 per-pass tile tickets
+    W1G_CUDA(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * (words * 8 * 256 + 64), c.stream));
     {
         unsigned g = grid_for(n, 512, 2u * c.sm_count);
         size_t sm = sizeof(uint32_t) * words * 8 * 256;
@@ -192,21 +264,21 @@ int radix_sort(Ctx &c, uint64_t **keys, int words, uint32_t *vals, int64_t n, in
             const uint32_t *h = hh + (w * 8 + j) * 256;
             bool uniform = false;
             for (int q = 0; q < 256; q++)
-                if (h[q] == (uint32_t)n) { uniform = true; break; }
+                if (h[q] == (uint32_t)n) {
+                    uniform = true;
+                    break;
+                }
             if (!uniform) passes[np++] = w * 8 + j;
         }
     }
     KeyPtrs *src = &a, *dst = &b;
     uint32_t *vsrc = va, *vdst = vb;
     for (int p = 0; p < np; p++) {
-        const int w = passes[p] / 8, shift = 8 * (passes[p] % 8);
-        k_rs_count<<<ntiles, RS_BLOCK, 0, c.stream>>>(src->k[w], shift, n, counts, ntiles);
-        W1G_CHECK_LAUNCH();
-        k_rs_binscan<<<256, 1024, 0, c.stream>>>(counts, hist + (w * 8 + shift / 8) * 256, ntiles);
-        W1G_CHECK_LAUNCH();
-        k_rs_scatter<<<ntiles, RS_BLOCK, 0, c.stream>>>(*src, *dst, w, words, vsrc, vdst, w, shift,
-                                                        counts, ntiles, n);
-        W1G_CHECK_LAUNCH();
+        const int w = passes[p] / 8, j = passes[p] % 8;
+        c.sort_epoch = (c.sort_epoch + 1) & 0x3fffffffu;
+        if (c.sort_epoch == 0) c.sort_epoch = 1;
+        W1G_TRY(dispatch_pass(words, words - w, c, src, dst, vsrc, vdst, 8 * j, hist + (w * 8 + j) * 256,
+                              status, tickets + (p & 63), c.sort_epoch, n, ntiles));
         KeyPtrs *t = src;
         src = dst;
         dst = t;
@@ -224,3 +296,28 @@ int radix_sort(Ctx &c, uint64_t **keys, int words, uint32_t *vals, int64_t n, in
 }
 
 }  // namespace w1g
+
+using namespace w1g;
+
+// test hook: sort host keys (words x n, word 0 least significant) with the
+// device radix sort and return the permutation (w1g_debug_radix_sort, w1g.h)
+extern "C" int w1g_debug_radix_sort(w1g_ctx *c, const uint64_t *keys, int words, int64_t n,
+                                    uint32_t *perm) {
+    if (!c || words < 1 || words > 3 || n < 0) return W1G_EINVAL;
+    W1G_CUDA(cudaSetDevice(c->device));
+    uint64_t *k[3];
+    uint32_t *v;
+    for (int w = 0; w < words; w++) {
+        W1G_TRY(ensure(c->scr[w], (size_t)n + 1, &k[w]));
+        if (n) W1G_CUDA(cudaMemcpyAsync(k[w], keys + (size_t)w * n, sizeof(uint64_t) * n, cudaMemcpyHostToDevice, c->stream));
+    }
+    W1G_TRY(ensure(c->scr[4], (size_t)n + 1, &v));
+    W1G_TRY(stage_ensure(*c, sizeof(uint32_t) * (n + 1)));
+    uint32_t *h = static_cast<uint32_t *>(c->h_stage);
+    for (int64_t i = 0; i < n; i++) h[i] = (uint32_t)i;
+    if (n) W1G_CUDA(cudaMemcpyAsync(v, h, sizeof(uint32_t) * n, cudaMemcpyHostToDevice, c->stream));
+    W1G_TRY(radix_sort(*c, k, words, v, n, 64));
+    if (n) W1G_CUDA(cudaMemcpyAsync(perm, v, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost, c->stream));
+    W1G_CUDA(cudaStreamSynchronize(c->stream));
+    return W1G_OK;
+}

@@ -10,12 +10,14 @@
 //  * two presorted index lists per segment: X-list by (x, y) and Y-list by
 //    (y, x); both hold the same point set in the same position range;
 //  * bbox = first/last of each list (O(1)); rep = first of the X-list;
-//  * the split along the chosen axis is a prefix of that axis' list (binary
-//    search), only the other list is stably partitioned (one device scan);
+//  * the split along the chosen axis is a prefix of that axis' list, found
+//    by a warp-cooperative 32-ary search (one warp per segment); only the
+//    other list is stably partitioned (flags -> device scan -> scatter);
 //  * leaf children are finalised immediately, internal children become the
 //    next level's segments.
-// Levels run in batches without host synchronisation; the host only polls
-// the number of live segments between batches.
+// Levels run in batches without host synchronisation (kernels of levels past
+// the last one exit at once); the host polls the live-segment count between
+// batches.
 #include "common.cuh"
 
 namespace w1g {
@@ -31,15 +33,22 @@ struct SegInfo {
     int8_t axis, strict, pad0, pad1;
 };
 
-__device__ __forceinline__ void write_node(int64_t nid, double xmin, double ymin, double xmax,
-                                           double ymax, int64_t rep, int64_t size, int64_t l, int64_t r,
-                                           int64_t *left, int64_t *right, double4 *bbox, int64_t *reps,
-                                           int64_t *sizes, NodeGeom *geom, int2 *lr, int32_t *rep32) {
-    left[nid] = l;
-    right[nid] = r;
-    bbox[nid] = make_double4(xmin, ymin, xmax, ymax);
-    reps[nid] = rep;
-    sizes[nid] = size;
+struct TreeOut {
+    int64_t *left, *right, *rep, *size;
+    double4 *bbox;
+    NodeGeom *geom;
+    int2 *lr;
+    int32_t *rep32;
+};
+
+__device__ __forceinline__ void write_node(const TreeOut &o, int64_t nid, double xmin, double ymin,
+                                           double xmax, double ymax, int64_t rep, int64_t size, int64_t l,
+                                           int64_t r) {
+    o.left[nid] = l;
+    o.right[nid] = r;
+    o.bbox[nid] = make_double4(xmin, ymin, xmax, ymax);
+    o.rep[nid] = rep;
+    o.size[nid] = size;
     // per-node terms of _ws_predicate / _diag_sq, spanner.py:178-194
     const double w = dsub(xmax, xmin), h = dsub(ymax, ymin);
     const double dsq = dadd(dmul(w, w), dmul(h, h));
@@ -48,18 +57,10 @@ __device__ __forceinline__ void write_node(int64_t nid, double xmin, double ymin
     g.cy = dmul(0.5, dadd(ymin, ymax));
     g.r = dmul(0.5, dsqrt(dsq));
     g.dsq = dsq;
-    geom[nid] = g;
-    lr[nid] = make_int2((int)l, (int)r);
-    rep32[nid] = (int32_t)rep;
+    o.geom[nid] = g;
+    o.lr[nid] = make_int2((int)l, (int)r);
+    o.rep32[nid] = (int32_t)rep;
 }
-
-struct TreeOut {
-    int64_t *left, *right, *rep, *size;
-    double4 *bbox;
-    NodeGeom *geom;
-    int2 *lr;
-    int32_t *rep32;
-};
 
 __global__ void k_presort_keys(const double2 *pts, int64_t n, uint64_t *xl0, uint64_t *xl1,
                                uint64_t *yl0, uint64_t *yl1, uint32_t *vx, uint32_t *vy) {
@@ -83,9 +84,8 @@ __global__ void k_tree_init(int64_t n, Seg *seg, int32_t *pos_seg, int32_t *cnt,
         pos_seg[i] = n == 1 ? -1 : 0;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         if (n == 1) {
-            double2 p = pts[xl[0]];
-            write_node(0, p.x, p.y, p.x, p.y, xl[0], 1, -1, -1, o.left, o.right, o.bbox, o.rep,
-                       o.size, o.geom, o.lr, o.rep32);
+            const double2 p = pts[xl[0]];
+            write_node(o, 0, p.x, p.y, p.x, p.y, xl[0], 1, -1, -1);
             cnt[0] = 0;
         } else {
             seg[0] = Seg{0, (int32_t)n, 0, 0};
@@ -95,159 +95,166 @@ __global__ void k_tree_init(int64_t n, Seg *seg, int32_t *pos_seg, int32_t *cnt,
 }
 
 __device__ __forceinline__ double coord(const double2 *pts, uint32_t i, int axis) {
-    double2 p = pts[i];
+    const double2 p = pts[i];
     return axis ? p.y : p.x;
 }
 
-// per segment: bbox, rep, axis, split point, children (spanner.py:124-148)
-__global__ void k_tree_segments(const double2 *__restrict__ pts, const uint32_t *__restrict__ xl,
-                                const uint32_t *__restrict__ yl, const Seg *__restrict__ seg,
-                                const int32_t *cnt_cur, int32_t *cnt_next, Seg *seg_next,
-                                SegInfo *info, TreeOut o, int64_t *flags) {
-    const int nseg = *cnt_cur;
+// warp-cooperative count of the prefix of sorted list[lo, hi) whose
+// coordinate satisfies `c <= t` (strict = 0) or `c < t` (strict = 1)
+__device__ int warp_prefix_count(const double2 *pts, const uint32_t *list, int lo, int hi, int axis,
+                                 double t, int strict) {
     const int lane = threadIdx.x & 31;
-    const int stride = gridDim.x * blockDim.x;
-    for (int base = (blockIdx.x * blockDim.x + threadIdx.x) & ~31; base < nseg; base += stride) {
-        const int s = base + lane;
-        const bool valid = s < nseg;
-        int want = 0;
-        Seg sg{0, 0, 0, 0};
+    int a = lo, b = hi;  // all < a satisfy, all >= b fail
+    while (b - a > 32) {
+        const int step = (b - a + 31) >> 5;
+        const int p = a + lane * step;
+        bool ok = false;
+        if (p < b) {
+            const double c = coord(pts, list[p], axis);
+            ok = strict ? (c < t) : (c <= t);
+        }
+        const int k = __popc(__ballot_sync(0xffffffffu, ok));
+        const int na = k ? a + (k - 1) * step + 1 : a;
+        const int nb = k < 32 ? min(b, a + k * step) : b;
+        a = na;
+        b = nb;
+    }
+    const int p = a + lane;
+    bool ok = false;
+    if (p < b) {
+        const double c = coord(pts, list[p], axis);
+        ok = strict ? (c < t) : (c <= t);
+    }
+    return a + __popc(__ballot_sync(0xffffffffu, ok)) - lo;
+}
+
+// one warp per segment: bbox, rep, axis, split point, children (spanner.py:124-148)
+__global__ void __launch_bounds__(256) k_tree_segments(const double2 *__restrict__ pts,
+                                                       const uint32_t *__restrict__ xl,
+                                                       const uint32_t *__restrict__ yl,
+                                                       const Seg *__restrict__ seg, const int32_t *cnt_cur,
+                                                       int32_t *cnt_next, Seg *seg_next, SegInfo *info,
+                                                       TreeOut o, int64_t *flags) {
+    const int nseg = *cnt_cur;
+    if (nseg == 0) return;
+    const int lane = threadIdx.x & 31;
+    const int warps = (gridDim.x * blockDim.x) >> 5;
+    for (int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; s < nseg; s += warps) {
+        const Seg sg = seg[s];
+        const int lo = sg.lo, hi = sg.hi, n = hi - lo;
+        const uint32_t r0 = xl[lo];
+        const double xmin = pts[r0].x, xmax = pts[xl[hi - 1]].x;
+        const double ymin = pts[yl[lo]].y, ymax = pts[yl[hi - 1]].y;
+        const double ext_x = dsub(xmax, xmin), ext_y = dsub(ymax, ymin);
         SegInfo in{};
-        if (valid) {
-            sg = seg[s];
-            const int lo = sg.lo, hi = sg.hi, n = hi - lo;
-            const uint32_t r0 = xl[lo];
-            const double2 pr = pts[r0];
-            const double xmin = pr.x, xmax = pts[xl[hi - 1]].x;
-            const double ymin = pts[yl[lo]].y, ymax = pts[yl[hi - 1]].y;
-            const double ext_x = dsub(xmax, xmin), ext_y = dsub(ymax, ymin);
-            in.lo = lo;
-            in.hi = hi;
-            if (ext_x == 0.0 && ext_y == 0.0) {
-                // spanner.py:134-135
+        in.lo = lo;
+        in.hi = hi;
+        in.cl = in.cr = -1;
+        if (ext_x == 0.0 && ext_y == 0.0) {
+            // spanner.py:134-135; every position keeps its place and is retired
+            if (lane == 0) {
                 atomicOr((unsigned long long *)&flags[F_DUP], 1ull);
-                write_node(sg.nid, xmin, ymin, xmax, ymax, r0, n, -1, -1, o.left, o.right, o.bbox,
-                           o.rep, o.size, o.geom, o.lr, o.rep32);
-                in.nl = n;  // every position keeps its place and is retired
-                in.cl = in.cr = -1;
-                in.axis = 0;
-                in.strict = 0;
+                write_node(o, sg.nid, xmin, ymin, xmax, ymax, r0, n, -1, -1);
+                in.nl = n;
                 in.thr = INFINITY;
-            } else {
-                const int axis = ext_x >= ext_y ? 0 : 1;
-                const uint32_t *al = axis ? yl : xl;
-                const double amin = axis ? ymin : xmin, amax = axis ? ymax : xmax;
-                const double mid = dmul(0.5, dadd(amin, amax));
-                // count of coord <= mid: the axis list is sorted by that coordinate
-                int a = lo, b = hi;
-                while (a < b) {
-                    int m = (a + b) >> 1;
-                    if (coord(pts, al[m], axis) <= mid) a = m + 1; else b = m;
-                }
-                int nl = a - lo;
-                int strict = 0;
-                double thr = mid;
-                if (nl == 0 || nl == n) {
-                    strict = 1;  // split off the max-attaining points instead
-                    thr = amax;
-                    a = lo;
-                    b = hi;
-                    while (a < b) {
-                        int m = (a + b) >> 1;
-                        if (coord(pts, al[m], axis) < amax) a = m + 1; else b = m;
-                    }
-                    nl = a - lo;
-                }
-                const int64_t lid = (int64_t)sg.nid + 1, rid = (int64_t)sg.nid + 2 * (int64_t)nl;
-                write_node(sg.nid, xmin, ymin, xmax, ymax, r0, n, lid, rid, o.left, o.right, o.bbox,
-                           o.rep, o.size, o.geom, o.lr, o.rep32);
-                in.nl = nl;
-                in.axis = (int8_t)axis;
-                in.strict = (int8_t)strict;
-                in.thr = thr;
-                in.cl = in.cr = -1;
-                if (nl == 1) {
-                    const uint32_t pi = al[lo];
-                    const double2 p = pts[pi];
-                    write_node(lid, p.x, p.y, p.x, p.y, pi, 1, -1, -1, o.left, o.right, o.bbox, o.rep,
-                               o.size, o.geom, o.lr, o.rep32);
-                } else {
-                    want++;
-                }
-                if (n - nl == 1) {
-                    const uint32_t pi = al[lo + nl];
-                    const double2 p = pts[pi];
-                    write_node(rid, p.x, p.y, p.x, p.y, pi, 1, -1, -1, o.left, o.right, o.bbox, o.rep,
-                               o.size, o.geom, o.lr, o.rep32);
-                } else {
-                    want++;
-                }
+                info[s] = in;
             }
+            continue;
         }
-        // warp-aggregated slot allocation for the internal children
-        int x = want;
-        for (int off = 1; off < 32; off <<= 1) {
-            int y = __shfl_up_sync(0xffffffffu, x, off);
-            if (lane >= off) x += y;
+        const int axis = ext_x >= ext_y ? 0 : 1;
+        const uint32_t *al = axis ? yl : xl;
+        const double amin = axis ? ymin : xmin, amax = axis ? ymax : xmax;
+        const double mid = dmul(0.5, dadd(amin, amax));
+        int nl = warp_prefix_count(pts, al, lo, hi, axis, mid, 0);
+        int strict = 0;
+        double thr = mid;
+        if (nl == 0 || nl == n) {
+            strict = 1;  // split off the max-attaining points instead
+            thr = amax;
+            nl = warp_prefix_count(pts, al, lo, hi, axis, amax, 1);
         }
-        const int tot = __shfl_sync(0xffffffffu, x, 31);
-        int wb = 0;
-        if (lane == 31 && tot) wb = atomicAdd(cnt_next, tot);
-        wb = __shfl_sync(0xffffffffu, wb, 31);
-        int slot = wb + x - want;
-        if (valid) {
-            if (want) {
-                const int nr = in.hi - in.lo - in.nl;
-                if (in.nl > 1) {
-                    in.cl = slot++;
-                    seg_next[in.cl] = Seg{in.lo, in.lo + in.nl, sg.nid + 1, 0};
-                }
-                if (nr > 1) {
-                    in.cr = slot;
-                    seg_next[in.cr] = Seg{in.lo + in.nl, in.hi, sg.nid + 2 * in.nl, 0};
-                }
+        if (lane == 0) {
+            const int64_t lid = (int64_t)sg.nid + 1, rid = (int64_t)sg.nid + 2 * (int64_t)nl;
+            write_node(o, sg.nid, xmin, ymin, xmax, ymax, r0, n, lid, rid);
+            in.nl = nl;
+            in.axis = (int8_t)axis;
+            in.strict = (int8_t)strict;
+            in.thr = thr;
+            const int nr = n - nl;
+            const int want = (nl > 1) + (nr > 1);
+            int slot = want ? atomicAdd(cnt_next, want) : 0;
+            if (nl == 1) {
+                const uint32_t pi = al[lo];
+                const double2 p = pts[pi];
+                write_node(o, lid, p.x, p.y, p.x, p.y, pi, 1, -1, -1);
+            } else {
+                in.cl = slot++;
+                seg_next[in.cl] = Seg{lo, lo + nl, (int32_t)lid, 0};
+            }
+            if (nr == 1) {
+                const uint32_t pi = al[lo + nl];
+                const double2 p = pts[pi];
+                write_node(o, rid, p.x, p.y, p.x, p.y, pi, 1, -1, -1);
+            } else {
+                in.cr = slot;
+                seg_next[in.cr] = Seg{lo + nl, hi, (int32_t)rid, 0};
             }
             info[s] = in;
         }
     }
 }
 
-struct PartFlag {
-    const double2 *pts;
-    const uint32_t *xl, *yl;
-    const int32_t *pos_seg;
-    const SegInfo *info;
-    __device__ int64_t operator()(int64_t p) const {
-        const int s = pos_seg[p];
-        if (s < 0) return 0;
-        const SegInfo &in = info[s];
-        const uint32_t e = in.axis ? xl[p] : yl[p];  // element of the OTHER list
-        const double c = coord(pts, e, in.axis);
-        return (in.strict ? (c < in.thr) : (c <= in.thr)) ? 1 : 0;
-    }
-};
-
-__global__ void k_tree_scatter(PartFlag f, int64_t n, const int64_t *excl, uint32_t *xl_new,
-                               uint32_t *yl_new, int32_t *pos_seg_new, int32_t *cnt_clear) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) *cnt_clear = 0;
+// per position: 1 if the OTHER list's element goes to the left child
+__global__ void k_tree_flags(const double2 *__restrict__ pts, const uint32_t *__restrict__ xl,
+                             const uint32_t *__restrict__ yl, const int32_t *__restrict__ pos_seg,
+                             const SegInfo *__restrict__ info, const int32_t *cnt_cur, int64_t n,
+                             int32_t *fl) {
+    if (*cnt_cur == 0) return;
     for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
          p += (int64_t)gridDim.x * blockDim.x) {
-        const int s = f.pos_seg[p];
+        const int s = pos_seg[p];
+        int f = 0;
+        if (s >= 0) {
+            const SegInfo &in = info[s];
+            const uint32_t e = in.axis ? xl[p] : yl[p];
+            const double c = coord(pts, e, in.axis);
+            f = (in.strict ? (c < in.thr) : (c <= in.thr)) ? 1 : 0;
+        }
+        fl[p] = f;
+    }
+}
+
+struct FlagVal {
+    const int32_t *fl;
+    __device__ int64_t operator()(int64_t i) const { return fl[i]; }
+};
+
+__global__ void k_tree_scatter(const uint32_t *__restrict__ xl, const uint32_t *__restrict__ yl,
+                               const int32_t *__restrict__ pos_seg, const SegInfo *__restrict__ info,
+                               const int32_t *__restrict__ fl, const int64_t *__restrict__ excl,
+                               const int32_t *cnt_cur, int64_t n, uint32_t *xl_new, uint32_t *yl_new,
+                               int32_t *pos_seg_new, int32_t *cnt_clear) {
+    // clear the counter two levels ahead even on a dead level, so stale counts
+    // can never revive a finished ring slot
+    if (blockIdx.x == 0 && threadIdx.x == 0) *cnt_clear = 0;
+    if (*cnt_cur == 0) return;
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        const int s = pos_seg[p];
         if (s < 0) {
             pos_seg_new[p] = -1;
             continue;
         }
-        const SegInfo in = f.info[s];
-        const bool fl = f(p) != 0;
+        const SegInfo in = info[s];
         const int64_t rt = excl[p] - excl[in.lo];
         const int64_t rf = (p - in.lo) - rt;
-        const int64_t np_ = fl ? in.lo + rt : in.lo + in.nl + rf;
+        const int64_t np_ = fl[p] ? in.lo + rt : in.lo + in.nl + rf;
         if (in.axis) {  // split on y: Y-list stays, X-list is partitioned
-            yl_new[p] = f.yl[p];
-            xl_new[np_] = f.xl[p];
+            yl_new[p] = yl[p];
+            xl_new[np_] = xl[p];
         } else {
-            xl_new[p] = f.xl[p];
-            yl_new[np_] = f.yl[p];
+            xl_new[p] = xl[p];
+            yl_new[np_] = yl[p];
         }
         pos_seg_new[p] = (p < in.lo + in.nl) ? in.cl : in.cr;
     }
@@ -333,7 +340,7 @@ int tree_run(Ctx &c, const double2 *pts, int64_t n, int64_t *n_nodes, int32_t *d
     // level state
     Seg *seg[2];
     SegInfo *info;
-    int32_t *pos_seg[2], *cnt;
+    int32_t *pos_seg[2], *cnt, *fl;
     int64_t *excl;
     const int64_t seg_cap = n / 2 + 2;
     W1G_TRY(ensure(c.scr[10], (size_t)seg_cap, &seg[0]));
@@ -341,6 +348,7 @@ int tree_run(Ctx &c, const double2 *pts, int64_t n, int64_t *n_nodes, int32_t *d
     W1G_TRY(ensure(c.scr[12], (size_t)seg_cap, &info));
     W1G_TRY(ensure(c.scr[13], (size_t)n, &pos_seg[0]));
     W1G_TRY(ensure(c.scr[14], (size_t)n, &pos_seg[1]));
+    W1G_TRY(ensure(c.scr[16], (size_t)n, &fl));
     W1G_TRY(ensure(c.scr[3], (size_t)n, &excl));
     const int max_levels = (int)(n + 2);
     // live-segment counters, a ring of 3: level l reads cnt[l%3], appends to
@@ -350,18 +358,21 @@ int tree_run(Ctx &c, const double2 *pts, int64_t n, int64_t *n_nodes, int32_t *d
     W1G_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * 8, c.stream));
     k_tree_init<<<g, 256, 0, c.stream>>>(n, seg[0], pos_seg[0], cnt, pts, xl[0], o);
     W1G_CHECK_LAUNCH();
-    const unsigned gseg = grid_for(seg_cap, 256, 4u * c.sm_count);
+    // one warp per segment
+    const unsigned gseg = grid_for(seg_cap * 32, 256, 16u * c.sm_count);
     int level = 0, cur = 0;
-    const int BATCH = 8;
+    const int BATCH = 12;
     while (true) {
         for (int b = 0; b < BATCH; b++, level++) {
-            k_tree_segments<<<gseg, 256, 0, c.stream>>>(pts, xl[cur], yl[cur], seg[cur], cnt + level % 3,
-                                                       cnt + (level + 1) % 3, seg[cur ^ 1], info, o, dflags(c));
+            const int32_t *cc = cnt + level % 3;
+            k_tree_segments<<<gseg, 256, 0, c.stream>>>(pts, xl[cur], yl[cur], seg[cur], cc, cnt + (level + 1) % 3,
+                                                       seg[cur ^ 1], info, o, dflags(c));
             W1G_CHECK_LAUNCH();
-            PartFlag f{pts, xl[cur], yl[cur], pos_seg[cur], info};
-            W1G_TRY(scan_i64(c, f, n, excl, nullptr));
-            k_tree_scatter<<<g, 256, 0, c.stream>>>(f, n, excl, xl[cur ^ 1], yl[cur ^ 1], pos_seg[cur ^ 1],
-                                                   cnt + (level + 2) % 3);
+            k_tree_flags<<<g, 256, 0, c.stream>>>(pts, xl[cur], yl[cur], pos_seg[cur], info, cc, n, fl);
+            W1G_CHECK_LAUNCH();
+            W1G_TRY(scan_i64(c, FlagVal{fl}, n, excl, nullptr, cc));
+            k_tree_scatter<<<g, 256, 0, c.stream>>>(xl[cur], yl[cur], pos_seg[cur], info, fl, excl, cc, n,
+                                                   xl[cur ^ 1], yl[cur ^ 1], pos_seg[cur ^ 1], cnt + (level + 2) % 3);
             W1G_CHECK_LAUNCH();
             cur ^= 1;
         }
@@ -377,7 +388,6 @@ int tree_run(Ctx &c, const double2 *pts, int64_t n, int64_t *n_nodes, int32_t *d
         }
         if (live == 0 || level > max_levels) break;
     }
-    // depth: levels that had live segments (+ the leaf level)
     c.tree_depth = level;
     *depth = level;
     c.tree_valid = true;

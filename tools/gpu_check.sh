@@ -1,8 +1,7 @@
-set -x
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
+# tests + smoke + bench on one B200 (used by gpurun)
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke_rc=$?
-tail -5 gpurun_out/smoke.log
+tail -3 gpurun_out/smoke.log
 timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest_rc=$?
-tail -30 gpurun_out/pytest_gpu.log
-timeout 600 python bench.py --steps 5 --warmup 3 > gpurun_out/bench.log 2>&1; echo bench_rc=$?
-tail -5 gpurun_out/bench.log
+tail -15 gpurun_out/pytest_gpu.log
+timeout 600 python bench.py --steps 10 --warmup 3 ${BENCH_ARGS} > gpurun_out/bench.log 2>&1; echo bench_rc=$?
+tail -3 gpurun_out/bench.log
