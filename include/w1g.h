@@ -64,6 +64,9 @@ typedef struct {
 } w1g_front_end_info;
 
 int w1g_version(void);
+/* page-locked host memory for zero-copy result arrays (cudaHostAlloc) */
+int w1g_host_alloc(uint64_t bytes, void **out);
+int w1g_host_free(void *p);
 /* number of CUDA kernels this library has launched (process-wide) */
 uint64_t w1g_launch_count(void);
 /* measurement hook: time `reps` launches of the FP32 all-pairs RWMD tile

@@ -70,6 +70,8 @@ STAGES = ("zero_condense", "rwmd", "delta_condense", "split_tree", "wspd", "emit
 # (name, restype, argtypes)
 _PROTOS = [
     ("w1g_version", ctypes.c_int, []),
+    ("w1g_host_alloc", ctypes.c_int, [ctypes.c_uint64, ctypes.POINTER(_vp)]),
+    ("w1g_host_free", ctypes.c_int, [_vp]),
     ("w1g_launch_count", ctypes.c_uint64, []),
     ("w1g_profile_rwmd_tile", ctypes.c_int, [_vp, ctypes.c_int, ctypes.POINTER(ctypes.c_float), _I64P]),
     ("w1g_debug_radix_sort", ctypes.c_int, [_vp, _vp, ctypes.c_int, _i64, _vp]),
@@ -224,6 +226,77 @@ def device_count() -> int:
     n = ctypes.c_int32(0)
     check(load().w1g_device_count(ctypes.byref(n)))
     return int(n.value)
+
+
+class _PinnedBlock:
+    """One page-locked allocation; returns itself to the pool when the last
+    numpy array carved from it is garbage-collected."""
+
+    __slots__ = ("ptr", "size", "__weakref__")
+
+    def __init__(self, ptr: int, size: int):
+        self.ptr = ptr
+        self.size = size
+
+    def __del__(self):
+        try:
+            _pool_release(self.ptr, self.size)
+        except Exception:
+            pass
+
+
+_pool_free: dict[int, list[int]] = {}
+_pool_lock = threading.Lock()
+_POOL_KEEP = 8  # free blocks kept per size class
+
+
+def _size_class(n: int) -> int:
+    c = 1 << 20
+    while c < n:
+        c <<= 1
+    return c
+
+
+def _pool_release(ptr: int, size: int):
+    with _pool_lock:
+        lst = _pool_free.setdefault(size, [])
+        if len(lst) < _POOL_KEEP:
+            lst.append(ptr)
+            return
+    load().w1g_host_free(ctypes.c_void_p(ptr))
+
+
+def pinned_arrays(specs):
+    """numpy arrays [(shape, dtype), ...] carved from one pooled page-locked
+    block, so device->host copies of results run at full link speed and the
+    arrays are handed to the caller without a host-side copy."""
+    offs, total = [], 0
+    for shape, dtype in specs:
+        total = (total + 63) & ~63
+        offs.append(total)
+        total += int(np.prod(shape, dtype=np.int64)) * np.dtype(dtype).itemsize
+    size = _size_class(max(total, 1))
+    with _pool_lock:
+        lst = _pool_free.get(size)
+        ptr = lst.pop() if lst else None
+    if ptr is None:
+        p = _vp()
+        check(load().w1g_host_alloc(size, ctypes.byref(p)))
+        ptr = p.value
+    block = _PinnedBlock(ptr, size)
+    holder_base = np.ctypeslib.as_array((ctypes.c_uint8 * size).from_address(ptr))
+    out = []
+    for (shape, dtype), off in zip(specs, offs):
+        nb = int(np.prod(shape, dtype=np.int64)) * np.dtype(dtype).itemsize
+        out.append(holder_base[off:off + nb].view(dtype).reshape(shape))
+    _keepalive[id(holder_base)] = block
+    import weakref
+
+    weakref.finalize(holder_base, _keepalive.pop, id(holder_base), None)
+    return out
+
+
+_keepalive: dict[int, _PinnedBlock] = {}
 
 
 def launch_count() -> int:

@@ -129,6 +129,18 @@ int w1g_version(void) { return 10000; }
 
 uint64_t w1g_launch_count(void) { return __atomic_load_n(&g_launches, __ATOMIC_RELAXED); }
 
+int w1g_host_alloc(uint64_t bytes, void **out) {
+    if (!out) return W1G_EINVAL;
+    *out = nullptr;
+    W1G_CUDA(cudaHostAlloc(out, bytes ? bytes : 1, cudaHostAllocPortable));
+    return W1G_OK;
+}
+
+int w1g_host_free(void *p) {
+    if (p) W1G_CUDA(cudaFreeHost(p));
+    return W1G_OK;
+}
+
 int w1g_profile_rwmd_tile(w1g_ctx *c, int reps, float *ms_per_launch, int64_t *evals_per_launch) {
     CTX_CHECK(c);
     if (!c->nodes[0].valid) {
@@ -184,6 +196,7 @@ int w1g_ctx_destroy(w1g_ctx *c) {
     }
     for (auto &b : c->scr) free_buf(b);
     for (auto &b : c->sort_scr) free_buf(b);
+    for (auto &b : c->lex_scr) free_buf(b);
     if (c->h_pinned) cudaFreeHost(c->h_pinned);
     if (c->h_stage) cudaFreeHost(c->h_stage);
     for (auto &e : c->ev)
@@ -620,8 +633,13 @@ int w1g_front_end(w1g_ctx *c, const double *a, int64_t na, const double *b, int6
     if (na < 0 || nb < 0) return W1G_EINVAL;
     double2 *d;
     W1G_TRY(ensure(c->in_pts, (size_t)(na + nb), &d));
-    if (na) W1G_CUDA(cudaMemcpyAsync(d, a, sizeof(double2) * na, cudaMemcpyHostToDevice, c->stream));
-    if (nb) W1G_CUDA(cudaMemcpyAsync(d + na, b, sizeof(double2) * nb, cudaMemcpyHostToDevice, c->stream));
+    // stage both diagrams through pinned memory: one full-speed H2D
+    const size_t bytes = sizeof(double2) * (size_t)(na + nb);
+    W1G_TRY(stage_ensure(*c, bytes));
+    W1G_CUDA(cudaStreamSynchronize(c->stream));
+    if (na) memcpy(c->h_stage, a, sizeof(double2) * na);
+    if (nb) memcpy(static_cast<char *>(c->h_stage) + sizeof(double2) * na, b, sizeof(double2) * nb);
+    if (bytes) W1G_CUDA(cudaMemcpyAsync(d, c->h_stage, bytes, cudaMemcpyHostToDevice, c->stream));
     return w1g_front_end_device(c, reinterpret_cast<double *>(d), na,
                                 reinterpret_cast<double *>(d + na), nb, s, use_condensation,
                                 delta_mode, delta, k, seed, info);

@@ -126,6 +126,7 @@ struct Ctx {
     // scratch
     DevBuf scr[SCR_N];
     DevBuf sort_scr[8];
+    DevBuf lex_scr[6];  // sort_lex2 scratch
     unsigned sort_epoch = 0;  // onesweep status-word epoch (sort.cu)
     DevBuf scan_state;
     DevBuf flags;  // small device flag block (int64 x 64)
@@ -309,6 +310,11 @@ int scan_i64(Ctx &c, F f, int64_t n, int64_t *out, int64_t *total, const int32_t
 // digit histogram per sort).  bits_hint limits the digits considered in the
 // most-significant word (64 = all).
 int radix_sort(Ctx &c, uint64_t **keys, int words, uint32_t *vals, int64_t n, int top_bits = 64);
+// Stable sort of vals (initially the element ids 0..n-1, or any payload that
+// indexes `secondary`) by (primary[i], secondary[vals[i]]): radix sort by the
+// primary word, then only the elements of primary-tie runs by both words.
+// `primary` is indexed by position in the input order, `secondary` by payload.
+int sort_lex2(Ctx &c, const uint64_t *primary, const uint64_t *secondary, uint32_t *vals, int64_t n);
 
 // ------------------------------------------------------------------ misc
 inline unsigned grid_for(int64_t n, int block, unsigned cap = 0x7fffffffu) {

@@ -208,8 +208,8 @@ int zc_run(Ctx &c, const double2 *d_a, int64_t na, const double2 *d_b, int64_t n
     W1G_TRY(flags_reset(c));
     k_zc_keys<<<gs(c, n), 256, 0, c.stream>>>(d_a, na, d_b, n, hi, lo, vals);
     W1G_CHECK_LAUNCH();
-    uint64_t *keys[2] = {lo, hi};
-    W1G_TRY(radix_sort(c, keys, 2, vals, n));
+    // lexicographic (x, y): radix by x, y only where x ties
+    W1G_TRY(sort_lex2(c, hi, lo, vals, n));
     ZcFlag f{d_a, d_b, na, vals};
     W1G_TRY(scan_i64(c, f, n, excl, dflags(c) + F_K0));
     W1G_CUDA(cudaMemsetAsync(am, 0, sizeof(int64_t) * n, c.stream));

@@ -156,6 +156,7 @@ __device__ __forceinline__ double upper_bound(float est, float qn) {
 
 constexpr int RF_BLOCK = 128;
 constexpr int RF_CAND = 2048;
+constexpr int RF_STAGE = 8;  // candidate tiles staged per round (8 x 64 targets, 8 KB)
 
 // exact fp64 refinement + mass * best (lower_bound.py:51-58); one source per
 // thread, sources in Morton order, target tiles kept by a box test
@@ -168,6 +169,8 @@ __global__ void __launch_bounds__(RF_BLOCK) k_refine(const double2 *__restrict__
                                                      const double4 *__restrict__ tbox,
                                                      double *__restrict__ best_out, double *__restrict__ terms) {
     __shared__ int32_t s_cand[RF_CAND];
+    __shared__ double2 s_t[RF_STAGE * RT];
+    __shared__ double4 s_tb[RF_STAGE];
     __shared__ int s_nc;
     __shared__ double s_r[RF_BLOCK / 32];
     __shared__ double4 s_box[RF_BLOCK / 32];
@@ -230,20 +233,32 @@ __global__ void __launch_bounds__(RF_BLOCK) k_refine(const double2 *__restrict__
                 if (box_gap(tbox[k], qb) <= rmax) s_cand[atomicAdd(&s_nc, 1)] = (int32_t)k;
             __syncthreads();
             const int nc = s_nc;
-            if (valid && r >= 0.0) {
-                for (int c = 0; c < nc; c++) {
-                    const int64_t k = s_cand[c];
-                    if (box_gap(tbox[k], pb) > r * (1.0 + 1e-9)) continue;
-                    const int64_t te = min(nt, (k + 1) * RT);
-                    for (int64_t j = k * RT; j < te; j++) {
-                        const double2 tt = t[j];
+            // candidate tiles are staged RF_STAGE at a time in shared memory; a
+            // warp evaluates a staged tile (all lanes, uniformly) iff one of its
+            // sources needs it -- extra exact distances never change the min
+            for (int c0 = 0; c0 < nc; c0 += RF_STAGE) {
+                const int ns = min(RF_STAGE, nc - c0);
+                for (int e = tid; e < ns * RT; e += RF_BLOCK) {
+                    const int64_t k = s_cand[c0 + e / RT];
+                    const int64_t j = k * RT + (e % RT);
+                    s_t[e] = j < nt ? t[j] : make_double2(INFINITY, INFINITY);
+                }
+                if (tid < ns) s_tb[tid] = tbox[s_cand[c0 + tid]];
+                __syncthreads();
+                for (int c = 0; c < ns; c++) {
+                    const bool need = valid && r >= 0.0 && box_gap(s_tb[c], pb) <= r * (1.0 + 1e-9);
+                    if (!__any_sync(0xffffffffu, need)) continue;
+                    const double2 *st = s_t + c * RT;
+#pragma unroll 8
+                    for (int j = 0; j < RT; j++) {
+                        const double2 tt = st[j];
                         const double dx = dsub(p.x, tt.x), dy = dsub(p.y, tt.y);
                         const double d2 = dadd(dmul(dx, dx), dmul(dy, dy));
                         m2 = d2 < m2 ? d2 : m2;
                     }
                 }
+                __syncthreads();
             }
-            __syncthreads();
         }
     }
     if (valid) {
@@ -352,7 +367,7 @@ int rwmd_run(Ctx &c, double *L, double *LA, double *LB) {
     W1G_TRY(ensure(c.scr[12], 4, &dres));
     W1G_TRY(ensure(c.scr[13], (size_t)mx, &mf));
     W1G_TRY(ensure(c.scr[14], (size_t)mx, &qn));
-    W1G_TRY(ensure(c.scr[15], (size_t)mx / 1024 + 2, &tbox));
+    W1G_TRY(ensure(c.scr[15], (size_t)mx / 64 + 2, &tbox));  // per-tile boxes (tiles >= 64 targets)
     W1G_TRY(ensure(c.scr[16], (size_t)mx / 64 + 2, &box64));
     for (int s = 0; s < 2; s++) {
         const int o = 1 - s;
@@ -400,7 +415,7 @@ int rwmd_tile_profile(Ctx &c, int reps, float *ms, int64_t *evals) {
     double4 *tbox;
     W1G_TRY(ensure(c.scr[13], (size_t)mx, &mf));
     W1G_TRY(ensure(c.scr[14], (size_t)mx, &qn));
-    W1G_TRY(ensure(c.scr[15], (size_t)mx / 1024 + 2, &tbox));
+    W1G_TRY(ensure(c.scr[15], (size_t)mx / 64 + 2, &tbox));  // per-tile boxes (tiles >= 64 targets)
     W1G_CUDA(cudaEventRecord(c.ev[8], c.stream));
     for (int r = 0; r < reps; r++) {
         W1G_TRY(rwmd_f32_min(c, F.mpts[0], na, F.mpts[1], nb, F.scale, mf, qn, tbox, c.culling));

@@ -33,8 +33,9 @@ namespace w1g {
 namespace {
 
 constexpr int T_BLOCK = 256;
-constexpr int T_TS = 1024;  // targets per shared-memory tile
-constexpr int CULL_STEPS = 3;  // culled mode: the Morton-nearest tile and its two neighbours
+constexpr int TS_FULL = 1024;  // targets per shared-memory tile, full mode
+constexpr int TS_CULL = 256;   // targets per shared-memory tile, culled mode
+constexpr int CULL_STEPS = 5;  // culled mode: the Morton-nearest tile and four neighbours
 
 __device__ __forceinline__ float min3(float a, float b, float c) {
     float d;
@@ -60,7 +61,7 @@ struct TileArgs {
     int chunk;              // targets per grid.y chunk (full mode)
 };
 
-template <int R, bool CULL>
+template <int R, bool CULL, int T_TS>
 __global__ void __launch_bounds__(T_BLOCK) k_rwmd_f32(TileArgs A) {
     __shared__ float4 s_xy[T_TS / 2];
     __shared__ float2 s_tt[T_TS / 2];
@@ -212,7 +213,7 @@ __global__ void __launch_bounds__(T_BLOCK) k_rwmd_f32(TileArgs A) {
     }
 }
 
-__global__ void k_tile_boxes(const double2 *t, int nt, double4 *box) {
+__global__ void k_tile_boxes(const double2 *t, int nt, int T_TS, double4 *box) {
     const int lane = threadIdx.x & 31;
     const int ntile = (nt + T_TS - 1) / T_TS;
     for (int tile = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; tile < ntile;
@@ -254,13 +255,13 @@ int rwmd_f32_min(Ctx &c, const double2 *q, int64_t nq, const double2 *t, int64_t
     A.mout = mout;
     A.qn_out = qn_out;
     if (culling) {
-        const int ntile = (int)((nt + T_TS - 1) / T_TS);
-        k_tile_boxes<<<grid_for((int64_t)ntile * 32, 256, 8u * c.sm_count), 256, 0, c.stream>>>(t, (int)nt, tbox);
+        const int ntile = (int)((nt + TS_CULL - 1) / TS_CULL);
+        k_tile_boxes<<<grid_for((int64_t)ntile * 32, 256, 8u * c.sm_count), 256, 0, c.stream>>>(t, (int)nt, TS_CULL, tbox);
         W1G_CHECK_LAUNCH();
         constexpr int R = 2;
         const int gx = (int)((nq + T_BLOCK * R - 1) / (T_BLOCK * R));
         A.chunk = (int)nt;
-        k_rwmd_f32<R, true><<<gx, T_BLOCK, 0, c.stream>>>(A);
+        k_rwmd_f32<R, true, TS_CULL><<<gx, T_BLOCK, 0, c.stream>>>(A);
         W1G_CHECK_LAUNCH();
         return W1G_OK;
     }
@@ -270,7 +271,7 @@ int rwmd_f32_min(Ctx &c, const double2 *q, int64_t nq, const double2 *t, int64_t
     // enough CTAs for several waves of the resident CTAs on every SM
     const int want = 16 * c.sm_count;
     int gy = (want + gx - 1) / gx;
-    const int64_t max_gy = (nt + T_TS - 1) / T_TS;
+    const int64_t max_gy = (nt + TS_FULL - 1) / TS_FULL;
     if (gy > max_gy) gy = (int)max_gy;
     if (gy < 1) gy = 1;
     if (gy > 65535) gy = 65535;
@@ -278,7 +279,7 @@ int rwmd_f32_min(Ctx &c, const double2 *q, int64_t nq, const double2 *t, int64_t
     chunk = (chunk + 1) & ~1;
     gy = (int)((nt + chunk - 1) / chunk);
     A.chunk = chunk;
-    k_rwmd_f32<R, false><<<dim3(gx, gy), T_BLOCK, 0, c.stream>>>(A);
+    k_rwmd_f32<R, false, TS_FULL><<<dim3(gx, gy), T_BLOCK, 0, c.stream>>>(A);
     W1G_CHECK_LAUNCH();
     return W1G_OK;
 }

@@ -21,8 +21,8 @@ namespace {
 
 constexpr int RS_BLOCK = 256;
 constexpr int RS_WARPS = RS_BLOCK / 32;
-constexpr int RS_IPT = 16;
-constexpr int RS_TILE = RS_BLOCK * RS_IPT;  // 4096
+constexpr int RS_IPT = 8;
+constexpr int RS_TILE = RS_BLOCK * RS_IPT;  // 2048
 constexpr int RS_WTILE = 32 * RS_IPT;       // items per warp
 
 struct KeyPtrs {
@@ -85,17 +85,21 @@ __global__ void __launch_bounds__(RS_BLOCK) k_rs_onesweep(KeyPtrs src, KeyPtrs d
     // 1. stable rank inside the tile (warp w owns items [w*512, (w+1)*512), striped)
     uint16_t rank[RS_IPT];
     uint16_t dig[RS_IPT];
+    // issue every load of the tile before the (warp-synchronous) ranking loop
 #pragma unroll
     for (int i = 0; i < RS_IPT; i++) {
         const int li = wid * RS_WTILE + i * 32 + lane;
-        const int d = li < tn ? (int)((kd[tbase + li] >> shift) & 255) : 256;
+        dig[i] = li < tn ? (uint16_t)((kd[tbase + li] >> shift) & 255) : (uint16_t)256;
+    }
+#pragma unroll
+    for (int i = 0; i < RS_IPT; i++) {
+        const int d = dig[i];
         const unsigned peers = __match_any_sync(0xffffffffu, d);
         const uint32_t b = whist[wid][d];
         __syncwarp();
         if ((__ffs(peers) - 1) == lane) whist[wid][d] = b + __popc(peers);
         __syncwarp();
         rank[i] = (uint16_t)(b + __popc(peers & lt));
-        dig[i] = (uint16_t)d;
     }
     __syncthreads();
     // 2. per-digit tile counts, warp prefixes, tile-local digit starts
@@ -292,6 +296,97 @@ int radix_sort(Ctx &c, uint64_t **keys, int words, uint32_t *vals, int64_t n, in
         W1G_CUDA(cudaMemcpyAsync(keys[words - 1], src->k[words - 1], sizeof(uint64_t) * n,
                                  cudaMemcpyDeviceToDevice, c.stream));
     }
+    return W1G_OK;
+}
+
+// ---------------------------------------------------------------- (primary, secondary) sort
+//
+// Stable sort by a 128-bit key (primary word, then secondary word) that only
+// pays for the secondary word where primaries tie: one 64-bit radix sort by
+// the primary, then the elements of tie runs (usually none for real-valued
+// coordinates; everything for H0-style diagrams whose births are all 0) are
+// sorted by (primary, secondary) and written back into their run slots.
+
+namespace {
+
+__global__ void k_copy_u64(const uint64_t *src, uint64_t *dst, int64_t n) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = src[i];
+}
+
+struct TieFlag {
+    const uint64_t *k;
+    int64_t n;
+    __device__ int64_t operator()(int64_t i) const {
+        const uint64_t v = k[i];
+        return ((i > 0 && k[i - 1] == v) || (i + 1 < n && k[i + 1] == v)) ? 1 : 0;
+    }
+};
+
+__global__ void k_tie_gather(TieFlag f, const int64_t *excl, const uint32_t *vals, const uint64_t *sec,
+                             uint32_t *tpos, uint64_t *kl, uint64_t *kh, uint32_t *pl) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < f.n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        if (!f(i)) continue;
+        const int64_t r = excl[i];
+        tpos[r] = (uint32_t)i;
+        kh[r] = f.k[i];
+        kl[r] = sec[vals[i]];
+        pl[r] = (uint32_t)r;
+    }
+}
+
+__global__ void k_tie_fetch(const uint32_t *tpos, const uint32_t *pl, const uint32_t *vals, int64_t t,
+                            uint32_t *tmp) {
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < t;
+         r += (int64_t)gridDim.x * blockDim.x)
+        tmp[r] = vals[tpos[pl[r]]];
+}
+
+__global__ void k_tie_put(const uint32_t *tpos, const uint32_t *tmp, int64_t t, uint32_t *vals) {
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < t;
+         r += (int64_t)gridDim.x * blockDim.x)
+        vals[tpos[r]] = tmp[r];
+}
+
+}  // namespace
+
+int sort_lex2(Ctx &c, const uint64_t *primary, const uint64_t *secondary, uint32_t *vals, int64_t n) {
+    if (n <= 1) return W1G_OK;
+    uint64_t *pk;
+    int64_t *excl;
+    W1G_TRY(ensure(c.lex_scr[0], (size_t)n, &pk));
+    W1G_TRY(ensure(c.lex_scr[1], (size_t)n, &excl));
+    const unsigned g = grid_for(n, 256, 8u * c.sm_count);
+    k_copy_u64<<<g, 256, 0, c.stream>>>(primary, pk, n);
+    W1G_CHECK_LAUNCH();
+    uint64_t *k1[1] = {pk};
+    W1G_TRY(radix_sort(c, k1, 1, vals, n, 64));
+    TieFlag f{pk, n};
+    int64_t *dt = ptr<int64_t>(c.flags) + F_MISC3;
+    W1G_TRY(scan_i64(c, f, n, excl, dt));
+    int64_t T = 0;
+    W1G_CUDA(cudaMemcpyAsync(&c.h_pinned[F_MISC3], dt, sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream));
+    W1G_CUDA(cudaStreamSynchronize(c.stream));
+    T = c.h_pinned[F_MISC3];
+    if (T == 0) return W1G_OK;
+    uint32_t *tpos, *pl, *tmp;
+    uint64_t *kl, *kh;
+    W1G_TRY(ensure(c.lex_scr[2], (size_t)T, &tpos));
+    W1G_TRY(ensure(c.lex_scr[3], (size_t)T, &kl));
+    W1G_TRY(ensure(c.lex_scr[4], (size_t)T, &kh));
+    W1G_TRY(ensure(c.lex_scr[5], (size_t)T * 2, &pl));
+    tmp = pl + T;
+    k_tie_gather<<<g, 256, 0, c.stream>>>(f, excl, vals, secondary, tpos, kl, kh, pl);
+    W1G_CHECK_LAUNCH();
+    uint64_t *k2[2] = {kl, kh};
+    W1G_TRY(radix_sort(c, k2, 2, pl, T, 64));
+    const unsigned gt = grid_for(T, 256, 8u * c.sm_count);
+    k_tie_fetch<<<gt, 256, 0, c.stream>>>(tpos, pl, vals, T, tmp);
+    W1G_CHECK_LAUNCH();
+    k_tie_put<<<gt, 256, 0, c.stream>>>(tpos, tmp, T, vals);
+    W1G_CHECK_LAUNCH();
     return W1G_OK;
 }
 

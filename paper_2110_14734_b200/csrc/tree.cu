@@ -332,11 +332,9 @@ int tree_run(Ctx &c, const double2 *pts, int64_t n, int64_t *n_nodes, int32_t *d
     const unsigned g = grid_for(n, 256, 8u * c.sm_count);
     k_presort_keys<<<g, 256, 0, c.stream>>>(pts, n, kx0, kx1, ky0, ky1, xl[0], yl[0]);
     W1G_CHECK_LAUNCH();
-    {
-        uint64_t *kx[2] = {kx0, kx1}, *ky[2] = {ky0, ky1};
-        W1G_TRY(radix_sort(c, kx, 2, xl[0], n));
-        W1G_TRY(radix_sort(c, ky, 2, yl[0], n));
-    }
+    // X-list by (x, y) and Y-list by (y, x): kx1 = key(x), kx0 = key(y)
+    W1G_TRY(sort_lex2(c, kx1, kx0, xl[0], n));
+    W1G_TRY(sort_lex2(c, kx0, kx1, yl[0], n));
     // level state
     Seg *seg[2];
     SegInfo *info;

@@ -40,11 +40,10 @@ class TransshipmentNetwork:
 
 
 def fetch_network(ctx, n: int, m: int) -> TransshipmentNetwork:
-    sup = np.empty(n, dtype=np.int64)
-    tails = np.empty(m, dtype=np.int64)
-    heads = np.empty(m, dtype=np.int64)
-    costs = np.empty(m, dtype=np.float64)
-    ro = np.empty(n + 1, dtype=np.int64)
+    # result arrays live in pooled page-locked memory: one full-speed D2H each,
+    # no host-side copy (the block returns to the pool when the arrays die)
+    sup, tails, heads, costs, ro = _lib.pinned_arrays(
+        [((n,), np.int64), ((m,), np.int64), ((m,), np.int64), ((m,), np.float64), ((n + 1,), np.int64)])
     ctx.call("w1g_fetch_network", _lib.i64p(sup), _lib.i64p(tails), _lib.i64p(heads), _lib.f64p(costs),
              _lib.i64p(ro))
     return TransshipmentNetwork(n, sup, tails, heads, costs, ro)
