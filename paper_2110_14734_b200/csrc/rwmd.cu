@@ -155,11 +155,14 @@ __device__ __forceinline__ double upper_bound(float est, float qn) {
 }
 
 constexpr int RF_BLOCK = 128;
+constexpr int RF_TPQ = 2;                     // threads per source
+constexpr int RF_QPB = RF_BLOCK / RF_TPQ;     // sources per block
 constexpr int RF_CAND = 2048;
-constexpr int RF_STAGE = 8;  // candidate tiles staged per round (8 x 64 targets, 8 KB)
+constexpr int RF_STAGE = 16;  // candidate tiles staged per round (16 x 64 targets, 16 KB)
 
-// exact fp64 refinement + mass * best (lower_bound.py:51-58); one source per
-// thread, sources in Morton order, target tiles kept by a box test
+// exact fp64 refinement + mass * best (lower_bound.py:51-58).  Two threads per
+// source (each takes every other target of a staged tile, then a shuffle
+// min), sources in Morton order, 64-target Morton tiles kept by a box test
 __global__ void __launch_bounds__(RF_BLOCK) k_refine(const double2 *__restrict__ q, const int32_t *__restrict__ qpos,
                                                      const int32_t *__restrict__ members,
                                                      const int64_t *__restrict__ mass, int64_t nq,
@@ -176,8 +179,8 @@ __global__ void __launch_bounds__(RF_BLOCK) k_refine(const double2 *__restrict__
     __shared__ double4 s_box[RF_BLOCK / 32];
     __shared__ double4 s_qb;
     __shared__ double s_rmax;
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const int64_t i = (int64_t)blockIdx.x * RF_BLOCK + tid;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, sub = tid & (RF_TPQ - 1);
+    const int64_t i = (int64_t)blockIdx.x * RF_QPB + tid / RF_TPQ;
     const bool valid = i < nq;
     double2 p = make_double2(0, 0);
     double diag = 0.0, r = -1.0;
@@ -190,7 +193,7 @@ __global__ void __launch_bounds__(RF_BLOCK) k_refine(const double2 *__restrict__
             r += 0x1p-50 * (fabs(p.x) + fabs(p.y) + r) + 1e-300;
         }
     }
-    double m2 = INFINITY;
+    double m2 = INFINITY, m2b = INFINITY;
     if (nt > 0) {
         // block bbox and radius
         double4 b = valid ? make_double4(p.x, p.y, p.x, p.y) : make_double4(INFINITY, INFINITY, -INFINITY, -INFINITY);
@@ -248,20 +251,26 @@ __global__ void __launch_bounds__(RF_BLOCK) k_refine(const double2 *__restrict__
                 for (int c = 0; c < ns; c++) {
                     const bool need = valid && r >= 0.0 && box_gap(s_tb[c], pb) <= r * (1.0 + 1e-9);
                     if (!__any_sync(0xffffffffu, need)) continue;
-                    const double2 *st = s_t + c * RT;
-#pragma unroll 8
-                    for (int j = 0; j < RT; j++) {
-                        const double2 tt = st[j];
-                        const double dx = dsub(p.x, tt.x), dy = dsub(p.y, tt.y);
-                        const double d2 = dadd(dmul(dx, dx), dmul(dy, dy));
-                        m2 = d2 < m2 ? d2 : m2;
+                    const double2 *st = s_t + c * RT + sub;
+#pragma unroll
+                    for (int j = 0; j < RT / RF_TPQ; j += 2) {
+                        const double2 ta = st[RF_TPQ * j], tb = st[RF_TPQ * (j + 1)];
+                        const double ax = dsub(p.x, ta.x), ay = dsub(p.y, ta.y);
+                        const double bx = dsub(p.x, tb.x), by = dsub(p.y, tb.y);
+                        const double da = dadd(dmul(ax, ax), dmul(ay, ay));
+                        const double db = dadd(dmul(bx, bx), dmul(by, by));
+                        m2 = da < m2 ? da : m2;
+                        m2b = db < m2b ? db : m2b;
                     }
                 }
                 __syncthreads();
             }
         }
     }
-    if (valid) {
+    m2 = m2b < m2 ? m2b : m2;
+    const double other = __shfl_xor_sync(0xffffffffu, m2, 1);
+    m2 = other < m2 ? other : m2;
+    if (valid && sub == 0) {
         double best = diag;
         if (nt > 0) {
             const double nnd = dsqrt(m2);
@@ -385,7 +394,7 @@ int rwmd_run(Ctx &c, double *L, double *LA, double *LB) {
             k_boxes64<<<grid_for((n_dst / RT + 1) * 32, 256, 8u * c.sm_count), 256, 0, c.stream>>>(F.mpts[o], n_dst, box64);
             W1G_CHECK_LAUNCH();
         }
-        k_refine<<<(unsigned)((n_src + RF_BLOCK - 1) / RF_BLOCK), RF_BLOCK, 0, c.stream>>>(
+        k_refine<<<(unsigned)((n_src + RF_QPB - 1) / RF_QPB), RF_BLOCK, 0, c.stream>>>(
             F.mpts[s], F.mpos[s], F.members[s], mass[s], n_src, mf, qn, F.unscale, F.mpts[o], n_dst, box64,
             best, terms);
         W1G_CHECK_LAUNCH();

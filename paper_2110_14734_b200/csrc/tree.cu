@@ -18,7 +18,11 @@
 // Levels run in batches without host synchronisation (kernels of levels past
 // the last one exit at once); the host polls the live-segment count between
 // batches.
+#include <cooperative_groups.h>
+
 #include "common.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace w1g {
 
@@ -129,17 +133,13 @@ __device__ int warp_prefix_count(const double2 *pts, const uint32_t *list, int l
 }
 
 // one warp per segment: bbox, rep, axis, split point, children (spanner.py:124-148)
-__global__ void __launch_bounds__(256) k_tree_segments(const double2 *__restrict__ pts,
-                                                       const uint32_t *__restrict__ xl,
-                                                       const uint32_t *__restrict__ yl,
-                                                       const Seg *__restrict__ seg, const int32_t *cnt_cur,
-                                                       int32_t *cnt_next, Seg *seg_next, SegInfo *info,
-                                                       TreeOut o, int64_t *flags) {
-    const int nseg = *cnt_cur;
-    if (nseg == 0) return;
+__device__ __forceinline__ void tree_segment(int s, const double2 *__restrict__ pts,
+                                             const uint32_t *__restrict__ xl,
+                                             const uint32_t *__restrict__ yl, const Seg *__restrict__ seg,
+                                             int32_t *cnt_next, Seg *seg_next, SegInfo *info,
+                                             const TreeOut &o, int64_t *flags) {
     const int lane = threadIdx.x & 31;
-    const int warps = (gridDim.x * blockDim.x) >> 5;
-    for (int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; s < nseg; s += warps) {
+    {
         const Seg sg = seg[s];
         const int lo = sg.lo, hi = sg.hi, n = hi - lo;
         const uint32_t r0 = xl[lo];
@@ -159,7 +159,7 @@ __global__ void __launch_bounds__(256) k_tree_segments(const double2 *__restrict
                 in.thr = INFINITY;
                 info[s] = in;
             }
-            continue;
+            return;
         }
         const int axis = ext_x >= ext_y ? 0 : 1;
         const uint32_t *al = axis ? yl : xl;
@@ -204,24 +204,58 @@ __global__ void __launch_bounds__(256) k_tree_segments(const double2 *__restrict
     }
 }
 
-// per position: 1 if the OTHER list's element goes to the left child
+__global__ void __launch_bounds__(256) k_tree_segments(const double2 *__restrict__ pts,
+                                                       const uint32_t *__restrict__ xl,
+                                                       const uint32_t *__restrict__ yl,
+                                                       const Seg *__restrict__ seg, const int32_t *cnt_cur,
+                                                       int32_t *cnt_next, Seg *seg_next, SegInfo *info,
+                                                       TreeOut o, int64_t *flags) {
+    const int nseg = *cnt_cur;
+    if (nseg == 0) return;
+    const int warps = (gridDim.x * blockDim.x) >> 5;
+    for (int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; s < nseg; s += warps)
+        tree_segment(s, pts, xl, yl, seg, cnt_next, seg_next, info, o, flags);
+}
+
+// 1 if the OTHER list's element at position p goes to the left child
+__device__ __forceinline__ int pos_flag(int64_t p, const double2 *__restrict__ pts,
+                                        const uint32_t *__restrict__ xl, const uint32_t *__restrict__ yl,
+                                        const int32_t *__restrict__ pos_seg, const SegInfo *__restrict__ info) {
+    const int s = pos_seg[p];
+    if (s < 0) return 0;
+    const SegInfo &in = info[s];
+    const uint32_t e = in.axis ? xl[p] : yl[p];
+    const double c = coord(pts, e, in.axis);
+    return (in.strict ? (c < in.thr) : (c <= in.thr)) ? 1 : 0;
+}
+
 __global__ void k_tree_flags(const double2 *__restrict__ pts, const uint32_t *__restrict__ xl,
                              const uint32_t *__restrict__ yl, const int32_t *__restrict__ pos_seg,
                              const SegInfo *__restrict__ info, const int32_t *cnt_cur, int64_t n,
                              int32_t *fl) {
     if (*cnt_cur == 0) return;
     for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
-         p += (int64_t)gridDim.x * blockDim.x) {
-        const int s = pos_seg[p];
-        int f = 0;
-        if (s >= 0) {
-            const SegInfo &in = info[s];
-            const uint32_t e = in.axis ? xl[p] : yl[p];
-            const double c = coord(pts, e, in.axis);
-            f = (in.strict ? (c < in.thr) : (c <= in.thr)) ? 1 : 0;
-        }
-        fl[p] = f;
+         p += (int64_t)gridDim.x * blockDim.x)
+        fl[p] = pos_flag(p, pts, xl, yl, pos_seg, info);
+}
+
+// stable partition of the other list inside the position's segment
+__device__ __forceinline__ void pos_scatter(int64_t p, int s, int f, int64_t excl_p, int64_t excl_lo,
+                                            const SegInfo &in, const uint32_t *__restrict__ xl,
+                                            const uint32_t *__restrict__ yl, uint32_t *xl_new,
+                                            uint32_t *yl_new, int32_t *pos_seg_new) {
+    const int64_t rt = excl_p - excl_lo;
+    const int64_t rf = (p - in.lo) - rt;
+    const int64_t np_ = f ? in.lo + rt : in.lo + in.nl + rf;
+    if (in.axis) {  // split on y: Y-list stays, X-list is partitioned
+        yl_new[p] = yl[p];
+        xl_new[np_] = xl[p];
+    } else {
+        xl_new[p] = xl[p];
+        yl_new[np_] = yl[p];
     }
+    pos_seg_new[p] = (p < in.lo + in.nl) ? in.cl : in.cr;
+    (void)s;
 }
 
 struct FlagVal {
@@ -258,6 +292,129 @@ __global__ void k_tree_scatter(const uint32_t *__restrict__ xl, const uint32_t *
         }
         pos_seg_new[p] = (p < in.lo + in.nl) ? in.cl : in.cr;
     }
+}
+
+// ---------------------------------------------------------------- persistent cooperative build
+// All levels in ONE cooperative launch: per level (A) one warp per segment,
+// grid sync, (B) flags + tile-local scans, grid sync, (C) tile prefixes
+// (every CTA scans the tile sums in shared memory) + scatter, grid sync.
+// Three grid barriers per level instead of four launches and a host poll.
+
+constexpr int TP_IPT = 8;
+constexpr int TP_TILE = 256 * TP_IPT;
+constexpr int COOP_MAX_TILES = 8192;
+
+struct CoopArgs {
+    const double2 *pts;
+    int64_t n;
+    uint32_t *xl[2], *yl[2];
+    int32_t *pos_seg[2];
+    Seg *seg[2];
+    SegInfo *info;
+    int32_t *cnt;  // ring of 3 live-segment counters
+    int32_t *lpre, *tsum;
+    int32_t *levels_out;
+    int64_t *flags;
+    TreeOut o;
+};
+
+__device__ __forceinline__ int block_excl_scan(int v, int *total, int32_t *s_warp) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_warp[wid] = x;
+    __syncthreads();
+    int off = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < 8; w++) {
+        const int sw = s_warp[w];
+        if (w < wid) off += sw;
+        tot += sw;
+    }
+    __syncthreads();
+    *total = tot;
+    return off + x - v;
+}
+
+__global__ void __launch_bounds__(256) k_tree_coop(CoopArgs A) {
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ int32_t s_tp[];  // exclusive prefix of the tile sums
+    __shared__ int32_t s_warp[8];
+    const int tid = threadIdx.x;
+    const int64_t n = A.n;
+    const int ntiles = (int)((n + TP_TILE - 1) / TP_TILE);
+    int cur = 0, level = 0;
+    while (true) {
+        const int nseg = *((volatile int32_t *)&A.cnt[level % 3]);
+        if (nseg == 0) break;
+        // (A) segments
+        const int warps = (gridDim.x * blockDim.x) >> 5;
+        for (int s = (blockIdx.x * blockDim.x + tid) >> 5; s < nseg; s += warps)
+            tree_segment(s, A.pts, A.xl[cur], A.yl[cur], A.seg[cur], &A.cnt[(level + 1) % 3], A.seg[cur ^ 1],
+                         A.info, A.o, A.flags);
+        grid.sync();
+        // (B) flags and tile-local exclusive prefixes
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            const int64_t base = (int64_t)t * TP_TILE + tid * TP_IPT;
+            int f[TP_IPT];
+            int sum = 0;
+#pragma unroll
+            for (int i = 0; i < TP_IPT; i++) {
+                const int64_t p = base + i;
+                f[i] = p < n ? pos_flag(p, A.pts, A.xl[cur], A.yl[cur], A.pos_seg[cur], A.info) : 0;
+                sum += f[i];
+            }
+            int tot;
+            int run = block_excl_scan(sum, &tot, s_warp);
+#pragma unroll
+            for (int i = 0; i < TP_IPT; i++) {
+                const int64_t p = base + i;
+                if (p < n) A.lpre[p] = run | (f[i] << 31);
+                run += f[i];
+            }
+            if (tid == 0) A.tsum[t] = tot;
+        }
+        grid.sync();
+        // (C) tile prefixes (redundantly per CTA) and the stable partition
+        {
+            int carry = 0;
+            for (int t0 = 0; t0 < ntiles; t0 += 256) {
+                const int t = t0 + tid;
+                const int v = t < ntiles ? A.tsum[t] : 0;
+                int tot;
+                const int ex = block_excl_scan(v, &tot, s_warp);
+                if (t < ntiles) s_tp[t] = carry + ex;
+                carry += tot;
+            }
+            __syncthreads();
+        }
+        if (blockIdx.x == 0 && tid == 0) A.cnt[(level + 2) % 3] = 0;
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            for (int i = tid; i < TP_TILE; i += 256) {
+                const int64_t p = (int64_t)t * TP_TILE + i;
+                if (p >= n) break;
+                const int s = A.pos_seg[cur][p];
+                if (s < 0) {
+                    A.pos_seg[cur ^ 1][p] = -1;
+                    continue;
+                }
+                const SegInfo in = A.info[s];
+                const int32_t lp = A.lpre[p], ll = A.lpre[in.lo];
+                const int64_t ep = (int64_t)s_tp[t] + (lp & 0x7fffffff);
+                const int64_t el = (int64_t)s_tp[in.lo / TP_TILE] + (ll & 0x7fffffff);
+                pos_scatter(p, s, (int)((uint32_t)lp >> 31), ep, el, in, A.xl[cur], A.yl[cur], A.xl[cur ^ 1],
+                            A.yl[cur ^ 1], A.pos_seg[cur ^ 1]);
+            }
+        }
+        grid.sync();
+        cur ^= 1;
+        level++;
+    }
+    if (blockIdx.x == 0 && tid == 0) *A.levels_out = level | (cur << 30);
 }
 
 __global__ void k_geom_from_arrays(const int64_t *left, const int64_t *right, const double4 *bbox,
@@ -356,7 +513,55 @@ int tree_run(Ctx &c, const double2 *pts, int64_t n, int64_t *n_nodes, int32_t *d
     W1G_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * 8, c.stream));
     k_tree_init<<<g, 256, 0, c.stream>>>(n, seg[0], pos_seg[0], cnt, pts, xl[0], o);
     W1G_CHECK_LAUNCH();
-    // one warp per segment
+    const int64_t ntiles = (n + TP_TILE - 1) / TP_TILE;
+    if (ntiles <= COOP_MAX_TILES) {
+        // all levels in one persistent cooperative launch
+        int32_t *lpre, *tsum, *lv;
+        W1G_TRY(ensure(c.scr[17], (size_t)n, &lpre));
+        W1G_TRY(ensure(c.scr[18], (size_t)ntiles + 1, &tsum));
+        W1G_TRY(ensure(c.scr[19], 4, &lv));
+        CoopArgs A;
+        A.pts = pts;
+        A.n = n;
+        A.xl[0] = xl[0];
+        A.xl[1] = xl[1];
+        A.yl[0] = yl[0];
+        A.yl[1] = yl[1];
+        A.pos_seg[0] = pos_seg[0];
+        A.pos_seg[1] = pos_seg[1];
+        A.seg[0] = seg[0];
+        A.seg[1] = seg[1];
+        A.info = info;
+        A.cnt = cnt;
+        A.lpre = lpre;
+        A.tsum = tsum;
+        A.levels_out = lv;
+        A.flags = dflags(c);
+        A.o = o;
+        const size_t smem = sizeof(int32_t) * (size_t)(ntiles + 1);
+        int per_sm = 0;
+        W1G_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tree_coop, 256, smem));
+        if (per_sm < 1) per_sm = 1;
+        if (per_sm > 4) per_sm = 4;
+        const int G = per_sm * c.sm_count;
+        void *args[] = {&A};
+        W1G_CUDA(cudaLaunchCooperativeKernel((void *)k_tree_coop, G, 256, args, smem, c.stream));
+        W1G_CHECK_LAUNCH();
+        W1G_CUDA(cudaMemcpyAsync(c.h_pinned + F_ACTIVE, lv, sizeof(int32_t), cudaMemcpyDeviceToHost, c.stream));
+        W1G_CUDA(cudaMemcpyAsync(c.h_pinned + F_DUP, dflags(c) + F_DUP, sizeof(int64_t), cudaMemcpyDeviceToHost,
+                                 c.stream));
+        W1G_CUDA(cudaStreamSynchronize(c.stream));
+        if (c.h_pinned[F_DUP]) {
+            set_error("split tree input contains duplicate points");
+            return W1G_EDUPLICATE;
+        }
+        const int32_t lvl = *reinterpret_cast<int32_t *>(c.h_pinned + F_ACTIVE) & 0x3fffffff;
+        c.tree_depth = lvl;
+        *depth = lvl;
+        c.tree_valid = true;
+        return W1G_OK;
+    }
+    // fallback for very large inputs: one launch per phase, host polls per batch
     const unsigned gseg = grid_for(seg_cap * 32, 256, 16u * c.sm_count);
     int level = 0, cur = 0;
     const int BATCH = 12;
