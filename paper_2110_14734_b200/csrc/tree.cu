@@ -37,6 +37,10 @@ struct SegInfo {
     int8_t axis, strict, pad0, pad1;
 };
 
+// segments of at most LOCAL_MAX points leave the global level loop and are
+// finished inside one CTA (k_tree_local)
+constexpr int LOCAL_MAX = 2048;
+
 struct TreeOut {
     int64_t *left, *right, *rep, *size;
     double4 *bbox;
@@ -82,18 +86,23 @@ __global__ void k_presort_keys(const double2 *pts, int64_t n, uint64_t *xl0, uin
 }
 
 __global__ void k_tree_init(int64_t n, Seg *seg, int32_t *pos_seg, int32_t *cnt, const double2 *pts,
-                            const uint32_t *xl, TreeOut o) {
+                            const uint32_t *xl, TreeOut o, Seg *local, int32_t *local_cnt) {
+    const bool global_root = n > LOCAL_MAX;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
-        pos_seg[i] = n == 1 ? -1 : 0;
+        pos_seg[i] = global_root ? 0 : -1;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
+        cnt[0] = 0;
+        *local_cnt = 0;
         if (n == 1) {
             const double2 p = pts[xl[0]];
             write_node(o, 0, p.x, p.y, p.x, p.y, xl[0], 1, -1, -1);
-            cnt[0] = 0;
-        } else {
+        } else if (global_root) {
             seg[0] = Seg{0, (int32_t)n, 0, 0};
             cnt[0] = 1;
+        } else {
+            local[0] = Seg{0, (int32_t)n, 0, 0};  // the whole tree fits one CTA
+            *local_cnt = 1;
         }
     }
 }
@@ -137,7 +146,8 @@ __device__ __forceinline__ void tree_segment(int s, const double2 *__restrict__ 
                                              const uint32_t *__restrict__ xl,
                                              const uint32_t *__restrict__ yl, const Seg *__restrict__ seg,
                                              int32_t *cnt_next, Seg *seg_next, SegInfo *info,
-                                             const TreeOut &o, int64_t *flags) {
+                                             const TreeOut &o, int64_t *flags, Seg *local,
+                                             int32_t *local_cnt, int parity_next) {
     const int lane = threadIdx.x & 31;
     {
         const Seg sg = seg[s];
@@ -181,23 +191,29 @@ __device__ __forceinline__ void tree_segment(int s, const double2 *__restrict__ 
             in.strict = (int8_t)strict;
             in.thr = thr;
             const int nr = n - nl;
-            const int want = (nl > 1) + (nr > 1);
+            // children larger than LOCAL_MAX stay in the global level loop; smaller
+            // internal children are finished later by one CTA each (k_tree_local)
+            const int want = (nl > LOCAL_MAX) + (nr > LOCAL_MAX);
             int slot = want ? atomicAdd(cnt_next, want) : 0;
             if (nl == 1) {
                 const uint32_t pi = al[lo];
                 const double2 p = pts[pi];
                 write_node(o, lid, p.x, p.y, p.x, p.y, pi, 1, -1, -1);
-            } else {
+            } else if (nl > LOCAL_MAX) {
                 in.cl = slot++;
                 seg_next[in.cl] = Seg{lo, lo + nl, (int32_t)lid, 0};
+            } else {
+                local[atomicAdd(local_cnt, 1)] = Seg{lo, lo + nl, (int32_t)lid, parity_next};
             }
             if (nr == 1) {
                 const uint32_t pi = al[lo + nl];
                 const double2 p = pts[pi];
                 write_node(o, rid, p.x, p.y, p.x, p.y, pi, 1, -1, -1);
-            } else {
+            } else if (nr > LOCAL_MAX) {
                 in.cr = slot;
                 seg_next[in.cr] = Seg{lo + nl, hi, (int32_t)rid, 0};
+            } else {
+                local[atomicAdd(local_cnt, 1)] = Seg{lo + nl, hi, (int32_t)rid, parity_next};
             }
             info[s] = in;
         }
@@ -209,12 +225,199 @@ __global__ void __launch_bounds__(256) k_tree_segments(const double2 *__restrict
                                                        const uint32_t *__restrict__ yl,
                                                        const Seg *__restrict__ seg, const int32_t *cnt_cur,
                                                        int32_t *cnt_next, Seg *seg_next, SegInfo *info,
-                                                       TreeOut o, int64_t *flags) {
+                                                       TreeOut o, int64_t *flags, Seg *local,
+                                                       int32_t *local_cnt, int parity_next) {
     const int nseg = *cnt_cur;
     if (nseg == 0) return;
     const int warps = (gridDim.x * blockDim.x) >> 5;
     for (int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; s < nseg; s += warps)
-        tree_segment(s, pts, xl, yl, seg, cnt_next, seg_next, info, o, flags);
+        tree_segment(s, pts, xl, yl, seg, cnt_next, seg_next, info, o, flags, local, local_cnt, parity_next);
+}
+
+// ---------------------------------------------------------------- local subtrees
+// A segment of at most LOCAL_MAX points is finished by ONE CTA: its two
+// lists are staged in shared memory and the same level-synchronous split
+// (segments -> flags -> block scan -> stable partition) runs with CTA
+// barriers instead of grid-wide ones.
+
+struct LocalSub {
+    int16_t lo, hi;
+    int32_t nid;
+};
+struct LocalInfo {
+    double thr;
+    int16_t lo, nl, cl, cr;
+    int8_t axis, strict, pad0, pad1;
+};
+
+struct LocalSmem {
+    uint32_t xl[2][LOCAL_MAX];
+    uint32_t yl[2][LOCAL_MAX];
+    int16_t ps[2][LOCAL_MAX];
+    int16_t ex[LOCAL_MAX];
+    LocalSub sub[2][LOCAL_MAX / 2 + 1];
+    LocalInfo info[LOCAL_MAX / 2 + 1];
+    int32_t warp_tot[8];
+    int32_t nsub_next;
+};
+
+__global__ void __launch_bounds__(256) k_tree_local(const double2 *__restrict__ pts, const uint32_t *xl0,
+                                                    const uint32_t *xl1, const uint32_t *yl0,
+                                                    const uint32_t *yl1, const Seg *__restrict__ local,
+                                                    const int32_t *local_cnt, TreeOut o, int64_t *flags) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    LocalSmem &S = *reinterpret_cast<LocalSmem *>(smem_raw);
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int nloc = *local_cnt;
+    for (int ls = blockIdx.x; ls < nloc; ls += gridDim.x) {
+        const Seg L = local[ls];
+        const int m = L.hi - L.lo;
+        const uint32_t *gx = L.pad ? xl1 : xl0, *gy = L.pad ? yl1 : yl0;
+        for (int i = tid; i < m; i += 256) {
+            S.xl[0][i] = gx[L.lo + i];
+            S.yl[0][i] = gy[L.lo + i];
+            S.ps[0][i] = 0;
+        }
+        if (tid == 0) {
+            S.sub[0][0] = LocalSub{0, (int16_t)m, L.nid};
+            S.nsub_next = 0;
+        }
+        __syncthreads();
+        int cur = 0, nsub = 1;
+        while (nsub > 0) {
+            // (A) one warp per sub-segment
+            for (int s = wid; s < nsub; s += 8) {
+                const LocalSub sg = S.sub[cur][s];
+                const int lo = sg.lo, hi = sg.hi, n = hi - lo;
+                const uint32_t *xl = S.xl[cur], *yl = S.yl[cur];
+                const uint32_t r0 = xl[lo];
+                const double xmin = pts[r0].x, xmax = pts[xl[hi - 1]].x;
+                const double ymin = pts[yl[lo]].y, ymax = pts[yl[hi - 1]].y;
+                const double ext_x = dsub(xmax, xmin), ext_y = dsub(ymax, ymin);
+                LocalInfo in{};
+                in.lo = (int16_t)lo;
+                in.cl = in.cr = -1;
+                if (ext_x == 0.0 && ext_y == 0.0) {
+                    if (lane == 0) {
+                        atomicOr((unsigned long long *)&flags[F_DUP], 1ull);
+                        write_node(o, sg.nid, xmin, ymin, xmax, ymax, r0, n, -1, -1);
+                        in.nl = (int16_t)n;
+                        in.thr = INFINITY;
+                        S.info[s] = in;
+                    }
+                    continue;
+                }
+                const int axis = ext_x >= ext_y ? 0 : 1;
+                const uint32_t *al = axis ? yl : xl;
+                const double amin = axis ? ymin : xmin, amax = axis ? ymax : xmax;
+                const double mid = dmul(0.5, dadd(amin, amax));
+                int nl = warp_prefix_count(pts, al, lo, hi, axis, mid, 0);
+                int strict = 0;
+                double thr = mid;
+                if (nl == 0 || nl == n) {
+                    strict = 1;
+                    thr = amax;
+                    nl = warp_prefix_count(pts, al, lo, hi, axis, amax, 1);
+                }
+                if (lane == 0) {
+                    const int64_t lid = (int64_t)sg.nid + 1, rid = (int64_t)sg.nid + 2 * (int64_t)nl;
+                    write_node(o, sg.nid, xmin, ymin, xmax, ymax, r0, n, lid, rid);
+                    in.nl = (int16_t)nl;
+                    in.axis = (int8_t)axis;
+                    in.strict = (int8_t)strict;
+                    in.thr = thr;
+                    const int nr = n - nl;
+                    const int want = (nl > 1) + (nr > 1);
+                    int slot = want ? atomicAdd(&S.nsub_next, want) : 0;
+                    if (nl == 1) {
+                        const uint32_t pi = al[lo];
+                        const double2 p = pts[pi];
+                        write_node(o, lid, p.x, p.y, p.x, p.y, pi, 1, -1, -1);
+                    } else {
+                        in.cl = (int16_t)slot;
+                        S.sub[cur ^ 1][slot++] = LocalSub{(int16_t)lo, (int16_t)(lo + nl), (int32_t)lid};
+                    }
+                    if (nr == 1) {
+                        const uint32_t pi = al[lo + nl];
+                        const double2 p = pts[pi];
+                        write_node(o, rid, p.x, p.y, p.x, p.y, pi, 1, -1, -1);
+                    } else {
+                        in.cr = (int16_t)slot;
+                        S.sub[cur ^ 1][slot] = LocalSub{(int16_t)(lo + nl), (int16_t)hi, (int32_t)rid};
+                    }
+                    S.info[s] = in;
+                }
+            }
+            __syncthreads();
+            // (B) flags of the other list + block exclusive scan (8 positions per thread)
+            int f[8], sum = 0;
+#pragma unroll
+            for (int i = 0; i < 8; i++) {
+                const int p = tid * 8 + i;
+                int v = 0;
+                if (p < m) {
+                    const int s = S.ps[cur][p];
+                    if (s >= 0) {
+                        const LocalInfo &in = S.info[s];
+                        const uint32_t e = in.axis ? S.xl[cur][p] : S.yl[cur][p];
+                        const double c = coord(pts, e, in.axis);
+                        v = (in.strict ? (c < in.thr) : (c <= in.thr)) ? 1 : 0;
+                    }
+                }
+                f[i] = v;
+                sum += v;
+            }
+            {
+                int x = sum;
+#pragma unroll
+                for (int off = 1; off < 32; off <<= 1) {
+                    const int y = __shfl_up_sync(0xffffffffu, x, off);
+                    if (lane >= off) x += y;
+                }
+                if (lane == 31) S.warp_tot[wid] = x;
+                __syncthreads();
+                int base = 0;
+                for (int w = 0; w < wid; w++) base += S.warp_tot[w];
+                int run = base + x - sum;
+#pragma unroll
+                for (int i = 0; i < 8; i++) {
+                    const int p = tid * 8 + i;
+                    if (p < m) S.ex[p] = (int16_t)run;
+                    run += f[i];
+                }
+            }
+            __syncthreads();
+            // (C) stable partition of the other list inside each sub-segment
+#pragma unroll
+            for (int i = 0; i < 8; i++) {
+                const int p = tid * 8 + i;
+                if (p >= m) continue;
+                const int s = S.ps[cur][p];
+                if (s < 0) {
+                    S.ps[cur ^ 1][p] = -1;
+                    continue;
+                }
+                const LocalInfo in = S.info[s];
+                const int rt = S.ex[p] - S.ex[in.lo];
+                const int rf = (p - in.lo) - rt;
+                const int np_ = f[i] ? in.lo + rt : in.lo + in.nl + rf;
+                if (in.axis) {
+                    S.yl[cur ^ 1][p] = S.yl[cur][p];
+                    S.xl[cur ^ 1][np_] = S.xl[cur][p];
+                } else {
+                    S.xl[cur ^ 1][p] = S.xl[cur][p];
+                    S.yl[cur ^ 1][np_] = S.yl[cur][p];
+                }
+                S.ps[cur ^ 1][p] = (p < in.lo + in.nl) ? in.cl : in.cr;
+            }
+            __syncthreads();
+            nsub = S.nsub_next;
+            __syncthreads();
+            if (tid == 0) S.nsub_next = 0;
+            cur ^= 1;
+        }
+        __syncthreads();
+    }
 }
 
 // 1 if the OTHER list's element at position p goes to the left child
@@ -315,6 +518,8 @@ struct CoopArgs {
     int32_t *lpre, *tsum;
     int32_t *levels_out;
     int64_t *flags;
+    Seg *local;
+    int32_t *local_cnt;
     TreeOut o;
 };
 
@@ -355,7 +560,7 @@ __global__ void __launch_bounds__(256) k_tree_coop(CoopArgs A) {
         const int warps = (gridDim.x * blockDim.x) >> 5;
         for (int s = (blockIdx.x * blockDim.x + tid) >> 5; s < nseg; s += warps)
             tree_segment(s, A.pts, A.xl[cur], A.yl[cur], A.seg[cur], &A.cnt[(level + 1) % 3], A.seg[cur ^ 1],
-                         A.info, A.o, A.flags);
+                         A.info, A.o, A.flags, A.local, A.local_cnt, cur ^ 1);
         grid.sync();
         // (B) flags and tile-local exclusive prefixes
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
@@ -508,14 +713,19 @@ int tree_run(Ctx &c, const double2 *pts, int64_t n, int64_t *n_nodes, int32_t *d
     const int max_levels = (int)(n + 2);
     // live-segment counters, a ring of 3: level l reads cnt[l%3], appends to
     // cnt[(l+1)%3]; its scatter kernel clears cnt[(l+2)%3]
-    W1G_TRY(ensure(c.scr[15], 8, &cnt));
+    Seg *local;
+    int32_t *local_cnt;
+    W1G_TRY(ensure(c.scr[15], 16, &cnt));
+    local_cnt = cnt + 8;
+    W1G_TRY(ensure(c.scr[20], (size_t)seg_cap + 2, &local));
     W1G_TRY(flags_reset(c));
-    W1G_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * 8, c.stream));
-    k_tree_init<<<g, 256, 0, c.stream>>>(n, seg[0], pos_seg[0], cnt, pts, xl[0], o);
+    W1G_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * 16, c.stream));
+    k_tree_init<<<g, 256, 0, c.stream>>>(n, seg[0], pos_seg[0], cnt, pts, xl[0], o, local, local_cnt);
     W1G_CHECK_LAUNCH();
+    int levels = 0;
     const int64_t ntiles = (n + TP_TILE - 1) / TP_TILE;
-    if (ntiles <= COOP_MAX_TILES) {
-        // all levels in one persistent cooperative launch
+    if (n > LOCAL_MAX && ntiles <= COOP_MAX_TILES) {
+        // the global levels (segments > LOCAL_MAX) in one persistent cooperative launch
         int32_t *lpre, *tsum, *lv;
         W1G_TRY(ensure(c.scr[17], (size_t)n, &lpre));
         W1G_TRY(ensure(c.scr[18], (size_t)ntiles + 1, &tsum));
@@ -537,62 +747,67 @@ int tree_run(Ctx &c, const double2 *pts, int64_t n, int64_t *n_nodes, int32_t *d
         A.tsum = tsum;
         A.levels_out = lv;
         A.flags = dflags(c);
+        A.local = local;
+        A.local_cnt = local_cnt;
         A.o = o;
         const size_t smem = sizeof(int32_t) * (size_t)(ntiles + 1);
         int per_sm = 0;
         W1G_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tree_coop, 256, smem));
         if (per_sm < 1) per_sm = 1;
-        if (per_sm > 4) per_sm = 4;
+        if (per_sm > 2) per_sm = 2;
         const int G = per_sm * c.sm_count;
         void *args[] = {&A};
         W1G_CUDA(cudaLaunchCooperativeKernel((void *)k_tree_coop, G, 256, args, smem, c.stream));
         W1G_CHECK_LAUNCH();
         W1G_CUDA(cudaMemcpyAsync(c.h_pinned + F_ACTIVE, lv, sizeof(int32_t), cudaMemcpyDeviceToHost, c.stream));
-        W1G_CUDA(cudaMemcpyAsync(c.h_pinned + F_DUP, dflags(c) + F_DUP, sizeof(int64_t), cudaMemcpyDeviceToHost,
-                                 c.stream));
         W1G_CUDA(cudaStreamSynchronize(c.stream));
-        if (c.h_pinned[F_DUP]) {
-            set_error("split tree input contains duplicate points");
-            return W1G_EDUPLICATE;
+        levels = *reinterpret_cast<int32_t *>(c.h_pinned + F_ACTIVE) & 0x3fffffff;
+    } else if (n > LOCAL_MAX) {
+        // fallback for very large inputs: one launch per phase, host polls per batch
+        const unsigned gseg = grid_for(seg_cap * 32, 256, 16u * c.sm_count);
+        int level = 0, cur = 0;
+        const int BATCH = 12;
+        while (true) {
+            for (int b = 0; b < BATCH; b++, level++) {
+                const int32_t *cc = cnt + level % 3;
+                k_tree_segments<<<gseg, 256, 0, c.stream>>>(pts, xl[cur], yl[cur], seg[cur], cc,
+                                                           cnt + (level + 1) % 3, seg[cur ^ 1], info, o, dflags(c),
+                                                           local, local_cnt, cur ^ 1);
+                W1G_CHECK_LAUNCH();
+                k_tree_flags<<<g, 256, 0, c.stream>>>(pts, xl[cur], yl[cur], pos_seg[cur], info, cc, n, fl);
+                W1G_CHECK_LAUNCH();
+                W1G_TRY(scan_i64(c, FlagVal{fl}, n, excl, nullptr, cc));
+                k_tree_scatter<<<g, 256, 0, c.stream>>>(xl[cur], yl[cur], pos_seg[cur], info, fl, excl, cc, n,
+                                                       xl[cur ^ 1], yl[cur ^ 1], pos_seg[cur ^ 1],
+                                                       cnt + (level + 2) % 3);
+                W1G_CHECK_LAUNCH();
+                cur ^= 1;
+            }
+            W1G_CUDA(cudaMemcpyAsync(c.h_pinned + F_ACTIVE, cnt + level % 3, sizeof(int32_t),
+                                     cudaMemcpyDeviceToHost, c.stream));
+            W1G_CUDA(cudaStreamSynchronize(c.stream));
+            const int32_t live = *reinterpret_cast<int32_t *>(c.h_pinned + F_ACTIVE);
+            if (live == 0 || level > max_levels) break;
         }
-        const int32_t lvl = *reinterpret_cast<int32_t *>(c.h_pinned + F_ACTIVE) & 0x3fffffff;
-        c.tree_depth = lvl;
-        *depth = lvl;
-        c.tree_valid = true;
-        return W1G_OK;
+        levels = level;
     }
-    // fallback for very large inputs: one launch per phase, host polls per batch
-    const unsigned gseg = grid_for(seg_cap * 32, 256, 16u * c.sm_count);
-    int level = 0, cur = 0;
-    const int BATCH = 12;
-    while (true) {
-        for (int b = 0; b < BATCH; b++, level++) {
-            const int32_t *cc = cnt + level % 3;
-            k_tree_segments<<<gseg, 256, 0, c.stream>>>(pts, xl[cur], yl[cur], seg[cur], cc, cnt + (level + 1) % 3,
-                                                       seg[cur ^ 1], info, o, dflags(c));
-            W1G_CHECK_LAUNCH();
-            k_tree_flags<<<g, 256, 0, c.stream>>>(pts, xl[cur], yl[cur], pos_seg[cur], info, cc, n, fl);
-            W1G_CHECK_LAUNCH();
-            W1G_TRY(scan_i64(c, FlagVal{fl}, n, excl, nullptr, cc));
-            k_tree_scatter<<<g, 256, 0, c.stream>>>(xl[cur], yl[cur], pos_seg[cur], info, fl, excl, cc, n,
-                                                   xl[cur ^ 1], yl[cur ^ 1], pos_seg[cur ^ 1], cnt + (level + 2) % 3);
-            W1G_CHECK_LAUNCH();
-            cur ^= 1;
-        }
-        W1G_CUDA(cudaMemcpyAsync(c.h_pinned + F_ACTIVE, cnt + level % 3, sizeof(int32_t),
-                                 cudaMemcpyDeviceToHost, c.stream));
-        W1G_CUDA(cudaMemcpyAsync(c.h_pinned + F_DUP, dflags(c) + F_DUP, sizeof(int64_t),
-                                 cudaMemcpyDeviceToHost, c.stream));
-        W1G_CUDA(cudaStreamSynchronize(c.stream));
-        const int32_t live = *reinterpret_cast<int32_t *>(c.h_pinned + F_ACTIVE);
-        if (c.h_pinned[F_DUP]) {
-            set_error("split tree input contains duplicate points");
-            return W1G_EDUPLICATE;
-        }
-        if (live == 0 || level > max_levels) break;
+    // the subtrees of <= LOCAL_MAX points: one CTA each, shared-memory levels
+    {
+        const size_t smem = sizeof(LocalSmem);
+        W1G_CUDA(cudaFuncSetAttribute(k_tree_local, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        const unsigned gl = (unsigned)(2 * c.sm_count);
+        k_tree_local<<<gl, 256, smem, c.stream>>>(pts, xl[0], xl[1], yl[0], yl[1], local, local_cnt, o, dflags(c));
+        W1G_CHECK_LAUNCH();
     }
-    c.tree_depth = level;
-    *depth = level;
+    W1G_CUDA(cudaMemcpyAsync(c.h_pinned + F_DUP, dflags(c) + F_DUP, sizeof(int64_t), cudaMemcpyDeviceToHost,
+                             c.stream));
+    W1G_CUDA(cudaStreamSynchronize(c.stream));
+    if (c.h_pinned[F_DUP]) {
+        set_error("split tree input contains duplicate points");
+        return W1G_EDUPLICATE;
+    }
+    c.tree_depth = levels;
+    *depth = levels;
     c.tree_valid = true;
     return W1G_OK;
 }
