@@ -251,20 +251,133 @@ struct LocalInfo {
 };
 
 struct LocalSmem {
-    uint32_t xl[2][LOCAL_MAX];
-    uint32_t yl[2][LOCAL_MAX];
+    double px[LOCAL_MAX], py[LOCAL_MAX];  // coordinates by local id (local id = X-list rank)
+    uint32_t gid[LOCAL_MAX];              // local id -> point index
+    uint16_t xl[2][LOCAL_MAX];            // local ids in X-list / Y-list order
+    uint16_t yl[2][LOCAL_MAX];
     int16_t ps[2][LOCAL_MAX];
     int16_t ex[LOCAL_MAX];
     LocalSub sub[2][LOCAL_MAX / 2 + 1];
     LocalInfo info[LOCAL_MAX / 2 + 1];
+    int16_t big[LOCAL_MAX / 2 + 1];
     int32_t warp_tot[8];
-    int32_t nsub_next;
+    int32_t nsub_next, nbig;
 };
+
+__device__ __forceinline__ double lcoord(const LocalSmem &S, int id, int axis) {
+    return axis ? S.py[id] : S.px[id];
+}
+
+// warp-cooperative prefix count on a shared-memory list (see warp_prefix_count)
+__device__ int local_prefix_count(const LocalSmem &S, const uint16_t *list, int lo, int hi, int axis, double t,
+                                  int strict) {
+    const int lane = threadIdx.x & 31;
+    int a = lo, b = hi;
+    while (b - a > 32) {
+        const int step = (b - a + 31) >> 5;
+        const int p = a + lane * step;
+        bool ok = false;
+        if (p < b) {
+            const double c = lcoord(S, list[p], axis);
+            ok = strict ? (c < t) : (c <= t);
+        }
+        const int k = __popc(__ballot_sync(0xffffffffu, ok));
+        const int na = k ? a + (k - 1) * step + 1 : a;
+        const int nb = k < 32 ? min(b, a + k * step) : b;
+        a = na;
+        b = nb;
+    }
+    const int p = a + lane;
+    bool ok = false;
+    if (p < b) {
+        const double c = lcoord(S, list[p], axis);
+        ok = strict ? (c < t) : (c <= t);
+    }
+    return a + __popc(__ballot_sync(0xffffffffu, ok)) - lo;
+}
+
+// scalar prefix count on a shared-memory list (one thread per small sub-segment)
+__device__ __forceinline__ int scalar_prefix_count(const LocalSmem &S, const uint16_t *list, int lo, int hi,
+                                                   int axis, double t, int strict) {
+    int a = lo, b = hi;
+    while (a < b) {
+        const int mm = (a + b) >> 1;
+        const double c = lcoord(S, list[mm], axis);
+        if (strict ? (c < t) : (c <= t)) a = mm + 1; else b = mm;
+    }
+    return a - lo;
+}
+
+// split one sub-segment (spanner.py:124-148); WARP = true: the calling warp
+// cooperates on the search and lane 0 writes, false: the calling thread alone
+template <bool WARP>
+__device__ __forceinline__ void local_split(LocalSmem &S, int s, int cur, const TreeOut &o, int64_t *flags) {
+    const int lane = threadIdx.x & 31;
+    const bool writer = WARP ? lane == 0 : true;
+    const LocalSub sg = S.sub[cur][s];
+    const int lo = sg.lo, hi = sg.hi, n = hi - lo;
+    const uint16_t *xl = S.xl[cur], *yl = S.yl[cur];
+    const int r0 = xl[lo];
+    const double xmin = S.px[r0], xmax = S.px[xl[hi - 1]];
+    const double ymin = S.py[yl[lo]], ymax = S.py[yl[hi - 1]];
+    const double ext_x = dsub(xmax, xmin), ext_y = dsub(ymax, ymin);
+    LocalInfo in{};
+    in.lo = (int16_t)lo;
+    in.cl = in.cr = -1;
+    if (ext_x == 0.0 && ext_y == 0.0) {
+        if (writer) {
+            atomicOr((unsigned long long *)&flags[F_DUP], 1ull);
+            write_node(o, sg.nid, xmin, ymin, xmax, ymax, S.gid[r0], n, -1, -1);
+            in.nl = (int16_t)n;
+            in.thr = INFINITY;
+            S.info[s] = in;
+        }
+        return;
+    }
+    const int axis = ext_x >= ext_y ? 0 : 1;
+    const uint16_t *al = axis ? yl : xl;
+    const double amin = axis ? ymin : xmin, amax = axis ? ymax : xmax;
+    const double mid = dmul(0.5, dadd(amin, amax));
+    int nl = WARP ? local_prefix_count(S, al, lo, hi, axis, mid, 0) : scalar_prefix_count(S, al, lo, hi, axis, mid, 0);
+    int strict = 0;
+    double thr = mid;
+    if (nl == 0 || nl == n) {
+        strict = 1;
+        thr = amax;
+        nl = WARP ? local_prefix_count(S, al, lo, hi, axis, amax, 1) : scalar_prefix_count(S, al, lo, hi, axis, amax, 1);
+    }
+    if (!writer) return;
+    const int64_t lid = (int64_t)sg.nid + 1, rid = (int64_t)sg.nid + 2 * (int64_t)nl;
+    write_node(o, sg.nid, xmin, ymin, xmax, ymax, S.gid[r0], n, lid, rid);
+    in.nl = (int16_t)nl;
+    in.axis = (int8_t)axis;
+    in.strict = (int8_t)strict;
+    in.thr = thr;
+    const int nr = n - nl;
+    const int want = (nl > 1) + (nr > 1);
+    int slot = want ? atomicAdd(&S.nsub_next, want) : 0;
+    if (nl == 1) {
+        const int li = al[lo];
+        write_node(o, lid, S.px[li], S.py[li], S.px[li], S.py[li], S.gid[li], 1, -1, -1);
+    } else {
+        in.cl = (int16_t)slot;
+        S.sub[cur ^ 1][slot++] = LocalSub{(int16_t)lo, (int16_t)(lo + nl), (int32_t)lid};
+    }
+    if (nr == 1) {
+        const int li = al[lo + nl];
+        write_node(o, rid, S.px[li], S.py[li], S.px[li], S.py[li], S.gid[li], 1, -1, -1);
+    } else {
+        in.cr = (int16_t)slot;
+        S.sub[cur ^ 1][slot] = LocalSub{(int16_t)(lo + nl), (int16_t)hi, (int32_t)rid};
+    }
+    S.info[s] = in;
+}
 
 __global__ void __launch_bounds__(256) k_tree_local(const double2 *__restrict__ pts, const uint32_t *xl0,
                                                     const uint32_t *xl1, const uint32_t *yl0,
                                                     const uint32_t *yl1, const Seg *__restrict__ local,
-                                                    const int32_t *local_cnt, TreeOut o, int64_t *flags) {
+                                                    const int32_t *local_cnt, int32_t *inv, TreeOut o,
+                                                    int64_t *flags) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     LocalSmem &S = *reinterpret_cast<LocalSmem *>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -273,81 +386,36 @@ __global__ void __launch_bounds__(256) k_tree_local(const double2 *__restrict__ 
         const Seg L = local[ls];
         const int m = L.hi - L.lo;
         const uint32_t *gx = L.pad ? xl1 : xl0, *gy = L.pad ? yl1 : yl0;
+        // stage the segment: local id = rank in the X-list
         for (int i = tid; i < m; i += 256) {
-            S.xl[0][i] = gx[L.lo + i];
-            S.yl[0][i] = gy[L.lo + i];
+            const uint32_t g = gx[L.lo + i];
+            const double2 p = pts[g];
+            S.px[i] = p.x;
+            S.py[i] = p.y;
+            S.gid[i] = g;
+            S.xl[0][i] = (uint16_t)i;
             S.ps[0][i] = 0;
+            inv[g] = i;
         }
+        __syncthreads();
+        for (int i = tid; i < m; i += 256) S.yl[0][i] = (uint16_t)inv[gy[L.lo + i]];
         if (tid == 0) {
             S.sub[0][0] = LocalSub{0, (int16_t)m, L.nid};
             S.nsub_next = 0;
+            S.nbig = 0;
         }
         __syncthreads();
         int cur = 0, nsub = 1;
         while (nsub > 0) {
-            // (A) one warp per sub-segment
-            for (int s = wid; s < nsub; s += 8) {
-                const LocalSub sg = S.sub[cur][s];
-                const int lo = sg.lo, hi = sg.hi, n = hi - lo;
-                const uint32_t *xl = S.xl[cur], *yl = S.yl[cur];
-                const uint32_t r0 = xl[lo];
-                const double xmin = pts[r0].x, xmax = pts[xl[hi - 1]].x;
-                const double ymin = pts[yl[lo]].y, ymax = pts[yl[hi - 1]].y;
-                const double ext_x = dsub(xmax, xmin), ext_y = dsub(ymax, ymin);
-                LocalInfo in{};
-                in.lo = (int16_t)lo;
-                in.cl = in.cr = -1;
-                if (ext_x == 0.0 && ext_y == 0.0) {
-                    if (lane == 0) {
-                        atomicOr((unsigned long long *)&flags[F_DUP], 1ull);
-                        write_node(o, sg.nid, xmin, ymin, xmax, ymax, r0, n, -1, -1);
-                        in.nl = (int16_t)n;
-                        in.thr = INFINITY;
-                        S.info[s] = in;
-                    }
-                    continue;
-                }
-                const int axis = ext_x >= ext_y ? 0 : 1;
-                const uint32_t *al = axis ? yl : xl;
-                const double amin = axis ? ymin : xmin, amax = axis ? ymax : xmax;
-                const double mid = dmul(0.5, dadd(amin, amax));
-                int nl = warp_prefix_count(pts, al, lo, hi, axis, mid, 0);
-                int strict = 0;
-                double thr = mid;
-                if (nl == 0 || nl == n) {
-                    strict = 1;
-                    thr = amax;
-                    nl = warp_prefix_count(pts, al, lo, hi, axis, amax, 1);
-                }
-                if (lane == 0) {
-                    const int64_t lid = (int64_t)sg.nid + 1, rid = (int64_t)sg.nid + 2 * (int64_t)nl;
-                    write_node(o, sg.nid, xmin, ymin, xmax, ymax, r0, n, lid, rid);
-                    in.nl = (int16_t)nl;
-                    in.axis = (int8_t)axis;
-                    in.strict = (int8_t)strict;
-                    in.thr = thr;
-                    const int nr = n - nl;
-                    const int want = (nl > 1) + (nr > 1);
-                    int slot = want ? atomicAdd(&S.nsub_next, want) : 0;
-                    if (nl == 1) {
-                        const uint32_t pi = al[lo];
-                        const double2 p = pts[pi];
-                        write_node(o, lid, p.x, p.y, p.x, p.y, pi, 1, -1, -1);
-                    } else {
-                        in.cl = (int16_t)slot;
-                        S.sub[cur ^ 1][slot++] = LocalSub{(int16_t)lo, (int16_t)(lo + nl), (int32_t)lid};
-                    }
-                    if (nr == 1) {
-                        const uint32_t pi = al[lo + nl];
-                        const double2 p = pts[pi];
-                        write_node(o, rid, p.x, p.y, p.x, p.y, pi, 1, -1, -1);
-                    } else {
-                        in.cr = (int16_t)slot;
-                        S.sub[cur ^ 1][slot] = LocalSub{(int16_t)(lo + nl), (int16_t)hi, (int32_t)rid};
-                    }
-                    S.info[s] = in;
-                }
+            // (A) small sub-segments: one thread each; large ones: one warp each
+            for (int s = tid; s < nsub; s += 256) {
+                if (S.sub[cur][s].hi - S.sub[cur][s].lo > 64)
+                    S.big[atomicAdd(&S.nbig, 1)] = (int16_t)s;
+                else
+                    local_split<false>(S, s, cur, o, flags);
             }
+            __syncthreads();
+            for (int k = wid; k < S.nbig; k += 8) local_split<true>(S, S.big[k], cur, o, flags);
             __syncthreads();
             // (B) flags of the other list + block exclusive scan (8 positions per thread)
             int f[8], sum = 0;
@@ -359,8 +427,8 @@ __global__ void __launch_bounds__(256) k_tree_local(const double2 *__restrict__ 
                     const int s = S.ps[cur][p];
                     if (s >= 0) {
                         const LocalInfo &in = S.info[s];
-                        const uint32_t e = in.axis ? S.xl[cur][p] : S.yl[cur][p];
-                        const double c = coord(pts, e, in.axis);
+                        const int e = in.axis ? S.xl[cur][p] : S.yl[cur][p];
+                        const double c = lcoord(S, e, in.axis);
                         v = (in.strict ? (c < in.thr) : (c <= in.thr)) ? 1 : 0;
                     }
                 }
@@ -413,7 +481,11 @@ __global__ void __launch_bounds__(256) k_tree_local(const double2 *__restrict__ 
             __syncthreads();
             nsub = S.nsub_next;
             __syncthreads();
-            if (tid == 0) S.nsub_next = 0;
+            if (tid == 0) {
+                S.nsub_next = 0;
+                S.nbig = 0;
+            }
+            __syncthreads();  // the resets must land before the next level's atomics
             cur ^= 1;
         }
         __syncthreads();
@@ -796,7 +868,8 @@ int tree_run(Ctx &c, const double2 *pts, int64_t n, int64_t *n_nodes, int32_t *d
         const size_t smem = sizeof(LocalSmem);
         W1G_CUDA(cudaFuncSetAttribute(k_tree_local, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         const unsigned gl = (unsigned)(2 * c.sm_count);
-        k_tree_local<<<gl, 256, smem, c.stream>>>(pts, xl[0], xl[1], yl[0], yl[1], local, local_cnt, o, dflags(c));
+        k_tree_local<<<gl, 256, smem, c.stream>>>(pts, xl[0], xl[1], yl[0], yl[1], local, local_cnt, fl, o,
+                                                  dflags(c));
         W1G_CHECK_LAUNCH();
     }
     W1G_CUDA(cudaMemcpyAsync(c.h_pinned + F_DUP, dflags(c) + F_DUP, sizeof(int64_t), cudaMemcpyDeviceToHost,
