@@ -102,6 +102,12 @@ int w1g_fetch_nodes(w1g_ctx *ctx, int slot, double *points, int64_t *a_mass, int
 int w1g_rwmd(w1g_ctx *ctx, double *L, double *LA, double *LB);
 /* per-source best distance min(nn, diag) for one side (0 = A, 1 = B), node order */
 int w1g_fetch_rwmd_best(w1g_ctx *ctx, int side, double *best, int64_t *n);
+/* row-sharded RWMD (one rank's share of lower_bound.py:43-58): the pairwise
+ * sum of mass*best over side `side`'s members [begin, end) (node order), which
+ * the host chooses as a subtree of numpy's summation tree so the ranks'
+ * partial sums combine bit-exactly; also returns the side's member count */
+int w1g_rwmd_range(w1g_ctx *ctx, int side, int64_t begin, int64_t end, double *partial,
+                   int64_t *n_members);
 /* tile culling in the FP32 all-pairs pass: 1 (default) or 0 (full brute force) */
 int w1g_set_rwmd_culling(w1g_ctx *ctx, int enabled);
 

@@ -89,6 +89,7 @@ _PROTOS = [
     ("w1g_rwmd", ctypes.c_int, [_vp, _F64P, _F64P, _F64P]),
     ("w1g_fetch_rwmd_best", ctypes.c_int, [_vp, ctypes.c_int, _F64P, _I64P]),
     ("w1g_set_rwmd_culling", ctypes.c_int, [_vp, ctypes.c_int]),
+    ("w1g_rwmd_range", ctypes.c_int, [_vp, ctypes.c_int, _i64, _i64, _F64P, _I64P]),
     ("w1g_delta_condense", ctypes.c_int, [_vp, _f64, _f64, _f64, _u64, _I64P]),
     ("w1g_split_tree", ctypes.c_int, [_vp, ctypes.c_int, _I64P, _I32P]),
     ("w1g_fetch_tree", ctypes.c_int, [_vp, _I64P, _I64P, _F64P, _I64P, _I64P]),

@@ -309,6 +309,17 @@ int w1g_fetch_rwmd_best(w1g_ctx *c, int side, double *best, int64_t *n) {
     return W1G_OK;
 }
 
+int w1g_rwmd_range(w1g_ctx *c, int side, int64_t begin, int64_t end, double *partial,
+                   int64_t *n_members) {
+    CTX_CHECK(c);
+    if (!c->nodes[0].valid) {
+        set_error("rwmd_range: no nodes0");
+        return W1G_ESTATE;
+    }
+    if (side < 0 || side > 1 || !partial || !n_members) return W1G_EINVAL;
+    return rwmd_range_run(*c, side, begin, end, partial, n_members);
+}
+
 int w1g_set_rwmd_culling(w1g_ctx *c, int enabled) {
     if (!c) return W1G_EINVAL;
     c->culling = enabled ? 1 : 0;

@@ -335,6 +335,7 @@ int zc_run(Ctx &c, const double2 *d_a, int64_t na, const double2 *d_b, int64_t n
            int32_t *balanced);
 int rwmd_run(Ctx &c, double *L, double *LA, double *LB);
 int rwmd_tile_profile(Ctx &c, int reps, float *ms, int64_t *evals);
+int rwmd_range_run(Ctx &c, int side, int64_t begin, int64_t end, double *partial, int64_t *n_members);
 int dc_run(Ctx &c, double delta, double pitch, double half_width, uint64_t seed, int64_t *k);
 int tree_run(Ctx &c, const double2 *d_pts, int64_t n, int64_t *n_nodes, int32_t *depth);
 int tree_geom(Ctx &c);

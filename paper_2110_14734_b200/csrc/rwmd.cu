@@ -102,12 +102,12 @@ __global__ void k_morton(const double2 *pts, const int32_t *members, int64_t n, 
 }
 
 __global__ void k_gather_members(const double2 *pts, const int32_t *members, const uint32_t *perm,
-                                  int64_t n, double2 *out, int32_t *pos) {
+                                  int64_t n, int64_t offset, double2 *out, int32_t *pos) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t m = perm[i];
         out[i] = pts[members[m]];
-        pos[i] = (int32_t)m;
+        pos[i] = (int32_t)(m + offset);
     }
 }
 
@@ -300,7 +300,9 @@ struct RwmdFrame {
     int32_t *mpos[2];  // member position (node order) of each Morton slot
 };
 
-static int rwmd_prepare(Ctx &c, RwmdFrame &F) {
+// range_side >= 0 restricts that side's SOURCE list to member positions
+// [begin, end) (row sharding across ranks); the other side stays complete
+static int rwmd_prepare(Ctx &c, RwmdFrame &F, int range_side = -1, int64_t begin = 0, int64_t end = 0) {
     NodeSet &ns = c.nodes[0];
     const int64_t k = ns.k;
     const double2 *pts = ptr<double2>(ns.pts);
@@ -337,7 +339,8 @@ static int rwmd_prepare(Ctx &c, RwmdFrame &F) {
     const double ext = H > 0.0 && std::isfinite(H) ? H : 1.0;
     const double inv = 65535.0 / ext;
     for (int s = 0; s < 2; s++) {
-        const int64_t n = F.nm[s];
+        const int64_t off = s == range_side ? begin : 0;
+        const int64_t n = s == range_side ? end - begin : F.nm[s];
         uint64_t *key;
         uint32_t *perm;
         W1G_TRY(ensure(c.scr[0], (size_t)n + 1, &key));
@@ -346,11 +349,11 @@ static int rwmd_prepare(Ctx &c, RwmdFrame &F) {
         W1G_TRY(ensure(c.scr[8 + 2 * s], (size_t)n + 1, &F.mpos[s]));
         if (n == 0) continue;
         const unsigned gn = grid_for(n, 256, 8u * c.sm_count);
-        k_morton<<<gn, 256, 0, c.stream>>>(pts, F.members[s], n, xmin, ymin, inv, key, perm);
+        k_morton<<<gn, 256, 0, c.stream>>>(pts, F.members[s] + off, n, xmin, ymin, inv, key, perm);
         W1G_CHECK_LAUNCH();
         uint64_t *keys[1] = {key};
         W1G_TRY(radix_sort(c, keys, 1, perm, n, 32));
-        k_gather_members<<<gn, 256, 0, c.stream>>>(pts, F.members[s], perm, n, F.mpts[s], F.mpos[s]);
+        k_gather_members<<<gn, 256, 0, c.stream>>>(pts, F.members[s] + off, perm, n, off, F.mpts[s], F.mpos[s]);
         W1G_CHECK_LAUNCH();
     }
     return W1G_OK;
@@ -406,6 +409,58 @@ int rwmd_run(Ctx &c, double *L, double *LA, double *LB) {
     *LA = h[0];
     *LB = h[1];
     *L = h[1] > h[0] ? h[1] : h[0];  // python max(l_a, l_b)
+    return W1G_OK;
+}
+
+// one rank's share of a row-sharded RWMD: side `side`'s sources restricted to
+// member positions [begin, end) (a subtree of numpy's summation tree, chosen
+// by the host), all targets; returns the subtree's pairwise sum
+int rwmd_range_run(Ctx &c, int side, int64_t begin, int64_t end, double *partial, int64_t *n_members) {
+    NodeSet &ns = c.nodes[0];
+    const int64_t *mass[2] = {ptr<int64_t>(ns.am), ptr<int64_t>(ns.bm)};
+    *partial = 0.0;
+    if (ns.k == 0) {
+        *n_members = 0;
+        return W1G_OK;
+    }
+    // member counts first (the range is validated against them)
+    RwmdFrame F;
+    W1G_TRY(rwmd_prepare(c, F, side, 0, 0));
+    *n_members = F.nm[side];
+    if (begin < 0 || end > F.nm[side] || begin > end) {
+        set_error("rwmd_range: [%lld, %lld) outside [0, %lld)", (long long)begin, (long long)end,
+                  (long long)F.nm[side]);
+        return W1G_EINVAL;
+    }
+    if (begin == end) return W1G_OK;
+    W1G_TRY(rwmd_prepare(c, F, side, begin, end));
+    const int s = side, o = 1 - side;
+    const int64_t n_src = end - begin, n_dst = F.nm[o];
+    const int64_t mx = (F.nm[0] > F.nm[1] ? F.nm[0] : F.nm[1]) + 1;
+    double *terms, *dres, *best;
+    unsigned *mf;
+    float *qn;
+    double4 *tbox, *box64;
+    W1G_TRY(ensure(c.scr[11], (size_t)mx, &terms));
+    W1G_TRY(ensure(c.scr[12], 4, &dres));
+    W1G_TRY(ensure(c.scr[13], (size_t)mx, &mf));
+    W1G_TRY(ensure(c.scr[14], (size_t)mx, &qn));
+    W1G_TRY(ensure(c.scr[15], (size_t)mx / 64 + 2, &tbox));
+    W1G_TRY(ensure(c.scr[16], (size_t)mx / 64 + 2, &box64));
+    W1G_TRY(ensure(c.best[s], (size_t)F.nm[s] + 1, &best));
+    if (n_dst > 0) {
+        W1G_CUDA(cudaMemsetAsync(mf, 0x7f, sizeof(unsigned) * n_src, c.stream));
+        W1G_TRY(rwmd_f32_min(c, F.mpts[s], n_src, F.mpts[o], n_dst, F.scale, mf, qn, tbox, c.culling));
+        k_boxes64<<<grid_for((n_dst / RT + 1) * 32, 256, 8u * c.sm_count), 256, 0, c.stream>>>(F.mpts[o], n_dst, box64);
+        W1G_CHECK_LAUNCH();
+    }
+    k_refine<<<(unsigned)((n_src + RF_QPB - 1) / RF_QPB), RF_BLOCK, 0, c.stream>>>(
+        F.mpts[s], F.mpos[s], F.members[s], mass[s], n_src, mf, qn, F.unscale, F.mpts[o], n_dst, box64, best,
+        terms);
+    W1G_CHECK_LAUNCH();
+    W1G_TRY(pairwise_sum(c, terms + begin, n_src, dres, c.scr[17], c.scr[18], c.scr[19]));
+    W1G_CUDA(cudaMemcpyAsync(partial, dres, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+    W1G_CUDA(cudaStreamSynchronize(c.stream));
     return W1G_OK;
 }
 
