@@ -135,6 +135,31 @@ __global__ void k_boxes64(const double2 *t, int64_t nt, double4 *box) {
     }
 }
 
+// super-tile boxes: the union of 64 consecutive refine-tile boxes (4096 targets)
+constexpr int SUP = 64;
+__global__ void k_superboxes(const double4 *box, int64_t ntile, double4 *sbox) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nsup = (ntile + SUP - 1) / SUP;
+    for (int64_t sp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; sp < nsup;
+         sp += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        double x0 = INFINITY, y0 = INFINITY, x1 = -INFINITY, y1 = -INFINITY;
+        for (int64_t k = sp * SUP + lane; k < min(ntile, (sp + 1) * SUP); k += 32) {
+            const double4 b = box[k];
+            x0 = fmin(x0, b.x);
+            y0 = fmin(y0, b.y);
+            x1 = fmax(x1, b.z);
+            y1 = fmax(y1, b.w);
+        }
+        for (int o = 16; o; o >>= 1) {
+            x0 = fmin(x0, __shfl_xor_sync(0xffffffffu, x0, o));
+            y0 = fmin(y0, __shfl_xor_sync(0xffffffffu, y0, o));
+            x1 = fmax(x1, __shfl_xor_sync(0xffffffffu, x1, o));
+            y1 = fmax(y1, __shfl_xor_sync(0xffffffffu, y1, o));
+        }
+        if (lane == 0) sbox[sp] = make_double4(x0, y0, x1, y1);
+    }
+}
+
 __device__ __forceinline__ double box_gap(double4 b, double4 a) {
     const double gx = fmax(0.0, fmax(b.x - a.z, a.x - b.z));
     const double gy = fmax(0.0, fmax(b.y - a.w, a.y - b.w));
@@ -170,8 +195,10 @@ __global__ void __launch_bounds__(RF_BLOCK) k_refine(const double2 *__restrict__
                                                      const float *__restrict__ qn, double unscale,
                                                      const double2 *__restrict__ t, int64_t nt,
                                                      const double4 *__restrict__ tbox,
+                                                     const double4 *__restrict__ sbox,
                                                      double *__restrict__ best_out, double *__restrict__ terms) {
     __shared__ int32_t s_cand[RF_CAND];
+    __shared__ bool s_supok[RF_CAND / SUP];
     __shared__ double2 s_t[RF_STAGE * RT];
     __shared__ double4 s_tb[RF_STAGE];
     __shared__ int s_nc;
@@ -228,12 +255,19 @@ __global__ void __launch_bounds__(RF_BLOCK) k_refine(const double2 *__restrict__
         const double rmax = s_rmax;
         const double4 pb = make_double4(p.x, p.y, p.x, p.y);
         const int64_t ntile = (nt + RT - 1) / RT;
-        for (int64_t t0 = 0; t0 < ntile; t0 += RF_CAND) {
+        const int64_t nsup = (ntile + SUP - 1) / SUP;
+        constexpr int SUP_ROUND = RF_CAND / SUP;  // super-tiles per round: <= RF_CAND child tiles
+        for (int64_t s0 = 0; s0 < nsup; s0 += SUP_ROUND) {
+            // two-level candidate search: super-tile boxes, then the child tiles
+            // of the super-tiles that pass (box tests in fp64 with slack)
             if (tid == 0) s_nc = 0;
+            if (tid < SUP_ROUND) s_supok[tid] = (s0 + tid < nsup) && box_gap(sbox[s0 + tid], qb) <= rmax;
             __syncthreads();
-            const int64_t t1 = min(ntile, t0 + RF_CAND);
-            for (int64_t k = t0 + tid; k < t1; k += RF_BLOCK)
-                if (box_gap(tbox[k], qb) <= rmax) s_cand[atomicAdd(&s_nc, 1)] = (int32_t)k;
+            for (int e = tid; e < SUP_ROUND * SUP; e += RF_BLOCK) {
+                if (!s_supok[e / SUP]) continue;
+                const int64_t k = s0 * SUP + e;
+                if (k < ntile && box_gap(tbox[k], qb) <= rmax) s_cand[atomicAdd(&s_nc, 1)] = (int32_t)k;
+            }
             __syncthreads();
             const int nc = s_nc;
             // candidate tiles are staged RF_STAGE at a time in shared memory; a
@@ -374,13 +408,14 @@ int rwmd_run(Ctx &c, double *L, double *LA, double *LB) {
     double *terms, *dres;
     unsigned *mf;
     float *qn;
-    double4 *tbox, *box64;
+    double4 *tbox, *box64, *sbox;
     W1G_TRY(ensure(c.scr[11], (size_t)mx, &terms));
     W1G_TRY(ensure(c.scr[12], 4, &dres));
     W1G_TRY(ensure(c.scr[13], (size_t)mx, &mf));
     W1G_TRY(ensure(c.scr[14], (size_t)mx, &qn));
     W1G_TRY(ensure(c.scr[15], (size_t)mx / 64 + 2, &tbox));  // per-tile boxes (tiles >= 64 targets)
     W1G_TRY(ensure(c.scr[16], (size_t)mx / 64 + 2, &box64));
+    W1G_TRY(ensure(c.scr[21], (size_t)mx / (64 * SUP) + 2, &sbox));
     for (int s = 0; s < 2; s++) {
         const int o = 1 - s;
         const int64_t n_src = F.nm[s], n_dst = F.nm[o];
@@ -396,10 +431,13 @@ int rwmd_run(Ctx &c, double *L, double *LA, double *LB) {
             W1G_TRY(rwmd_f32_min(c, F.mpts[s], n_src, F.mpts[o], n_dst, F.scale, mf, qn, tbox, c.culling));
             k_boxes64<<<grid_for((n_dst / RT + 1) * 32, 256, 8u * c.sm_count), 256, 0, c.stream>>>(F.mpts[o], n_dst, box64);
             W1G_CHECK_LAUNCH();
+            k_superboxes<<<grid_for((n_dst / RT / SUP + 1) * 32, 256, 8u * c.sm_count), 256, 0, c.stream>>>(
+                box64, (n_dst + RT - 1) / RT, sbox);
+            W1G_CHECK_LAUNCH();
         }
         k_refine<<<(unsigned)((n_src + RF_QPB - 1) / RF_QPB), RF_BLOCK, 0, c.stream>>>(
             F.mpts[s], F.mpos[s], F.members[s], mass[s], n_src, mf, qn, F.unscale, F.mpts[o], n_dst, box64,
-            best, terms);
+            sbox, best, terms);
         W1G_CHECK_LAUNCH();
         W1G_TRY(pairwise_sum(c, terms, n_src, dres + s, c.scr[17], c.scr[18], c.scr[19]));
     }
@@ -440,23 +478,27 @@ int rwmd_range_run(Ctx &c, int side, int64_t begin, int64_t end, double *partial
     double *terms, *dres, *best;
     unsigned *mf;
     float *qn;
-    double4 *tbox, *box64;
+    double4 *tbox, *box64, *sbox;
     W1G_TRY(ensure(c.scr[11], (size_t)mx, &terms));
     W1G_TRY(ensure(c.scr[12], 4, &dres));
     W1G_TRY(ensure(c.scr[13], (size_t)mx, &mf));
     W1G_TRY(ensure(c.scr[14], (size_t)mx, &qn));
     W1G_TRY(ensure(c.scr[15], (size_t)mx / 64 + 2, &tbox));
     W1G_TRY(ensure(c.scr[16], (size_t)mx / 64 + 2, &box64));
+    W1G_TRY(ensure(c.scr[21], (size_t)mx / (64 * SUP) + 2, &sbox));
     W1G_TRY(ensure(c.best[s], (size_t)F.nm[s] + 1, &best));
     if (n_dst > 0) {
         W1G_CUDA(cudaMemsetAsync(mf, 0x7f, sizeof(unsigned) * n_src, c.stream));
         W1G_TRY(rwmd_f32_min(c, F.mpts[s], n_src, F.mpts[o], n_dst, F.scale, mf, qn, tbox, c.culling));
         k_boxes64<<<grid_for((n_dst / RT + 1) * 32, 256, 8u * c.sm_count), 256, 0, c.stream>>>(F.mpts[o], n_dst, box64);
         W1G_CHECK_LAUNCH();
+        k_superboxes<<<grid_for((n_dst / RT / SUP + 1) * 32, 256, 8u * c.sm_count), 256, 0, c.stream>>>(
+            box64, (n_dst + RT - 1) / RT, sbox);
+        W1G_CHECK_LAUNCH();
     }
     k_refine<<<(unsigned)((n_src + RF_QPB - 1) / RF_QPB), RF_BLOCK, 0, c.stream>>>(
-        F.mpts[s], F.mpos[s], F.members[s], mass[s], n_src, mf, qn, F.unscale, F.mpts[o], n_dst, box64, best,
-        terms);
+        F.mpts[s], F.mpos[s], F.members[s], mass[s], n_src, mf, qn, F.unscale, F.mpts[o], n_dst, box64, sbox,
+        best, terms);
     W1G_CHECK_LAUNCH();
     W1G_TRY(pairwise_sum(c, terms + begin, n_src, dres, c.scr[17], c.scr[18], c.scr[19]));
     W1G_CUDA(cudaMemcpyAsync(partial, dres, sizeof(double), cudaMemcpyDeviceToHost, c.stream));

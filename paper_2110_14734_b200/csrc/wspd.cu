@@ -15,7 +15,11 @@
 // the pairs by (w, DFS pop order) -- the reference's exact output layout
 // (owner ascending, right child popped first, spanner.py:226-236) -- and
 // produces count_pairs' per-node counts.
+#include <cooperative_groups.h>
+
 #include "common.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace w1g {
 
@@ -92,16 +96,16 @@ struct ItemT<true> {
 };
 
 template <bool ORDER>
-__global__ void __launch_bounds__(256) k_wspd_level(const typename ItemT<ORDER>::T *__restrict__ cur,
-                                                    typename ItemT<ORDER>::T *__restrict__ next,
-                                                    int64_t cap, int level, Counters k,
-                                                    int2 *__restrict__ out_uv, int32_t *__restrict__ out_w,
-                                                    uint64_t *__restrict__ out_p0,
-                                                    uint64_t *__restrict__ out_p1, int64_t pair_cap,
-                                                    double s, const NodeGeom *__restrict__ geom,
-                                                    const int2 *__restrict__ lr) {
+__device__ __forceinline__ void wspd_level(const typename ItemT<ORDER>::T *__restrict__ cur,
+                                           typename ItemT<ORDER>::T *__restrict__ next,
+                                           int64_t cap, int level, Counters k,
+                                           int2 *__restrict__ out_uv, int32_t *__restrict__ out_w,
+                                           uint64_t *__restrict__ out_p0,
+                                           uint64_t *__restrict__ out_p1, int64_t pair_cap,
+                                           double s, const NodeGeom *__restrict__ geom,
+                                           const int2 *__restrict__ lr) {
     using Item = typename ItemT<ORDER>::T;
-    int64_t n = k.cnt[level % 3];
+    int64_t n = *((volatile int64_t *)&k.cnt[level % 3]);
     if (n > cap) n = cap;  // previous level overflowed: its flag is already set
     if (blockIdx.x == 0 && threadIdx.x == 0) k.cnt[(level + 2) % 3] = 0;
     const int lane = threadIdx.x & 31;
@@ -171,6 +175,40 @@ __global__ void __launch_bounds__(256) k_wspd_level(const typename ItemT<ORDER>:
             }
         }
     }
+}
+
+template <bool ORDER>
+__global__ void __launch_bounds__(256) k_wspd_level(const typename ItemT<ORDER>::T *__restrict__ cur,
+                                                    typename ItemT<ORDER>::T *__restrict__ next,
+                                                    int64_t cap, int level, Counters k,
+                                                    int2 *__restrict__ out_uv, int32_t *__restrict__ out_w,
+                                                    uint64_t *__restrict__ out_p0,
+                                                    uint64_t *__restrict__ out_p1, int64_t pair_cap,
+                                                    double s, const NodeGeom *__restrict__ geom,
+                                                    const int2 *__restrict__ lr) {
+    wspd_level<ORDER>(cur, next, cap, level, k, out_uv, out_w, out_p0, out_p1, pair_cap, s, geom, lr);
+}
+
+// all frontier levels in ONE persistent cooperative launch: a grid barrier
+// per level instead of a launch per level and a host poll per batch
+template <bool ORDER>
+__global__ void __launch_bounds__(256) k_wspd_coop(typename ItemT<ORDER>::T *fa, typename ItemT<ORDER>::T *fb,
+                                                   int64_t cap, Counters k, int2 *__restrict__ out_uv,
+                                                   int32_t *__restrict__ out_w, uint64_t *__restrict__ out_p0,
+                                                   uint64_t *__restrict__ out_p1, int64_t pair_cap, double s,
+                                                   const NodeGeom *__restrict__ geom, const int2 *__restrict__ lr,
+                                                   int32_t *levels_out) {
+    cg::grid_group grid = cg::this_grid();
+    int level = 0;
+    while (true) {
+        const int64_t n = *((volatile int64_t *)&k.cnt[level % 3]);
+        if (n == 0 || n > cap) break;  // done, or the last level overflowed (flag set)
+        wspd_level<ORDER>((level & 1) ? fb : fa, (level & 1) ? fa : fb, cap, level, k, out_uv, out_w, out_p0,
+                          out_p1, pair_cap, s, geom, lr);
+        grid.sync();
+        level++;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) *levels_out = level;
 }
 
 __global__ void k_order_keys(const int32_t *w, const uint64_t *p0, const uint64_t *p1, int64_t n,
@@ -263,9 +301,42 @@ int wspd_run(Ctx &c, double s, int reference_order, int64_t *n_pairs) {
         }
         const unsigned gl = 8u * c.sm_count;
         int level = 0;
-        bool ovf = false;
+        bool ovf = false, nn_done = false;
         const int BATCH = 8;
-        while (nn > 1) {
+        if (nn > 1) {
+            // persistent cooperative launch: every level, one grid barrier each
+            int per_sm = 0;
+            const void *fn = ORDER ? (const void *)k_wspd_coop<true> : (const void *)k_wspd_coop<false>;
+            W1G_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, 0));
+            if (per_sm > 4) per_sm = 4;
+            if (per_sm >= 1) {
+                const int G = per_sm * c.sm_count;
+                int32_t *lv = reinterpret_cast<int32_t *>(ctr + 6);
+                NodeGeom *geom = ptr<NodeGeom>(c.t_geom);
+                int2 *lr = ptr<int2>(c.t_lr);
+                int2 *uvp = uv;
+                int32_t *wp = w;
+                uint64_t *p0p = p0, *p1p = p1;
+                void *fap = fa, *fbp = fb;
+                int64_t fc = front_cap, pc = pair_cap;
+                double sv = s;
+                void *args[] = {&fap, &fbp, &fc, &k, &uvp, &wp, &p0p, &p1p, &pc, &sv, &geom, &lr, &lv};
+                W1G_CUDA(cudaLaunchCooperativeKernel(fn, G, 256, args, 0, c.stream));
+                W1G_CHECK_LAUNCH();
+                W1G_CUDA(cudaMemcpyAsync(c.h_pinned + F_MISC0, ctr, sizeof(int64_t) * 8, cudaMemcpyDeviceToHost, c.stream));
+                W1G_CUDA(cudaMemcpyAsync(c.h_pinned + F_PAIR_OVF, dflags(c) + F_PAIR_OVF, sizeof(int64_t) * 5,
+                                         cudaMemcpyDeviceToHost, c.stream));
+                W1G_CUDA(cudaStreamSynchronize(c.stream));
+                level = (int)(c.h_pinned[F_MISC0 + 6] & 0x7fffffff);
+                const int64_t live = c.h_pinned[F_MISC0 + level % 3];
+                if (c.h_pinned[F_FRONT_OVF] || live > front_cap) {
+                    ovf = true;
+                    front_cap = front_cap * 2 + (live > front_cap ? live : 0);
+                }
+                nn_done = true;
+            }
+        }
+        while (nn > 1 && !nn_done) {
             for (int b = 0; b < BATCH; b++, level++) {
                 void *cur = (level & 1) ? fb : fa, *nxt = (level & 1) ? fa : fb;
                 if (ORDER)
