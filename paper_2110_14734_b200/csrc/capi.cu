@@ -170,6 +170,7 @@ int w1g_ctx_create(int device, w1g_ctx **out) {
     w1g_ctx *c = new w1g_ctx();
     c->device = device;
     c->sm_count = prop.multiProcessorCount;
+    if (const char *e = getenv("W1G_CULL_STEPS")) c->cull_steps = atoi(e) > 0 ? atoi(e) : 0;
     W1G_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     int64_t *f;
     W1G_TRY(ensure(c->flags, F_NSLOTS, &f));

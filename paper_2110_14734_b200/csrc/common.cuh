@@ -87,6 +87,7 @@ struct Ctx {
 
     // rwmd
     int culling = 1;
+    int cull_steps = 0;  // 0 = by size; W1G_CULL_STEPS overrides (tuning)
     DevBuf best[2];
     int64_t n_best[2] = {0, 0};
     int64_t rw_members[2] = {0, 0};  // A- and B-member counts of the last rwmd_run

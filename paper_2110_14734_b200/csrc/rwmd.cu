@@ -179,6 +179,123 @@ __device__ __forceinline__ double upper_bound(float est, float qn) {
     return dt * (1.0 + 0x1p-20) + 0x1p-20 * x + 0x1p-40;
 }
 
+// exact fp64 refinement + mass * best (lower_bound.py:51-58), warp-centric:
+// every warp owns 16 Morton-consecutive sources (two lanes per source, each
+// taking every other target of a tile) and finds its own candidate tiles with
+// its own radius -- super-tile boxes first, then the 64 child-tile boxes of the
+// super-tiles that pass -- so one distant source never widens the search of
+// its neighbours' warps.  Targets are read straight from L1/L2 (all lanes of
+// the warp read the same tile).
+constexpr int64_t REFINE_WARP_MIN = 300000;  // targets from which the warp-centric refine wins (measured)
+constexpr int RW_WARPS = 4;        // warps per CTA
+constexpr int RW_QPW = 16;         // sources per warp
+constexpr int RW_CAND = 256;       // candidate tiles per round and warp
+
+__global__ void __launch_bounds__(32 * RW_WARPS) k_refine_w(
+    const double2 *__restrict__ q, const int32_t *__restrict__ qpos, const int32_t *__restrict__ members,
+    const int64_t *__restrict__ mass, int64_t nq, const unsigned *__restrict__ mf32,
+    const float *__restrict__ qn, double unscale, const double2 *__restrict__ t, int64_t nt,
+    const double4 *__restrict__ tbox, const double4 *__restrict__ sbox, double *__restrict__ best_out,
+    double *__restrict__ terms) {
+    __shared__ int32_t s_cand[RW_WARPS][RW_CAND];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, sub = lane & 1;
+    int32_t *cand = s_cand[wid];
+    const int64_t i = ((int64_t)blockIdx.x * RW_WARPS + wid) * RW_QPW + (lane >> 1);
+    const bool valid = i < nq;
+    double2 p = make_double2(0, 0);
+    double diag = 0.0, r = -1.0;
+    if (valid) {
+        p = q[i];
+        diag = ddiv(fabs(dsub(p.y, p.x)), SQRT2);  // diagram.py:47
+        if (nt > 0) {
+            const double U = upper_bound(__uint_as_float(mf32[i]), qn[i]) * unscale * (1.0 + 1e-9);
+            r = fmin(U, diag * (1.0 + 1e-12));
+            r += 0x1p-50 * (fabs(p.x) + fabs(p.y) + r) + 1e-300;
+        }
+    }
+    double m2 = INFINITY, m2b = INFINITY;
+    if (nt > 0) {
+        double4 qb = valid ? make_double4(p.x, p.y, p.x, p.y) : make_double4(INFINITY, INFINITY, -INFINITY, -INFINITY);
+        double rmax = r;
+        for (int o = 16; o; o >>= 1) {
+            qb.x = fmin(qb.x, __shfl_xor_sync(0xffffffffu, qb.x, o));
+            qb.y = fmin(qb.y, __shfl_xor_sync(0xffffffffu, qb.y, o));
+            qb.z = fmax(qb.z, __shfl_xor_sync(0xffffffffu, qb.z, o));
+            qb.w = fmax(qb.w, __shfl_xor_sync(0xffffffffu, qb.w, o));
+            rmax = fmax(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
+        }
+        rmax *= 1.0 + 1e-9;
+        const double4 pb = make_double4(p.x, p.y, p.x, p.y);
+        const int64_t ntile = (nt + RT - 1) / RT;
+        const int64_t nsup = (ntile + SUP - 1) / SUP;
+        int nc = 0;
+        auto flush = [&]() {
+            for (int c = 0; c < nc; c++) {
+                const int64_t k = cand[c];
+                const bool need = valid && r >= 0.0 && box_gap(tbox[k], pb) <= r * (1.0 + 1e-9);
+                if (!__any_sync(0xffffffffu, need)) continue;
+                const double2 *tt = t + k * RT + sub;
+                const int cnt = (int)min((int64_t)RT, nt - k * RT);
+                if (cnt == RT) {
+#pragma unroll
+                    for (int j = 0; j < RT / 2; j += 2) {
+                        const double2 ta = tt[2 * j], tb = tt[2 * j + 2];
+                        const double ax = dsub(p.x, ta.x), ay = dsub(p.y, ta.y);
+                        const double bx = dsub(p.x, tb.x), by = dsub(p.y, tb.y);
+                        const double da = dadd(dmul(ax, ax), dmul(ay, ay));
+                        const double db = dadd(dmul(bx, bx), dmul(by, by));
+                        m2 = da < m2 ? da : m2;
+                        m2b = db < m2b ? db : m2b;
+                    }
+                } else {
+                    for (int j = sub; j < cnt; j += 2) {
+                        const double2 ta = t[k * RT + j];
+                        const double ax = dsub(p.x, ta.x), ay = dsub(p.y, ta.y);
+                        const double da = dadd(dmul(ax, ax), dmul(ay, ay));
+                        m2 = da < m2 ? da : m2;
+                    }
+                }
+            }
+            __syncwarp();
+            nc = 0;
+        };
+        for (int64_t s0 = 0; s0 < nsup; s0 += 32) {
+            const int64_t sp = s0 + lane;
+            const bool ok = sp < nsup && box_gap(sbox[sp], qb) <= rmax;
+            unsigned sm = __ballot_sync(0xffffffffu, ok);
+            while (sm) {
+                const int b = __ffs(sm) - 1;
+                sm &= sm - 1;
+                const int64_t base = (s0 + b) * SUP;
+#pragma unroll
+                for (int h = 0; h < SUP / 32; h++) {
+                    const int64_t k = base + h * 32 + lane;
+                    const bool c_ok = k < ntile && box_gap(tbox[k], qb) <= rmax;
+                    const unsigned cm = __ballot_sync(0xffffffffu, c_ok);
+                    if (c_ok) cand[nc + __popc(cm & lanemask_lt())] = (int32_t)k;
+                    nc += __popc(cm);
+                    __syncwarp();
+                    if (nc > RW_CAND - 32) flush();
+                }
+            }
+        }
+        flush();
+    }
+    m2 = m2b < m2 ? m2b : m2;
+    const double other = __shfl_xor_sync(0xffffffffu, m2, 1);
+    m2 = other < m2 ? other : m2;
+    if (valid && sub == 0) {
+        double best = diag;
+        if (nt > 0) {
+            const double nnd = dsqrt(m2);
+            best = nnd < diag ? nnd : diag;  // np.minimum(nnd, diag)
+        }
+        const int32_t pos = qpos[i];
+        best_out[pos] = best;
+        terms[pos] = dmul(__ll2double_rn(mass[members[pos]]), best);  // float64(src_mass) * best
+    }
+}
+
 constexpr int RF_BLOCK = 128;
 constexpr int RF_TPQ = 2;                     // threads per source
 constexpr int RF_QPB = RF_BLOCK / RF_TPQ;     // sources per block
@@ -435,9 +552,14 @@ int rwmd_run(Ctx &c, double *L, double *LA, double *LB) {
                 box64, (n_dst + RT - 1) / RT, sbox);
             W1G_CHECK_LAUNCH();
         }
-        k_refine<<<(unsigned)((n_src + RF_QPB - 1) / RF_QPB), RF_BLOCK, 0, c.stream>>>(
-            F.mpts[s], F.mpos[s], F.members[s], mass[s], n_src, mf, qn, F.unscale, F.mpts[o], n_dst, box64,
-            sbox, best, terms);
+        if (n_dst >= REFINE_WARP_MIN)
+            k_refine_w<<<(unsigned)((n_src + RW_WARPS * RW_QPW - 1) / (RW_WARPS * RW_QPW)), 32 * RW_WARPS, 0, c.stream>>>(
+                F.mpts[s], F.mpos[s], F.members[s], mass[s], n_src, mf, qn, F.unscale, F.mpts[o], n_dst, box64,
+                sbox, best, terms);
+        else
+            k_refine<<<(unsigned)((n_src + RF_QPB - 1) / RF_QPB), RF_BLOCK, 0, c.stream>>>(
+                F.mpts[s], F.mpos[s], F.members[s], mass[s], n_src, mf, qn, F.unscale, F.mpts[o], n_dst, box64,
+                sbox, best, terms);
         W1G_CHECK_LAUNCH();
         W1G_TRY(pairwise_sum(c, terms, n_src, dres + s, c.scr[17], c.scr[18], c.scr[19]));
     }
@@ -496,9 +618,14 @@ int rwmd_range_run(Ctx &c, int side, int64_t begin, int64_t end, double *partial
             box64, (n_dst + RT - 1) / RT, sbox);
         W1G_CHECK_LAUNCH();
     }
-    k_refine<<<(unsigned)((n_src + RF_QPB - 1) / RF_QPB), RF_BLOCK, 0, c.stream>>>(
-        F.mpts[s], F.mpos[s], F.members[s], mass[s], n_src, mf, qn, F.unscale, F.mpts[o], n_dst, box64, sbox,
-        best, terms);
+    if (n_dst >= REFINE_WARP_MIN)
+        k_refine_w<<<(unsigned)((n_src + RW_WARPS * RW_QPW - 1) / (RW_WARPS * RW_QPW)), 32 * RW_WARPS, 0, c.stream>>>(
+            F.mpts[s], F.mpos[s], F.members[s], mass[s], n_src, mf, qn, F.unscale, F.mpts[o], n_dst, box64, sbox,
+            best, terms);
+    else
+        k_refine<<<(unsigned)((n_src + RF_QPB - 1) / RF_QPB), RF_BLOCK, 0, c.stream>>>(
+            F.mpts[s], F.mpos[s], F.members[s], mass[s], n_src, mf, qn, F.unscale, F.mpts[o], n_dst, box64, sbox,
+            best, terms);
     W1G_CHECK_LAUNCH();
     W1G_TRY(pairwise_sum(c, terms + begin, n_src, dres, c.scr[17], c.scr[18], c.scr[19]));
     W1G_CUDA(cudaMemcpyAsync(partial, dres, sizeof(double), cudaMemcpyDeviceToHost, c.stream));

@@ -20,8 +20,10 @@
 //  * full mode (culling off): every source meets every target, the target
 //    range is split across grid.y to fill the 148 SMs and per-chunk minima
 //    merge with an order-independent atomicMin on the float bits;
-//  * culled mode: one CTA per source block walks the Morton-ordered target
-//    tiles outward from its own position and skips every tile whose bbox is
+//  * culled mode (the production path): any real target's distance is a
+//    valid upper bound for the exact pass, so each CTA only evaluates the
+//    Morton-nearest target tiles (walking outward from its own position,
+//    5 tiles, or 17 for large target sets) and skips tiles whose bbox is
 //    farther than the CTA's current worst upper bound.
 //
 // The result only sizes the exact fp64 search in rwmd.cu.  This translation
@@ -35,7 +37,6 @@ namespace {
 constexpr int T_BLOCK = 256;
 constexpr int TS_FULL = 1024;  // targets per shared-memory tile, full mode
 constexpr int TS_CULL = 256;   // targets per shared-memory tile, culled mode
-constexpr int CULL_STEPS = 5;  // culled mode: the Morton-nearest tile and four neighbours
 
 __device__ __forceinline__ float min3(float a, float b, float c) {
     float d;
@@ -59,6 +60,7 @@ struct TileArgs {
     unsigned *mout;         // min d^2 estimate (float bits), scaled units
     float *qn_out;          // |q'| per source
     int chunk;              // targets per grid.y chunk (full mode)
+    int cull_steps;         // culled mode: tiles walked outward from the Morton position
 };
 
 template <int R, bool CULL, int T_TS>
@@ -138,7 +140,7 @@ __global__ void __launch_bounds__(T_BLOCK) k_rwmd_f32(TileArgs A) {
     // culled mode only needs SOME real target per source (any target's distance
     // is a valid upper bound for the exact pass), so it walks a few Morton
     // neighbours of the CTA and stops; full mode meets every target
-    const int n_steps = CULL ? min(2 * n_tiles, CULL_STEPS) : n_tiles;
+    const int n_steps = CULL ? min(2 * n_tiles, A.cull_steps) : n_tiles;
     for (int k = 0; k < n_steps; k++) {
         int tile;
         if (CULL) {
@@ -254,6 +256,9 @@ int rwmd_f32_min(Ctx &c, const double2 *q, int64_t nq, const double2 *t, int64_t
     A.scale = scale;
     A.mout = mout;
     A.qn_out = qn_out;
+    // tiles walked per CTA in culled mode: more for large target sets, where
+    // Morton-order jumps make the nearest tiles a poorer seed (measured)
+    A.cull_steps = c.cull_steps > 0 ? c.cull_steps : (nt >= 300000 ? 17 : 5);
     if (culling) {
         const int ntile = (int)((nt + TS_CULL - 1) / TS_CULL);
         k_tile_boxes<<<grid_for((int64_t)ntile * 32, 256, 8u * c.sm_count), 256, 0, c.stream>>>(t, (int)nt, TS_CULL, tbox);
