@@ -9,6 +9,7 @@
 #include <stdint.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <string>
 
 #include "../../include/w1g.h"
@@ -88,6 +89,8 @@ struct Ctx {
     // rwmd
     int culling = 1;
     int cull_steps = 0;  // 0 = by size; W1G_CULL_STEPS overrides (tuning)
+    int debug_radius = 0;  // W1G_DEBUG_RADIUS=1: rwmd "best" reports the exact-pass radius
+    int64_t refine_warp_min = 300000;  // targets from which the warp-centric refine is used (W1G_REFINE_WARP_MIN)
     DevBuf best[2];
     int64_t n_best[2] = {0, 0};
     int64_t rw_members[2] = {0, 0};  // A- and B-member counts of the last rwmd_run
@@ -330,6 +333,40 @@ __device__ __forceinline__ unsigned lanemask_lt() {
     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
     return m;
 }
+
+// Optional sub-stage timing (W1G_TIMING=1): CUDA events on the context stream,
+// one line per mark printed to stderr when the timer goes out of scope.
+struct SubTimer {
+    Ctx &c;
+    const char *stage;
+    bool on;
+    int n = 0;
+    cudaEvent_t ev[24];
+    const char *name[24];
+    SubTimer(Ctx &ctx, const char *s) : c(ctx), stage(s) {
+        const char *e = getenv("W1G_TIMING");
+        on = e && *e == '1';
+        if (on) mark("start");
+    }
+    void mark(const char *nm) {
+        if (!on || n >= 24) return;
+        cudaEventCreate(&ev[n]);
+        cudaEventRecord(ev[n], c.stream);
+        name[n++] = nm;
+    }
+    ~SubTimer() {
+        if (!on || n < 2) return;
+        cudaEventSynchronize(ev[n - 1]);
+        fprintf(stderr, "[w1g %s]", stage);
+        for (int i = 1; i < n; i++) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, ev[i - 1], ev[i]);
+            fprintf(stderr, " %s=%.1fus", name[i], 1e3f * ms);
+        }
+        fprintf(stderr, "\n");
+        for (int i = 0; i < n; i++) cudaEventDestroy(ev[i]);
+    }
+};
 
 // stage launchers (one translation unit each)
 int zc_run(Ctx &c, const double2 *d_a, int64_t na, const double2 *d_b, int64_t nb, int64_t *k0,

@@ -160,10 +160,12 @@ __global__ void k_superboxes(const double4 *box, int64_t ntile, double4 *sbox) {
     }
 }
 
-__device__ __forceinline__ double box_gap(double4 b, double4 a) {
+// is box b within distance R of box a?  (squared compare: no sqrt on the hot path;
+// R carries the caller's relative slack, a negative R matches nothing)
+__device__ __forceinline__ bool within(double4 b, double4 a, double R) {
     const double gx = fmax(0.0, fmax(b.x - a.z, a.x - b.z));
     const double gy = fmax(0.0, fmax(b.y - a.w, a.y - b.w));
-    return sqrt(gx * gx + gy * gy);
+    return R >= 0.0 && gx * gx + gy * gy <= R * R;
 }
 
 // Rigorous upper bound (scaled units) on the distance from a source to the
@@ -173,10 +175,21 @@ __device__ __forceinline__ double box_gap(double4 b, double4 a) {
 //   |est - D~^2| <= 5u (2|x| + D~)^2          (expanded form, FFMA/FFMA2)
 //   |D - D~|     <= u (2|x| + D~)              (one rounding per coordinate)
 // so with c = 2^-20 >= 5u:  D~ <= (sqrt(est) + 2 sqrt(c) |x|) / (1 - sqrt(c)).
-__device__ __forceinline__ double upper_bound(float est, float qn) {
+__device__ __forceinline__ double upper_bound_expanded(float est, float qn) {
     const double x = (double)qn * (1.0 + 0x1p-20) + 0x1p-60;
     const double dt = (sqrt(fmax((double)est, 0.0)) + 0x1p-9 * x) / (1.0 - 0x1p-10);
     return dt * (1.0 + 0x1p-20) + 0x1p-20 * x + 0x1p-40;
+}
+// The direct form (culled mode: dx = x - y, est = fl(dy^2 + fl(dx^2))) does
+// not cancel: est >= |(dx,dy)|^2 (1 - 2.01u), |(dx,dy)| >= |x - y| (1 - u) and
+// |D - |x - y|| <= u (2|x| + D), hence
+//   D <= (sqrt(est)(1 + 1.01u)/(1 - u) + 2u|x|(1 + 3u)) / (1 - u);
+// 2^-20 = 16u covers every factor.
+__device__ __forceinline__ double upper_bound_direct(float est, float qn) {
+    return (sqrt(fmax((double)est, 0.0)) * (1.0 + 0x1p-20) + 0x1p-20 * (double)qn) * (1.0 + 0x1p-20) + 0x1p-60;
+}
+__device__ __forceinline__ double upper_bound(float est, float qn, int direct) {
+    return direct ? upper_bound_direct(est, qn) : upper_bound_expanded(est, qn);
 }
 
 // exact fp64 refinement + mass * best (lower_bound.py:51-58), warp-centric:
@@ -186,7 +199,7 @@ __device__ __forceinline__ double upper_bound(float est, float qn) {
 // super-tiles that pass -- so one distant source never widens the search of
 // its neighbours' warps.  Targets are read straight from L1/L2 (all lanes of
 // the warp read the same tile).
-constexpr int64_t REFINE_WARP_MIN = 300000;  // targets from which the warp-centric refine wins (measured)
+constexpr int64_t REFINE_WARP_MIN = 0;  // targets from which the warp-centric refine is used
 constexpr int RW_WARPS = 4;        // warps per CTA
 constexpr int RW_QPW = 16;         // sources per warp
 constexpr int RW_CAND = 256;       // candidate tiles per round and warp
@@ -196,10 +209,8 @@ __global__ void __launch_bounds__(32 * RW_WARPS) k_refine_w(
     const int64_t *__restrict__ mass, int64_t nq, const unsigned *__restrict__ mf32,
     const float *__restrict__ qn, double unscale, const double2 *__restrict__ t, int64_t nt,
     const double4 *__restrict__ tbox, const double4 *__restrict__ sbox, double *__restrict__ best_out,
-    double *__restrict__ terms) {
-    __shared__ int32_t s_cand[RW_WARPS][RW_CAND];
+    double *__restrict__ terms, int direct) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, sub = lane & 1;
-    int32_t *cand = s_cand[wid];
     const int64_t i = ((int64_t)blockIdx.x * RW_WARPS + wid) * RW_QPW + (lane >> 1);
     const bool valid = i < nq;
     double2 p = make_double2(0, 0);
@@ -208,7 +219,7 @@ __global__ void __launch_bounds__(32 * RW_WARPS) k_refine_w(
         p = q[i];
         diag = ddiv(fabs(dsub(p.y, p.x)), SQRT2);  // diagram.py:47
         if (nt > 0) {
-            const double U = upper_bound(__uint_as_float(mf32[i]), qn[i]) * unscale * (1.0 + 1e-9);
+            const double U = upper_bound(__uint_as_float(mf32[i]), qn[i], direct & 1) * unscale * (1.0 + 1e-9);
             r = fmin(U, diag * (1.0 + 1e-12));
             r += 0x1p-50 * (fabs(p.x) + fabs(p.y) + r) + 1e-300;
         }
@@ -228,12 +239,9 @@ __global__ void __launch_bounds__(32 * RW_WARPS) k_refine_w(
         const double4 pb = make_double4(p.x, p.y, p.x, p.y);
         const int64_t ntile = (nt + RT - 1) / RT;
         const int64_t nsup = (ntile + SUP - 1) / SUP;
-        int nc = 0;
-        auto flush = [&]() {
-            for (int c = 0; c < nc; c++) {
-                const int64_t k = cand[c];
-                const bool need = valid && r >= 0.0 && box_gap(tbox[k], pb) <= r * (1.0 + 1e-9);
-                if (!__any_sync(0xffffffffu, need)) continue;
+        const double rr = r * (1.0 + 1e-9);
+        auto eval_tile = [&](int64_t k) {
+            {
                 const double2 *tt = t + k * RT + sub;
                 const int cnt = (int)min((int64_t)RT, nt - k * RT);
                 if (cnt == RT) {
@@ -256,30 +264,24 @@ __global__ void __launch_bounds__(32 * RW_WARPS) k_refine_w(
                     }
                 }
             }
-            __syncwarp();
-            nc = 0;
         };
+        // super-tiles: 32 at a time against the warp's box (cheap pre-filter),
+        // then each source tests the super-tile and its 64 child tiles against
+        // its own radius; a tile is evaluated by the warp iff some source needs it
         for (int64_t s0 = 0; s0 < nsup; s0 += 32) {
             const int64_t sp = s0 + lane;
-            const bool ok = sp < nsup && box_gap(sbox[sp], qb) <= rmax;
+            const bool ok = sp < nsup && within(sbox[sp], qb, rmax);
             unsigned sm = __ballot_sync(0xffffffffu, ok);
             while (sm) {
                 const int b = __ffs(sm) - 1;
                 sm &= sm - 1;
-                const int64_t base = (s0 + b) * SUP;
-#pragma unroll
-                for (int h = 0; h < SUP / 32; h++) {
-                    const int64_t k = base + h * 32 + lane;
-                    const bool c_ok = k < ntile && box_gap(tbox[k], qb) <= rmax;
-                    const unsigned cm = __ballot_sync(0xffffffffu, c_ok);
-                    if (c_ok) cand[nc + __popc(cm & lanemask_lt())] = (int32_t)k;
-                    nc += __popc(cm);
-                    __syncwarp();
-                    if (nc > RW_CAND - 32) flush();
-                }
+                const int64_t si = s0 + b;
+                if (!__any_sync(0xffffffffu, valid && within(sbox[si], pb, rr))) continue;
+                const int64_t kend = min(ntile, (si + 1) * SUP);
+                for (int64_t k = si * SUP; k < kend; k++)
+                    if (__any_sync(0xffffffffu, valid && within(tbox[k], pb, rr))) eval_tile(k);
             }
         }
-        flush();
     }
     m2 = m2b < m2 ? m2b : m2;
     const double other = __shfl_xor_sync(0xffffffffu, m2, 1);
@@ -291,7 +293,7 @@ __global__ void __launch_bounds__(32 * RW_WARPS) k_refine_w(
             best = nnd < diag ? nnd : diag;  // np.minimum(nnd, diag)
         }
         const int32_t pos = qpos[i];
-        best_out[pos] = best;
+        best_out[pos] = (direct & 2) ? r : best;  // bit 1: debug, report the search radius
         terms[pos] = dmul(__ll2double_rn(mass[members[pos]]), best);  // float64(src_mass) * best
     }
 }
@@ -313,7 +315,8 @@ __global__ void __launch_bounds__(RF_BLOCK) k_refine(const double2 *__restrict__
                                                      const double2 *__restrict__ t, int64_t nt,
                                                      const double4 *__restrict__ tbox,
                                                      const double4 *__restrict__ sbox,
-                                                     double *__restrict__ best_out, double *__restrict__ terms) {
+                                                     double *__restrict__ best_out, double *__restrict__ terms,
+                                                     int direct) {
     __shared__ int32_t s_cand[RF_CAND];
     __shared__ bool s_supok[RF_CAND / SUP];
     __shared__ double2 s_t[RF_STAGE * RT];
@@ -332,7 +335,7 @@ __global__ void __launch_bounds__(RF_BLOCK) k_refine(const double2 *__restrict__
         p = q[i];
         diag = ddiv(fabs(dsub(p.y, p.x)), SQRT2);  // diagram.py:47
         if (nt > 0) {
-            const double U = upper_bound(__uint_as_float(mf32[i]), qn[i]) * unscale * (1.0 + 1e-9);
+            const double U = upper_bound(__uint_as_float(mf32[i]), qn[i], direct & 1) * unscale * (1.0 + 1e-9);
             r = fmin(U, diag * (1.0 + 1e-12));
             r += 0x1p-50 * (fabs(p.x) + fabs(p.y) + r) + 1e-300;
         }
@@ -378,12 +381,12 @@ __global__ void __launch_bounds__(RF_BLOCK) k_refine(const double2 *__restrict__
             // two-level candidate search: super-tile boxes, then the child tiles
             // of the super-tiles that pass (box tests in fp64 with slack)
             if (tid == 0) s_nc = 0;
-            if (tid < SUP_ROUND) s_supok[tid] = (s0 + tid < nsup) && box_gap(sbox[s0 + tid], qb) <= rmax;
+            if (tid < SUP_ROUND) s_supok[tid] = (s0 + tid < nsup) && within(sbox[s0 + tid], qb, rmax);
             __syncthreads();
             for (int e = tid; e < SUP_ROUND * SUP; e += RF_BLOCK) {
                 if (!s_supok[e / SUP]) continue;
                 const int64_t k = s0 * SUP + e;
-                if (k < ntile && box_gap(tbox[k], qb) <= rmax) s_cand[atomicAdd(&s_nc, 1)] = (int32_t)k;
+                if (k < ntile && within(tbox[k], qb, rmax)) s_cand[atomicAdd(&s_nc, 1)] = (int32_t)k;
             }
             __syncthreads();
             const int nc = s_nc;
@@ -400,7 +403,7 @@ __global__ void __launch_bounds__(RF_BLOCK) k_refine(const double2 *__restrict__
                 if (tid < ns) s_tb[tid] = tbox[s_cand[c0 + tid]];
                 __syncthreads();
                 for (int c = 0; c < ns; c++) {
-                    const bool need = valid && r >= 0.0 && box_gap(s_tb[c], pb) <= r * (1.0 + 1e-9);
+                    const bool need = valid && r >= 0.0 && within(s_tb[c], pb, r * (1.0 + 1e-9));
                     if (!__any_sync(0xffffffffu, need)) continue;
                     const double2 *st = s_t + c * RT + sub;
 #pragma unroll
@@ -428,7 +431,7 @@ __global__ void __launch_bounds__(RF_BLOCK) k_refine(const double2 *__restrict__
             best = nnd < diag ? nnd : diag;  // np.minimum(nnd, diag)
         }
         const int32_t pos = qpos[i];
-        best_out[pos] = best;
+        best_out[pos] = (direct & 2) ? r : best;  // bit 1: debug, report the search radius
         terms[pos] = dmul(__ll2double_rn(mass[members[pos]]), best);  // float64(src_mass) * best
     }
 }
@@ -519,8 +522,10 @@ int rwmd_run(Ctx &c, double *L, double *LA, double *LB) {
         c.n_best[0] = c.n_best[1] = 0;
         return W1G_OK;
     }
+    SubTimer T(c, "rwmd");
     RwmdFrame F;
     W1G_TRY(rwmd_prepare(c, F));
+    T.mark("prepare");
     const int64_t mx = (F.nm[0] > F.nm[1] ? F.nm[0] : F.nm[1]) + 1;
     double *terms, *dres;
     unsigned *mf;
@@ -546,22 +551,26 @@ int rwmd_run(Ctx &c, double *L, double *LA, double *LB) {
         if (n_dst > 0) {
             W1G_CUDA(cudaMemsetAsync(mf, 0x7f, sizeof(unsigned) * n_src, c.stream));
             W1G_TRY(rwmd_f32_min(c, F.mpts[s], n_src, F.mpts[o], n_dst, F.scale, mf, qn, tbox, c.culling));
+            T.mark(s ? "f32_b" : "f32_a");
             k_boxes64<<<grid_for((n_dst / RT + 1) * 32, 256, 8u * c.sm_count), 256, 0, c.stream>>>(F.mpts[o], n_dst, box64);
             W1G_CHECK_LAUNCH();
             k_superboxes<<<grid_for((n_dst / RT / SUP + 1) * 32, 256, 8u * c.sm_count), 256, 0, c.stream>>>(
                 box64, (n_dst + RT - 1) / RT, sbox);
             W1G_CHECK_LAUNCH();
+            T.mark("boxes");
         }
-        if (n_dst >= REFINE_WARP_MIN)
+        if (n_dst >= c.refine_warp_min)
             k_refine_w<<<(unsigned)((n_src + RW_WARPS * RW_QPW - 1) / (RW_WARPS * RW_QPW)), 32 * RW_WARPS, 0, c.stream>>>(
                 F.mpts[s], F.mpos[s], F.members[s], mass[s], n_src, mf, qn, F.unscale, F.mpts[o], n_dst, box64,
-                sbox, best, terms);
+                sbox, best, terms, c.culling | (c.debug_radius << 1));
         else
             k_refine<<<(unsigned)((n_src + RF_QPB - 1) / RF_QPB), RF_BLOCK, 0, c.stream>>>(
                 F.mpts[s], F.mpos[s], F.members[s], mass[s], n_src, mf, qn, F.unscale, F.mpts[o], n_dst, box64,
-                sbox, best, terms);
+                sbox, best, terms, c.culling | (c.debug_radius << 1));
         W1G_CHECK_LAUNCH();
+        T.mark("refine");
         W1G_TRY(pairwise_sum(c, terms, n_src, dres + s, c.scr[17], c.scr[18], c.scr[19]));
+        T.mark("sum");
     }
     double h[2];
     W1G_CUDA(cudaMemcpyAsync(h, dres, sizeof(double) * 2, cudaMemcpyDeviceToHost, c.stream));
@@ -618,14 +627,14 @@ int rwmd_range_run(Ctx &c, int side, int64_t begin, int64_t end, double *partial
             box64, (n_dst + RT - 1) / RT, sbox);
         W1G_CHECK_LAUNCH();
     }
-    if (n_dst >= REFINE_WARP_MIN)
+    if (n_dst >= c.refine_warp_min)
         k_refine_w<<<(unsigned)((n_src + RW_WARPS * RW_QPW - 1) / (RW_WARPS * RW_QPW)), 32 * RW_WARPS, 0, c.stream>>>(
             F.mpts[s], F.mpos[s], F.members[s], mass[s], n_src, mf, qn, F.unscale, F.mpts[o], n_dst, box64, sbox,
-            best, terms);
+            best, terms, c.culling | (c.debug_radius << 1));
     else
         k_refine<<<(unsigned)((n_src + RF_QPB - 1) / RF_QPB), RF_BLOCK, 0, c.stream>>>(
             F.mpts[s], F.mpos[s], F.members[s], mass[s], n_src, mf, qn, F.unscale, F.mpts[o], n_dst, box64, sbox,
-            best, terms);
+            best, terms, c.culling | (c.debug_radius << 1));
     W1G_CHECK_LAUNCH();
     W1G_TRY(pairwise_sum(c, terms + begin, n_src, dres, c.scr[17], c.scr[18], c.scr[19]));
     W1G_CUDA(cudaMemcpyAsync(partial, dres, sizeof(double), cudaMemcpyDeviceToHost, c.stream));

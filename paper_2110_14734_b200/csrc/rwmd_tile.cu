@@ -84,8 +84,10 @@ __global__ void __launch_bounds__(T_BLOCK) k_rwmd_f32(TileArgs A) {
         const bool v = i < A.nq;
         const double2 p = v ? A.q[i] : s_org;
         const float x = (float)((p.x - ox) * sc), y = (float)((p.y - oy) * sc);
-        ax[r] = make_float2(-2.f * x, -2.f * x);
-        ay[r] = make_float2(-2.f * y, -2.f * y);
+        // expanded form keeps (-2x, -2x); the direct form (culled mode) keeps (x, x)
+        const float fx = CULL ? x : -2.f * x, fy = CULL ? y : -2.f * y;
+        ax[r] = make_float2(fx, fx);
+        ay[r] = make_float2(fy, fy);
         qq[r] = fmaf(x, x, y * y);
         qn[r] = sqrtf(qq[r]);
         m[r] = INFINITY;
@@ -173,19 +175,34 @@ __global__ void __launch_bounds__(T_BLOCK) k_rwmd_f32(TileArgs A) {
                 xb = (float)((p.x - ox) * sc);
                 yb = (float)((p.y - oy) * sc);
             }
-            s_xy[j] = make_float4(xa, xb, ya, yb);
-            s_tt[j] = make_float2(fmaf(xa, xa, ya * ya), fmaf(xb, xb, yb * yb));
+            if (CULL) {
+                // direct form: targets stored negated, d = (q - t)^2 without cancellation
+                s_xy[j] = make_float4(-xa, -xb, -ya, -yb);
+            } else {
+                s_xy[j] = make_float4(xa, xb, ya, yb);
+                s_tt[j] = make_float2(fmaf(xa, xa, ya * ya), fmaf(xb, xb, yb * yb));
+            }
         }
         __syncthreads();
         const int pairs = (cnt + 1) >> 1;
 #pragma unroll 4
         for (int j = 0; j < pairs; j++) {
             const float4 v = s_xy[j];
-            const float2 tx = make_float2(v.x, v.y), ty = make_float2(v.z, v.w), tt = s_tt[j];
+            const float2 tx = make_float2(v.x, v.y), ty = make_float2(v.z, v.w);
+            if (CULL) {
 #pragma unroll
-            for (int r = 0; r < R; r++) {
-                const float2 s = __ffma2_rn(ay[r], ty, __ffma2_rn(ax[r], tx, tt));
-                m[r] = min3(m[r], s.x, s.y);
+                for (int r = 0; r < R; r++) {
+                    const float2 dx = __fadd2_rn(ax[r], tx), dy = __fadd2_rn(ay[r], ty);
+                    const float2 d = __ffma2_rn(dy, dy, __fmul2_rn(dx, dx));
+                    m[r] = min3(m[r], d.x, d.y);
+                }
+            } else {
+                const float2 tt = s_tt[j];
+#pragma unroll
+                for (int r = 0; r < R; r++) {
+                    const float2 s = __ffma2_rn(ay[r], ty, __ffma2_rn(ax[r], tx, tt));
+                    m[r] = min3(m[r], s.x, s.y);
+                }
             }
         }
         if (CULL) {
@@ -193,7 +210,7 @@ __global__ void __launch_bounds__(T_BLOCK) k_rwmd_f32(TileArgs A) {
 #pragma unroll
             for (int r = 0; r < R; r++) {
                 const int i = q0 + r * T_BLOCK + tid;
-                if (i < A.nq) ub = fmaxf(ub, upper_bound(m[r] + qq[r], qn[r]));
+                if (i < A.nq) ub = fmaxf(ub, sqrtf(m[r]) * (1.f + 0x1p-18f) + 0x1p-18f * qn[r]);
             }
             for (int o = 16; o; o >>= 1) ub = fmaxf(ub, __shfl_xor_sync(0xffffffffu, ub, o));
             if (lane == 0) s_red[wid] = ub;
@@ -208,7 +225,7 @@ __global__ void __launch_bounds__(T_BLOCK) k_rwmd_f32(TileArgs A) {
     for (int r = 0; r < R; r++) {
         const int i = q0 + r * T_BLOCK + tid;
         if (i < A.nq) {
-            const float est = fmaxf(m[r] + qq[r], 0.f);
+            const float est = CULL ? m[r] : fmaxf(m[r] + qq[r], 0.f);
             atomicMin(&A.mout[i], __float_as_uint(est));
             if (blockIdx.y == 0) A.qn_out[i] = qn[r];
         }

@@ -826,7 +826,11 @@ int tree_run(Ctx &c, const double2 *pts, int64_t n, int64_t *n_nodes, int32_t *d
         int per_sm = 0;
         W1G_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tree_coop, 256, smem));
         if (per_sm < 1) per_sm = 1;
-        if (per_sm > 2) per_sm = 2;
+        {
+            const char *e = getenv("W1G_COOP_PER_SM");
+            const int cap = e ? atoi(e) : 2;
+            if (per_sm > cap) per_sm = cap;
+        }
         const int G = per_sm * c.sm_count;
         void *args[] = {&A};
         W1G_CUDA(cudaLaunchCooperativeKernel((void *)k_tree_coop, G, 256, args, smem, c.stream));

@@ -308,7 +308,12 @@ int wspd_run(Ctx &c, double s, int reference_order, int64_t *n_pairs) {
             int per_sm = 0;
             const void *fn = ORDER ? (const void *)k_wspd_coop<true> : (const void *)k_wspd_coop<false>;
             W1G_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, 0));
-            if (per_sm > 4) per_sm = 4;
+            // fewer CTAs -> cheaper grid barriers; W1G_COOP_PER_SM overrides (tuning)
+            {
+                const char *e = getenv("W1G_COOP_PER_SM");
+                const int cap = e ? atoi(e) : 2;
+                if (per_sm > cap) per_sm = cap;
+            }
             if (per_sm >= 1) {
                 const int G = per_sm * c.sm_count;
                 int32_t *lv = reinterpret_cast<int32_t *>(ctr + 6);
