@@ -235,10 +235,12 @@ int net_run(Ctx &c, const int64_t *d_sup, int64_t n, int64_t *n_arcs) {
     const int64_t m = c.n_arcs;
     const int64_t *t = ptr<int64_t>(c.arc_t), *h = ptr<int64_t>(c.arc_h);
     const double *cs = ptr<double>(c.arc_c);
+    SubTimer T(c, "csr");
     W1G_TRY(flags_reset(c));
     k_validate<<<gs(c, m > n ? m : n), 256, 0, c.stream>>>(d_sup, n, t, h, cs, m, dflags(c));
     W1G_CHECK_LAUNCH();
     W1G_TRY(flags_fetch(c, 0, F_NSLOTS / 2));
+    T.mark("validate");
     if (c.h_pinned[F_MISC0] != 0) {
         set_error("unbalanced supplies (sum = %lld)", (long long)c.h_pinned[F_MISC0]);
         return W1G_ENETWORK;
@@ -270,12 +272,15 @@ int net_run(Ctx &c, const int64_t *d_sup, int64_t n, int64_t *n_arcs) {
         k_arc_keys<<<gs(c, m), 256, 0, c.stream>>>(t, h, m, hb, keys, vals);
         W1G_CHECK_LAUNCH();
         uint64_t *kk[1] = {keys};
+        T.mark("keys");
         W1G_TRY(radix_sort(c, kk, 1, vals, m, 2 * hb));
+        T.mark("sort");
         GroupFlag f{keys};
         W1G_TRY(scan_i64(c, f, m, excl, dflags(c) + F_TOTAL));
         k_net_emit<<<gs(c, m), 256, 0, c.stream>>>(f, m, excl, vals, t, h, cs, ot, oh, oc, rowcnt);
         W1G_CHECK_LAUNCH();
     }
+    T.mark("dedup_emit");
     // row_offsets = [0, cumsum(bincount(t, n))], network.py:84-85
     W1G_TRY(scan_i64(c, RowCount{rowcnt, n}, n + 1, ro, nullptr));
     W1G_TRY(flags_fetch(c, F_TOTAL, 1));

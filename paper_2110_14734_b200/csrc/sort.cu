@@ -21,9 +21,11 @@ namespace {
 
 constexpr int RS_BLOCK = 256;
 constexpr int RS_WARPS = RS_BLOCK / 32;
-constexpr int RS_IPT = 8;
-constexpr int RS_TILE = RS_BLOCK * RS_IPT;  // 2048
-constexpr int RS_WTILE = 32 * RS_IPT;       // items per warp
+// items per thread: 8 (2048-key tiles) in general, 32 (8192-key tiles) for
+// large inputs so the decoupled look-back chain stays short
+constexpr int RS_IPT_SMALL = 8;
+constexpr int RS_IPT_LARGE = 32;
+constexpr int64_t RS_LARGE_N = 1 << 20;
 
 struct KeyPtrs {
     uint64_t *k[4];
@@ -55,7 +57,7 @@ __device__ __forceinline__ unsigned long long st_make(unsigned epoch, unsigned l
     return ((unsigned long long)epoch << 34) | (kind << 32) | cnt;
 }
 
-template <int W, int M>
+template <int W, int M, int RS_IPT>
 __global__ void __launch_bounds__(RS_BLOCK) k_rs_onesweep(KeyPtrs src, KeyPtrs dst,
                                                           const uint32_t *__restrict__ vsrc,
                                                           uint32_t *__restrict__ vdst, int shift,
@@ -63,6 +65,8 @@ __global__ void __launch_bounds__(RS_BLOCK) k_rs_onesweep(KeyPtrs src, KeyPtrs d
                                                           unsigned long long *status, unsigned *ticket,
                                                           unsigned epoch, int64_t n) {
     constexpr int DW = W - M;  // word holding the digit; words DW..W-1 move
+    constexpr int RS_TILE = RS_BLOCK * RS_IPT;
+    constexpr int RS_WTILE = 32 * RS_IPT;  // items per warp
     extern __shared__ __align__(16) unsigned char smem[];
     uint64_t *s_key = reinterpret_cast<uint64_t *>(smem);           // M * RS_TILE
     uint32_t *s_val = reinterpret_cast<uint32_t *>(s_key + M * RS_TILE);  // RS_TILE
@@ -192,23 +196,31 @@ __global__ void __launch_bounds__(RS_BLOCK) k_rs_onesweep(KeyPtrs src, KeyPtrs d
     }
 }
 
-template <int W, int M>
+template <int W, int M, int IPT>
 int launch_pass(Ctx &c, KeyPtrs *src, KeyPtrs *dst, const uint32_t *vsrc, uint32_t *vdst, int shift,
                 const uint32_t *dhist, unsigned long long *status, unsigned *ticket, unsigned epoch,
-                int64_t n, int ntiles) {
-    const size_t sm = (size_t)RS_TILE * (8 * M + 4);
-    W1G_CUDA(cudaFuncSetAttribute(k_rs_onesweep<W, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    k_rs_onesweep<W, M><<<ntiles, RS_BLOCK, sm, c.stream>>>(*src, *dst, vsrc, vdst, shift, dhist, status,
-                                                           ticket, epoch, n);
+                int64_t n) {
+    const int64_t tile = (int64_t)RS_BLOCK * IPT;
+    const int ntiles = (int)((n + tile - 1) / tile);
+    const size_t sm = (size_t)tile * (8 * M + 4);
+    W1G_CUDA(cudaFuncSetAttribute(k_rs_onesweep<W, M, IPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    k_rs_onesweep<W, M, IPT><<<ntiles, RS_BLOCK, sm, c.stream>>>(*src, *dst, vsrc, vdst, shift, dhist, status,
+                                                                ticket, epoch, n);
     W1G_CHECK_LAUNCH();
     return W1G_OK;
 }
 
 int dispatch_pass(int W, int M, Ctx &c, KeyPtrs *src, KeyPtrs *dst, const uint32_t *vsrc, uint32_t *vdst,
                   int shift, const uint32_t *dhist, unsigned long long *status, unsigned *ticket,
-                  unsigned epoch, int64_t n, int ntiles) {
-#define RS_CASE(w, m) \
-    if (W == w && M == m) return launch_pass<w, m>(c, src, dst, vsrc, vdst, shift, dhist, status, ticket, epoch, n, ntiles);
+                  unsigned epoch, int64_t n) {
+    // large inputs: 8192-key tiles when the staged words fit in shared memory
+    const bool large = n >= RS_LARGE_N && M <= 2;
+#define RS_CASE(w, m)                                                                                          \
+    if (W == w && M == m)                                                                                      \
+        return large ? launch_pass<w, m, RS_IPT_LARGE>(c, src, dst, vsrc, vdst, shift, dhist, status, ticket,  \
+                                                       epoch, n)                                               \
+                     : launch_pass<w, m, RS_IPT_SMALL>(c, src, dst, vsrc, vdst, shift, dhist, status, ticket,  \
+                                                       epoch, n);
     RS_CASE(1, 1)
     RS_CASE(2, 2)
     RS_CASE(2, 1)
@@ -228,7 +240,8 @@ int radix_sort(Ctx &c, uint64_t **keys, int words, uint32_t *vals, int64_t n, in
         set_error("radix_sort: unsupported shape (words=%d, n=%lld)", words, (long long)n);
         return W1G_EINVAL;
     }
-    const int ntiles = (int)((n + RS_TILE - 1) / RS_TILE);
+    const int64_t small_tile = (int64_t)RS_BLOCK * RS_IPT_SMALL;
+    const int ntiles = (int)((n + small_tile - 1) / small_tile);  // upper bound for the status array
     KeyPtrs a, b;
     for (int w = 0; w < 4; w++) a.k[w] = b.k[w] = nullptr;
     for (int w = 0; w < words; w++) {
@@ -282,7 +295,7 @@ int radix_sort(Ctx &c, uint64_t **keys, int words, uint32_t *vals, int64_t n, in
         c.sort_epoch = (c.sort_epoch + 1) & 0x3fffffffu;
         if (c.sort_epoch == 0) c.sort_epoch = 1;
         W1G_TRY(dispatch_pass(words, words - w, c, src, dst, vsrc, vdst, 8 * j, hist + (w * 8 + j) * 256,
-                              status, tickets + (p & 63), c.sort_epoch, n, ntiles));
+                              status, tickets + (p & 63), c.sort_epoch, n));
         KeyPtrs *t = src;
         src = dst;
         dst = t;

@@ -639,11 +639,30 @@ __global__ void __launch_bounds__(256) k_tree_coop(CoopArgs A) {
             const int64_t base = (int64_t)t * TP_TILE + tid * TP_IPT;
             int f[TP_IPT];
             int sum = 0;
+            // the flag is a chain of four dependent loads; issue each link for all
+            // items before the next so the chains overlap instead of serialising
+            int sg[TP_IPT];
+            uint32_t el[TP_IPT];
+            SegInfo inf[TP_IPT];
+#pragma unroll
+            for (int i = 0; i < TP_IPT; i++) sg[i] = base + i < n ? A.pos_seg[cur][base + i] : -1;
 #pragma unroll
             for (int i = 0; i < TP_IPT; i++) {
-                const int64_t p = base + i;
-                f[i] = p < n ? pos_flag(p, A.pts, A.xl[cur], A.yl[cur], A.pos_seg[cur], A.info) : 0;
-                sum += f[i];
+                if (sg[i] >= 0) inf[i] = A.info[sg[i]];
+                else inf[i].axis = 0;
+            }
+#pragma unroll
+            for (int i = 0; i < TP_IPT; i++)
+                el[i] = sg[i] >= 0 ? (inf[i].axis ? A.xl[cur][base + i] : A.yl[cur][base + i]) : 0u;
+#pragma unroll
+            for (int i = 0; i < TP_IPT; i++) {
+                int v = 0;
+                if (sg[i] >= 0) {
+                    const double c = coord(A.pts, el[i], inf[i].axis);
+                    v = (inf[i].strict ? (c < inf[i].thr) : (c <= inf[i].thr)) ? 1 : 0;
+                }
+                f[i] = v;
+                sum += v;
             }
             int tot;
             int run = block_excl_scan(sum, &tot, s_warp);
@@ -671,20 +690,35 @@ __global__ void __launch_bounds__(256) k_tree_coop(CoopArgs A) {
         }
         if (blockIdx.x == 0 && tid == 0) A.cnt[(level + 2) % 3] = 0;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-            for (int i = tid; i < TP_TILE; i += 256) {
-                const int64_t p = (int64_t)t * TP_TILE + i;
-                if (p >= n) break;
-                const int s = A.pos_seg[cur][p];
-                if (s < 0) {
-                    A.pos_seg[cur ^ 1][p] = -1;
-                    continue;
+            // same staging as (B): every dependent load issued for all items at once
+            constexpr int J = TP_TILE / 256;
+            int64_t pp[J];
+            int sg[J];
+            SegInfo inf[J];
+            int32_t lp[J], ll[J];
+#pragma unroll
+            for (int j = 0; j < J; j++) {
+                pp[j] = (int64_t)t * TP_TILE + tid + 256 * j;
+                sg[j] = pp[j] < n ? A.pos_seg[cur][pp[j]] : -2;
+            }
+#pragma unroll
+            for (int j = 0; j < J; j++) {
+                if (sg[j] >= 0) {
+                    inf[j] = A.info[sg[j]];
+                    lp[j] = A.lpre[pp[j]];
                 }
-                const SegInfo in = A.info[s];
-                const int32_t lp = A.lpre[p], ll = A.lpre[in.lo];
-                const int64_t ep = (int64_t)s_tp[t] + (lp & 0x7fffffff);
-                const int64_t el = (int64_t)s_tp[in.lo / TP_TILE] + (ll & 0x7fffffff);
-                pos_scatter(p, s, (int)((uint32_t)lp >> 31), ep, el, in, A.xl[cur], A.yl[cur], A.xl[cur ^ 1],
-                            A.yl[cur ^ 1], A.pos_seg[cur ^ 1]);
+            }
+#pragma unroll
+            for (int j = 0; j < J; j++)
+                if (sg[j] >= 0) ll[j] = A.lpre[inf[j].lo];
+#pragma unroll
+            for (int j = 0; j < J; j++) {
+                if (sg[j] == -1) A.pos_seg[cur ^ 1][pp[j]] = -1;
+                if (sg[j] < 0) continue;
+                const int64_t ep = (int64_t)s_tp[t] + (lp[j] & 0x7fffffff);
+                const int64_t el = (int64_t)s_tp[inf[j].lo / TP_TILE] + (ll[j] & 0x7fffffff);
+                pos_scatter(pp[j], sg[j], (int)((uint32_t)lp[j] >> 31), ep, el, inf[j], A.xl[cur], A.yl[cur],
+                            A.xl[cur ^ 1], A.yl[cur ^ 1], A.pos_seg[cur ^ 1]);
             }
         }
         grid.sync();
@@ -767,8 +801,11 @@ int tree_run(Ctx &c, const double2 *pts, int64_t n, int64_t *n_nodes, int32_t *d
     k_presort_keys<<<g, 256, 0, c.stream>>>(pts, n, kx0, kx1, ky0, ky1, xl[0], yl[0]);
     W1G_CHECK_LAUNCH();
     // X-list by (x, y) and Y-list by (y, x): kx1 = key(x), kx0 = key(y)
+    SubTimer T(c, "tree");
     W1G_TRY(sort_lex2(c, kx1, kx0, xl[0], n));
+    T.mark("sort_x");
     W1G_TRY(sort_lex2(c, kx0, kx1, yl[0], n));
+    T.mark("sort_y");
     // level state
     Seg *seg[2];
     SegInfo *info;
@@ -867,6 +904,7 @@ int tree_run(Ctx &c, const double2 *pts, int64_t n, int64_t *n_nodes, int32_t *d
         }
         levels = level;
     }
+    T.mark("global_levels");
     // the subtrees of <= LOCAL_MAX points: one CTA each, shared-memory levels
     {
         const size_t smem = sizeof(LocalSmem);
@@ -876,6 +914,7 @@ int tree_run(Ctx &c, const double2 *pts, int64_t n, int64_t *n_nodes, int32_t *d
                                                   dflags(c));
         W1G_CHECK_LAUNCH();
     }
+    T.mark("local");
     W1G_CUDA(cudaMemcpyAsync(c.h_pinned + F_DUP, dflags(c) + F_DUP, sizeof(int64_t), cudaMemcpyDeviceToHost,
                              c.stream));
     W1G_CUDA(cudaStreamSynchronize(c.stream));
