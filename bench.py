@@ -49,6 +49,26 @@ FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # 74.4, derived nominal (no F
 N_POINTS = 100_000
 S = 1.0
 DELTA = 0.01
+NCU_SUMMARY = os.path.join(ROOT, "profiles", "r01_ncu_rwmd_tile.jsonl")
+
+
+def _ncu_traffic(kernel: str, capture: str = "prof_rwmd_all"):
+    """dram__bytes_read.sum + dram__bytes_write.sum of one launch of `kernel` at this workload,
+    from the committed `ncu --set full` capture summary (cfg2, same command as this bench)."""
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    try:
+        with open(NCU_SUMMARY) as f:
+            for line in f:
+                row = json.loads(line)
+                if row["capture"] == capture and kernel in row["Kernel Name"]:
+                    total = 0.0
+                    for key in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                        v, u = row[key].split()
+                        total += float(v) * scale[u]
+                    return int(total)
+    except (OSError, KeyError, ValueError):
+        pass
+    return None
 
 
 def parse():
@@ -286,7 +306,8 @@ def run_ours(args, dist: Dist):
     ctx.call("w1g_set_rwmd_culling", 1)
     tflops = 5.0 * evals.value / (ms.value * 1e-3) / 1e12
     roofline = {"bound": "fp32", "achieved": tflops, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
-                "frac": tflops / FP32_PEAK_TFLOPS, "traffic": None,
+                "frac": tflops / FP32_PEAK_TFLOPS, "traffic": _ncu_traffic("k_rwmd_f32<8, 0, 1024>"),
+                "traffic_unit": "bytes/launch (dram read+write, ncu --set full, profiles/r01_ncu_rwmd_tile.jsonl)",
                 "kernel": "k_rwmd_f32 (rwmd_tile.cu)",
                 "ms_per_launch": ms.value, "evals_per_launch": evals.value,
                 "note": "5 FLOP per directed (source,target) evaluation, full brute force (culling off); "
