@@ -172,7 +172,7 @@ int w1g_ctx_create(int device, w1g_ctx **out) {
     c->sm_count = prop.multiProcessorCount;
     if (const char *e = getenv("W1G_CULL_STEPS")) c->cull_steps = atoi(e) > 0 ? atoi(e) : 0;
     if (const char *e = getenv("W1G_DEBUG_RADIUS")) c->debug_radius = atoi(e) ? 1 : 0;
-    if (const char *e = getenv("W1G_REFINE_WARP_MIN")) c->refine_warp_min = atoll(e);
+    if (const char *e = getenv("W1G_HEAVY")) c->heavy_ratio = atoi(e) > 0 ? atoi(e) : 0;
     W1G_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     int64_t *f;
     W1G_TRY(ensure(c->flags, F_NSLOTS, &f));

@@ -90,7 +90,7 @@ struct Ctx {
     int culling = 1;
     int cull_steps = 0;  // 0 = by size; W1G_CULL_STEPS overrides (tuning)
     int debug_radius = 0;  // W1G_DEBUG_RADIUS=1: rwmd "best" reports the exact-pass radius
-    int64_t refine_warp_min = 300000;  // targets from which the warp-centric refine is used (W1G_REFINE_WARP_MIN)
+    int heavy_ratio = 16;  // exact pass: disc / median disc beyond which a source is searched alone (W1G_HEAVY, 0 off)
     DevBuf best[2];
     int64_t n_best[2] = {0, 0};
     int64_t rw_members[2] = {0, 0};  // A- and B-member counts of the last rwmd_run

@@ -22,7 +22,8 @@
 
 namespace w1g {
 
-int rwmd_f32_min(Ctx &c, const double2 *q, int64_t nq, const double2 *t, int64_t nt, double scale,
+int rwmd_f32_min(Ctx &c, const double2 *q, const uint64_t *qkey, int64_t nq, const double2 *t,
+                 const uint64_t *tkey, int64_t nt, double scale,
                  unsigned *mout, float *qn_out, double4 *tbox, int culling);
 int pairwise_sum(Ctx &c, const double *d_v, int64_t n, double *d_out, DevBuf &nodes_buf,
                  DevBuf &val_buf, DevBuf &lev_buf);
@@ -192,110 +193,106 @@ __device__ __forceinline__ double upper_bound(float est, float qn, int direct) {
     return direct ? upper_bound_direct(est, qn) : upper_bound_expanded(est, qn);
 }
 
-// exact fp64 refinement + mass * best (lower_bound.py:51-58), warp-centric:
-// every warp owns 16 Morton-consecutive sources (two lanes per source, each
-// taking every other target of a tile) and finds its own candidate tiles with
-// its own radius -- super-tile boxes first, then the 64 child-tile boxes of the
-// super-tiles that pass -- so one distant source never widens the search of
-// its neighbours' warps.  Targets are read straight from L1/L2 (all lanes of
-// the warp read the same tile).
-constexpr int64_t REFINE_WARP_MIN = 0;  // targets from which the warp-centric refine is used
-constexpr int RW_WARPS = 4;        // warps per CTA
-constexpr int RW_QPW = 16;         // sources per warp
-constexpr int RW_CAND = 256;       // candidate tiles per round and warp
 
-__global__ void __launch_bounds__(32 * RW_WARPS) k_refine_w(
-    const double2 *__restrict__ q, const int32_t *__restrict__ qpos, const int32_t *__restrict__ members,
-    const int64_t *__restrict__ mass, int64_t nq, const unsigned *__restrict__ mf32,
-    const float *__restrict__ qn, double unscale, const double2 *__restrict__ t, int64_t nt,
-    const double4 *__restrict__ tbox, const double4 *__restrict__ sbox, double *__restrict__ best_out,
-    double *__restrict__ terms, int direct) {
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, sub = lane & 1;
-    const int64_t i = ((int64_t)blockIdx.x * RW_WARPS + wid) * RW_QPW + (lane >> 1);
-    const bool valid = i < nq;
-    double2 p = make_double2(0, 0);
-    double diag = 0.0, r = -1.0;
-    if (valid) {
-        p = q[i];
-        diag = ddiv(fabs(dsub(p.y, p.x)), SQRT2);  // diagram.py:47
-        if (nt > 0) {
-            const double U = upper_bound(__uint_as_float(mf32[i]), qn[i], direct & 1) * unscale * (1.0 + 1e-9);
-            r = fmin(U, diag * (1.0 + 1e-12));
-            r += 0x1p-50 * (fabs(p.x) + fabs(p.y) + r) + 1e-300;
+__device__ __forceinline__ double gap2(double4 b, double4 a) {  // squared box gap, as within()
+    const double gx = fmax(0.0, fmax(b.x - a.z, a.x - b.z));
+    const double gy = fmax(0.0, fmax(b.y - a.w, a.y - b.w));
+    return gx * gx + gy * gy;
+}
+
+// Exact nearest squared distance of one source by warp-level branch and bound
+// over the tile hierarchy: the nearest super-tile first (nearest child tile
+// first inside a super-tile), every exact distance found shrinking the search
+// radius (R = sqrt(m2)(1 + 1e-9) keeps every target that could still lower
+// the min), then the remaining super-tiles against the shrunk radius.  The
+// min VALUE is all the caller needs, so skipping targets that cannot lower it
+// is exact.  All lanes return the same m2.
+__device__ double solo_nn(double2 pj, double rad, const double2 *__restrict__ t, int64_t nt,
+                          const double4 *__restrict__ tbox, const double4 *__restrict__ sbox, int64_t ntile,
+                          int64_t nsup, int lane) {
+    const double4 pb = make_double4(pj.x, pj.y, pj.x, pj.y);
+    double m2 = INFINITY, R = rad;
+    auto eval_tile = [&](int64_t k) {
+        double ma = INFINITY;
+        for (int64_t jt = k * RT + lane; jt < min(nt, (k + 1) * RT); jt += 32) {
+            const double2 ta = t[jt];
+            const double ax = dsub(pj.x, ta.x), ay = dsub(pj.y, ta.y);
+            const double da = dadd(dmul(ax, ax), dmul(ay, ay));
+            ma = da < ma ? da : ma;
         }
-    }
-    double m2 = INFINITY, m2b = INFINITY;
-    if (nt > 0) {
-        double4 qb = valid ? make_double4(p.x, p.y, p.x, p.y) : make_double4(INFINITY, INFINITY, -INFINITY, -INFINITY);
-        double rmax = r;
         for (int o = 16; o; o >>= 1) {
-            qb.x = fmin(qb.x, __shfl_xor_sync(0xffffffffu, qb.x, o));
-            qb.y = fmin(qb.y, __shfl_xor_sync(0xffffffffu, qb.y, o));
-            qb.z = fmax(qb.z, __shfl_xor_sync(0xffffffffu, qb.z, o));
-            qb.w = fmax(qb.w, __shfl_xor_sync(0xffffffffu, qb.w, o));
-            rmax = fmax(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
+            const double ot = __shfl_xor_sync(0xffffffffu, ma, o);
+            ma = ot < ma ? ot : ma;
         }
-        rmax *= 1.0 + 1e-9;
-        const double4 pb = make_double4(p.x, p.y, p.x, p.y);
-        const int64_t ntile = (nt + RT - 1) / RT;
-        const int64_t nsup = (ntile + SUP - 1) / SUP;
-        const double rr = r * (1.0 + 1e-9);
-        auto eval_tile = [&](int64_t k) {
-            {
-                const double2 *tt = t + k * RT + sub;
-                const int cnt = (int)min((int64_t)RT, nt - k * RT);
-                if (cnt == RT) {
-#pragma unroll
-                    for (int j = 0; j < RT / 2; j += 2) {
-                        const double2 ta = tt[2 * j], tb = tt[2 * j + 2];
-                        const double ax = dsub(p.x, ta.x), ay = dsub(p.y, ta.y);
-                        const double bx = dsub(p.x, tb.x), by = dsub(p.y, tb.y);
-                        const double da = dadd(dmul(ax, ax), dmul(ay, ay));
-                        const double db = dadd(dmul(bx, bx), dmul(by, by));
-                        m2 = da < m2 ? da : m2;
-                        m2b = db < m2b ? db : m2b;
-                    }
-                } else {
-                    for (int j = sub; j < cnt; j += 2) {
-                        const double2 ta = t[k * RT + j];
-                        const double ax = dsub(p.x, ta.x), ay = dsub(p.y, ta.y);
-                        const double da = dadd(dmul(ax, ax), dmul(ay, ay));
-                        m2 = da < m2 ? da : m2;
-                    }
-                }
-            }
-        };
-        // super-tiles: 32 at a time against the warp's box (cheap pre-filter),
-        // then each source tests the super-tile and its 64 child tiles against
-        // its own radius; a tile is evaluated by the warp iff some source needs it
-        for (int64_t s0 = 0; s0 < nsup; s0 += 32) {
-            const int64_t sp = s0 + lane;
-            const bool ok = sp < nsup && within(sbox[sp], qb, rmax);
-            unsigned sm = __ballot_sync(0xffffffffu, ok);
-            while (sm) {
-                const int b = __ffs(sm) - 1;
-                sm &= sm - 1;
-                const int64_t si = s0 + b;
-                if (!__any_sync(0xffffffffu, valid && within(sbox[si], pb, rr))) continue;
-                const int64_t kend = min(ntile, (si + 1) * SUP);
-                for (int64_t k = si * SUP; k < kend; k++)
-                    if (__any_sync(0xffffffffu, valid && within(tbox[k], pb, rr))) eval_tile(k);
+        ma = __shfl_sync(0xffffffffu, ma, 0);  // keep every decision warp-uniform (NaN-safe)
+        if (ma < m2) {
+            m2 = ma;
+            R = fmin(rad, sqrt(m2) * (1.0 + 1e-9) + 1e-300);
+        }
+    };
+    auto do_super = [&](int64_t si) {
+        const int64_t kend = min(ntile, (si + 1) * SUP);
+        const int64_t k1 = si * SUP + lane, k2 = k1 + 32;
+        const double g1 = k1 < kend ? gap2(tbox[k1], pb) : INFINITY;
+        const double g2 = k2 < kend ? gap2(tbox[k2], pb) : INFINITY;
+        double gm = g1 <= g2 ? g1 : g2;
+        int km = g1 <= g2 ? lane : lane + 32;
+        for (int o = 16; o; o >>= 1) {
+            const double og = __shfl_xor_sync(0xffffffffu, gm, o);
+            const int ok = __shfl_xor_sync(0xffffffffu, km, o);
+            if (og < gm || (og == gm && ok < km)) {
+                gm = og;
+                km = ok;
             }
         }
-    }
-    m2 = m2b < m2 ? m2b : m2;
-    const double other = __shfl_xor_sync(0xffffffffu, m2, 1);
-    m2 = other < m2 ? other : m2;
-    if (valid && sub == 0) {
-        double best = diag;
-        if (nt > 0) {
-            const double nnd = dsqrt(m2);
-            best = nnd < diag ? nnd : diag;  // np.minimum(nnd, diag)
+        gm = __shfl_sync(0xffffffffu, gm, 0);
+        km = __shfl_sync(0xffffffffu, km, 0);
+        if (gm <= R * R) eval_tile(si * SUP + km);
+        unsigned b1 = __ballot_sync(0xffffffffu, g1 <= R * R && lane != km);
+        unsigned b2 = __ballot_sync(0xffffffffu, g2 <= R * R && lane + 32 != km);
+        while (b1) {
+            const int l = __ffs(b1) - 1;
+            b1 &= b1 - 1;
+            if (__shfl_sync(0xffffffffu, g1, l) <= R * R) eval_tile(si * SUP + l);
         }
-        const int32_t pos = qpos[i];
-        best_out[pos] = (direct & 2) ? r : best;  // bit 1: debug, report the search radius
-        terms[pos] = dmul(__ll2double_rn(mass[members[pos]]), best);  // float64(src_mass) * best
+        while (b2) {
+            const int l = __ffs(b2) - 1;
+            b2 &= b2 - 1;
+            if (__shfl_sync(0xffffffffu, g2, l) <= R * R) eval_tile(si * SUP + 32 + l);
+        }
+    };
+    // nearest super-tile first
+    double sg = INFINITY;
+    int64_t sk = -1;
+    for (int64_t sp = lane; sp < nsup; sp += 32) {
+        const double g = gap2(sbox[sp], pb);
+        if (g < sg) {
+            sg = g;
+            sk = sp;
+        }
     }
+    for (int o = 16; o; o >>= 1) {
+        const double og = __shfl_xor_sync(0xffffffffu, sg, o);
+        const int64_t ok = __shfl_xor_sync(0xffffffffu, sk, o);
+        if (og < sg || (og == sg && ok < sk)) {
+            sg = og;
+            sk = ok;
+        }
+    }
+    sg = __shfl_sync(0xffffffffu, sg, 0);
+    sk = __shfl_sync(0xffffffffu, sk, 0);
+    if (sk >= 0 && sg <= R * R) do_super(sk);
+    for (int64_t sp0 = 0; sp0 < nsup; sp0 += 32) {
+        const int64_t sp = sp0 + lane;
+        const double g = (sp < nsup && sp != sk) ? gap2(sbox[sp], pb) : INFINITY;
+        unsigned bal = __ballot_sync(0xffffffffu, g <= R * R);
+        while (bal) {
+            const int l = __ffs(bal) - 1;
+            bal &= bal - 1;
+            if (__shfl_sync(0xffffffffu, g, l) <= R * R) do_super(sp0 + l);
+        }
+    }
+    return m2;
 }
 
 constexpr int RF_BLOCK = 128;
@@ -303,6 +300,7 @@ constexpr int RF_TPQ = 2;                     // threads per source
 constexpr int RF_QPB = RF_BLOCK / RF_TPQ;     // sources per block
 constexpr int RF_CAND = 2048;
 constexpr int RF_STAGE = 16;  // candidate tiles staged per round (16 x 64 targets, 16 KB)
+constexpr int RF_SUPCAP = 1024;  // super-tiles listed per outer round (4M targets)
 
 // exact fp64 refinement + mass * best (lower_bound.py:51-58).  Two threads per
 // source (each takes every other target of a staged tile, then a shuffle
@@ -318,14 +316,18 @@ __global__ void __launch_bounds__(RF_BLOCK) k_refine(const double2 *__restrict__
                                                      double *__restrict__ best_out, double *__restrict__ terms,
                                                      int direct) {
     __shared__ int32_t s_cand[RF_CAND];
-    __shared__ bool s_supok[RF_CAND / SUP];
+    __shared__ int32_t s_sup[RF_SUPCAP];
     __shared__ double2 s_t[RF_STAGE * RT];
     __shared__ double4 s_tb[RF_STAGE];
-    __shared__ int s_nc;
+    __shared__ int s_nc, s_nsup;
     __shared__ double s_r[RF_BLOCK / 32];
     __shared__ double4 s_box[RF_BLOCK / 32];
     __shared__ double4 s_qb;
     __shared__ double s_rmax;
+    __shared__ double2 s_p[RF_QPB];  // per-source point and search radius, for the
+    __shared__ double s_rad[RF_QPB]; // per-source candidate filter
+    __shared__ double s_solo_r[RF_QPB], s_solo_m2[RF_QPB];  // heavy sources: radius (-1: none), result
+    __shared__ int s_cursor;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, sub = tid & (RF_TPQ - 1);
     const int64_t i = (int64_t)blockIdx.x * RF_QPB + tid / RF_TPQ;
     const bool valid = i < nq;
@@ -340,10 +342,31 @@ __global__ void __launch_bounds__(RF_BLOCK) k_refine(const double2 *__restrict__
             r += 0x1p-50 * (fabs(p.x) + fabs(p.y) + r) + 1e-300;
         }
     }
+    // a disc far wider than the warp's median (a poor FP32 seed or an isolated
+    // point) would flood the block's shared search: such a source is searched
+    // alone afterwards (solo_nn) and takes no part in the block search
+    double v = (valid && r >= 0.0) ? r : INFINITY;  // warp median by a 32-wide bitonic sort
+    for (int k = 2; k <= 32; k <<= 1)
+        for (int jb = k >> 1; jb; jb >>= 1) {
+            const double o = __shfl_xor_sync(0xffffffffu, v, jb);
+            const bool up = ((lane & k) == 0) == ((lane & jb) == 0);
+            v = up ? fmin(v, o) : fmax(v, o);
+        }
+    const double wmed = __shfl_sync(0xffffffffu, v, 16);
+    const bool heavy = (direct >> 8) > 0 && valid && r >= 0.0 && r > (double)(direct >> 8) * wmed;
+    const double rh = r;
+    if (heavy) r = -1.0;  // block-search radius
+    if (sub == 0) {
+        s_p[tid / RF_TPQ] = p;
+        s_rad[tid / RF_TPQ] = (valid && r >= 0.0) ? r * (1.0 + 1e-9) : -1.0;
+        s_solo_r[tid / RF_TPQ] = heavy ? rh * (1.0 + 1e-9) : -1.0;
+    }
+    if (tid == 0) s_cursor = s_nsup = s_nc = 0;
     double m2 = INFINITY, m2b = INFINITY;
     if (nt > 0) {
         // block bbox and radius
-        double4 b = valid ? make_double4(p.x, p.y, p.x, p.y) : make_double4(INFINITY, INFINITY, -INFINITY, -INFINITY);
+        double4 b = (valid && !heavy) ? make_double4(p.x, p.y, p.x, p.y)
+                                      : make_double4(INFINITY, INFINITY, -INFINITY, -INFINITY);
         double rm = r;
         for (int o = 16; o; o >>= 1) {
             b.x = fmin(b.x, __shfl_xor_sync(0xffffffffu, b.x, o));
@@ -377,16 +400,37 @@ __global__ void __launch_bounds__(RF_BLOCK) k_refine(const double2 *__restrict__
         const int64_t ntile = (nt + RT - 1) / RT;
         const int64_t nsup = (ntile + SUP - 1) / SUP;
         constexpr int SUP_ROUND = RF_CAND / SUP;  // super-tiles per round: <= RF_CAND child tiles
-        for (int64_t s0 = 0; s0 < nsup; s0 += SUP_ROUND) {
-            // two-level candidate search: super-tile boxes, then the child tiles
-            // of the super-tiles that pass (box tests in fp64 with slack)
-            if (tid == 0) s_nc = 0;
-            if (tid < SUP_ROUND) s_supok[tid] = (s0 + tid < nsup) && within(sbox[s0 + tid], qb, rmax);
-            __syncthreads();
-            for (int e = tid; e < SUP_ROUND * SUP; e += RF_BLOCK) {
-                if (!s_supok[e / SUP]) continue;
-                const int64_t k = s0 * SUP + e;
-                if (k < ntile && within(tbox[k], qb, rmax)) s_cand[atomicAdd(&s_nc, 1)] = (int32_t)k;
+        // two-level candidate search: the super-tiles meeting the block are
+        // listed once, then their child tiles are tested SUP_ROUND super-tiles
+        // at a time (box tests in fp64 with slack)
+        for (int64_t sb = 0; sb < nsup; sb += RF_SUPCAP) {
+          for (int64_t sp = sb + tid; sp < min(nsup, sb + RF_SUPCAP); sp += RF_BLOCK)
+            if (within(sbox[sp], qb, rmax)) s_sup[atomicAdd(&s_nsup, 1)] = (int32_t)sp;
+          __syncthreads();
+          const int n_sup = s_nsup;
+          for (int u0 = 0; u0 < n_sup; u0 += SUP_ROUND) {
+            const int nsr = min(SUP_ROUND, n_sup - u0);
+            // a tile is staged iff some source of the block needs it: the block box
+            // first, then the warp boxes, then the warp's sources one by one (the
+            // same test the evaluation uses) -- a Morton block straddling a jump
+            // has a huge box but only a handful of tiles its sources need
+            for (int e = tid; e < nsr * SUP; e += RF_BLOCK) {
+                const int64_t k = (int64_t)s_sup[u0 + e / SUP] * SUP + (e % SUP);
+                if (k >= ntile) continue;
+                const double4 tb = tbox[k];
+                if (!within(tb, qb, rmax)) continue;
+                bool need = false;
+                for (int w = 0; w < RF_BLOCK / 32 && !need; w++) {
+                    if (!within(tb, s_box[w], s_r[w] * (1.0 + 1e-9))) continue;
+                    for (int j = w * (32 / RF_TPQ); j < (w + 1) * (32 / RF_TPQ); j++) {
+                        const double2 pj = s_p[j];
+                        if (within(tb, make_double4(pj.x, pj.y, pj.x, pj.y), s_rad[j])) {
+                            need = true;
+                            break;
+                        }
+                    }
+                }
+                if (need) s_cand[atomicAdd(&s_nc, 1)] = (int32_t)k;
             }
             __syncthreads();
             const int nc = s_nc;
@@ -419,7 +463,24 @@ __global__ void __launch_bounds__(RF_BLOCK) k_refine(const double2 *__restrict__
                 }
                 __syncthreads();
             }
+            if (tid == 0) s_nc = 0;
+            __syncthreads();
+          }
+          if (tid == 0) s_nsup = 0;
+          __syncthreads();
         }
+        // heavy sources: one warp each, taken dynamically
+        for (;;) {
+            int j = 0;
+            if (lane == 0) j = atomicAdd(&s_cursor, 1);
+            j = __shfl_sync(0xffffffffu, j, 0);
+            if (j >= RF_QPB) break;
+            if (s_solo_r[j] < 0.0) continue;  // warp-uniform
+            const double ms = solo_nn(s_p[j], s_solo_r[j], t, nt, tbox, sbox, ntile, nsup, lane);
+            if (lane == 0) s_solo_m2[j] = ms;
+        }
+        __syncthreads();
+        if (heavy) m2 = fmin(m2, s_solo_m2[tid / RF_TPQ]);
     }
     m2 = m2b < m2 ? m2b : m2;
     const double other = __shfl_xor_sync(0xffffffffu, m2, 1);
@@ -431,12 +492,24 @@ __global__ void __launch_bounds__(RF_BLOCK) k_refine(const double2 *__restrict__
             best = nnd < diag ? nnd : diag;  // np.minimum(nnd, diag)
         }
         const int32_t pos = qpos[i];
-        best_out[pos] = (direct & 2) ? r : best;  // bit 1: debug, report the search radius
+        best_out[pos] = (direct & 2) ? rh : best;  // bit 1: debug, report the search radius
         terms[pos] = dmul(__ll2double_rn(mass[members[pos]]), best);  // float64(src_mass) * best
     }
 }
-
 }  // namespace
+
+// the exact pass for one direction
+static int launch_refine(Ctx &c, const double2 *q, const int32_t *qpos, const int32_t *members,
+                         const int64_t *mass, int64_t nq, const unsigned *mf, const float *qn, double unscale,
+                         const double2 *t, int64_t nt, const double4 *tbox, const double4 *sbox, double *best,
+                         double *terms) {
+    // bit 0 culled (direct-form bound), bit 1 debug, bits 8+ heavy ratio (0: off)
+    const int flags = c.culling | (c.debug_radius << 1) | (c.heavy_ratio << 8);
+    k_refine<<<(unsigned)((nq + RF_QPB - 1) / RF_QPB), RF_BLOCK, 0, c.stream>>>(
+        q, qpos, members, mass, nq, mf, qn, unscale, t, nt, tbox, sbox, best, terms, flags);
+    W1G_CHECK_LAUNCH();
+    return W1G_OK;
+}
 
 static inline double key_to_double(uint64_t k) {
     uint64_t b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
@@ -452,6 +525,7 @@ struct RwmdFrame {
     int32_t *members[2];
     double2 *mpts[2];  // member points in Morton order
     int32_t *mpos[2];  // member position (node order) of each Morton slot
+    uint64_t *mkey[2]; // sorted Morton keys (seed the culled FP32 pass)
 };
 
 // range_side >= 0 restricts that side's SOURCE list to member positions
@@ -497,7 +571,8 @@ static int rwmd_prepare(Ctx &c, RwmdFrame &F, int range_side = -1, int64_t begin
         const int64_t n = s == range_side ? end - begin : F.nm[s];
         uint64_t *key;
         uint32_t *perm;
-        W1G_TRY(ensure(c.scr[0], (size_t)n + 1, &key));
+        W1G_TRY(ensure(c.scr[s == 0 ? 0 : 22], (size_t)n + 1, &key));
+        F.mkey[s] = key;
         W1G_TRY(ensure(c.scr[2], (size_t)n + 1, &perm));
         W1G_TRY(ensure(c.scr[7 + 2 * s], (size_t)n + 1, &F.mpts[s]));
         W1G_TRY(ensure(c.scr[8 + 2 * s], (size_t)n + 1, &F.mpos[s]));
@@ -550,7 +625,7 @@ int rwmd_run(Ctx &c, double *L, double *LA, double *LB) {
         }
         if (n_dst > 0) {
             W1G_CUDA(cudaMemsetAsync(mf, 0x7f, sizeof(unsigned) * n_src, c.stream));
-            W1G_TRY(rwmd_f32_min(c, F.mpts[s], n_src, F.mpts[o], n_dst, F.scale, mf, qn, tbox, c.culling));
+            W1G_TRY(rwmd_f32_min(c, F.mpts[s], F.mkey[s], n_src, F.mpts[o], F.mkey[o], n_dst, F.scale, mf, qn, tbox, c.culling));
             T.mark(s ? "f32_b" : "f32_a");
             k_boxes64<<<grid_for((n_dst / RT + 1) * 32, 256, 8u * c.sm_count), 256, 0, c.stream>>>(F.mpts[o], n_dst, box64);
             W1G_CHECK_LAUNCH();
@@ -559,15 +634,8 @@ int rwmd_run(Ctx &c, double *L, double *LA, double *LB) {
             W1G_CHECK_LAUNCH();
             T.mark("boxes");
         }
-        if (n_dst >= c.refine_warp_min)
-            k_refine_w<<<(unsigned)((n_src + RW_WARPS * RW_QPW - 1) / (RW_WARPS * RW_QPW)), 32 * RW_WARPS, 0, c.stream>>>(
-                F.mpts[s], F.mpos[s], F.members[s], mass[s], n_src, mf, qn, F.unscale, F.mpts[o], n_dst, box64,
-                sbox, best, terms, c.culling | (c.debug_radius << 1));
-        else
-            k_refine<<<(unsigned)((n_src + RF_QPB - 1) / RF_QPB), RF_BLOCK, 0, c.stream>>>(
-                F.mpts[s], F.mpos[s], F.members[s], mass[s], n_src, mf, qn, F.unscale, F.mpts[o], n_dst, box64,
-                sbox, best, terms, c.culling | (c.debug_radius << 1));
-        W1G_CHECK_LAUNCH();
+        W1G_TRY(launch_refine(c, F.mpts[s], F.mpos[s], F.members[s], mass[s], n_src, mf, qn, F.unscale, F.mpts[o],
+                              n_dst, box64, sbox, best, terms));
         T.mark("refine");
         W1G_TRY(pairwise_sum(c, terms, n_src, dres + s, c.scr[17], c.scr[18], c.scr[19]));
         T.mark("sum");
@@ -620,22 +688,15 @@ int rwmd_range_run(Ctx &c, int side, int64_t begin, int64_t end, double *partial
     W1G_TRY(ensure(c.best[s], (size_t)F.nm[s] + 1, &best));
     if (n_dst > 0) {
         W1G_CUDA(cudaMemsetAsync(mf, 0x7f, sizeof(unsigned) * n_src, c.stream));
-        W1G_TRY(rwmd_f32_min(c, F.mpts[s], n_src, F.mpts[o], n_dst, F.scale, mf, qn, tbox, c.culling));
+        W1G_TRY(rwmd_f32_min(c, F.mpts[s], F.mkey[s], n_src, F.mpts[o], F.mkey[o], n_dst, F.scale, mf, qn, tbox, c.culling));
         k_boxes64<<<grid_for((n_dst / RT + 1) * 32, 256, 8u * c.sm_count), 256, 0, c.stream>>>(F.mpts[o], n_dst, box64);
         W1G_CHECK_LAUNCH();
         k_superboxes<<<grid_for((n_dst / RT / SUP + 1) * 32, 256, 8u * c.sm_count), 256, 0, c.stream>>>(
             box64, (n_dst + RT - 1) / RT, sbox);
         W1G_CHECK_LAUNCH();
     }
-    if (n_dst >= c.refine_warp_min)
-        k_refine_w<<<(unsigned)((n_src + RW_WARPS * RW_QPW - 1) / (RW_WARPS * RW_QPW)), 32 * RW_WARPS, 0, c.stream>>>(
-            F.mpts[s], F.mpos[s], F.members[s], mass[s], n_src, mf, qn, F.unscale, F.mpts[o], n_dst, box64, sbox,
-            best, terms, c.culling | (c.debug_radius << 1));
-    else
-        k_refine<<<(unsigned)((n_src + RF_QPB - 1) / RF_QPB), RF_BLOCK, 0, c.stream>>>(
-            F.mpts[s], F.mpos[s], F.members[s], mass[s], n_src, mf, qn, F.unscale, F.mpts[o], n_dst, box64, sbox,
-            best, terms, c.culling | (c.debug_radius << 1));
-    W1G_CHECK_LAUNCH();
+    W1G_TRY(launch_refine(c, F.mpts[s], F.mpos[s], F.members[s], mass[s], n_src, mf, qn, F.unscale, F.mpts[o], n_dst,
+                          box64, sbox, best, terms));
     W1G_TRY(pairwise_sum(c, terms + begin, n_src, dres, c.scr[17], c.scr[18], c.scr[19]));
     W1G_CUDA(cudaMemcpyAsync(partial, dres, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
     W1G_CUDA(cudaStreamSynchronize(c.stream));
@@ -660,8 +721,8 @@ int rwmd_tile_profile(Ctx &c, int reps, float *ms, int64_t *evals) {
     W1G_TRY(ensure(c.scr[15], (size_t)mx / 64 + 2, &tbox));  // per-tile boxes (tiles >= 64 targets)
     W1G_CUDA(cudaEventRecord(c.ev[8], c.stream));
     for (int r = 0; r < reps; r++) {
-        W1G_TRY(rwmd_f32_min(c, F.mpts[0], na, F.mpts[1], nb, F.scale, mf, qn, tbox, c.culling));
-        W1G_TRY(rwmd_f32_min(c, F.mpts[1], nb, F.mpts[0], na, F.scale, mf, qn, tbox, c.culling));
+        W1G_TRY(rwmd_f32_min(c, F.mpts[0], F.mkey[0], na, F.mpts[1], F.mkey[1], nb, F.scale, mf, qn, tbox, c.culling));
+        W1G_TRY(rwmd_f32_min(c, F.mpts[1], F.mkey[1], nb, F.mpts[0], F.mkey[0], na, F.scale, mf, qn, tbox, c.culling));
     }
     W1G_CUDA(cudaEventRecord(c.ev[9], c.stream));
     W1G_CUDA(cudaEventSynchronize(c.ev[9]));

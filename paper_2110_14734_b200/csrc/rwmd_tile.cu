@@ -22,9 +22,11 @@
 //    merge with an order-independent atomicMin on the float bits;
 //  * culled mode (the production path): any real target's distance is a
 //    valid upper bound for the exact pass, so each CTA only evaluates the
-//    Morton-nearest target tiles (walking outward from its own position,
-//    5 tiles, or 17 for large target sets) and skips tiles whose bbox is
-//    farther than the CTA's current worst upper bound.
+//    Morton-nearest target tiles (walking 5 tiles outward from the tile
+//    holding its middle source's Morton key, found by a warp-wide 32-ary
+//    search of the target keys) and skips tiles whose bbox is farther than
+//    the CTA's current worst upper bound; sources whose seed stays poor are
+//    searched alone by the exact pass (rwmd.cu, solo_nn).
 //
 // The result only sizes the exact fp64 search in rwmd.cu.  This translation
 // unit is compiled with FMA contraction allowed.
@@ -55,6 +57,8 @@ struct TileArgs {
     const double2 *q;       // sources (Morton order), original coordinates
     const double2 *t;       // targets (Morton order)
     const double4 *tbox;    // per T_TS-tile bbox of the targets (culled mode)
+    const uint64_t *qkey;   // sorted Morton keys of the sources / targets (culled mode)
+    const uint64_t *tkey;
     int nq, nt;
     double scale;           // 2^-e
     unsigned *mout;         // min d^2 estimate (float bits), scaled units
@@ -115,6 +119,26 @@ __global__ void __launch_bounds__(T_BLOCK) k_rwmd_f32(TileArgs A) {
             s_b[3][wid] = by1;
         }
         __syncthreads();
+        __shared__ int s_center;
+        if (wid == 0) {
+            // start at the target tile holding the Morton key of the CTA's middle
+            // source: warp-wide 32-ary search for the first target key >= it
+            const uint64_t key = A.qkey[min(q0 + T_BLOCK * R / 2, A.nq - 1)];
+            int lo = 0, hi = A.nt;  // answer in [lo, hi]
+            while (hi - lo > 32) {
+                const int step = (hi - lo + 31) / 32;
+                const int idx = lo + (lane + 1) * step - 1;
+                const bool less = idx < hi && A.tkey[idx] < key;
+                const int cnt = __popc(__ballot_sync(0xffffffffu, less));
+                const int nlo = lo + cnt * step;
+                hi = min(hi, lo + (cnt + 1) * step - 1);
+                lo = nlo;
+            }
+            const int idx = lo + lane;
+            const bool less = idx < hi && A.tkey[idx] < key;
+            const int pos = lo + __popc(__ballot_sync(0xffffffffu, less));
+            if (lane == 0) s_center = pos;
+        }
         if (tid == 0) {
             double4 b = make_double4(INFINITY, INFINITY, -INFINITY, -INFINITY);
             for (int w = 0; w < T_BLOCK / 32; w++) {
@@ -128,9 +152,7 @@ __global__ void __launch_bounds__(T_BLOCK) k_rwmd_f32(TileArgs A) {
         __syncthreads();  // every thread must see s_qbox: skip decisions are CTA-uniform
         n_tiles = (A.nt + T_TS - 1) / T_TS;
         t_first = 0;
-        // start at the target tile whose Morton range meets this source block:
-        // sources and targets share one Morton frame, so proportional position is a good guess
-        center = (int)(((long long)q0 * n_tiles) / (A.nq > 0 ? A.nq : 1));
+        center = s_center / T_TS;
         if (center >= n_tiles) center = n_tiles - 1;
     } else {
         const int tb = blockIdx.y * A.chunk;
@@ -261,21 +283,24 @@ __global__ void k_tile_boxes(const double2 *t, int nt, int T_TS, double4 *box) {
 // FP32 pass for one direction: sources q (nq, Morton order) against targets t
 // (nt, Morton order).  mout (float bits, pre-set to +huge) receives the
 // scaled squared-distance estimate, qn_out the local radius |q'|.
-int rwmd_f32_min(Ctx &c, const double2 *q, int64_t nq, const double2 *t, int64_t nt, double scale,
-                 unsigned *mout, float *qn_out, double4 *tbox, int culling) {
+int rwmd_f32_min(Ctx &c, const double2 *q, const uint64_t *qkey, int64_t nq, const double2 *t,
+                 const uint64_t *tkey, int64_t nt, double scale, unsigned *mout, float *qn_out, double4 *tbox,
+                 int culling) {
     if (nq == 0 || nt == 0) return W1G_OK;
     TileArgs A;
     A.q = q;
     A.t = t;
     A.tbox = tbox;
+    A.qkey = qkey;
+    A.tkey = tkey;
     A.nq = (int)nq;
     A.nt = (int)nt;
     A.scale = scale;
     A.mout = mout;
     A.qn_out = qn_out;
-    // tiles walked per CTA in culled mode: more for large target sets, where
-    // Morton-order jumps make the nearest tiles a poorer seed (measured)
-    A.cull_steps = c.cull_steps > 0 ? c.cull_steps : (nt >= 300000 ? 17 : 5);
+    // tiles walked per CTA in culled mode (measured: 3 already seeds cfg2 and
+    // 1M points tightly, 1-2 do not; 5 leaves a margin)
+    A.cull_steps = c.cull_steps > 0 ? c.cull_steps : 5;
     if (culling) {
         const int ntile = (int)((nt + TS_CULL - 1) / TS_CULL);
         k_tile_boxes<<<grid_for((int64_t)ntile * 32, 256, 8u * c.sm_count), 256, 0, c.stream>>>(t, (int)nt, TS_CULL, tbox);
