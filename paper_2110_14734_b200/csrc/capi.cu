@@ -3,6 +3,8 @@
 // units.  Each entry point cites the reference function it replaces.
 #include <cstdarg>
 #include <cstring>
+#include <string>
+#include <thread>
 
 #include "common.cuh"
 
@@ -173,6 +175,7 @@ int w1g_ctx_create(int device, w1g_ctx **out) {
     if (const char *e = getenv("W1G_CULL_STEPS")) c->cull_steps = atoi(e) > 0 ? atoi(e) : 0;
     if (const char *e = getenv("W1G_DEBUG_RADIUS")) c->debug_radius = atoi(e) ? 1 : 0;
     if (const char *e = getenv("W1G_HEAVY")) c->heavy_ratio = atoi(e) > 0 ? atoi(e) : 0;
+    if (const char *e = getenv("W1G_OVERLAP")) c->overlap = atoi(e) > 0 ? atoi(e) : 0;
     W1G_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     int64_t *f;
     W1G_TRY(ensure(c->flags, F_NSLOTS, &f));
@@ -186,6 +189,11 @@ int w1g_ctx_destroy(w1g_ctx *c) {
     if (!c) return W1G_OK;
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
+    if (c->aux) {
+        c->aux->nodes[0] = NodeSet{};  // aliases this context's nodes0: not owned
+        w1g_ctx_destroy(static_cast<w1g_ctx *>(c->aux));
+        c->aux = nullptr;
+    }
     DevBuf *bufs[] = {&c->in_pts, &c->best[0], &c->best[1], &c->tree_pts, &c->t_left, &c->t_right,
                       &c->t_rep, &c->t_size, &c->t_bbox, &c->t_geom, &c->t_lr, &c->t_rep32,
                       &c->pair_uv, &c->pair_w, &c->pair_path, &c->pair_idx, &c->pair_counts,
@@ -198,8 +206,10 @@ int w1g_ctx_destroy(w1g_ctx *c) {
         free_buf(ns.bm);
     }
     for (auto &b : c->scr) free_buf(b);
-    for (auto &b : c->sort_scr) free_buf(b);
-    for (auto &b : c->lex_scr) free_buf(b);
+    for (auto &job : c->sort_scr)
+        for (auto &b : job) free_buf(b);
+    for (auto &job : c->lex_scr)
+        for (auto &b : job) free_buf(b);
     if (c->h_pinned) cudaFreeHost(c->h_pinned);
     if (c->h_stage) cudaFreeHost(c->h_stage);
     for (auto &e : c->ev)
@@ -589,54 +599,103 @@ int w1g_front_end_device(w1g_ctx *c, const double *d_a, int64_t na, const double
         W1G_CUDA(cudaStreamSynchronize(c->stream));
         return W1G_OK;
     }
-    double L, LA, LB;
-    W1G_TRY(rwmd_run(*c, &L, &LA, &LB));
-    W1G_CUDA(cudaEventRecord(ev[2], c->stream));
-    info->lower_bound = L;
-    info->lower_bound_a = LA;
-    info->lower_bound_b = LB;
     // pipeline.py:67-69, condensation.py:47-59 (same IEEE operation order as the Python)
     const double eps_c = s >= 12 ? 8.0 / (s - 4.0) : 1.0;
     info->epsilon_condense = eps_c;
-    double d = 0.0;
-    if (use_condensation && L > 0.0) {
+    // With a fixed delta, L only feeds the diagnostics and the `L > 0` test of
+    // pipeline.py:115, so RWMD runs on the auxiliary context concurrently with
+    // emit + assemble, the back end speculating L > 0 (redone with delta = 0 in
+    // the rare case L == 0).
+    const bool overlap = c->overlap && use_condensation && delta_mode != 0 && delta > 0.0;
+    double L = 0.0, LA = 0.0, LB = 0.0;
+    if (!overlap) W1G_TRY(rwmd_run(*c, &L, &LA, &LB));
+    W1G_CUDA(cudaEventRecord(ev[2], c->stream));
+    std::thread worker;
+    int rc_aux = W1G_OK;
+    std::string err_aux;
+    auto start_rwmd = [&]() -> int {
+        if (!c->aux) {
+            w1g_ctx *x = nullptr;
+            W1G_TRY(w1g_ctx_create(c->device, &x));
+            c->aux = x;
+        }
+        Ctx *x = c->aux;
+        x->culling = c->culling;
+        x->cull_steps = c->cull_steps;
+        x->heavy_ratio = c->heavy_ratio;
+        x->nodes[0] = c->nodes[0];  // alias (read only; nothing downstream rewrites nodes0)
+        W1G_CUDA(cudaEventRecord(c->ev[8], c->stream));  // nodes0 complete on the main stream
+        W1G_CUDA(cudaStreamWaitEvent(x->stream, c->ev[8], 0));
+        worker = std::thread([&, x]() {
+            cudaSetDevice(x->device);
+            cudaEventRecord(x->ev[0], x->stream);
+            rc_aux = rwmd_run(*x, &L, &LA, &LB);
+            if (rc_aux == W1G_OK) rc_aux = cudaEventRecord(x->ev[1], x->stream) == cudaSuccess ? W1G_OK : W1G_ECUDA;
+            if (rc_aux != W1G_OK) err_aux = g_err;
+        });
+        return W1G_OK;
+    };
+    auto back_end = [&](double d, bool spawn) -> int {
+        info->delta = d;
+        if (spawn && c->overlap == 2) W1G_TRY(start_rwmd());
+        int64_t kk;
+        const double pitch = k * d;
+        const double half_width = (1.0 - k) * d / 2.0;
+        W1G_TRY(dc_run(*c, d > 0.0 ? d : 0.0, pitch, half_width, seed, &kk));
+        W1G_CUDA(cudaEventRecord(ev[3], c->stream));
+        info->n_points = kk;
+        int64_t nn;
+        int32_t depth;
+        W1G_TRY(tree_run(*c, ptr<double2>(c->nodes[1].pts), kk, &nn, &depth));
+        W1G_CUDA(cudaEventRecord(ev[4], c->stream));
+        info->n_tree_nodes = nn;
+        info->tree_depth = depth;
+        int64_t P;
+        W1G_TRY(wspd_run(*c, s, 0, &P));
+        W1G_CUDA(cudaEventRecord(ev[5], c->stream));
+        info->n_pairs = P;
+        info->n_levels_wspd = c->wspd_levels;
+        // RWMD joins here: emit and assemble have no cooperative (grid-synchronised) kernels
+        if (spawn && c->overlap != 2) W1G_TRY(start_rwmd());
+        int64_t M;
+        W1G_TRY(emit_run(*c, &M));
+        W1G_CUDA(cudaEventRecord(ev[6], c->stream));
+        int64_t *dsup, nsup, mm;
+        W1G_TRY(assemble_supplies(*c, &dsup, &nsup));
+        W1G_TRY(net_run(*c, dsup, nsup, &mm));
+        W1G_CUDA(cudaEventRecord(ev[7], c->stream));
+        info->n_arcs = mm;
+        info->node_count = nsup;
+        return W1G_OK;
+    };
+    auto delta_for = [&](double lower) {
+        if (!(use_condensation && lower > 0.0)) return 0.0;
         if (delta_mode == 0) {
             const double n_points = (double)(na + nb);
-            d = 2.0 * eps_c * L / (SQRT2 * n_points);
-        } else {
-            d = delta;
+            return 2.0 * eps_c * lower / (SQRT2 * n_points);
         }
+        return delta;
+    };
+    int rc = back_end(overlap ? delta : delta_for(L), overlap);
+    if (worker.joinable()) worker.join();
+    if (overlap && c->aux) c->aux->nodes[0] = NodeSet{};
+    if (rc != W1G_OK) return rc;
+    if (rc_aux != W1G_OK) {
+        set_error("%s", err_aux.c_str());
+        return rc_aux;
     }
-    info->delta = d;
-    int64_t kk;
-    const double pitch = k * d;
-    const double half_width = (1.0 - k) * d / 2.0;
-    W1G_TRY(dc_run(*c, d > 0.0 ? d : 0.0, pitch, half_width, seed, &kk));
-    W1G_CUDA(cudaEventRecord(ev[3], c->stream));
-    info->n_points = kk;
-    int64_t nn;
-    int32_t depth;
-    W1G_TRY(tree_run(*c, ptr<double2>(c->nodes[1].pts), kk, &nn, &depth));
-    W1G_CUDA(cudaEventRecord(ev[4], c->stream));
-    info->n_tree_nodes = nn;
-    info->tree_depth = depth;
-    int64_t P;
-    W1G_TRY(wspd_run(*c, s, 0, &P));
-    W1G_CUDA(cudaEventRecord(ev[5], c->stream));
-    info->n_pairs = P;
-    info->n_levels_wspd = c->wspd_levels;
-    int64_t M;
-    W1G_TRY(emit_run(*c, &M));
-    W1G_CUDA(cudaEventRecord(ev[6], c->stream));
-    int64_t *dsup, nsup, mm;
-    W1G_TRY(assemble_supplies(*c, &dsup, &nsup));
-    W1G_TRY(net_run(*c, dsup, nsup, &mm));
-    W1G_CUDA(cudaEventRecord(ev[7], c->stream));
-    W1G_CUDA(cudaEventSynchronize(ev[7]));
-    info->n_arcs = mm;
-    info->node_count = nsup;
+    if (overlap) {
+        W1G_CUDA(cudaStreamWaitEvent(c->stream, c->aux->ev[1], 0));
+        if (!(L > 0.0)) W1G_TRY(back_end(0.0, false));  // pipeline.py:115: no condensation when L == 0
+    }
+    info->lower_bound = L;
+    info->lower_bound_a = LA;
+    info->lower_bound_b = LB;
+    W1G_CUDA(cudaEventRecord(ev[9], c->stream));  // everything, RWMD included, is done
+    W1G_CUDA(cudaEventSynchronize(ev[9]));
     for (int i = 0; i < 7; i++) W1G_CUDA(cudaEventElapsedTime(&info->stage_ms[i], ev[i], ev[i + 1]));
-    W1G_CUDA(cudaEventElapsedTime(&info->stage_ms[7], ev[0], ev[7]));
+    if (overlap) W1G_CUDA(cudaEventElapsedTime(&info->stage_ms[1], c->aux->ev[0], c->aux->ev[1]));
+    W1G_CUDA(cudaEventElapsedTime(&info->stage_ms[7], ev[0], ev[9]));
     return W1G_OK;
 }
 

@@ -129,8 +129,8 @@ struct Ctx {
 
     // scratch
     DevBuf scr[SCR_N];
-    DevBuf sort_scr[8];
-    DevBuf lex_scr[6];  // sort_lex2 scratch
+    DevBuf sort_scr[2][8];  // radix sort scratch per job
+    DevBuf lex_scr[2][6];   // sort_lex2 scratch per job
     unsigned sort_epoch = 0;  // onesweep status-word epoch (sort.cu)
     DevBuf scan_state;
     DevBuf flags;  // small device flag block (int64 x 64)
@@ -139,6 +139,12 @@ struct Ctx {
     size_t h_stage_cap = 0;
 
     cudaEvent_t ev[16] = {};
+
+    // fixed-delta front end: RWMD (which then only feeds diagnostics and the
+    // L > 0 test) runs on a second context -- own stream, scratch and host
+    // thread -- concurrently with emit + assemble (W1G_OVERLAP=0 disables)
+    int overlap = 1;
+    Ctx *aux = nullptr;
 };
 
 // device flag block layout (int64 slots)
@@ -314,11 +320,26 @@ int scan_i64(Ctx &c, F f, int64_t n, int64_t *out, int64_t *total, const int32_t
 // digit histogram per sort).  bits_hint limits the digits considered in the
 // most-significant word (64 = all).
 int radix_sort(Ctx &c, uint64_t **keys, int words, uint32_t *vals, int64_t n, int top_bits = 64);
+// Up to two independent sorts of the same shape in the same launches (one
+// histogram D2H, each pass one kernel over the tiles of both): small sorts
+// that would each leave most SMs idle run side by side.
+struct SortJob {
+    uint64_t *keys[3];
+    uint32_t *vals;
+    int64_t n;
+};
+int radix_sort_multi(Ctx &c, const SortJob *jobs, int njobs, int words, int top_bits = 64);
 // Stable sort of vals (initially the element ids 0..n-1, or any payload that
 // indexes `secondary`) by (primary[i], secondary[vals[i]]): radix sort by the
 // primary word, then only the elements of primary-tie runs by both words.
 // `primary` is indexed by position in the input order, `secondary` by payload.
 int sort_lex2(Ctx &c, const uint64_t *primary, const uint64_t *secondary, uint32_t *vals, int64_t n);
+struct Lex2Job {
+    const uint64_t *primary, *secondary;
+    uint32_t *vals;
+    int64_t n;
+};
+int sort_lex2_multi(Ctx &c, const Lex2Job *jobs, int njobs);
 
 // ------------------------------------------------------------------ misc
 inline unsigned grid_for(int64_t n, int block, unsigned cap = 0x7fffffffu) {

@@ -566,23 +566,30 @@ static int rwmd_prepare(Ctx &c, RwmdFrame &F, int range_side = -1, int64_t begin
     F.unscale = std::ldexp(1.0, e);
     const double ext = H > 0.0 && std::isfinite(H) ? H : 1.0;
     const double inv = 65535.0 / ext;
+    SortJob jobs[2];
+    int64_t off[2];
     for (int s = 0; s < 2; s++) {
-        const int64_t off = s == range_side ? begin : 0;
+        off[s] = s == range_side ? begin : 0;
         const int64_t n = s == range_side ? end - begin : F.nm[s];
         uint64_t *key;
         uint32_t *perm;
         W1G_TRY(ensure(c.scr[s == 0 ? 0 : 22], (size_t)n + 1, &key));
-        F.mkey[s] = key;
-        W1G_TRY(ensure(c.scr[2], (size_t)n + 1, &perm));
+        W1G_TRY(ensure(c.scr[s == 0 ? 2 : 23], (size_t)n + 1, &perm));
         W1G_TRY(ensure(c.scr[7 + 2 * s], (size_t)n + 1, &F.mpts[s]));
         W1G_TRY(ensure(c.scr[8 + 2 * s], (size_t)n + 1, &F.mpos[s]));
+        F.mkey[s] = key;
+        jobs[s] = SortJob{{key, nullptr, nullptr}, perm, n};
         if (n == 0) continue;
-        const unsigned gn = grid_for(n, 256, 8u * c.sm_count);
-        k_morton<<<gn, 256, 0, c.stream>>>(pts, F.members[s] + off, n, xmin, ymin, inv, key, perm);
+        k_morton<<<grid_for(n, 256, 8u * c.sm_count), 256, 0, c.stream>>>(pts, F.members[s] + off[s], n, xmin, ymin,
+                                                                          inv, key, perm);
         W1G_CHECK_LAUNCH();
-        uint64_t *keys[1] = {key};
-        W1G_TRY(radix_sort(c, keys, 1, perm, n, 32));
-        k_gather_members<<<gn, 256, 0, c.stream>>>(pts, F.members[s] + off, perm, n, off, F.mpts[s], F.mpos[s]);
+    }
+    W1G_TRY(radix_sort_multi(c, jobs, 2, 1, 32));  // both sides in the same launches
+    for (int s = 0; s < 2; s++) {
+        const int64_t n = jobs[s].n;
+        if (n == 0) continue;
+        k_gather_members<<<grid_for(n, 256, 8u * c.sm_count), 256, 0, c.stream>>>(
+            pts, F.members[s] + off[s], jobs[s].vals, n, off[s], F.mpts[s], F.mpos[s]);
         W1G_CHECK_LAUNCH();
     }
     return W1G_OK;

@@ -57,13 +57,28 @@ __device__ __forceinline__ unsigned long long st_make(unsigned epoch, unsigned l
     return ((unsigned long long)epoch << 34) | (kind << 32) | cnt;
 }
 
+// One pass over up to RS_JOBS independent sorts (same word count, same digit):
+// tiles [tile0[j], tile0[j+1]) of the launch belong to job j, so two small
+// sorts share one launch and fill twice the SMs.
+constexpr int RS_JOBS = 2;
+struct PassJob {
+    KeyPtrs src, dst;
+    const uint32_t *vsrc;
+    uint32_t *vdst;
+    const uint32_t *dhist;         // this digit's global histogram
+    unsigned long long *status;    // per-tile status words
+    int64_t n;
+};
+struct PassArgs {
+    PassJob j[RS_JOBS];
+    int tile0[RS_JOBS + 1];
+    int njobs, shift;
+    unsigned *ticket;
+    unsigned epoch;
+};
+
 template <int W, int M, int RS_IPT>
-__global__ void __launch_bounds__(RS_BLOCK) k_rs_onesweep(KeyPtrs src, KeyPtrs dst,
-                                                          const uint32_t *__restrict__ vsrc,
-                                                          uint32_t *__restrict__ vdst, int shift,
-                                                          const uint32_t *__restrict__ dhist,
-                                                          unsigned long long *status, unsigned *ticket,
-                                                          unsigned epoch, int64_t n) {
+__global__ void __launch_bounds__(RS_BLOCK) k_rs_onesweep(const __grid_constant__ PassArgs A) {
     constexpr int DW = W - M;  // word holding the digit; words DW..W-1 move
     constexpr int RS_TILE = RS_BLOCK * RS_IPT;
     constexpr int RS_WTILE = 32 * RS_IPT;  // items per warp
@@ -76,14 +91,19 @@ __global__ void __launch_bounds__(RS_BLOCK) k_rs_onesweep(KeyPtrs src, KeyPtrs d
     __shared__ uint32_t s_tile;
 
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    if (tid == 0) s_tile = atomicAdd(ticket, 1u);
+    if (tid == 0) s_tile = atomicAdd(A.ticket, 1u);
     for (int w = 0; w < RS_WARPS; w++) whist[w][tid] = 0;
     if (tid < RS_WARPS) whist[tid][256] = 0;
     __syncthreads();
-    const int64_t tile = s_tile;
+    const int jb = (A.njobs > 1 && (int)s_tile >= A.tile0[1]) ? 1 : 0;
+    const PassJob &J = A.j[jb];
+    const int shift = A.shift;
+    const int64_t n = J.n;
+    unsigned long long *status = J.status;
+    const int64_t tile = (int64_t)s_tile - A.tile0[jb];
     const int64_t tbase = tile * RS_TILE;
     const int tn = (n - tbase) < RS_TILE ? (int)(n - tbase) : RS_TILE;
-    const uint64_t *kd = src.k[DW];
+    const uint64_t *kd = J.src.k[DW];
     const unsigned lt = lanemask_lt();
 
     // 1. stable rank inside the tile (warp w owns items [w*512, (w+1)*512), striped)
@@ -114,10 +134,10 @@ __global__ void __launch_bounds__(RS_BLOCK) k_rs_onesweep(KeyPtrs src, KeyPtrs d
         cnt += t;
     }
     // publish this tile's count for digit `tid` as early as possible
-    if (tile > 0) atomicExch(&status[tile * 256 + tid], st_make(epoch, ST_AGG, cnt));
+    if (tile > 0) atomicExch(&status[tile * 256 + tid], st_make(A.epoch, ST_AGG, cnt));
     uint32_t hbase;
     {  // block exclusive scans over digits: tile counts -> t_start, global histogram -> hbase
-        const uint32_t hd = dhist[tid];
+        const uint32_t hd = J.dhist[tid];
         uint32_t x = cnt, y = hd;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -159,7 +179,7 @@ __global__ void __launch_bounds__(RS_BLOCK) k_rs_onesweep(KeyPtrs src, KeyPtrs d
 #pragma unroll
             for (int w = 0; w < LB_W; w++) {
                 if (done || used < w) break;
-                if (j - w < 0 || (unsigned)(s[w] >> 34) != epoch) break;  // not published yet
+                if (j - w < 0 || (unsigned)(s[w] >> 34) != A.epoch) break;  // not published yet
                 prefix += (uint32_t)s[w];
                 used = w + 1;
                 if (((s[w] >> 32) & 3) == ST_INC) done = true;
@@ -167,7 +187,7 @@ __global__ void __launch_bounds__(RS_BLOCK) k_rs_onesweep(KeyPtrs src, KeyPtrs d
             if (done) break;
             j -= used;  // consumed aggregates; re-poll from the first unpublished tile
         }
-        atomicExch(&status[tile * 256 + tid], st_make(epoch, ST_INC, prefix + cnt));
+        atomicExch(&status[tile * 256 + tid], st_make(A.epoch, ST_INC, prefix + cnt));
         // global start of digit `tid`: smaller digits over all keys + this digit in earlier tiles
         g_base[tid] = hbase + prefix;
     }
@@ -180,8 +200,8 @@ __global__ void __launch_bounds__(RS_BLOCK) k_rs_onesweep(KeyPtrs src, KeyPtrs d
             const int d = dig[i];
             const int lp = t_start[d] + whist[wid][d] + rank[i];
 #pragma unroll
-            for (int m = 0; m < M; m++) s_key[m * RS_TILE + lp] = src.k[DW + m][tbase + li];
-            s_val[lp] = vsrc[tbase + li];
+            for (int m = 0; m < M; m++) s_key[m * RS_TILE + lp] = J.src.k[DW + m][tbase + li];
+            s_val[lp] = J.vsrc[tbase + li];
         }
     }
     __syncthreads();
@@ -191,36 +211,26 @@ __global__ void __launch_bounds__(RS_BLOCK) k_rs_onesweep(KeyPtrs src, KeyPtrs d
         const int d = (int)((k0 >> shift) & 255);
         const uint32_t pos = g_base[d] + (uint32_t)j - t_start[d];
 #pragma unroll
-        for (int m = 0; m < M; m++) dst.k[DW + m][pos] = s_key[m * RS_TILE + j];
-        vdst[pos] = s_val[j];
+        for (int m = 0; m < M; m++) J.dst.k[DW + m][pos] = s_key[m * RS_TILE + j];
+        J.vdst[pos] = s_val[j];
     }
 }
 
 template <int W, int M, int IPT>
-int launch_pass(Ctx &c, KeyPtrs *src, KeyPtrs *dst, const uint32_t *vsrc, uint32_t *vdst, int shift,
-                const uint32_t *dhist, unsigned long long *status, unsigned *ticket, unsigned epoch,
-                int64_t n) {
+int launch_pass(Ctx &c, PassArgs &A) {
     const int64_t tile = (int64_t)RS_BLOCK * IPT;
-    const int ntiles = (int)((n + tile - 1) / tile);
+    A.tile0[0] = 0;
+    for (int j = 0; j < A.njobs; j++) A.tile0[j + 1] = A.tile0[j] + (int)((A.j[j].n + tile - 1) / tile);
     const size_t sm = (size_t)tile * (8 * M + 4);
     W1G_CUDA(cudaFuncSetAttribute(k_rs_onesweep<W, M, IPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    k_rs_onesweep<W, M, IPT><<<ntiles, RS_BLOCK, sm, c.stream>>>(*src, *dst, vsrc, vdst, shift, dhist, status,
-                                                                ticket, epoch, n);
+    k_rs_onesweep<W, M, IPT><<<A.tile0[A.njobs], RS_BLOCK, sm, c.stream>>>(A);
     W1G_CHECK_LAUNCH();
     return W1G_OK;
 }
 
-int dispatch_pass(int W, int M, Ctx &c, KeyPtrs *src, KeyPtrs *dst, const uint32_t *vsrc, uint32_t *vdst,
-                  int shift, const uint32_t *dhist, unsigned long long *status, unsigned *ticket,
-                  unsigned epoch, int64_t n) {
-    // large inputs: 8192-key tiles when the staged words fit in shared memory
-    const bool large = n >= RS_LARGE_N && M <= 2;
+int dispatch_pass(int W, int M, Ctx &c, PassArgs &A, bool large) {
 #define RS_CASE(w, m)                                                                                          \
-    if (W == w && M == m)                                                                                      \
-        return large ? launch_pass<w, m, RS_IPT_LARGE>(c, src, dst, vsrc, vdst, shift, dhist, status, ticket,  \
-                                                       epoch, n)                                               \
-                     : launch_pass<w, m, RS_IPT_SMALL>(c, src, dst, vsrc, vdst, shift, dhist, status, ticket,  \
-                                                       epoch, n);
+    if (W == w && M == m) return large ? launch_pass<w, m, RS_IPT_LARGE>(c, A) : launch_pass<w, m, RS_IPT_SMALL>(c, A);
     RS_CASE(1, 1)
     RS_CASE(2, 2)
     RS_CASE(2, 1)
@@ -234,82 +244,143 @@ int dispatch_pass(int W, int M, Ctx &c, KeyPtrs *src, KeyPtrs *dst, const uint32
 
 }  // namespace
 
-int radix_sort(Ctx &c, uint64_t **keys, int words, uint32_t *vals, int64_t n, int top_bits) {
-    if (n <= 1) return W1G_OK;
-    if (words < 1 || words > 3 || n > 0xffffffffll) {
-        set_error("radix_sort: unsupported shape (words=%d, n=%lld)", words, (long long)n);
+int radix_sort_multi(Ctx &c, const SortJob *jobs, int njobs, int words, int top_bits) {
+    if (njobs < 1 || njobs > RS_JOBS || words < 1 || words > 3) {
+        set_error("radix_sort: unsupported shape (jobs=%d, words=%d)", njobs, words);
         return W1G_EINVAL;
     }
-    const int64_t small_tile = (int64_t)RS_BLOCK * RS_IPT_SMALL;
-    const int ntiles = (int)((n + small_tile - 1) / small_tile);  // upper bound for the status array
-    KeyPtrs a, b;
-    for (int w = 0; w < 4; w++) a.k[w] = b.k[w] = nullptr;
-    for (int w = 0; w < words; w++) {
-        a.k[w] = keys[w];
-        W1G_TRY(ensure(c.sort_scr[w], (size_t)n, &b.k[w]));
+    // jobs with fewer than two keys are already sorted
+    const SortJob *J[RS_JOBS];
+    int nj = 0;
+    for (int j = 0; j < njobs; j++) {
+        if (jobs[j].n > 0xffffffffll) {
+            set_error("radix_sort: %lld keys exceed the 32-bit payload", (long long)jobs[j].n);
+            return W1G_EINVAL;
+        }
+        if (jobs[j].n > 1) J[nj++] = &jobs[j];
     }
-    uint32_t *va = vals, *vb, *hist;
-    unsigned long long *status;
-    W1G_TRY(ensure(c.sort_scr[4], (size_t)n, &vb));
-    W1G_TRY(ensure(c.sort_scr[5], (size_t)words * 8 * 256 + 64, &hist));
-    const size_t cap0 = c.sort_scr[6].cap;
-    W1G_TRY(ensure(c.sort_scr[6], (size_t)ntiles * 256, &status));
-    if (c.sort_scr[6].cap != cap0) {
-        // fresh status words: make sure no stale bits can match an epoch
-        W1G_CUDA(cudaMemsetAsync(status, 0, c.sort_scr[6].cap, c.stream));
+    if (nj == 0) return W1G_OK;
+    const int64_t small_tile = (int64_t)RS_BLOCK * RS_IPT_SMALL;
+    const int nh = words * 8 * 256;
+    KeyPtrs a[RS_JOBS], b[RS_JOBS];
+    uint32_t *vb[RS_JOBS], *hist[RS_JOBS];
+    unsigned long long *status[RS_JOBS];
+    bool fresh = false;
+    for (int j = 0; j < nj; j++) {
+        const int64_t n = J[j]->n;
+        const int ntiles = (int)((n + small_tile - 1) / small_tile);  // upper bound for the status array
+        DevBuf *scr = c.sort_scr[j];
+        for (int w = 0; w < 4; w++) a[j].k[w] = b[j].k[w] = nullptr;
+        for (int w = 0; w < words; w++) {
+            a[j].k[w] = J[j]->keys[w];
+            W1G_TRY(ensure(scr[w], (size_t)n, &b[j].k[w]));
+        }
+        W1G_TRY(ensure(scr[4], (size_t)n, &vb[j]));
+        W1G_TRY(ensure(scr[5], (size_t)nh + 64, &hist[j]));
+        const size_t cap0 = scr[6].cap;
+        W1G_TRY(ensure(scr[6], (size_t)ntiles * 256, &status[j]));
+        fresh |= scr[6].cap != cap0;
+    }
+    if (fresh) {
+        // fresh status words: no stale word of any job may match a future epoch
+        for (auto &job : c.sort_scr)
+            if (job[6].p) W1G_CUDA(cudaMemsetAsync(job[6].p, 0, job[6].cap, c.stream));
         c.sort_epoch = 0;
     }
-    unsigned *tickets = hist + words * 8 * 256;  // 64 per-pass tile tickets
-    W1G_CUDA(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * (words * 8 * 256 + 64), c.stream));
-    {
-        unsigned g = grid_for(n, 512, 2u * c.sm_count);
-        size_t sm = sizeof(uint32_t) * words * 8 * 256;
+    unsigned *tickets = hist[0] + nh;  // 64 per-pass tile tickets, shared by the jobs of a launch
+    W1G_CUDA(cudaMemsetAsync(tickets, 0, sizeof(unsigned) * 64, c.stream));
+    for (int j = 0; j < nj; j++) {
+        W1G_CUDA(cudaMemsetAsync(hist[j], 0, sizeof(uint32_t) * nh, c.stream));
+        unsigned g = grid_for(J[j]->n, 512, 2u * c.sm_count);
+        size_t sm = sizeof(uint32_t) * nh;
         if (sm > 48 * 1024)
             W1G_CUDA(cudaFuncSetAttribute(k_rs_hist_all, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-        k_rs_hist_all<<<g, 512, sm, c.stream>>>(a, words, n, hist);
+        k_rs_hist_all<<<g, 512, sm, c.stream>>>(a[j], words, J[j]->n, hist[j]);
         W1G_CHECK_LAUNCH();
     }
-    W1G_TRY(stage_ensure(c, sizeof(uint32_t) * words * 8 * 256));
+    W1G_TRY(stage_ensure(c, sizeof(uint32_t) * nh * nj));
     uint32_t *hh = static_cast<uint32_t *>(c.h_stage);
-    W1G_CUDA(cudaMemcpyAsync(hh, hist, sizeof(uint32_t) * words * 8 * 256, cudaMemcpyDeviceToHost, c.stream));
+    for (int j = 0; j < nj; j++)
+        W1G_CUDA(cudaMemcpyAsync(hh + j * nh, hist[j], sizeof(uint32_t) * nh, cudaMemcpyDeviceToHost, c.stream));
     W1G_CUDA(cudaStreamSynchronize(c.stream));
-    int passes[32];
-    int np = 0;
-    for (int w = 0; w < words; w++) {
-        int jmax = (w == words - 1) ? (top_bits + 7) / 8 : 8;
-        for (int j = 0; j < jmax && j < 8; j++) {
-            const uint32_t *h = hh + (w * 8 + j) * 256;
-            bool uniform = false;
-            for (int q = 0; q < 256; q++)
-                if (h[q] == (uint32_t)n) {
-                    uniform = true;
-                    break;
+    // digits to sort per job (a digit shared by every key of a job is skipped for it)
+    bool need[RS_JOBS][32];
+    for (int j = 0; j < nj; j++)
+        for (int w = 0; w < words; w++) {
+            const int jmax = (w == words - 1) ? (top_bits + 7) / 8 : 8;
+            for (int d = 0; d < 8; d++) {
+                bool uniform = false;
+                if (d < jmax) {
+                    const uint32_t *h = hh + j * nh + (w * 8 + d) * 256;
+                    for (int q = 0; q < 256; q++)
+                        if (h[q] == (uint32_t)J[j]->n) {
+                            uniform = true;
+                            break;
+                        }
                 }
-            if (!uniform) passes[np++] = w * 8 + j;
+                need[j][w * 8 + d] = d < jmax && !uniform;
+            }
         }
+    KeyPtrs *src[RS_JOBS], *dst[RS_JOBS];
+    uint32_t *vsrc[RS_JOBS], *vdst[RS_JOBS];
+    for (int j = 0; j < nj; j++) {
+        src[j] = &a[j];
+        dst[j] = &b[j];
+        vsrc[j] = J[j]->vals;
+        vdst[j] = vb[j];
     }
-    KeyPtrs *src = &a, *dst = &b;
-    uint32_t *vsrc = va, *vdst = vb;
-    for (int p = 0; p < np; p++) {
-        const int w = passes[p] / 8, j = passes[p] % 8;
+    int launch = 0;
+    for (int dg = 0; dg < words * 8; dg++) {
+        PassArgs A;
+        A.njobs = 0;
+        bool large = false;
+        int idx[RS_JOBS];
+        for (int j = 0; j < nj; j++) {
+            if (!need[j][dg]) continue;
+            PassJob &P = A.j[A.njobs];
+            P.src = *src[j];
+            P.dst = *dst[j];
+            P.vsrc = vsrc[j];
+            P.vdst = vdst[j];
+            P.dhist = hist[j] + dg * 256;
+            P.status = status[j];
+            P.n = J[j]->n;
+            large |= J[j]->n >= RS_LARGE_N;
+            idx[A.njobs++] = j;
+        }
+        if (A.njobs == 0) continue;
+        const int w = dg / 8;
         c.sort_epoch = (c.sort_epoch + 1) & 0x3fffffffu;
         if (c.sort_epoch == 0) c.sort_epoch = 1;
-        W1G_TRY(dispatch_pass(words, words - w, c, src, dst, vsrc, vdst, 8 * j, hist + (w * 8 + j) * 256,
-                              status, tickets + (p & 63), c.sort_epoch, n));
-        KeyPtrs *t = src;
-        src = dst;
-        dst = t;
-        uint32_t *tv = vsrc;
-        vsrc = vdst;
-        vdst = tv;
+        A.shift = 8 * (dg % 8);
+        A.ticket = tickets + (launch++ & 63);
+        A.epoch = c.sort_epoch;
+        // large inputs: 8192-key tiles when the staged words fit in shared memory
+        W1G_TRY(dispatch_pass(words, words - w, c, A, large && words - w <= 2));
+        for (int q = 0; q < A.njobs; q++) {
+            const int j = idx[q];
+            KeyPtrs *t = src[j];
+            src[j] = dst[j];
+            dst[j] = t;
+            uint32_t *tv = vsrc[j];
+            vsrc[j] = vdst[j];
+            vdst[j] = tv;
+        }
     }
-    if (vsrc != vals) {
-        // result lives in the scratch buffers: copy the payload and the top key word back
-        W1G_CUDA(cudaMemcpyAsync(vals, vsrc, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, c.stream));
-        W1G_CUDA(cudaMemcpyAsync(keys[words - 1], src->k[words - 1], sizeof(uint64_t) * n,
-                                 cudaMemcpyDeviceToDevice, c.stream));
-    }
+    for (int j = 0; j < nj; j++)
+        if (vsrc[j] != J[j]->vals) {
+            // result lives in the scratch buffers: copy the payload and the top key word back
+            W1G_CUDA(cudaMemcpyAsync(J[j]->vals, vsrc[j], sizeof(uint32_t) * J[j]->n, cudaMemcpyDeviceToDevice,
+                                     c.stream));
+            W1G_CUDA(cudaMemcpyAsync(J[j]->keys[words - 1], src[j]->k[words - 1], sizeof(uint64_t) * J[j]->n,
+                                     cudaMemcpyDeviceToDevice, c.stream));
+        }
     return W1G_OK;
+}
+
+int radix_sort(Ctx &c, uint64_t **keys, int words, uint32_t *vals, int64_t n, int top_bits) {
+    SortJob job{{keys[0], words > 1 ? keys[1] : nullptr, words > 2 ? keys[2] : nullptr}, vals, n};
+    return radix_sort_multi(c, &job, 1, words, top_bits);
 }
 
 // ---------------------------------------------------------------- (primary, secondary) sort
@@ -365,42 +436,72 @@ __global__ void k_tie_put(const uint32_t *tpos, const uint32_t *tmp, int64_t t, 
 
 }  // namespace
 
+int sort_lex2_multi(Ctx &c, const Lex2Job *jobs, int njobs) {
+    if (njobs < 1 || njobs > RS_JOBS) {
+        set_error("sort_lex2: unsupported job count %d", njobs);
+        return W1G_EINVAL;
+    }
+    uint64_t *pk[RS_JOBS];
+    int64_t *excl[RS_JOBS];
+    SortJob sj[RS_JOBS];
+    int64_t *dt = ptr<int64_t>(c.flags) + F_MISC2;  // tie counts (F_MISC2, F_MISC3)
+    for (int j = 0; j < njobs; j++) {
+        const int64_t n = jobs[j].n;
+        W1G_TRY(ensure(c.lex_scr[j][0], (size_t)n + 1, &pk[j]));
+        W1G_TRY(ensure(c.lex_scr[j][1], (size_t)n + 1, &excl[j]));
+        if (n > 0) {
+            k_copy_u64<<<grid_for(n, 256, 8u * c.sm_count), 256, 0, c.stream>>>(jobs[j].primary, pk[j], n);
+            W1G_CHECK_LAUNCH();
+        }
+        sj[j] = SortJob{{pk[j], nullptr, nullptr}, jobs[j].vals, n};
+    }
+    W1G_TRY(radix_sort_multi(c, sj, njobs, 1, 64));
+    for (int j = 0; j < njobs; j++) {
+        if (jobs[j].n > 1) {
+            W1G_TRY(scan_i64(c, TieFlag{pk[j], jobs[j].n}, jobs[j].n, excl[j], dt + j));
+        } else {
+            W1G_CUDA(cudaMemsetAsync(dt + j, 0, sizeof(int64_t), c.stream));
+        }
+    }
+    W1G_CUDA(cudaMemcpyAsync(&c.h_pinned[F_MISC2], dt, sizeof(int64_t) * njobs, cudaMemcpyDeviceToHost, c.stream));
+    W1G_CUDA(cudaStreamSynchronize(c.stream));
+    // elements of primary-tie runs: sort them by (primary, secondary), put them back
+    SortJob tj[RS_JOBS];
+    uint32_t *tpos[RS_JOBS], *pl[RS_JOBS];
+    int nt = 0, which[RS_JOBS];
+    for (int j = 0; j < njobs; j++) {
+        const int64_t T = c.h_pinned[F_MISC2 + j];
+        if (T == 0) continue;
+        uint64_t *kl, *kh;
+        W1G_TRY(ensure(c.lex_scr[j][2], (size_t)T, &tpos[j]));
+        W1G_TRY(ensure(c.lex_scr[j][3], (size_t)T, &kl));
+        W1G_TRY(ensure(c.lex_scr[j][4], (size_t)T, &kh));
+        W1G_TRY(ensure(c.lex_scr[j][5], (size_t)T * 2, &pl[j]));
+        k_tie_gather<<<grid_for(jobs[j].n, 256, 8u * c.sm_count), 256, 0, c.stream>>>(
+            TieFlag{pk[j], jobs[j].n}, excl[j], jobs[j].vals, jobs[j].secondary, tpos[j], kl, kh, pl[j]);
+        W1G_CHECK_LAUNCH();
+        tj[nt] = SortJob{{kl, kh, nullptr}, pl[j], T};
+        which[nt++] = j;
+    }
+    if (nt == 0) return W1G_OK;
+    W1G_TRY(radix_sort_multi(c, tj, nt, 2, 64));
+    for (int q = 0; q < nt; q++) {
+        const int j = which[q];
+        const int64_t T = tj[q].n;
+        uint32_t *tmp = pl[j] + T;
+        const unsigned gt = grid_for(T, 256, 8u * c.sm_count);
+        k_tie_fetch<<<gt, 256, 0, c.stream>>>(tpos[j], pl[j], jobs[j].vals, T, tmp);
+        W1G_CHECK_LAUNCH();
+        k_tie_put<<<gt, 256, 0, c.stream>>>(tpos[j], tmp, T, jobs[j].vals);
+        W1G_CHECK_LAUNCH();
+    }
+    return W1G_OK;
+}
+
 int sort_lex2(Ctx &c, const uint64_t *primary, const uint64_t *secondary, uint32_t *vals, int64_t n) {
     if (n <= 1) return W1G_OK;
-    uint64_t *pk;
-    int64_t *excl;
-    W1G_TRY(ensure(c.lex_scr[0], (size_t)n, &pk));
-    W1G_TRY(ensure(c.lex_scr[1], (size_t)n, &excl));
-    const unsigned g = grid_for(n, 256, 8u * c.sm_count);
-    k_copy_u64<<<g, 256, 0, c.stream>>>(primary, pk, n);
-    W1G_CHECK_LAUNCH();
-    uint64_t *k1[1] = {pk};
-    W1G_TRY(radix_sort(c, k1, 1, vals, n, 64));
-    TieFlag f{pk, n};
-    int64_t *dt = ptr<int64_t>(c.flags) + F_MISC3;
-    W1G_TRY(scan_i64(c, f, n, excl, dt));
-    int64_t T = 0;
-    W1G_CUDA(cudaMemcpyAsync(&c.h_pinned[F_MISC3], dt, sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream));
-    W1G_CUDA(cudaStreamSynchronize(c.stream));
-    T = c.h_pinned[F_MISC3];
-    if (T == 0) return W1G_OK;
-    uint32_t *tpos, *pl, *tmp;
-    uint64_t *kl, *kh;
-    W1G_TRY(ensure(c.lex_scr[2], (size_t)T, &tpos));
-    W1G_TRY(ensure(c.lex_scr[3], (size_t)T, &kl));
-    W1G_TRY(ensure(c.lex_scr[4], (size_t)T, &kh));
-    W1G_TRY(ensure(c.lex_scr[5], (size_t)T * 2, &pl));
-    tmp = pl + T;
-    k_tie_gather<<<g, 256, 0, c.stream>>>(f, excl, vals, secondary, tpos, kl, kh, pl);
-    W1G_CHECK_LAUNCH();
-    uint64_t *k2[2] = {kl, kh};
-    W1G_TRY(radix_sort(c, k2, 2, pl, T, 64));
-    const unsigned gt = grid_for(T, 256, 8u * c.sm_count);
-    k_tie_fetch<<<gt, 256, 0, c.stream>>>(tpos, pl, vals, T, tmp);
-    W1G_CHECK_LAUNCH();
-    k_tie_put<<<gt, 256, 0, c.stream>>>(tpos, tmp, T, vals);
-    W1G_CHECK_LAUNCH();
-    return W1G_OK;
+    Lex2Job job{primary, secondary, vals, n};
+    return sort_lex2_multi(c, &job, 1);
 }
 
 }  // namespace w1g

@@ -802,10 +802,11 @@ int tree_run(Ctx &c, const double2 *pts, int64_t n, int64_t *n_nodes, int32_t *d
     W1G_CHECK_LAUNCH();
     // X-list by (x, y) and Y-list by (y, x): kx1 = key(x), kx0 = key(y)
     SubTimer T(c, "tree");
-    W1G_TRY(sort_lex2(c, kx1, kx0, xl[0], n));
-    T.mark("sort_x");
-    W1G_TRY(sort_lex2(c, kx0, kx1, yl[0], n));
-    T.mark("sort_y");
+    {  // both lists in the same launches
+        const Lex2Job jobs[2] = {{kx1, kx0, xl[0], n}, {kx0, kx1, yl[0], n}};
+        W1G_TRY(sort_lex2_multi(c, jobs, 2));
+    }
+    T.mark("sort_xy");
     // level state
     Seg *seg[2];
     SegInfo *info;
