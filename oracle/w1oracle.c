@@ -629,7 +629,9 @@ int64_t orc_build_network(int64_t n, const int64_t *supplies, const int64_t *tai
         if (e == 0 || r[e].t != r[e - 1].t || r[e].h != r[e - 1].h) {
             g++;
             ot[g] = r[e].t; oh[g] = r[e].h; oc[g] = c;
-        } else if (c < oc[g]) {
+        } else if (!(oc[g] < c)) {
+            /* np.minimum(acc, c) keeps acc only when strictly smaller: among
+               equal minima (+0.0 / -0.0) the later arc wins */
             oc[g] = c;
         }
     }

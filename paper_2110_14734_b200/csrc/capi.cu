@@ -58,17 +58,35 @@ int flags_reset(Ctx &c) {
     return W1G_OK;
 }
 
+int stream_sync(Ctx &c) {
+    c.n_syncs++;
+    if (!c.timing) {
+        W1G_CUDA(cudaStreamSynchronize(c.stream));
+        return W1G_OK;
+    }
+    // the gap: from the last queued work finishing to the next work the host
+    // can issue (an event recorded right after the wake-up runs immediately)
+    W1G_CUDA(cudaEventRecord(c.sync_ev[0], c.stream));
+    W1G_CUDA(cudaStreamSynchronize(c.stream));
+    W1G_CUDA(cudaEventRecord(c.sync_ev[1], c.stream));
+    W1G_CUDA(cudaEventSynchronize(c.sync_ev[1]));
+    float ms = 0.f;
+    W1G_CUDA(cudaEventElapsedTime(&ms, c.sync_ev[0], c.sync_ev[1]));
+    c.sync_gap_us += 1e3 * ms;
+    return W1G_OK;
+}
+
 int flags_fetch(Ctx &c, int first, int count) {
     W1G_CUDA(cudaMemcpyAsync(c.h_pinned + first, dflags(c) + first, sizeof(int64_t) * count,
                              cudaMemcpyDeviceToHost, c.stream));
-    W1G_CUDA(cudaStreamSynchronize(c.stream));
+    W1G_TRY(stream_sync(c));
     return W1G_OK;
 }
 
 int stage_ensure(Ctx &c, size_t bytes) {
     if (bytes <= c.h_stage_cap) return W1G_OK;
     if (c.h_stage) {
-        W1G_CUDA(cudaStreamSynchronize(c.stream));
+        W1G_TRY(stream_sync(c));
         cudaFreeHost(c.h_stage);
         c.h_stage = nullptr;
         c.h_stage_cap = 0;
@@ -181,6 +199,8 @@ int w1g_ctx_create(int device, w1g_ctx **out) {
     W1G_TRY(ensure(c->flags, F_NSLOTS, &f));
     W1G_CUDA(cudaHostAlloc(&c->h_pinned, sizeof(int64_t) * F_NSLOTS, cudaHostAllocDefault));
     for (auto &e : c->ev) W1G_CUDA(cudaEventCreate(&e));
+    for (auto &e : c->sync_ev) W1G_CUDA(cudaEventCreate(&e));
+    if (const char *e = getenv("W1G_TIMING")) c->timing = *e == '1';
     *out = c;
     return W1G_OK;
 }
@@ -214,6 +234,8 @@ int w1g_ctx_destroy(w1g_ctx *c) {
     if (c->h_stage) cudaFreeHost(c->h_stage);
     for (auto &e : c->ev)
         if (e) cudaEventDestroy(e);
+    for (auto &e : c->sync_ev)
+        if (e) cudaEventDestroy(e);
     cudaStreamDestroy(c->stream);
     delete c;
     return W1G_OK;
@@ -223,7 +245,7 @@ void *w1g_ctx_stream(w1g_ctx *c) { return c ? (void *)c->stream : nullptr; }
 
 int w1g_synchronize(w1g_ctx *c) {
     CTX_CHECK(c);
-    W1G_CUDA(cudaStreamSynchronize(c->stream));
+    W1G_TRY(stream_sync(*c));
     return W1G_OK;
 }
 
@@ -291,7 +313,7 @@ int w1g_fetch_nodes(w1g_ctx *c, int slot, double *points, int64_t *am, int64_t *
     W1G_TRY(download(*c, points, ns.pts.p, sizeof(double2) * ns.k));
     W1G_TRY(download(*c, am, ns.am.p, sizeof(int64_t) * ns.k));
     W1G_TRY(download(*c, bm, ns.bm.p, sizeof(int64_t) * ns.k));
-    W1G_CUDA(cudaStreamSynchronize(c->stream));
+    W1G_TRY(stream_sync(*c));
     return W1G_OK;
 }
 
@@ -317,7 +339,7 @@ int w1g_fetch_rwmd_best(w1g_ctx *c, int side, double *best, int64_t *n) {
     *n = c->n_best[side];
     if (best) {
         W1G_TRY(download(*c, best, c->best[side].p, sizeof(double) * c->n_best[side]));
-        W1G_CUDA(cudaStreamSynchronize(c->stream));
+        W1G_TRY(stream_sync(*c));
     }
     return W1G_OK;
 }
@@ -384,7 +406,7 @@ int w1g_fetch_tree(w1g_ctx *c, int64_t *left, int64_t *right, double *bbox, int6
     W1G_TRY(download(*c, bbox, c->t_bbox.p, sizeof(double) * 4 * nn));
     W1G_TRY(download(*c, rep, c->t_rep.p, sizeof(int64_t) * nn));
     W1G_TRY(download(*c, size, c->t_size.p, sizeof(int64_t) * nn));
-    W1G_CUDA(cudaStreamSynchronize(c->stream));
+    W1G_TRY(stream_sync(*c));
     return W1G_OK;
 }
 
@@ -443,7 +465,7 @@ int w1g_fetch_pairs(w1g_ctx *c, int64_t *node_pairs, int64_t *indices) {
         // int2 (u, v) -> int64 (P, 2)
         W1G_TRY(stage_ensure(*c, sizeof(int2) * P));
         W1G_TRY(download(*c, c->h_stage, c->pair_uv.p, sizeof(int2) * P));
-        W1G_CUDA(cudaStreamSynchronize(c->stream));
+        W1G_TRY(stream_sync(*c));
         const int2 *uv = static_cast<const int2 *>(c->h_stage);
         for (size_t i = 0; i < P; i++) {
             node_pairs[2 * i] = uv[i].x;
@@ -452,7 +474,7 @@ int w1g_fetch_pairs(w1g_ctx *c, int64_t *node_pairs, int64_t *indices) {
     }
     if (indices) {
         W1G_TRY(download(*c, indices, c->pair_idx.p, sizeof(int64_t) * 2 * P));
-        W1G_CUDA(cudaStreamSynchronize(c->stream));
+        W1G_TRY(stream_sync(*c));
     }
     return W1G_OK;
 }
@@ -467,7 +489,7 @@ int w1g_fetch_pair_counts(w1g_ctx *c, int64_t *counts, int64_t *n_internal) {
     *n_internal = ni;
     if (counts) {
         W1G_TRY(download(*c, counts, c->pair_counts.p, sizeof(int64_t) * ni));
-        W1G_CUDA(cudaStreamSynchronize(c->stream));
+        W1G_TRY(stream_sync(*c));
     }
     return W1G_OK;
 }
@@ -509,7 +531,7 @@ int w1g_fetch_arcs(w1g_ctx *c, int64_t *tails, int64_t *heads, double *costs) {
     W1G_TRY(download(*c, tails, c->arc_t.p, sizeof(int64_t) * m));
     W1G_TRY(download(*c, heads, c->arc_h.p, sizeof(int64_t) * m));
     W1G_TRY(download(*c, costs, c->arc_c.p, sizeof(double) * m));
-    W1G_CUDA(cudaStreamSynchronize(c->stream));
+    W1G_TRY(stream_sync(*c));
     return W1G_OK;
 }
 
@@ -564,7 +586,7 @@ int w1g_fetch_network(w1g_ctx *c, int64_t *supplies, int64_t *tails, int64_t *he
     W1G_TRY(download(*c, heads, c->net_h.p, sizeof(int64_t) * m));
     W1G_TRY(download(*c, costs, c->net_c.p, sizeof(double) * m));
     W1G_TRY(download(*c, row_offsets, c->net_ro.p, sizeof(int64_t) * (n + 1)));
-    W1G_CUDA(cudaStreamSynchronize(c->stream));
+    W1G_TRY(stream_sync(*c));
     return W1G_OK;
 }
 
@@ -587,6 +609,8 @@ int w1g_front_end_device(w1g_ctx *c, const double *d_a, int64_t na, const double
         return W1G_EINVAL;
     }
     cudaEvent_t *ev = c->ev;
+    c->n_syncs = 0;
+    c->sync_gap_us = 0.0;
     W1G_CUDA(cudaEventRecord(ev[0], c->stream));
     int64_t k0;
     int32_t balanced;
@@ -596,7 +620,7 @@ int w1g_front_end_device(w1g_ctx *c, const double *d_a, int64_t na, const double
     if (k0 == 0 || balanced) {
         // pipeline.py:106-109: empty inputs or identical multisets -> 0.0
         info->short_circuit = 1;
-        W1G_CUDA(cudaStreamSynchronize(c->stream));
+        W1G_TRY(stream_sync(*c));
         return W1G_OK;
     }
     // pipeline.py:67-69, condensation.py:47-59 (same IEEE operation order as the Python)
@@ -696,6 +720,8 @@ int w1g_front_end_device(w1g_ctx *c, const double *d_a, int64_t na, const double
     for (int i = 0; i < 7; i++) W1G_CUDA(cudaEventElapsedTime(&info->stage_ms[i], ev[i], ev[i + 1]));
     if (overlap) W1G_CUDA(cudaEventElapsedTime(&info->stage_ms[1], c->aux->ev[0], c->aux->ev[1]));
     W1G_CUDA(cudaEventElapsedTime(&info->stage_ms[7], ev[0], ev[9]));
+    if (c->timing)
+        fprintf(stderr, "[w1g syncs] host round trips=%lld idle=%.1fus\n", (long long)c->n_syncs, c->sync_gap_us);
     return W1G_OK;
 }
 
@@ -709,7 +735,7 @@ int w1g_front_end(w1g_ctx *c, const double *a, int64_t na, const double *b, int6
     // stage both diagrams through pinned memory: one full-speed H2D
     const size_t bytes = sizeof(double2) * (size_t)(na + nb);
     W1G_TRY(stage_ensure(*c, bytes));
-    W1G_CUDA(cudaStreamSynchronize(c->stream));
+    W1G_TRY(stream_sync(*c));
     if (na) memcpy(c->h_stage, a, sizeof(double2) * na);
     if (nb) memcpy(static_cast<char *>(c->h_stage) + sizeof(double2) * na, b, sizeof(double2) * nb);
     if (bytes) W1G_CUDA(cudaMemcpyAsync(d, c->h_stage, bytes, cudaMemcpyHostToDevice, c->stream));

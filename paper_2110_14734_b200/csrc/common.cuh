@@ -145,6 +145,12 @@ struct Ctx {
     // thread -- concurrently with emit + assemble (W1G_OVERLAP=0 disables)
     int overlap = 1;
     Ctx *aux = nullptr;
+
+    // host round-trip accounting (stream_sync)
+    int timing = 0;
+    int64_t n_syncs = 0;
+    double sync_gap_us = 0.0;
+    cudaEvent_t sync_ev[2] = {};
 };
 
 // device flag block layout (int64 slots)
@@ -172,6 +178,10 @@ enum FlagSlot {
 };
 
 int flags_reset(Ctx &c);
+// host wait for the context stream.  Every host round trip leaves the GPU
+// idle (D2H + wake-up + next launch); with W1G_TIMING=1 the idle time is
+// measured with events on both sides and printed per front end.
+int stream_sync(Ctx &c);
 int flags_fetch(Ctx &c, int first, int count);  // D2H into h_pinned + stream sync
 inline int64_t *dflags(Ctx &c) { return ptr<int64_t>(c.flags); }
 

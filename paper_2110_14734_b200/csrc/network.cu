@@ -159,10 +159,12 @@ __global__ void k_net_emit(GroupFlag f, int64_t m, const int64_t *excl, const ui
         const int64_t g = excl[i];
         const uint32_t e = perm[i];
         double cm = c[e];
-        // np.minimum.at over the duplicate group (network.py:75-76)
+        // np.minimum.at over the duplicate group (network.py:75-76), a fold in
+        // arc order: minimum(acc, c) keeps acc only when strictly smaller, so
+        // among equal minima (+0.0 / -0.0) the later arc wins
         for (int64_t j = i + 1; j < m && !f(j); j++) {
             const double cj = c[perm[j]];
-            cm = cj < cm ? cj : cm;
+            cm = cm < cj ? cm : cj;
         }
         ot[g] = t[e];
         oh[g] = h[e];
@@ -178,6 +180,376 @@ struct RowCount {
 };
 
 inline unsigned gs(const Ctx &c, int64_t n) { return grid_for(n, 256, 8u * c.sm_count); }
+
+// ---------------------------------------------------------------- row-bucketed CSR
+//
+// np.lexsort((heads, tails)) + duplicate reduction (network.py:70-82) without a
+// full-width sort: arcs are bucketed by tail (count, scan, scatter -- rows are
+// what the CSR needs anyway), then every row is sorted by (head, arc index)
+// on chip -- a warp per row of <= 32 arcs, a CTA per longer row -- and its
+// duplicate (tail, head) groups reduced as np.minimum.at does: a fold in arc
+// order from +inf, so among equal minima (+0.0 / -0.0) the LAST arc wins.
+// Row offsets are the scan of the deduplicated row lengths.
+
+// validation (network.py:55-68) + arcs per tail row; out-of-range arcs are
+// flagged and never counted.  Arcs of one tail come in runs (all diagonal arcs
+// leave b-bar), so counts are warp-aggregated: one atomic per tail per warp.
+__global__ void k_csr_count(const int64_t *sup, int64_t n, const int64_t *t, const int64_t *h, const double *c,
+                            int64_t m, unsigned *cnt, int64_t *f) {
+    int64_t s = 0;
+    unsigned bits = 0;
+    const int lane = threadIdx.x & 31;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) s += sup[i];
+    const int64_t mr = (m + 31) & ~31ll;  // whole warps iterate together
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < mr; e += stride) {
+        int64_t a = -1;
+        if (e < m) {
+            const int64_t b = h[e];
+            const double cc = c[e];
+            a = t[e];
+            const bool ok = a >= 0 && a < n && b >= 0 && b < n;
+            if (!ok) bits |= 1u;
+            if (a == b) bits |= 2u;
+            if (!isfinite(cc)) bits |= 4u;
+            if (cc < 0) bits |= 8u;
+            if (!ok) a = -1;
+        }
+        const unsigned peers = __match_any_sync(0xffffffffu, a);
+        if (a >= 0 && (__ffs(peers) - 1) == lane) atomicAdd(&cnt[a], (unsigned)__popc(peers));
+    }
+    for (int o = 16; o; o >>= 1) {
+        s += __shfl_xor_sync(0xffffffffu, s, o);
+        bits |= __shfl_xor_sync(0xffffffffu, bits, o);
+    }
+    if (lane == 0) {
+        if (s) atomicAdd((unsigned long long *)&f[F_MISC0], (unsigned long long)s);
+        if (bits) atomicOr((unsigned long long *)&f[F_NET_ERR], (unsigned long long)bits);
+    }
+}
+
+struct RowLen {
+    const unsigned *cnt;
+    int64_t n;
+    __device__ int64_t operator()(int64_t i) const { return i < n ? (int64_t)cnt[i] : 0; }
+};
+
+// arc -> slot in its tail row, warp-aggregated (order inside a row is fixed
+// later by the row sort)
+__global__ void k_csr_scatter(const int64_t *t, const int64_t *h, int64_t m, int64_t n, const int64_t *start,
+                              unsigned *cursor, int32_t *slot_h, uint32_t *slot_e) {
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = lanemask_lt();
+    const int64_t mr = (m + 31) & ~31ll;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < mr;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        int64_t a = -1, b = 0;
+        if (e < m) {
+            a = t[e];
+            b = h[e];
+            if (a < 0 || a >= n || b < 0 || b >= n) a = -1;
+        }
+        const unsigned peers = __match_any_sync(0xffffffffu, a);
+        const int leader = __ffs(peers) - 1;
+        unsigned base = 0;
+        if (a >= 0 && lane == leader) base = atomicAdd(&cursor[a], (unsigned)__popc(peers));
+        base = __shfl_sync(0xffffffffu, base, leader);
+        if (a >= 0) {
+            const int64_t p = start[a] + base + __popc(peers & lt);
+            slot_h[p] = (int32_t)b;
+            slot_e[p] = (uint32_t)e;
+        }
+    }
+}
+
+// np.minimum.at order: (cost, arc) pairs, smaller cost first, then the later arc
+__device__ __forceinline__ bool min_at_better(double c2, uint32_t e2, double c1, uint32_t e1) {
+    return c2 < c1 || (c2 == c1 && e2 > e1);
+}
+
+// row classes by length: <= 32 a warp in registers, <= CSR_MED_MAX a warp in
+// shared memory, <= CSR_LONG_MAX a CTA in shared memory, longer ("huge": the
+// b-bar row of every front end) a CTA with head-indexed minima
+constexpr int CSR_MED_MAX = 256;
+constexpr int CSR_LONG_MAX = 4096;
+constexpr int CSR_HUGE_CAP = 2;  // more huge rows than this: radix-sort fallback
+enum { CL_MED = 0, CL_LONG = 1, CL_HUGE = 2 };
+
+__global__ void k_csr_short_rows(const int64_t *start, int64_t n, int32_t *slot_h, const uint32_t *slot_e,
+                                 const double *c, double *slot_c, int64_t *dcnt, int32_t *lists,
+                                 int32_t *n_list, int64_t *f) {
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = lanemask_lt();
+    for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n;
+         r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t s0 = start[r];
+        const int64_t len = start[r + 1] - s0;
+        if (len > 32) {
+            if (lane == 0) {
+                const int cl = len <= CSR_MED_MAX ? CL_MED : len <= CSR_LONG_MAX ? CL_LONG : CL_HUGE;
+                const int k = atomicAdd(&n_list[cl], 1);
+                if (cl != CL_HUGE || k < CSR_HUGE_CAP) {
+                    lists[(int64_t)cl * n + k] = (int32_t)r;
+                } else {  // no table left: emit nothing, the host redoes it with the full sort
+                    dcnt[r] = 0;
+                    atomicOr((unsigned long long *)&f[F_OVERFLOW], 1ull);
+                }
+            }
+            continue;
+        }
+        if (len == 0) {
+            if (lane == 0) dcnt[r] = 0;
+            continue;
+        }
+        uint64_t key = ~0ull;
+        if (lane < len) key = ((uint64_t)(uint32_t)slot_h[s0 + lane] << 32) | slot_e[s0 + lane];
+        for (int k = 2; k <= 32; k <<= 1)
+            for (int j = k >> 1; j; j >>= 1) {
+                const uint64_t o = __shfl_xor_sync(0xffffffffu, key, j);
+                const bool up = ((lane & k) == 0) == ((lane & j) == 0);
+                key = up ? (key < o ? key : o) : (key > o ? key : o);
+            }
+        const bool valid = lane < len;
+        const int32_t head = (int32_t)(key >> 32);
+        const uint32_t e = (uint32_t)key;
+        double cost = valid ? c[e] : INFINITY;
+        const int32_t prev = __shfl_up_sync(0xffffffffu, head, 1);
+        const bool first = valid && (lane == 0 || prev != head);
+        const unsigned firsts = __ballot_sync(0xffffffffu, first);
+        // suffix reduction inside each (head) group: lanes of a group are contiguous
+        const int gid = __popc(firsts & (lt | (1u << lane)));
+        uint32_t eb = e;
+        for (int o = 1; o < 32; o <<= 1) {
+            const double c2 = __shfl_down_sync(0xffffffffu, cost, o);
+            const uint32_t e2 = __shfl_down_sync(0xffffffffu, eb, o);
+            const int g2 = __shfl_down_sync(0xffffffffu, gid, o);
+            if (lane + o < len && g2 == gid && min_at_better(c2, e2, cost, eb)) {
+                cost = c2;
+                eb = e2;
+            }
+        }
+        if (first) {
+            const int64_t q = s0 + __popc(firsts & lt);
+            slot_h[q] = head;
+            slot_c[q] = cost;
+        }
+        if (lane == 0) dcnt[r] = __popc(firsts);
+    }
+}
+
+// sorted keys (head << 32 | arc) of one row in shared memory -> deduplicated
+// (head, min cost) back into the row's slots; `per` items per participant
+template <class Sync>
+__device__ void dedup_sorted(const uint64_t *sk, int len, int part, int nparts, int *s_cnt, int64_t s0,
+                             const double *c, int32_t *slot_h, double *slot_c, int64_t *dcnt_r, Sync sync) {
+    const int per = (len + nparts - 1) / nparts;
+    const int b0 = part * per, b1 = min(len, b0 + per);
+    int nf = 0;
+    for (int i = b0; i < b1; i++) nf += (i == 0 || (sk[i] >> 32) != (sk[i - 1] >> 32));
+    s_cnt[part] = nf;
+    sync();
+    int q = 0, tot = 0;
+    for (int p = 0; p < nparts; p++) {
+        if (p < part) q += s_cnt[p];
+        tot += s_cnt[p];
+    }
+    for (int i = b0; i < b1; i++) {
+        const uint64_t ki = sk[i];
+        if (i > 0 && (ki >> 32) == (sk[i - 1] >> 32)) continue;
+        double cost = c[(uint32_t)ki];
+        uint32_t eb = (uint32_t)ki;
+        for (int j = i + 1; j < len && (sk[j] >> 32) == (ki >> 32); j++) {
+            const double c2 = c[(uint32_t)sk[j]];
+            if (min_at_better(c2, (uint32_t)sk[j], cost, eb)) {
+                cost = c2;
+                eb = (uint32_t)sk[j];
+            }
+        }
+        slot_h[s0 + q] = (int32_t)(ki >> 32);
+        slot_c[s0 + q] = cost;
+        q++;
+    }
+    if (part == 0) *dcnt_r = tot;
+}
+
+// rows of 33..CSR_MED_MAX arcs: a warp each, bitonic sort in its shared-memory slice
+constexpr int CSR_MB = 256;
+__global__ void __launch_bounds__(CSR_MB) k_csr_med_rows(const int64_t *start, const int32_t *rows,
+                                                         const int32_t *n_rows, int32_t *slot_h,
+                                                         const uint32_t *slot_e, const double *c, double *slot_c,
+                                                         int64_t *dcnt) {
+    __shared__ uint64_t sk_all[CSR_MB / 32][CSR_MED_MAX];
+    __shared__ int cnt_all[CSR_MB / 32][32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint64_t *sk = sk_all[wid];
+    const int nr = *n_rows;
+    for (int ri = blockIdx.x * (CSR_MB / 32) + wid; ri < nr; ri += gridDim.x * (CSR_MB / 32)) {
+        const int64_t r = rows[ri];
+        const int64_t s0 = start[r];
+        const int len = (int)(start[r + 1] - s0);
+        int np2 = 64;
+        while (np2 < len) np2 <<= 1;
+        __syncwarp();
+        for (int i = lane; i < np2; i += 32)
+            sk[i] = i < len ? (((uint64_t)(uint32_t)slot_h[s0 + i] << 32) | slot_e[s0 + i]) : ~0ull;
+        __syncwarp();
+        for (int k = 2; k <= np2; k <<= 1)
+            for (int j = k >> 1; j; j >>= 1) {
+                for (int i = lane; i < np2; i += 32) {
+                    const int p = i ^ j;
+                    if (p > i) {
+                        const uint64_t a = sk[i], b = sk[p];
+                        if ((a > b) == ((i & k) == 0)) {
+                            sk[i] = b;
+                            sk[p] = a;
+                        }
+                    }
+                }
+                __syncwarp();
+            }
+        dedup_sorted(sk, len, lane, 32, cnt_all[wid], s0, c, slot_h, slot_c, dcnt + r, []() { __syncwarp(); });
+        __syncwarp();
+    }
+}
+
+// rows of CSR_MED_MAX+1..CSR_LONG_MAX arcs: one CTA each, bitonic sort in shared memory
+constexpr int CSR_LB = 512;
+__global__ void __launch_bounds__(CSR_LB) k_csr_long_rows(const int64_t *start, const int32_t *rows,
+                                                          const int32_t *n_rows, int32_t *slot_h,
+                                                          const uint32_t *slot_e, const double *c,
+                                                          double *slot_c, int64_t *dcnt) {
+    __shared__ uint64_t sk[CSR_LONG_MAX];
+    __shared__ int s_cnt[CSR_LB];
+    const int tid = threadIdx.x;
+    const int nr = *n_rows;
+    for (int ri = blockIdx.x; ri < nr; ri += gridDim.x) {
+        const int64_t r = rows[ri];
+        const int64_t s0 = start[r];
+        const int len = (int)(start[r + 1] - s0);
+        int np2 = 64;
+        while (np2 < len) np2 <<= 1;
+        __syncthreads();
+        for (int i = tid; i < np2; i += CSR_LB)
+            sk[i] = i < len ? (((uint64_t)(uint32_t)slot_h[s0 + i] << 32) | slot_e[s0 + i]) : ~0ull;
+        __syncthreads();
+        for (int k = 2; k <= np2; k <<= 1)
+            for (int j = k >> 1; j; j >>= 1) {
+                for (int i = tid; i < np2; i += CSR_LB) {
+                    const int p = i ^ j;
+                    if (p > i) {
+                        const uint64_t a = sk[i], b = sk[p];
+                        if ((a > b) == ((i & k) == 0)) {
+                            sk[i] = b;
+                            sk[p] = a;
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+        dedup_sorted(sk, len, tid, CSR_LB, s_cnt, s0, c, slot_h, slot_c, dcnt + r, []() { __syncthreads(); });
+        __syncthreads();
+    }
+}
+
+// huge rows (> CSR_LONG_MAX arcs: the b-bar row of every front end): per-head
+// minima in a dense head-indexed table (cost with -0 folded onto +0, then the
+// latest arc among the minimal ones, as np.minimum.at's fold), read back in
+// head order by a device scan.  Grid-wide kernels over the (<= CSR_HUGE_CAP)
+// listed rows; the row count is read on the device.
+__device__ __forceinline__ unsigned long long cost_key(double x) {
+    return x == 0.0 ? 0ull : (unsigned long long)__double_as_longlong(x);  // costs are >= 0
+}
+__global__ void k_huge_init(const int32_t *n_rows, int64_t n, unsigned long long *tab_c, unsigned *tab_e) {
+    const int64_t tot = (int64_t)min(*n_rows, CSR_HUGE_CAP) * n;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
+        tab_c[i] = ~0ull;
+        tab_e[i] = 0u;
+    }
+}
+template <int PHASE>
+__global__ void k_huge_fold(const int64_t *start, const int32_t *rows, const int32_t *n_rows, int64_t n,
+                            const int32_t *slot_h, const uint32_t *slot_e, const double *c,
+                            unsigned long long *tab_c, unsigned *tab_e) {
+    const int nr = min(*n_rows, CSR_HUGE_CAP);
+    for (int ri = 0; ri < nr; ri++) {
+        const int64_t r = rows[ri];
+        const int64_t s0 = start[r], len = start[r + 1] - s0;
+        unsigned long long *tc = tab_c + (int64_t)ri * n;
+        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < len;
+             i += (int64_t)gridDim.x * blockDim.x) {
+            const uint32_t e = slot_e[s0 + i];
+            const int32_t hd = slot_h[s0 + i];
+            if (PHASE == 0) atomicMin(&tc[hd], cost_key(c[e]));
+            else if (cost_key(c[e]) == tc[hd]) atomicMax(&tab_e[(int64_t)ri * n + hd], e);
+        }
+    }
+}
+struct HugeHit {
+    const unsigned long long *tab_c;
+    const int32_t *n_rows;
+    int64_t n;
+    __device__ int64_t operator()(int64_t i) const {
+        return (i / n < min(*n_rows, CSR_HUGE_CAP) && tab_c[i] != ~0ull) ? 1 : 0;
+    }
+};
+__global__ void k_huge_write(const int64_t *start, const int32_t *rows, const int32_t *n_rows, int64_t n,
+                             const unsigned long long *tab_c, const unsigned *tab_e, const int64_t *pos,
+                             const double *c, int32_t *slot_h, double *slot_c, int64_t *dcnt) {
+    const int nr = min(*n_rows, CSR_HUGE_CAP);
+    for (int ri = 0; ri < nr; ri++) {
+        const int64_t r = rows[ri], s0 = start[r];
+        const int64_t base = pos[(int64_t)ri * n];
+        for (int64_t hd = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; hd < n;
+             hd += (int64_t)gridDim.x * blockDim.x) {
+            const int64_t i = (int64_t)ri * n + hd;
+            if (tab_c[i] == ~0ull) continue;
+            const int64_t q = s0 + pos[i] - base;
+            slot_h[q] = (int32_t)hd;
+            slot_c[q] = c[tab_e[i]];
+        }
+        if (blockIdx.x == 0 && threadIdx.x == 0) dcnt[r] = pos[(int64_t)ri * n + n] - base;
+    }
+}
+
+struct DCount {
+    const int64_t *d;
+    int64_t n;
+    __device__ int64_t operator()(int64_t i) const { return i < n ? d[i] : 0; }
+};
+
+// deduplicated rows to their CSR positions: a warp per row of <= CSR_MED_MAX
+// deduplicated arcs, a CTA per listed longer row
+__global__ void k_csr_emit(const int64_t *start, const int64_t *ro, int64_t n, const int32_t *slot_h,
+                           const double *slot_c, int64_t *ot, int64_t *oh, double *oc) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n;
+         r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t s0 = start[r], d0 = ro[r], len = ro[r + 1] - d0;
+        if (start[r + 1] - s0 > CSR_MED_MAX) continue;  // k_csr_emit_long
+        for (int64_t k = lane; k < len; k += 32) {
+            ot[d0 + k] = r;
+            oh[d0 + k] = slot_h[s0 + k];
+            oc[d0 + k] = slot_c[s0 + k];
+        }
+    }
+}
+__global__ void k_csr_emit_long(const int64_t *__restrict__ start, const int64_t *__restrict__ ro, int64_t n,
+                                const int32_t *__restrict__ lists, const int32_t *__restrict__ n_list,
+                                const int32_t *__restrict__ slot_h, const double *__restrict__ slot_c,
+                                int64_t *__restrict__ ot, int64_t *__restrict__ oh, double *__restrict__ oc) {
+    // few rows, possibly very long (b-bar): the whole grid copies one row at a time
+    const int n_long = n_list[CL_LONG], n_huge = min(n_list[CL_HUGE], CSR_HUGE_CAP);
+    for (int li = 0; li < n_long + n_huge; li++) {
+        const int64_t r = li < n_long ? lists[CL_LONG * n + li] : lists[CL_HUGE * n + li - n_long];
+        const int64_t s0 = start[r], d0 = ro[r], len = ro[r + 1] - d0;
+        for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < len;
+             k += (int64_t)gridDim.x * blockDim.x) {
+            ot[d0 + k] = r;
+            oh[d0 + k] = slot_h[s0 + k];
+            oc[d0 + k] = slot_c[s0 + k];
+        }
+    }
+}
 
 }  // namespace
 
@@ -230,7 +602,8 @@ int assemble_supplies(Ctx &c, int64_t **d_sup, int64_t *n) {
     return W1G_OK;
 }
 
-int net_run(Ctx &c, const int64_t *d_sup, int64_t n, int64_t *n_arcs) {
+// fallback for rows longer than CSR_LONG_MAX arcs: one (tail, head) radix sort
+static int net_run_sorted(Ctx &c, const int64_t *d_sup, int64_t n, int64_t *n_arcs) {
     c.net_valid = false;
     const int64_t m = c.n_arcs;
     const int64_t *t = ptr<int64_t>(c.arc_t), *h = ptr<int64_t>(c.arc_h);
@@ -285,6 +658,105 @@ int net_run(Ctx &c, const int64_t *d_sup, int64_t n, int64_t *n_arcs) {
     W1G_TRY(scan_i64(c, RowCount{rowcnt, n}, n + 1, ro, nullptr));
     W1G_TRY(flags_fetch(c, F_TOTAL, 1));
     mm = m > 0 ? c.h_pinned[F_TOTAL] : 0;
+    if (d_sup != ptr<int64_t>(c.net_sup))
+        W1G_CUDA(cudaMemcpyAsync(c.net_sup.p, d_sup, sizeof(int64_t) * n, cudaMemcpyDeviceToDevice, c.stream));
+    c.net_n = n;
+    c.net_m = mm;
+    c.net_valid = true;
+    *n_arcs = mm;
+    return W1G_OK;
+}
+
+int net_run(Ctx &c, const int64_t *d_sup, int64_t n, int64_t *n_arcs) {
+    c.net_valid = false;
+    const int64_t m = c.n_arcs;
+    const int64_t *t = ptr<int64_t>(c.arc_t), *h = ptr<int64_t>(c.arc_h);
+    const double *cs = ptr<double>(c.arc_c);
+    SubTimer T(c, "csr");
+    int64_t *ro, *ot, *oh, *start, *dcnt;
+    double *oc, *slot_c;
+    unsigned *cnt, *cursor, *tab_e;
+    unsigned long long *tab_c;
+    int32_t *slot_h, *lists;
+    uint32_t *slot_e;
+    W1G_TRY(ensure(c.net_ro, (size_t)n + 2, &ro));
+    W1G_TRY(ensure(c.net_t, (size_t)m + 1, &ot));
+    W1G_TRY(ensure(c.net_h, (size_t)m + 1, &oh));
+    W1G_TRY(ensure(c.net_c, (size_t)m + 1, &oc));
+    W1G_TRY(ensure(c.scr[13], (size_t)2 * (n + 2), &cnt));
+    cursor = cnt + n + 2;
+    W1G_TRY(ensure(c.scr[3], (size_t)n + 2, &start));
+    W1G_TRY(ensure(c.scr[5], (size_t)n + 1, &dcnt));
+    W1G_TRY(ensure(c.scr[6], (size_t)3 * (n + 1), &lists));
+    W1G_TRY(ensure(c.scr[0], (size_t)m + 1, &slot_h));
+    W1G_TRY(ensure(c.scr[2], (size_t)m + 1, &slot_e));
+    W1G_TRY(ensure(c.scr[4], (size_t)m + 1, &slot_c));
+    W1G_TRY(ensure(c.scr[7], (size_t)CSR_HUGE_CAP * (n + 1), &tab_c));
+    W1G_TRY(ensure(c.scr[8], (size_t)CSR_HUGE_CAP * (n + 1), &tab_e));
+    int64_t *hpos;
+    W1G_TRY(ensure(c.scr[9], (size_t)CSR_HUGE_CAP * n + 2, &hpos));
+    int32_t *n_list = reinterpret_cast<int32_t *>(dflags(c) + F_MISC2);  // 3 counters (F_MISC2..)
+    W1G_TRY(flags_reset(c));
+    W1G_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned) * 2 * (n + 2), c.stream));
+    // validation is checked at the one host round trip at the end; invalid
+    // arcs are never bucketed, so nothing is written out of range meanwhile
+    k_csr_count<<<gs(c, m > n ? m : n), 256, 0, c.stream>>>(d_sup, n, t, h, cs, m, cnt, dflags(c));
+    W1G_CHECK_LAUNCH();
+    W1G_TRY(scan_i64(c, RowLen{cnt, n}, n + 1, start, nullptr));
+    if (m > 0) {
+        k_csr_scatter<<<gs(c, m), 256, 0, c.stream>>>(t, h, m, n, start, cursor, slot_h, slot_e);
+        W1G_CHECK_LAUNCH();
+    }
+    T.mark("bucket");
+    if (n > 0) {
+        k_csr_short_rows<<<grid_for(n * 32, 256, 16u * c.sm_count), 256, 0, c.stream>>>(
+            start, n, slot_h, slot_e, cs, slot_c, dcnt, lists, n_list, dflags(c));
+        W1G_CHECK_LAUNCH();
+        T.mark("short");
+        k_csr_med_rows<<<8 * c.sm_count, CSR_MB, 0, c.stream>>>(start, lists + CL_MED * n, n_list + CL_MED,
+                                                                slot_h, slot_e, cs, slot_c, dcnt);
+        W1G_CHECK_LAUNCH();
+        k_csr_long_rows<<<c.sm_count, CSR_LB, 0, c.stream>>>(start, lists + CL_LONG * n, n_list + CL_LONG, slot_h,
+                                                             slot_e, cs, slot_c, dcnt);
+        W1G_CHECK_LAUNCH();
+        T.mark("med_long");
+        const int32_t *hrows = lists + CL_HUGE * n, *nh = n_list + CL_HUGE;
+        const unsigned gh = grid_for((int64_t)CSR_HUGE_CAP * n, 256, 8u * c.sm_count);
+        k_huge_init<<<gh, 256, 0, c.stream>>>(nh, n, tab_c, tab_e);
+        W1G_CHECK_LAUNCH();
+        k_huge_fold<0><<<gs(c, m), 256, 0, c.stream>>>(start, hrows, nh, n, slot_h, slot_e, cs, tab_c, tab_e);
+        W1G_CHECK_LAUNCH();
+        k_huge_fold<1><<<gs(c, m), 256, 0, c.stream>>>(start, hrows, nh, n, slot_h, slot_e, cs, tab_c, tab_e);
+        W1G_CHECK_LAUNCH();
+        W1G_TRY(scan_i64(c, HugeHit{tab_c, nh, n}, (int64_t)CSR_HUGE_CAP * n + 1, hpos, nullptr));
+        k_huge_write<<<gs(c, n), 256, 0, c.stream>>>(start, hrows, nh, n, tab_c, tab_e, hpos, cs, slot_h, slot_c,
+                                                     dcnt);
+        W1G_CHECK_LAUNCH();
+    }
+    T.mark("huge");
+    // row_offsets = [0, cumsum(bincount(t, n))], network.py:84-85
+    W1G_TRY(scan_i64(c, DCount{dcnt, n}, n + 1, ro, dflags(c) + F_TOTAL));
+    if (n > 0) {
+        k_csr_emit<<<grid_for(n * 32, 256, 16u * c.sm_count), 256, 0, c.stream>>>(start, ro, n, slot_h, slot_c, ot,
+                                                                                  oh, oc);
+        W1G_CHECK_LAUNCH();
+        k_csr_emit_long<<<2 * c.sm_count, 256, 0, c.stream>>>(start, ro, n, lists, n_list, slot_h, slot_c, ot, oh, oc);
+        W1G_CHECK_LAUNCH();
+    }
+    W1G_TRY(flags_fetch(c, 0, F_NSLOTS / 2));
+    T.mark("emit");
+    // network.py:55-68, in the reference's order
+    if (c.h_pinned[F_MISC0] != 0) {
+        set_error("unbalanced supplies (sum = %lld)", (long long)c.h_pinned[F_MISC0]);
+        return W1G_ENETWORK;
+    }
+    const int64_t bits = c.h_pinned[F_NET_ERR];
+    if (bits & 1) { set_error("arc endpoint out of range"); return W1G_ENETWORK; }
+    if (bits & 2) { set_error("self-loop arc"); return W1G_ENETWORK; }
+    if (bits & 4) { set_error("non-finite arc cost"); return W1G_ENETWORK; }
+    if (bits & 8) { set_error("negative arc cost"); return W1G_ENETWORK; }
+    if (c.h_pinned[F_OVERFLOW]) return net_run_sorted(c, d_sup, n, n_arcs);
+    const int64_t mm = c.h_pinned[F_TOTAL];
     if (d_sup != ptr<int64_t>(c.net_sup))
         W1G_CUDA(cudaMemcpyAsync(c.net_sup.p, d_sup, sizeof(int64_t) * n, cudaMemcpyDeviceToDevice, c.stream));
     c.net_n = n;

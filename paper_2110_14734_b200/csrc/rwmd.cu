@@ -649,7 +649,7 @@ int rwmd_run(Ctx &c, double *L, double *LA, double *LB) {
     }
     double h[2];
     W1G_CUDA(cudaMemcpyAsync(h, dres, sizeof(double) * 2, cudaMemcpyDeviceToHost, c.stream));
-    W1G_CUDA(cudaStreamSynchronize(c.stream));
+    W1G_TRY(stream_sync(c));
     *LA = h[0];
     *LB = h[1];
     *L = h[1] > h[0] ? h[1] : h[0];  // python max(l_a, l_b)
@@ -706,7 +706,7 @@ int rwmd_range_run(Ctx &c, int side, int64_t begin, int64_t end, double *partial
                           box64, sbox, best, terms));
     W1G_TRY(pairwise_sum(c, terms + begin, n_src, dres, c.scr[17], c.scr[18], c.scr[19]));
     W1G_CUDA(cudaMemcpyAsync(partial, dres, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
-    W1G_CUDA(cudaStreamSynchronize(c.stream));
+    W1G_TRY(stream_sync(c));
     return W1G_OK;
 }
 

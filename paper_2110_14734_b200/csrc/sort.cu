@@ -62,9 +62,9 @@ __device__ __forceinline__ unsigned long long st_make(unsigned epoch, unsigned l
 // sorts share one launch and fill twice the SMs.
 constexpr int RS_JOBS = 2;
 struct PassJob {
-    KeyPtrs src, dst;
-    const uint32_t *vsrc;
-    uint32_t *vdst;
+    KeyPtrs a, b;                  // the two key buffers (ping-pong)
+    uint32_t *va, *vb;             // the two payload buffers
+    const int8_t *plan;            // this digit's plan entry: -1 skip, 0 a->b, 1 b->a
     const uint32_t *dhist;         // this digit's global histogram
     unsigned long long *status;    // per-tile status words
     int64_t n;
@@ -97,13 +97,21 @@ __global__ void __launch_bounds__(RS_BLOCK) k_rs_onesweep(const __grid_constant_
     __syncthreads();
     const int jb = (A.njobs > 1 && (int)s_tile >= A.tile0[1]) ? 1 : 0;
     const PassJob &J = A.j[jb];
+    // the digit plan is made on the device (k_rs_plan): a digit shared by every
+    // key of this job is skipped without a host round trip
+    const int par = *J.plan;
+    if (par < 0) return;  // CTA-uniform
+    const KeyPtrs &src = par ? J.b : J.a;
+    const KeyPtrs &dst = par ? J.a : J.b;
+    const uint32_t *vsrc = par ? J.vb : J.va;
+    uint32_t *vdst = par ? J.va : J.vb;
     const int shift = A.shift;
     const int64_t n = J.n;
     unsigned long long *status = J.status;
     const int64_t tile = (int64_t)s_tile - A.tile0[jb];
     const int64_t tbase = tile * RS_TILE;
     const int tn = (n - tbase) < RS_TILE ? (int)(n - tbase) : RS_TILE;
-    const uint64_t *kd = J.src.k[DW];
+    const uint64_t *kd = src.k[DW];
     const unsigned lt = lanemask_lt();
 
     // 1. stable rank inside the tile (warp w owns items [w*512, (w+1)*512), striped)
@@ -200,8 +208,8 @@ __global__ void __launch_bounds__(RS_BLOCK) k_rs_onesweep(const __grid_constant_
             const int d = dig[i];
             const int lp = t_start[d] + whist[wid][d] + rank[i];
 #pragma unroll
-            for (int m = 0; m < M; m++) s_key[m * RS_TILE + lp] = J.src.k[DW + m][tbase + li];
-            s_val[lp] = J.vsrc[tbase + li];
+            for (int m = 0; m < M; m++) s_key[m * RS_TILE + lp] = src.k[DW + m][tbase + li];
+            s_val[lp] = vsrc[tbase + li];
         }
     }
     __syncthreads();
@@ -211,8 +219,56 @@ __global__ void __launch_bounds__(RS_BLOCK) k_rs_onesweep(const __grid_constant_
         const int d = (int)((k0 >> shift) & 255);
         const uint32_t pos = g_base[d] + (uint32_t)j - t_start[d];
 #pragma unroll
-        for (int m = 0; m < M; m++) J.dst.k[DW + m][pos] = s_key[m * RS_TILE + j];
-        J.vdst[pos] = s_val[j];
+        for (int m = 0; m < M; m++) dst.k[DW + m][pos] = s_key[m * RS_TILE + j];
+        vdst[pos] = s_val[j];
+    }
+}
+
+// digit plan per job: plan[j*RS_PLAN + d] = parity of the pass (-1: digit
+// uniform over all keys, or beyond top_bits) and plan[j*RS_PLAN + 32] = the
+// parity after the last pass (1: the result sits in the b buffers)
+constexpr int RS_PLAN = 40;
+struct PlanArgs {
+    const uint32_t *hist[RS_JOBS];
+    int64_t n[RS_JOBS];
+    int njobs, words, top_bits;
+    int8_t *plan;
+};
+__global__ void k_rs_plan(const __grid_constant__ PlanArgs A) {
+    __shared__ int8_t act[RS_JOBS][32];
+    const int t = threadIdx.x;  // (job, digit)
+    const int j = t / 32, d = t % 32;
+    if (j < A.njobs) {
+        bool active = false;
+        const int w = d / 8;
+        const int dmax = (w == A.words - 1) ? (A.top_bits + 7) / 8 : 8;
+        if (w < A.words && d % 8 < dmax) {
+            const uint32_t *h = A.hist[j] + d * 256;
+            bool uniform = false;
+            for (int q = 0; q < 256; q++) uniform |= h[q] == (uint32_t)A.n[j];
+            active = !uniform;
+        }
+        act[j][d] = active;
+    }
+    __syncthreads();
+    if (j < A.njobs && d == 0) {
+        int par = 0;
+        for (int e = 0; e < 32; e++) {
+            A.plan[j * RS_PLAN + e] = act[j][e] ? (int8_t)par : (int8_t)-1;
+            par ^= act[j][e];
+        }
+        A.plan[j * RS_PLAN + 32] = (int8_t)par;
+    }
+}
+
+// result in the b buffers (odd number of passes): copy payload and top key word back
+__global__ void k_rs_fixup(const int8_t *final_par, const uint32_t *vb, uint32_t *va, const uint64_t *kb,
+                           uint64_t *ka, int64_t n) {
+    if (*final_par == 0) return;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        va[i] = vb[i];
+        ka[i] = kb[i];
     }
 }
 
@@ -288,7 +344,14 @@ int radix_sort_multi(Ctx &c, const SortJob *jobs, int njobs, int words, int top_
         c.sort_epoch = 0;
     }
     unsigned *tickets = hist[0] + nh;  // 64 per-pass tile tickets, shared by the jobs of a launch
+    int8_t *plan;
+    W1G_TRY(ensure(c.sort_scr[0][7], (size_t)RS_JOBS * RS_PLAN, &plan));
     W1G_CUDA(cudaMemsetAsync(tickets, 0, sizeof(unsigned) * 64, c.stream));
+    PlanArgs P;
+    P.njobs = nj;
+    P.words = words;
+    P.top_bits = top_bits;
+    P.plan = plan;
     for (int j = 0; j < nj; j++) {
         W1G_CUDA(cudaMemsetAsync(hist[j], 0, sizeof(uint32_t) * nh, c.stream));
         unsigned g = grid_for(J[j]->n, 512, 2u * c.sm_count);
@@ -297,58 +360,30 @@ int radix_sort_multi(Ctx &c, const SortJob *jobs, int njobs, int words, int top_
             W1G_CUDA(cudaFuncSetAttribute(k_rs_hist_all, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
         k_rs_hist_all<<<g, 512, sm, c.stream>>>(a[j], words, J[j]->n, hist[j]);
         W1G_CHECK_LAUNCH();
+        P.hist[j] = hist[j];
+        P.n[j] = J[j]->n;
     }
-    W1G_TRY(stage_ensure(c, sizeof(uint32_t) * nh * nj));
-    uint32_t *hh = static_cast<uint32_t *>(c.h_stage);
-    for (int j = 0; j < nj; j++)
-        W1G_CUDA(cudaMemcpyAsync(hh + j * nh, hist[j], sizeof(uint32_t) * nh, cudaMemcpyDeviceToHost, c.stream));
-    W1G_CUDA(cudaStreamSynchronize(c.stream));
-    // digits to sort per job (a digit shared by every key of a job is skipped for it)
-    bool need[RS_JOBS][32];
-    for (int j = 0; j < nj; j++)
-        for (int w = 0; w < words; w++) {
-            const int jmax = (w == words - 1) ? (top_bits + 7) / 8 : 8;
-            for (int d = 0; d < 8; d++) {
-                bool uniform = false;
-                if (d < jmax) {
-                    const uint32_t *h = hh + j * nh + (w * 8 + d) * 256;
-                    for (int q = 0; q < 256; q++)
-                        if (h[q] == (uint32_t)J[j]->n) {
-                            uniform = true;
-                            break;
-                        }
-                }
-                need[j][w * 8 + d] = d < jmax && !uniform;
-            }
-        }
-    KeyPtrs *src[RS_JOBS], *dst[RS_JOBS];
-    uint32_t *vsrc[RS_JOBS], *vdst[RS_JOBS];
-    for (int j = 0; j < nj; j++) {
-        src[j] = &a[j];
-        dst[j] = &b[j];
-        vsrc[j] = J[j]->vals;
-        vdst[j] = vb[j];
-    }
+    k_rs_plan<<<1, 32 * RS_JOBS, 0, c.stream>>>(P);
+    W1G_CHECK_LAUNCH();
+    // every digit that may be active is launched; the kernels of skipped digits exit at once
+    const int ndig = (words - 1) * 8 + (top_bits + 7) / 8;
     int launch = 0;
-    for (int dg = 0; dg < words * 8; dg++) {
+    bool large = false;
+    for (int j = 0; j < nj; j++) large |= J[j]->n >= RS_LARGE_N;
+    for (int dg = 0; dg < ndig; dg++) {
         PassArgs A;
-        A.njobs = 0;
-        bool large = false;
-        int idx[RS_JOBS];
+        A.njobs = nj;
         for (int j = 0; j < nj; j++) {
-            if (!need[j][dg]) continue;
-            PassJob &P = A.j[A.njobs];
-            P.src = *src[j];
-            P.dst = *dst[j];
-            P.vsrc = vsrc[j];
-            P.vdst = vdst[j];
-            P.dhist = hist[j] + dg * 256;
-            P.status = status[j];
-            P.n = J[j]->n;
-            large |= J[j]->n >= RS_LARGE_N;
-            idx[A.njobs++] = j;
+            PassJob &Q = A.j[j];
+            Q.a = a[j];
+            Q.b = b[j];
+            Q.va = J[j]->vals;
+            Q.vb = vb[j];
+            Q.plan = plan + j * RS_PLAN + dg;
+            Q.dhist = hist[j] + dg * 256;
+            Q.status = status[j];
+            Q.n = J[j]->n;
         }
-        if (A.njobs == 0) continue;
         const int w = dg / 8;
         c.sort_epoch = (c.sort_epoch + 1) & 0x3fffffffu;
         if (c.sort_epoch == 0) c.sort_epoch = 1;
@@ -357,24 +392,12 @@ int radix_sort_multi(Ctx &c, const SortJob *jobs, int njobs, int words, int top_
         A.epoch = c.sort_epoch;
         // large inputs: 8192-key tiles when the staged words fit in shared memory
         W1G_TRY(dispatch_pass(words, words - w, c, A, large && words - w <= 2));
-        for (int q = 0; q < A.njobs; q++) {
-            const int j = idx[q];
-            KeyPtrs *t = src[j];
-            src[j] = dst[j];
-            dst[j] = t;
-            uint32_t *tv = vsrc[j];
-            vsrc[j] = vdst[j];
-            vdst[j] = tv;
-        }
     }
-    for (int j = 0; j < nj; j++)
-        if (vsrc[j] != J[j]->vals) {
-            // result lives in the scratch buffers: copy the payload and the top key word back
-            W1G_CUDA(cudaMemcpyAsync(J[j]->vals, vsrc[j], sizeof(uint32_t) * J[j]->n, cudaMemcpyDeviceToDevice,
-                                     c.stream));
-            W1G_CUDA(cudaMemcpyAsync(J[j]->keys[words - 1], src[j]->k[words - 1], sizeof(uint64_t) * J[j]->n,
-                                     cudaMemcpyDeviceToDevice, c.stream));
-        }
+    for (int j = 0; j < nj; j++) {
+        k_rs_fixup<<<grid_for(J[j]->n, 256, 8u * c.sm_count), 256, 0, c.stream>>>(
+            plan + j * RS_PLAN + 32, vb[j], J[j]->vals, b[j].k[words - 1], J[j]->keys[words - 1], J[j]->n);
+        W1G_CHECK_LAUNCH();
+    }
     return W1G_OK;
 }
 
@@ -464,7 +487,7 @@ int sort_lex2_multi(Ctx &c, const Lex2Job *jobs, int njobs) {
         }
     }
     W1G_CUDA(cudaMemcpyAsync(&c.h_pinned[F_MISC2], dt, sizeof(int64_t) * njobs, cudaMemcpyDeviceToHost, c.stream));
-    W1G_CUDA(cudaStreamSynchronize(c.stream));
+    W1G_TRY(stream_sync(c));
     // elements of primary-tie runs: sort them by (primary, secondary), put them back
     SortJob tj[RS_JOBS];
     uint32_t *tpos[RS_JOBS], *pl[RS_JOBS];
@@ -527,6 +550,6 @@ extern "C" int w1g_debug_radix_sort(w1g_ctx *c, const uint64_t *keys, int words,
     if (n) W1G_CUDA(cudaMemcpyAsync(v, h, sizeof(uint32_t) * n, cudaMemcpyHostToDevice, c->stream));
     W1G_TRY(radix_sort(*c, k, words, v, n, 64));
     if (n) W1G_CUDA(cudaMemcpyAsync(perm, v, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost, c->stream));
-    W1G_CUDA(cudaStreamSynchronize(c->stream));
+    W1G_TRY(stream_sync(*c));
     return W1G_OK;
 }

@@ -874,7 +874,7 @@ int tree_run(Ctx &c, const double2 *pts, int64_t n, int64_t *n_nodes, int32_t *d
         W1G_CUDA(cudaLaunchCooperativeKernel((void *)k_tree_coop, G, 256, args, smem, c.stream));
         W1G_CHECK_LAUNCH();
         W1G_CUDA(cudaMemcpyAsync(c.h_pinned + F_ACTIVE, lv, sizeof(int32_t), cudaMemcpyDeviceToHost, c.stream));
-        W1G_CUDA(cudaStreamSynchronize(c.stream));
+        W1G_TRY(stream_sync(c));
         levels = *reinterpret_cast<int32_t *>(c.h_pinned + F_ACTIVE) & 0x3fffffff;
     } else if (n > LOCAL_MAX) {
         // fallback for very large inputs: one launch per phase, host polls per batch
@@ -899,7 +899,7 @@ int tree_run(Ctx &c, const double2 *pts, int64_t n, int64_t *n_nodes, int32_t *d
             }
             W1G_CUDA(cudaMemcpyAsync(c.h_pinned + F_ACTIVE, cnt + level % 3, sizeof(int32_t),
                                      cudaMemcpyDeviceToHost, c.stream));
-            W1G_CUDA(cudaStreamSynchronize(c.stream));
+            W1G_TRY(stream_sync(c));
             const int32_t live = *reinterpret_cast<int32_t *>(c.h_pinned + F_ACTIVE);
             if (live == 0 || level > max_levels) break;
         }
@@ -918,7 +918,7 @@ int tree_run(Ctx &c, const double2 *pts, int64_t n, int64_t *n_nodes, int32_t *d
     T.mark("local");
     W1G_CUDA(cudaMemcpyAsync(c.h_pinned + F_DUP, dflags(c) + F_DUP, sizeof(int64_t), cudaMemcpyDeviceToHost,
                              c.stream));
-    W1G_CUDA(cudaStreamSynchronize(c.stream));
+    W1G_TRY(stream_sync(c));
     if (c.h_pinned[F_DUP]) {
         set_error("split tree input contains duplicate points");
         return W1G_EDUPLICATE;

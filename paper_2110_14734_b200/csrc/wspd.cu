@@ -331,7 +331,7 @@ int wspd_run(Ctx &c, double s, int reference_order, int64_t *n_pairs) {
                 W1G_CUDA(cudaMemcpyAsync(c.h_pinned + F_MISC0, ctr, sizeof(int64_t) * 8, cudaMemcpyDeviceToHost, c.stream));
                 W1G_CUDA(cudaMemcpyAsync(c.h_pinned + F_PAIR_OVF, dflags(c) + F_PAIR_OVF, sizeof(int64_t) * 5,
                                          cudaMemcpyDeviceToHost, c.stream));
-                W1G_CUDA(cudaStreamSynchronize(c.stream));
+                W1G_TRY(stream_sync(c));
                 level = (int)(c.h_pinned[F_MISC0 + 6] & 0x7fffffff);
                 const int64_t live = c.h_pinned[F_MISC0 + level % 3];
                 if (c.h_pinned[F_FRONT_OVF] || live > front_cap) {
@@ -357,7 +357,7 @@ int wspd_run(Ctx &c, double s, int reference_order, int64_t *n_pairs) {
             W1G_CUDA(cudaMemcpyAsync(c.h_pinned + F_MISC0, ctr, sizeof(int64_t) * 8, cudaMemcpyDeviceToHost, c.stream));
             W1G_CUDA(cudaMemcpyAsync(c.h_pinned + F_PAIR_OVF, dflags(c) + F_PAIR_OVF, sizeof(int64_t) * 5,
                                      cudaMemcpyDeviceToHost, c.stream));
-            W1G_CUDA(cudaStreamSynchronize(c.stream));
+            W1G_TRY(stream_sync(c));
             const int64_t live = c.h_pinned[F_MISC0 + level % 3];
             if (c.h_pinned[F_FRONT_OVF] || live > front_cap) {
                 ovf = true;

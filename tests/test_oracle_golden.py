@@ -8,7 +8,7 @@ bit before it is trusted as the checker for the CUDA path.
 import numpy as np
 import pytest
 
-from conftest import bits_equal, golden_cases, load_golden
+from conftest import bits_equal, golden_cases, load_golden, numpy_build_network, row_class_arcs
 from oracle import w1oracle as O
 
 
@@ -81,3 +81,14 @@ def test_error_paths():
         O.build_network([1, -2], [0], [1], [1.0])
     net = O.build_network([1, -1], [0, 0], [1, 1], [5.0, 3.0])
     assert net.arc_count == 1 and net.costs[0] == 3.0
+
+
+def test_build_network_matches_numpy_ties():
+    """Duplicate arcs whose minimal costs tie as +0.0 / -0.0: np.minimum.at keeps the later arc."""
+    n, tails, heads, costs = row_class_arcs(1, n=3000, seed=11)
+    sup = np.zeros(n, dtype=np.int64)
+    net = O.build_network(sup, tails, heads, costs)
+    t, h, c, ro = numpy_build_network(sup, tails, heads, costs)
+    assert bits_equal(net.tails, t) and bits_equal(net.heads, h)
+    assert bits_equal(net.costs, c)
+    assert bits_equal(net.row_offsets, ro)
