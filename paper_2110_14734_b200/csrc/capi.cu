@@ -1,6 +1,7 @@
 // capi.cu -- the extern "C" boundary of libw1g.so (include/w1g.h) plus the
 // context, buffer, flag and error plumbing shared by the stage translation
 // units.  Each entry point cites the reference function it replaces.
+#include <chrono>
 #include <cstdarg>
 #include <cstring>
 #include <string>
@@ -609,13 +610,16 @@ int w1g_front_end_device(w1g_ctx *c, const double *d_a, int64_t na, const double
         return W1G_EINVAL;
     }
     cudaEvent_t *ev = c->ev;
+    std::chrono::steady_clock::time_point host_t[10];
     c->n_syncs = 0;
     c->sync_gap_us = 0.0;
     W1G_CUDA(cudaEventRecord(ev[0], c->stream));
+    host_t[0] = std::chrono::steady_clock::now();
     int64_t k0;
     int32_t balanced;
     W1G_TRY(w1g_zero_condense_device(c, d_a, na, d_b, nb, &k0, &balanced));
     W1G_CUDA(cudaEventRecord(ev[1], c->stream));
+    host_t[1] = std::chrono::steady_clock::now();
     info->n_points0 = k0;
     if (k0 == 0 || balanced) {
         // pipeline.py:106-109: empty inputs or identical multisets -> 0.0
@@ -634,6 +638,7 @@ int w1g_front_end_device(w1g_ctx *c, const double *d_a, int64_t na, const double
     double L = 0.0, LA = 0.0, LB = 0.0;
     if (!overlap) W1G_TRY(rwmd_run(*c, &L, &LA, &LB));
     W1G_CUDA(cudaEventRecord(ev[2], c->stream));
+    host_t[2] = std::chrono::steady_clock::now();
     std::thread worker;
     int rc_aux = W1G_OK;
     std::string err_aux;
@@ -667,16 +672,19 @@ int w1g_front_end_device(w1g_ctx *c, const double *d_a, int64_t na, const double
         const double half_width = (1.0 - k) * d / 2.0;
         W1G_TRY(dc_run(*c, d > 0.0 ? d : 0.0, pitch, half_width, seed, &kk));
         W1G_CUDA(cudaEventRecord(ev[3], c->stream));
+    host_t[3] = std::chrono::steady_clock::now();
         info->n_points = kk;
         int64_t nn;
         int32_t depth;
         W1G_TRY(tree_run(*c, ptr<double2>(c->nodes[1].pts), kk, &nn, &depth));
         W1G_CUDA(cudaEventRecord(ev[4], c->stream));
+    host_t[4] = std::chrono::steady_clock::now();
         info->n_tree_nodes = nn;
         info->tree_depth = depth;
         int64_t P;
         W1G_TRY(wspd_run(*c, s, 0, &P));
         W1G_CUDA(cudaEventRecord(ev[5], c->stream));
+    host_t[5] = std::chrono::steady_clock::now();
         info->n_pairs = P;
         info->n_levels_wspd = c->wspd_levels;
         // RWMD joins here: emit and assemble have no cooperative (grid-synchronised) kernels
@@ -684,10 +692,12 @@ int w1g_front_end_device(w1g_ctx *c, const double *d_a, int64_t na, const double
         int64_t M;
         W1G_TRY(emit_run(*c, &M));
         W1G_CUDA(cudaEventRecord(ev[6], c->stream));
+    host_t[6] = std::chrono::steady_clock::now();
         int64_t *dsup, nsup, mm;
         W1G_TRY(assemble_supplies(*c, &dsup, &nsup));
         W1G_TRY(net_run(*c, dsup, nsup, &mm));
         W1G_CUDA(cudaEventRecord(ev[7], c->stream));
+    host_t[7] = std::chrono::steady_clock::now();
         info->n_arcs = mm;
         info->node_count = nsup;
         return W1G_OK;
@@ -715,13 +725,23 @@ int w1g_front_end_device(w1g_ctx *c, const double *d_a, int64_t na, const double
     info->lower_bound = L;
     info->lower_bound_a = LA;
     info->lower_bound_b = LB;
-    W1G_CUDA(cudaEventRecord(ev[9], c->stream));  // everything, RWMD included, is done
+    W1G_CUDA(cudaEventRecord(ev[9], c->stream));
+    host_t[9] = std::chrono::steady_clock::now();  // everything, RWMD included, is done
     W1G_CUDA(cudaEventSynchronize(ev[9]));
     for (int i = 0; i < 7; i++) W1G_CUDA(cudaEventElapsedTime(&info->stage_ms[i], ev[i], ev[i + 1]));
     if (overlap) W1G_CUDA(cudaEventElapsedTime(&info->stage_ms[1], c->aux->ev[0], c->aux->ev[1]));
     W1G_CUDA(cudaEventElapsedTime(&info->stage_ms[7], ev[0], ev[9]));
     if (c->timing)
+    {
         fprintf(stderr, "[w1g syncs] host round trips=%lld idle=%.1fus\n", (long long)c->n_syncs, c->sync_gap_us);
+        fprintf(stderr, "[w1g host]");
+        for (int i = 0; i < 7; i++)
+            fprintf(stderr, " %d=%.1fus", i,
+                    1e-3 * std::chrono::duration_cast<std::chrono::nanoseconds>(host_t[i + 1] - host_t[i]).count());
+        fprintf(stderr, "\n[w1g dev] ");
+        for (int i = 0; i < 8; i++) fprintf(stderr, " %d=%.1fus", i, 1e3 * info->stage_ms[i]);
+        fprintf(stderr, "\n");
+    }
     return W1G_OK;
 }
 

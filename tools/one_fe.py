@@ -10,3 +10,4 @@ ctx = _lib.context()
 c0 = _lib.launch_count(); _front_end(ctx, a, b, p); c1 = _lib.launch_count()
 info = _front_end(ctx, a, b, p)
 print("launches per front end", c1 - c0, "total ms", info.stage_ms[7])
+print("tree_depth", info.tree_depth, "wspd_levels", info.n_levels_wspd, "n_points", info.n_points, "pairs", info.n_pairs)
