@@ -667,9 +667,14 @@ static int net_run_sorted(Ctx &c, const int64_t *d_sup, int64_t n, int64_t *n_ar
     return W1G_OK;
 }
 
+// rows average <= this many arcs: bucket by tail (cheaper for s ~ 1); longer
+// rows (large s) are cheaper to order with one (tail, head) radix sort
+constexpr int64_t CSR_BUCKET_MAX_AVG = 24;
+
 int net_run(Ctx &c, const int64_t *d_sup, int64_t n, int64_t *n_arcs) {
     c.net_valid = false;
     const int64_t m = c.n_arcs;
+    if (m > CSR_BUCKET_MAX_AVG * n) return net_run_sorted(c, d_sup, n, n_arcs);
     const int64_t *t = ptr<int64_t>(c.arc_t), *h = ptr<int64_t>(c.arc_h);
     const double *cs = ptr<double>(c.arc_c);
     SubTimer T(c, "csr");

@@ -21,9 +21,10 @@ namespace {
 
 constexpr int RS_BLOCK = 256;
 constexpr int RS_WARPS = RS_BLOCK / 32;
-// items per thread: 8 (2048-key tiles) in general, 32 (8192-key tiles) for
+// items per thread: 4 (1024-key tiles: 8 CTAs per SM, measured best for the
+// 10^4-10^5-key sorts of the front end) in general, 32 (8192-key tiles) for
 // large inputs so the decoupled look-back chain stays short
-constexpr int RS_IPT_SMALL = 8;
+constexpr int RS_IPT_SMALL = 4;
 constexpr int RS_IPT_LARGE = 32;
 constexpr int64_t RS_LARGE_N = 1 << 20;
 
