@@ -108,41 +108,57 @@ __device__ __forceinline__ void wspd_level(const typename ItemT<ORDER>::T *__res
     int64_t n = *((volatile int64_t *)&k.cnt[level % 3]);
     if (n > cap) n = cap;  // previous level overflowed: its flag is already set
     if (blockIdx.x == 0 && threadIdx.x == 0) k.cnt[(level + 2) % 3] = 0;
-    const int lane = threadIdx.x & 31;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const unsigned lt = lanemask_lt();
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t base = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) & ~31ll; base < n; base += stride) {
-        const int64_t i = base + lane;
+    __shared__ int s_np[8], s_ns[8];
+    __shared__ int64_t s_bp, s_bs;
+    // block-uniform trip count: appends are aggregated per CTA (two global
+    // atomics per CTA and round instead of two per warp)
+    for (int64_t bbase = (int64_t)blockIdx.x * blockDim.x; bbase < n; bbase += stride) {
+        const int64_t i = bbase + threadIdx.x;
         const bool valid = i < n;
         Item it;
         bool ws = false;
         int2 c0 = make_int2(0, 0), c1 = make_int2(0, 0);
         if (valid) {
             it = cur[i];
+            // every load the item may need, issued together
             const NodeGeom gu = geom[it.u], gv = geom[it.v];
+            const int2 lu = lr[it.u], lv = lr[it.v];
             ws = ws_predicate(gu, gv, s);
             if (!ws) {
                 if (gu.dsq > gv.dsq) {  // spanner.py:226-230
-                    const int2 ch = lr[it.u];
-                    c0 = make_int2(ch.x, it.v);
-                    c1 = make_int2(ch.y, it.v);
+                    c0 = make_int2(lu.x, it.v);
+                    c1 = make_int2(lu.y, it.v);
                 } else {                // spanner.py:231-235
-                    const int2 ch = lr[it.v];
-                    c0 = make_int2(it.u, ch.x);
-                    c1 = make_int2(it.u, ch.y);
+                    c0 = make_int2(it.u, lv.x);
+                    c1 = make_int2(it.u, lv.y);
                 }
             }
         }
         const unsigned mp = __ballot_sync(0xffffffffu, valid && ws);
         const unsigned ms = __ballot_sync(0xffffffffu, valid && !ws);
-        int64_t bp = 0, bs = 0;
         if (lane == 0) {
-            if (mp) bp = (int64_t)atomicAdd((unsigned long long *)k.pairs, (unsigned long long)__popc(mp));
-            if (ms) bs = (int64_t)atomicAdd((unsigned long long *)&k.cnt[(level + 1) % 3],
-                                            (unsigned long long)(2 * __popc(ms)));
+            s_np[wid] = __popc(mp);
+            s_ns[wid] = 2 * __popc(ms);
         }
-        bp = __shfl_sync(0xffffffffu, bp, 0);
-        bs = __shfl_sync(0xffffffffu, bs, 0);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int tp = 0, ts = 0;
+            for (int w = 0; w < 8; w++) {
+                const int a = s_np[w], b = s_ns[w];
+                s_np[w] = tp;
+                s_ns[w] = ts;
+                tp += a;
+                ts += b;
+            }
+            s_bp = tp ? (int64_t)atomicAdd((unsigned long long *)k.pairs, (unsigned long long)tp) : 0;
+            s_bs = ts ? (int64_t)atomicAdd((unsigned long long *)&k.cnt[(level + 1) % 3], (unsigned long long)ts) : 0;
+        }
+        __syncthreads();
+        const int64_t bp = s_bp + s_np[wid], bs = s_bs + s_ns[wid];
+        __syncthreads();  // s_* are rewritten by the next round
         if (valid && ws) {
             const int64_t slot = bp + __popc(mp & lt);
             if (slot < pair_cap) {
