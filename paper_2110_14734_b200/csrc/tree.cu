@@ -86,11 +86,17 @@ __global__ void k_presort_keys(const double2 *pts, int64_t n, uint64_t *xl0, uin
 }
 
 __global__ void k_tree_init(int64_t n, Seg *seg, int32_t *pos_seg, int32_t *cnt, const double2 *pts,
-                            const uint32_t *xl, TreeOut o, Seg *local, int32_t *local_cnt) {
+                            const uint32_t *xl, TreeOut o, Seg *local, int32_t *local_cnt,
+                            const uint32_t *yl = nullptr, double2 *xc = nullptr, double2 *yc = nullptr) {
     const bool global_root = n > LOCAL_MAX;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x)
+         i += (int64_t)gridDim.x * blockDim.x) {
         pos_seg[i] = global_root ? 0 : -1;
+        if (xc) {  // inline coordinates for the cooperative level loop
+            xc[i] = pts[xl[i]];
+            yc[i] = pts[yl[i]];
+        }
+    }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         cnt[0] = 0;
         *local_cnt = 0;
@@ -141,20 +147,63 @@ __device__ int warp_prefix_count(const double2 *pts, const uint32_t *list, int l
     return a + __popc(__ballot_sync(0xffffffffu, ok)) - lo;
 }
 
+// the same search on a list that carries its points' coordinates inline (one
+// dependent load per step instead of two)
+__device__ int warp_prefix_count_c(const double2 *list_c, int lo, int hi, int axis, double t, int strict) {
+    const int lane = threadIdx.x & 31;
+    int a = lo, b = hi;
+    while (b - a > 32) {
+        const int step = (b - a + 31) >> 5;
+        const int p = a + lane * step;
+        bool ok = false;
+        if (p < b) {
+            const double2 q = list_c[p];
+            const double c = axis ? q.y : q.x;
+            ok = strict ? (c < t) : (c <= t);
+        }
+        const int k = __popc(__ballot_sync(0xffffffffu, ok));
+        const int na = k ? a + (k - 1) * step + 1 : a;
+        const int nb = k < 32 ? min(b, a + k * step) : b;
+        a = na;
+        b = nb;
+    }
+    const int p = a + lane;
+    bool ok = false;
+    if (p < b) {
+        const double2 q = list_c[p];
+        const double c = axis ? q.y : q.x;
+        ok = strict ? (c < t) : (c <= t);
+    }
+    return a + __popc(__ballot_sync(0xffffffffu, ok)) - lo;
+}
+
 // one warp per segment: bbox, rep, axis, split point, children (spanner.py:124-148)
+// xc / yc (optional): the lists' point coordinates inline, aligned with xl / yl
 __device__ __forceinline__ void tree_segment(int s, const double2 *__restrict__ pts,
                                              const uint32_t *__restrict__ xl,
                                              const uint32_t *__restrict__ yl, const Seg *__restrict__ seg,
                                              int32_t *cnt_next, Seg *seg_next, SegInfo *info,
                                              const TreeOut &o, int64_t *flags, Seg *local,
-                                             int32_t *local_cnt, int parity_next) {
+                                             int32_t *local_cnt, int parity_next,
+                                             const double2 *__restrict__ xc = nullptr,
+                                             const double2 *__restrict__ yc = nullptr) {
     const int lane = threadIdx.x & 31;
     {
         const Seg sg = seg[s];
         const int lo = sg.lo, hi = sg.hi, n = hi - lo;
         const uint32_t r0 = xl[lo];
-        const double xmin = pts[r0].x, xmax = pts[xl[hi - 1]].x;
-        const double ymin = pts[yl[lo]].y, ymax = pts[yl[hi - 1]].y;
+        double xmin, xmax, ymin, ymax;
+        if (xc) {
+            xmin = xc[lo].x;
+            xmax = xc[hi - 1].x;
+            ymin = yc[lo].y;
+            ymax = yc[hi - 1].y;
+        } else {
+            xmin = pts[r0].x;
+            xmax = pts[xl[hi - 1]].x;
+            ymin = pts[yl[lo]].y;
+            ymax = pts[yl[hi - 1]].y;
+        }
         const double ext_x = dsub(xmax, xmin), ext_y = dsub(ymax, ymin);
         SegInfo in{};
         in.lo = lo;
@@ -175,13 +224,14 @@ __device__ __forceinline__ void tree_segment(int s, const double2 *__restrict__ 
         const uint32_t *al = axis ? yl : xl;
         const double amin = axis ? ymin : xmin, amax = axis ? ymax : xmax;
         const double mid = dmul(0.5, dadd(amin, amax));
-        int nl = warp_prefix_count(pts, al, lo, hi, axis, mid, 0);
+        const double2 *alc = axis ? yc : xc;
+        int nl = xc ? warp_prefix_count_c(alc, lo, hi, axis, mid, 0) : warp_prefix_count(pts, al, lo, hi, axis, mid, 0);
         int strict = 0;
         double thr = mid;
         if (nl == 0 || nl == n) {
             strict = 1;  // split off the max-attaining points instead
             thr = amax;
-            nl = warp_prefix_count(pts, al, lo, hi, axis, amax, 1);
+            nl = xc ? warp_prefix_count_c(alc, lo, hi, axis, amax, 1) : warp_prefix_count(pts, al, lo, hi, axis, amax, 1);
         }
         if (lane == 0) {
             const int64_t lid = (int64_t)sg.nid + 1, rid = (int64_t)sg.nid + 2 * (int64_t)nl;
@@ -515,6 +565,14 @@ __global__ void k_tree_flags(const double2 *__restrict__ pts, const uint32_t *__
 }
 
 // stable partition of the other list inside the position's segment
+// destination of position p's other-list entry in the stable partition
+__device__ __forceinline__ int64_t scatter_dest(int64_t p, int f, int64_t excl_p, int64_t excl_lo,
+                                               const SegInfo &in) {
+    const int64_t rt = excl_p - excl_lo;
+    const int64_t rf = (p - in.lo) - rt;
+    return f ? in.lo + rt : in.lo + in.nl + rf;
+}
+
 __device__ __forceinline__ void pos_scatter(int64_t p, int s, int f, int64_t excl_p, int64_t excl_lo,
                                             const SegInfo &in, const uint32_t *__restrict__ xl,
                                             const uint32_t *__restrict__ yl, uint32_t *xl_new,
@@ -583,6 +641,7 @@ struct CoopArgs {
     const double2 *pts;
     int64_t n;
     uint32_t *xl[2], *yl[2];
+    double2 *xc[2], *yc[2];  // the lists' coordinates, inline
     int32_t *pos_seg[2];
     Seg *seg[2];
     SegInfo *info;
@@ -632,33 +691,39 @@ __global__ void __launch_bounds__(256) k_tree_coop(CoopArgs A) {
         const int warps = (gridDim.x * blockDim.x) >> 5;
         for (int s = (blockIdx.x * blockDim.x + tid) >> 5; s < nseg; s += warps)
             tree_segment(s, A.pts, A.xl[cur], A.yl[cur], A.seg[cur], &A.cnt[(level + 1) % 3], A.seg[cur ^ 1],
-                         A.info, A.o, A.flags, A.local, A.local_cnt, cur ^ 1);
+                         A.info, A.o, A.flags, A.local, A.local_cnt, cur ^ 1, A.xc[cur], A.yc[cur]);
         grid.sync();
         // (B) flags and tile-local exclusive prefixes
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
             const int64_t base = (int64_t)t * TP_TILE + tid * TP_IPT;
             int f[TP_IPT];
             int sum = 0;
-            // the flag is a chain of four dependent loads; issue each link for all
-            // items before the next so the chains overlap instead of serialising
+            // the flag needs the position's segment, that segment's split and the
+            // other list's coordinate (inline): two dependent links, each issued
+            // for all items before the next
             int sg[TP_IPT];
-            uint32_t el[TP_IPT];
+            double2 qx[TP_IPT], qy[TP_IPT];
             SegInfo inf[TP_IPT];
 #pragma unroll
-            for (int i = 0; i < TP_IPT; i++) sg[i] = base + i < n ? A.pos_seg[cur][base + i] : -1;
+            for (int i = 0; i < TP_IPT; i++) {
+                const bool in_n = base + i < n;
+                sg[i] = in_n ? A.pos_seg[cur][base + i] : -1;
+                if (in_n) {
+                    qx[i] = A.xc[cur][base + i];
+                    qy[i] = A.yc[cur][base + i];
+                }
+            }
 #pragma unroll
             for (int i = 0; i < TP_IPT; i++) {
                 if (sg[i] >= 0) inf[i] = A.info[sg[i]];
                 else inf[i].axis = 0;
             }
 #pragma unroll
-            for (int i = 0; i < TP_IPT; i++)
-                el[i] = sg[i] >= 0 ? (inf[i].axis ? A.xl[cur][base + i] : A.yl[cur][base + i]) : 0u;
-#pragma unroll
             for (int i = 0; i < TP_IPT; i++) {
                 int v = 0;
                 if (sg[i] >= 0) {
-                    const double c = coord(A.pts, el[i], inf[i].axis);
+                    // split on y: the X-list is partitioned by its points' y, and vice versa
+                    const double c = inf[i].axis ? qx[i].y : qy[i].x;
                     v = (inf[i].strict ? (c < inf[i].thr) : (c <= inf[i].thr)) ? 1 : 0;
                 }
                 f[i] = v;
@@ -690,24 +755,31 @@ __global__ void __launch_bounds__(256) k_tree_coop(CoopArgs A) {
         }
         if (blockIdx.x == 0 && tid == 0) A.cnt[(level + 2) % 3] = 0;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-            // same staging as (B): every dependent load issued for all items at once
+            // same staging as (B): every dependent load issued for all items at
+            // once; the entries to move do not depend on the split and load first
             constexpr int J = TP_TILE / 256;
             int64_t pp[J];
             int sg[J];
             SegInfo inf[J];
             int32_t lp[J], ll[J];
+            uint32_t ex[J], ey[J];
+            double2 cx[J], cy[J];
 #pragma unroll
             for (int j = 0; j < J; j++) {
                 pp[j] = (int64_t)t * TP_TILE + tid + 256 * j;
-                sg[j] = pp[j] < n ? A.pos_seg[cur][pp[j]] : -2;
-            }
-#pragma unroll
-            for (int j = 0; j < J; j++) {
-                if (sg[j] >= 0) {
-                    inf[j] = A.info[sg[j]];
+                const bool in_n = pp[j] < n;
+                sg[j] = in_n ? A.pos_seg[cur][pp[j]] : -2;
+                if (in_n) {
                     lp[j] = A.lpre[pp[j]];
+                    ex[j] = A.xl[cur][pp[j]];
+                    ey[j] = A.yl[cur][pp[j]];
+                    cx[j] = A.xc[cur][pp[j]];
+                    cy[j] = A.yc[cur][pp[j]];
                 }
             }
+#pragma unroll
+            for (int j = 0; j < J; j++)
+                if (sg[j] >= 0) inf[j] = A.info[sg[j]];
 #pragma unroll
             for (int j = 0; j < J; j++)
                 if (sg[j] >= 0) ll[j] = A.lpre[inf[j].lo];
@@ -717,8 +789,19 @@ __global__ void __launch_bounds__(256) k_tree_coop(CoopArgs A) {
                 if (sg[j] < 0) continue;
                 const int64_t ep = (int64_t)s_tp[t] + (lp[j] & 0x7fffffff);
                 const int64_t el = (int64_t)s_tp[inf[j].lo / TP_TILE] + (ll[j] & 0x7fffffff);
-                pos_scatter(pp[j], sg[j], (int)((uint32_t)lp[j] >> 31), ep, el, inf[j], A.xl[cur], A.yl[cur],
-                            A.xl[cur ^ 1], A.yl[cur ^ 1], A.pos_seg[cur ^ 1]);
+                const int64_t np_ = scatter_dest(pp[j], (int)((uint32_t)lp[j] >> 31), ep, el, inf[j]);
+                if (inf[j].axis) {  // split on y: Y-list stays, X-list is partitioned
+                    A.yl[cur ^ 1][pp[j]] = ey[j];
+                    A.yc[cur ^ 1][pp[j]] = cy[j];
+                    A.xl[cur ^ 1][np_] = ex[j];
+                    A.xc[cur ^ 1][np_] = cx[j];
+                } else {
+                    A.xl[cur ^ 1][pp[j]] = ex[j];
+                    A.xc[cur ^ 1][pp[j]] = cx[j];
+                    A.yl[cur ^ 1][np_] = ey[j];
+                    A.yc[cur ^ 1][np_] = cy[j];
+                }
+                A.pos_seg[cur ^ 1][pp[j]] = (pp[j] < inf[j].lo + inf[j].nl) ? inf[j].cl : inf[j].cr;
             }
         }
         grid.sync();
@@ -830,11 +913,20 @@ int tree_run(Ctx &c, const double2 *pts, int64_t n, int64_t *n_nodes, int32_t *d
     W1G_TRY(ensure(c.scr[20], (size_t)seg_cap + 2, &local));
     W1G_TRY(flags_reset(c));
     W1G_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * 16, c.stream));
-    k_tree_init<<<g, 256, 0, c.stream>>>(n, seg[0], pos_seg[0], cnt, pts, xl[0], o, local, local_cnt);
-    W1G_CHECK_LAUNCH();
     int levels = 0;
     const int64_t ntiles = (n + TP_TILE - 1) / TP_TILE;
-    if (n > LOCAL_MAX && ntiles <= COOP_MAX_TILES) {
+    const bool coop = n > LOCAL_MAX && ntiles <= COOP_MAX_TILES;
+    double2 *xc[2] = {nullptr, nullptr}, *yc[2] = {nullptr, nullptr};
+    if (coop) {
+        W1G_TRY(ensure(c.scr[2], (size_t)n, &xc[0]));
+        W1G_TRY(ensure(c.scr[21], (size_t)n, &xc[1]));
+        W1G_TRY(ensure(c.scr[22], (size_t)n, &yc[0]));
+        W1G_TRY(ensure(c.scr[23], (size_t)n, &yc[1]));
+    }
+    k_tree_init<<<g, 256, 0, c.stream>>>(n, seg[0], pos_seg[0], cnt, pts, xl[0], o, local, local_cnt, yl[0], xc[0],
+                                         yc[0]);
+    W1G_CHECK_LAUNCH();
+    if (coop) {
         // the global levels (segments > LOCAL_MAX) in one persistent cooperative launch
         int32_t *lpre, *tsum, *lv;
         W1G_TRY(ensure(c.scr[17], (size_t)n, &lpre));
@@ -847,6 +939,10 @@ int tree_run(Ctx &c, const double2 *pts, int64_t n, int64_t *n_nodes, int32_t *d
         A.xl[1] = xl[1];
         A.yl[0] = yl[0];
         A.yl[1] = yl[1];
+        A.xc[0] = xc[0];
+        A.xc[1] = xc[1];
+        A.yc[0] = yc[0];
+        A.yc[1] = yc[1];
         A.pos_seg[0] = pos_seg[0];
         A.pos_seg[1] = pos_seg[1];
         A.seg[0] = seg[0];
