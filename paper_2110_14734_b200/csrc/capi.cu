@@ -123,6 +123,17 @@ static int download(Ctx &c, void *dst, const void *src, size_t bytes) {
     return W1G_OK;
 }
 
+// page-locked host memory the device can DMA from directly (null / empty: trivially yes)
+static bool is_pinned(const void *p) {
+    if (!p) return true;
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+}
+
 static void invalidate_from_nodes(Ctx &c) {
     c.tree_valid = false;
     c.pairs_valid = false;
@@ -752,13 +763,19 @@ int w1g_front_end(w1g_ctx *c, const double *a, int64_t na, const double *b, int6
     if (na < 0 || nb < 0) return W1G_EINVAL;
     double2 *d;
     W1G_TRY(ensure(c->in_pts, (size_t)(na + nb), &d));
-    // stage both diagrams through pinned memory: one full-speed H2D
     const size_t bytes = sizeof(double2) * (size_t)(na + nb);
-    W1G_TRY(stage_ensure(*c, bytes));
-    W1G_TRY(stream_sync(*c));
-    if (na) memcpy(c->h_stage, a, sizeof(double2) * na);
-    if (nb) memcpy(static_cast<char *>(c->h_stage) + sizeof(double2) * na, b, sizeof(double2) * nb);
-    if (bytes) W1G_CUDA(cudaMemcpyAsync(d, c->h_stage, bytes, cudaMemcpyHostToDevice, c->stream));
+    if (is_pinned(a) && is_pinned(b)) {
+        // page-locked inputs (w1g_host_alloc or any cudaHostAlloc'd memory): DMA directly
+        if (na) W1G_CUDA(cudaMemcpyAsync(d, a, sizeof(double2) * na, cudaMemcpyHostToDevice, c->stream));
+        if (nb) W1G_CUDA(cudaMemcpyAsync(d + na, b, sizeof(double2) * nb, cudaMemcpyHostToDevice, c->stream));
+    } else {
+        // pageable inputs: stage both diagrams through pinned memory, one full-speed H2D
+        W1G_TRY(stage_ensure(*c, bytes));
+        W1G_TRY(stream_sync(*c));
+        if (na) memcpy(c->h_stage, a, sizeof(double2) * na);
+        if (nb) memcpy(static_cast<char *>(c->h_stage) + sizeof(double2) * na, b, sizeof(double2) * nb);
+        if (bytes) W1G_CUDA(cudaMemcpyAsync(d, c->h_stage, bytes, cudaMemcpyHostToDevice, c->stream));
+    }
     return w1g_front_end_device(c, reinterpret_cast<double *>(d), na,
                                 reinterpret_cast<double *>(d + na), nb, s, use_condensation,
                                 delta_mode, delta, k, seed, info);

@@ -82,6 +82,16 @@ def points_of(d) -> np.ndarray:
     return _lib.as_points(pts)
 
 
+def pinned_points(d) -> np.ndarray:
+    """A page-locked (n, 2) float64 copy of a diagram's points.  Passing it to
+    sparsify / approx_w1 lets the front end DMA the input straight to the
+    device instead of staging it through its own pinned buffer."""
+    p = points_of(d)
+    (out,) = _lib.pinned_arrays([(p.shape, np.float64)])
+    out[...] = p
+    return out
+
+
 @dataclass(frozen=True)
 class SuppliedNodes:
     """Deduplicated planar nodes with per-side integer masses (diagram.py:150-187)."""
