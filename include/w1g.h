@@ -59,7 +59,7 @@ typedef struct {
     int32_t short_circuit;  /* empty input or a_mass == b_mass (pipeline.py:106-109) */
     int32_t tree_depth;     /* split tree levels */
     int32_t n_levels_wspd;  /* WSPD frontier levels */
-    int32_t pad;
+    int32_t network_copied; /* 1: the network was written to the w1g_set_network_out target */
     float stage_ms[8];      /* device time per stage: zc, rwmd, dc, tree, wspd, emit, csr, total */
 } w1g_front_end_info;
 
@@ -148,6 +148,12 @@ int w1g_build_network(w1g_ctx *ctx, const int64_t *supplies, int64_t n, int64_t 
 int w1g_assemble(w1g_ctx *ctx, int64_t *node_count, int64_t *n_arcs);
 int w1g_fetch_network(w1g_ctx *ctx, int64_t *supplies, int64_t *tails, int64_t *heads,
                       double *costs, int64_t *row_offsets);
+/* one-shot output target for the NEXT fused front end: when its network fits
+ * (node_count <= node_cap, arcs <= arc_cap) it is copied there inside the call,
+ * overlapping whatever device work is still running (info->network_copied = 1);
+ * page-locked buffers (w1g_host_alloc) give full-speed copies */
+int w1g_set_network_out(w1g_ctx *ctx, int64_t *supplies, int64_t *tails, int64_t *heads, double *costs,
+                        int64_t *row_offsets, int64_t node_cap, int64_t arc_cap);
 
 /* fused front end: pipeline.py:105-130 (zero_condense .. assemble).
  * delta_mode 0: delta from the RWMD bound as the reference (pipeline.py:116-122);

@@ -60,7 +60,7 @@ class FrontEndInfo(ctypes.Structure):
         ("short_circuit", _i32),
         ("tree_depth", _i32),
         ("n_levels_wspd", _i32),
-        ("pad", _i32),
+        ("network_copied", _i32),
         ("stage_ms", ctypes.c_float * 8),
     ]
 
@@ -104,6 +104,7 @@ _PROTOS = [
     ("w1g_build_network", ctypes.c_int, [_vp, _I64P, _i64, _I64P]),
     ("w1g_assemble", ctypes.c_int, [_vp, _I64P, _I64P]),
     ("w1g_fetch_network", ctypes.c_int, [_vp, _I64P, _I64P, _I64P, _F64P, _I64P]),
+    ("w1g_set_network_out", ctypes.c_int, [_vp, _I64P, _I64P, _I64P, _F64P, _I64P, _i64, _i64]),
     ("w1g_front_end", ctypes.c_int,
      [_vp, _F64P, _i64, _F64P, _i64, _f64, ctypes.c_int, ctypes.c_int, _f64, _f64, _u64,
       ctypes.POINTER(FrontEndInfo)]),

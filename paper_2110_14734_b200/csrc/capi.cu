@@ -602,6 +602,28 @@ int w1g_fetch_network(w1g_ctx *c, int64_t *supplies, int64_t *tails, int64_t *he
     return W1G_OK;
 }
 
+int w1g_set_network_out(w1g_ctx *c, int64_t *supplies, int64_t *tails, int64_t *heads, double *costs,
+                        int64_t *row_offsets, int64_t node_cap, int64_t arc_cap) {
+    CTX_CHECK(c);
+    c->net_out = Ctx::NetOut{supplies, tails, heads, row_offsets, costs, node_cap, arc_cap};
+    return W1G_OK;
+}
+
+// the network into the armed output target (asynchronously, on the context stream)
+static int copy_network_out(Ctx &c, int *copied) {
+    *copied = 0;
+    const Ctx::NetOut &o = c.net_out;
+    if (!c.net_valid || !o.sup || c.net_n > o.node_cap || c.net_m > o.arc_cap) return W1G_OK;
+    const size_t n = (size_t)c.net_n, m = (size_t)c.net_m;
+    W1G_TRY(download(c, o.sup, c.net_sup.p, sizeof(int64_t) * n));
+    W1G_TRY(download(c, o.t, c.net_t.p, sizeof(int64_t) * m));
+    W1G_TRY(download(c, o.h, c.net_h.p, sizeof(int64_t) * m));
+    W1G_TRY(download(c, o.c, c.net_c.p, sizeof(double) * m));
+    W1G_TRY(download(c, o.ro, c.net_ro.p, sizeof(int64_t) * (n + 1)));
+    *copied = 1;
+    return W1G_OK;
+}
+
 // ---------------------------------------------------------------- fused front end
 
 static const double SQRT2 = 1.4142135623730951;  // math.sqrt(2.0)
@@ -622,6 +644,10 @@ int w1g_front_end_device(w1g_ctx *c, const double *d_a, int64_t na, const double
     }
     cudaEvent_t *ev = c->ev;
     std::chrono::steady_clock::time_point host_t[10];
+    struct Disarm {  // the output target is one-shot, whatever path this call takes
+        Ctx &c;
+        ~Disarm() { c.net_out = Ctx::NetOut{}; }
+    } disarm{*c};
     c->n_syncs = 0;
     c->sync_gap_us = 0.0;
     W1G_CUDA(cudaEventRecord(ev[0], c->stream));
@@ -722,6 +748,8 @@ int w1g_front_end_device(w1g_ctx *c, const double *d_a, int64_t na, const double
         return delta;
     };
     int rc = back_end(overlap ? delta : delta_for(L), overlap);
+    // the network leaves for the host while RWMD may still run on the auxiliary stream
+    if (rc == W1G_OK) rc = copy_network_out(*c, &info->network_copied);
     if (worker.joinable()) worker.join();
     if (overlap && c->aux) c->aux->nodes[0] = NodeSet{};
     if (rc != W1G_OK) return rc;
@@ -731,7 +759,10 @@ int w1g_front_end_device(w1g_ctx *c, const double *d_a, int64_t na, const double
     }
     if (overlap) {
         W1G_CUDA(cudaStreamWaitEvent(c->stream, c->aux->ev[1], 0));
-        if (!(L > 0.0)) W1G_TRY(back_end(0.0, false));  // pipeline.py:115: no condensation when L == 0
+        if (!(L > 0.0)) {  // pipeline.py:115: no condensation when L == 0
+            W1G_TRY(back_end(0.0, false));
+            W1G_TRY(copy_network_out(*c, &info->network_copied));
+        }
     }
     info->lower_bound = L;
     info->lower_bound_a = LA;

@@ -146,6 +146,13 @@ struct Ctx {
     int overlap = 1;
     Ctx *aux = nullptr;
 
+    // one-shot host target for the next fused front end's network (w1g_set_network_out)
+    struct NetOut {
+        int64_t *sup = nullptr, *t = nullptr, *h = nullptr, *ro = nullptr;
+        double *c = nullptr;
+        int64_t node_cap = 0, arc_cap = 0;
+    } net_out;
+
     // host round-trip accounting (stream_sync)
     int timing = 0;
     int64_t n_syncs = 0;

@@ -144,11 +144,27 @@ def sparsify(a, b, params: ApproxParams, device: int | None = None
     approx_w1 hands to the solver, or None when the distance short-circuits."""
     ap, bp = points_of(a), points_of(b)
     ctx = _lib.context(device)
+    # arm a page-locked output block sized from the previous network of this
+    # context: the front end then copies the network out inside the call,
+    # overlapping the device work still running (the RWMD stream)
+    out = None
+    hint = getattr(ctx, "net_hint", None)
+    if hint is not None:
+        ncap, mcap = hint
+        out = _lib.pinned_arrays([((ncap,), np.int64), ((mcap,), np.int64), ((mcap,), np.int64),
+                                  ((mcap,), np.float64), ((ncap + 1,), np.int64)])
+        ctx.call("w1g_set_network_out", _lib.i64p(out[0]), _lib.i64p(out[1]), _lib.i64p(out[2]),
+                 _lib.f64p(out[3]), _lib.i64p(out[4]), ncap, mcap)
     info = _front_end(ctx, ap, bp, params)
     diag = _diagnostics(info)
     if info.short_circuit:
         return None, diag
-    return fetch_network(ctx, int(info.node_count), int(info.n_arcs)), diag
+    n, m = int(info.node_count), int(info.n_arcs)
+    ctx.net_hint = (n + n // 8 + 64, m + m // 8 + 1024)
+    if info.network_copied:
+        sup, tails, heads, costs, ro = out
+        return TransshipmentNetwork(n, sup[:n], tails[:m], heads[:m], costs[:m], ro[:n + 1]), diag
+    return fetch_network(ctx, n, m), diag
 
 
 def solve_network(network: TransshipmentNetwork, params: ApproxParams, diag: ApproxDiagnostics) -> float:
