@@ -718,6 +718,7 @@ int w1g_front_end_device(w1g_ctx *c, const double *d_a, int64_t na, const double
     host_t[4] = std::chrono::steady_clock::now();
         info->n_tree_nodes = nn;
         info->tree_depth = depth;
+        if (spawn && c->overlap == 3) W1G_TRY(start_rwmd());
         int64_t P;
         W1G_TRY(wspd_run(*c, s, 0, &P));
         W1G_CUDA(cudaEventRecord(ev[5], c->stream));
@@ -725,7 +726,7 @@ int w1g_front_end_device(w1g_ctx *c, const double *d_a, int64_t na, const double
         info->n_pairs = P;
         info->n_levels_wspd = c->wspd_levels;
         // RWMD joins here: emit and assemble have no cooperative (grid-synchronised) kernels
-        if (spawn && c->overlap != 2) W1G_TRY(start_rwmd());
+        if (spawn && c->overlap == 1) W1G_TRY(start_rwmd());
         int64_t M;
         W1G_TRY(emit_run(*c, &M));
         W1G_CUDA(cudaEventRecord(ev[6], c->stream));
