@@ -346,10 +346,13 @@ struct SortJob {
     int64_t n;
 };
 int radix_sort_multi(Ctx &c, const SortJob *jobs, int njobs, int words, int top_bits = 64);
-// Stable sort of vals (initially the element ids 0..n-1, or any payload that
-// indexes `secondary`) by (primary[i], secondary[vals[i]]): radix sort by the
-// primary word, then only the elements of primary-tie runs by both words.
-// `primary` is indexed by position in the input order, `secondary` by payload.
+// Stable sort of vals (initially the element ids 0..n-1) by (primary[i],
+// secondary[i]) -- both dkey()s of doubles: radix passes over a 32-bit
+// order-preserving compression of the primary (linear in value over its
+// range), then the elements of
+// compressed-key tie runs by the full (primary, secondary, id) -- in place by
+// one thread per run when every run is short, else by a two-word radix sort.
+// `primary` and `secondary` are indexed by element id.
 int sort_lex2(Ctx &c, const uint64_t *primary, const uint64_t *secondary, uint32_t *vals, int64_t n);
 struct Lex2Job {
     const uint64_t *primary, *secondary;

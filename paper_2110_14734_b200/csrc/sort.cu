@@ -417,12 +417,6 @@ int radix_sort(Ctx &c, uint64_t **keys, int words, uint32_t *vals, int64_t n, in
 
 namespace {
 
-__global__ void k_copy_u64(const uint64_t *src, uint64_t *dst, int64_t n) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x)
-        dst[i] = src[i];
-}
-
 struct TieFlag {
     const uint64_t *k;
     int64_t n;
@@ -432,15 +426,18 @@ struct TieFlag {
     }
 };
 
-__global__ void k_tie_gather(TieFlag f, const int64_t *excl, const uint32_t *vals, const uint64_t *sec,
-                             uint32_t *tpos, uint64_t *kl, uint64_t *kh, uint32_t *pl) {
+// the full (primary, secondary) keys of the tie elements (the sorted keys f.k
+// are compressed, so the primary is read through the payload = input position)
+__global__ void k_tie_gather(TieFlag f, const int64_t *excl, const uint32_t *vals, const uint64_t *prim,
+                             const uint64_t *sec, uint32_t *tpos, uint64_t *kl, uint64_t *kh, uint32_t *pl) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < f.n;
          i += (int64_t)gridDim.x * blockDim.x) {
         if (!f(i)) continue;
         const int64_t r = excl[i];
+        const uint32_t v = vals[i];
         tpos[r] = (uint32_t)i;
-        kh[r] = f.k[i];
-        kl[r] = sec[vals[i]];
+        kh[r] = prim[v];
+        kl[r] = sec[v];
         pl[r] = (uint32_t)r;
     }
 }
@@ -458,6 +455,105 @@ __global__ void k_tie_put(const uint32_t *tpos, const uint32_t *tmp, int64_t t, 
         vals[tpos[r]] = tmp[r];
 }
 
+// ---- compressed primary keys: the radix passes run on a 32-bit key that
+// preserves the primary's order weakly (k_key_compress) and elements whose
+// compressed keys tie (true primary ties and compression collisions alike)
+// are ordered afterwards by the full (primary, secondary, input position).
+__global__ void k_key_range(const uint64_t *k, int64_t n, unsigned long long *mm) {
+    unsigned long long lo = ~0ull, hi = 0ull;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned long long v = k[i];
+        lo = v < lo ? v : lo;
+        hi = v > hi ? v : hi;
+    }
+    for (int o = 16; o; o >>= 1) {
+        const unsigned long long a = __shfl_xor_sync(0xffffffffu, lo, o), b = __shfl_xor_sync(0xffffffffu, hi, o);
+        lo = a < lo ? a : lo;
+        hi = b > hi ? b : hi;
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(&mm[0], lo);
+        atomicMax(&mm[1], hi);
+    }
+}
+
+// the primaries are order-preserving keys of doubles (dkey); the compression
+// is linear in VALUE space, (v - vmin) * (2^32 - 1) / (vmax - vmin) rounded
+// down -- monotone under IEEE rounding, and unlike a shifted key range it keeps
+// close values apart however wide the range of exponents is
+__device__ __forceinline__ double dkey_value(unsigned long long k) {
+    return __longlong_as_double((long long)((k >> 63) ? (k & 0x7fffffffffffffffull) : ~k));
+}
+__global__ void k_key_compress(const uint64_t *k, int64_t n, const unsigned long long *mm, uint64_t *out) {
+    const double lo = dkey_value(mm[0]), hi = dkey_value(mm[1]);
+    const double range = hi - lo;
+    const bool flat = !(range > 0.0) || !isfinite(range);
+    const double scale = flat ? 0.0 : 4294967295.0 / range;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        double t = flat ? 0.0 : floor((dkey_value(k[i]) - lo) * scale);
+        t = t < 0.0 ? 0.0 : (t > 4294967295.0 ? 4294967295.0 : t);
+        out[i] = (uint64_t)t;
+    }
+}
+
+// tie runs of at most TIE_SMALL elements: one thread orders its run by
+// (primary, secondary, input position) with an insertion sort; the longest run
+// is reported so the host can take the radix path for long runs instead
+constexpr int TIE_SMALL = 32;
+__global__ void k_tie_runs(const uint64_t *pk, int64_t n, unsigned long long *maxrun, int64_t *count) {
+    unsigned long long mr = 0;
+    int64_t cnt = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t v = pk[i];
+        if (i > 0 && pk[i - 1] == v) continue;  // not a run start
+        int64_t j = i + 1;
+        while (j < n && pk[j] == v && j - i <= TIE_SMALL) j++;
+        const int64_t len = j - i;
+        if (len > 1) {
+            cnt += len;
+            mr = (unsigned long long)len > mr ? (unsigned long long)len : mr;
+        }
+    }
+    for (int o = 16; o; o >>= 1) {
+        const unsigned long long a = __shfl_xor_sync(0xffffffffu, mr, o);
+        mr = a > mr ? a : mr;
+        cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (mr) atomicMax(maxrun, mr);
+        if (cnt) atomicAdd((unsigned long long *)count, (unsigned long long)cnt);
+    }
+}
+
+__global__ void k_tie_small(const uint64_t *pk, int64_t n, const uint64_t *primary, const uint64_t *secondary,
+                            uint32_t *vals) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t v = pk[i];
+        if ((i > 0 && pk[i - 1] == v) || i + 1 >= n || pk[i + 1] != v) continue;  // run starts only
+        int64_t j = i + 1;
+        while (j < n && pk[j] == v) j++;
+        // insertion sort of vals[i..j) by (primary[val], secondary[val], val)
+        for (int64_t a = i + 1; a < j; a++) {
+            const uint32_t x = vals[a];
+            const uint64_t xp = primary[x], xs = secondary[x];
+            int64_t b = a - 1;
+            while (b >= i) {
+                const uint32_t y = vals[b];
+                const uint64_t yp = primary[y], ys = secondary[y];
+                const bool gt = yp > xp || (yp == xp && (ys > xs || (ys == xs && y > x)));
+                if (!gt) break;
+                vals[b + 1] = y;
+                b--;
+            }
+            vals[b + 1] = x;
+        }
+    }
+}
+
 }  // namespace
 
 int sort_lex2_multi(Ctx &c, const Lex2Job *jobs, int njobs) {
@@ -467,47 +563,77 @@ int sort_lex2_multi(Ctx &c, const Lex2Job *jobs, int njobs) {
     }
     uint64_t *pk[RS_JOBS];
     int64_t *excl[RS_JOBS];
+    unsigned long long *mm;  // per job: key min, key max, longest tie run, tie count
     SortJob sj[RS_JOBS];
-    int64_t *dt = ptr<int64_t>(c.flags) + F_MISC2;  // tie counts (F_MISC2, F_MISC3)
+    W1G_TRY(ensure(c.sort_scr[1][3], (size_t)4 * RS_JOBS, &mm));
+    {
+        const unsigned long long init[4 * RS_JOBS] = {~0ull, 0ull, 0ull, 0ull, ~0ull, 0ull, 0ull, 0ull};
+        W1G_CUDA(cudaMemcpyAsync(mm, init, sizeof init, cudaMemcpyHostToDevice, c.stream));
+    }
     for (int j = 0; j < njobs; j++) {
         const int64_t n = jobs[j].n;
         W1G_TRY(ensure(c.lex_scr[j][0], (size_t)n + 1, &pk[j]));
         W1G_TRY(ensure(c.lex_scr[j][1], (size_t)n + 1, &excl[j]));
         if (n > 0) {
-            k_copy_u64<<<grid_for(n, 256, 8u * c.sm_count), 256, 0, c.stream>>>(jobs[j].primary, pk[j], n);
+            const unsigned g = grid_for(n, 256, 8u * c.sm_count);
+            k_key_range<<<g, 256, 0, c.stream>>>(jobs[j].primary, n, mm + 4 * j);
+            W1G_CHECK_LAUNCH();
+            k_key_compress<<<g, 256, 0, c.stream>>>(jobs[j].primary, n, mm + 4 * j, pk[j]);
             W1G_CHECK_LAUNCH();
         }
         sj[j] = SortJob{{pk[j], nullptr, nullptr}, jobs[j].vals, n};
     }
-    W1G_TRY(radix_sort_multi(c, sj, njobs, 1, 64));
+    W1G_TRY(radix_sort_multi(c, sj, njobs, 1, 32));
     for (int j = 0; j < njobs; j++) {
         if (jobs[j].n > 1) {
-            W1G_TRY(scan_i64(c, TieFlag{pk[j], jobs[j].n}, jobs[j].n, excl[j], dt + j));
-        } else {
-            W1G_CUDA(cudaMemsetAsync(dt + j, 0, sizeof(int64_t), c.stream));
+            k_tie_runs<<<grid_for(jobs[j].n, 256, 8u * c.sm_count), 256, 0, c.stream>>>(
+                pk[j], jobs[j].n, mm + 4 * j + 2, reinterpret_cast<int64_t *>(mm + 4 * j + 3));
+            W1G_CHECK_LAUNCH();
         }
     }
+    unsigned long long *hm = reinterpret_cast<unsigned long long *>(c.h_pinned + F_SCAL);
+    W1G_CUDA(cudaMemcpyAsync(hm, mm, sizeof(unsigned long long) * 4 * njobs, cudaMemcpyDeviceToHost, c.stream));
+    W1G_TRY(stream_sync(c));
+    // elements of tie runs: short runs in place by one thread each; jobs with a
+    // long run (e.g. an H0 diagram whose births are all 0) by a two-word radix
+    // sort of all their tie elements
+    bool is_long[RS_JOBS] = {false, false};
+    int64_t *dt = ptr<int64_t>(c.flags) + F_MISC2;  // long-path tie counts (F_MISC2, F_MISC3)
+    bool any_long = false;
+    for (int j = 0; j < njobs; j++) {
+        if (hm[4 * j + 3] == 0) continue;
+        if (hm[4 * j + 2] <= (unsigned long long)TIE_SMALL) {
+            k_tie_small<<<grid_for(jobs[j].n, 256, 8u * c.sm_count), 256, 0, c.stream>>>(
+                pk[j], jobs[j].n, jobs[j].primary, jobs[j].secondary, jobs[j].vals);
+            W1G_CHECK_LAUNCH();
+        } else {
+            is_long[j] = any_long = true;
+            W1G_TRY(scan_i64(c, TieFlag{pk[j], jobs[j].n}, jobs[j].n, excl[j], dt + j));
+        }
+    }
+    if (!any_long) return W1G_OK;
     W1G_CUDA(cudaMemcpyAsync(&c.h_pinned[F_MISC2], dt, sizeof(int64_t) * njobs, cudaMemcpyDeviceToHost, c.stream));
     W1G_TRY(stream_sync(c));
-    // elements of primary-tie runs: sort them by (primary, secondary), put them back
     SortJob tj[RS_JOBS];
     uint32_t *tpos[RS_JOBS], *pl[RS_JOBS];
     int nt = 0, which[RS_JOBS];
     for (int j = 0; j < njobs; j++) {
+        if (!is_long[j]) continue;
         const int64_t T = c.h_pinned[F_MISC2 + j];
-        if (T == 0) continue;
         uint64_t *kl, *kh;
         W1G_TRY(ensure(c.lex_scr[j][2], (size_t)T, &tpos[j]));
         W1G_TRY(ensure(c.lex_scr[j][3], (size_t)T, &kl));
         W1G_TRY(ensure(c.lex_scr[j][4], (size_t)T, &kh));
         W1G_TRY(ensure(c.lex_scr[j][5], (size_t)T * 2, &pl[j]));
         k_tie_gather<<<grid_for(jobs[j].n, 256, 8u * c.sm_count), 256, 0, c.stream>>>(
-            TieFlag{pk[j], jobs[j].n}, excl[j], jobs[j].vals, jobs[j].secondary, tpos[j], kl, kh, pl[j]);
+            TieFlag{pk[j], jobs[j].n}, excl[j], jobs[j].vals, jobs[j].primary, jobs[j].secondary, tpos[j], kl, kh,
+            pl[j]);
         W1G_CHECK_LAUNCH();
         tj[nt] = SortJob{{kl, kh, nullptr}, pl[j], T};
         which[nt++] = j;
     }
-    if (nt == 0) return W1G_OK;
+    // (primary, secondary) ties keep their input order: the radix sort is stable
+    // and the tie elements are gathered in sorted (= input-stable) order
     W1G_TRY(radix_sort_multi(c, tj, nt, 2, 64));
     for (int q = 0; q < nt; q++) {
         const int j = which[q];
