@@ -71,6 +71,33 @@ def _ncu_traffic(kernel: str, capture: str = "prof_rwmd_all"):
     return None
 
 
+HBM_PEAK_GBS = 6528.7  # MEASURED_PEAKS.json hbm_gbs (copy bandwidth, read + write)
+
+
+def hbm_stages(n_in: int, k0: int, k: int, p: int, m: int, stage_ms: dict) -> dict:
+    """Algorithmic HBM bytes of the byte-moving stages (each stage's inputs read once and
+    outputs written once) over their measured device time, against
+    the measured copy bandwidth.  Raw arcs are bounded below by 2P + K + 1."""
+    m_raw = 2 * p + k + 1
+    nn = max(2 * k - 1, 0)
+    bytes_ = {
+        "zero_condense": 16 * n_in + 32 * k0,
+        "delta_condense": 32 * k0 + 32 * k,
+        "split_tree": 16 * k + 64 * nn,
+        "wspd": 40 * nn + 24 * p,
+        "emit_arcs": 16 * p + 16 * k + 24 * m_raw,
+        "assemble": 24 * m_raw + 24 * m + 16 * (k + 3),
+    }
+    out = {}
+    for name, b in bytes_.items():
+        t = stage_ms.get(name)
+        if not t:
+            continue
+        gbs = b / (t * 1e-3) / 1e9
+        out[name] = {"bytes": int(b), "ms": t, "gbs": gbs, "frac": gbs / HBM_PEAK_GBS}
+    return out
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -352,6 +379,10 @@ def run_ours(args, dist: Dist):
             "e2e": {"value": n / e2e_s, "unit": "pairs/s", "ms_per_pair": e2e_s * 1e3,
                     "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
             "roofline": roofline,
+            "hbm_stages": {"peak_gbs": HBM_PEAK_GBS, "note": "algorithmic bytes / stage device time; "
+                           "latency-bound at this size (few-microsecond dependent phases), see DESIGN.md",
+                           "stages": hbm_stages(2 * args.n, int(info.n_points0), int(info.n_points),
+                                                int(info.n_pairs), int(info.n_arcs), stage_avg)},
             "gpu_launches": int(launches),
             "clocks": clk,
         }
