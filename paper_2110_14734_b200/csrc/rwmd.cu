@@ -327,7 +327,7 @@ __global__ void __launch_bounds__(RF_BLOCK) k_refine(const double2 *__restrict__
     __shared__ double2 s_p[RF_QPB];  // per-source point and search radius, for the
     __shared__ double s_rad[RF_QPB]; // per-source candidate filter
     __shared__ double s_solo_r[RF_QPB], s_solo_m2[RF_QPB];  // heavy sources: radius (-1: none), result
-    __shared__ int s_cursor;
+    __shared__ unsigned s_hmask[RF_BLOCK / 32];  // heavy sources per warp (lanes with sub == 0)
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, sub = tid & (RF_TPQ - 1);
     const int64_t i = (int64_t)blockIdx.x * RF_QPB + tid / RF_TPQ;
     const bool valid = i < nq;
@@ -361,7 +361,11 @@ __global__ void __launch_bounds__(RF_BLOCK) k_refine(const double2 *__restrict__
         s_rad[tid / RF_TPQ] = (valid && r >= 0.0) ? r * (1.0 + 1e-9) : -1.0;
         s_solo_r[tid / RF_TPQ] = heavy ? rh * (1.0 + 1e-9) : -1.0;
     }
-    if (tid == 0) s_cursor = s_nsup = s_nc = 0;
+    {
+        const unsigned hm = __ballot_sync(0xffffffffu, heavy && sub == 0);
+        if (lane == 0) s_hmask[wid] = hm;
+    }
+    if (tid == 0) s_nsup = s_nc = 0;
     double m2 = INFINITY, m2b = INFINITY;
     if (nt > 0) {
         // block bbox and radius
@@ -469,17 +473,19 @@ __global__ void __launch_bounds__(RF_BLOCK) k_refine(const double2 *__restrict__
           if (tid == 0) s_nsup = 0;
           __syncthreads();
         }
-        // heavy sources: one warp each, taken dynamically
-        for (;;) {
-            int j = 0;
-            if (lane == 0) j = atomicAdd(&s_cursor, 1);
-            j = __shfl_sync(0xffffffffu, j, 0);
-            if (j >= RF_QPB) break;
-            if (s_solo_r[j] < 0.0) continue;  // warp-uniform
+        // heavy sources (usually none): the k-th of them goes to warp k % 4
+        int H = 0;
+        for (int w = 0; w < RF_BLOCK / 32; w++) H += __popc(s_hmask[w]);
+        for (int k = wid; k < H; k += RF_BLOCK / 32) {
+            int w2 = 0, kk = k;
+            while (kk >= __popc(s_hmask[w2])) kk -= __popc(s_hmask[w2++]);
+            unsigned m = s_hmask[w2];
+            for (int q = 0; q < kk; q++) m &= m - 1;
+            const int j = w2 * (32 / RF_TPQ) + (__ffs(m) - 1) / RF_TPQ;
             const double ms = solo_nn(s_p[j], s_solo_r[j], t, nt, tbox, sbox, ntile, nsup, lane);
             if (lane == 0) s_solo_m2[j] = ms;
         }
-        __syncthreads();
+        if (H) __syncthreads();  // H is block-uniform
         if (heavy) m2 = fmin(m2, s_solo_m2[tid / RF_TPQ]);
     }
     m2 = m2b < m2 ? m2b : m2;
