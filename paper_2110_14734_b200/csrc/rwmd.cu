@@ -88,15 +88,18 @@ __device__ __forceinline__ uint32_t spread16(uint32_t v) {
     return v;
 }
 
-// Morton code on a 65536^2 grid over the node bbox; payload = member position
+// Morton code on a 4096^2 grid over the node bbox (24-bit keys: three
+// radix passes; a finer grid buys nothing at 64-target tiles); payload = member position
+constexpr double MORTON_MAX = 4095.0;
+constexpr int MORTON_BITS = 24;
 __global__ void k_morton(const double2 *pts, const int32_t *members, int64_t n, double x0, double y0,
                          double inv, uint64_t *key, uint32_t *val) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         const double2 p = pts[members[i]];
         double fx = (p.x - x0) * inv, fy = (p.y - y0) * inv;
-        fx = fx < 0 ? 0 : (fx > 65535.0 ? 65535.0 : fx);
-        fy = fy < 0 ? 0 : (fy > 65535.0 ? 65535.0 : fy);
+        fx = fx < 0 ? 0 : (fx > MORTON_MAX ? MORTON_MAX : fx);
+        fy = fy < 0 ? 0 : (fy > MORTON_MAX ? MORTON_MAX : fy);
         key[i] = (uint64_t)(spread16((uint32_t)fx) | (spread16((uint32_t)fy) << 1));
         val[i] = (uint32_t)i;
     }
@@ -571,7 +574,7 @@ static int rwmd_prepare(Ctx &c, RwmdFrame &F, int range_side = -1, int64_t begin
     F.scale = std::ldexp(1.0, -e);
     F.unscale = std::ldexp(1.0, e);
     const double ext = H > 0.0 && std::isfinite(H) ? H : 1.0;
-    const double inv = 65535.0 / ext;
+    const double inv = MORTON_MAX / ext;
     SortJob jobs[2];
     int64_t off[2];
     for (int s = 0; s < 2; s++) {
@@ -590,7 +593,7 @@ static int rwmd_prepare(Ctx &c, RwmdFrame &F, int range_side = -1, int64_t begin
                                                                           inv, key, perm);
         W1G_CHECK_LAUNCH();
     }
-    W1G_TRY(radix_sort_multi(c, jobs, 2, 1, 32));  // both sides in the same launches
+    W1G_TRY(radix_sort_multi(c, jobs, 2, 1, MORTON_BITS));  // both sides in the same launches
     for (int s = 0; s < 2; s++) {
         const int64_t n = jobs[s].n;
         if (n == 0) continue;
