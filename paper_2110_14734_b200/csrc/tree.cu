@@ -40,6 +40,8 @@ struct SegInfo {
 // segments of at most LOCAL_MAX points leave the global level loop and are
 // finished inside one CTA (k_tree_local)
 constexpr int LOCAL_MAX = 2048;
+constexpr int LT = 1024;                // threads of the shared-memory subtree kernel
+constexpr int LPT = LOCAL_MAX / LT;     // list positions per thread
 
 struct TreeOut {
     int64_t *left, *right, *rep, *size;
@@ -310,7 +312,7 @@ struct LocalSmem {
     LocalSub sub[2][LOCAL_MAX / 2 + 1];
     LocalInfo info[LOCAL_MAX / 2 + 1];
     int16_t big[LOCAL_MAX / 2 + 1];
-    int32_t warp_tot[8];
+    int32_t warp_tot[LT / 32];
     int32_t nsub_next, nbig;
 };
 
@@ -423,7 +425,7 @@ __device__ __forceinline__ void local_split(LocalSmem &S, int s, int cur, const 
     S.info[s] = in;
 }
 
-__global__ void __launch_bounds__(256) k_tree_local(const double2 *__restrict__ pts, const uint32_t *xl0,
+__global__ void __launch_bounds__(LT) k_tree_local(const double2 *__restrict__ pts, const uint32_t *xl0,
                                                     const uint32_t *xl1, const uint32_t *yl0,
                                                     const uint32_t *yl1, const Seg *__restrict__ local,
                                                     const int32_t *local_cnt, int32_t *inv, TreeOut o,
@@ -437,7 +439,7 @@ __global__ void __launch_bounds__(256) k_tree_local(const double2 *__restrict__ 
         const int m = L.hi - L.lo;
         const uint32_t *gx = L.pad ? xl1 : xl0, *gy = L.pad ? yl1 : yl0;
         // stage the segment: local id = rank in the X-list
-        for (int i = tid; i < m; i += 256) {
+        for (int i = tid; i < m; i += LT) {
             const uint32_t g = gx[L.lo + i];
             const double2 p = pts[g];
             S.px[i] = p.x;
@@ -448,7 +450,7 @@ __global__ void __launch_bounds__(256) k_tree_local(const double2 *__restrict__ 
             inv[g] = i;
         }
         __syncthreads();
-        for (int i = tid; i < m; i += 256) S.yl[0][i] = (uint16_t)inv[gy[L.lo + i]];
+        for (int i = tid; i < m; i += LT) S.yl[0][i] = (uint16_t)inv[gy[L.lo + i]];
         if (tid == 0) {
             S.sub[0][0] = LocalSub{0, (int16_t)m, L.nid};
             S.nsub_next = 0;
@@ -458,20 +460,20 @@ __global__ void __launch_bounds__(256) k_tree_local(const double2 *__restrict__ 
         int cur = 0, nsub = 1;
         while (nsub > 0) {
             // (A) small sub-segments: one thread each; large ones: one warp each
-            for (int s = tid; s < nsub; s += 256) {
+            for (int s = tid; s < nsub; s += LT) {
                 if (S.sub[cur][s].hi - S.sub[cur][s].lo > 64)
                     S.big[atomicAdd(&S.nbig, 1)] = (int16_t)s;
                 else
                     local_split<false>(S, s, cur, o, flags);
             }
             __syncthreads();
-            for (int k = wid; k < S.nbig; k += 8) local_split<true>(S, S.big[k], cur, o, flags);
+            for (int k = wid; k < S.nbig; k += LT / 32) local_split<true>(S, S.big[k], cur, o, flags);
             __syncthreads();
             // (B) flags of the other list + block exclusive scan (8 positions per thread)
-            int f[8], sum = 0;
+            int f[LPT], sum = 0;
 #pragma unroll
-            for (int i = 0; i < 8; i++) {
-                const int p = tid * 8 + i;
+            for (int i = 0; i < LPT; i++) {
+                const int p = tid * LPT + i;
                 int v = 0;
                 if (p < m) {
                     const int s = S.ps[cur][p];
@@ -498,8 +500,8 @@ __global__ void __launch_bounds__(256) k_tree_local(const double2 *__restrict__ 
                 for (int w = 0; w < wid; w++) base += S.warp_tot[w];
                 int run = base + x - sum;
 #pragma unroll
-                for (int i = 0; i < 8; i++) {
-                    const int p = tid * 8 + i;
+                for (int i = 0; i < LPT; i++) {
+                    const int p = tid * LPT + i;
                     if (p < m) S.ex[p] = (int16_t)run;
                     run += f[i];
                 }
@@ -507,8 +509,8 @@ __global__ void __launch_bounds__(256) k_tree_local(const double2 *__restrict__ 
             __syncthreads();
             // (C) stable partition of the other list inside each sub-segment
 #pragma unroll
-            for (int i = 0; i < 8; i++) {
-                const int p = tid * 8 + i;
+            for (int i = 0; i < LPT; i++) {
+                const int p = tid * LPT + i;
                 if (p >= m) continue;
                 const int s = S.ps[cur][p];
                 if (s < 0) {
@@ -1007,7 +1009,7 @@ int tree_run(Ctx &c, const double2 *pts, int64_t n, int64_t *n_nodes, int32_t *d
         const size_t smem = sizeof(LocalSmem);
         W1G_CUDA(cudaFuncSetAttribute(k_tree_local, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         const unsigned gl = (unsigned)(2 * c.sm_count);
-        k_tree_local<<<gl, 256, smem, c.stream>>>(pts, xl[0], xl[1], yl[0], yl[1], local, local_cnt, fl, o,
+        k_tree_local<<<gl, LT, smem, c.stream>>>(pts, xl[0], xl[1], yl[0], yl[1], local, local_cnt, fl, o,
                                                   dflags(c));
         W1G_CHECK_LAUNCH();
     }
