@@ -635,7 +635,7 @@ __global__ void k_tree_scatter(const uint32_t *__restrict__ xl, const uint32_t *
 // (every CTA scans the tile sums in shared memory) + scatter, grid sync.
 // Three grid barriers per level instead of four launches and a host poll.
 
-constexpr int TP_IPT = 8;
+constexpr int TP_IPT = 2;
 constexpr int TP_TILE = 256 * TP_IPT;
 constexpr int COOP_MAX_TILES = 8192;
 
