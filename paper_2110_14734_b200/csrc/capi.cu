@@ -669,7 +669,7 @@ int w1g_front_end_device(w1g_ctx *c, const double *d_a, int64_t na, const double
     info->epsilon_condense = eps_c;
     // With a fixed delta, L only feeds the diagnostics and the `L > 0` test of
     // pipeline.py:115, so RWMD runs on the auxiliary context concurrently with
-    // emit + assemble, the back end speculating L > 0 (redone with delta = 0 in
+    // the back end (from the point W1G_OVERLAP selects), which speculates L > 0 (redone with delta = 0 in
     // the rare case L == 0).
     const bool overlap = c->overlap && use_condensation && delta_mode != 0 && delta > 0.0;
     double L = 0.0, LA = 0.0, LB = 0.0;
@@ -725,7 +725,6 @@ int w1g_front_end_device(w1g_ctx *c, const double *d_a, int64_t na, const double
     host_t[5] = std::chrono::steady_clock::now();
         info->n_pairs = P;
         info->n_levels_wspd = c->wspd_levels;
-        // RWMD joins here: emit and assemble have no cooperative (grid-synchronised) kernels
         if (spawn && c->overlap == 1) W1G_TRY(start_rwmd());
         int64_t M;
         W1G_TRY(emit_run(*c, &M));

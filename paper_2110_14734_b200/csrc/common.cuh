@@ -142,8 +142,10 @@ struct Ctx {
 
     // fixed-delta front end: RWMD (which then only feeds diagnostics and the
     // L > 0 test) runs on a second context -- own stream, scratch and host
-    // thread -- concurrently with emit + assemble (W1G_OVERLAP=0 disables)
-    int overlap = 1;
+    // thread -- concurrently with the back end.  W1G_OVERLAP selects where it
+    // starts: 3 (default) after the split tree, 1 after the WSPD, 2 after
+    // zero_condense, 0 = sequential (measured: 3 is best at cfg2)
+    int overlap = 3;
     Ctx *aux = nullptr;
 
     // one-shot host target for the next fused front end's network (w1g_set_network_out)
