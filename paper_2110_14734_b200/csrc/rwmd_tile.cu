@@ -22,7 +22,7 @@
 //    merge with an order-independent atomicMin on the float bits;
 //  * culled mode (the production path): any real target's distance is a
 //    valid upper bound for the exact pass, so each CTA only evaluates the
-//    Morton-nearest target tiles (walking 5 tiles outward from the tile
+//    Morton-nearest target tiles (walking 3 tiles outward from the tile
 //    holding its middle source's Morton key, found by a warp-wide 32-ary
 //    search of the target keys) and skips tiles whose bbox is farther than
 //    the CTA's current worst upper bound; sources whose seed stays poor are
@@ -298,9 +298,11 @@ int rwmd_f32_min(Ctx &c, const double2 *q, const uint64_t *qkey, int64_t nq, con
     A.scale = scale;
     A.mout = mout;
     A.qn_out = qn_out;
-    // tiles walked per CTA in culled mode (measured: 3 already seeds cfg2 and
-    // 1M points tightly, 1-2 do not; 5 leaves a margin)
-    A.cull_steps = c.cull_steps > 0 ? c.cull_steps : 5;
+    // tiles walked per CTA in culled mode: the centre tile and its two Morton
+    // neighbours (measured: 3 seeds cfg2 and 1M points as tightly as 5 -- same
+    // exact-pass time -- while 1-2 do not; the few sources a short walk leaves
+    // with a poor seed are caught by the exact pass's heavy-source path)
+    A.cull_steps = c.cull_steps > 0 ? c.cull_steps : 3;
     if (culling) {
         const int ntile = (int)((nt + TS_CULL - 1) / TS_CULL);
         k_tile_boxes<<<grid_for((int64_t)ntile * 32, 256, 8u * c.sm_count), 256, 0, c.stream>>>(t, (int)nt, TS_CULL, tbox);
