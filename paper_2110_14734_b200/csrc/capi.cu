@@ -236,6 +236,8 @@ int w1g_ctx_destroy(w1g_ctx *c) {
         free_buf(ns.pts);
         free_buf(ns.am);
         free_buf(ns.bm);
+        free_buf(ns.exa);
+        free_buf(ns.exb);
     }
     for (auto &b : c->scr) free_buf(b);
     for (auto &job : c->sort_scr)
@@ -300,6 +302,7 @@ int w1g_load_nodes(w1g_ctx *c, int slot, const double *points, const int64_t *am
     ns.valid = true;
     ns.abar = abar;
     ns.bbar = bbar;
+    ns.na = ns.nb = -1;
     invalidate_from_nodes(*c);
     if (slot == 0) c->nodes[1].valid = false;
     return W1G_OK;
@@ -713,14 +716,16 @@ int w1g_front_end_device(w1g_ctx *c, const double *d_a, int64_t na, const double
         info->n_points = kk;
         int64_t nn;
         int32_t depth;
-        W1G_TRY(tree_run(*c, ptr<double2>(c->nodes[1].pts), kk, &nn, &depth));
+        W1G_TRY(tree_run(*c, ptr<double2>(c->nodes[1].pts), kk, &nn, &depth, true));
         W1G_CUDA(cudaEventRecord(ev[4], c->stream));
     host_t[4] = std::chrono::steady_clock::now();
         info->n_tree_nodes = nn;
         info->tree_depth = depth;
         if (spawn && c->overlap == 3) W1G_TRY(start_rwmd());
         int64_t P;
-        W1G_TRY(wspd_run(*c, s, 0, &P));
+        W1G_TRY(wspd_run(*c, s, 0, &P));  // its round trip also delivers the tree's depth / duplicate flag
+        W1G_TRY(tree_deferred_check(*c, &depth));
+        info->tree_depth = depth;
         W1G_CUDA(cudaEventRecord(ev[5], c->stream));
     host_t[5] = std::chrono::steady_clock::now();
         info->n_pairs = P;

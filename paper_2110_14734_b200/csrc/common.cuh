@@ -66,6 +66,10 @@ struct NodeSet {
     DevBuf am;   // (k) int64 a_mass
     DevBuf bm;   // (k) int64 b_mass
     int64_t abar = 0, bbar = 0;
+    // positions of the nodes with a- / b-mass among themselves (exclusive scans)
+    // and their counts, computed by delta_condense for emit_arcs (na < 0: absent)
+    DevBuf exa, exb;
+    int64_t na = -1, nb = -1;
 };
 
 // per-node geometry used by the WSPD predicate (spanner.py:176-194), computed
@@ -418,7 +422,12 @@ int rwmd_run(Ctx &c, double *L, double *LA, double *LB);
 int rwmd_tile_profile(Ctx &c, int reps, float *ms, int64_t *evals);
 int rwmd_range_run(Ctx &c, int side, int64_t begin, int64_t end, double *partial, int64_t *n_members);
 int dc_run(Ctx &c, double delta, double pitch, double half_width, uint64_t seed, int64_t *k);
-int tree_run(Ctx &c, const double2 *d_pts, int64_t n, int64_t *n_nodes, int32_t *depth);
+// defer = true (fused front end): no host round trip of its own -- the depth and the
+// duplicate flag land in h_pinned[H_TREE_DEPTH / H_TREE_DUP] at the caller's next
+// synchronisation, and the caller checks the flag (tree_deferred_check)
+int tree_run(Ctx &c, const double2 *d_pts, int64_t n, int64_t *n_nodes, int32_t *depth, bool defer = false);
+int tree_deferred_check(Ctx &c, int32_t *depth);
+enum { H_TREE_DEPTH = F_NSLOTS - 2, H_TREE_DUP = F_NSLOTS - 1 };  // h_pinned slots no flags fetch touches
 int tree_geom(Ctx &c);
 int wspd_run(Ctx &c, double s, int reference_order, int64_t *n_pairs);
 int emit_run(Ctx &c, int64_t *n_arcs);

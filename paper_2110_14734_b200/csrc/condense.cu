@@ -225,6 +225,21 @@ int zc_run(Ctx &c, const double2 *d_a, int64_t na, const double2 *d_b, int64_t n
     return W1G_OK;
 }
 
+struct MassFlag {
+    const int64_t *m;
+    __device__ int64_t operator()(int64_t i) const { return m[i] > 0 ? 1 : 0; }
+};
+
+// exclusive positions of the a- and b-mass nodes (totals -> flags F_MISC0 / F_MISC1)
+static int member_scans(Ctx &c, NodeSet &ns, int64_t k) {
+    int64_t *exa, *exb;
+    W1G_TRY(ensure(ns.exa, (size_t)k + 1, &exa));
+    W1G_TRY(ensure(ns.exb, (size_t)k + 1, &exb));
+    W1G_TRY(scan_i64(c, MassFlag{ptr<int64_t>(ns.am)}, k, exa, dflags(c) + F_MISC0));
+    W1G_TRY(scan_i64(c, MassFlag{ptr<int64_t>(ns.bm)}, k, exb, dflags(c) + F_MISC1));
+    return W1G_OK;
+}
+
 int dc_run(Ctx &c, double delta, double pitch, double half_width, uint64_t seed, int64_t *kout) {
     NodeSet &src = c.nodes[0], &dst = c.nodes[1];
     const int64_t k = src.k;
@@ -244,6 +259,10 @@ int dc_run(Ctx &c, double delta, double pitch, double half_width, uint64_t seed,
         }
         dst.k = k;
         dst.valid = true;
+        W1G_TRY(member_scans(c, dst, k));
+        W1G_TRY(flags_fetch(c, F_MISC0, 2));
+        dst.na = c.h_pinned[F_MISC0];
+        dst.nb = c.h_pinned[F_MISC1];
         *kout = k;
         return W1G_OK;
     }
@@ -291,8 +310,13 @@ int dc_run(Ctx &c, double delta, double pitch, double half_width, uint64_t seed,
     k_dc_emit<<<gs(c, k), 256, 0, c.stream>>>(f, k, excl, ptr<int64_t>(src.am), ptr<int64_t>(src.bm),
                                               pitch, half_width, base, pts, am, bm);
     W1G_CHECK_LAUNCH();
-    W1G_TRY(flags_fetch(c, F_TOTAL, 1));
+    // node positions per side for emit_arcs, over k >= K (the masses past K are 0),
+    // so their totals come back with K in the same round trip
+    W1G_TRY(member_scans(c, dst, k));
+    W1G_TRY(flags_fetch(c, F_TOTAL, F_MISC1 - F_TOTAL + 1));
     dst.k = c.h_pinned[F_TOTAL];
+    dst.na = c.h_pinned[F_MISC0];
+    dst.nb = c.h_pinned[F_MISC1];
     dst.valid = true;
     *kout = dst.k;
     return W1G_OK;

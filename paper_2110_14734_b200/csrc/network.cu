@@ -76,9 +76,8 @@ struct PosFlag {
 };
 
 __global__ void k_emit_diag(const double2 *pts, const int64_t *am, const int64_t *bm, int64_t K,
-                            const int64_t *exa, const int64_t *exb, const int64_t *n_a, int64_t base,
+                            const int64_t *exa, const int64_t *exb, int64_t na, int64_t base,
                             int64_t *tails, int64_t *heads, double *costs) {
-    const int64_t na = *n_a;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < K;
          i += (int64_t)gridDim.x * blockDim.x) {
         const double2 p = pts[i];
@@ -557,14 +556,23 @@ int emit_run(Ctx &c, int64_t *n_arcs) {
     NodeSet &ns = c.nodes[1];
     const int64_t K = ns.k, P = c.n_pairs;
     const int64_t *am = ptr<int64_t>(ns.am), *bm = ptr<int64_t>(ns.bm);
-    int64_t *exa, *exb;
-    W1G_TRY(ensure(c.scr[3], (size_t)K + 1, &exa));
-    W1G_TRY(ensure(c.scr[6], (size_t)K + 1, &exb));
-    W1G_TRY(flags_reset(c));
-    W1G_TRY(scan_i64(c, PosFlag{am}, K, exa, dflags(c) + F_MISC0));
-    W1G_TRY(scan_i64(c, PosFlag{bm}, K, exb, dflags(c) + F_MISC1));
-    W1G_TRY(flags_fetch(c, F_MISC0, 2));
-    const int64_t na = c.h_pinned[F_MISC0], nb = c.h_pinned[F_MISC1];
+    int64_t *exa, *exb, na, nb;
+    if (ns.na >= 0 && ns.exa.p && ns.exb.p) {
+        // positions and counts from delta_condense: no host round trip here
+        exa = ptr<int64_t>(ns.exa);
+        exb = ptr<int64_t>(ns.exb);
+        na = ns.na;
+        nb = ns.nb;
+    } else {
+        W1G_TRY(ensure(c.scr[3], (size_t)K + 1, &exa));
+        W1G_TRY(ensure(c.scr[6], (size_t)K + 1, &exb));
+        W1G_TRY(flags_reset(c));
+        W1G_TRY(scan_i64(c, PosFlag{am}, K, exa, dflags(c) + F_MISC0));
+        W1G_TRY(scan_i64(c, PosFlag{bm}, K, exb, dflags(c) + F_MISC1));
+        W1G_TRY(flags_fetch(c, F_MISC0, 2));
+        na = c.h_pinned[F_MISC0];
+        nb = c.h_pinned[F_MISC1];
+    }
     const int64_t M = 2 * P + na + nb + 1;
     int64_t *t, *h;
     double *cs;
@@ -577,8 +585,8 @@ int emit_run(Ctx &c, int64_t *n_arcs) {
         W1G_CHECK_LAUNCH();
     }
     if (K) {
-        k_emit_diag<<<gs(c, K), 256, 0, c.stream>>>(ptr<double2>(ns.pts), am, bm, K, exa, exb,
-                                                    dflags(c) + F_MISC0, 2 * P, t, h, cs);
+        k_emit_diag<<<gs(c, K), 256, 0, c.stream>>>(ptr<double2>(ns.pts), am, bm, K, exa, exb, na, 2 * P, t, h,
+                                                    cs);
         W1G_CHECK_LAUNCH();
     }
     k_emit_free<<<1, 1, 0, c.stream>>>(K, M - 1, t, h, cs);

@@ -850,7 +850,7 @@ int tree_geom(Ctx &c) {
     return W1G_OK;
 }
 
-int tree_run(Ctx &c, const double2 *pts, int64_t n, int64_t *n_nodes, int32_t *depth) {
+int tree_run(Ctx &c, const double2 *pts, int64_t n, int64_t *n_nodes, int32_t *depth, bool defer) {
     c.tree_valid = false;
     c.pair_pts = pts;
     const int64_t nn = n > 0 ? 2 * n - 1 : 0;
@@ -971,9 +971,9 @@ int tree_run(Ctx &c, const double2 *pts, int64_t n, int64_t *n_nodes, int32_t *d
         void *args[] = {&A};
         W1G_CUDA(cudaLaunchCooperativeKernel((void *)k_tree_coop, G, 256, args, smem, c.stream));
         W1G_CHECK_LAUNCH();
-        W1G_CUDA(cudaMemcpyAsync(c.h_pinned + F_ACTIVE, lv, sizeof(int32_t), cudaMemcpyDeviceToHost, c.stream));
-        W1G_TRY(stream_sync(c));
-        levels = *reinterpret_cast<int32_t *>(c.h_pinned + F_ACTIVE) & 0x3fffffff;
+        // the depth is read after the stage's (or, deferred, the caller's) next round trip
+        W1G_CUDA(cudaMemcpyAsync(c.h_pinned + H_TREE_DEPTH, lv, sizeof(int32_t), cudaMemcpyDeviceToHost, c.stream));
+        levels = -1;
     } else if (n > LOCAL_MAX) {
         // fallback for very large inputs: one launch per phase, host polls per batch
         const unsigned gseg = grid_for(seg_cap * 32, 256, 16u * c.sm_count);
@@ -1014,16 +1014,29 @@ int tree_run(Ctx &c, const double2 *pts, int64_t n, int64_t *n_nodes, int32_t *d
         W1G_CHECK_LAUNCH();
     }
     T.mark("local");
-    W1G_CUDA(cudaMemcpyAsync(c.h_pinned + F_DUP, dflags(c) + F_DUP, sizeof(int64_t), cudaMemcpyDeviceToHost,
+    if (levels >= 0) c.h_pinned[H_TREE_DEPTH] = levels;  // host-known (multi-kernel path / no global levels)
+    W1G_CUDA(cudaMemcpyAsync(c.h_pinned + H_TREE_DUP, dflags(c) + F_DUP, sizeof(int64_t), cudaMemcpyDeviceToHost,
                              c.stream));
+    W1G_CUDA(cudaEventRecord(c.ev[10], c.stream));  // the two copies above have landed once this has
+    c.tree_valid = true;
+    if (defer) {
+        *depth = 0;
+        return W1G_OK;
+    }
     W1G_TRY(stream_sync(c));
-    if (c.h_pinned[F_DUP]) {
+    return tree_deferred_check(c, depth);
+}
+
+int tree_deferred_check(Ctx &c, int32_t *depth) {
+    W1G_CUDA(cudaEventSynchronize(c.ev[10]));  // already complete after any later round trip
+    if (c.h_pinned[H_TREE_DUP]) {
+        c.tree_valid = false;
         set_error("split tree input contains duplicate points");
         return W1G_EDUPLICATE;
     }
+    const int32_t levels = (int32_t)(c.h_pinned[H_TREE_DEPTH] & 0x3fffffff);
     c.tree_depth = levels;
     *depth = levels;
-    c.tree_valid = true;
     return W1G_OK;
 }
 
