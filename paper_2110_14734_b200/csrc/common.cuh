@@ -359,13 +359,18 @@ int radix_sort_multi(Ctx &c, const SortJob *jobs, int njobs, int words, int top_
 // compressed-key tie runs by the full (primary, secondary, id) -- in place by
 // one thread per run when every run is short, else by a two-word radix sort.
 // `primary` and `secondary` are indexed by element id.
-int sort_lex2(Ctx &c, const uint64_t *primary, const uint64_t *secondary, uint32_t *vals, int64_t n);
+int sort_lex2(Ctx &c, const uint64_t *primary, const uint64_t *secondary, uint32_t *vals, int64_t n,
+              bool speculative = false);
+// speculative = true: no host round trip -- short tie runs are ordered in place and
+// the longest run is copied to h_pinned[H_LEX_MAXRUN + job] for the caller to check
+// after its next synchronisation (lex2_speculation_failed -> redo non-speculatively)
+bool lex2_speculation_failed(Ctx &c, int njobs);
 struct Lex2Job {
     const uint64_t *primary, *secondary;
     uint32_t *vals;
     int64_t n;
 };
-int sort_lex2_multi(Ctx &c, const Lex2Job *jobs, int njobs);
+int sort_lex2_multi(Ctx &c, const Lex2Job *jobs, int njobs, bool speculative = false);
 
 // ------------------------------------------------------------------ misc
 inline unsigned grid_for(int64_t n, int block, unsigned cap = 0x7fffffffu) {
@@ -417,7 +422,7 @@ struct SubTimer {
 
 // stage launchers (one translation unit each)
 int zc_run(Ctx &c, const double2 *d_a, int64_t na, const double2 *d_b, int64_t nb, int64_t *k0,
-           int32_t *balanced);
+           int32_t *balanced, bool speculative = true);
 int rwmd_run(Ctx &c, double *L, double *LA, double *LB);
 int rwmd_tile_profile(Ctx &c, int reps, float *ms, int64_t *evals);
 int rwmd_range_run(Ctx &c, int side, int64_t begin, int64_t end, double *partial, int64_t *n_members);
@@ -427,7 +432,8 @@ int dc_run(Ctx &c, double delta, double pitch, double half_width, uint64_t seed,
 // synchronisation, and the caller checks the flag (tree_deferred_check)
 int tree_run(Ctx &c, const double2 *d_pts, int64_t n, int64_t *n_nodes, int32_t *depth, bool defer = false);
 int tree_deferred_check(Ctx &c, int32_t *depth);
-enum { H_TREE_DEPTH = F_NSLOTS - 2, H_TREE_DUP = F_NSLOTS - 1 };  // h_pinned slots no flags fetch touches
+// h_pinned slots no flags fetch touches
+enum { H_LEX_MAXRUN = F_NSLOTS - 4, H_TREE_DEPTH = F_NSLOTS - 2, H_TREE_DUP = F_NSLOTS - 1 };
 int tree_geom(Ctx &c);
 int wspd_run(Ctx &c, double s, int reference_order, int64_t *n_pairs);
 int emit_run(Ctx &c, int64_t *n_arcs);

@@ -180,7 +180,7 @@ inline unsigned gs(const Ctx &c, int64_t n) { return grid_for(n, 256, 8u * c.sm_
 }  // namespace
 
 int zc_run(Ctx &c, const double2 *d_a, int64_t na, const double2 *d_b, int64_t nb, int64_t *k0,
-           int32_t *balanced) {
+           int32_t *balanced, bool speculative) {
     const int64_t n = na + nb;
     NodeSet &ns = c.nodes[0];
     ns.abar = -na;
@@ -209,7 +209,9 @@ int zc_run(Ctx &c, const double2 *d_a, int64_t na, const double2 *d_b, int64_t n
     k_zc_keys<<<gs(c, n), 256, 0, c.stream>>>(d_a, na, d_b, n, hi, lo, vals);
     W1G_CHECK_LAUNCH();
     // lexicographic (x, y): radix by x, y only where x ties
-    W1G_TRY(sort_lex2(c, hi, lo, vals, n));
+    // speculative: short tie runs only (no round trip of the sort's own); redone
+    // below in the rare case of a long run (many equal x, e.g. births all 0)
+    W1G_TRY(sort_lex2(c, hi, lo, vals, n, speculative));
     ZcFlag f{d_a, d_b, na, vals};
     W1G_TRY(scan_i64(c, f, n, excl, dflags(c) + F_K0));
     W1G_CUDA(cudaMemsetAsync(am, 0, sizeof(int64_t) * n, c.stream));
@@ -219,6 +221,7 @@ int zc_run(Ctx &c, const double2 *d_a, int64_t na, const double2 *d_b, int64_t n
     k_unbalanced<<<gs(c, n), 256, 0, c.stream>>>(am, bm, dflags(c) + F_K0, dflags(c) + F_UNBALANCED);
     W1G_CHECK_LAUNCH();
     W1G_TRY(flags_fetch(c, F_K0, 2));
+    if (speculative && lex2_speculation_failed(c, 1)) return zc_run(c, d_a, na, d_b, nb, k0, balanced, false);
     ns.k = c.h_pinned[F_K0];
     *k0 = ns.k;
     *balanced = c.h_pinned[F_UNBALANCED] ? 0 : 1;

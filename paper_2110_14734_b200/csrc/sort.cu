@@ -535,7 +535,8 @@ __global__ void k_tie_small(const uint64_t *pk, int64_t n, const uint64_t *prima
         const uint64_t v = pk[i];
         if ((i > 0 && pk[i - 1] == v) || i + 1 >= n || pk[i + 1] != v) continue;  // run starts only
         int64_t j = i + 1;
-        while (j < n && pk[j] == v) j++;
+        while (j < n && pk[j] == v && j - i <= TIE_SMALL) j++;
+        if (j - i > TIE_SMALL) continue;  // long run: the two-word path's (speculative callers redo)
         // insertion sort of vals[i..j) by (primary[val], secondary[val], val)
         for (int64_t a = i + 1; a < j; a++) {
             const uint32_t x = vals[a];
@@ -556,7 +557,7 @@ __global__ void k_tie_small(const uint64_t *pk, int64_t n, const uint64_t *prima
 
 }  // namespace
 
-int sort_lex2_multi(Ctx &c, const Lex2Job *jobs, int njobs) {
+int sort_lex2_multi(Ctx &c, const Lex2Job *jobs, int njobs, bool speculative) {
     if (njobs < 1 || njobs > RS_JOBS) {
         set_error("sort_lex2: unsupported job count %d", njobs);
         return W1G_EINVAL;
@@ -590,6 +591,17 @@ int sort_lex2_multi(Ctx &c, const Lex2Job *jobs, int njobs) {
                 pk[j], jobs[j].n, mm + 4 * j + 2, reinterpret_cast<int64_t *>(mm + 4 * j + 3));
             W1G_CHECK_LAUNCH();
         }
+    }
+    if (speculative) {
+        for (int j = 0; j < njobs; j++) {
+            if (jobs[j].n <= 1) continue;
+            k_tie_small<<<grid_for(jobs[j].n, 256, 8u * c.sm_count), 256, 0, c.stream>>>(
+                pk[j], jobs[j].n, jobs[j].primary, jobs[j].secondary, jobs[j].vals);
+            W1G_CHECK_LAUNCH();
+            W1G_CUDA(cudaMemcpyAsync(c.h_pinned + H_LEX_MAXRUN + j, mm + 4 * j + 2, sizeof(unsigned long long),
+                                     cudaMemcpyDeviceToHost, c.stream));
+        }
+        return W1G_OK;
     }
     unsigned long long *hm = reinterpret_cast<unsigned long long *>(c.h_pinned + F_SCAL);
     W1G_CUDA(cudaMemcpyAsync(hm, mm, sizeof(unsigned long long) * 4 * njobs, cudaMemcpyDeviceToHost, c.stream));
@@ -648,10 +660,20 @@ int sort_lex2_multi(Ctx &c, const Lex2Job *jobs, int njobs) {
     return W1G_OK;
 }
 
-int sort_lex2(Ctx &c, const uint64_t *primary, const uint64_t *secondary, uint32_t *vals, int64_t n) {
-    if (n <= 1) return W1G_OK;
+int sort_lex2(Ctx &c, const uint64_t *primary, const uint64_t *secondary, uint32_t *vals, int64_t n,
+              bool speculative) {
+    if (n <= 1) {
+        c.h_pinned[H_LEX_MAXRUN] = 0;
+        return W1G_OK;
+    }
     Lex2Job job{primary, secondary, vals, n};
-    return sort_lex2_multi(c, &job, 1);
+    return sort_lex2_multi(c, &job, 1, speculative);
+}
+
+bool lex2_speculation_failed(Ctx &c, int njobs) {
+    for (int j = 0; j < njobs; j++)
+        if ((unsigned long long)c.h_pinned[H_LEX_MAXRUN + j] > (unsigned long long)TIE_SMALL) return true;
+    return false;
 }
 
 }  // namespace w1g
