@@ -714,6 +714,7 @@ int w1g_front_end_device(w1g_ctx *c, const double *d_a, int64_t na, const double
         W1G_CUDA(cudaEventRecord(ev[3], c->stream));
     host_t[3] = std::chrono::steady_clock::now();
         info->n_points = kk;
+        if (spawn && c->overlap == 4) W1G_TRY(start_rwmd());
         int64_t nn;
         int32_t depth;
         W1G_TRY(tree_run(*c, ptr<double2>(c->nodes[1].pts), kk, &nn, &depth, true));

@@ -147,9 +147,10 @@ struct Ctx {
     // fixed-delta front end: RWMD (which then only feeds diagnostics and the
     // L > 0 test) runs on a second context -- own stream, scratch and host
     // thread -- concurrently with the back end.  W1G_OVERLAP selects where it
-    // starts: 3 (default) after the split tree, 1 after the WSPD, 2 after
-    // zero_condense, 0 = sequential (measured: 3 is best at cfg2)
-    int overlap = 3;
+    // starts: 4 (default) after delta_condense, 3 after the split tree, 1 after
+    // the WSPD, 2 right after zero_condense, 0 = sequential (measured at cfg2:
+    // 4 -> 1.44 ms, 3 -> 1.55, 1 -> 1.66, 2 -> 1.60, 0 -> 1.74)
+    int overlap = 4;
     Ctx *aux = nullptr;
 
     // one-shot host target for the next fused front end's network (w1g_set_network_out)
