@@ -280,7 +280,9 @@ int dc_run(Ctx &c, double delta, double pitch, double half_width, uint64_t seed,
     W1G_TRY(ensure(c.scr[3], k, &excl));
     W1G_TRY(flags_reset(c));
     k_init_ranges<<<1, 1, 0, c.stream>>>(dflags(c));
-    k_dc_snap<<<gs(c, k), 256, 0, c.stream>>>(ptr<double2>(src.pts), k, pitch, cells, dflags(c));
+    // few CTAs: the range is reduced per warp and merged with global atomics
+    k_dc_snap<<<grid_for(k, 256, 2u * c.sm_count), 256, 0, c.stream>>>(ptr<double2>(src.pts), k, pitch, cells,
+                                                                      dflags(c));
     W1G_CHECK_LAUNCH();
     W1G_TRY(flags_fetch(c, 0, F_CELL_MIN + 4));
     if (c.h_pinned[F_OVERFLOW]) {

@@ -221,9 +221,24 @@ __global__ void k_csr_count(const int64_t *sup, int64_t n, const int64_t *t, con
         s += __shfl_xor_sync(0xffffffffu, s, o);
         bits |= __shfl_xor_sync(0xffffffffu, bits, o);
     }
+    // one atomic per CTA for the supply sum (it is non-zero almost everywhere)
+    __shared__ long long s_sum[8];
+    __shared__ unsigned s_bits[8];
+    const int wid = threadIdx.x >> 5;
     if (lane == 0) {
-        if (s) atomicAdd((unsigned long long *)&f[F_MISC0], (unsigned long long)s);
-        if (bits) atomicOr((unsigned long long *)&f[F_NET_ERR], (unsigned long long)bits);
+        s_sum[wid] = s;
+        s_bits[wid] = bits;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        long long ts = 0;
+        unsigned tb = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); w++) {
+            ts += s_sum[w];
+            tb |= s_bits[w];
+        }
+        if (ts) atomicAdd((unsigned long long *)&f[F_MISC0], (unsigned long long)ts);
+        if (tb) atomicOr((unsigned long long *)&f[F_NET_ERR], (unsigned long long)tb);
     }
 }
 

@@ -556,7 +556,7 @@ static int rwmd_prepare(Ctx &c, RwmdFrame &F, int range_side = -1, int64_t begin
         W1G_CHECK_LAUNCH();
     }
     k_bbox_init<<<1, 1, 0, c.stream>>>(dflags(c));
-    k_bbox<<<g, 256, 0, c.stream>>>(pts, k, dflags(c));
+    k_bbox<<<grid_for(k, 256, 2u * c.sm_count), 256, 0, c.stream>>>(pts, k, dflags(c));  // few CTAs: fewer atomics
     W1G_CHECK_LAUNCH();
     W1G_TRY(flags_fetch(c, 0, F_BBOX + 4));
     F.nm[0] = c.h_pinned[F_MISC0];

@@ -577,7 +577,7 @@ int sort_lex2_multi(Ctx &c, const Lex2Job *jobs, int njobs, bool speculative) {
         W1G_TRY(ensure(c.lex_scr[j][1], (size_t)n + 1, &excl[j]));
         if (n > 0) {
             const unsigned g = grid_for(n, 256, 8u * c.sm_count);
-            k_key_range<<<g, 256, 0, c.stream>>>(jobs[j].primary, n, mm + 4 * j);
+            k_key_range<<<grid_for(n, 256, 2u * c.sm_count), 256, 0, c.stream>>>(jobs[j].primary, n, mm + 4 * j);
             W1G_CHECK_LAUNCH();
             k_key_compress<<<g, 256, 0, c.stream>>>(jobs[j].primary, n, mm + 4 * j, pk[j]);
             W1G_CHECK_LAUNCH();
