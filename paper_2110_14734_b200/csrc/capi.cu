@@ -240,6 +240,10 @@ int w1g_ctx_destroy(w1g_ctx *c) {
         free_buf(ns.exb);
     }
     for (auto &b : c->scr) free_buf(b);
+    for (int s2 = 0; s2 < 2; s2++) {
+        free_buf(c->pw_nodes[s2]);
+        free_buf(c->pw_lev[s2]);
+    }
     for (auto &job : c->sort_scr)
         for (auto &b : job) free_buf(b);
     for (auto &job : c->lex_scr)

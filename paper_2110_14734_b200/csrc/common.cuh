@@ -97,6 +97,9 @@ struct Ctx {
     int heavy_ratio = 16;  // exact pass: disc / median disc beyond which a source is searched alone (W1G_HEAVY, 0 off)
     DevBuf best[2];
     int64_t n_best[2] = {0, 0};
+    // numpy pairwise-sum trees per side, rebuilt only when the length changes
+    DevBuf pw_nodes[2], pw_lev[2];
+    int64_t pw_n[2] = {-1, -1};
     int64_t rw_members[2] = {0, 0};  // A- and B-member counts of the last rwmd_run
 
     // split tree (over `tree_pts`, a copy of the slot's points)

@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(1024) k_pw_combine(const PwNode *nodes, const 
 
 // np.sum of a contiguous float64 vector on device -> *d_out (device)
 int pairwise_sum(Ctx &c, const double *d_v, int64_t n, double *d_out, DevBuf &nodes_buf,
-                 DevBuf &val_buf, DevBuf &lev_buf) {
+                 DevBuf &val_buf, DevBuf &lev_buf, int64_t *cached_n) {
     if (n == 0) {
         W1G_CUDA(cudaMemsetAsync(d_out, 0, sizeof(double), c.stream));
         return W1G_OK;
@@ -152,8 +152,12 @@ int pairwise_sum(Ctx &c, const double *d_v, int64_t n, double *d_out, DevBuf &no
     W1G_TRY(ensure(nodes_buf, (size_t)cap, &nodes));
     W1G_TRY(ensure(val_buf, (size_t)cap, &val));
     W1G_TRY(ensure(lev_buf, PW_MAX_LEVELS + 2, &lev));
-    k_pw_build<<<1, 1024, 0, c.stream>>>(n, nodes, lev, lev + PW_MAX_LEVELS);
-    W1G_CHECK_LAUNCH();
+    // the tree is a function of n alone: kept across calls when the caller owns the buffers
+    if (!cached_n || *cached_n != n) {
+        k_pw_build<<<1, 1024, 0, c.stream>>>(n, nodes, lev, lev + PW_MAX_LEVELS);
+        W1G_CHECK_LAUNCH();
+        if (cached_n) *cached_n = n;
+    }
     const unsigned warps = (unsigned)(n / 64 + 2);
     k_pw_leaves<<<grid_for(warps * 32, 256, 4u * c.sm_count), 256, 0, c.stream>>>(d_v, nodes, lev, lev + PW_MAX_LEVELS, val);
     W1G_CHECK_LAUNCH();

@@ -26,7 +26,7 @@ int rwmd_f32_min(Ctx &c, const double2 *q, const uint64_t *qkey, int64_t nq, con
                  const uint64_t *tkey, int64_t nt, double scale,
                  unsigned *mout, float *qn_out, double4 *tbox, int culling);
 int pairwise_sum(Ctx &c, const double *d_v, int64_t n, double *d_out, DevBuf &nodes_buf,
-                 DevBuf &val_buf, DevBuf &lev_buf);
+                 DevBuf &val_buf, DevBuf &lev_buf, int64_t *cached_n = nullptr);
 
 static const double SQRT2 = 1.4142135623730951;  // math.sqrt(2.0), diagram.py:17
 
@@ -653,7 +653,7 @@ int rwmd_run(Ctx &c, double *L, double *LA, double *LB) {
         W1G_TRY(launch_refine(c, F.mpts[s], F.mpos[s], F.members[s], mass[s], n_src, mf, qn, F.unscale, F.mpts[o],
                               n_dst, box64, sbox, best, terms));
         T.mark("refine");
-        W1G_TRY(pairwise_sum(c, terms, n_src, dres + s, c.scr[17], c.scr[18], c.scr[19]));
+        W1G_TRY(pairwise_sum(c, terms, n_src, dres + s, c.pw_nodes[s], c.scr[18], c.pw_lev[s], &c.pw_n[s]));
         T.mark("sum");
     }
     double h[2];

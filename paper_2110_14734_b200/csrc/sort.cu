@@ -235,24 +235,28 @@ struct PlanArgs {
     int njobs, words, top_bits;
     int8_t *plan;
 };
-__global__ void k_rs_plan(const __grid_constant__ PlanArgs A) {
+__global__ void __launch_bounds__(1024) k_rs_plan(const __grid_constant__ PlanArgs A) {
     __shared__ int8_t act[RS_JOBS][32];
-    const int t = threadIdx.x;  // (job, digit)
-    const int j = t / 32, d = t % 32;
-    if (j < A.njobs) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;  // one warp per (job, digit)
+    for (int t = wid; t < RS_JOBS * 32; t += blockDim.x >> 5) {
+        const int j = t / 32, d = t % 32;
         bool active = false;
-        const int w = d / 8;
-        const int dmax = (w == A.words - 1) ? (A.top_bits + 7) / 8 : 8;
-        if (w < A.words && d % 8 < dmax) {
-            const uint32_t *h = A.hist[j] + d * 256;
-            bool uniform = false;
-            for (int q = 0; q < 256; q++) uniform |= h[q] == (uint32_t)A.n[j];
-            active = !uniform;
+        if (j < A.njobs) {
+            const int w = d / 8;
+            const int dmax = (w == A.words - 1) ? (A.top_bits + 7) / 8 : 8;
+            if (w < A.words && d % 8 < dmax) {
+                const uint32_t *h = A.hist[j] + d * 256;
+                bool uniform = false;
+#pragma unroll
+                for (int q = 0; q < 8; q++) uniform |= h[q * 32 + lane] == (uint32_t)A.n[j];
+                active = !__any_sync(0xffffffffu, uniform);
+            }
         }
-        act[j][d] = active;
+        if (lane == 0) act[j][d] = active;
     }
     __syncthreads();
-    if (j < A.njobs && d == 0) {
+    if (threadIdx.x < A.njobs) {
+        const int j = threadIdx.x;
         int par = 0;
         for (int e = 0; e < 32; e++) {
             A.plan[j * RS_PLAN + e] = act[j][e] ? (int8_t)par : (int8_t)-1;
@@ -364,7 +368,7 @@ int radix_sort_multi(Ctx &c, const SortJob *jobs, int njobs, int words, int top_
         P.hist[j] = hist[j];
         P.n[j] = J[j]->n;
     }
-    k_rs_plan<<<1, 32 * RS_JOBS, 0, c.stream>>>(P);
+    k_rs_plan<<<1, 1024, 0, c.stream>>>(P);
     W1G_CHECK_LAUNCH();
     // every digit that may be active is launched; the kernels of skipped digits exit at once
     const int ndig = (words - 1) * 8 + (top_bits + 7) / 8;
