@@ -287,67 +287,98 @@ __device__ __forceinline__ bool min_at_better(double c2, uint32_t e2, double c1,
 constexpr int CSR_MED_MAX = 256;
 constexpr int CSR_LONG_MAX = 4096;
 constexpr int CSR_HUGE_CAP = 2;  // more huge rows than this: radix-sort fallback
-enum { CL_MED = 0, CL_LONG = 1, CL_HUGE = 2 };
+enum { CL_MED = 0, CL_LONG = 1, CL_HUGE = 2, CL_W32 = 3 };
 
+// rows of <= W arcs on W-lane groups (W = 16: two rows per warp; W = 32: one):
+// bitonic sort by (head, arc) in registers, then the duplicate groups reduced
+// with a segmented shuffle scan.  Every lane of the warp runs the same network
+// (rows that are empty or handled elsewhere take part with len = 0).
+template <int W>
+__device__ __forceinline__ void row_sort_reg(int64_t r, int64_t s0, int len, int32_t *slot_h,
+                                             const uint32_t *slot_e, const double *c, double *slot_c,
+                                             int64_t *dcnt) {
+    const int lane = threadIdx.x & 31, gl = lane & (W - 1);
+    const unsigned gmask = W == 32 ? 0xffffffffu : (0xffffu << (lane & 16));
+    const unsigned lt = lanemask_lt() & gmask;
+    uint64_t key = ~0ull;
+    if (gl < len) key = ((uint64_t)(uint32_t)slot_h[s0 + gl] << 32) | slot_e[s0 + gl];
+#pragma unroll
+    for (int k = 2; k <= W; k <<= 1)
+#pragma unroll
+        for (int j = k >> 1; j; j >>= 1) {
+            const uint64_t o = __shfl_xor_sync(0xffffffffu, key, j);
+            const bool up = ((gl & k) == 0) == ((gl & j) == 0);
+            key = up ? (key < o ? key : o) : (key > o ? key : o);
+        }
+    const bool valid = gl < len;
+    const int32_t head = (int32_t)(key >> 32);
+    const uint32_t e = (uint32_t)key;
+    double cost = valid ? c[e] : INFINITY;
+    const int32_t prev = __shfl_up_sync(0xffffffffu, head, 1);
+    const bool first = valid && (gl == 0 || prev != head);
+    const unsigned firsts = __ballot_sync(0xffffffffu, first) & gmask;
+    // suffix reduction inside each (head) group: lanes of a group are contiguous
+    const int gid = __popc(firsts & (lt | (1u << lane)));
+    uint32_t eb = e;
+#pragma unroll
+    for (int o = 1; o < W; o <<= 1) {
+        const double c2 = __shfl_down_sync(0xffffffffu, cost, o);
+        const uint32_t e2 = __shfl_down_sync(0xffffffffu, eb, o);
+        const int g2 = __shfl_down_sync(0xffffffffu, gid, o);
+        if (gl + o < len && g2 == gid && min_at_better(c2, e2, cost, eb)) {
+            cost = c2;
+            eb = e2;
+        }
+    }
+    if (first) {
+        const int64_t q = s0 + __popc(firsts & lt);
+        slot_h[q] = head;
+        slot_c[q] = cost;
+    }
+    if (gl == 0 && r >= 0) dcnt[r] = __popc(firsts);
+}
+
+// every row: <= 16 arcs sorted here on half warps, longer rows queued by class
 __global__ void k_csr_short_rows(const int64_t *start, int64_t n, int32_t *slot_h, const uint32_t *slot_e,
                                  const double *c, double *slot_c, int64_t *dcnt, int32_t *lists,
                                  int32_t *n_list, int64_t *f) {
-    const int lane = threadIdx.x & 31;
-    const unsigned lt = lanemask_lt();
-    for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n;
-         r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-        const int64_t s0 = start[r];
-        const int64_t len = start[r + 1] - s0;
-        if (len > 32) {
-            if (lane == 0) {
-                const int cl = len <= CSR_MED_MAX ? CL_MED : len <= CSR_LONG_MAX ? CL_LONG : CL_HUGE;
-                const int k = atomicAdd(&n_list[cl], 1);
-                if (cl != CL_HUGE || k < CSR_HUGE_CAP) {
-                    lists[(int64_t)cl * n + k] = (int32_t)r;
-                } else {  // no table left: emit nothing, the host redoes it with the full sort
-                    dcnt[r] = 0;
-                    atomicOr((unsigned long long *)&f[F_OVERFLOW], 1ull);
+    const int lane = threadIdx.x & 31, gl = lane & 15;
+    const int64_t groups = ((int64_t)gridDim.x * blockDim.x) >> 4;
+    const int64_t nr = (n + 1) & ~1ll;  // both halves of a warp iterate together
+    for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 4; r < nr; r += groups) {
+        int len = 0;
+        int64_t s0 = 0;
+        if (r < n) {
+            s0 = start[r];
+            const int64_t l = start[r + 1] - s0;
+            if (l > 16) {
+                if (gl == 0) {
+                    const int cl = l <= 32 ? CL_W32 : l <= CSR_MED_MAX ? CL_MED : l <= CSR_LONG_MAX ? CL_LONG : CL_HUGE;
+                    const int k = atomicAdd(&n_list[cl], 1);
+                    if (cl != CL_HUGE || k < CSR_HUGE_CAP) {
+                        lists[(int64_t)cl * n + k] = (int32_t)r;
+                    } else {  // no table left: emit nothing, the host redoes it with the full sort
+                        dcnt[r] = 0;
+                        atomicOr((unsigned long long *)&f[F_OVERFLOW], 1ull);
+                    }
                 }
-            }
-            continue;
-        }
-        if (len == 0) {
-            if (lane == 0) dcnt[r] = 0;
-            continue;
-        }
-        uint64_t key = ~0ull;
-        if (lane < len) key = ((uint64_t)(uint32_t)slot_h[s0 + lane] << 32) | slot_e[s0 + lane];
-        for (int k = 2; k <= 32; k <<= 1)
-            for (int j = k >> 1; j; j >>= 1) {
-                const uint64_t o = __shfl_xor_sync(0xffffffffu, key, j);
-                const bool up = ((lane & k) == 0) == ((lane & j) == 0);
-                key = up ? (key < o ? key : o) : (key > o ? key : o);
-            }
-        const bool valid = lane < len;
-        const int32_t head = (int32_t)(key >> 32);
-        const uint32_t e = (uint32_t)key;
-        double cost = valid ? c[e] : INFINITY;
-        const int32_t prev = __shfl_up_sync(0xffffffffu, head, 1);
-        const bool first = valid && (lane == 0 || prev != head);
-        const unsigned firsts = __ballot_sync(0xffffffffu, first);
-        // suffix reduction inside each (head) group: lanes of a group are contiguous
-        const int gid = __popc(firsts & (lt | (1u << lane)));
-        uint32_t eb = e;
-        for (int o = 1; o < 32; o <<= 1) {
-            const double c2 = __shfl_down_sync(0xffffffffu, cost, o);
-            const uint32_t e2 = __shfl_down_sync(0xffffffffu, eb, o);
-            const int g2 = __shfl_down_sync(0xffffffffu, gid, o);
-            if (lane + o < len && g2 == gid && min_at_better(c2, e2, cost, eb)) {
-                cost = c2;
-                eb = e2;
+            } else {
+                len = (int)l;
             }
         }
-        if (first) {
-            const int64_t q = s0 + __popc(firsts & lt);
-            slot_h[q] = head;
-            slot_c[q] = cost;
-        }
-        if (lane == 0) dcnt[r] = __popc(firsts);
+        const int64_t rr = (r < n && len > 0) ? r : -1;
+        if (r < n && len == 0 && start[r + 1] == s0 && gl == 0) dcnt[r] = 0;  // empty row
+        row_sort_reg<16>(rr, s0, len, slot_h, slot_e, c, slot_c, dcnt);
+    }
+}
+
+// rows of 17..32 arcs: a warp each
+__global__ void k_csr_w32_rows(const int64_t *start, const int32_t *rows, const int32_t *n_rows, int32_t *slot_h,
+                               const uint32_t *slot_e, const double *c, double *slot_c, int64_t *dcnt) {
+    const int nr = *n_rows;
+    for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < nr; i += (gridDim.x * blockDim.x) >> 5) {
+        const int64_t r = rows[i], s0 = start[r];
+        row_sort_reg<32>(r, s0, (int)(start[r + 1] - s0), slot_h, slot_e, c, slot_c, dcnt);
     }
 }
 
@@ -386,7 +417,50 @@ __device__ void dedup_sorted(const uint64_t *sk, int len, int part, int nparts, 
     if (part == 0) *dcnt_r = tot;
 }
 
-// rows of 33..CSR_MED_MAX arcs: a warp each, bitonic sort in its shared-memory slice
+// one warp sorts 32*E keys (head << 32 | arc) held E per lane in registers
+// (element i = lane * E + q): bitonic stages with partner distance >= E are
+// shuffles, shorter ones swaps inside the lane; the sorted row goes to sk
+template <int E>
+__device__ __forceinline__ void warp_sort_rows(uint64_t *sk, int len, int64_t s0, const int32_t *slot_h,
+                                               const uint32_t *slot_e, int lane) {
+    uint64_t v[E];
+#pragma unroll
+    for (int q = 0; q < E; q++) {
+        const int i = lane * E + q;
+        v[q] = i < len ? (((uint64_t)(uint32_t)slot_h[s0 + i] << 32) | slot_e[s0 + i]) : ~0ull;
+    }
+#pragma unroll
+    for (int k = 2; k <= 32 * E; k <<= 1)
+#pragma unroll
+        for (int j = k >> 1; j; j >>= 1) {
+            if (j >= E) {
+#pragma unroll
+                for (int q = 0; q < E; q++) {
+                    const uint64_t o = __shfl_xor_sync(0xffffffffu, v[q], j / E);
+                    const int i = lane * E + q;
+                    const bool keep_min = ((i & k) == 0) == ((i & j) == 0);
+                    v[q] = keep_min ? (v[q] < o ? v[q] : o) : (v[q] > o ? v[q] : o);
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < E; q++) {
+                    if (q & j) continue;
+                    const int p = q | j;
+                    const bool up = ((lane * E + q) & k) == 0;
+                    const uint64_t a = v[q], b = v[p];
+                    if ((a > b) == up) {
+                        v[q] = b;
+                        v[p] = a;
+                    }
+                }
+            }
+        }
+#pragma unroll
+    for (int q = 0; q < E; q++) sk[lane * E + q] = v[q];
+}
+
+// rows of 33..CSR_MED_MAX arcs: a warp each, sorted in registers, deduplicated
+// from its shared-memory slice
 constexpr int CSR_MB = 256;
 __global__ void __launch_bounds__(CSR_MB) k_csr_med_rows(const int64_t *start, const int32_t *rows,
                                                          const int32_t *n_rows, int32_t *slot_h,
@@ -401,26 +475,11 @@ __global__ void __launch_bounds__(CSR_MB) k_csr_med_rows(const int64_t *start, c
         const int64_t r = rows[ri];
         const int64_t s0 = start[r];
         const int len = (int)(start[r + 1] - s0);
-        int np2 = 64;
-        while (np2 < len) np2 <<= 1;
         __syncwarp();
-        for (int i = lane; i < np2; i += 32)
-            sk[i] = i < len ? (((uint64_t)(uint32_t)slot_h[s0 + i] << 32) | slot_e[s0 + i]) : ~0ull;
+        if (len <= 64) warp_sort_rows<2>(sk, len, s0, slot_h, slot_e, lane);
+        else if (len <= 128) warp_sort_rows<4>(sk, len, s0, slot_h, slot_e, lane);
+        else warp_sort_rows<8>(sk, len, s0, slot_h, slot_e, lane);
         __syncwarp();
-        for (int k = 2; k <= np2; k <<= 1)
-            for (int j = k >> 1; j; j >>= 1) {
-                for (int i = lane; i < np2; i += 32) {
-                    const int p = i ^ j;
-                    if (p > i) {
-                        const uint64_t a = sk[i], b = sk[p];
-                        if ((a > b) == ((i & k) == 0)) {
-                            sk[i] = b;
-                            sk[p] = a;
-                        }
-                    }
-                }
-                __syncwarp();
-            }
         dedup_sorted(sk, len, lane, 32, cnt_all[wid], s0, c, slot_h, slot_c, dcnt + r, []() { __syncwarp(); });
         __syncwarp();
     }
@@ -533,14 +592,16 @@ struct DCount {
 
 // deduplicated rows to their CSR positions: a warp per row of <= CSR_MED_MAX
 // deduplicated arcs, a CTA per listed longer row
-__global__ void k_csr_emit(const int64_t *start, const int64_t *ro, int64_t n, const int32_t *slot_h,
-                           const double *slot_c, int64_t *ot, int64_t *oh, double *oc) {
-    const int lane = threadIdx.x & 31;
-    for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n;
-         r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+__global__ void k_csr_emit(const int64_t *__restrict__ start, const int64_t *__restrict__ ro, int64_t n,
+                           const int32_t *__restrict__ slot_h, const double *__restrict__ slot_c,
+                           int64_t *__restrict__ ot, int64_t *__restrict__ oh, double *__restrict__ oc) {
+    // half a warp per row: rows average ~16 arcs at s = 1
+    const int hl = threadIdx.x & 15;
+    for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 4; r < n;
+         r += ((int64_t)gridDim.x * blockDim.x) >> 4) {
         const int64_t s0 = start[r], d0 = ro[r], len = ro[r + 1] - d0;
         if (start[r + 1] - s0 > CSR_MED_MAX) continue;  // k_csr_emit_long
-        for (int64_t k = lane; k < len; k += 32) {
+        for (int64_t k = hl; k < len; k += 16) {
             ot[d0 + k] = r;
             oh[d0 + k] = slot_h[s0 + k];
             oc[d0 + k] = slot_c[s0 + k];
@@ -715,7 +776,7 @@ int net_run(Ctx &c, const int64_t *d_sup, int64_t n, int64_t *n_arcs) {
     cursor = cnt + n + 2;
     W1G_TRY(ensure(c.scr[3], (size_t)n + 2, &start));
     W1G_TRY(ensure(c.scr[5], (size_t)n + 1, &dcnt));
-    W1G_TRY(ensure(c.scr[6], (size_t)3 * (n + 1), &lists));
+    W1G_TRY(ensure(c.scr[6], (size_t)4 * (n + 1), &lists));
     W1G_TRY(ensure(c.scr[0], (size_t)m + 1, &slot_h));
     W1G_TRY(ensure(c.scr[2], (size_t)m + 1, &slot_e));
     W1G_TRY(ensure(c.scr[4], (size_t)m + 1, &slot_c));
@@ -723,7 +784,7 @@ int net_run(Ctx &c, const int64_t *d_sup, int64_t n, int64_t *n_arcs) {
     W1G_TRY(ensure(c.scr[8], (size_t)CSR_HUGE_CAP * (n + 1), &tab_e));
     int64_t *hpos;
     W1G_TRY(ensure(c.scr[9], (size_t)CSR_HUGE_CAP * n + 2, &hpos));
-    int32_t *n_list = reinterpret_cast<int32_t *>(dflags(c) + F_MISC2);  // 3 counters (F_MISC2..)
+    int32_t *n_list = reinterpret_cast<int32_t *>(dflags(c) + F_MISC2);  // 4 int32 counters (F_MISC2, F_MISC3)
     W1G_TRY(flags_reset(c));
     W1G_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned) * 2 * (n + 2), c.stream));
     // validation is checked at the one host round trip at the end; invalid
@@ -737,8 +798,11 @@ int net_run(Ctx &c, const int64_t *d_sup, int64_t n, int64_t *n_arcs) {
     }
     T.mark("bucket");
     if (n > 0) {
-        k_csr_short_rows<<<grid_for(n * 32, 256, 16u * c.sm_count), 256, 0, c.stream>>>(
+        k_csr_short_rows<<<grid_for(n * 16, 256, 16u * c.sm_count), 256, 0, c.stream>>>(
             start, n, slot_h, slot_e, cs, slot_c, dcnt, lists, n_list, dflags(c));
+        W1G_CHECK_LAUNCH();
+        k_csr_w32_rows<<<4 * c.sm_count, 256, 0, c.stream>>>(start, lists + CL_W32 * n, n_list + CL_W32, slot_h,
+                                                             slot_e, cs, slot_c, dcnt);
         W1G_CHECK_LAUNCH();
         T.mark("short");
         k_csr_med_rows<<<8 * c.sm_count, CSR_MB, 0, c.stream>>>(start, lists + CL_MED * n, n_list + CL_MED,
@@ -765,7 +829,7 @@ int net_run(Ctx &c, const int64_t *d_sup, int64_t n, int64_t *n_arcs) {
     // row_offsets = [0, cumsum(bincount(t, n))], network.py:84-85
     W1G_TRY(scan_i64(c, DCount{dcnt, n}, n + 1, ro, dflags(c) + F_TOTAL));
     if (n > 0) {
-        k_csr_emit<<<grid_for(n * 32, 256, 16u * c.sm_count), 256, 0, c.stream>>>(start, ro, n, slot_h, slot_c, ot,
+        k_csr_emit<<<grid_for(n * 16, 256, 16u * c.sm_count), 256, 0, c.stream>>>(start, ro, n, slot_h, slot_c, ot,
                                                                                   oh, oc);
         W1G_CHECK_LAUNCH();
         k_csr_emit_long<<<2 * c.sm_count, 256, 0, c.stream>>>(start, ro, n, lists, n_list, slot_h, slot_c, ot, oh, oc);
