@@ -489,15 +489,16 @@ __global__ void k_key_range(const uint64_t *k, int64_t n, unsigned long long *mm
 __device__ __forceinline__ double dkey_value(unsigned long long k) {
     return __longlong_as_double((long long)((k >> 63) ? (k & 0x7fffffffffffffffull) : ~k));
 }
-__global__ void k_key_compress(const uint64_t *k, int64_t n, const unsigned long long *mm, uint64_t *out) {
+__global__ void k_key_compress(const uint64_t *k, int64_t n, const unsigned long long *mm, double kmax,
+                               uint64_t *out) {
     const double lo = dkey_value(mm[0]), hi = dkey_value(mm[1]);
     const double range = hi - lo;
     const bool flat = !(range > 0.0) || !isfinite(range);
-    const double scale = flat ? 0.0 : 4294967295.0 / range;
+    const double scale = flat ? 0.0 : kmax / range;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         double t = flat ? 0.0 : floor((dkey_value(k[i]) - lo) * scale);
-        t = t < 0.0 ? 0.0 : (t > 4294967295.0 ? 4294967295.0 : t);
+        t = t < 0.0 ? 0.0 : (t > kmax ? kmax : t);
         out[i] = (uint64_t)t;
     }
 }
@@ -506,6 +507,10 @@ __global__ void k_key_compress(const uint64_t *k, int64_t n, const unsigned long
 // (primary, secondary, input position) with an insertion sort; the longest run
 // is reported so the host can take the radix path for long runs instead
 constexpr int TIE_SMALL = 32;
+#ifndef W1G_LEX_BITS
+#define W1G_LEX_BITS 32
+#endif
+constexpr int LEX_BITS = W1G_LEX_BITS;  // compressed key width (8-bit radix digits)
 __global__ void k_tie_runs(const uint64_t *pk, int64_t n, unsigned long long *maxrun, int64_t *count) {
     unsigned long long mr = 0;
     int64_t cnt = 0;
@@ -583,12 +588,13 @@ int sort_lex2_multi(Ctx &c, const Lex2Job *jobs, int njobs, bool speculative) {
             const unsigned g = grid_for(n, 256, 8u * c.sm_count);
             k_key_range<<<grid_for(n, 256, 2u * c.sm_count), 256, 0, c.stream>>>(jobs[j].primary, n, mm + 4 * j);
             W1G_CHECK_LAUNCH();
-            k_key_compress<<<g, 256, 0, c.stream>>>(jobs[j].primary, n, mm + 4 * j, pk[j]);
+            k_key_compress<<<g, 256, 0, c.stream>>>(jobs[j].primary, n, mm + 4 * j, (double)((1ull << LEX_BITS) - 1),
+                                                   pk[j]);
             W1G_CHECK_LAUNCH();
         }
         sj[j] = SortJob{{pk[j], nullptr, nullptr}, jobs[j].vals, n};
     }
-    W1G_TRY(radix_sort_multi(c, sj, njobs, 1, 32));
+    W1G_TRY(radix_sort_multi(c, sj, njobs, 1, LEX_BITS));
     for (int j = 0; j < njobs; j++) {
         if (jobs[j].n > 1) {
             k_tie_runs<<<grid_for(jobs[j].n, 256, 8u * c.sm_count), 256, 0, c.stream>>>(
