@@ -28,16 +28,24 @@ int cuda_fail(cudaError_t e, const char *what, const char *file, int line) {
     return W1G_ECUDA;
 }
 
+// the stream the calling thread's context launches on (set at every C-ABI entry
+// and by the auxiliary RWMD thread): buffers grow stream-ordered on it, from the
+// device's memory pool, so a first call at a new size does not stall the device
+// on cudaFree's implicit synchronisation
+static thread_local cudaStream_t g_tl_stream = nullptr;
+void set_thread_stream(cudaStream_t s) { g_tl_stream = s; }
+
 int ensure_bytes(DevBuf &b, size_t bytes) {
     if (bytes <= b.cap) return W1G_OK;
     size_t want = bytes + bytes / 4 + 4096;
+    cudaStream_t st = g_tl_stream;
     if (b.p) {
-        cudaError_t e = cudaFree(b.p);
+        cudaError_t e = st ? cudaFreeAsync(b.p, st) : cudaFree(b.p);
         b.p = nullptr;
         b.cap = 0;
         if (e != cudaSuccess) return cuda_fail(e, "cudaFree", __FILE__, __LINE__);
     }
-    cudaError_t e = cudaMalloc(&b.p, want);
+    cudaError_t e = st ? cudaMallocAsync(&b.p, want, st) : cudaMalloc(&b.p, want);
     if (e != cudaSuccess) {
         cudaGetLastError();
         b.p = nullptr;
@@ -153,6 +161,7 @@ using namespace w1g;
         }                                                \
         cudaError_t _e = cudaSetDevice((ctx)->device);   \
         if (_e != cudaSuccess) return cuda_fail(_e, "cudaSetDevice", __FILE__, __LINE__); \
+        set_thread_stream((ctx)->stream);                \
     } while (0)
 
 extern "C" {
@@ -207,6 +216,21 @@ int w1g_ctx_create(int device, w1g_ctx **out) {
     if (const char *e = getenv("W1G_HEAVY")) c->heavy_ratio = atoi(e) > 0 ? atoi(e) : 0;
     if (const char *e = getenv("W1G_OVERLAP")) c->overlap = atoi(e) > 0 ? atoi(e) : 0;
     W1G_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    {
+        // freed pool memory stays cached for the next growth (stream-ordered buffers)
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+            uint64_t keep = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+    }
+    // the context's own buffers are ordered on its own stream; the caller's
+    // thread keeps whatever stream it was working on
+    struct RestoreStream {
+        cudaStream_t prev;
+        ~RestoreStream() { set_thread_stream(prev); }
+    } restore{g_tl_stream};
+    set_thread_stream(c->stream);
     int64_t *f;
     W1G_TRY(ensure(c->flags, F_NSLOTS, &f));
     W1G_CUDA(cudaHostAlloc(&c->h_pinned, sizeof(int64_t) * F_NSLOTS, cudaHostAllocDefault));
@@ -701,6 +725,7 @@ int w1g_front_end_device(w1g_ctx *c, const double *d_a, int64_t na, const double
         W1G_CUDA(cudaStreamWaitEvent(x->stream, c->ev[8], 0));
         worker = std::thread([&, x]() {
             cudaSetDevice(x->device);
+            set_thread_stream(x->stream);
             cudaEventRecord(x->ev[0], x->stream);
             rc_aux = rwmd_run(*x, &L, &LA, &LB);
             if (rc_aux == W1G_OK) rc_aux = cudaEventRecord(x->ev[1], x->stream) == cudaSuccess ? W1G_OK : W1G_ECUDA;

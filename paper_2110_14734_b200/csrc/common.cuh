@@ -49,6 +49,7 @@ struct DevBuf {
 };
 // grow-only device buffer (geometric); contents are NOT preserved on growth
 int ensure_bytes(DevBuf &b, size_t bytes);
+void set_thread_stream(cudaStream_t s);  // stream-ordered growth for this thread's context
 template <class T>
 inline int ensure(DevBuf &b, size_t n, T **out) {
     int rc = ensure_bytes(b, n * sizeof(T) + 16);
