@@ -103,9 +103,9 @@ __device__ __forceinline__ void wspd_level(const typename ItemT<ORDER>::T *__res
                                            uint64_t *__restrict__ out_p0,
                                            uint64_t *__restrict__ out_p1, int64_t pair_cap,
                                            double s, const NodeGeom *__restrict__ geom,
-                                           const int2 *__restrict__ lr) {
+                                           const int2 *__restrict__ lr, int64_t n_known = -1) {
     using Item = typename ItemT<ORDER>::T;
-    int64_t n = *((volatile int64_t *)&k.cnt[level % 3]);
+    int64_t n = n_known >= 0 ? n_known : *((volatile int64_t *)&k.cnt[level % 3]);
     if (n > cap) n = cap;  // previous level overflowed: its flag is already set
     if (blockIdx.x == 0 && threadIdx.x == 0) k.cnt[(level + 2) % 3] = 0;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -220,7 +220,7 @@ __global__ void __launch_bounds__(256) k_wspd_coop(typename ItemT<ORDER>::T *fa,
         const int64_t n = *((volatile int64_t *)&k.cnt[level % 3]);
         if (n == 0 || n > cap) break;  // done, or the last level overflowed (flag set)
         wspd_level<ORDER>((level & 1) ? fb : fa, (level & 1) ? fa : fb, cap, level, k, out_uv, out_w, out_p0,
-                          out_p1, pair_cap, s, geom, lr);
+                          out_p1, pair_cap, s, geom, lr, n);
         grid.sync();
         level++;
     }
