@@ -215,7 +215,14 @@ int w1g_ctx_create(int device, w1g_ctx **out) {
     if (const char *e = getenv("W1G_DEBUG_RADIUS")) c->debug_radius = atoi(e) ? 1 : 0;
     if (const char *e = getenv("W1G_HEAVY")) c->heavy_ratio = atoi(e) > 0 ? atoi(e) : 0;
     if (const char *e = getenv("W1G_OVERLAP")) c->overlap = atoi(e) > 0 ? atoi(e) : 0;
-    W1G_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    {
+        // contexts launch at the highest stream priority; the auxiliary RWMD
+        // context drops to the lowest (start_rwmd), so when both have work the
+        // block scheduler feeds the critical back end first
+        int least = 0, greatest = 0;
+        W1G_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+        W1G_CUDA(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, greatest));
+    }
     {
         // freed pool memory stays cached for the next growth (stream-ordered buffers)
         cudaMemPool_t pool;
@@ -714,6 +721,11 @@ int w1g_front_end_device(w1g_ctx *c, const double *d_a, int64_t na, const double
         if (!c->aux) {
             w1g_ctx *x = nullptr;
             W1G_TRY(w1g_ctx_create(c->device, &x));
+            int least = 0, greatest = 0;
+            W1G_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+            W1G_CUDA(cudaStreamSynchronize(x->stream));  // its first allocations are ordered on it
+            W1G_CUDA(cudaStreamDestroy(x->stream));
+            W1G_CUDA(cudaStreamCreateWithPriority(&x->stream, cudaStreamNonBlocking, least));
             c->aux = x;
         }
         Ctx *x = c->aux;
