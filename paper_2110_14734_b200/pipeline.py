@@ -14,6 +14,7 @@ from __future__ import annotations
 import ctypes
 import math
 import os
+import threading
 from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass, field
 
@@ -197,14 +198,43 @@ def pair_shard(n_diagrams: int, rank: int, world: int) -> list[tuple[int, int]]:
     return pairs[rank::world]
 
 
+def _run_pairs(pts, todo, params: ApproxParams, devs, streams_per_device: int, on_network) -> None:
+    """Front ends of `todo` pairs, round-robin over devices x streams: every
+    (device, stream) worker is one host thread with its own context -- own CUDA
+    stream, buffers and RWMD side stream -- so several latency-bound front ends
+    of small diagrams share a GPU.  on_network(i, j, net, diag) runs in the worker."""
+    workers = [(d, k) for k in range(max(1, streams_per_device)) for d in devs]
+
+    def worker(w: int):
+        dev = workers[w][0]
+        for i, j in todo[w::len(workers)]:
+            net, diag = sparsify(pts[i], pts[j], params, device=dev)
+            on_network(i, j, net, diag)
+
+    with ThreadPoolExecutor(max_workers=len(workers)) as wp:
+        list(wp.map(worker, range(len(workers))))
+
+
+def sparsify_batch(diagrams, params: ApproxParams, pairs: list[tuple[int, int]] | None = None, devices=None,
+                   streams_per_device: int = 3, on_network=None) -> int:
+    """The front end of every pair (i < j, or `pairs`) of a diagram batch, sharded
+    over devices and streams; on_network(i, j, network | None, diag) receives each
+    result (in a worker thread).  Returns the number of pairs processed."""
+    pts = [points_of(d) for d in diagrams]
+    n = len(pts)
+    todo = pairs if pairs is not None else [(i, j) for i in range(n) for j in range(i + 1, n)]
+    _run_pairs(pts, todo, params, _devices(devices), streams_per_device, on_network or (lambda *a: None))
+    return len(todo)
+
+
 def pairwise_w1(diagrams, params: ApproxParams, devices=None, solver_threads: int | None = None,
-                pairs: list[tuple[int, int]] | None = None) -> np.ndarray:
+                pairs: list[tuple[int, int]] | None = None, streams_per_device: int = 3) -> np.ndarray:
     """Symmetric matrix of approx_w1(D[i], D[j]) for i < j, mirrored to (j, i).
 
-    Pairs are sharded round-robin over `devices` (one host thread and one
-    context per device, no collective); each device's networks go to a pool
-    of `solver_threads` host threads running the reference solver (numba,
-    GIL released).  `pairs` restricts the work to a subset (other entries NaN).
+    Pairs are sharded round-robin over `devices` x `streams_per_device` (one host
+    thread and one context each, no collective); the networks go to a pool of
+    `solver_threads` host threads running the reference solver (numba, GIL
+    released).  `pairs` restricts the work to a subset (other entries NaN).
     """
     pts = [points_of(d) for d in diagrams]
     n = len(pts)
@@ -213,20 +243,20 @@ def pairwise_w1(diagrams, params: ApproxParams, devices=None, solver_threads: in
     out = np.full((n, n), np.nan)
     np.fill_diagonal(out, 0.0)
     if solver_threads is None:
-        solver_threads = max(1, (os.cpu_count() or 1) - len(devs))
+        solver_threads = max(1, (os.cpu_count() or 1) - len(devs) * max(1, streams_per_device))
     pool = ThreadPoolExecutor(max_workers=solver_threads)
     futures = []
+    lock = threading.Lock()
 
-    def device_worker(dev: int, mine: list[tuple[int, int]]):
-        for i, j in mine:
-            net, diag = sparsify(pts[i], pts[j], params, device=dev)
-            if net is None:
-                out[i, j] = out[j, i] = 0.0
-                continue
-            futures.append((i, j, pool.submit(solve_network, net, params, diag)))
+    def on_network(i, j, net, diag):
+        if net is None:
+            out[i, j] = out[j, i] = 0.0
+            return
+        f = pool.submit(solve_network, net, params, diag)
+        with lock:
+            futures.append((i, j, f))
 
-    with ThreadPoolExecutor(max_workers=len(devs)) as dpool:
-        list(dpool.map(lambda k: device_worker(devs[k], todo[k::len(devs)]), range(len(devs))))
+    _run_pairs(pts, todo, params, devs, streams_per_device, on_network)
     for i, j, f in futures:
         out[i, j] = out[j, i] = f.result()
     pool.shutdown()
