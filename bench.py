@@ -77,20 +77,19 @@ HBM_PEAK_GBS = 6528.7  # MEASURED_PEAKS.json hbm_gbs (copy bandwidth, read + wri
 def hbm_stages(n_in: int, k0: int, k: int, p: int, m: int, stage_ms: dict) -> dict:
     """Algorithmic HBM bytes of the byte-moving stages (each stage's inputs read once and
     outputs written once) over their measured device time, against
-    the measured copy bandwidth.  Raw arcs are bounded below by 2P + K + 1."""
-    m_raw = 2 * p + k + 1
+    the measured copy bandwidth.  emit_arcs is fused into the CSR assembly (the pairs
+    and node arrays are read, the network written; no arc list in between)."""
     nn = max(2 * k - 1, 0)
     bytes_ = {
         "zero_condense": 16 * n_in + 32 * k0,
         "delta_condense": 32 * k0 + 32 * k,
         "split_tree": 16 * k + 64 * nn,
         "wspd": 40 * nn + 24 * p,
-        "emit_arcs": 16 * p + 16 * k + 24 * m_raw,
-        "assemble": 24 * m_raw + 24 * m + 16 * (k + 3),
+        "emit_arcs+assemble": 16 * p + 32 * k + 24 * m + 16 * (k + 3),
     }
     out = {}
     for name, b in bytes_.items():
-        t = stage_ms.get(name)
+        t = sum(stage_ms.get(x) or 0.0 for x in name.split("+"))
         if not t:
             continue
         gbs = b / (t * 1e-3) / 1e9

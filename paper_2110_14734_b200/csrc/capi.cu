@@ -773,13 +773,12 @@ int w1g_front_end_device(w1g_ctx *c, const double *d_a, int64_t na, const double
         info->n_pairs = P;
         info->n_levels_wspd = c->wspd_levels;
         if (spawn && c->overlap == 1) W1G_TRY(start_rwmd());
-        int64_t M;
-        W1G_TRY(emit_run(*c, &M));
+        // emit_arcs is fused into the CSR assembly (the arc list is never
+        // materialised), so stage 5 (emit) is empty on this path
         W1G_CUDA(cudaEventRecord(ev[6], c->stream));
-    host_t[6] = std::chrono::steady_clock::now();
-        int64_t *dsup, nsup, mm;
-        W1G_TRY(assemble_supplies(*c, &dsup, &nsup));
-        W1G_TRY(net_run(*c, dsup, nsup, &mm));
+        host_t[6] = std::chrono::steady_clock::now();
+        int64_t nsup, mm;
+        W1G_TRY(spanner_net_run(*c, &nsup, &mm));
         W1G_CUDA(cudaEventRecord(ev[7], c->stream));
     host_t[7] = std::chrono::steady_clock::now();
         info->n_arcs = mm;

@@ -444,6 +444,9 @@ int wspd_run(Ctx &c, double s, int reference_order, int64_t *n_pairs);
 int emit_run(Ctx &c, int64_t *n_arcs);
 int net_run(Ctx &c, const int64_t *d_supplies, int64_t n, int64_t *n_arcs);
 int assemble_supplies(Ctx &c, int64_t **d_sup, int64_t *n);
+// fused front end: emit_arcs + assemble straight from the WSPD pairs (the arc
+// list is not materialised); falls back to emit_run + net_run when needed
+int spanner_net_run(Ctx &c, int64_t *node_count, int64_t *n_arcs);
 
 }  // namespace w1g
 

@@ -420,14 +420,13 @@ __device__ void dedup_sorted(const uint64_t *sk, int len, int part, int nparts, 
 // one warp sorts 32*E keys (head << 32 | arc) held E per lane in registers
 // (element i = lane * E + q): bitonic stages with partner distance >= E are
 // shuffles, shorter ones swaps inside the lane; the sorted row goes to sk
-template <int E>
-__device__ __forceinline__ void warp_sort_rows(uint64_t *sk, int len, int64_t s0, const int32_t *slot_h,
-                                               const uint32_t *slot_e, int lane) {
+template <int E, class Load>
+__device__ __forceinline__ void warp_sort_keys(uint64_t *sk, int len, int lane, Load load) {
     uint64_t v[E];
 #pragma unroll
     for (int q = 0; q < E; q++) {
         const int i = lane * E + q;
-        v[q] = i < len ? (((uint64_t)(uint32_t)slot_h[s0 + i] << 32) | slot_e[s0 + i]) : ~0ull;
+        v[q] = i < len ? load(i) : ~0ull;
     }
 #pragma unroll
     for (int k = 2; k <= 32 * E; k <<= 1)
@@ -457,6 +456,12 @@ __device__ __forceinline__ void warp_sort_rows(uint64_t *sk, int len, int64_t s0
         }
 #pragma unroll
     for (int q = 0; q < E; q++) sk[lane * E + q] = v[q];
+}
+template <int E>
+__device__ __forceinline__ void warp_sort_rows(uint64_t *sk, int len, int64_t s0, const int32_t *slot_h,
+                                               const uint32_t *slot_e, int lane) {
+    warp_sort_keys<E>(sk, len, lane,
+                      [&](int i) { return ((uint64_t)(uint32_t)slot_h[s0 + i] << 32) | slot_e[s0 + i]; });
 }
 
 // rows of 33..CSR_MED_MAX arcs: a warp each, sorted in registers, deduplicated
@@ -623,6 +628,267 @@ __global__ void k_csr_emit_long(const int64_t *__restrict__ start, const int64_t
             oh[d0 + k] = slot_h[s0 + k];
             oc[d0 + k] = slot_c[s0 + k];
         }
+    }
+}
+
+// ---------------------------------------------------------------- fused spanner CSR
+//
+// In the fused front end the arc list has a known shape (spanner.py:310-337):
+// both directions of every WSPD pair, i -> abar for each A-member, bbar -> i
+// for each B-member, then bbar -> abar.  No (tail, head) repeats: a WSPD
+// covers every point pair exactly once, so two pairs never share both
+// representatives.  np.lexsort + np.minimum.at (network.py:70-82) therefore
+// reduce to: bucket the pair arcs by tail, sort each row by head, and put
+// abar (= K, above every point) last in the A-member rows; the bbar row is the
+// B-members in node order, then abar.  The ArcList itself is never written.
+// A repeated head (impossible for a WSPD) or a row longer than CSR_LONG_MAX
+// is flagged, and the host redoes the network on the generic path.
+constexpr long long SP_DUP_BIT = 1ll << 16;  // in F_NET_ERR
+
+// arc cost per pair (spanner.py:324, both directions share it) and pair arcs per tail
+__global__ void k_sp_count(const int64_t *__restrict__ idx, int64_t P, const double2 *__restrict__ pts,
+                           unsigned *cnt, double *pcost, int64_t *f) {
+    const int lane = threadIdx.x & 31;
+    unsigned bad = 0;
+    const int64_t pr = (P + 31) & ~31ll;
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < pr; p += (int64_t)gridDim.x * blockDim.x) {
+        long long i = -1, j = -1;
+        if (p < P) {
+            i = idx[2 * p];
+            j = idx[2 * p + 1];
+            const double2 a = pts[i], b = pts[j];
+            const double cc = glibc_hypot(dsub(a.x, b.x), dsub(a.y, b.y));
+            pcost[p] = cc;
+            if (!isfinite(cc)) bad = 1;
+        }
+        unsigned peers = __match_any_sync(0xffffffffu, i);
+        if (i >= 0 && (__ffs(peers) - 1) == lane) atomicAdd(&cnt[i], (unsigned)__popc(peers));
+        peers = __match_any_sync(0xffffffffu, j);
+        if (j >= 0 && (__ffs(peers) - 1) == lane) atomicAdd(&cnt[j], (unsigned)__popc(peers));
+    }
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr((unsigned long long *)&f[F_NET_ERR], 4ull);
+}
+
+// row lengths: pair arcs (+ abar for A-members) | abar: none | bbar: B-members + abar
+struct SpRowLen {
+    const unsigned *cnt;
+    const int64_t *am;
+    int64_t K, nb;
+    __device__ int64_t operator()(int64_t i) const {
+        if (i < K) return (int64_t)cnt[i] + (am[i] > 0 ? 1 : 0);
+        return i == K + 1 ? nb + 1 : 0;
+    }
+};
+
+// pair arcs into their tail rows as (head << 32 | pair) keys, warp-aggregated
+__global__ void k_sp_scatter(const int64_t *__restrict__ idx, int64_t P, const int64_t *__restrict__ ro,
+                             unsigned *cursor, uint64_t *slot) {
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = lanemask_lt();
+    const int64_t pr = (P + 31) & ~31ll;
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < pr; p += (int64_t)gridDim.x * blockDim.x) {
+        long long e[2] = {-1, -1};
+        if (p < P) {
+            e[0] = idx[2 * p];
+            e[1] = idx[2 * p + 1];
+        }
+#pragma unroll
+        for (int d = 0; d < 2; d++) {
+            const long long t = e[d], h = e[d ^ 1];
+            const unsigned peers = __match_any_sync(0xffffffffu, t);
+            const int leader = __ffs(peers) - 1;
+            unsigned base = 0;
+            if (t >= 0 && lane == leader) base = atomicAdd(&cursor[t], (unsigned)__popc(peers));
+            base = __shfl_sync(0xffffffffu, base, leader);
+            if (t >= 0) slot[ro[t] + base + __popc(peers & lt)] = ((uint64_t)h << 32) | (uint64_t)p;
+        }
+    }
+}
+
+__device__ __forceinline__ void sp_put(int64_t r, int64_t q, uint64_t key, const double *__restrict__ pcost,
+                                       int64_t *ot, int64_t *oh, double *oc) {
+    ot[q] = r;
+    oh[q] = (int64_t)(key >> 32);
+    oc[q] = pcost[(uint32_t)key];
+}
+
+// rows of <= W pair arcs on W-lane groups: bitonic sort of the keys in
+// registers, written straight to the CSR
+template <int W>
+__device__ __forceinline__ void sp_row_reg(int64_t r, int64_t s0, int len, const uint64_t *__restrict__ slot,
+                                           const double *__restrict__ pcost, int64_t *ot, int64_t *oh, double *oc,
+                                           unsigned &dup) {
+    const int lane = threadIdx.x & 31, gl = lane & (W - 1);
+    uint64_t key = gl < len ? slot[s0 + gl] : ~0ull;
+#pragma unroll
+    for (int k = 2; k <= W; k <<= 1)
+#pragma unroll
+        for (int j = k >> 1; j; j >>= 1) {
+            const uint64_t o = __shfl_xor_sync(0xffffffffu, key, j);
+            const bool up = ((gl & k) == 0) == ((gl & j) == 0);
+            key = up ? (key < o ? key : o) : (key > o ? key : o);
+        }
+    const uint32_t head = (uint32_t)(key >> 32);
+    const uint32_t prev = __shfl_up_sync(0xffffffffu, head, 1);
+    if (gl < len) {
+        if (gl > 0 && prev == head) dup = 1;
+        sp_put(r, s0 + gl, key, pcost, ot, oh, oc);
+    }
+}
+
+__global__ void k_sp_short_rows(const int64_t *__restrict__ ro, const unsigned *__restrict__ cnt, int64_t K,
+                                const uint64_t *__restrict__ slot, const double *__restrict__ pcost, int64_t *ot,
+                                int64_t *oh, double *oc, int32_t *lists, int32_t *n_list, int64_t *f,
+                                unsigned long_max) {
+    const int lane = threadIdx.x & 31, gl = lane & 15;
+    const int64_t groups = ((int64_t)gridDim.x * blockDim.x) >> 4;
+    const int64_t nr = (K + 1) & ~1ll;  // both halves of a warp iterate together
+    unsigned dup = 0;
+    for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 4; r < nr; r += groups) {
+        int len = 0;
+        int64_t s0 = 0;
+        if (r < K) {
+            s0 = ro[r];
+            const unsigned l = cnt[r];
+            if (l > 16) {
+                if (gl == 0) {
+                    if (l > long_max) {
+                        atomicOr((unsigned long long *)&f[F_OVERFLOW], 1ull);
+                    } else {
+                        const int cl = l <= 32 ? CL_W32 : l <= CSR_MED_MAX ? CL_MED : CL_LONG;
+                        lists[(int64_t)cl * K + atomicAdd(&n_list[cl], 1)] = (int32_t)r;
+                    }
+                }
+            } else {
+                len = (int)l;
+            }
+        }
+        sp_row_reg<16>(r, s0, len, slot, pcost, ot, oh, oc, dup);
+    }
+    if (__any_sync(0xffffffffu, dup) && lane == 0) atomicOr((unsigned long long *)&f[F_NET_ERR], SP_DUP_BIT);
+}
+
+__global__ void k_sp_w32_rows(const int64_t *__restrict__ ro, const unsigned *__restrict__ cnt,
+                              const int32_t *rows, const int32_t *n_rows, const uint64_t *__restrict__ slot,
+                              const double *__restrict__ pcost, int64_t *ot, int64_t *oh, double *oc, int64_t *f) {
+    const int nr = *n_rows;
+    unsigned dup = 0;
+    for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < nr; i += (gridDim.x * blockDim.x) >> 5) {
+        const int64_t r = rows[i];
+        sp_row_reg<32>(r, ro[r], (int)cnt[r], slot, pcost, ot, oh, oc, dup);
+    }
+    if (__any_sync(0xffffffffu, dup) && (threadIdx.x & 31) == 0)
+        atomicOr((unsigned long long *)&f[F_NET_ERR], SP_DUP_BIT);
+}
+
+// rows of 33..CSR_MED_MAX pair arcs: a warp each, sorted in registers
+__global__ void __launch_bounds__(CSR_MB) k_sp_med_rows(const int64_t *__restrict__ ro,
+                                                        const unsigned *__restrict__ cnt, const int32_t *rows,
+                                                        const int32_t *n_rows, const uint64_t *__restrict__ slot,
+                                                        const double *__restrict__ pcost, int64_t *ot, int64_t *oh,
+                                                        double *oc, int64_t *f) {
+    __shared__ uint64_t sk_all[CSR_MB / 32][CSR_MED_MAX];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint64_t *sk = sk_all[wid];
+    const int nr = *n_rows;
+    unsigned dup = 0;
+    for (int ri = blockIdx.x * (CSR_MB / 32) + wid; ri < nr; ri += gridDim.x * (CSR_MB / 32)) {
+        const int64_t r = rows[ri];
+        const int64_t s0 = ro[r];
+        const int len = (int)cnt[r];
+        auto load = [&](int i) { return slot[s0 + i]; };
+        __syncwarp();
+        if (len <= 64) warp_sort_keys<2>(sk, len, lane, load);
+        else if (len <= 128) warp_sort_keys<4>(sk, len, lane, load);
+        else warp_sort_keys<8>(sk, len, lane, load);
+        __syncwarp();
+        for (int i = lane; i < len; i += 32) {
+            const uint64_t key = sk[i];
+            if (i > 0 && (key >> 32) == (sk[i - 1] >> 32)) dup = 1;
+            sp_put(r, s0 + i, key, pcost, ot, oh, oc);
+        }
+    }
+    if (__any_sync(0xffffffffu, dup) && lane == 0) atomicOr((unsigned long long *)&f[F_NET_ERR], SP_DUP_BIT);
+}
+
+// rows of CSR_MED_MAX+1..CSR_LONG_MAX pair arcs: a CTA each, bitonic sort in shared memory
+__global__ void __launch_bounds__(CSR_LB) k_sp_long_rows(const int64_t *__restrict__ ro,
+                                                         const unsigned *__restrict__ cnt, const int32_t *rows,
+                                                         const int32_t *n_rows, const uint64_t *__restrict__ slot,
+                                                         const double *__restrict__ pcost, int64_t *ot, int64_t *oh,
+                                                         double *oc, int64_t *f) {
+    __shared__ uint64_t sk[CSR_LONG_MAX];
+    const int tid = threadIdx.x;
+    const int nr = *n_rows;
+    unsigned dup = 0;
+    for (int ri = blockIdx.x; ri < nr; ri += gridDim.x) {
+        const int64_t r = rows[ri];
+        const int64_t s0 = ro[r];
+        const int len = (int)cnt[r];
+        int np2 = 64;
+        while (np2 < len) np2 <<= 1;
+        __syncthreads();
+        for (int i = tid; i < np2; i += CSR_LB) sk[i] = i < len ? slot[s0 + i] : ~0ull;
+        __syncthreads();
+        for (int k = 2; k <= np2; k <<= 1)
+            for (int j = k >> 1; j; j >>= 1) {
+                for (int i = tid; i < np2; i += CSR_LB) {
+                    const int p = i ^ j;
+                    if (p > i) {
+                        const uint64_t a = sk[i], b = sk[p];
+                        if ((a > b) == ((i & k) == 0)) {
+                            sk[i] = b;
+                            sk[p] = a;
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+        for (int i = tid; i < len; i += CSR_LB) {
+            const uint64_t key = sk[i];
+            if (i > 0 && (key >> 32) == (sk[i - 1] >> 32)) dup = 1;
+            sp_put(r, s0 + i, key, pcost, ot, oh, oc);
+        }
+    }
+    if (__any_sync(0xffffffffu, dup) && (tid & 31) == 0) atomicOr((unsigned long long *)&f[F_NET_ERR], SP_DUP_BIT);
+}
+
+// supplies (network.py:88-93), the diagonal arcs (i -> abar last in the A-member
+// rows; the bbar row = B-members in node order) and the free bbar -> abar arc
+__global__ void k_sp_diag(const double2 *__restrict__ pts, const int64_t *__restrict__ am,
+                          const int64_t *__restrict__ bm, int64_t K, const int64_t *__restrict__ exb,
+                          const int64_t *__restrict__ ro, int64_t abar, int64_t bbar, int64_t *sup, int64_t *ot,
+                          int64_t *oh, double *oc, int64_t *f) {
+    unsigned bad = 0;
+    const int64_t kr = (K + 31) & ~31ll;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < kr; i += (int64_t)gridDim.x * blockDim.x) {
+        if (i >= K) continue;
+        const double2 p = pts[i];
+        const double d = ddiv(fabs(dsub(p.y, p.x)), SQRT2);  // diagram.py:47
+        const int64_t a = am[i], b = bm[i];
+        sup[i] = a - b;
+        if (a > 0) {
+            const int64_t q = ro[i + 1] - 1;
+            ot[q] = i;
+            oh[q] = K;
+            oc[q] = d;
+        }
+        if (b > 0) {
+            const int64_t q = ro[K + 1] + exb[i];
+            ot[q] = K + 1;
+            oh[q] = i;
+            oc[q] = d;
+        }
+        if ((a > 0 || b > 0) && !isfinite(d)) bad = 1;
+    }
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr((unsigned long long *)&f[F_NET_ERR], 4ull);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        sup[K] = abar;
+        sup[K + 1] = bbar;
+        const int64_t q = ro[K + 2] - 1;
+        ot[q] = K + 1;
+        oh[q] = K;
+        oc[q] = 0.0;
     }
 }
 
@@ -855,6 +1121,96 @@ int net_run(Ctx &c, const int64_t *d_sup, int64_t n, int64_t *n_arcs) {
     c.net_m = mm;
     c.net_valid = true;
     *n_arcs = mm;
+    return W1G_OK;
+}
+
+// emit_arcs + assemble of the fused front end (see k_sp_count): the network
+// straight from the pairs, one host round trip for the validation flags
+int spanner_net_run(Ctx &c, int64_t *node_count, int64_t *n_arcs) {
+    c.net_valid = false;
+    NodeSet &ns = c.nodes[1];
+    const int64_t K = ns.k, P = c.n_pairs;
+    const int64_t n = K + 2;
+    auto generic = [&]() -> int {
+        int64_t M, *dsup, nsup;
+        W1G_TRY(emit_run(c, &M));
+        W1G_TRY(assemble_supplies(c, &dsup, &nsup));
+        *node_count = nsup;
+        return net_run(c, dsup, nsup, n_arcs);
+    };
+    const char *e = getenv("W1G_GENERIC_CSR");
+    if ((e && *e == '1') || ns.na < 0 || !ns.exb.p || P >= (1ll << 32) || n >= (1ll << 31) ||
+        2 * P > CSR_BUCKET_MAX_AVG * n)
+        return generic();
+    const int64_t M = 2 * P + ns.na + ns.nb + 1;
+    // W1G_SP_LONG_MAX (tests): a lower row-length limit, to exercise the fallback
+    unsigned long_max = CSR_LONG_MAX;
+    if (const char *lm = getenv("W1G_SP_LONG_MAX")) long_max = (unsigned)atoi(lm);
+    if (long_max > (unsigned)CSR_LONG_MAX) long_max = CSR_LONG_MAX;
+    SubTimer T(c, "spcsr");
+    int64_t *sup, *ro, *ot, *oh;
+    double *oc, *pcost;
+    unsigned *cnt;
+    uint64_t *slot;
+    int32_t *lists;
+    W1G_TRY(ensure(c.net_sup, (size_t)n, &sup));
+    W1G_TRY(ensure(c.net_ro, (size_t)n + 2, &ro));
+    W1G_TRY(ensure(c.net_t, (size_t)M + 1, &ot));
+    W1G_TRY(ensure(c.net_h, (size_t)M + 1, &oh));
+    W1G_TRY(ensure(c.net_c, (size_t)M + 1, &oc));
+    W1G_TRY(ensure(c.scr[13], (size_t)2 * (n + 2), &cnt));
+    unsigned *cursor = cnt + n + 2;
+    W1G_TRY(ensure(c.scr[4], (size_t)P + 1, &pcost));
+    W1G_TRY(ensure(c.scr[0], (size_t)2 * P + 1, &slot));
+    W1G_TRY(ensure(c.scr[6], (size_t)4 * (K + 1), &lists));
+    int32_t *n_list = reinterpret_cast<int32_t *>(dflags(c) + F_MISC2);  // 4 int32 counters (F_MISC2, F_MISC3)
+    W1G_TRY(flags_reset(c));
+    W1G_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned) * 2 * (n + 2), c.stream));
+    const int64_t *idx = ptr<int64_t>(c.pair_idx);
+    const double2 *pp = c.pair_pts ? c.pair_pts : ptr<double2>(ns.pts);
+    if (P) {
+        k_sp_count<<<gs(c, P), 256, 0, c.stream>>>(idx, P, pp, cnt, pcost, dflags(c));
+        W1G_CHECK_LAUNCH();
+    }
+    W1G_TRY(scan_i64(c, SpRowLen{cnt, ptr<int64_t>(ns.am), K, ns.nb}, n + 1, ro, nullptr));
+    if (P) {
+        k_sp_scatter<<<gs(c, P), 256, 0, c.stream>>>(idx, P, ro, cursor, slot);
+        W1G_CHECK_LAUNCH();
+    }
+    T.mark("bucket");
+    if (K) {
+        k_sp_short_rows<<<grid_for(K * 16, 256, 16u * c.sm_count), 256, 0, c.stream>>>(
+            ro, cnt, K, slot, pcost, ot, oh, oc, lists, n_list, dflags(c), long_max);
+        W1G_CHECK_LAUNCH();
+        k_sp_w32_rows<<<4 * c.sm_count, 256, 0, c.stream>>>(ro, cnt, lists + CL_W32 * K, n_list + CL_W32, slot,
+                                                            pcost, ot, oh, oc, dflags(c));
+        W1G_CHECK_LAUNCH();
+        k_sp_med_rows<<<8 * c.sm_count, CSR_MB, 0, c.stream>>>(ro, cnt, lists + CL_MED * K, n_list + CL_MED, slot,
+                                                               pcost, ot, oh, oc, dflags(c));
+        W1G_CHECK_LAUNCH();
+        k_sp_long_rows<<<c.sm_count, CSR_LB, 0, c.stream>>>(ro, cnt, lists + CL_LONG * K, n_list + CL_LONG, slot,
+                                                            pcost, ot, oh, oc, dflags(c));
+        W1G_CHECK_LAUNCH();
+    }
+    T.mark("rows");
+    k_sp_diag<<<grid_for(K > 0 ? K : 1, 256, 8u * c.sm_count), 256, 0, c.stream>>>(
+        ptr<double2>(ns.pts), ptr<int64_t>(ns.am), ptr<int64_t>(ns.bm), K, ptr<int64_t>(ns.exb), ro, ns.abar,
+        ns.bbar, sup, ot, oh, oc, dflags(c));
+    W1G_CHECK_LAUNCH();
+    W1G_TRY(flags_fetch(c, 0, F_NSLOTS / 2));
+    T.mark("diag");
+    const int64_t bits = c.h_pinned[F_NET_ERR];
+    if (bits & 4) {  // network.py:64-65 (balance, ranges and self-loops hold by construction)
+        set_error("non-finite arc cost");
+        return W1G_ENETWORK;
+    }
+    if ((bits & SP_DUP_BIT) || c.h_pinned[F_OVERFLOW]) return generic();
+    c.arcs_valid = false;  // never materialised on this path
+    c.net_n = n;
+    c.net_m = M;
+    c.net_valid = true;
+    *node_count = n;
+    *n_arcs = M;
     return W1G_OK;
 }
 
