@@ -523,6 +523,7 @@ int w1g_fetch_pairs(w1g_ctx *c, int64_t *node_pairs, int64_t *indices) {
         }
     }
     if (indices) {
+        W1G_TRY(wspd_pair_idx(*c));
         W1G_TRY(download(*c, indices, c->pair_idx.p, sizeof(int64_t) * 2 * P));
         W1G_TRY(stream_sync(*c));
     }
@@ -554,6 +555,7 @@ int w1g_load_pairs(w1g_ctx *c, const int64_t *indices, int64_t n_pairs, const do
     c->n_pairs = n_pairs;
     c->pairs_valid = true;
     c->pairs_have_nodes = false;
+    c->pair_idx_valid = true;
     c->arcs_valid = false;
     c->net_valid = false;
     return W1G_OK;
@@ -626,6 +628,12 @@ int w1g_assemble(w1g_ctx *c, int64_t *node_count, int64_t *n_arcs) {
 int w1g_fetch_network(w1g_ctx *c, int64_t *supplies, int64_t *tails, int64_t *heads, double *costs,
                       int64_t *row_offsets) {
     CTX_CHECK(c);
+    if (c->net_check_pending) {  // a fused front end that returned early: validate first
+        int64_t nn, mm;
+        bool redone;
+        W1G_TRY(stream_sync(*c));
+        W1G_TRY(spanner_net_check(*c, &nn, &mm, &redone));
+    }
     if (!c->net_valid) {
         set_error("no network");
         return W1G_ESTATE;
@@ -765,7 +773,7 @@ int w1g_front_end_device(w1g_ctx *c, const double *d_a, int64_t na, const double
         info->tree_depth = depth;
         if (spawn && c->overlap == 3) W1G_TRY(start_rwmd());
         int64_t P;
-        W1G_TRY(wspd_run(*c, s, 0, &P));  // its round trip also delivers the tree's depth / duplicate flag
+        W1G_TRY(wspd_run(*c, s, 0, &P, false));  // its round trip also delivers the tree's depth / duplicate flag
         W1G_TRY(tree_deferred_check(*c, &depth));
         info->tree_depth = depth;
         W1G_CUDA(cudaEventRecord(ev[5], c->stream));
@@ -816,6 +824,17 @@ int w1g_front_end_device(w1g_ctx *c, const double *d_a, int64_t na, const double
     W1G_CUDA(cudaEventRecord(ev[9], c->stream));
     host_t[9] = std::chrono::steady_clock::now();  // everything, RWMD included, is done
     W1G_CUDA(cudaEventSynchronize(ev[9]));
+    {
+        bool redone = false;
+        int64_t nsup = info->node_count, mm = info->n_arcs;
+        W1G_TRY(spanner_net_check(*c, &nsup, &mm, &redone));
+        if (redone) {  // the network was rebuilt on the generic path: copy it out again
+            info->node_count = nsup;
+            info->n_arcs = mm;
+            W1G_TRY(copy_network_out(*c, &info->network_copied));
+            W1G_TRY(stream_sync(*c));
+        }
+    }
     for (int i = 0; i < 7; i++) W1G_CUDA(cudaEventElapsedTime(&info->stage_ms[i], ev[i], ev[i + 1]));
     if (overlap) W1G_CUDA(cudaEventElapsedTime(&info->stage_ms[1], c->aux->ev[0], c->aux->ev[1]));
     W1G_CUDA(cudaEventElapsedTime(&info->stage_ms[7], ev[0], ev[9]));

@@ -124,6 +124,7 @@ struct Ctx {
     DevBuf pair_idx;   // int64 (P,2) representative point indices
     DevBuf pair_counts;
     bool pairs_have_nodes = false;
+    bool pair_idx_valid = false;  // pair_idx matches pair_uv (or was loaded)
 
     // arcs (emit_arcs output, reference order)
     bool arcs_valid = false;
@@ -132,6 +133,7 @@ struct Ctx {
 
     // network (CSR)
     bool net_valid = false;
+    bool net_check_pending = false;  // spanner_net_run's flags not yet read
     int64_t net_n = 0, net_m = 0;
     DevBuf net_sup, net_t, net_h, net_c, net_ro;
 
@@ -440,13 +442,16 @@ int tree_deferred_check(Ctx &c, int32_t *depth);
 // h_pinned slots no flags fetch touches
 enum { H_LEX_MAXRUN = F_NSLOTS - 4, H_TREE_DEPTH = F_NSLOTS - 2, H_TREE_DUP = F_NSLOTS - 1 };
 int tree_geom(Ctx &c);
-int wspd_run(Ctx &c, double s, int reference_order, int64_t *n_pairs);
+int wspd_run(Ctx &c, double s, int reference_order, int64_t *n_pairs, bool want_idx = true);
+int wspd_pair_idx(Ctx &c);  // pair_idx from pair_uv and the tree's reps, unless current
 int emit_run(Ctx &c, int64_t *n_arcs);
 int net_run(Ctx &c, const int64_t *d_supplies, int64_t n, int64_t *n_arcs);
 int assemble_supplies(Ctx &c, int64_t **d_sup, int64_t *n);
 // fused front end: emit_arcs + assemble straight from the WSPD pairs (the arc
 // list is not materialised); falls back to emit_run + net_run when needed
+// its validation flags are read by spanner_net_check once the stream has drained
 int spanner_net_run(Ctx &c, int64_t *node_count, int64_t *n_arcs);
+int spanner_net_check(Ctx &c, int64_t *node_count, int64_t *n_arcs, bool *redone);
 
 }  // namespace w1g
 

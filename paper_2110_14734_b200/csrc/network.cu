@@ -645,17 +645,19 @@ __global__ void k_csr_emit_long(const int64_t *__restrict__ start, const int64_t
 // is flagged, and the host redoes the network on the generic path.
 constexpr long long SP_DUP_BIT = 1ll << 16;  // in F_NET_ERR
 
-// arc cost per pair (spanner.py:324, both directions share it) and pair arcs per tail
-__global__ void k_sp_count(const int64_t *__restrict__ idx, int64_t P, const double2 *__restrict__ pts,
-                           unsigned *cnt, double *pcost, int64_t *f) {
+// arc cost per pair (spanner.py:324, both directions share it) and pair arcs
+// per tail; the pairs' representatives are rep[u], rep[v] (spanner.py:296)
+__global__ void k_sp_count(const int2 *__restrict__ uv, const int32_t *__restrict__ rep, int64_t P,
+                           const double2 *__restrict__ pts, unsigned *cnt, double *pcost, int64_t *f) {
     const int lane = threadIdx.x & 31;
     unsigned bad = 0;
     const int64_t pr = (P + 31) & ~31ll;
     for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < pr; p += (int64_t)gridDim.x * blockDim.x) {
-        long long i = -1, j = -1;
+        int i = -1, j = -1;
         if (p < P) {
-            i = idx[2 * p];
-            j = idx[2 * p + 1];
+            const int2 q = uv[p];
+            i = rep[q.x];
+            j = rep[q.y];
             const double2 a = pts[i], b = pts[j];
             const double cc = glibc_hypot(dsub(a.x, b.x), dsub(a.y, b.y));
             pcost[p] = cc;
@@ -681,20 +683,21 @@ struct SpRowLen {
 };
 
 // pair arcs into their tail rows as (head << 32 | pair) keys, warp-aggregated
-__global__ void k_sp_scatter(const int64_t *__restrict__ idx, int64_t P, const int64_t *__restrict__ ro,
-                             unsigned *cursor, uint64_t *slot) {
+__global__ void k_sp_scatter(const int2 *__restrict__ uv, const int32_t *__restrict__ rep, int64_t P,
+                             const int64_t *__restrict__ ro, unsigned *cursor, uint64_t *slot) {
     const int lane = threadIdx.x & 31;
     const unsigned lt = lanemask_lt();
     const int64_t pr = (P + 31) & ~31ll;
     for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < pr; p += (int64_t)gridDim.x * blockDim.x) {
-        long long e[2] = {-1, -1};
+        int e[2] = {-1, -1};
         if (p < P) {
-            e[0] = idx[2 * p];
-            e[1] = idx[2 * p + 1];
+            const int2 q = uv[p];
+            e[0] = rep[q.x];
+            e[1] = rep[q.y];
         }
 #pragma unroll
         for (int d = 0; d < 2; d++) {
-            const long long t = e[d], h = e[d ^ 1];
+            const int t = e[d], h = e[d ^ 1];
             const unsigned peers = __match_any_sync(0xffffffffu, t);
             const int leader = __ffs(peers) - 1;
             unsigned base = 0;
@@ -736,17 +739,55 @@ __device__ __forceinline__ void sp_row_reg(int64_t r, int64_t s0, int len, const
     }
 }
 
+struct DiagArgs {
+    const double2 *pts;
+    const int64_t *am, *bm, *exb;
+    int64_t abar, bbar;
+    int64_t *sup;
+};
+
+// every row: <= 16 pair arcs sorted here on half warps (longer rows queued by
+// class); lane 1 of the half warp writes the row's supply and its diagonal
+// arcs (network.py:88-93, spanner.py:326-335): i -> abar last in an A-member
+// row, bbar -> i at the member's place in the bbar row
 __global__ void k_sp_short_rows(const int64_t *__restrict__ ro, const unsigned *__restrict__ cnt, int64_t K,
                                 const uint64_t *__restrict__ slot, const double *__restrict__ pcost, int64_t *ot,
                                 int64_t *oh, double *oc, int32_t *lists, int32_t *n_list, int64_t *f,
-                                unsigned long_max) {
+                                unsigned long_max, const __grid_constant__ DiagArgs D) {
     const int lane = threadIdx.x & 31, gl = lane & 15;
     const int64_t groups = ((int64_t)gridDim.x * blockDim.x) >> 4;
     const int64_t nr = (K + 1) & ~1ll;  // both halves of a warp iterate together
-    unsigned dup = 0;
+    unsigned dup = 0, bad = 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        D.sup[K] = D.abar;
+        D.sup[K + 1] = D.bbar;
+        const int64_t q = ro[K + 2] - 1;  // the free bbar -> abar arc closes the bbar row
+        ot[q] = K + 1;
+        oh[q] = K;
+        oc[q] = 0.0;
+    }
     for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 4; r < nr; r += groups) {
         int len = 0;
         int64_t s0 = 0;
+        if (r < K && gl == 1) {
+            const double2 p = D.pts[r];
+            const int64_t a = D.am[r], b = D.bm[r];
+            const double d = ddiv(fabs(dsub(p.y, p.x)), SQRT2);  // diagram.py:47
+            D.sup[r] = a - b;
+            if (a > 0) {
+                const int64_t q = ro[r + 1] - 1;
+                ot[q] = r;
+                oh[q] = K;
+                oc[q] = d;
+            }
+            if (b > 0) {
+                const int64_t q = ro[K + 1] + D.exb[r];
+                ot[q] = K + 1;
+                oh[q] = r;
+                oc[q] = d;
+            }
+            if ((a > 0 || b > 0) && !isfinite(d)) bad = 1;
+        }
         if (r < K) {
             s0 = ro[r];
             const unsigned l = cnt[r];
@@ -766,6 +807,7 @@ __global__ void k_sp_short_rows(const int64_t *__restrict__ ro, const unsigned *
         sp_row_reg<16>(r, s0, len, slot, pcost, ot, oh, oc, dup);
     }
     if (__any_sync(0xffffffffu, dup) && lane == 0) atomicOr((unsigned long long *)&f[F_NET_ERR], SP_DUP_BIT);
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr((unsigned long long *)&f[F_NET_ERR], 4ull);
 }
 
 __global__ void k_sp_w32_rows(const int64_t *__restrict__ ro, const unsigned *__restrict__ cnt,
@@ -853,45 +895,6 @@ __global__ void __launch_bounds__(CSR_LB) k_sp_long_rows(const int64_t *__restri
     if (__any_sync(0xffffffffu, dup) && (tid & 31) == 0) atomicOr((unsigned long long *)&f[F_NET_ERR], SP_DUP_BIT);
 }
 
-// supplies (network.py:88-93), the diagonal arcs (i -> abar last in the A-member
-// rows; the bbar row = B-members in node order) and the free bbar -> abar arc
-__global__ void k_sp_diag(const double2 *__restrict__ pts, const int64_t *__restrict__ am,
-                          const int64_t *__restrict__ bm, int64_t K, const int64_t *__restrict__ exb,
-                          const int64_t *__restrict__ ro, int64_t abar, int64_t bbar, int64_t *sup, int64_t *ot,
-                          int64_t *oh, double *oc, int64_t *f) {
-    unsigned bad = 0;
-    const int64_t kr = (K + 31) & ~31ll;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < kr; i += (int64_t)gridDim.x * blockDim.x) {
-        if (i >= K) continue;
-        const double2 p = pts[i];
-        const double d = ddiv(fabs(dsub(p.y, p.x)), SQRT2);  // diagram.py:47
-        const int64_t a = am[i], b = bm[i];
-        sup[i] = a - b;
-        if (a > 0) {
-            const int64_t q = ro[i + 1] - 1;
-            ot[q] = i;
-            oh[q] = K;
-            oc[q] = d;
-        }
-        if (b > 0) {
-            const int64_t q = ro[K + 1] + exb[i];
-            ot[q] = K + 1;
-            oh[q] = i;
-            oc[q] = d;
-        }
-        if ((a > 0 || b > 0) && !isfinite(d)) bad = 1;
-    }
-    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr((unsigned long long *)&f[F_NET_ERR], 4ull);
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        sup[K] = abar;
-        sup[K + 1] = bbar;
-        const int64_t q = ro[K + 2] - 1;
-        ot[q] = K + 1;
-        oh[q] = K;
-        oc[q] = 0.0;
-    }
-}
-
 }  // namespace
 
 int emit_run(Ctx &c, int64_t *n_arcs) {
@@ -922,6 +925,7 @@ int emit_run(Ctx &c, int64_t *n_arcs) {
     W1G_TRY(ensure(c.arc_h, (size_t)M, &h));
     W1G_TRY(ensure(c.arc_c, (size_t)M, &cs));
     if (P) {
+        W1G_TRY(wspd_pair_idx(c));
         const double2 *pp = c.pair_pts ? c.pair_pts : ptr<double2>(ns.pts);
         k_emit_spanner<<<gs(c, P), 256, 0, c.stream>>>(ptr<int64_t>(c.pair_idx), P, pp, t, h, cs);
         W1G_CHECK_LAUNCH();
@@ -1125,23 +1129,27 @@ int net_run(Ctx &c, const int64_t *d_sup, int64_t n, int64_t *n_arcs) {
 }
 
 // emit_arcs + assemble of the fused front end (see k_sp_count): the network
-// straight from the pairs, one host round trip for the validation flags
+// straight from the pairs.  Its validation flags travel to the host with the
+// front end's final wait; spanner_net_check reads them (and redoes the
+// network on the generic path in the cases that need it).
+static int spanner_generic(Ctx &c, int64_t *node_count, int64_t *n_arcs) {
+    int64_t M, *dsup, nsup;
+    W1G_TRY(emit_run(c, &M));
+    W1G_TRY(assemble_supplies(c, &dsup, &nsup));
+    *node_count = nsup;
+    return net_run(c, dsup, nsup, n_arcs);
+}
+
 int spanner_net_run(Ctx &c, int64_t *node_count, int64_t *n_arcs) {
     c.net_valid = false;
+    c.net_check_pending = false;
     NodeSet &ns = c.nodes[1];
     const int64_t K = ns.k, P = c.n_pairs;
     const int64_t n = K + 2;
-    auto generic = [&]() -> int {
-        int64_t M, *dsup, nsup;
-        W1G_TRY(emit_run(c, &M));
-        W1G_TRY(assemble_supplies(c, &dsup, &nsup));
-        *node_count = nsup;
-        return net_run(c, dsup, nsup, n_arcs);
-    };
     const char *e = getenv("W1G_GENERIC_CSR");
-    if ((e && *e == '1') || ns.na < 0 || !ns.exb.p || P >= (1ll << 32) || n >= (1ll << 31) ||
-        2 * P > CSR_BUCKET_MAX_AVG * n)
-        return generic();
+    if ((e && *e == '1') || K < 1 || ns.na < 0 || !ns.exb.p || !c.pairs_have_nodes || P >= (1ll << 31) ||
+        n >= (1ll << 31) || 2 * P > CSR_BUCKET_MAX_AVG * n)
+        return spanner_generic(c, node_count, n_arcs);
     const int64_t M = 2 * P + ns.na + ns.nb + 1;
     // W1G_SP_LONG_MAX (tests): a lower row-length limit, to exercise the fallback
     unsigned long_max = CSR_LONG_MAX;
@@ -1166,51 +1174,64 @@ int spanner_net_run(Ctx &c, int64_t *node_count, int64_t *n_arcs) {
     int32_t *n_list = reinterpret_cast<int32_t *>(dflags(c) + F_MISC2);  // 4 int32 counters (F_MISC2, F_MISC3)
     W1G_TRY(flags_reset(c));
     W1G_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned) * 2 * (n + 2), c.stream));
-    const int64_t *idx = ptr<int64_t>(c.pair_idx);
+    const int2 *uv = ptr<int2>(c.pair_uv);
+    const int32_t *rep = ptr<int32_t>(c.t_rep32);
     const double2 *pp = c.pair_pts ? c.pair_pts : ptr<double2>(ns.pts);
     if (P) {
-        k_sp_count<<<gs(c, P), 256, 0, c.stream>>>(idx, P, pp, cnt, pcost, dflags(c));
+        k_sp_count<<<gs(c, P), 256, 0, c.stream>>>(uv, rep, P, pp, cnt, pcost, dflags(c));
         W1G_CHECK_LAUNCH();
     }
     W1G_TRY(scan_i64(c, SpRowLen{cnt, ptr<int64_t>(ns.am), K, ns.nb}, n + 1, ro, nullptr));
     if (P) {
-        k_sp_scatter<<<gs(c, P), 256, 0, c.stream>>>(idx, P, ro, cursor, slot);
+        k_sp_scatter<<<gs(c, P), 256, 0, c.stream>>>(uv, rep, P, ro, cursor, slot);
         W1G_CHECK_LAUNCH();
     }
     T.mark("bucket");
-    if (K) {
-        k_sp_short_rows<<<grid_for(K * 16, 256, 16u * c.sm_count), 256, 0, c.stream>>>(
-            ro, cnt, K, slot, pcost, ot, oh, oc, lists, n_list, dflags(c), long_max);
-        W1G_CHECK_LAUNCH();
-        k_sp_w32_rows<<<4 * c.sm_count, 256, 0, c.stream>>>(ro, cnt, lists + CL_W32 * K, n_list + CL_W32, slot,
-                                                            pcost, ot, oh, oc, dflags(c));
-        W1G_CHECK_LAUNCH();
-        k_sp_med_rows<<<8 * c.sm_count, CSR_MB, 0, c.stream>>>(ro, cnt, lists + CL_MED * K, n_list + CL_MED, slot,
-                                                               pcost, ot, oh, oc, dflags(c));
-        W1G_CHECK_LAUNCH();
-        k_sp_long_rows<<<c.sm_count, CSR_LB, 0, c.stream>>>(ro, cnt, lists + CL_LONG * K, n_list + CL_LONG, slot,
-                                                            pcost, ot, oh, oc, dflags(c));
-        W1G_CHECK_LAUNCH();
-    }
-    T.mark("rows");
-    k_sp_diag<<<grid_for(K > 0 ? K : 1, 256, 8u * c.sm_count), 256, 0, c.stream>>>(
-        ptr<double2>(ns.pts), ptr<int64_t>(ns.am), ptr<int64_t>(ns.bm), K, ptr<int64_t>(ns.exb), ro, ns.abar,
-        ns.bbar, sup, ot, oh, oc, dflags(c));
+    const DiagArgs D{ptr<double2>(ns.pts), ptr<int64_t>(ns.am), ptr<int64_t>(ns.bm), ptr<int64_t>(ns.exb),
+                     ns.abar, ns.bbar, sup};
+    k_sp_short_rows<<<grid_for(K * 16, 256, 16u * c.sm_count), 256, 0, c.stream>>>(
+        ro, cnt, K, slot, pcost, ot, oh, oc, lists, n_list, dflags(c), long_max, D);
     W1G_CHECK_LAUNCH();
-    W1G_TRY(flags_fetch(c, 0, F_NSLOTS / 2));
-    T.mark("diag");
-    const int64_t bits = c.h_pinned[F_NET_ERR];
-    if (bits & 4) {  // network.py:64-65 (balance, ranges and self-loops hold by construction)
-        set_error("non-finite arc cost");
-        return W1G_ENETWORK;
-    }
-    if ((bits & SP_DUP_BIT) || c.h_pinned[F_OVERFLOW]) return generic();
+    k_sp_w32_rows<<<4 * c.sm_count, 256, 0, c.stream>>>(ro, cnt, lists + CL_W32 * K, n_list + CL_W32, slot, pcost,
+                                                        ot, oh, oc, dflags(c));
+    W1G_CHECK_LAUNCH();
+    k_sp_med_rows<<<8 * c.sm_count, CSR_MB, 0, c.stream>>>(ro, cnt, lists + CL_MED * K, n_list + CL_MED, slot,
+                                                           pcost, ot, oh, oc, dflags(c));
+    W1G_CHECK_LAUNCH();
+    k_sp_long_rows<<<c.sm_count, CSR_LB, 0, c.stream>>>(ro, cnt, lists + CL_LONG * K, n_list + CL_LONG, slot,
+                                                        pcost, ot, oh, oc, dflags(c));
+    W1G_CHECK_LAUNCH();
+    T.mark("rows");
+    // the flags ride on the caller's final wait (no round trip here)
+    W1G_CUDA(cudaMemcpyAsync(c.h_pinned + F_OVERFLOW, dflags(c) + F_OVERFLOW, sizeof(int64_t) * (F_NET_ERR - F_OVERFLOW + 1),
+                             cudaMemcpyDeviceToHost, c.stream));
+    c.net_check_pending = true;
     c.arcs_valid = false;  // never materialised on this path
     c.net_n = n;
     c.net_m = M;
     c.net_valid = true;
     *node_count = n;
     *n_arcs = M;
+    return W1G_OK;
+}
+
+// after the stream has drained: network.py:64-65 (balance, ranges and
+// self-loops hold by construction), or the generic path when a row was too
+// long or a (tail, head) repeated
+int spanner_net_check(Ctx &c, int64_t *node_count, int64_t *n_arcs, bool *redone) {
+    *redone = false;
+    if (!c.net_check_pending) return W1G_OK;
+    c.net_check_pending = false;
+    const int64_t bits = c.h_pinned[F_NET_ERR];
+    if (bits & 4) {
+        c.net_valid = false;
+        set_error("non-finite arc cost");
+        return W1G_ENETWORK;
+    }
+    if ((bits & SP_DUP_BIT) || c.h_pinned[F_OVERFLOW]) {
+        *redone = true;
+        return spanner_generic(c, node_count, n_arcs);
+    }
     return W1G_OK;
 }
 

@@ -274,7 +274,23 @@ __global__ void k_uv_to_idx(const int2 *uv, const int32_t *rep, int64_t n, int64
 
 }  // namespace
 
-int wspd_run(Ctx &c, double s, int reference_order, int64_t *n_pairs) {
+// WSPairList.indices = rep[node_pairs] (spanner.py:296); the fused front end
+// reads the representatives itself and leaves this to a later fetch
+int wspd_pair_idx(Ctx &c) {
+    if (c.pair_idx_valid) return W1G_OK;
+    const int64_t P = c.n_pairs;
+    int64_t *idx;
+    W1G_TRY(ensure(c.pair_idx, (size_t)(2 * P + 2), &idx));
+    if (P) {
+        k_uv_to_idx<<<grid_for(P, 256, 8u * c.sm_count), 256, 0, c.stream>>>(ptr<int2>(c.pair_uv),
+                                                                             ptr<int32_t>(c.t_rep32), P, idx);
+        W1G_CHECK_LAUNCH();
+    }
+    c.pair_idx_valid = true;
+    return W1G_OK;
+}
+
+int wspd_run(Ctx &c, double s, int reference_order, int64_t *n_pairs, bool want_idx) {
     c.pairs_valid = false;
     const int64_t nn = c.tree_n_nodes, K = c.tree_n_points;
     *n_pairs = 0;
@@ -435,15 +451,10 @@ int wspd_run(Ctx &c, double s, int reference_order, int64_t *n_pairs) {
                                                                                        excl, nn, out);
             W1G_CHECK_LAUNCH();
         }
-        int64_t *idx;
-        W1G_TRY(ensure(c.pair_idx, (size_t)(2 * P + 2), &idx));
-        if (P) {
-            k_uv_to_idx<<<grid_for(P, 256, 8u * c.sm_count), 256, 0, c.stream>>>(uv, ptr<int32_t>(c.t_rep32), P, idx);
-            W1G_CHECK_LAUNCH();
-        }
         c.pairs_valid = true;
         c.pairs_have_nodes = true;
-        return W1G_OK;
+        c.pair_idx_valid = false;
+        return want_idx ? wspd_pair_idx(c) : W1G_OK;
     }
     set_error("WSPD buffers kept overflowing");
     return W1G_ENOMEM;
