@@ -420,14 +420,8 @@ __device__ void dedup_sorted(const uint64_t *sk, int len, int part, int nparts, 
 // one warp sorts 32*E keys (head << 32 | arc) held E per lane in registers
 // (element i = lane * E + q): bitonic stages with partner distance >= E are
 // shuffles, shorter ones swaps inside the lane; the sorted row goes to sk
-template <int E, class Load>
-__device__ __forceinline__ void warp_sort_keys(uint64_t *sk, int len, int lane, Load load) {
-    uint64_t v[E];
-#pragma unroll
-    for (int q = 0; q < E; q++) {
-        const int i = lane * E + q;
-        v[q] = i < len ? load(i) : ~0ull;
-    }
+template <int E>
+__device__ __forceinline__ void warp_bitonic(uint64_t (&v)[E], int lane) {
 #pragma unroll
     for (int k = 2; k <= 32 * E; k <<= 1)
 #pragma unroll
@@ -454,6 +448,16 @@ __device__ __forceinline__ void warp_sort_keys(uint64_t *sk, int len, int lane, 
                 }
             }
         }
+}
+template <int E, class Load>
+__device__ __forceinline__ void warp_sort_keys(uint64_t *sk, int len, int lane, Load load) {
+    uint64_t v[E];
+#pragma unroll
+    for (int q = 0; q < E; q++) {
+        const int i = lane * E + q;
+        v[q] = i < len ? load(i) : ~0ull;
+    }
+    warp_bitonic<E>(v, lane);
 #pragma unroll
     for (int q = 0; q < E; q++) sk[lane * E + q] = v[q];
 }
@@ -644,13 +648,24 @@ __global__ void k_csr_emit_long(const int64_t *__restrict__ start, const int64_t
 // A repeated head (impossible for a WSPD) or a row longer than CSR_LONG_MAX
 // is flagged, and the host redoes the network on the generic path.
 constexpr long long SP_DUP_BIT = 1ll << 16;  // in F_NET_ERR
+constexpr int SP_MED_MAX = 512;              // longest row a warp sorts in registers
+constexpr int SP_CL_BIG = CL_HUGE;           // list of rows of 257..SP_MED_MAX (no huge class here)
 
-// arc cost per pair (spanner.py:324, both directions share it) and pair arcs
-// per tail; the pairs' representatives are rep[u], rep[v] (spanner.py:296)
-__global__ void k_sp_count(const int2 *__restrict__ uv, const int32_t *__restrict__ rep, int64_t P,
-                           const double2 *__restrict__ pts, unsigned *cnt, double *pcost, int64_t *f) {
+// the bucketed pair arcs: per CSR slot the head and the cost; rows are sorted
+// by (head << 32 | position in the row), the position then fetches the cost
+struct SpRows {
+    const int64_t *ro;     // row offsets (final CSR positions)
+    const unsigned *cnt;   // pair arcs per row
+    const uint32_t *sh;    // slot heads
+    const double *sc;      // slot costs
+    int64_t *ot, *oh;
+    double *oc;
+    int64_t *f;
+};
+
+// pair arcs per tail; the pairs' representatives are rep[u], rep[v] (spanner.py:296)
+__global__ void k_sp_count(const int2 *__restrict__ uv, const int32_t *__restrict__ rep, int64_t P, unsigned *cnt) {
     const int lane = threadIdx.x & 31;
-    unsigned bad = 0;
     const int64_t pr = (P + 31) & ~31ll;
     for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < pr; p += (int64_t)gridDim.x * blockDim.x) {
         int i = -1, j = -1;
@@ -658,17 +673,12 @@ __global__ void k_sp_count(const int2 *__restrict__ uv, const int32_t *__restric
             const int2 q = uv[p];
             i = rep[q.x];
             j = rep[q.y];
-            const double2 a = pts[i], b = pts[j];
-            const double cc = glibc_hypot(dsub(a.x, b.x), dsub(a.y, b.y));
-            pcost[p] = cc;
-            if (!isfinite(cc)) bad = 1;
         }
         unsigned peers = __match_any_sync(0xffffffffu, i);
         if (i >= 0 && (__ffs(peers) - 1) == lane) atomicAdd(&cnt[i], (unsigned)__popc(peers));
         peers = __match_any_sync(0xffffffffu, j);
         if (j >= 0 && (__ffs(peers) - 1) == lane) atomicAdd(&cnt[j], (unsigned)__popc(peers));
     }
-    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr((unsigned long long *)&f[F_NET_ERR], 4ull);
 }
 
 // row lengths: pair arcs (+ abar for A-members) | abar: none | bbar: B-members + abar
@@ -682,11 +692,14 @@ struct SpRowLen {
     }
 };
 
-// pair arcs into their tail rows as (head << 32 | pair) keys, warp-aggregated
+// both arcs of every pair into their tail rows (warp-aggregated slots) with
+// the pair's cost, np.hypot of the representatives (spanner.py:322-325)
 __global__ void k_sp_scatter(const int2 *__restrict__ uv, const int32_t *__restrict__ rep, int64_t P,
-                             const int64_t *__restrict__ ro, unsigned *cursor, uint64_t *slot) {
+                             const double2 *__restrict__ pts, const int64_t *__restrict__ ro, unsigned *cursor,
+                             uint32_t *sh, double *sc, int64_t *f) {
     const int lane = threadIdx.x & 31;
     const unsigned lt = lanemask_lt();
+    unsigned bad = 0;
     const int64_t pr = (P + 31) & ~31ll;
     for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < pr; p += (int64_t)gridDim.x * blockDim.x) {
         int e[2] = {-1, -1};
@@ -695,34 +708,44 @@ __global__ void k_sp_scatter(const int2 *__restrict__ uv, const int32_t *__restr
             e[0] = rep[q.x];
             e[1] = rep[q.y];
         }
+        // the slot atomics first; the cost's point loads overlap them
+        int64_t slot[2];
 #pragma unroll
         for (int d = 0; d < 2; d++) {
-            const int t = e[d], h = e[d ^ 1];
+            const int t = e[d];
             const unsigned peers = __match_any_sync(0xffffffffu, t);
             const int leader = __ffs(peers) - 1;
             unsigned base = 0;
             if (t >= 0 && lane == leader) base = atomicAdd(&cursor[t], (unsigned)__popc(peers));
             base = __shfl_sync(0xffffffffu, base, leader);
-            if (t >= 0) slot[ro[t] + base + __popc(peers & lt)] = ((uint64_t)h << 32) | (uint64_t)p;
+            slot[d] = t >= 0 ? ro[t] + base + __popc(peers & lt) : 0;
+        }
+        if (p < P) {
+            const double2 a = pts[e[0]], b = pts[e[1]];
+            const double cc = glibc_hypot(dsub(a.x, b.x), dsub(a.y, b.y));
+            if (!isfinite(cc)) bad = 1;
+            sh[slot[0]] = (uint32_t)e[1];
+            sc[slot[0]] = cc;
+            sh[slot[1]] = (uint32_t)e[0];
+            sc[slot[1]] = cc;
         }
     }
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr((unsigned long long *)&f[F_NET_ERR], 4ull);
 }
 
-__device__ __forceinline__ void sp_put(int64_t r, int64_t q, uint64_t key, const double *__restrict__ pcost,
-                                       int64_t *ot, int64_t *oh, double *oc) {
-    ot[q] = r;
-    oh[q] = (int64_t)(key >> 32);
-    oc[q] = pcost[(uint32_t)key];
+// sorted element i of row r: key = head << 32 | original position in the row
+__device__ __forceinline__ void sp_put(const SpRows &R, int64_t r, int64_t s0, int64_t i, uint64_t key) {
+    R.ot[s0 + i] = r;
+    R.oh[s0 + i] = (int64_t)(key >> 32);
+    R.oc[s0 + i] = R.sc[s0 + (uint32_t)key];
 }
 
 // rows of <= W pair arcs on W-lane groups: bitonic sort of the keys in
 // registers, written straight to the CSR
 template <int W>
-__device__ __forceinline__ void sp_row_reg(int64_t r, int64_t s0, int len, const uint64_t *__restrict__ slot,
-                                           const double *__restrict__ pcost, int64_t *ot, int64_t *oh, double *oc,
-                                           unsigned &dup) {
+__device__ __forceinline__ void sp_row_reg(const SpRows &R, int64_t r, int64_t s0, int len, unsigned &dup) {
     const int lane = threadIdx.x & 31, gl = lane & (W - 1);
-    uint64_t key = gl < len ? slot[s0 + gl] : ~0ull;
+    uint64_t key = gl < len ? (((uint64_t)R.sh[s0 + gl] << 32) | (uint32_t)gl) : ~0ull;
 #pragma unroll
     for (int k = 2; k <= W; k <<= 1)
 #pragma unroll
@@ -735,7 +758,7 @@ __device__ __forceinline__ void sp_row_reg(int64_t r, int64_t s0, int len, const
     const uint32_t prev = __shfl_up_sync(0xffffffffu, head, 1);
     if (gl < len) {
         if (gl > 0 && prev == head) dup = 1;
-        sp_put(r, s0 + gl, key, pcost, ot, oh, oc);
+        sp_put(R, r, s0, gl, key);
     }
 }
 
@@ -750,10 +773,8 @@ struct DiagArgs {
 // class); lane 1 of the half warp writes the row's supply and its diagonal
 // arcs (network.py:88-93, spanner.py:326-335): i -> abar last in an A-member
 // row, bbar -> i at the member's place in the bbar row
-__global__ void k_sp_short_rows(const int64_t *__restrict__ ro, const unsigned *__restrict__ cnt, int64_t K,
-                                const uint64_t *__restrict__ slot, const double *__restrict__ pcost, int64_t *ot,
-                                int64_t *oh, double *oc, int32_t *lists, int32_t *n_list, int64_t *f,
-                                unsigned long_max, const __grid_constant__ DiagArgs D) {
+__global__ void k_sp_short_rows(const __grid_constant__ SpRows R, int64_t K, int32_t *lists, int32_t *n_list,
+                                unsigned long_max, unsigned big_max, const __grid_constant__ DiagArgs D) {
     const int lane = threadIdx.x & 31, gl = lane & 15;
     const int64_t groups = ((int64_t)gridDim.x * blockDim.x) >> 4;
     const int64_t nr = (K + 1) & ~1ll;  // both halves of a warp iterate together
@@ -761,10 +782,10 @@ __global__ void k_sp_short_rows(const int64_t *__restrict__ ro, const unsigned *
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         D.sup[K] = D.abar;
         D.sup[K + 1] = D.bbar;
-        const int64_t q = ro[K + 2] - 1;  // the free bbar -> abar arc closes the bbar row
-        ot[q] = K + 1;
-        oh[q] = K;
-        oc[q] = 0.0;
+        const int64_t q = R.ro[K + 2] - 1;  // the free bbar -> abar arc closes the bbar row
+        R.ot[q] = K + 1;
+        R.oh[q] = K;
+        R.oc[q] = 0.0;
     }
     for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 4; r < nr; r += groups) {
         int len = 0;
@@ -775,28 +796,28 @@ __global__ void k_sp_short_rows(const int64_t *__restrict__ ro, const unsigned *
             const double d = ddiv(fabs(dsub(p.y, p.x)), SQRT2);  // diagram.py:47
             D.sup[r] = a - b;
             if (a > 0) {
-                const int64_t q = ro[r + 1] - 1;
-                ot[q] = r;
-                oh[q] = K;
-                oc[q] = d;
+                const int64_t q = R.ro[r + 1] - 1;
+                R.ot[q] = r;
+                R.oh[q] = K;
+                R.oc[q] = d;
             }
             if (b > 0) {
-                const int64_t q = ro[K + 1] + D.exb[r];
-                ot[q] = K + 1;
-                oh[q] = r;
-                oc[q] = d;
+                const int64_t q = R.ro[K + 1] + D.exb[r];
+                R.ot[q] = K + 1;
+                R.oh[q] = r;
+                R.oc[q] = d;
             }
             if ((a > 0 || b > 0) && !isfinite(d)) bad = 1;
         }
         if (r < K) {
-            s0 = ro[r];
-            const unsigned l = cnt[r];
+            s0 = R.ro[r];
+            const unsigned l = R.cnt[r];
             if (l > 16) {
                 if (gl == 0) {
                     if (l > long_max) {
-                        atomicOr((unsigned long long *)&f[F_OVERFLOW], 1ull);
+                        atomicOr((unsigned long long *)&R.f[F_OVERFLOW], 1ull);
                     } else {
-                        const int cl = l <= 32 ? CL_W32 : l <= CSR_MED_MAX ? CL_MED : CL_LONG;
+                        const int cl = l <= 32 ? CL_W32 : l <= 256 ? CL_MED : l <= big_max ? SP_CL_BIG : CL_LONG;
                         lists[(int64_t)cl * K + atomicAdd(&n_list[cl], 1)] = (int32_t)r;
                     }
                 }
@@ -804,73 +825,149 @@ __global__ void k_sp_short_rows(const int64_t *__restrict__ ro, const unsigned *
                 len = (int)l;
             }
         }
-        sp_row_reg<16>(r, s0, len, slot, pcost, ot, oh, oc, dup);
+        sp_row_reg<16>(R, r, s0, len, dup);
     }
-    if (__any_sync(0xffffffffu, dup) && lane == 0) atomicOr((unsigned long long *)&f[F_NET_ERR], SP_DUP_BIT);
-    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr((unsigned long long *)&f[F_NET_ERR], 4ull);
+    if (__any_sync(0xffffffffu, dup) && lane == 0) atomicOr((unsigned long long *)&R.f[F_NET_ERR], SP_DUP_BIT);
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr((unsigned long long *)&R.f[F_NET_ERR], 4ull);
 }
 
-__global__ void k_sp_w32_rows(const int64_t *__restrict__ ro, const unsigned *__restrict__ cnt,
-                              const int32_t *rows, const int32_t *n_rows, const uint64_t *__restrict__ slot,
-                              const double *__restrict__ pcost, int64_t *ot, int64_t *oh, double *oc, int64_t *f) {
+__global__ void k_sp_w32_rows(const __grid_constant__ SpRows R, const int32_t *rows, const int32_t *n_rows) {
     const int nr = *n_rows;
     unsigned dup = 0;
     for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < nr; i += (gridDim.x * blockDim.x) >> 5) {
         const int64_t r = rows[i];
-        sp_row_reg<32>(r, ro[r], (int)cnt[r], slot, pcost, ot, oh, oc, dup);
+        sp_row_reg<32>(R, r, R.ro[r], (int)R.cnt[r], dup);
     }
     if (__any_sync(0xffffffffu, dup) && (threadIdx.x & 31) == 0)
-        atomicOr((unsigned long long *)&f[F_NET_ERR], SP_DUP_BIT);
+        atomicOr((unsigned long long *)&R.f[F_NET_ERR], SP_DUP_BIT);
 }
 
-// rows of 33..CSR_MED_MAX pair arcs: a warp each, sorted in registers
-__global__ void __launch_bounds__(CSR_MB) k_sp_med_rows(const int64_t *__restrict__ ro,
-                                                        const unsigned *__restrict__ cnt, const int32_t *rows,
-                                                        const int32_t *n_rows, const uint64_t *__restrict__ slot,
-                                                        const double *__restrict__ pcost, int64_t *ot, int64_t *oh,
-                                                        double *oc, int64_t *f) {
-    __shared__ uint64_t sk_all[CSR_MB / 32][CSR_MED_MAX];
+// rows of 33..SP_MED_MAX pair arcs: a warp each; keys staged through shared
+// memory (coalesced loads and stores), 32*E of them sorted in registers
+template <int E>
+__device__ __forceinline__ void sp_warp_row(const SpRows &R, int64_t r, int64_t s0, int len, uint64_t *sk,
+                                            unsigned &dup, int lane) {
+    for (int i = lane; i < 32 * E; i += 32) sk[i] = i < len ? (((uint64_t)R.sh[s0 + i] << 32) | (uint32_t)i) : ~0ull;
+    __syncwarp();
+    uint64_t v[E];
+#pragma unroll
+    for (int q = 0; q < E; q++) v[q] = sk[lane * E + q];
+    warp_bitonic<E>(v, lane);
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < E; q++) sk[lane * E + q] = v[q];
+    __syncwarp();
+    for (int i = lane; i < len; i += 32) {
+        const uint64_t key = sk[i];
+        if (i > 0 && (key >> 32) == (sk[i - 1] >> 32)) dup = 1;
+        sp_put(R, r, s0, i, key);
+    }
+    __syncwarp();
+}
+
+// BIG: rows of 257..SP_MED_MAX (more registers: a kernel of their own so the
+// common classes keep their occupancy)
+template <bool BIG>
+__global__ void __launch_bounds__(CSR_MB) k_sp_med_rows(const __grid_constant__ SpRows R, const int32_t *rows,
+                                                        const int32_t *n_rows) {
+    constexpr int SK = BIG ? SP_MED_MAX : 256;
+    __shared__ uint64_t sk_all[CSR_MB / 32][SK];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     uint64_t *sk = sk_all[wid];
     const int nr = *n_rows;
     unsigned dup = 0;
     for (int ri = blockIdx.x * (CSR_MB / 32) + wid; ri < nr; ri += gridDim.x * (CSR_MB / 32)) {
         const int64_t r = rows[ri];
-        const int64_t s0 = ro[r];
-        const int len = (int)cnt[r];
-        auto load = [&](int i) { return slot[s0 + i]; };
-        __syncwarp();
-        if (len <= 64) warp_sort_keys<2>(sk, len, lane, load);
-        else if (len <= 128) warp_sort_keys<4>(sk, len, lane, load);
-        else warp_sort_keys<8>(sk, len, lane, load);
-        __syncwarp();
-        for (int i = lane; i < len; i += 32) {
-            const uint64_t key = sk[i];
-            if (i > 0 && (key >> 32) == (sk[i - 1] >> 32)) dup = 1;
-            sp_put(r, s0 + i, key, pcost, ot, oh, oc);
+        const int64_t s0 = R.ro[r];
+        const int len = (int)R.cnt[r];
+        if (BIG) {
+            sp_warp_row<SP_MED_MAX / 32>(R, r, s0, len, sk, dup, lane);
+        } else {
+            if (len <= 64) sp_warp_row<2>(R, r, s0, len, sk, dup, lane);
+            else if (len <= 128) sp_warp_row<4>(R, r, s0, len, sk, dup, lane);
+            else sp_warp_row<8>(R, r, s0, len, sk, dup, lane);
         }
     }
-    if (__any_sync(0xffffffffu, dup) && lane == 0) atomicOr((unsigned long long *)&f[F_NET_ERR], SP_DUP_BIT);
+    if (__any_sync(0xffffffffu, dup) && lane == 0) atomicOr((unsigned long long *)&R.f[F_NET_ERR], SP_DUP_BIT);
 }
 
-// rows of CSR_MED_MAX+1..CSR_LONG_MAX pair arcs: a CTA each, bitonic sort in shared memory
-__global__ void __launch_bounds__(CSR_LB) k_sp_long_rows(const int64_t *__restrict__ ro,
-                                                         const unsigned *__restrict__ cnt, const int32_t *rows,
-                                                         const int32_t *n_rows, const uint64_t *__restrict__ slot,
-                                                         const double *__restrict__ pcost, int64_t *ot, int64_t *oh,
-                                                         double *oc, int64_t *f) {
+// long rows by rank instead of comparison: heads are distinct within a row
+// and below K, so a row's heads mark a K-bit bitmap in shared memory; a block
+// scan of the per-word popcounts then gives every head its rank (its place in
+// the sorted row) directly.  O(len + K/32) per row, a CTA per row.  A head
+// already marked is a repeated (tail, head).
+constexpr int SP_BM_THREADS = 512;
+__global__ void __launch_bounds__(SP_BM_THREADS) k_sp_long_bitmap(const __grid_constant__ SpRows R,
+                                                                  const int32_t *rows, const int32_t *n_rows,
+                                                                  int64_t K) {
+    extern __shared__ uint32_t sbm[];  // W bitmap words, then W exclusive popcount prefixes
+    const int W = (int)((K + 31) >> 5);
+    uint32_t *pre = sbm + W;
+    __shared__ uint32_t s_warp[SP_BM_THREADS / 32];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int per = (W + SP_BM_THREADS - 1) / SP_BM_THREADS;  // words per thread in the scan
+    for (int i = tid; i < W; i += SP_BM_THREADS) sbm[i] = 0;
+    const int nr = *n_rows;
+    unsigned dup = 0;
+    for (int ri = blockIdx.x; ri < nr; ri += gridDim.x) {
+        const int64_t r = rows[ri];
+        const int64_t s0 = R.ro[r];
+        const int len = (int)R.cnt[r];
+        __syncthreads();  // bitmap clear (previous row)
+        for (int i = tid; i < len; i += SP_BM_THREADS) {
+            const uint32_t h = R.sh[s0 + i];
+            const uint32_t bit = 1u << (h & 31);
+            if (atomicOr(&sbm[h >> 5], bit) & bit) dup = 1;
+        }
+        __syncthreads();
+        // exclusive prefix of the word popcounts: a contiguous run of words per thread
+        const int w0 = tid * per, w1 = min(W, w0 + per);
+        uint32_t mine = 0;
+        for (int w = w0; w < w1; w++) mine += __popc(sbm[w]);
+        uint32_t x = mine;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) s_warp[wid] = x;
+        __syncthreads();
+        uint32_t base = x - mine;
+        for (int w = 0; w < wid; w++) base += s_warp[w];
+        for (int w = w0; w < w1; w++) {
+            pre[w] = base;
+            base += __popc(sbm[w]);
+        }
+        __syncthreads();
+        for (int i = tid; i < len; i += SP_BM_THREADS) {
+            const uint32_t h = R.sh[s0 + i];
+            const uint32_t rank = pre[h >> 5] + __popc(sbm[h >> 5] & ((1u << (h & 31)) - 1u));
+            R.ot[s0 + rank] = r;
+            R.oh[s0 + rank] = h;
+            R.oc[s0 + rank] = R.sc[s0 + i];
+        }
+        __syncthreads();
+        for (int i = tid; i < len; i += SP_BM_THREADS) sbm[R.sh[s0 + i] >> 5] = 0;
+    }
+    if (__any_sync(0xffffffffu, dup) && lane == 0) atomicOr((unsigned long long *)&R.f[F_NET_ERR], SP_DUP_BIT);
+}
+
+// long rows when the bitmap does not fit (K above ~800k): a CTA each,
+// bitonic sort in shared memory
+__global__ void __launch_bounds__(CSR_LB) k_sp_long_rows(const __grid_constant__ SpRows R, const int32_t *rows,
+                                                         const int32_t *n_rows) {
     __shared__ uint64_t sk[CSR_LONG_MAX];
     const int tid = threadIdx.x;
     const int nr = *n_rows;
     unsigned dup = 0;
     for (int ri = blockIdx.x; ri < nr; ri += gridDim.x) {
         const int64_t r = rows[ri];
-        const int64_t s0 = ro[r];
-        const int len = (int)cnt[r];
+        const int64_t s0 = R.ro[r];
+        const int len = (int)R.cnt[r];
         int np2 = 64;
         while (np2 < len) np2 <<= 1;
         __syncthreads();
-        for (int i = tid; i < np2; i += CSR_LB) sk[i] = i < len ? slot[s0 + i] : ~0ull;
+        for (int i = tid; i < np2; i += CSR_LB) sk[i] = i < len ? (((uint64_t)R.sh[s0 + i] << 32) | (uint32_t)i) : ~0ull;
         __syncthreads();
         for (int k = 2; k <= np2; k <<= 1)
             for (int j = k >> 1; j; j >>= 1) {
@@ -889,10 +986,10 @@ __global__ void __launch_bounds__(CSR_LB) k_sp_long_rows(const int64_t *__restri
         for (int i = tid; i < len; i += CSR_LB) {
             const uint64_t key = sk[i];
             if (i > 0 && (key >> 32) == (sk[i - 1] >> 32)) dup = 1;
-            sp_put(r, s0 + i, key, pcost, ot, oh, oc);
+            sp_put(R, r, s0, i, key);
         }
     }
-    if (__any_sync(0xffffffffu, dup) && (tid & 31) == 0) atomicOr((unsigned long long *)&f[F_NET_ERR], SP_DUP_BIT);
+    if (__any_sync(0xffffffffu, dup) && (tid & 31) == 0) atomicOr((unsigned long long *)&R.f[F_NET_ERR], SP_DUP_BIT);
 }
 
 }  // namespace
@@ -1148,18 +1245,22 @@ int spanner_net_run(Ctx &c, int64_t *node_count, int64_t *n_arcs) {
     const int64_t n = K + 2;
     const char *e = getenv("W1G_GENERIC_CSR");
     if ((e && *e == '1') || K < 1 || ns.na < 0 || !ns.exb.p || !c.pairs_have_nodes || P >= (1ll << 31) ||
-        n >= (1ll << 31) || 2 * P > CSR_BUCKET_MAX_AVG * n)
+        n >= (1ll << 31))
         return spanner_generic(c, node_count, n_arcs);
     const int64_t M = 2 * P + ns.na + ns.nb + 1;
     // W1G_SP_LONG_MAX (tests): a lower row-length limit, to exercise the fallback
     unsigned long_max = CSR_LONG_MAX;
     if (const char *lm = getenv("W1G_SP_LONG_MAX")) long_max = (unsigned)atoi(lm);
     if (long_max > (unsigned)CSR_LONG_MAX) long_max = CSR_LONG_MAX;
+    // rows of 257..big_max: a warp in registers, longer: the bitmap ranks (W1G_SP_BIG_MAX: tuning)
+    unsigned big_max = SP_MED_MAX;
+    if (const char *bm = getenv("W1G_SP_BIG_MAX")) big_max = (unsigned)atoi(bm);
+    if (big_max > (unsigned)SP_MED_MAX) big_max = SP_MED_MAX;
     SubTimer T(c, "spcsr");
     int64_t *sup, *ro, *ot, *oh;
-    double *oc, *pcost;
+    double *oc, *sc;
     unsigned *cnt;
-    uint64_t *slot;
+    uint32_t *sh;
     int32_t *lists;
     W1G_TRY(ensure(c.net_sup, (size_t)n, &sup));
     W1G_TRY(ensure(c.net_ro, (size_t)n + 2, &ro));
@@ -1168,8 +1269,9 @@ int spanner_net_run(Ctx &c, int64_t *node_count, int64_t *n_arcs) {
     W1G_TRY(ensure(c.net_c, (size_t)M + 1, &oc));
     W1G_TRY(ensure(c.scr[13], (size_t)2 * (n + 2), &cnt));
     unsigned *cursor = cnt + n + 2;
-    W1G_TRY(ensure(c.scr[4], (size_t)P + 1, &pcost));
-    W1G_TRY(ensure(c.scr[0], (size_t)2 * P + 1, &slot));
+    // slots sit at their final CSR positions (the diagonal ones stay unused)
+    W1G_TRY(ensure(c.scr[0], (size_t)M + 1, &sh));
+    W1G_TRY(ensure(c.scr[4], (size_t)M + 1, &sc));
     W1G_TRY(ensure(c.scr[6], (size_t)4 * (K + 1), &lists));
     int32_t *n_list = reinterpret_cast<int32_t *>(dflags(c) + F_MISC2);  // 4 int32 counters (F_MISC2, F_MISC3)
     W1G_TRY(flags_reset(c));
@@ -1178,30 +1280,44 @@ int spanner_net_run(Ctx &c, int64_t *node_count, int64_t *n_arcs) {
     const int32_t *rep = ptr<int32_t>(c.t_rep32);
     const double2 *pp = c.pair_pts ? c.pair_pts : ptr<double2>(ns.pts);
     if (P) {
-        k_sp_count<<<gs(c, P), 256, 0, c.stream>>>(uv, rep, P, pp, cnt, pcost, dflags(c));
+        k_sp_count<<<gs(c, P), 256, 0, c.stream>>>(uv, rep, P, cnt);
         W1G_CHECK_LAUNCH();
     }
     W1G_TRY(scan_i64(c, SpRowLen{cnt, ptr<int64_t>(ns.am), K, ns.nb}, n + 1, ro, nullptr));
     if (P) {
-        k_sp_scatter<<<gs(c, P), 256, 0, c.stream>>>(uv, rep, P, ro, cursor, slot);
+        k_sp_scatter<<<gs(c, P), 256, 0, c.stream>>>(uv, rep, P, pp, ro, cursor, sh, sc, dflags(c));
         W1G_CHECK_LAUNCH();
     }
     T.mark("bucket");
+    const SpRows R{ro, cnt, sh, sc, ot, oh, oc, dflags(c)};
     const DiagArgs D{ptr<double2>(ns.pts), ptr<int64_t>(ns.am), ptr<int64_t>(ns.bm), ptr<int64_t>(ns.exb),
                      ns.abar, ns.bbar, sup};
-    k_sp_short_rows<<<grid_for(K * 16, 256, 16u * c.sm_count), 256, 0, c.stream>>>(
-        ro, cnt, K, slot, pcost, ot, oh, oc, lists, n_list, dflags(c), long_max, D);
+    k_sp_short_rows<<<grid_for(K * 16, 256, 16u * c.sm_count), 256, 0, c.stream>>>(R, K, lists, n_list, long_max,
+                                                                                   big_max, D);
     W1G_CHECK_LAUNCH();
-    k_sp_w32_rows<<<4 * c.sm_count, 256, 0, c.stream>>>(ro, cnt, lists + CL_W32 * K, n_list + CL_W32, slot, pcost,
-                                                        ot, oh, oc, dflags(c));
+    k_sp_w32_rows<<<4 * c.sm_count, 256, 0, c.stream>>>(R, lists + CL_W32 * K, n_list + CL_W32);
     W1G_CHECK_LAUNCH();
-    k_sp_med_rows<<<8 * c.sm_count, CSR_MB, 0, c.stream>>>(ro, cnt, lists + CL_MED * K, n_list + CL_MED, slot,
-                                                           pcost, ot, oh, oc, dflags(c));
+    k_sp_med_rows<false><<<8 * c.sm_count, CSR_MB, 0, c.stream>>>(R, lists + CL_MED * K, n_list + CL_MED);
     W1G_CHECK_LAUNCH();
-    k_sp_long_rows<<<c.sm_count, CSR_LB, 0, c.stream>>>(ro, cnt, lists + CL_LONG * K, n_list + CL_LONG, slot,
-                                                        pcost, ot, oh, oc, dflags(c));
+    T.mark("short_med");
+    k_sp_med_rows<true><<<4 * c.sm_count, CSR_MB, 0, c.stream>>>(R, lists + SP_CL_BIG * K, n_list + SP_CL_BIG);
     W1G_CHECK_LAUNCH();
-    T.mark("rows");
+    T.mark("big");
+    {
+        // long rows: bitmap ranks while a K-bit bitmap (+ prefixes) fits in shared memory
+        const size_t bm_bytes = (size_t)8 * ((K + 31) / 32);
+        if (bm_bytes <= 200 * 1024) {
+            if (bm_bytes > 48 * 1024)
+                W1G_CUDA(cudaFuncSetAttribute(k_sp_long_bitmap, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)bm_bytes));
+            k_sp_long_bitmap<<<c.sm_count, SP_BM_THREADS, bm_bytes, c.stream>>>(R, lists + CL_LONG * K,
+                                                                                 n_list + CL_LONG, K);
+        } else {
+            k_sp_long_rows<<<c.sm_count, CSR_LB, 0, c.stream>>>(R, lists + CL_LONG * K, n_list + CL_LONG);
+        }
+        W1G_CHECK_LAUNCH();
+    }
+    T.mark("long");
     // the flags ride on the caller's final wait (no round trip here)
     W1G_CUDA(cudaMemcpyAsync(c.h_pinned + F_OVERFLOW, dflags(c) + F_OVERFLOW, sizeof(int64_t) * (F_NET_ERR - F_OVERFLOW + 1),
                              cudaMemcpyDeviceToHost, c.stream));
