@@ -26,7 +26,7 @@ constexpr int RS_WARPS = RS_BLOCK / 32;
 // large inputs so the decoupled look-back chain stays short
 constexpr int RS_IPT_SMALL = 4;
 constexpr int RS_IPT_LARGE = 32;
-constexpr int64_t RS_LARGE_N = 1 << 20;
+constexpr int64_t RS_LARGE_N = 1 << 19;  // measured: 1M-key Morton sorts -37 us, 342k-key tree sorts unchanged
 
 struct KeyPtrs {
     uint64_t *k[4];
@@ -374,7 +374,11 @@ int radix_sort_multi(Ctx &c, const SortJob *jobs, int njobs, int words, int top_
     const int ndig = (words - 1) * 8 + (top_bits + 7) / 8;
     int launch = 0;
     bool large = false;
-    for (int j = 0; j < nj; j++) large |= J[j]->n >= RS_LARGE_N;
+    static const int64_t large_n = [] {  // W1G_RS_LARGE_N: tuning override
+        const char *e = getenv("W1G_RS_LARGE_N");
+        return e ? (int64_t)atoll(e) : RS_LARGE_N;
+    }();
+    for (int j = 0; j < nj; j++) large |= J[j]->n >= large_n;
     for (int dg = 0; dg < ndig; dg++) {
         PassArgs A;
         A.njobs = nj;
