@@ -215,6 +215,7 @@ int w1g_ctx_create(int device, w1g_ctx **out) {
     if (const char *e = getenv("W1G_DEBUG_RADIUS")) c->debug_radius = atoi(e) ? 1 : 0;
     if (const char *e = getenv("W1G_HEAVY")) c->heavy_ratio = atoi(e) > 0 ? atoi(e) : 0;
     if (const char *e = getenv("W1G_OVERLAP")) c->overlap = atoi(e) > 0 ? atoi(e) : 0;
+    if (const char *e = getenv("W1G_OVERLAP_E2E")) c->overlap_e2e = atoi(e) > 0 ? atoi(e) : 0;
     {
         // contexts launch at the highest stream priority; the auxiliary RWMD
         // context drops to the lowest (start_rwmd), so when both have work the
@@ -717,7 +718,10 @@ int w1g_front_end_device(w1g_ctx *c, const double *d_a, int64_t na, const double
     // pipeline.py:115, so RWMD runs on the auxiliary context concurrently with
     // the back end (from the point W1G_OVERLAP selects), which speculates L > 0 (redone with delta = 0 in
     // the rare case L == 0).
-    const bool overlap = c->overlap && use_condensation && delta_mode != 0 && delta > 0.0;
+    // with an armed output target the network's D2H copy ends the call: RWMD
+    // then starts later and runs under the CSR and the copy (overlap_e2e)
+    const int ov = c->net_out.sup ? c->overlap_e2e : c->overlap;
+    const bool overlap = ov && use_condensation && delta_mode != 0 && delta > 0.0;
     double L = 0.0, LA = 0.0, LB = 0.0;
     if (!overlap) W1G_TRY(rwmd_run(*c, &L, &LA, &LB));
     W1G_CUDA(cudaEventRecord(ev[2], c->stream));
@@ -755,7 +759,7 @@ int w1g_front_end_device(w1g_ctx *c, const double *d_a, int64_t na, const double
     };
     auto back_end = [&](double d, bool spawn) -> int {
         info->delta = d;
-        if (spawn && c->overlap == 2) W1G_TRY(start_rwmd());
+        if (spawn && ov == 2) W1G_TRY(start_rwmd());
         int64_t kk;
         const double pitch = k * d;
         const double half_width = (1.0 - k) * d / 2.0;
@@ -763,7 +767,7 @@ int w1g_front_end_device(w1g_ctx *c, const double *d_a, int64_t na, const double
         W1G_CUDA(cudaEventRecord(ev[3], c->stream));
     host_t[3] = std::chrono::steady_clock::now();
         info->n_points = kk;
-        if (spawn && c->overlap == 4) W1G_TRY(start_rwmd());
+        if (spawn && ov == 4) W1G_TRY(start_rwmd());
         int64_t nn;
         int32_t depth;
         W1G_TRY(tree_run(*c, ptr<double2>(c->nodes[1].pts), kk, &nn, &depth, true));
@@ -771,7 +775,7 @@ int w1g_front_end_device(w1g_ctx *c, const double *d_a, int64_t na, const double
     host_t[4] = std::chrono::steady_clock::now();
         info->n_tree_nodes = nn;
         info->tree_depth = depth;
-        if (spawn && c->overlap == 3) W1G_TRY(start_rwmd());
+        if (spawn && ov == 3) W1G_TRY(start_rwmd());
         int64_t P;
         W1G_TRY(wspd_run(*c, s, 0, &P, false));  // its round trip also delivers the tree's depth / duplicate flag
         W1G_TRY(tree_deferred_check(*c, &depth));
@@ -780,13 +784,14 @@ int w1g_front_end_device(w1g_ctx *c, const double *d_a, int64_t na, const double
     host_t[5] = std::chrono::steady_clock::now();
         info->n_pairs = P;
         info->n_levels_wspd = c->wspd_levels;
-        if (spawn && c->overlap == 1) W1G_TRY(start_rwmd());
+        if (spawn && ov == 1) W1G_TRY(start_rwmd());
         // emit_arcs is fused into the CSR assembly (the arc list is never
         // materialised), so stage 5 (emit) is empty on this path
         W1G_CUDA(cudaEventRecord(ev[6], c->stream));
         host_t[6] = std::chrono::steady_clock::now();
         int64_t nsup, mm;
         W1G_TRY(spanner_net_run(*c, &nsup, &mm));
+        if (spawn && ov == 5) W1G_TRY(start_rwmd());
         W1G_CUDA(cudaEventRecord(ev[7], c->stream));
     host_t[7] = std::chrono::steady_clock::now();
         info->n_arcs = mm;

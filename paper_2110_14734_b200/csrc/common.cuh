@@ -157,6 +157,11 @@ struct Ctx {
     // the WSPD, 2 right after zero_condense, 0 = sequential (measured at cfg2:
     // 4 -> 1.44 ms, 3 -> 1.55, 1 -> 1.66, 2 -> 1.60, 0 -> 1.74)
     int overlap = 4;
+    // when the network is copied out inside the call (an armed w1g_set_network_out
+    // target) RWMD starts after the WSPD and runs under the CSR and the copy
+    // (W1G_OVERLAP_E2E; measured e2e: 1 -> 5.48 ms at 1M / 2.24 at cfg2, 4 -> 6.87 / 2.32,
+    // 3 -> 7.01 / 2.29, 5 (after the CSR) -> 7.28 / 2.65)
+    int overlap_e2e = 1;
     Ctx *aux = nullptr;
 
     // one-shot host target for the next fused front end's network (w1g_set_network_out)
