@@ -2,6 +2,8 @@
 // context, buffer, flag and error plumbing shared by the stage translation
 // units.  Each entry point cites the reference function it replaces.
 #include <chrono>
+#include <condition_variable>
+#include <mutex>
 #include <cstdarg>
 #include <cstring>
 #include <string>
@@ -216,6 +218,8 @@ int w1g_ctx_create(int device, w1g_ctx **out) {
     if (const char *e = getenv("W1G_HEAVY")) c->heavy_ratio = atoi(e) > 0 ? atoi(e) : 0;
     if (const char *e = getenv("W1G_OVERLAP")) c->overlap = atoi(e) > 0 ? atoi(e) : 0;
     if (const char *e = getenv("W1G_OVERLAP_E2E")) c->overlap_e2e = atoi(e) > 0 ? atoi(e) : 0;
+    if (const char *e = getenv("W1G_SPLIT_GATE")) c->split_gate = atoi(e) > 0 ? atoi(e) : 0;
+    if (const char *e = getenv("W1G_SPLIT_GATE_E2E")) c->split_gate_e2e = atoi(e) > 0 ? atoi(e) : 0;
     {
         // contexts launch at the highest stream priority; the auxiliary RWMD
         // context drops to the lowest (start_rwmd), so when both have work the
@@ -699,37 +703,40 @@ int w1g_front_end_device(w1g_ctx *c, const double *d_a, int64_t na, const double
     c->sync_gap_us = 0.0;
     W1G_CUDA(cudaEventRecord(ev[0], c->stream));
     host_t[0] = std::chrono::steady_clock::now();
-    int64_t k0;
-    int32_t balanced;
-    W1G_TRY(w1g_zero_condense_device(c, d_a, na, d_b, nb, &k0, &balanced));
-    W1G_CUDA(cudaEventRecord(ev[1], c->stream));
-    host_t[1] = std::chrono::steady_clock::now();
-    info->n_points0 = k0;
-    if (k0 == 0 || balanced) {
-        // pipeline.py:106-109: empty inputs or identical multisets -> 0.0
-        info->short_circuit = 1;
-        W1G_TRY(stream_sync(*c));
-        return W1G_OK;
-    }
     // pipeline.py:67-69, condensation.py:47-59 (same IEEE operation order as the Python)
     const double eps_c = s >= 12 ? 8.0 / (s - 4.0) : 1.0;
-    info->epsilon_condense = eps_c;
     // With a fixed delta, L only feeds the diagnostics and the `L > 0` test of
     // pipeline.py:115, so RWMD runs on the auxiliary context concurrently with
-    // the back end (from the point W1G_OVERLAP selects), which speculates L > 0 (redone with delta = 0 in
-    // the rare case L == 0).
-    // with an armed output target the network's D2H copy ends the call: RWMD
-    // then starts later and runs under the CSR and the copy (overlap_e2e)
+    // the back end (from the point W1G_OVERLAP selects), which speculates L > 0
+    // (redone with delta = 0 in the rare case L == 0).  With an armed output
+    // target the network's D2H copy ends the call: RWMD then starts later and
+    // runs under the CSR and the copy (overlap_e2e).
     const int ov = c->net_out.sup ? c->overlap_e2e : c->overlap;
     const bool overlap = ov && use_condensation && delta_mode != 0 && delta > 0.0;
+    // split (W1G_SPLIT, default on): zero_condense and RWMD both go to the
+    // auxiliary context, and the back end condenses the RAW diagrams (the same
+    // cells and summed masses as condensing zero_condense's output), so the main
+    // stream starts delta_condense at once
+    static const bool split_env = [] {
+        const char *e = getenv("W1G_SPLIT");
+        return !(e && *e == '0');
+    }();
+    const bool split = overlap && split_env && na + nb > 0;
+    // in split mode RWMD follows zero_condense on the auxiliary stream at once, or
+    // (gate) only once the main stream has reached the point `gate` names (the
+    // spawn points below); with an armed output target it waits for the WSPD so
+    // it runs under the CSR and the network's D2H copy
+    const int gate = split ? (c->net_out.sup ? c->split_gate_e2e : c->split_gate) : 0;
+    std::mutex gate_mu;
+    std::condition_variable gate_cv;
+    bool gate_open = gate == 0;
+    int64_t k0 = 0;
+    int32_t balanced = 0;
     double L = 0.0, LA = 0.0, LB = 0.0;
-    if (!overlap) W1G_TRY(rwmd_run(*c, &L, &LA, &LB));
-    W1G_CUDA(cudaEventRecord(ev[2], c->stream));
-    host_t[2] = std::chrono::steady_clock::now();
     std::thread worker;
     int rc_aux = W1G_OK;
     std::string err_aux;
-    auto start_rwmd = [&]() -> int {
+    auto ensure_aux = [&]() -> int {
         if (!c->aux) {
             w1g_ctx *x = nullptr;
             W1G_TRY(w1g_ctx_create(c->device, &x));
@@ -744,6 +751,54 @@ int w1g_front_end_device(w1g_ctx *c, const double *d_a, int64_t na, const double
         x->culling = c->culling;
         x->cull_steps = c->cull_steps;
         x->heavy_ratio = c->heavy_ratio;
+        return W1G_OK;
+    };
+    if (split) {
+        W1G_TRY(ensure_aux());
+        Ctx *x = c->aux;
+        W1G_CUDA(cudaEventRecord(c->ev[8], c->stream));  // the inputs are on the device
+        W1G_CUDA(cudaStreamWaitEvent(x->stream, c->ev[8], 0));
+        const double2 *pa = reinterpret_cast<const double2 *>(d_a), *pb = reinterpret_cast<const double2 *>(d_b);
+        worker = std::thread([&, x, pa, pb]() {
+            cudaSetDevice(x->device);
+            set_thread_stream(x->stream);
+            cudaEventRecord(x->ev[2], x->stream);
+            invalidate_from_nodes(*x);
+            rc_aux = zc_run(*x, pa, na, pb, nb, &k0, &balanced);
+            cudaEventRecord(x->ev[3], x->stream);
+            if (rc_aux == W1G_OK && gate) {
+                std::unique_lock<std::mutex> lk(gate_mu);
+                gate_cv.wait(lk, [&] { return gate_open; });
+                cudaStreamWaitEvent(x->stream, c->ev[11], 0);  // recorded before the gate opened
+            }
+            cudaEventRecord(x->ev[0], x->stream);
+            if (rc_aux == W1G_OK && k0 > 0 && !balanced) rc_aux = rwmd_run(*x, &L, &LA, &LB);
+            if (rc_aux == W1G_OK) rc_aux = cudaEventRecord(x->ev[1], x->stream) == cudaSuccess ? W1G_OK : W1G_ECUDA;
+            if (rc_aux != W1G_OK) err_aux = g_err;
+        });
+        W1G_TRY(raw_nodes(*c, pa, na, pb, nb));
+        W1G_CUDA(cudaEventRecord(ev[1], c->stream));
+        W1G_CUDA(cudaEventRecord(ev[2], c->stream));
+        host_t[1] = host_t[2] = std::chrono::steady_clock::now();
+    } else {
+        W1G_TRY(w1g_zero_condense_device(c, d_a, na, d_b, nb, &k0, &balanced));
+        W1G_CUDA(cudaEventRecord(ev[1], c->stream));
+        host_t[1] = std::chrono::steady_clock::now();
+        info->n_points0 = k0;
+        if (k0 == 0 || balanced) {
+            // pipeline.py:106-109: empty inputs or identical multisets -> 0.0
+            info->short_circuit = 1;
+            W1G_TRY(stream_sync(*c));
+            return W1G_OK;
+        }
+        if (!overlap) W1G_TRY(rwmd_run(*c, &L, &LA, &LB));
+        W1G_CUDA(cudaEventRecord(ev[2], c->stream));
+        host_t[2] = std::chrono::steady_clock::now();
+    }
+    info->epsilon_condense = eps_c;
+    auto start_rwmd = [&]() -> int {
+        W1G_TRY(ensure_aux());
+        Ctx *x = c->aux;
         x->nodes[0] = c->nodes[0];  // alias (read only; nothing downstream rewrites nodes0)
         W1G_CUDA(cudaEventRecord(c->ev[8], c->stream));  // nodes0 complete on the main stream
         W1G_CUDA(cudaStreamWaitEvent(x->stream, c->ev[8], 0));
@@ -757,17 +812,33 @@ int w1g_front_end_device(w1g_ctx *c, const double *d_a, int64_t na, const double
         });
         return W1G_OK;
     };
+    NodeSet *dc_src = split ? &c->raw : nullptr;
+    auto open_gate = [&]() -> int {
+        W1G_CUDA(cudaEventRecord(c->ev[11], c->stream));
+        {
+            std::lock_guard<std::mutex> lk(gate_mu);
+            gate_open = true;
+        }
+        gate_cv.notify_all();
+        return W1G_OK;
+    };
+    // a spawn point: start RWMD (overlap) or open the split gate
+    auto spawn_at = [&](bool spawn, int point) -> int {
+        if (spawn && ov == point) W1G_TRY(start_rwmd());
+        if (split && gate == point && !gate_open) W1G_TRY(open_gate());
+        return W1G_OK;
+    };
     auto back_end = [&](double d, bool spawn) -> int {
         info->delta = d;
-        if (spawn && ov == 2) W1G_TRY(start_rwmd());
+        W1G_TRY(spawn_at(spawn, 2));
         int64_t kk;
         const double pitch = k * d;
         const double half_width = (1.0 - k) * d / 2.0;
-        W1G_TRY(dc_run(*c, d > 0.0 ? d : 0.0, pitch, half_width, seed, &kk));
+        W1G_TRY(dc_run(*c, d > 0.0 ? d : 0.0, pitch, half_width, seed, &kk, dc_src));
         W1G_CUDA(cudaEventRecord(ev[3], c->stream));
     host_t[3] = std::chrono::steady_clock::now();
         info->n_points = kk;
-        if (spawn && ov == 4) W1G_TRY(start_rwmd());
+        W1G_TRY(spawn_at(spawn, 4));
         int64_t nn;
         int32_t depth;
         W1G_TRY(tree_run(*c, ptr<double2>(c->nodes[1].pts), kk, &nn, &depth, true));
@@ -775,7 +846,7 @@ int w1g_front_end_device(w1g_ctx *c, const double *d_a, int64_t na, const double
     host_t[4] = std::chrono::steady_clock::now();
         info->n_tree_nodes = nn;
         info->tree_depth = depth;
-        if (spawn && ov == 3) W1G_TRY(start_rwmd());
+        W1G_TRY(spawn_at(spawn, 3));
         int64_t P;
         W1G_TRY(wspd_run(*c, s, 0, &P, false));  // its round trip also delivers the tree's depth / duplicate flag
         W1G_TRY(tree_deferred_check(*c, &depth));
@@ -784,14 +855,14 @@ int w1g_front_end_device(w1g_ctx *c, const double *d_a, int64_t na, const double
     host_t[5] = std::chrono::steady_clock::now();
         info->n_pairs = P;
         info->n_levels_wspd = c->wspd_levels;
-        if (spawn && ov == 1) W1G_TRY(start_rwmd());
+        W1G_TRY(spawn_at(spawn, 1));
         // emit_arcs is fused into the CSR assembly (the arc list is never
         // materialised), so stage 5 (emit) is empty on this path
         W1G_CUDA(cudaEventRecord(ev[6], c->stream));
         host_t[6] = std::chrono::steady_clock::now();
         int64_t nsup, mm;
         W1G_TRY(spanner_net_run(*c, &nsup, &mm));
-        if (spawn && ov == 5) W1G_TRY(start_rwmd());
+        W1G_TRY(spawn_at(spawn, 5));
         W1G_CUDA(cudaEventRecord(ev[7], c->stream));
     host_t[7] = std::chrono::steady_clock::now();
         info->n_arcs = mm;
@@ -806,23 +877,52 @@ int w1g_front_end_device(w1g_ctx *c, const double *d_a, int64_t na, const double
         }
         return delta;
     };
-    int rc = back_end(overlap ? delta : delta_for(L), overlap);
+    int rc = back_end(overlap ? delta : delta_for(L), overlap && !split);
     // the network leaves for the host while RWMD may still run on the auxiliary stream
     if (rc == W1G_OK) rc = copy_network_out(*c, &info->network_copied);
+    if (split && !gate_open) {  // the back end stopped early: let the worker finish
+        const int rg = open_gate();
+        if (rc == W1G_OK) rc = rg;
+    }
     if (worker.joinable()) worker.join();
-    if (overlap && c->aux) c->aux->nodes[0] = NodeSet{};
+    if (overlap && !split && c->aux) c->aux->nodes[0] = NodeSet{};
+    if (split) {
+        if (rc_aux != W1G_OK) {
+            set_error("%s", err_aux.c_str());
+            return rc_aux;
+        }
+        // nodes0 (zero_condense's output) becomes the main context's, as on the sequential path
+        W1G_CUDA(cudaStreamWaitEvent(c->stream, c->aux->ev[1], 0));
+        std::swap(c->nodes[0], c->aux->nodes[0]);
+        info->n_points0 = k0;
+        if (k0 == 0 || balanced) {
+            // pipeline.py:106-109: identical multisets -> 0.0 (the speculative back end is dropped,
+            // whatever it returned: the reference never gets there)
+            invalidate_from_nodes(*c);
+            c->nodes[1].valid = false;
+            c->net_check_pending = false;
+            info->short_circuit = 1;
+            info->network_copied = 0;
+            info->delta = 0.0;
+            info->n_points = info->n_tree_nodes = info->n_pairs = info->n_arcs = info->node_count = 0;
+            info->tree_depth = info->n_levels_wspd = 0;
+            W1G_TRY(stream_sync(*c));
+            return W1G_OK;
+        }
+        dc_src = nullptr;  // any redo below condenses nodes0 itself
+    }
+    if (overlap && !(L > 0.0) && rc_aux == W1G_OK) {
+        // pipeline.py:115: no condensation when L == 0 (whatever the speculative back end returned)
+        W1G_CUDA(cudaStreamWaitEvent(c->stream, c->aux->ev[1], 0));
+        W1G_TRY(back_end(0.0, false));
+        rc = copy_network_out(*c, &info->network_copied);
+    }
     if (rc != W1G_OK) return rc;
     if (rc_aux != W1G_OK) {
         set_error("%s", err_aux.c_str());
         return rc_aux;
     }
-    if (overlap) {
-        W1G_CUDA(cudaStreamWaitEvent(c->stream, c->aux->ev[1], 0));
-        if (!(L > 0.0)) {  // pipeline.py:115: no condensation when L == 0
-            W1G_TRY(back_end(0.0, false));
-            W1G_TRY(copy_network_out(*c, &info->network_copied));
-        }
-    }
+    if (overlap) W1G_CUDA(cudaStreamWaitEvent(c->stream, c->aux->ev[1], 0));
     info->lower_bound = L;
     info->lower_bound_a = LA;
     info->lower_bound_b = LB;
@@ -842,6 +942,7 @@ int w1g_front_end_device(w1g_ctx *c, const double *d_a, int64_t na, const double
     }
     for (int i = 0; i < 7; i++) W1G_CUDA(cudaEventElapsedTime(&info->stage_ms[i], ev[i], ev[i + 1]));
     if (overlap) W1G_CUDA(cudaEventElapsedTime(&info->stage_ms[1], c->aux->ev[0], c->aux->ev[1]));
+    if (split) W1G_CUDA(cudaEventElapsedTime(&info->stage_ms[0], c->aux->ev[2], c->aux->ev[3]));
     W1G_CUDA(cudaEventElapsedTime(&info->stage_ms[7], ev[0], ev[9]));
     if (c->timing)
     {

@@ -90,6 +90,7 @@ struct Ctx {
 
     DevBuf in_pts;  // (na+nb) double2
     NodeSet nodes[2];
+    NodeSet raw;    // the raw inputs as nodes (split fixed-delta front end)
 
     // rwmd
     int culling = 1;
@@ -162,6 +163,9 @@ struct Ctx {
     // (W1G_OVERLAP_E2E; measured e2e: 1 -> 5.48 ms at 1M / 2.24 at cfg2, 4 -> 6.87 / 2.32,
     // 3 -> 7.01 / 2.29, 5 (after the CSR) -> 7.28 / 2.65)
     int overlap_e2e = 1;
+    // split front end: the main-stream point RWMD waits for (0 = none, else a
+    // spawn point as above), without / with an armed output target
+    int split_gate = 0, split_gate_e2e = 1;
     Ctx *aux = nullptr;
 
     // one-shot host target for the next fused front end's network (w1g_set_network_out)
@@ -438,7 +442,12 @@ int zc_run(Ctx &c, const double2 *d_a, int64_t na, const double2 *d_b, int64_t n
 int rwmd_run(Ctx &c, double *L, double *LA, double *LB);
 int rwmd_tile_profile(Ctx &c, int reps, float *ms, int64_t *evals);
 int rwmd_range_run(Ctx &c, int side, int64_t begin, int64_t end, double *partial, int64_t *n_members);
-int dc_run(Ctx &c, double delta, double pitch, double half_width, uint64_t seed, int64_t *k);
+// src: the node set to condense (default nodes[0]); the result goes to nodes[1]
+int dc_run(Ctx &c, double delta, double pitch, double half_width, uint64_t seed, int64_t *k,
+           NodeSet *src = nullptr);
+// the raw diagrams as a node set (unit masses, duplicates kept) into c.raw:
+// delta_condense of it equals delta_condense of zero_condense's output
+int raw_nodes(Ctx &c, const double2 *d_a, int64_t na, const double2 *d_b, int64_t nb);
 // defer = true (fused front end): no host round trip of its own -- the depth and the
 // duplicate flag land in h_pinned[H_TREE_DEPTH / H_TREE_DUP] at the caller's next
 // synchronisation, and the caller checks the flag (tree_deferred_check)

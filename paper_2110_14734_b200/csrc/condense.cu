@@ -243,8 +243,45 @@ static int member_scans(Ctx &c, NodeSet &ns, int64_t k) {
     return W1G_OK;
 }
 
-int dc_run(Ctx &c, double delta, double pitch, double half_width, uint64_t seed, int64_t *kout) {
-    NodeSet &src = c.nodes[0], &dst = c.nodes[1];
+namespace {
+__global__ void k_raw_nodes(const double2 *a, int64_t na, const double2 *b, int64_t n, double2 *pts, int64_t *am,
+                            int64_t *bm) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const bool in_a = i < na;
+        pts[i] = in_a ? a[i] : b[i - na];
+        am[i] = in_a ? 1 : 0;
+        bm[i] = in_a ? 0 : 1;
+    }
+}
+}  // namespace
+
+// condensation.py:105-124 only sees the node SET with its summed masses:
+// every duplicate point lands in the same cell, so delta_condense of the raw
+// diagrams (unit masses) equals delta_condense of zero_condense's output --
+// same cells, same order, same offsets, same integer mass sums
+int raw_nodes(Ctx &c, const double2 *d_a, int64_t na, const double2 *d_b, int64_t nb) {
+    NodeSet &r = c.raw;
+    const int64_t n = na + nb;
+    double2 *pts;
+    int64_t *am, *bm;
+    W1G_TRY(ensure(r.pts, (size_t)n + 1, &pts));
+    W1G_TRY(ensure(r.am, (size_t)n + 1, &am));
+    W1G_TRY(ensure(r.bm, (size_t)n + 1, &bm));
+    if (n) {
+        k_raw_nodes<<<gs(c, n), 256, 0, c.stream>>>(d_a, na, d_b, n, pts, am, bm);
+        W1G_CHECK_LAUNCH();
+    }
+    r.k = n;
+    r.abar = -na;
+    r.bbar = nb;
+    r.valid = true;
+    r.na = r.nb = -1;
+    return W1G_OK;
+}
+
+int dc_run(Ctx &c, double delta, double pitch, double half_width, uint64_t seed, int64_t *kout,
+           NodeSet *src_override) {
+    NodeSet &src = src_override ? *src_override : c.nodes[0], &dst = c.nodes[1];
     const int64_t k = src.k;
     dst.abar = src.abar;
     dst.bbar = src.bbar;
