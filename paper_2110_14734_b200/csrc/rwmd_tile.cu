@@ -46,13 +46,6 @@ __device__ __forceinline__ float min3(float a, float b, float c) {
     return d;
 }
 
-// error bound of an estimate m (scaled units^2) for a source at local radius qn
-__device__ __forceinline__ float upper_bound(float m, float qn) {
-    const float d = sqrtf(fmaxf(m, 0.f));
-    const float e = 2.f * qn + d + 0x1p-20f;
-    return sqrtf(fmaxf(m, 0.f) + 0x1p-20f * e * e) * (1.f + 0x1p-20f) + 0x1p-22f;
-}
-
 struct TileArgs {
     const double2 *q;       // sources (Morton order), original coordinates
     const double2 *t;       // targets (Morton order)

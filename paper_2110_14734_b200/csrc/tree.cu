@@ -575,24 +575,6 @@ __device__ __forceinline__ int64_t scatter_dest(int64_t p, int f, int64_t excl_p
     return f ? in.lo + rt : in.lo + in.nl + rf;
 }
 
-__device__ __forceinline__ void pos_scatter(int64_t p, int s, int f, int64_t excl_p, int64_t excl_lo,
-                                            const SegInfo &in, const uint32_t *__restrict__ xl,
-                                            const uint32_t *__restrict__ yl, uint32_t *xl_new,
-                                            uint32_t *yl_new, int32_t *pos_seg_new) {
-    const int64_t rt = excl_p - excl_lo;
-    const int64_t rf = (p - in.lo) - rt;
-    const int64_t np_ = f ? in.lo + rt : in.lo + in.nl + rf;
-    if (in.axis) {  // split on y: Y-list stays, X-list is partitioned
-        yl_new[p] = yl[p];
-        xl_new[np_] = xl[p];
-    } else {
-        xl_new[p] = xl[p];
-        yl_new[np_] = yl[p];
-    }
-    pos_seg_new[p] = (p < in.lo + in.nl) ? in.cl : in.cr;
-    (void)s;
-}
-
 struct FlagVal {
     const int32_t *fl;
     __device__ int64_t operator()(int64_t i) const { return fl[i]; }
