@@ -367,6 +367,17 @@ def run_ours(args, dist: Dist):
                            "pairs_per_s": 1.0 / t_w1, "solver": "reference w1flow.simplex (host, 1 thread)"}
     if dist.rank == 0:
         n = dist.world
+        hs = hbm_stages(2 * args.n, int(info.n_points0), int(info.n_points), int(info.n_pairs), int(info.n_arcs),
+                        stage_avg)
+        if hs:
+            # the timed step's longest byte-moving stage against HBM (the RWMD tile above is
+            # the north star's named kernel; this says where the step's own time goes)
+            nm, st = max(hs.items(), key=lambda kv: kv[1]["ms"])
+            roofline["step_longest_stage"] = {
+                "stage": nm, "bound": "hbm", "achieved": st["gbs"], "peak": HBM_PEAK_GBS, "unit": "GB/s",
+                "frac": st["frac"], "ms": st["ms"], "algorithmic_bytes": st["bytes"],
+                "note": "latency-bound: dependent grid-wide phases (levels, sorts, round trips), "
+                        "not bandwidth; see DESIGN.md section 4"}
         line = {
             "metric": METRIC,
             "value": n / (dev_ms_max * 1e-3),
@@ -392,8 +403,7 @@ def run_ours(args, dist: Dist):
             "roofline": roofline,
             "hbm_stages": {"peak_gbs": HBM_PEAK_GBS, "note": "algorithmic bytes / stage device time; "
                            "latency-bound at this size (few-microsecond dependent phases), see DESIGN.md",
-                           "stages": hbm_stages(2 * args.n, int(info.n_points0), int(info.n_points),
-                                                int(info.n_pairs), int(info.n_arcs), stage_avg)},
+                           "stages": hs},
             "gpu_launches": int(launches),
             "clocks": clk,
         }
