@@ -227,6 +227,8 @@ int w1g_ctx_create(int device, w1g_ctx **out) {
         int least = 0, greatest = 0;
         W1G_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
         W1G_CUDA(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, greatest));
+        // the early part of the network's D2H copy (tails, row offsets) runs on its own stream
+        W1G_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
     }
     {
         // freed pool memory stays cached for the next growth (stream-ordered buffers)
@@ -291,6 +293,7 @@ int w1g_ctx_destroy(w1g_ctx *c) {
     for (auto &e : c->sync_ev)
         if (e) cudaEventDestroy(e);
     cudaStreamDestroy(c->stream);
+    if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     delete c;
     return W1G_OK;
 }
@@ -660,17 +663,23 @@ int w1g_set_network_out(w1g_ctx *c, int64_t *supplies, int64_t *tails, int64_t *
     return W1G_OK;
 }
 
-// the network into the armed output target (asynchronously, on the context stream)
+// the network into the armed output target (asynchronously, on the context
+// stream); the tails and row offsets may already be on their way (spanner_net_run
+// starts them on the copy stream as soon as the row offsets are known)
 static int copy_network_out(Ctx &c, int *copied) {
     *copied = 0;
     const Ctx::NetOut &o = c.net_out;
     if (!c.net_valid || !o.sup || c.net_n > o.node_cap || c.net_m > o.arc_cap) return W1G_OK;
     const size_t n = (size_t)c.net_n, m = (size_t)c.net_m;
     W1G_TRY(download(c, o.sup, c.net_sup.p, sizeof(int64_t) * n));
-    W1G_TRY(download(c, o.t, c.net_t.p, sizeof(int64_t) * m));
     W1G_TRY(download(c, o.h, c.net_h.p, sizeof(int64_t) * m));
     W1G_TRY(download(c, o.c, c.net_c.p, sizeof(double) * m));
-    W1G_TRY(download(c, o.ro, c.net_ro.p, sizeof(int64_t) * (n + 1)));
+    if (c.net_early_copy) {
+        W1G_CUDA(cudaStreamWaitEvent(c.stream, c.ev[13], 0));  // the early copies are part of this one
+    } else {
+        W1G_TRY(download(c, o.t, c.net_t.p, sizeof(int64_t) * m));
+        W1G_TRY(download(c, o.ro, c.net_ro.p, sizeof(int64_t) * (n + 1)));
+    }
     *copied = 1;
     return W1G_OK;
 }

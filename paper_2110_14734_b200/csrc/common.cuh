@@ -86,6 +86,7 @@ enum { SCR_N = 24 };
 struct Ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
+    cudaStream_t copy_stream = nullptr;  // early D2H of the fused network (tails, row offsets)
     int sm_count = 148;
 
     DevBuf in_pts;  // (na+nb) double2
@@ -135,6 +136,7 @@ struct Ctx {
     // network (CSR)
     bool net_valid = false;
     bool net_check_pending = false;  // spanner_net_run's flags not yet read
+    bool net_early_copy = false;     // tails + row offsets already copied out (copy_stream, ev[13])
     int64_t net_n = 0, net_m = 0;
     DevBuf net_sup, net_t, net_h, net_c, net_ro;
 

@@ -733,9 +733,24 @@ __global__ void k_sp_scatter(const int2 *__restrict__ uv, const int32_t *__restr
     if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr((unsigned long long *)&f[F_NET_ERR], 4ull);
 }
 
+// the tails column of the CSR: a function of the row offsets alone (a warp per
+// row, the long bbar row by the whole grid), written before the rows are
+// sorted so its D2H copy can start early
+__global__ void k_sp_tails(const int64_t *__restrict__ ro, int64_t K, int64_t *ot) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r <= K; r += warps) {
+        const int64_t b = ro[r], e = ro[r + 1];
+        for (int64_t q = b + lane; q < e; q += 32) ot[q] = r;
+    }
+    const int64_t b = ro[K + 1], e = ro[K + 2];
+    for (int64_t q = b + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < e; q += (int64_t)gridDim.x * blockDim.x)
+        ot[q] = K + 1;
+}
+
 // sorted element i of row r: key = head << 32 | original position in the row
 __device__ __forceinline__ void sp_put(const SpRows &R, int64_t r, int64_t s0, int64_t i, uint64_t key) {
-    R.ot[s0 + i] = r;
+    (void)r;  // the tails are written by k_sp_tails
     R.oh[s0 + i] = (int64_t)(key >> 32);
     R.oc[s0 + i] = R.sc[s0 + (uint32_t)key];
 }
@@ -783,7 +798,6 @@ __global__ void k_sp_short_rows(const __grid_constant__ SpRows R, int64_t K, int
         D.sup[K] = D.abar;
         D.sup[K + 1] = D.bbar;
         const int64_t q = R.ro[K + 2] - 1;  // the free bbar -> abar arc closes the bbar row
-        R.ot[q] = K + 1;
         R.oh[q] = K;
         R.oc[q] = 0.0;
     }
@@ -797,13 +811,11 @@ __global__ void k_sp_short_rows(const __grid_constant__ SpRows R, int64_t K, int
             D.sup[r] = a - b;
             if (a > 0) {
                 const int64_t q = R.ro[r + 1] - 1;
-                R.ot[q] = r;
                 R.oh[q] = K;
                 R.oc[q] = d;
             }
             if (b > 0) {
                 const int64_t q = R.ro[K + 1] + D.exb[r];
-                R.ot[q] = K + 1;
                 R.oh[q] = r;
                 R.oc[q] = d;
             }
@@ -942,7 +954,6 @@ __global__ void __launch_bounds__(SP_BM_THREADS) k_sp_long_bitmap(const __grid_c
         for (int i = tid; i < len; i += SP_BM_THREADS) {
             const uint32_t h = R.sh[s0 + i];
             const uint32_t rank = pre[h >> 5] + __popc(sbm[h >> 5] & ((1u << (h & 31)) - 1u));
-            R.ot[s0 + rank] = r;
             R.oh[s0 + rank] = h;
             R.oc[s0 + rank] = R.sc[s0 + i];
         }
@@ -1230,6 +1241,7 @@ int net_run(Ctx &c, const int64_t *d_sup, int64_t n, int64_t *n_arcs) {
 // front end's final wait; spanner_net_check reads them (and redoes the
 // network on the generic path in the cases that need it).
 static int spanner_generic(Ctx &c, int64_t *node_count, int64_t *n_arcs) {
+    c.net_early_copy = false;
     int64_t M, *dsup, nsup;
     W1G_TRY(emit_run(c, &M));
     W1G_TRY(assemble_supplies(c, &dsup, &nsup));
@@ -1287,6 +1299,25 @@ int spanner_net_run(Ctx &c, int64_t *node_count, int64_t *n_arcs) {
     if (P) {
         k_sp_scatter<<<gs(c, P), 256, 0, c.stream>>>(uv, rep, P, pp, ro, cursor, sh, sc, dflags(c));
         W1G_CHECK_LAUNCH();
+    }
+    k_sp_tails<<<gs(c, M), 256, 0, c.stream>>>(ro, K, ot);
+    W1G_CHECK_LAUNCH();
+    c.net_early_copy = false;
+    {
+        const Ctx::NetOut &o = c.net_out;
+        static const bool early_env = [] {  // W1G_EARLY_COPY=0: copy everything after the rows
+            const char *e = getenv("W1G_EARLY_COPY");
+            return !(e && *e == '0');
+        }();
+        if (early_env && o.sup && n <= o.node_cap && M <= o.arc_cap && c.copy_stream) {
+            // tails and row offsets leave for the host while the rows are sorted
+            W1G_CUDA(cudaEventRecord(c.ev[12], c.stream));
+            W1G_CUDA(cudaStreamWaitEvent(c.copy_stream, c.ev[12], 0));
+            W1G_CUDA(cudaMemcpyAsync(o.t, ot, sizeof(int64_t) * M, cudaMemcpyDeviceToHost, c.copy_stream));
+            W1G_CUDA(cudaMemcpyAsync(o.ro, ro, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost, c.copy_stream));
+            W1G_CUDA(cudaEventRecord(c.ev[13], c.copy_stream));
+            c.net_early_copy = true;
+        }
     }
     T.mark("bucket");
     const SpRows R{ro, cnt, sh, sc, ot, oh, oc, dflags(c)};
