@@ -11,6 +11,7 @@ is missing or no B200 is visible, calls fail loudly.
 from __future__ import annotations
 
 import ctypes
+import math
 import os
 import threading
 
@@ -104,7 +105,7 @@ _PROTOS = [
     ("w1g_build_network", ctypes.c_int, [_vp, _I64P, _i64, _I64P]),
     ("w1g_assemble", ctypes.c_int, [_vp, _I64P, _I64P]),
     ("w1g_fetch_network", ctypes.c_int, [_vp, _I64P, _I64P, _I64P, _F64P, _I64P]),
-    ("w1g_set_network_out", ctypes.c_int, [_vp, _I64P, _I64P, _I64P, _F64P, _I64P, _i64, _i64]),
+    ("w1g_set_network_out", ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64]),
     ("w1g_front_end", ctypes.c_int,
      [_vp, _F64P, _i64, _F64P, _i64, _f64, ctypes.c_int, ctypes.c_int, _f64, _f64, _u64,
       ctypes.POINTER(FrontEndInfo)]),
@@ -230,23 +231,6 @@ def device_count() -> int:
     return int(n.value)
 
 
-class _PinnedBlock:
-    """One page-locked allocation; returns itself to the pool when the last
-    numpy array carved from it is garbage-collected."""
-
-    __slots__ = ("ptr", "size", "__weakref__")
-
-    def __init__(self, ptr: int, size: int):
-        self.ptr = ptr
-        self.size = size
-
-    def __del__(self):
-        try:
-            _pool_release(self.ptr, self.size)
-        except Exception:
-            pass
-
-
 _pool_free: dict[int, list[int]] = {}
 _pool_lock = threading.Lock()
 _POOL_KEEP = 8  # free blocks kept per size class
@@ -268,15 +252,35 @@ def _pool_release(ptr: int, size: int):
     load().w1g_host_free(ctypes.c_void_p(ptr))
 
 
+class _PinnedHolder:
+    """The numpy-visible owner of one pooled page-locked block: the arrays
+    carved from it keep it alive (it is their .base), and when the last one is
+    garbage-collected the block returns to the pool."""
+
+    __slots__ = ("ptr", "size", "__array_interface__")
+
+    def __init__(self, ptr: int, size: int):
+        self.ptr = ptr
+        self.size = size
+        self.__array_interface__ = {"shape": (size,), "typestr": "|u1", "data": (ptr, False), "version": 3}
+
+    def __del__(self):
+        try:
+            _pool_release(self.ptr, self.size)
+        except Exception:
+            pass
+
+
 def pinned_arrays(specs):
     """numpy arrays [(shape, dtype), ...] carved from one pooled page-locked
     block, so device->host copies of results run at full link speed and the
     arrays are handed to the caller without a host-side copy."""
-    offs, total = [], 0
+    offs, nbytes, total = [], [], 0
     for shape, dtype in specs:
         total = (total + 63) & ~63
         offs.append(total)
-        total += int(np.prod(shape, dtype=np.int64)) * np.dtype(dtype).itemsize
+        nbytes.append(math.prod(shape) * np.dtype(dtype).itemsize)
+        total += nbytes[-1]
     size = _size_class(max(total, 1))
     with _pool_lock:
         lst = _pool_free.get(size)
@@ -285,20 +289,18 @@ def pinned_arrays(specs):
         p = _vp()
         check(load().w1g_host_alloc(size, ctypes.byref(p)))
         ptr = p.value
-    block = _PinnedBlock(ptr, size)
-    holder_base = np.ctypeslib.as_array((ctypes.c_uint8 * size).from_address(ptr))
+    base = np.asarray(_PinnedHolder(ptr, size))
     out = []
-    for (shape, dtype), off in zip(specs, offs):
-        nb = int(np.prod(shape, dtype=np.int64)) * np.dtype(dtype).itemsize
-        out.append(holder_base[off:off + nb].view(dtype).reshape(shape))
-    _keepalive[id(holder_base)] = block
-    import weakref
-
-    weakref.finalize(holder_base, _keepalive.pop, id(holder_base), None)
+    for (shape, dtype), off, nb in zip(specs, offs, nbytes):
+        out.append(base[off:off + nb].view(dtype).reshape(shape))
     return out
 
 
-_keepalive: dict[int, _PinnedBlock] = {}
+def addr(a: np.ndarray) -> int:
+    """Raw data address of a contiguous array (a cheap ctypes void* argument)."""
+    return a.__array_interface__["data"][0]
+
+
 
 
 def launch_count() -> int:

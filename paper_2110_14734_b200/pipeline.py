@@ -154,8 +154,8 @@ def sparsify(a, b, params: ApproxParams, device: int | None = None
         ncap, mcap = hint
         out = _lib.pinned_arrays([((ncap,), np.int64), ((mcap,), np.int64), ((mcap,), np.int64),
                                   ((mcap,), np.float64), ((ncap + 1,), np.int64)])
-        ctx.call("w1g_set_network_out", _lib.i64p(out[0]), _lib.i64p(out[1]), _lib.i64p(out[2]),
-                 _lib.f64p(out[3]), _lib.i64p(out[4]), ncap, mcap)
+        ctx.call("w1g_set_network_out", _lib.addr(out[0]), _lib.addr(out[1]), _lib.addr(out[2]),
+                 _lib.addr(out[3]), _lib.addr(out[4]), ncap, mcap)
     info = _front_end(ctx, ap, bp, params)
     diag = _diagnostics(info)
     if info.short_circuit:
