@@ -114,6 +114,10 @@ struct Ctx {
     DevBuf t_geom;                                  // NodeGeom per node
     DevBuf t_lr;                                    // int2 (left, right) per node, -1 leaf
     DevBuf t_rep32;                                 // int32 rep
+    // the split tree's X- and Y-lists, built by delta_condense from its cell
+    // order (pre_n = node count they are for, 0 = none; consumed by tree_run)
+    DevBuf pre_xl, pre_yl, pre_cells, pre_rows;
+    int64_t pre_n = 0;
     const double2 *pair_pts = nullptr;              // points the pairs' reps index
 
     // WSPD
@@ -205,6 +209,7 @@ enum FlagSlot {
     F_CELL_MIN = 16,  // 4 slots: min cx, max cx, min cy, max cy
     F_BBOX = 24,      // 4 doubles (as bits)
     F_SCAL = 32,      // 8 doubles of scalar results
+    F_LISTS = 40,     // delta_condense's presorted tree lists failed a check (tree sorts itself)
     F_NSLOTS = 64
 };
 

@@ -150,7 +150,7 @@ struct DcFlag {
 
 __global__ void k_dc_emit(DcFlag f, int64_t k, const int64_t *excl, const int64_t *am_in,
                           const int64_t *bm_in, double pitch, double half_width, uint64_t base,
-                          double2 *pts, int64_t *am, int64_t *bm) {
+                          double2 *pts, int64_t *am, int64_t *bm, longlong2 *ncell) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < k;
          i += (int64_t)gridDim.x * blockDim.x) {
         int64_t fl = f(i);
@@ -169,6 +169,7 @@ __global__ void k_dc_emit(DcFlag f, int64_t k, const int64_t *excl, const int64_
             // condensation.py:123: cells.astype(f64) * (k*delta) + offsets
             pts[rid] = make_double2(dadd(dmul(__ll2double_rn(c.x), pitch), o1),
                                     dadd(dmul(__ll2double_rn(c.y), pitch), o2));
+            if (ncell) ncell[rid] = c;
         }
         if (am_in[src]) atomicAdd((unsigned long long *)&am[rid], (unsigned long long)am_in[src]);
         if (bm_in[src]) atomicAdd((unsigned long long *)&bm[rid], (unsigned long long)bm_in[src]);
@@ -176,6 +177,177 @@ __global__ void k_dc_emit(DcFlag f, int64_t k, const int64_t *excl, const int64_
 }
 
 inline unsigned gs(const Ctx &c, int64_t n) { return grid_for(n, 256, 8u * c.sm_count); }
+// ---------------------------------------------------------------- the tree's lists from the cell order
+//
+// The split tree (tree.cu) starts from the nodes sorted by (x, y) and by
+// (y, x).  Condensed coordinates are cell * pitch + an offset below pitch / 2
+// (k > 1/2), so the x order is the column (cx) order refined inside each
+// column, and the y order the row (cy) order refined inside each row:
+// delta_condense's output is already in column order, rows are a counting
+// sort away, and columns / rows hold a few dozen nodes.  Each segment is sorted
+// by one warp in registers on (dkey(coord) with its low 9 bits replaced by the
+// node's place in the segment).  A final check demands strictly increasing x
+// along the X-list and y along the Y-list (so ties, rounding across cells or
+// truncated keys that collide all fail it); then the lists ARE the (x, y) /
+// (y, x) orders.  Otherwise (or for a segment over 512 nodes) F_LISTS is set
+// and the tree sorts for itself.
+constexpr int CL_MAX = 512;
+
+// one warp sorts a segment of <= CL_MAX nodes in registers: E full 64-bit
+// dkey(coord) keys per lane with the node's place in the segment alongside
+// (element i = lane * E + q), a bitonic network whose stages with partner
+// distance >= E are shuffles.  Equal keys may come out in either order: an
+// equal pair fails k_cl_check anyway.
+template <int E>
+__device__ __forceinline__ void cl_sort_segment(const double2 *__restrict__ pts, const uint32_t *__restrict__ ids,
+                                                int64_t s, int len, bool by_y, uint32_t *out, int lane) {
+    uint64_t v[E];
+    uint32_t w[E];
+#pragma unroll
+    for (int q = 0; q < E; q++) {
+        const int i = lane * E + q;
+        w[q] = (uint32_t)i;
+        if (i < len) {
+            const uint32_t id = ids ? ids[s + i] : (uint32_t)(s + i);
+            const double2 p = pts[id];
+            v[q] = dkey(by_y ? p.y : p.x);
+        } else {
+            v[q] = ~0ull;
+        }
+    }
+#pragma unroll
+    for (int k = 2; k <= 32 * E; k <<= 1)
+#pragma unroll
+        for (int j = k >> 1; j; j >>= 1) {
+            if (j >= E) {
+#pragma unroll
+                for (int q = 0; q < E; q++) {
+                    const uint64_t o = __shfl_xor_sync(0xffffffffu, v[q], j / E);
+                    const uint32_t ow = __shfl_xor_sync(0xffffffffu, w[q], j / E);
+                    const int i = lane * E + q;
+                    const bool keep_min = ((i & k) == 0) == ((i & j) == 0);
+                    const bool take = keep_min ? (o < v[q]) : (o > v[q]);
+                    if (take) {
+                        v[q] = o;
+                        w[q] = ow;
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < E; q++) {
+                    if (q & j) continue;
+                    const int p = q | j;
+                    const bool up = ((lane * E + q) & k) == 0;
+                    if ((v[q] > v[p]) == up && v[q] != v[p]) {
+                        const uint64_t t = v[q];
+                        v[q] = v[p];
+                        v[p] = t;
+                        const uint32_t tw = w[q];
+                        w[q] = w[p];
+                        w[p] = tw;
+                    }
+                }
+            }
+        }
+#pragma unroll
+    for (int q = 0; q < E; q++) {
+        const int i = lane * E + q;
+        if (i < len) out[s + i] = ids ? ids[s + w[q]] : (uint32_t)(s + w[q]);
+    }
+}
+
+__device__ __forceinline__ void cl_sort_any(const double2 *pts, const uint32_t *ids, int64_t s, int len, bool by_y,
+                                            uint32_t *out, int lane, int64_t *f) {
+    if (len <= 32) cl_sort_segment<1>(pts, ids, s, len, by_y, out, lane);
+    else if (len <= 64) cl_sort_segment<2>(pts, ids, s, len, by_y, out, lane);
+    else if (len <= 128) cl_sort_segment<4>(pts, ids, s, len, by_y, out, lane);
+    else if (len <= 256) cl_sort_segment<8>(pts, ids, s, len, by_y, out, lane);
+    else if (len <= CL_MAX) cl_sort_segment<16>(pts, ids, s, len, by_y, out, lane);
+    else if (lane == 0) atomicOr((unsigned long long *)&f[F_LISTS], 4ull);
+}
+
+// X-list: every column (a run of equal cx in node order) sorted by x; a warp
+// handles the columns that start inside its 32-node chunk
+__global__ void __launch_bounds__(256) k_cl_columns(const longlong2 *__restrict__ ncell,
+                                                    const double2 *__restrict__ pts, const int64_t *__restrict__ kp,
+                                                    uint32_t *xl, int64_t *f) {
+    const int64_t K = *kp;
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t base = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; base < K; base += warps * 32) {
+        const int64_t p = base + lane;
+        const bool start = p < K && (p == 0 || ncell[p].x != ncell[p - 1].x);
+        unsigned m = __ballot_sync(0xffffffffu, start);
+        while (m) {
+            const int b = __ffs(m) - 1;
+            m &= m - 1;
+            const int64_t s = base + b;
+            const long long cx = ncell[s].x;
+            int64_t e = s + 1;
+            while (true) {  // the column's end: first node of another column
+                const int64_t q = e + lane;
+                const bool stop = q >= K || ncell[q].x != cx;
+                const unsigned sm = __ballot_sync(0xffffffffu, stop);
+                if (sm) {
+                    e += __ffs(sm) - 1;
+                    break;
+                }
+                e += 32;
+                if (e - s > CL_MAX) break;
+            }
+            cl_sort_any(pts, nullptr, s, (int)((e - s) < (int64_t)(CL_MAX + 1) ? (e - s) : (int64_t)(CL_MAX + 1)), false, xl,
+                        lane, f);
+        }
+    }
+}
+
+// Y-list: nodes counted per row, scattered to their row, each row sorted by y
+__global__ void k_cl_rowcount(const longlong2 *__restrict__ ncell, const int64_t *__restrict__ kp, long long mny,
+                              unsigned *rcnt) {
+    const int64_t K = *kp;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < K; i += (int64_t)gridDim.x * blockDim.x)
+        atomicAdd(&rcnt[ncell[i].y - mny], 1u);
+}
+struct RowCnt {
+    const unsigned *c;
+    int64_t R;
+    __device__ int64_t operator()(int64_t i) const { return i < R ? (int64_t)c[i] : 0; }
+};
+__global__ void k_cl_rowscatter(const longlong2 *__restrict__ ncell, const int64_t *__restrict__ kp, long long mny,
+                                const int64_t *__restrict__ rstart, unsigned *rcur, uint32_t *rows) {
+    const int64_t K = *kp;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < K; i += (int64_t)gridDim.x * blockDim.x) {
+        const long long r = ncell[i].y - mny;
+        rows[rstart[r] + atomicAdd(&rcur[r], 1u)] = (uint32_t)i;
+    }
+}
+__global__ void __launch_bounds__(256) k_cl_rows(const double2 *__restrict__ pts, const uint32_t *__restrict__ rows,
+                                                 const int64_t *__restrict__ rstart, int64_t R, uint32_t *yl,
+                                                 int64_t *f) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < R; r += warps) {
+        const int64_t s = rstart[r], len = rstart[r + 1] - s;
+        if (len > 0)
+            cl_sort_any(pts, rows, s, (int)(len < (int64_t)(CL_MAX + 1) ? len : (int64_t)(CL_MAX + 1)), true, yl, lane,
+                        f);
+    }
+}
+
+// strictly increasing x along the X-list and y along the Y-list
+__global__ void k_cl_check(const double2 *__restrict__ pts, const int64_t *__restrict__ kp,
+                           const uint32_t *__restrict__ xl, const uint32_t *__restrict__ yl, int64_t *f) {
+    const int64_t K = *kp;
+    int bx = 0, by = 0;
+    for (int64_t i = 1 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < K; i += (int64_t)gridDim.x * blockDim.x) {
+        bx |= !(dkey(pts[xl[i - 1]].x) < dkey(pts[xl[i]].x));
+        by |= !(dkey(pts[yl[i - 1]].y) < dkey(pts[yl[i]].y));
+    }
+    if (__syncthreads_or(bx) && threadIdx.x == 0) atomicOr((unsigned long long *)&f[F_LISTS], 1ull);
+    if (__syncthreads_or(by) && threadIdx.x == 0) atomicOr((unsigned long long *)&f[F_LISTS], 2ull);
+}
+
+
 
 }  // namespace
 
@@ -283,6 +455,7 @@ int dc_run(Ctx &c, double delta, double pitch, double half_width, uint64_t seed,
            NodeSet *src_override) {
     NodeSet &src = src_override ? *src_override : c.nodes[0], &dst = c.nodes[1];
     const int64_t k = src.k;
+    c.pre_n = 0;
     dst.abar = src.abar;
     dst.bbar = src.bbar;
     if (delta == 0.0 || k == 0) {
@@ -349,9 +522,50 @@ int dc_run(Ctx &c, double delta, double pitch, double half_width, uint64_t seed,
     x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
     x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
     const uint64_t base = x ^ (x >> 31);
+    // the split tree's X- / Y-lists from the cell order (k_cl_columns), while the
+    // row range allows a counting sort (W1G_DC_LISTS=0: the tree sorts itself)
+    static const bool lists_env = [] {
+        const char *e = getenv("W1G_DC_LISTS");
+        return !(e && *e == '0');
+    }();
+    const int64_t R = (int64_t)(mxy - mny) + 1;
+    const bool lists = lists_env && k >= 2 && R > 0 && R <= 4 * k + 1024;
+    longlong2 *ncell = nullptr;
+    if (lists) W1G_TRY(ensure(c.pre_cells, (size_t)k, &ncell));
     k_dc_emit<<<gs(c, k), 256, 0, c.stream>>>(f, k, excl, ptr<int64_t>(src.am), ptr<int64_t>(src.bm),
-                                              pitch, half_width, base, pts, am, bm);
+                                              pitch, half_width, base, pts, am, bm, ncell);
     W1G_CHECK_LAUNCH();
+    if (lists) {
+        SubTimer T(c, "dc_lists");
+        uint32_t *xl, *yl, *rows;
+        unsigned *rcnt;
+        int64_t *rstart;
+        W1G_TRY(ensure(c.pre_xl, (size_t)k, &xl));
+        W1G_TRY(ensure(c.pre_yl, (size_t)k, &yl));
+        W1G_TRY(ensure(c.pre_rows, (size_t)k, &rows));
+        W1G_TRY(ensure(c.scr[0], (size_t)2 * (R + 2), &rcnt));  // the sort keys are dead by now
+        W1G_TRY(ensure(c.scr[1], (size_t)R + 2, &rstart));
+        W1G_CUDA(cudaMemsetAsync(rcnt, 0, sizeof(unsigned) * 2 * (R + 2), c.stream));
+        const int64_t *dK = dflags(c) + F_TOTAL;
+        const unsigned gk = grid_for(k, 256, 8u * c.sm_count);
+        k_cl_columns<<<gk, 256, 0, c.stream>>>(ncell, pts, dK, xl, dflags(c));
+        W1G_CHECK_LAUNCH();
+        T.mark("columns");
+        k_cl_rowcount<<<gk, 256, 0, c.stream>>>(ncell, dK, mny, rcnt);
+        W1G_CHECK_LAUNCH();
+        W1G_TRY(scan_i64(c, RowCnt{rcnt, R}, R + 1, rstart, nullptr));
+        k_cl_rowscatter<<<gk, 256, 0, c.stream>>>(ncell, dK, mny, rstart, rcnt + R + 2, rows);
+        W1G_CHECK_LAUNCH();
+        T.mark("row_bucket");
+        k_cl_rows<<<grid_for(R * 32, 256, 8u * c.sm_count), 256, 0, c.stream>>>(pts, rows, rstart, R, yl, dflags(c));
+        W1G_CHECK_LAUNCH();
+        T.mark("rows");
+        k_cl_check<<<grid_for(k, 256, 2u * c.sm_count), 256, 0, c.stream>>>(pts, dK, xl, yl, dflags(c));
+        W1G_CHECK_LAUNCH();
+        T.mark("check");
+        W1G_CUDA(cudaMemcpyAsync(c.h_pinned + F_LISTS, dflags(c) + F_LISTS, sizeof(int64_t), cudaMemcpyDeviceToHost,
+                                 c.stream));
+    }
     // node positions per side for emit_arcs, over k >= K (the masses past K are 0),
     // so their totals come back with K in the same round trip
     W1G_TRY(member_scans(c, dst, k));
@@ -360,6 +574,7 @@ int dc_run(Ctx &c, double delta, double pitch, double half_width, uint64_t seed,
     dst.na = c.h_pinned[F_MISC0];
     dst.nb = c.h_pinned[F_MISC1];
     dst.valid = true;
+    if (lists && !c.h_pinned[F_LISTS]) c.pre_n = dst.k;
     *kout = dst.k;
     return W1G_OK;
 }

@@ -865,11 +865,17 @@ int tree_run(Ctx &c, const double2 *pts, int64_t n, int64_t *n_nodes, int32_t *d
     W1G_TRY(ensure(c.scr[8], n, &xl[1]));
     W1G_TRY(ensure(c.scr[9], n, &yl[1]));
     const unsigned g = grid_for(n, 256, 8u * c.sm_count);
-    k_presort_keys<<<g, 256, 0, c.stream>>>(pts, n, kx0, kx1, ky0, ky1, xl[0], yl[0]);
-    W1G_CHECK_LAUNCH();
-    // X-list by (x, y) and Y-list by (y, x): kx1 = key(x), kx0 = key(y)
     SubTimer T(c, "tree");
-    {  // both lists in the same launches
+    // delta_condense may have built both lists already from its cell order (k_cl_columns)
+    const bool pre = c.pre_n == n && pts == ptr<double2>(c.nodes[1].pts);
+    c.pre_n = 0;
+    if (pre) {
+        xl[0] = ptr<uint32_t>(c.pre_xl);
+        yl[0] = ptr<uint32_t>(c.pre_yl);
+    } else {
+        k_presort_keys<<<g, 256, 0, c.stream>>>(pts, n, kx0, kx1, ky0, ky1, xl[0], yl[0]);
+        W1G_CHECK_LAUNCH();
+        // X-list by (x, y) and Y-list by (y, x): kx1 = key(x), kx0 = key(y); both in the same launches
         const Lex2Job jobs[2] = {{kx1, kx0, xl[0], n}, {kx0, kx1, yl[0], n}};
         W1G_TRY(sort_lex2_multi(c, jobs, 2));
     }
