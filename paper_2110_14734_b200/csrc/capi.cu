@@ -726,7 +726,7 @@ int w1g_front_end_device(w1g_ctx *c, const double *d_a, int64_t na, const double
     // auxiliary context, and the back end condenses the RAW diagrams (the same
     // cells and summed masses as condensing zero_condense's output), so the main
     // stream starts delta_condense at once
-    static const bool split_env = [] {
+    const bool split_env = [] {  // read per call (tests toggle it)
         const char *e = getenv("W1G_SPLIT");
         return !(e && *e == '0');
     }();

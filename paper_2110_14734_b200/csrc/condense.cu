@@ -524,7 +524,7 @@ int dc_run(Ctx &c, double delta, double pitch, double half_width, uint64_t seed,
     const uint64_t base = x ^ (x >> 31);
     // the split tree's X- / Y-lists from the cell order (k_cl_columns), while the
     // row range allows a counting sort (W1G_DC_LISTS=0: the tree sorts itself)
-    static const bool lists_env = [] {
+    const bool lists_env = [] {  // read per call (tests toggle it)
         const char *e = getenv("W1G_DC_LISTS");
         return !(e && *e == '0');
     }();

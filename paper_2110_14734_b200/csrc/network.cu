@@ -1305,7 +1305,7 @@ int spanner_net_run(Ctx &c, int64_t *node_count, int64_t *n_arcs) {
     c.net_early_copy = false;
     {
         const Ctx::NetOut &o = c.net_out;
-        static const bool early_env = [] {  // W1G_EARLY_COPY=0: copy everything after the rows
+        const bool early_env = [] {  // W1G_EARLY_COPY=0: copy everything after the rows (read per call)
             const char *e = getenv("W1G_EARLY_COPY");
             return !(e && *e == '0');
         }();
