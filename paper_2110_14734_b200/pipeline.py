@@ -216,7 +216,7 @@ def _run_pairs(pts, todo, params: ApproxParams, devs, streams_per_device: int, o
 
 
 def sparsify_batch(diagrams, params: ApproxParams, pairs: list[tuple[int, int]] | None = None, devices=None,
-                   streams_per_device: int = 3, on_network=None) -> int:
+                   streams_per_device: int = 4, on_network=None) -> int:
     """The front end of every pair (i < j, or `pairs`) of a diagram batch, sharded
     over devices and streams; on_network(i, j, network | None, diag) receives each
     result (in a worker thread).  Returns the number of pairs processed."""
@@ -228,7 +228,7 @@ def sparsify_batch(diagrams, params: ApproxParams, pairs: list[tuple[int, int]] 
 
 
 def pairwise_w1(diagrams, params: ApproxParams, devices=None, solver_threads: int | None = None,
-                pairs: list[tuple[int, int]] | None = None, streams_per_device: int = 3) -> np.ndarray:
+                pairs: list[tuple[int, int]] | None = None, streams_per_device: int = 4) -> np.ndarray:
     """Symmetric matrix of approx_w1(D[i], D[j]) for i < j, mirrored to (j, i).
 
     Pairs are sharded round-robin over `devices` x `streams_per_device` (one host
