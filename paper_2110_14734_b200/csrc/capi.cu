@@ -259,8 +259,10 @@ int w1g_ctx_destroy(w1g_ctx *c) {
     if (!c) return W1G_OK;
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
+    if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
     if (c->aux) {
-        c->aux->nodes[0] = NodeSet{};  // aliases this context's nodes0: not owned
+        // its nodes0 is its own here: the non-split schedule drops the alias after every call,
+        // the split one swaps buffers with this context
         w1g_ctx_destroy(static_cast<w1g_ctx *>(c->aux));
         c->aux = nullptr;
     }
@@ -268,9 +270,11 @@ int w1g_ctx_destroy(w1g_ctx *c) {
                       &c->t_rep, &c->t_size, &c->t_bbox, &c->t_geom, &c->t_lr, &c->t_rep32,
                       &c->pair_uv, &c->pair_w, &c->pair_path, &c->pair_idx, &c->pair_counts,
                       &c->arc_t, &c->arc_h, &c->arc_c, &c->net_sup, &c->net_t, &c->net_h,
-                      &c->net_c, &c->net_ro, &c->scan_state, &c->flags};
+                      &c->net_c, &c->net_ro, &c->scan_state, &c->flags, &c->pre_xl, &c->pre_yl,
+                      &c->pre_cells, &c->pre_rows, &c->pre_rcnt};
     for (DevBuf *b : bufs) free_buf(*b);
-    for (auto &ns : c->nodes) {
+    for (NodeSet *ns_p : {&c->nodes[0], &c->nodes[1], &c->raw}) {
+        NodeSet &ns = *ns_p;
         free_buf(ns.pts);
         free_buf(ns.am);
         free_buf(ns.bm);

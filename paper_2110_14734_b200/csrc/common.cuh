@@ -116,7 +116,7 @@ struct Ctx {
     DevBuf t_rep32;                                 // int32 rep
     // the split tree's X- and Y-lists, built by delta_condense from its cell
     // order (pre_n = node count they are for, 0 = none; consumed by tree_run)
-    DevBuf pre_xl, pre_yl, pre_cells, pre_rows;
+    DevBuf pre_xl, pre_yl, pre_cells, pre_rows, pre_rcnt;
     int64_t pre_n = 0;
     const double2 *pair_pts = nullptr;              // points the pairs' reps index
 

@@ -150,7 +150,8 @@ struct DcFlag {
 
 __global__ void k_dc_emit(DcFlag f, int64_t k, const int64_t *excl, const int64_t *am_in,
                           const int64_t *bm_in, double pitch, double half_width, uint64_t base,
-                          double2 *pts, int64_t *am, int64_t *bm, longlong2 *ncell) {
+                          double2 *pts, int64_t *am, int64_t *bm, longlong2 *ncell, long long mny,
+                          unsigned *rcnt) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < k;
          i += (int64_t)gridDim.x * blockDim.x) {
         int64_t fl = f(i);
@@ -169,7 +170,10 @@ __global__ void k_dc_emit(DcFlag f, int64_t k, const int64_t *excl, const int64_
             // condensation.py:123: cells.astype(f64) * (k*delta) + offsets
             pts[rid] = make_double2(dadd(dmul(__ll2double_rn(c.x), pitch), o1),
                                     dadd(dmul(__ll2double_rn(c.y), pitch), o2));
-            if (ncell) ncell[rid] = c;
+            if (ncell) {  // the tree's lists: node cell, and the node counted in its row
+                ncell[rid] = c;
+                atomicAdd(&rcnt[c.y - mny], 1u);
+            }
         }
         if (am_in[src]) atomicAdd((unsigned long long *)&am[rid], (unsigned long long)am_in[src]);
         if (bm_in[src]) atomicAdd((unsigned long long *)&bm[rid], (unsigned long long)bm_in[src]);
@@ -302,12 +306,6 @@ __global__ void __launch_bounds__(256) k_cl_columns(const longlong2 *__restrict_
 }
 
 // Y-list: nodes counted per row, scattered to their row, each row sorted by y
-__global__ void k_cl_rowcount(const longlong2 *__restrict__ ncell, const int64_t *__restrict__ kp, long long mny,
-                              unsigned *rcnt) {
-    const int64_t K = *kp;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < K; i += (int64_t)gridDim.x * blockDim.x)
-        atomicAdd(&rcnt[ncell[i].y - mny], 1u);
-}
 struct RowCnt {
     const unsigned *c;
     int64_t R;
@@ -531,28 +529,28 @@ int dc_run(Ctx &c, double delta, double pitch, double half_width, uint64_t seed,
     const int64_t R = (int64_t)(mxy - mny) + 1;
     const bool lists = lists_env && k >= 2 && R > 0 && R <= 4 * k + 1024;
     longlong2 *ncell = nullptr;
-    if (lists) W1G_TRY(ensure(c.pre_cells, (size_t)k, &ncell));
+    unsigned *rcnt = nullptr;
+    if (lists) {
+        W1G_TRY(ensure(c.pre_cells, (size_t)k, &ncell));
+        W1G_TRY(ensure(c.pre_rcnt, (size_t)2 * (R + 2), &rcnt));
+        W1G_CUDA(cudaMemsetAsync(rcnt, 0, sizeof(unsigned) * 2 * (R + 2), c.stream));
+    }
     k_dc_emit<<<gs(c, k), 256, 0, c.stream>>>(f, k, excl, ptr<int64_t>(src.am), ptr<int64_t>(src.bm),
-                                              pitch, half_width, base, pts, am, bm, ncell);
+                                              pitch, half_width, base, pts, am, bm, ncell, mny, rcnt);
     W1G_CHECK_LAUNCH();
     if (lists) {
         SubTimer T(c, "dc_lists");
         uint32_t *xl, *yl, *rows;
-        unsigned *rcnt;
         int64_t *rstart;
         W1G_TRY(ensure(c.pre_xl, (size_t)k, &xl));
         W1G_TRY(ensure(c.pre_yl, (size_t)k, &yl));
         W1G_TRY(ensure(c.pre_rows, (size_t)k, &rows));
-        W1G_TRY(ensure(c.scr[0], (size_t)2 * (R + 2), &rcnt));  // the sort keys are dead by now
-        W1G_TRY(ensure(c.scr[1], (size_t)R + 2, &rstart));
-        W1G_CUDA(cudaMemsetAsync(rcnt, 0, sizeof(unsigned) * 2 * (R + 2), c.stream));
+        W1G_TRY(ensure(c.scr[1], (size_t)R + 2, &rstart));  // the sort keys are dead by now
         const int64_t *dK = dflags(c) + F_TOTAL;
         const unsigned gk = grid_for(k, 256, 8u * c.sm_count);
         k_cl_columns<<<gk, 256, 0, c.stream>>>(ncell, pts, dK, xl, dflags(c));
         W1G_CHECK_LAUNCH();
         T.mark("columns");
-        k_cl_rowcount<<<gk, 256, 0, c.stream>>>(ncell, dK, mny, rcnt);
-        W1G_CHECK_LAUNCH();
         W1G_TRY(scan_i64(c, RowCnt{rcnt, R}, R + 1, rstart, nullptr));
         k_cl_rowscatter<<<gk, 256, 0, c.stream>>>(ncell, dK, mny, rstart, rcnt + R + 2, rows);
         W1G_CHECK_LAUNCH();
