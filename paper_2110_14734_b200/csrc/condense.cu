@@ -272,7 +272,7 @@ __device__ __forceinline__ void cl_sort_any(const double2 *pts, const uint32_t *
 
 // X-list: every column (a run of equal cx in node order) sorted by x; a warp
 // handles the columns that start inside its 32-node chunk
-__global__ void __launch_bounds__(256) k_cl_columns(const longlong2 *__restrict__ ncell,
+__global__ void __launch_bounds__(256, 3) k_cl_columns(const longlong2 *__restrict__ ncell,
                                                     const double2 *__restrict__ pts, const int64_t *__restrict__ kp,
                                                     uint32_t *xl, int64_t *f) {
     const int64_t K = *kp;
@@ -319,7 +319,7 @@ __global__ void k_cl_rowscatter(const longlong2 *__restrict__ ncell, const int64
         rows[rstart[r] + atomicAdd(&rcur[r], 1u)] = (uint32_t)i;
     }
 }
-__global__ void __launch_bounds__(256) k_cl_rows(const double2 *__restrict__ pts, const uint32_t *__restrict__ rows,
+__global__ void __launch_bounds__(256, 3) k_cl_rows(const double2 *__restrict__ pts, const uint32_t *__restrict__ rows,
                                                  const int64_t *__restrict__ rstart, int64_t R, uint32_t *yl,
                                                  int64_t *f) {
     const int lane = threadIdx.x & 31;
