@@ -809,10 +809,15 @@ int w1g_front_end_device(w1g_ctx *c, const double *d_a, int64_t na, const double
         host_t[2] = std::chrono::steady_clock::now();
     }
     info->epsilon_condense = eps_c;
+    bool aliased = false;
     auto start_rwmd = [&]() -> int {
         W1G_TRY(ensure_aux());
         Ctx *x = c->aux;
-        x->nodes[0] = c->nodes[0];  // alias (read only; nothing downstream rewrites nodes0)
+        // alias (read only; nothing downstream rewrites nodes0); the auxiliary
+        // context's own nodes0 buffers (the split schedule's) wait aside
+        x->nodes0_stash = x->nodes[0];
+        x->nodes[0] = c->nodes[0];
+        aliased = true;
         W1G_CUDA(cudaEventRecord(c->ev[8], c->stream));  // nodes0 complete on the main stream
         W1G_CUDA(cudaStreamWaitEvent(x->stream, c->ev[8], 0));
         worker = std::thread([&, x]() {
@@ -898,7 +903,10 @@ int w1g_front_end_device(w1g_ctx *c, const double *d_a, int64_t na, const double
         if (rc == W1G_OK) rc = rg;
     }
     if (worker.joinable()) worker.join();
-    if (overlap && !split && c->aux) c->aux->nodes[0] = NodeSet{};
+    if (aliased) {
+        c->aux->nodes[0] = c->aux->nodes0_stash;  // drop the alias, keep its own buffers
+        c->aux->nodes0_stash = NodeSet{};
+    }
     if (split) {
         if (rc_aux != W1G_OK) {
             set_error("%s", err_aux.c_str());

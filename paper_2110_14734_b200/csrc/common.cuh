@@ -92,6 +92,7 @@ struct Ctx {
     DevBuf in_pts;  // (na+nb) double2
     NodeSet nodes[2];
     NodeSet raw;    // the raw inputs as nodes (split fixed-delta front end)
+    NodeSet nodes0_stash;  // an auxiliary context's own nodes0 while it aliases the main one's
 
     // rwmd
     int culling = 1;
