@@ -548,8 +548,15 @@ int dc_run(Ctx &c, double delta, double pitch, double half_width, uint64_t seed,
         W1G_TRY(ensure(c.scr[1], (size_t)R + 2, &rstart));  // the sort keys are dead by now
         const int64_t *dK = dflags(c) + F_TOTAL;
         const unsigned gk = grid_for(k, 256, 8u * c.sm_count);
-        k_cl_columns<<<gk, 256, 0, c.stream>>>(ncell, pts, dK, xl, dflags(c));
+        // the columns (X-list) on the side stream, concurrently with the rows' bucketing and sort
+        cudaStream_t side = c.copy_stream ? c.copy_stream : c.stream;
+        if (side != c.stream) {
+            W1G_CUDA(cudaEventRecord(c.ev[14], c.stream));
+            W1G_CUDA(cudaStreamWaitEvent(side, c.ev[14], 0));
+        }
+        k_cl_columns<<<gk, 256, 0, side>>>(ncell, pts, dK, xl, dflags(c));
         W1G_CHECK_LAUNCH();
+        if (side != c.stream) W1G_CUDA(cudaEventRecord(c.ev[15], side));
         T.mark("columns");
         W1G_TRY(scan_i64(c, RowCnt{rcnt, R}, R + 1, rstart, nullptr));
         k_cl_rowscatter<<<gk, 256, 0, c.stream>>>(ncell, dK, mny, rstart, rcnt + R + 2, rows);
@@ -558,6 +565,7 @@ int dc_run(Ctx &c, double delta, double pitch, double half_width, uint64_t seed,
         k_cl_rows<<<grid_for(R * 32, 256, 8u * c.sm_count), 256, 0, c.stream>>>(pts, rows, rstart, R, yl, dflags(c));
         W1G_CHECK_LAUNCH();
         T.mark("rows");
+        if (side != c.stream) W1G_CUDA(cudaStreamWaitEvent(c.stream, c.ev[15], 0));
         k_cl_check<<<grid_for(k, 256, 2u * c.sm_count), 256, 0, c.stream>>>(pts, dK, xl, yl, dflags(c));
         W1G_CHECK_LAUNCH();
         T.mark("check");
