@@ -1296,11 +1296,14 @@ int spanner_net_run(Ctx &c, int64_t *node_count, int64_t *n_arcs) {
         W1G_CHECK_LAUNCH();
     }
     W1G_TRY(scan_i64(c, SpRowLen{cnt, ptr<int64_t>(ns.am), K, ns.nb}, n + 1, ro, nullptr));
-    if (P) {
-        k_sp_scatter<<<gs(c, P), 256, 0, c.stream>>>(uv, rep, P, pp, ro, cursor, sh, sc, dflags(c));
-        W1G_CHECK_LAUNCH();
+    // the tails depend on the row offsets alone: on the side stream, concurrently with the
+    // scatter and the row sorts, followed there by their early D2H copy (when armed)
+    cudaStream_t side = c.copy_stream ? c.copy_stream : c.stream;
+    if (side != c.stream) {
+        W1G_CUDA(cudaEventRecord(c.ev[12], c.stream));
+        W1G_CUDA(cudaStreamWaitEvent(side, c.ev[12], 0));
     }
-    k_sp_tails<<<gs(c, M), 256, 0, c.stream>>>(ro, K, ot);
+    k_sp_tails<<<gs(c, M), 256, 0, side>>>(ro, K, ot);
     W1G_CHECK_LAUNCH();
     c.net_early_copy = false;
     {
@@ -1309,15 +1312,16 @@ int spanner_net_run(Ctx &c, int64_t *node_count, int64_t *n_arcs) {
             const char *e = getenv("W1G_EARLY_COPY");
             return !(e && *e == '0');
         }();
-        if (early_env && o.sup && n <= o.node_cap && M <= o.arc_cap && c.copy_stream) {
-            // tails and row offsets leave for the host while the rows are sorted
-            W1G_CUDA(cudaEventRecord(c.ev[12], c.stream));
-            W1G_CUDA(cudaStreamWaitEvent(c.copy_stream, c.ev[12], 0));
-            W1G_CUDA(cudaMemcpyAsync(o.t, ot, sizeof(int64_t) * M, cudaMemcpyDeviceToHost, c.copy_stream));
-            W1G_CUDA(cudaMemcpyAsync(o.ro, ro, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost, c.copy_stream));
-            W1G_CUDA(cudaEventRecord(c.ev[13], c.copy_stream));
+        if (early_env && o.sup && n <= o.node_cap && M <= o.arc_cap && side != c.stream) {
+            W1G_CUDA(cudaMemcpyAsync(o.t, ot, sizeof(int64_t) * M, cudaMemcpyDeviceToHost, side));
+            W1G_CUDA(cudaMemcpyAsync(o.ro, ro, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost, side));
             c.net_early_copy = true;
         }
+    }
+    if (side != c.stream) W1G_CUDA(cudaEventRecord(c.ev[13], side));
+    if (P) {
+        k_sp_scatter<<<gs(c, P), 256, 0, c.stream>>>(uv, rep, P, pp, ro, cursor, sh, sc, dflags(c));
+        W1G_CHECK_LAUNCH();
     }
     T.mark("bucket");
     const SpRows R{ro, cnt, sh, sc, ot, oh, oc, dflags(c)};
@@ -1349,6 +1353,7 @@ int spanner_net_run(Ctx &c, int64_t *node_count, int64_t *n_arcs) {
         W1G_CHECK_LAUNCH();
     }
     T.mark("long");
+    if (side != c.stream) W1G_CUDA(cudaStreamWaitEvent(c.stream, c.ev[13], 0));  // the tails (and their copy)
     // the flags ride on the caller's final wait (no round trip here)
     W1G_CUDA(cudaMemcpyAsync(c.h_pinned + F_OVERFLOW, dflags(c) + F_OVERFLOW, sizeof(int64_t) * (F_NET_ERR - F_OVERFLOW + 1),
                              cudaMemcpyDeviceToHost, c.stream));
