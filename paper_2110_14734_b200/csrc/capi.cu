@@ -270,7 +270,7 @@ int w1g_ctx_destroy(w1g_ctx *c) {
                       &c->t_rep, &c->t_size, &c->t_bbox, &c->t_geom, &c->t_lr, &c->t_rep32,
                       &c->pair_uv, &c->pair_w, &c->pair_path, &c->pair_idx, &c->pair_counts,
                       &c->arc_t, &c->arc_h, &c->arc_c, &c->net_sup, &c->net_t, &c->net_h,
-                      &c->net_c, &c->net_ro, &c->scan_state, &c->flags, &c->pre_xl, &c->pre_yl,
+                      &c->net_c, &c->net_ro, &c->scan_state, &c->scan_state2, &c->flags, &c->pre_xl, &c->pre_yl,
                       &c->pre_cells, &c->pre_rows, &c->pre_rcnt};
     for (DevBuf *b : bufs) free_buf(*b);
     for (NodeSet *ns_p : {&c->nodes[0], &c->nodes[1], &c->raw}) {

@@ -151,6 +151,7 @@ struct Ctx {
     DevBuf lex_scr[2][6];   // sort_lex2 scratch per job
     unsigned sort_epoch = 0;  // onesweep status-word epoch (sort.cu)
     DevBuf scan_state;
+    DevBuf scan_state2;  // a second decoupled-look-back state for a scan on the side stream
     DevBuf flags;  // small device flag block (int64 x 64)
     int64_t *h_pinned = nullptr;  // pinned host mirror of `flags`
     void *h_stage = nullptr;      // pinned staging buffer for H2D / D2H

@@ -530,6 +530,7 @@ int dc_run(Ctx &c, double delta, double pitch, double half_width, uint64_t seed,
     const bool lists = lists_env && k >= 2 && R > 0 && R <= 4 * k + 1024;
     longlong2 *ncell = nullptr;
     unsigned *rcnt = nullptr;
+    bool members_done = false;
     if (lists) {
         W1G_TRY(ensure(c.pre_cells, (size_t)k, &ncell));
         W1G_TRY(ensure(c.pre_rcnt, (size_t)2 * (R + 2), &rcnt));
@@ -548,15 +549,31 @@ int dc_run(Ctx &c, double delta, double pitch, double half_width, uint64_t seed,
         W1G_TRY(ensure(c.scr[1], (size_t)R + 2, &rstart));  // the sort keys are dead by now
         const int64_t *dK = dflags(c) + F_TOTAL;
         const unsigned gk = grid_for(k, 256, 8u * c.sm_count);
-        // the columns (X-list) on the side stream, concurrently with the rows' bucketing and sort
+        // the columns (X-list) and the member scans on the side stream, concurrently with the
+        // rows' bucketing and sort; everything they use is allocated (on the main stream) first
         cudaStream_t side = c.copy_stream ? c.copy_stream : c.stream;
+        int64_t *exa_, *exb_;
+        unsigned long long *st2;
+        W1G_TRY(ensure(dst.exa, (size_t)k + 1, &exa_));
+        W1G_TRY(ensure(dst.exb, (size_t)k + 1, &exb_));
+        W1G_TRY(ensure(c.scan_state2, (size_t)((k + SCAN_TILE - 1) / SCAN_TILE) + 16, &st2));
         if (side != c.stream) {
             W1G_CUDA(cudaEventRecord(c.ev[14], c.stream));
             W1G_CUDA(cudaStreamWaitEvent(side, c.ev[14], 0));
         }
         k_cl_columns<<<gk, 256, 0, side>>>(ncell, pts, dK, xl, dflags(c));
         W1G_CHECK_LAUNCH();
-        if (side != c.stream) W1G_CUDA(cudaEventRecord(c.ev[15], side));
+        if (side != c.stream) {
+            // member_scans on the side stream with its own scan state
+            std::swap(c.stream, side);
+            std::swap(c.scan_state, c.scan_state2);
+            const int rc = member_scans(c, dst, k);
+            std::swap(c.scan_state, c.scan_state2);
+            std::swap(c.stream, side);
+            W1G_TRY(rc);
+            members_done = true;
+            W1G_CUDA(cudaEventRecord(c.ev[15], side));
+        }
         T.mark("columns");
         W1G_TRY(scan_i64(c, RowCnt{rcnt, R}, R + 1, rstart, nullptr));
         k_cl_rowscatter<<<gk, 256, 0, c.stream>>>(ncell, dK, mny, rstart, rcnt + R + 2, rows);
@@ -574,7 +591,7 @@ int dc_run(Ctx &c, double delta, double pitch, double half_width, uint64_t seed,
     }
     // node positions per side for emit_arcs, over k >= K (the masses past K are 0),
     // so their totals come back with K in the same round trip
-    W1G_TRY(member_scans(c, dst, k));
+    if (!members_done) W1G_TRY(member_scans(c, dst, k));
     W1G_TRY(flags_fetch(c, F_TOTAL, F_MISC1 - F_TOTAL + 1));
     dst.k = c.h_pinned[F_TOTAL];
     dst.na = c.h_pinned[F_MISC0];
