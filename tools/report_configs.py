@@ -80,7 +80,7 @@ def cfg1():
 
 def cfg3():
     a, b = synth.gaussian_cluster_pair(1_000_000, 1_000_000, seed=0)
-    ms, stages, i = front_end(a, b, 1.0, 0.01, reps=2)
+    ms, stages, i = front_end(a, b, 1.0, 0.01, reps=6)
     sc = np.load(os.path.join(ROOT, "tests", "golden", "scalars.npz"))
     emit({"config": "cfg3", "n_each": 1_000_000, "front_end_ms": ms, "stage_ms": stages,
           "lower_bound": i.lower_bound, "reference_lower_bound": float(sc["cfg3_L"]),
