@@ -350,6 +350,7 @@ int w1g_load_nodes(w1g_ctx *c, int slot, const double *points, const int64_t *am
     ns.abar = abar;
     ns.bbar = bbar;
     ns.na = ns.nb = -1;
+    ns.stats = false;
     invalidate_from_nodes(*c);
     if (slot == 0) c->nodes[1].valid = false;
     return W1G_OK;

@@ -71,6 +71,11 @@ struct NodeSet {
     // and their counts, computed by delta_condense for emit_arcs (na < 0: absent)
     DevBuf exa, exb;
     int64_t na = -1, nb = -1;
+    // from zero_condense (stats = true): the per-side member counts and the
+    // bbox as dkey()s [xmin, xmax, ymin, ymax] -- RWMD's frame without a round trip
+    bool stats = false;
+    int64_t nmem[2] = {0, 0};
+    uint64_t bbox_key[4] = {0, 0, 0, 0};
 };
 
 // per-node geometry used by the WSPD predicate (spanner.py:176-194), computed
@@ -212,6 +217,7 @@ enum FlagSlot {
     F_BBOX = 24,      // 4 doubles (as bits)
     F_SCAL = 32,      // 8 doubles of scalar results
     F_LISTS = 40,     // delta_condense's presorted tree lists failed a check (tree sorts itself)
+    F_ZSTAT = 41,     // 6 slots: zero_condense's member counts (a, b), ~min / max dkey of x, of y
     F_NSLOTS = 64
 };
 

@@ -54,13 +54,42 @@ __global__ void k_zc_emit(ZcFlag f, int64_t n, const int64_t *excl, double2 *pts
     }
 }
 
-__global__ void k_unbalanced(const int64_t *am, const int64_t *bm, const int64_t *kp, int64_t *flag) {
+// identical multisets (pipeline.py:106-109), plus what RWMD's frame needs
+// (lower_bound.py:61-75): the member count of each side and the bbox
+__global__ void k_zc_stats(const int64_t *am, const int64_t *bm, const double2 *pts, const int64_t *kp, int64_t *f) {
     const int64_t k = *kp;
     int any = 0;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < k;
-         i += (int64_t)gridDim.x * blockDim.x)
-        any |= am[i] != bm[i];
-    if (__syncthreads_or(any) && threadIdx.x == 0) atomicOr((unsigned long long *)flag, 1ull);
+    unsigned long long na = 0, nb = 0, nx = 0, xx = 0, ny = 0, xy = 0;  // nx/ny: max of ~key = ~min key
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t a = am[i], b = bm[i];
+        const double2 p = pts[i];
+        any |= a != b;
+        na += a > 0;
+        nb += b > 0;
+        const unsigned long long kx = dkey(p.x), ky = dkey(p.y);
+        nx = max(nx, ~kx);
+        xx = max(xx, kx);
+        ny = max(ny, ~ky);
+        xy = max(xy, ky);
+    }
+    for (int o = 16; o; o >>= 1) {
+        na += __shfl_xor_sync(0xffffffffu, na, o);
+        nb += __shfl_xor_sync(0xffffffffu, nb, o);
+        nx = max(nx, __shfl_xor_sync(0xffffffffu, nx, o));
+        xx = max(xx, __shfl_xor_sync(0xffffffffu, xx, o));
+        ny = max(ny, __shfl_xor_sync(0xffffffffu, ny, o));
+        xy = max(xy, __shfl_xor_sync(0xffffffffu, xy, o));
+    }
+    if (__syncthreads_or(any) && threadIdx.x == 0) atomicOr((unsigned long long *)&f[F_UNBALANCED], 1ull);
+    if ((threadIdx.x & 31) == 0) {
+        unsigned long long *u = reinterpret_cast<unsigned long long *>(f + F_ZSTAT);
+        if (na) atomicAdd(&u[0], na);
+        if (nb) atomicAdd(&u[1], nb);
+        atomicMax(&u[2], nx);
+        atomicMax(&u[3], xx);
+        atomicMax(&u[4], ny);
+        atomicMax(&u[5], xy);
+    }
 }
 
 // ------------------------------------------------------------ delta condense
@@ -357,6 +386,7 @@ int zc_run(Ctx &c, const double2 *d_a, int64_t na, const double2 *d_b, int64_t n
     ns.bbar = nb;
     ns.valid = true;
     c.nodes[1].valid = false;
+    ns.stats = false;
     if (n == 0) {
         ns.k = 0;
         *k0 = 0;
@@ -388,13 +418,22 @@ int zc_run(Ctx &c, const double2 *d_a, int64_t na, const double2 *d_b, int64_t n
     W1G_CUDA(cudaMemsetAsync(bm, 0, sizeof(int64_t) * n, c.stream));
     k_zc_emit<<<gs(c, n), 256, 0, c.stream>>>(f, n, excl, pts, am, bm);
     W1G_CHECK_LAUNCH();
-    k_unbalanced<<<gs(c, n), 256, 0, c.stream>>>(am, bm, dflags(c) + F_K0, dflags(c) + F_UNBALANCED);
+    k_zc_stats<<<grid_for(n, 256, 2u * c.sm_count), 256, 0, c.stream>>>(am, bm, pts, dflags(c) + F_K0, dflags(c));
     W1G_CHECK_LAUNCH();
+    W1G_CUDA(cudaMemcpyAsync(c.h_pinned + F_ZSTAT, dflags(c) + F_ZSTAT, sizeof(int64_t) * 6, cudaMemcpyDeviceToHost,
+                             c.stream));
     W1G_TRY(flags_fetch(c, F_K0, 2));
     if (speculative && lex2_speculation_failed(c, 1)) return zc_run(c, d_a, na, d_b, nb, k0, balanced, false);
     ns.k = c.h_pinned[F_K0];
     *k0 = ns.k;
     *balanced = c.h_pinned[F_UNBALANCED] ? 0 : 1;
+    ns.stats = true;
+    ns.nmem[0] = c.h_pinned[F_ZSTAT + 0];
+    ns.nmem[1] = c.h_pinned[F_ZSTAT + 1];
+    ns.bbox_key[0] = ~(uint64_t)c.h_pinned[F_ZSTAT + 2];
+    ns.bbox_key[1] = (uint64_t)c.h_pinned[F_ZSTAT + 3];
+    ns.bbox_key[2] = ~(uint64_t)c.h_pinned[F_ZSTAT + 4];
+    ns.bbox_key[3] = (uint64_t)c.h_pinned[F_ZSTAT + 5];
     return W1G_OK;
 }
 

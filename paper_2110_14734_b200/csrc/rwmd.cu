@@ -555,18 +555,27 @@ static int rwmd_prepare(Ctx &c, RwmdFrame &F, int range_side = -1, int64_t begin
         k_compact<<<g, 256, 0, c.stream>>>(mass[s], k, excl, F.members[s]);
         W1G_CHECK_LAUNCH();
     }
-    k_bbox_init<<<1, 1, 0, c.stream>>>(dflags(c));
-    k_bbox<<<grid_for(k, 256, 2u * c.sm_count), 256, 0, c.stream>>>(pts, k, dflags(c));  // few CTAs: fewer atomics
-    W1G_CHECK_LAUNCH();
-    W1G_TRY(flags_fetch(c, 0, F_BBOX + 4));
-    F.nm[0] = c.h_pinned[F_MISC0];
-    F.nm[1] = c.h_pinned[F_MISC1];
+    uint64_t bk[4];
+    if (ns.stats && range_side < 0) {
+        // zero_condense delivered the member counts and the bbox: no round trip here
+        F.nm[0] = ns.nmem[0];
+        F.nm[1] = ns.nmem[1];
+        for (int q = 0; q < 4; q++) bk[q] = ns.bbox_key[q];
+    } else {
+        k_bbox_init<<<1, 1, 0, c.stream>>>(dflags(c));
+        k_bbox<<<grid_for(k, 256, 2u * c.sm_count), 256, 0, c.stream>>>(pts, k, dflags(c));  // few CTAs: fewer atomics
+        W1G_CHECK_LAUNCH();
+        W1G_TRY(flags_fetch(c, 0, F_BBOX + 4));
+        F.nm[0] = c.h_pinned[F_MISC0];
+        F.nm[1] = c.h_pinned[F_MISC1];
+        for (int q = 0; q < 4; q++) bk[q] = (uint64_t)c.h_pinned[F_BBOX + q];
+    }
     c.rw_members[0] = F.nm[0];
     c.rw_members[1] = F.nm[1];
-    const double xmin = key_to_double((uint64_t)c.h_pinned[F_BBOX + 0]);
-    const double xmax = key_to_double((uint64_t)c.h_pinned[F_BBOX + 1]);
-    const double ymin = key_to_double((uint64_t)c.h_pinned[F_BBOX + 2]);
-    const double ymax = key_to_double((uint64_t)c.h_pinned[F_BBOX + 3]);
+    const double xmin = key_to_double(bk[0]);
+    const double xmax = key_to_double(bk[1]);
+    const double ymin = key_to_double(bk[2]);
+    const double ymax = key_to_double(bk[3]);
     // scaled FP32 frame: a power-of-two scale (exact in fp64) bringing the extent below 1
     double H = std::fmax(xmax - xmin, ymax - ymin);
     int e = 0;
