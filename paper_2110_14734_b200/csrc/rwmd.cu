@@ -627,43 +627,74 @@ int rwmd_run(Ctx &c, double *L, double *LA, double *LB) {
     W1G_TRY(rwmd_prepare(c, F));
     T.mark("prepare");
     const int64_t mx = (F.nm[0] > F.nm[1] ? F.nm[0] : F.nm[1]) + 1;
+    const int64_t mtb = mx / 64 + 2, msb = mx / (64 * SUP) + 2;
     double *terms, *dres;
     unsigned *mf;
     float *qn;
     double4 *tbox, *box64, *sbox;
-    W1G_TRY(ensure(c.scr[11], (size_t)mx, &terms));
+    // per-side scratch (the two sides may run concurrently), all allocated up front
+    W1G_TRY(ensure(c.scr[11], (size_t)2 * mx, &terms));
     W1G_TRY(ensure(c.scr[12], 4, &dres));
-    W1G_TRY(ensure(c.scr[13], (size_t)mx, &mf));
-    W1G_TRY(ensure(c.scr[14], (size_t)mx, &qn));
-    W1G_TRY(ensure(c.scr[15], (size_t)mx / 64 + 2, &tbox));  // per-tile boxes (tiles >= 64 targets)
-    W1G_TRY(ensure(c.scr[16], (size_t)mx / 64 + 2, &box64));
-    W1G_TRY(ensure(c.scr[21], (size_t)mx / (64 * SUP) + 2, &sbox));
-    for (int s = 0; s < 2; s++) {
+    W1G_TRY(ensure(c.scr[13], (size_t)2 * mx, &mf));
+    W1G_TRY(ensure(c.scr[14], (size_t)2 * mx, &qn));
+    W1G_TRY(ensure(c.scr[15], (size_t)2 * mtb, &tbox));  // per-tile boxes (tiles >= 64 targets)
+    W1G_TRY(ensure(c.scr[16], (size_t)2 * mtb, &box64));
+    W1G_TRY(ensure(c.scr[21], (size_t)2 * msb, &sbox));
+    double *best_s[2];
+    for (int s = 0; s < 2; s++) W1G_TRY(ensure(c.best[s], (size_t)F.nm[s] + 1, &best_s[s]));
+    double *val1;
+    W1G_TRY(ensure(c.scr[17], (size_t)F.nm[1] / 32 + 64, &val1));
+    // side B on the side stream, concurrently with side A, once its summation tree is cached
+    // (nothing left to allocate inside)
+    cudaStream_t side = c.copy_stream;
+    const bool conc = side && F.nm[0] > 0 && F.nm[1] > 0 && c.pw_n[1] == F.nm[1];
+    auto run_side = [&](int s) -> int {
         const int o = 1 - s;
         const int64_t n_src = F.nm[s], n_dst = F.nm[o];
         c.n_best[s] = n_src;
-        double *best;
-        W1G_TRY(ensure(c.best[s], (size_t)n_src + 1, &best));
+        double *best = best_s[s];
+        unsigned *mf_s = mf + s * mx;
+        float *qn_s = qn + s * mx;
+        double *terms_s = terms + s * mx;
+        double4 *tbox_s = tbox + s * mtb, *box64_s = box64 + s * mtb, *sbox_s = sbox + s * msb;
         if (n_src == 0) {
             W1G_CUDA(cudaMemsetAsync(dres + s, 0, sizeof(double), c.stream));
-            continue;
+            return W1G_OK;
         }
         if (n_dst > 0) {
-            W1G_CUDA(cudaMemsetAsync(mf, 0x7f, sizeof(unsigned) * n_src, c.stream));
-            W1G_TRY(rwmd_f32_min(c, F.mpts[s], F.mkey[s], n_src, F.mpts[o], F.mkey[o], n_dst, F.scale, mf, qn, tbox, c.culling));
+            W1G_CUDA(cudaMemsetAsync(mf_s, 0x7f, sizeof(unsigned) * n_src, c.stream));
+            W1G_TRY(rwmd_f32_min(c, F.mpts[s], F.mkey[s], n_src, F.mpts[o], F.mkey[o], n_dst, F.scale, mf_s, qn_s,
+                                 tbox_s, c.culling));
             T.mark(s ? "f32_b" : "f32_a");
-            k_boxes64<<<grid_for((n_dst / RT + 1) * 32, 256, 8u * c.sm_count), 256, 0, c.stream>>>(F.mpts[o], n_dst, box64);
+            k_boxes64<<<grid_for((n_dst / RT + 1) * 32, 256, 8u * c.sm_count), 256, 0, c.stream>>>(F.mpts[o], n_dst,
+                                                                                                    box64_s);
             W1G_CHECK_LAUNCH();
             k_superboxes<<<grid_for((n_dst / RT / SUP + 1) * 32, 256, 8u * c.sm_count), 256, 0, c.stream>>>(
-                box64, (n_dst + RT - 1) / RT, sbox);
+                box64_s, (n_dst + RT - 1) / RT, sbox_s);
             W1G_CHECK_LAUNCH();
             T.mark("boxes");
         }
-        W1G_TRY(launch_refine(c, F.mpts[s], F.mpos[s], F.members[s], mass[s], n_src, mf, qn, F.unscale, F.mpts[o],
-                              n_dst, box64, sbox, best, terms));
+        W1G_TRY(launch_refine(c, F.mpts[s], F.mpos[s], F.members[s], mass[s], n_src, mf_s, qn_s, F.unscale,
+                              F.mpts[o], n_dst, box64_s, sbox_s, best, terms_s));
         T.mark("refine");
-        W1G_TRY(pairwise_sum(c, terms, n_src, dres + s, c.pw_nodes[s], c.scr[18], c.pw_lev[s], &c.pw_n[s]));
+        W1G_TRY(pairwise_sum(c, terms_s, n_src, dres + s, c.pw_nodes[s], s ? c.scr[17] : c.scr[18], c.pw_lev[s],
+                             &c.pw_n[s]));
         T.mark("sum");
+        return W1G_OK;
+    };
+    if (conc) {
+        W1G_CUDA(cudaEventRecord(c.ev[14], c.stream));
+        W1G_CUDA(cudaStreamWaitEvent(side, c.ev[14], 0));
+        std::swap(c.stream, side);
+        const int rc = run_side(1);
+        std::swap(c.stream, side);
+        W1G_TRY(rc);
+        W1G_CUDA(cudaEventRecord(c.ev[15], side));
+        W1G_TRY(run_side(0));
+        W1G_CUDA(cudaStreamWaitEvent(c.stream, c.ev[15], 0));
+    } else {
+        W1G_TRY(run_side(0));
+        W1G_TRY(run_side(1));
     }
     double h[2];
     W1G_CUDA(cudaMemcpyAsync(h, dres, sizeof(double) * 2, cudaMemcpyDeviceToHost, c.stream));
