@@ -145,6 +145,9 @@ static bool is_pinned(const void *p) {
 }
 
 static void invalidate_from_nodes(Ctx &c) {
+    // delta_condense's presorted split-tree lists describe the node set they were
+    // built with: any rewrite of a node slot drops them (dc_run re-arms them)
+    c.pre_n = 0;
     c.tree_valid = false;
     c.pairs_valid = false;
     c.arcs_valid = false;
@@ -260,6 +263,11 @@ int w1g_ctx_destroy(w1g_ctx *c) {
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
     if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
+    if (c->aux_worker) {
+        c->aux_worker->stop();
+        delete c->aux_worker;
+        c->aux_worker = nullptr;
+    }
     if (c->aux) {
         // its nodes0 is its own here: the non-split schedule drops the alias after every call,
         // the split one swaps buffers with this context
@@ -268,7 +276,7 @@ int w1g_ctx_destroy(w1g_ctx *c) {
     }
     DevBuf *bufs[] = {&c->in_pts, &c->best[0], &c->best[1], &c->tree_pts, &c->t_left, &c->t_right,
                       &c->t_rep, &c->t_size, &c->t_bbox, &c->t_geom, &c->t_lr, &c->t_rep32,
-                      &c->pair_uv, &c->pair_w, &c->pair_path, &c->pair_idx, &c->pair_counts,
+                      &c->pair_uv, &c->pair_w, &c->pair_idx, &c->pair_counts,
                       &c->arc_t, &c->arc_h, &c->arc_c, &c->net_sup, &c->net_t, &c->net_h,
                       &c->net_c, &c->net_ro, &c->scan_state, &c->scan_state2, &c->flags, &c->pre_xl, &c->pre_yl,
                       &c->pre_cells, &c->pre_rows, &c->pre_rcnt};
@@ -693,10 +701,9 @@ static int copy_network_out(Ctx &c, int *copied) {
 
 static const double SQRT2 = 1.4142135623730951;  // math.sqrt(2.0)
 
-int w1g_front_end_device(w1g_ctx *c, const double *d_a, int64_t na, const double *d_b, int64_t nb,
-                         double s, int use_condensation, int delta_mode, double delta, double k,
-                         uint64_t seed, w1g_front_end_info *info) {
-    CTX_CHECK(c);
+static int front_end_impl(w1g_ctx *c, const double *d_a, int64_t na, const double *d_b, int64_t nb,
+                          double s, int use_condensation, int delta_mode, double delta, double k,
+                          uint64_t seed, w1g_front_end_info *info) {
     if (!info) return W1G_EINVAL;
     memset(info, 0, sizeof *info);
     if (!(s > 0.0)) {
@@ -747,9 +754,28 @@ int w1g_front_end_device(w1g_ctx *c, const double *d_a, int64_t na, const double
     int64_t k0 = 0;
     int32_t balanced = 0;
     double L = 0.0, LA = 0.0, LB = 0.0;
-    std::thread worker;
     int rc_aux = W1G_OK;
     std::string err_aux;
+    // the auxiliary leg runs on the context's persistent worker thread; on every
+    // exit path (errors included) the gate is opened and the job waited for
+    // before the locals it references go out of scope
+    struct AuxJoin {
+        AuxWorker *w = nullptr;
+        std::mutex *mu;
+        std::condition_variable *cv;
+        bool *open;
+        ~AuxJoin() { join(); }
+        void join() {
+            if (!w) return;
+            {
+                std::lock_guard<std::mutex> lk(*mu);
+                *open = true;
+            }
+            cv->notify_all();
+            w->wait();
+            w = nullptr;
+        }
+    } aux_join{nullptr, &gate_mu, &gate_cv, &gate_open};
     auto ensure_aux = [&]() -> int {
         if (!c->aux) {
             w1g_ctx *x = nullptr;
@@ -760,6 +786,10 @@ int w1g_front_end_device(w1g_ctx *c, const double *d_a, int64_t na, const double
             W1G_CUDA(cudaStreamDestroy(x->stream));
             W1G_CUDA(cudaStreamCreateWithPriority(&x->stream, cudaStreamNonBlocking, least));
             c->aux = x;
+        }
+        if (!c->aux_worker) {
+            c->aux_worker = new AuxWorker();
+            c->aux_worker->start();
         }
         Ctx *x = c->aux;
         x->culling = c->culling;
@@ -773,7 +803,8 @@ int w1g_front_end_device(w1g_ctx *c, const double *d_a, int64_t na, const double
         W1G_CUDA(cudaEventRecord(c->ev[8], c->stream));  // the inputs are on the device
         W1G_CUDA(cudaStreamWaitEvent(x->stream, c->ev[8], 0));
         const double2 *pa = reinterpret_cast<const double2 *>(d_a), *pb = reinterpret_cast<const double2 *>(d_b);
-        worker = std::thread([&, x, pa, pb]() {
+        aux_join.w = c->aux_worker;
+        c->aux_worker->submit([&, x, pa, pb]() {
             cudaSetDevice(x->device);
             set_thread_stream(x->stream);
             cudaEventRecord(x->ev[2], x->stream);
@@ -821,7 +852,8 @@ int w1g_front_end_device(w1g_ctx *c, const double *d_a, int64_t na, const double
         aliased = true;
         W1G_CUDA(cudaEventRecord(c->ev[8], c->stream));  // nodes0 complete on the main stream
         W1G_CUDA(cudaStreamWaitEvent(x->stream, c->ev[8], 0));
-        worker = std::thread([&, x]() {
+        aux_join.w = c->aux_worker;
+        c->aux_worker->submit([&, x]() {
             cudaSetDevice(x->device);
             set_thread_stream(x->stream);
             cudaEventRecord(x->ev[0], x->stream);
@@ -903,7 +935,7 @@ int w1g_front_end_device(w1g_ctx *c, const double *d_a, int64_t na, const double
         const int rg = open_gate();
         if (rc == W1G_OK) rc = rg;
     }
-    if (worker.joinable()) worker.join();
+    aux_join.join();
     if (aliased) {
         c->aux->nodes[0] = c->aux->nodes0_stash;  // drop the alias, keep its own buffers
         c->aux->nodes0_stash = NodeSet{};
@@ -978,6 +1010,25 @@ int w1g_front_end_device(w1g_ctx *c, const double *d_a, int64_t na, const double
         fprintf(stderr, "\n");
     }
     return W1G_OK;
+}
+
+int w1g_front_end_device(w1g_ctx *c, const double *d_a, int64_t na, const double *d_b, int64_t nb,
+                         double s, int use_condensation, int delta_mode, double delta, double k,
+                         uint64_t seed, w1g_front_end_info *info) {
+    CTX_CHECK(c);
+    const int rc = front_end_impl(c, d_a, na, d_b, nb, s, use_condensation, delta_mode, delta, k, seed, info);
+    if (rc != W1G_OK) {
+        // an error can leave copies into the caller's output target (or reads of
+        // the inputs on the auxiliary stream) in flight: drain every stream this
+        // call used before the caller may reuse those buffers
+        std::string msg = g_err;
+        cudaStreamSynchronize(c->stream);
+        if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
+        if (c->aux) cudaStreamSynchronize(c->aux->stream);
+        cudaGetLastError();
+        set_error("%s", msg.c_str());
+    }
+    return rc;
 }
 
 int w1g_front_end(w1g_ctx *c, const double *a, int64_t na, const double *b, int64_t nb, double s,

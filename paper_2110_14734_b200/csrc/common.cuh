@@ -8,9 +8,13 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <condition_variable>
 #include <cstdio>
 #include <cstdlib>
+#include <functional>
+#include <mutex>
 #include <string>
+#include <thread>
 
 #include "../../include/w1g.h"
 
@@ -88,6 +92,55 @@ struct NodeGeom {
 
 enum { SCR_N = 24 };
 
+// A persistent host thread that runs one job at a time for an auxiliary
+// context (the fused front end's zero_condense + RWMD leg): created with the
+// context, joined when it is destroyed, so no call creates a thread.
+// submit() hands a job over; wait() blocks until it has finished.  The job
+// may reference the submitter's stack: every submitter waits before returning
+// (the front end's scope guard does so on every exit path).
+struct AuxWorker {
+    std::thread th;
+    std::mutex mu;
+    std::condition_variable cv;
+    std::function<void()> job;
+    bool busy = false, quit = false;
+    void start() {
+        th = std::thread([this] {
+            std::unique_lock<std::mutex> lk(mu);
+            for (;;) {
+                cv.wait(lk, [this] { return quit || (busy && job); });
+                if (quit) return;
+                std::function<void()> f = std::move(job);
+                job = nullptr;
+                lk.unlock();
+                f();
+                lk.lock();
+                busy = false;
+                cv.notify_all();
+            }
+        });
+    }
+    void submit(std::function<void()> f) {
+        std::lock_guard<std::mutex> lk(mu);
+        job = std::move(f);
+        busy = true;
+        cv.notify_all();
+    }
+    void wait() {
+        std::unique_lock<std::mutex> lk(mu);
+        cv.wait(lk, [this] { return !busy; });
+    }
+    void stop() {
+        if (!th.joinable()) return;
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            quit = true;
+        }
+        cv.notify_all();
+        th.join();
+    }
+};
+
 struct Ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -131,8 +184,7 @@ struct Ctx {
     int64_t n_pairs = 0;
     int32_t wspd_levels = 0;
     DevBuf pair_uv;    // int2 (u, v) tree node ids
-    DevBuf pair_w;     // int32 owner internal node
-    DevBuf pair_path;  // uint64 left-aligned DFS path bits (1 = right child)
+    DevBuf pair_w;     // int32 owner internal node of each level-0 recursion item (reference order)
     DevBuf pair_idx;   // int64 (P,2) representative point indices
     DevBuf pair_counts;
     bool pairs_have_nodes = false;
@@ -180,6 +232,7 @@ struct Ctx {
     // spawn point as above), without / with an armed output target
     int split_gate = 0, split_gate_e2e = 1;
     Ctx *aux = nullptr;
+    AuxWorker *aux_worker = nullptr;  // the host thread that drives `aux` (owned by this context)
 
     // one-shot host target for the next fused front end's network (w1g_set_network_out)
     struct NetOut {
@@ -208,7 +261,7 @@ enum FlagSlot {
     F_FRONT_OVF = 8,
     F_NET_ERR = 9,
     F_TOTAL = 10,
-    F_PATH_OVF = 11,
+    F_RESERVED11 = 11,
     F_MISC0 = 12,
     F_MISC1 = 13,
     F_MISC2 = 14,

@@ -395,7 +395,13 @@ int radix_sort_multi(Ctx &c, const SortJob *jobs, int njobs, int words, int top_
         }
         const int w = dg / 8;
         c.sort_epoch = (c.sort_epoch + 1) & 0x3fffffffu;
-        if (c.sort_epoch == 0) c.sort_epoch = 1;
+        if (c.sort_epoch == 0) {
+            // the 30-bit epoch wrapped: a status word left from 2^30 passes ago could
+            // match again, so every job's status words are cleared before reuse
+            for (auto &job : c.sort_scr)
+                if (job[6].p) W1G_CUDA(cudaMemsetAsync(job[6].p, 0, job[6].cap, c.stream));
+            c.sort_epoch = 1;
+        }
         A.shift = 8 * (dg % 8);
         A.ticket = tickets + (launch++ & 63);
         A.epoch = c.sort_epoch;

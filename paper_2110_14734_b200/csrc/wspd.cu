@@ -11,10 +11,16 @@
 // either a pair or two children.  Levels run in batches; the host polls the
 // frontier size between batches and regrows buffers on overflow.
 //
-// reference_order = 1 additionally carries (owner w, DFS path bits) and sorts
-// the pairs by (w, DFS pop order) -- the reference's exact output layout
-// (owner ascending, right child popped first, spanner.py:226-236) -- and
-// produces count_pairs' per-node counts.
+// reference_order = 1 additionally keeps every level of the frontier (the
+// whole recursion forest, one item per (u, v) the reference's stacks ever
+// hold) with a link per item -- its pair slot, or the index of its two
+// children -- and then lays the pairs out in the reference's exact order
+// (owner ascending, DFS pop order with the right child popped first,
+// spanner.py:206-241) the way the reference's own two passes do, one level at
+// a time: leaf counts bottom-up (count_pairs), an exclusive scan over the
+// owners (build_wspd's offsets), and offsets top-down (the right child at its
+// parent's offset, the left child after the right child's leaves).  Any
+// recursion depth works, like the reference's explicit stack.
 #include <cooperative_groups.h>
 
 #include "common.cuh"
@@ -25,12 +31,8 @@ namespace w1g {
 
 namespace {
 
-struct ItemF {  // fused path: only the node pair
+struct ItemF {  // one (u, v) recursion item
     int32_t u, v;
-};
-struct ItemO {  // reference-order path
-    int32_t u, v, w, pad;
-    uint64_t p0, p1;  // left-aligned path bits, 1 = right child
 };
 
 __device__ __forceinline__ bool ws_predicate(const NodeGeom &a, const NodeGeom &b, double s) {
@@ -65,7 +67,8 @@ __global__ void k_wspd_init_f(const int2 *lr, int64_t nn, ItemF *items, int64_t 
     }
 }
 
-__global__ void k_wspd_init_o(const int2 *lr, int64_t nn, ItemO *items, int64_t cap, int64_t *cnt) {
+// reference order: level 0 also records each item's owner internal node
+__global__ void k_wspd_init_o(const int2 *lr, int64_t nn, ItemF *items, int32_t *own0, int64_t cap, int64_t *cnt) {
     const int lane = threadIdx.x & 31;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t base = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) & ~31ll; base < nn; base += stride) {
@@ -79,32 +82,25 @@ __global__ void k_wspd_init_o(const int2 *lr, int64_t nn, ItemO *items, int64_t 
         b = __shfl_sync(0xffffffffu, b, 0);
         if (need) {
             int64_t slot = b + __popc(m & lanemask_lt());
-            if (slot < cap) items[slot] = ItemO{c.x, c.y, (int32_t)w, 0, 0ull, 0ull};
+            if (slot < cap) {
+                items[slot] = ItemF{c.x, c.y};
+                own0[slot] = (int32_t)w;
+            }
         }
     }
 }
 
+// one frontier level.  ORDER: cur / next are consecutive levels of the one
+// item array (global indices base_cur + i / base_next + slot) and every item
+// records its link: ~pair slot, or the index of its first child
 template <bool ORDER>
-struct ItemT;
-template <>
-struct ItemT<false> {
-    using T = ItemF;
-};
-template <>
-struct ItemT<true> {
-    using T = ItemO;
-};
-
-template <bool ORDER>
-__device__ __forceinline__ void wspd_level(const typename ItemT<ORDER>::T *__restrict__ cur,
-                                           typename ItemT<ORDER>::T *__restrict__ next,
+__device__ __forceinline__ void wspd_level(const ItemF *__restrict__ cur, ItemF *__restrict__ next,
                                            int64_t cap, int level, Counters k,
-                                           int2 *__restrict__ out_uv, int32_t *__restrict__ out_w,
-                                           uint64_t *__restrict__ out_p0,
-                                           uint64_t *__restrict__ out_p1, int64_t pair_cap,
+                                           int2 *__restrict__ out_uv, int64_t *__restrict__ links,
+                                           int64_t base_cur, int64_t base_next, int64_t pair_cap,
                                            double s, const NodeGeom *__restrict__ geom,
                                            const int2 *__restrict__ lr, int64_t n_known = -1) {
-    using Item = typename ItemT<ORDER>::T;
+    using Item = ItemF;
     int64_t n = n_known >= 0 ? n_known : *((volatile int64_t *)&k.cnt[level % 3]);
     if (n > cap) n = cap;  // previous level overflowed: its flag is already set
     if (blockIdx.x == 0 && threadIdx.x == 0) k.cnt[(level + 2) % 3] = 0;
@@ -161,31 +157,19 @@ __device__ __forceinline__ void wspd_level(const typename ItemT<ORDER>::T *__res
         __syncthreads();  // s_* are rewritten by the next round
         if (valid && ws) {
             const int64_t slot = bp + __popc(mp & lt);
+            if constexpr (ORDER) links[base_cur + i] = ~slot;
             if (slot < pair_cap) {
                 out_uv[slot] = make_int2(it.u, it.v);
-                if constexpr (ORDER) {
-                    out_w[slot] = it.w;
-                    out_p0[slot] = it.p0;
-                    out_p1[slot] = it.p1;
-                }
             } else if (slot == pair_cap) {
                 atomicOr((unsigned long long *)&k.flags[F_PAIR_OVF], 1ull);
             }
         }
         if (valid && !ws) {
             const int64_t slot = bs + 2 * __popc(ms & lt);
+            if constexpr (ORDER) links[base_cur + i] = base_next + slot;
             if (slot + 1 < cap) {
-                if constexpr (ORDER) {
-                    uint64_t q0 = it.p0, q1 = it.p1;
-                    if (level < 64) q0 |= 1ull << (63 - level);
-                    else if (level < 128) q1 |= 1ull << (127 - level);
-                    else atomicOr((unsigned long long *)&k.flags[F_PATH_OVF], 1ull);
-                    next[slot] = ItemO{c0.x, c0.y, it.w, 0, it.p0, it.p1};  // left child: bit 0
-                    next[slot + 1] = ItemO{c1.x, c1.y, it.w, 0, q0, q1};     // right child: bit 1
-                } else {
-                    next[slot] = ItemF{c0.x, c0.y};
-                    next[slot + 1] = ItemF{c1.x, c1.y};
-                }
+                next[slot] = ItemF{c0.x, c0.y};      // left child
+                next[slot + 1] = ItemF{c1.x, c1.y};  // right child
             } else {
                 atomicOr((unsigned long long *)&k.flags[F_FRONT_OVF], 1ull);
             }
@@ -193,25 +177,18 @@ __device__ __forceinline__ void wspd_level(const typename ItemT<ORDER>::T *__res
     }
 }
 
-template <bool ORDER>
-__global__ void __launch_bounds__(256) k_wspd_level(const typename ItemT<ORDER>::T *__restrict__ cur,
-                                                    typename ItemT<ORDER>::T *__restrict__ next,
+__global__ void __launch_bounds__(256) k_wspd_level(const ItemF *__restrict__ cur, ItemF *__restrict__ next,
                                                     int64_t cap, int level, Counters k,
-                                                    int2 *__restrict__ out_uv, int32_t *__restrict__ out_w,
-                                                    uint64_t *__restrict__ out_p0,
-                                                    uint64_t *__restrict__ out_p1, int64_t pair_cap,
-                                                    double s, const NodeGeom *__restrict__ geom,
+                                                    int2 *__restrict__ out_uv, int64_t pair_cap, double s,
+                                                    const NodeGeom *__restrict__ geom,
                                                     const int2 *__restrict__ lr) {
-    wspd_level<ORDER>(cur, next, cap, level, k, out_uv, out_w, out_p0, out_p1, pair_cap, s, geom, lr);
+    wspd_level<false>(cur, next, cap, level, k, out_uv, nullptr, 0, 0, pair_cap, s, geom, lr);
 }
 
 // all frontier levels in ONE persistent cooperative launch: a grid barrier
 // per level instead of a launch per level and a host poll per batch
-template <bool ORDER>
-__global__ void __launch_bounds__(256) k_wspd_coop(typename ItemT<ORDER>::T *fa, typename ItemT<ORDER>::T *fb,
-                                                   int64_t cap, Counters k, int2 *__restrict__ out_uv,
-                                                   int32_t *__restrict__ out_w, uint64_t *__restrict__ out_p0,
-                                                   uint64_t *__restrict__ out_p1, int64_t pair_cap, double s,
+__global__ void __launch_bounds__(256) k_wspd_coop(ItemF *fa, ItemF *fb, int64_t cap, Counters k,
+                                                   int2 *__restrict__ out_uv, int64_t pair_cap, double s,
                                                    const NodeGeom *__restrict__ geom, const int2 *__restrict__ lr,
                                                    int32_t *levels_out) {
     cg::grid_group grid = cg::this_grid();
@@ -219,23 +196,90 @@ __global__ void __launch_bounds__(256) k_wspd_coop(typename ItemT<ORDER>::T *fa,
     while (true) {
         const int64_t n = *((volatile int64_t *)&k.cnt[level % 3]);
         if (n == 0 || n > cap) break;  // done, or the last level overflowed (flag set)
-        wspd_level<ORDER>((level & 1) ? fb : fa, (level & 1) ? fa : fb, cap, level, k, out_uv, out_w, out_p0,
-                          out_p1, pair_cap, s, geom, lr, n);
+        wspd_level<false>((level & 1) ? fb : fa, (level & 1) ? fa : fb, cap, level, k, out_uv, nullptr, 0, 0,
+                          pair_cap, s, geom, lr, n);
         grid.sync();
         level++;
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) *levels_out = level;
 }
 
-__global__ void k_order_keys(const int32_t *w, const uint64_t *p0, const uint64_t *p1, int64_t n,
-                             uint64_t *k0, uint64_t *k1, uint64_t *k2, uint32_t *vals) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        // DFS pop order = descending path bits -> ascending complement
-        k0[i] = ~p1[i];
-        k1[i] = ~p0[i];
-        k2[i] = (uint64_t)(uint32_t)w[i];
-        vals[i] = (uint32_t)i;
+// reference order: the levels are appended to one array (level l occupies
+// [starts[l], starts[l+1])), so the whole recursion forest stays for the
+// ordering passes; `cap` is the array's capacity, max_levels starts' capacity
+__global__ void __launch_bounds__(256) k_wspd_coop_o(ItemF *items, int64_t cap, Counters k,
+                                                     int2 *__restrict__ out_uv, int64_t *__restrict__ links,
+                                                     int64_t *__restrict__ starts, int64_t max_levels,
+                                                     int64_t pair_cap, double s, const NodeGeom *__restrict__ geom,
+                                                     const int2 *__restrict__ lr, int32_t *levels_out) {
+    cg::grid_group grid = cg::this_grid();
+    int level = 0;
+    int64_t base = 0;
+    while (true) {
+        const int64_t n = *((volatile int64_t *)&k.cnt[level % 3]);
+        if (n == 0) break;
+        if (base + n > cap || level + 1 >= max_levels) {  // overflow (the flag is set by whoever saw it)
+            if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr((unsigned long long *)&k.flags[F_FRONT_OVF], 1ull);
+            break;
+        }
+        if (blockIdx.x == 0 && threadIdx.x == 0) starts[level] = base;
+        wspd_level<true>(items + base, items + base + n, cap - (base + n), level, k, out_uv, links, base,
+                         base + n, pair_cap, s, geom, lr, n);
+        grid.sync();
+        base += n;
+        level++;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        *levels_out = level;
+        starts[level] = base;
+    }
+}
+
+// count_pairs, bottom-up: leaves below each item (deepest level first); then
+// each owner's count from its level-0 item
+__global__ void __launch_bounds__(256) k_order_up(const int64_t *__restrict__ links, const int64_t *__restrict__ starts,
+                                                  int levels, int64_t *__restrict__ cnt,
+                                                  const int32_t *__restrict__ own0, int64_t *__restrict__ full) {
+    cg::grid_group grid = cg::this_grid();
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, stride = (int64_t)gridDim.x * blockDim.x;
+    for (int l = levels - 1; l >= 0; l--) {
+        const int64_t b = starts[l], e = starts[l + 1];
+        for (int64_t i = b + tid; i < e; i += stride) {
+            const int64_t ln = links[i];
+            cnt[i] = ln < 0 ? 1 : cnt[ln] + cnt[ln + 1];
+        }
+        grid.sync();
+    }
+    const int64_t n0 = levels > 0 ? starts[1] : 0;
+    for (int64_t i = tid; i < n0; i += stride) full[own0[i]] = cnt[i];
+}
+
+// write_pairs, top-down: an item's first pair lands at its offset; the DFS pops
+// the right child first, so the right child starts at the parent's offset and
+// the left child after the right child's leaves.  `cnt` is overwritten by the
+// offsets level by level (each child is read by its one parent before that).
+__global__ void __launch_bounds__(256) k_order_down(const int64_t *__restrict__ links,
+                                                    const int64_t *__restrict__ starts, int levels,
+                                                    int64_t *__restrict__ cnt, const int32_t *__restrict__ own0,
+                                                    const int64_t *__restrict__ owner_off, uint32_t *__restrict__ perm) {
+    cg::grid_group grid = cg::this_grid();
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t n0 = levels > 0 ? starts[1] : 0;
+    for (int64_t i = tid; i < n0; i += stride) cnt[i] = owner_off[own0[i]];
+    grid.sync();
+    for (int l = 0; l < levels; l++) {
+        const int64_t b = starts[l], e = starts[l + 1];
+        for (int64_t i = b + tid; i < e; i += stride) {
+            const int64_t ln = links[i], off = cnt[i];
+            if (ln < 0) {
+                perm[off] = (uint32_t)~ln;
+            } else {
+                const int64_t right = cnt[ln + 1];
+                cnt[ln + 1] = off;
+                cnt[ln] = off + right;
+            }
+        }
+        grid.sync();
     }
 }
 
@@ -245,11 +289,10 @@ __global__ void k_gather_uv(const int2 *src, const uint32_t *perm, int64_t n, in
         dst[i] = src[perm[i]];
 }
 
-__global__ void k_count_owner(const int32_t *w, int64_t n, int64_t *counts) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x)
-        atomicAdd((unsigned long long *)&counts[w[i]], 1ull);
-}
+struct OwnerCount {  // the owners' counts in internal-node id order (0 for leaves)
+    const int64_t *full;
+    __device__ int64_t operator()(int64_t i) const { return full[i]; }
+};
 
 struct InternalFlag {
     const int2 *lr;
@@ -297,38 +340,40 @@ int wspd_run(Ctx &c, double s, int reference_order, int64_t *n_pairs, bool want_
     c.n_pairs = 0;
     c.wspd_levels = 0;
     const int ORDER = reference_order ? 1 : 0;
-    const size_t isz = ORDER ? sizeof(ItemO) : sizeof(ItemF);
     int64_t *ctr;
     W1G_TRY(ensure(c.scr[20], 8, &ctr));
     // capacity estimate (P/K ~ 6.5 + 0.95 s^2 on the benchmark sets)
     int64_t pair_cap = (int64_t)((double)K * (8.0 + 1.25 * s * s)) + 4096;
-    int64_t front_cap = pair_cap / 2 + 2 * K + 4096;
     const int64_t prev_pair_cap = (int64_t)(c.pair_uv.cap / sizeof(int2));
     if (prev_pair_cap > pair_cap) pair_cap = prev_pair_cap - 16;
+    // fused: two ping-pong frontiers; reference order: one array holding every
+    // level (the recursion forest has ~2P items)
+    int64_t front_cap = ORDER ? 2 * pair_cap + K + 4096 : pair_cap / 2 + 2 * K + 4096;
+    // the recursion depth is at most depth(u) + depth(v) <= 2 nn
+    const int64_t max_levels = 2 * nn + 8;
     for (int attempt = 0; attempt < 8; attempt++) {
         int2 *uv;
-        int32_t *w = nullptr;
-        uint64_t *p0 = nullptr, *p1 = nullptr;
-        void *fa, *fb;
+        ItemF *fa, *fb = nullptr;
+        int64_t *links = nullptr, *starts = nullptr;
+        int32_t *own0 = nullptr;
         W1G_TRY(ensure(c.pair_uv, (size_t)pair_cap, &uv));
+        W1G_TRY(ensure(c.scr[21], (size_t)front_cap + 8, &fa));
         if (ORDER) {
-            W1G_TRY(ensure(c.pair_w, (size_t)pair_cap, &w));
-            W1G_TRY(ensure(c.pair_path, (size_t)pair_cap * 2, &p0));
-            p1 = p0 + pair_cap;
+            W1G_TRY(ensure(c.scr[22], (size_t)front_cap + 8, &links));
+            W1G_TRY(ensure(c.scr[23], (size_t)max_levels + 8, &starts));
+            W1G_TRY(ensure(c.pair_w, (size_t)nn + 8, &own0));
+        } else {
+            W1G_TRY(ensure(c.scr[22], (size_t)front_cap + 8, &fb));
         }
-        W1G_TRY(ensure_bytes(c.scr[21], (size_t)front_cap * isz + 64));
-        W1G_TRY(ensure_bytes(c.scr[22], (size_t)front_cap * isz + 64));
-        fa = c.scr[21].p;
-        fb = c.scr[22].p;
         W1G_TRY(flags_reset(c));
         W1G_CUDA(cudaMemsetAsync(ctr, 0, sizeof(int64_t) * 8, c.stream));
         Counters k{ctr, ctr + 4, dflags(c)};
         const unsigned gi = grid_for(nn, 256, 8u * c.sm_count);
         if (nn > 1) {
             if (ORDER)
-                k_wspd_init_o<<<gi, 256, 0, c.stream>>>(ptr<int2>(c.t_lr), nn, (ItemO *)fa, front_cap, ctr);
+                k_wspd_init_o<<<gi, 256, 0, c.stream>>>(ptr<int2>(c.t_lr), nn, fa, own0, front_cap, ctr);
             else
-                k_wspd_init_f<<<gi, 256, 0, c.stream>>>(ptr<int2>(c.t_lr), nn, (ItemF *)fa, front_cap, ctr);
+                k_wspd_init_f<<<gi, 256, 0, c.stream>>>(ptr<int2>(c.t_lr), nn, fa, front_cap, ctr);
             W1G_CHECK_LAUNCH();
         }
         const unsigned gl = 8u * c.sm_count;
@@ -338,7 +383,7 @@ int wspd_run(Ctx &c, double s, int reference_order, int64_t *n_pairs, bool want_
         if (nn > 1) {
             // persistent cooperative launch: every level, one grid barrier each
             int per_sm = 0;
-            const void *fn = ORDER ? (const void *)k_wspd_coop<true> : (const void *)k_wspd_coop<false>;
+            const void *fn = ORDER ? (const void *)k_wspd_coop_o : (const void *)k_wspd_coop;
             W1G_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, 0));
             // fewer CTAs -> cheaper grid barriers; W1G_COOP_PER_SM overrides (tuning)
             {
@@ -346,19 +391,26 @@ int wspd_run(Ctx &c, double s, int reference_order, int64_t *n_pairs, bool want_
                 const int cap = e ? atoi(e) : 2;
                 if (per_sm > cap) per_sm = cap;
             }
+            if (ORDER && per_sm < 1) {
+                set_error("WSPD (reference order): cooperative launch unavailable");
+                return W1G_ECUDA;
+            }
             if (per_sm >= 1) {
                 const int G = per_sm * c.sm_count;
                 int32_t *lv = reinterpret_cast<int32_t *>(ctr + 6);
                 NodeGeom *geom = ptr<NodeGeom>(c.t_geom);
                 int2 *lr = ptr<int2>(c.t_lr);
                 int2 *uvp = uv;
-                int32_t *wp = w;
-                uint64_t *p0p = p0, *p1p = p1;
-                void *fap = fa, *fbp = fb;
-                int64_t fc = front_cap, pc = pair_cap;
+                ItemF *fap = fa, *fbp = fb;
+                int64_t fc = front_cap, pc = pair_cap, ml = max_levels;
                 double sv = s;
-                void *args[] = {&fap, &fbp, &fc, &k, &uvp, &wp, &p0p, &p1p, &pc, &sv, &geom, &lr, &lv};
-                W1G_CUDA(cudaLaunchCooperativeKernel(fn, G, 256, args, 0, c.stream));
+                if (ORDER) {
+                    void *args[] = {&fap, &fc, &k, &uvp, &links, &starts, &ml, &pc, &sv, &geom, &lr, &lv};
+                    W1G_CUDA(cudaLaunchCooperativeKernel(fn, G, 256, args, 0, c.stream));
+                } else {
+                    void *args[] = {&fap, &fbp, &fc, &k, &uvp, &pc, &sv, &geom, &lr, &lv};
+                    W1G_CUDA(cudaLaunchCooperativeKernel(fn, G, 256, args, 0, c.stream));
+                }
                 W1G_CHECK_LAUNCH();
                 W1G_CUDA(cudaMemcpyAsync(c.h_pinned + F_MISC0, ctr, sizeof(int64_t) * 8, cudaMemcpyDeviceToHost, c.stream));
                 W1G_CUDA(cudaMemcpyAsync(c.h_pinned + F_PAIR_OVF, dflags(c) + F_PAIR_OVF, sizeof(int64_t) * 5,
@@ -366,7 +418,7 @@ int wspd_run(Ctx &c, double s, int reference_order, int64_t *n_pairs, bool want_
                 W1G_TRY(stream_sync(c));
                 level = (int)(c.h_pinned[F_MISC0 + 6] & 0x7fffffff);
                 const int64_t live = c.h_pinned[F_MISC0 + level % 3];
-                if (c.h_pinned[F_FRONT_OVF] || live > front_cap) {
+                if (c.h_pinned[F_FRONT_OVF] || (!ORDER && live > front_cap)) {
                     ovf = true;
                     front_cap = front_cap * 2 + (live > front_cap ? live : 0);
                 }
@@ -375,15 +427,9 @@ int wspd_run(Ctx &c, double s, int reference_order, int64_t *n_pairs, bool want_
         }
         while (nn > 1 && !nn_done) {
             for (int b = 0; b < BATCH; b++, level++) {
-                void *cur = (level & 1) ? fb : fa, *nxt = (level & 1) ? fa : fb;
-                if (ORDER)
-                    k_wspd_level<true><<<gl, 256, 0, c.stream>>>((const ItemO *)cur, (ItemO *)nxt, front_cap, level, k,
-                                                                uv, w, p0, p1, pair_cap, s,
-                                                                ptr<NodeGeom>(c.t_geom), ptr<int2>(c.t_lr));
-                else
-                    k_wspd_level<false><<<gl, 256, 0, c.stream>>>((const ItemF *)cur, (ItemF *)nxt, front_cap, level, k,
-                                                                 uv, nullptr, nullptr, nullptr, pair_cap, s,
-                                                                 ptr<NodeGeom>(c.t_geom), ptr<int2>(c.t_lr));
+                ItemF *cur = (level & 1) ? fb : fa, *nxt = (level & 1) ? fa : fb;
+                k_wspd_level<<<gl, 256, 0, c.stream>>>(cur, nxt, front_cap, level, k, uv, pair_cap, s,
+                                                       ptr<NodeGeom>(c.t_geom), ptr<int2>(c.t_lr));
                 W1G_CHECK_LAUNCH();
             }
             W1G_CUDA(cudaMemcpyAsync(c.h_pinned + F_MISC0, ctr, sizeof(int64_t) * 8, cudaMemcpyDeviceToHost, c.stream));
@@ -409,11 +455,6 @@ int wspd_run(Ctx &c, double s, int reference_order, int64_t *n_pairs, bool want_
             pair_cap = P + P / 8 + 1024;
         }
         if (ovf) continue;
-        if (ORDER && c.h_pinned[F_PATH_OVF]) {
-            set_error("WSPD recursion deeper than 128 levels: the reference pair order is not "
-                      "representable (use reference_order=0)");
-            return W1G_EINVAL;
-        }
         c.wspd_levels = level;
         c.n_pairs = P;
         *n_pairs = P;
@@ -422,33 +463,50 @@ int wspd_run(Ctx &c, double s, int reference_order, int64_t *n_pairs, bool want_
                 set_error("too many pairs to order");
                 return W1G_EINVAL;
             }
-            uint64_t *k0, *k1, *k2;
-            uint32_t *vals;
+            // count_pairs (bottom-up leaf counts), build_wspd's offsets (a scan over the
+            // owners in id order) and write_pairs' layout (top-down offsets)
+            auto coop_grid = [&](const void *fn) {
+                int per = 0;
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, 256, 0);
+                return (per > 2 ? 2 : (per < 1 ? 1 : per)) * c.sm_count;
+            };
+            int64_t *cnt, *full, *excl, *out;
+            uint32_t *perm;
             int2 *uv2;
-            W1G_TRY(ensure(c.scr[0], P, &k0));
-            W1G_TRY(ensure(c.scr[1], P, &k1));
-            W1G_TRY(ensure(c.scr[4], P, &k2));
-            W1G_TRY(ensure(c.scr[2], P, &vals));
-            const unsigned gp = grid_for(P, 256, 8u * c.sm_count);
-            k_order_keys<<<gp, 256, 0, c.stream>>>(w, p0, p1, P, k0, k1, k2, vals);
-            W1G_CHECK_LAUNCH();
-            uint64_t *keys[3] = {k0, k1, k2};
-            W1G_TRY(radix_sort(c, keys, 3, vals, P, 32));
-            W1G_TRY(ensure(c.scr[5], P, &uv2));
-            k_gather_uv<<<gp, 256, 0, c.stream>>>(uv, vals, P, uv2);
-            W1G_CHECK_LAUNCH();
-            W1G_CUDA(cudaMemcpyAsync(uv, uv2, sizeof(int2) * P, cudaMemcpyDeviceToDevice, c.stream));
-            // count_pairs: pairs per internal node, internal nodes in id order
-            int64_t *full, *excl, *out;
+            W1G_TRY(ensure(c.scr[0], (size_t)front_cap + 8, &cnt));
             W1G_TRY(ensure(c.scr[6], nn + 1, &full));
             W1G_TRY(ensure(c.scr[3], nn + 1, &excl));
             W1G_TRY(ensure(c.pair_counts, nn / 2 + 1, &out));
+            W1G_TRY(ensure(c.scr[2], P + 1, &perm));
             W1G_CUDA(cudaMemsetAsync(full, 0, sizeof(int64_t) * (nn + 1), c.stream));
-            k_count_owner<<<gp, 256, 0, c.stream>>>(w, P, full);
-            W1G_CHECK_LAUNCH();
-            W1G_TRY(scan_i64(c, InternalFlag{ptr<int2>(c.t_lr)}, nn, excl, nullptr));
+            if (nn > 1 && level > 0) {
+                int lv = level;
+                void *up[] = {&links, &starts, &lv, &cnt, &own0, &full};
+                W1G_CUDA(cudaLaunchCooperativeKernel((const void *)k_order_up, coop_grid((const void *)k_order_up), 256,
+                                                     up, 0, c.stream));
+                W1G_CHECK_LAUNCH();
+            }
+            W1G_TRY(scan_i64(c, OwnerCount{full}, nn, excl, nullptr));
+            if (nn > 1 && level > 0) {
+                int lv = level;
+                void *down[] = {&links, &starts, &lv, &cnt, &own0, &excl, &perm};
+                W1G_CUDA(cudaLaunchCooperativeKernel((const void *)k_order_down, coop_grid((const void *)k_order_down),
+                                                     256, down, 0, c.stream));
+                W1G_CHECK_LAUNCH();
+            }
+            const unsigned gp = grid_for(P, 256, 8u * c.sm_count);
+            W1G_TRY(ensure(c.scr[5], P + 1, &uv2));
+            if (P) {
+                k_gather_uv<<<gp, 256, 0, c.stream>>>(uv, perm, P, uv2);
+                W1G_CHECK_LAUNCH();
+                W1G_CUDA(cudaMemcpyAsync(uv, uv2, sizeof(int2) * P, cudaMemcpyDeviceToDevice, c.stream));
+            }
+            // count_pairs: pairs per internal node, internal nodes in id order
+            int64_t *iexcl;
+            W1G_TRY(ensure(c.scr[4], nn + 1, &iexcl));
+            W1G_TRY(scan_i64(c, InternalFlag{ptr<int2>(c.t_lr)}, nn, iexcl, nullptr));
             k_compact_counts<<<grid_for(nn, 256, 8u * c.sm_count), 256, 0, c.stream>>>(ptr<int2>(c.t_lr), full,
-                                                                                       excl, nn, out);
+                                                                                       iexcl, nn, out);
             W1G_CHECK_LAUNCH();
         }
         c.pairs_valid = true;

@@ -247,12 +247,27 @@ def pairwise_w1(diagrams, params: ApproxParams, devices=None, solver_threads: in
     pool = ThreadPoolExecutor(max_workers=solver_threads)
     futures = []
     lock = threading.Lock()
+    # every queued network holds a page-locked result block until it is solved:
+    # bound the networks in flight so fast front ends cannot pin host memory
+    # without limit while the (much slower) host solver drains the queue
+    in_flight = threading.BoundedSemaphore(2 * solver_threads + len(devs) * max(1, streams_per_device))
+
+    def solve_one(net, diag):
+        try:
+            return solve_network(net, params, diag)
+        finally:
+            in_flight.release()
 
     def on_network(i, j, net, diag):
         if net is None:
             out[i, j] = out[j, i] = 0.0
             return
-        f = pool.submit(solve_network, net, params, diag)
+        in_flight.acquire()
+        try:
+            f = pool.submit(solve_one, net, diag)
+        except BaseException:
+            in_flight.release()
+            raise
         with lock:
             futures.append((i, j, f))
 

@@ -90,7 +90,18 @@ def save(name, a, b, s, delta=None, seed=0, w1=False, **extra):
     print(name, {k: v.shape for k, v in out.items() if hasattr(v, "shape") and v.ndim})
 
 
+def deep_cases():
+    """Inputs whose WSPD recursion is far deeper than 128 levels (the reference's
+    explicit stack has no limit, spanner.py:206-241): births +-2^-i, deaths b+1."""
+    P = PersistenceDiagram
+    births = np.array([sg * 2.0 ** -i for i in range(100) for sg in (1.0, -1.0)])
+    deep = P(np.stack([births, births + 1.0], axis=1))
+    save("deep_pm2i", deep, P([(0.5, 1.5)]), 2.0, delta=0.0)
+    save("deep_pm2i_s8", deep, P([(0.25, 2.5), (0.0, 1.0)]), 8.0, delta=0.0)
+
+
 def main():
+    deep_cases()
     # cfg1: BASELINE.json configs[0] -- 1k points each, s=1, delta=0.01
     a, b = synth.gaussian_cluster_pair(1000, 1000, seed=0)
     save("cfg1_s1_d001", a, b, 1.0, delta=0.01)
@@ -172,4 +183,7 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["deep"]:
+        deep_cases()
+    else:
+        main()
