@@ -36,6 +36,7 @@ extern "C" {
 #define W1G_ENETWORK (-6)   /* build_network validation, network.py:56-68 (NetworkError) */
 #define W1G_ENOMEM (-7)     /* device allocation failed (MemoryError) */
 #define W1G_ESTATE (-8)     /* stage called before its inputs exist (RuntimeError) */
+#define W1G_DONE 1          /* w1g_batch_next: every result has been delivered */
 
 /* node-set slots held by a context */
 #define W1G_NODES0 0 /* output of zero_condense */
@@ -117,6 +118,11 @@ int w1g_set_rwmd_culling(w1g_ctx *ctx, int enabled);
 int w1g_delta_condense(w1g_ctx *ctx, double delta, double pitch, double half_width,
                        uint64_t seed, int64_t *k);
 
+/* replaces condensation.snap_points, condensation.py:66-77: cells = round-half-away(p / pitch)
+ * (int64, (n,2)), snapped = cells * pitch; W1G_EOVERFLOW when |cell| >= 2^62 */
+int w1g_snap_points(w1g_ctx *ctx, const double *points, int64_t n, double pitch, double *snapped,
+                    int64_t *cells);
+
 /* replaces spanner.build_split_tree, spanner.py:96-159, over a slot's points */
 int w1g_split_tree(w1g_ctx *ctx, int slot, int64_t *n_nodes, int32_t *depth);
 int w1g_fetch_tree(w1g_ctx *ctx, int64_t *left, int64_t *right, double *bbox, int64_t *rep,
@@ -164,6 +170,64 @@ int w1g_front_end(w1g_ctx *ctx, const double *a, int64_t na, const double *b, in
 int w1g_front_end_device(w1g_ctx *ctx, const double *d_a, int64_t na, const double *d_b,
                          int64_t nb, double s, int use_condensation, int delta_mode,
                          double delta, double k, uint64_t seed, w1g_front_end_info *info);
+
+/* ---- batched front ends: the pairwise matrix (cfg4) and any pair list ----
+ * The reference computes a batch as a loop of approx_w1 over pairs;
+ * here one call runs the loop natively: the diagrams come from the context's
+ * corpus (w1g_corpus_load, uploaded once), `streams` worker threads each drive
+ * a child context (own stream, scratch, RWMD side context) and pull pairs from
+ * a shared counter.  pairs = n_pairs (i, j) int32 index pairs. */
+
+/* synchronous: every front end runs, networks stay in device memory; infos
+ * (n_pairs entries, may be null) receives each pair's diagnostics */
+int w1g_front_end_batch(w1g_ctx *ctx, const int32_t *pairs, int64_t n_pairs, double s, int use_condensation,
+                        int delta_mode, double delta, double k, uint64_t seed, int streams,
+                        w1g_front_end_info *infos);
+
+/* one delivered network: host arrays inside a page-locked block owned by the
+ * library until w1g_batch_release(block); status != W1G_OK carries the pair's error */
+typedef struct {
+    int64_t pair;             /* index into the pair list */
+    int32_t i, j;             /* diagram indices */
+    int32_t status;           /* W1G_OK or the pair's error code */
+    int32_t pad;
+    w1g_front_end_info info;  /* info.short_circuit: no network (W1 = 0) */
+    int64_t *supplies, *tails, *heads, *row_offsets;  /* node_count, n_arcs, n_arcs, node_count + 1 */
+    double *costs;            /* n_arcs */
+    void *block;
+    char message[256];
+} w1g_batch_result;
+
+/* asynchronous: start the batch; networks are copied out into pooled page-locked
+ * blocks (at most max_inflight_bytes held by results not yet released; <= 0 keeps
+ * the current limit, 8 GiB by default) */
+int w1g_batch_begin(w1g_ctx *ctx, const int32_t *pairs, int64_t n_pairs, double s, int use_condensation,
+                    int delta_mode, double delta, double k, uint64_t seed, int streams,
+                    int64_t max_inflight_bytes);
+/* the next finished pair (completion order); blocks; W1G_DONE when all are delivered */
+int w1g_batch_next(w1g_ctx *ctx, w1g_batch_result *out);
+/* give a result's block back to the pool (thread-safe, any thread) */
+int w1g_batch_release(void *block);
+/* stop (cancel what has not started) and join the workers; undelivered blocks are released */
+int w1g_batch_end(w1g_ctx *ctx);
+
+/* ---- retrieval (pipeline.py:146-243 nn_search) and the exact oracle (oracle.py:66-108) ---- */
+
+/* upload a diagram corpus once: points of all diagrams back to back ((total,2)
+ * float64), diagram i = rows [offsets[i], offsets[i+1]) (n_diagrams + 1 offsets) */
+int w1g_corpus_load(w1g_ctx *ctx, const double *points, const int64_t *offsets, int64_t n_diagrams);
+/* replaces lower_bound.wcd (lower_bound.py:78-92) for query vs corpus[candidates[i]],
+ * all candidates in one launch: scores[i] = wcd(query, corpus[candidates[i]]) bit for bit */
+int w1g_wcd_corpus(w1g_ctx *ctx, const double *query, int64_t nq, const int64_t *candidates,
+                   int64_t n_candidates, double *scores);
+/* the RWMD stage of nn_search (pipeline.py:202-203): scores[i] =
+ * rwmd(zero_condense(query, corpus[candidates[i]])), device zero_condense + RWMD per candidate */
+int w1g_rwmd_corpus(w1g_ctx *ctx, const double *query, int64_t nq, const int64_t *candidates,
+                    int64_t n_candidates, double *scores);
+/* replaces oracle.dense_network (oracle.py:66-93) over slot W1G_NODES0: the complete
+ * A-member x B-member network plus the diagonal arcs, already in CSR order; fetch it
+ * with w1g_fetch_network.  The caller applies the DENSE_ARC_LIMIT guard (oracle.py:71-72). */
+int w1g_dense_network(w1g_ctx *ctx, int64_t *node_count, int64_t *n_arcs);
 
 #ifdef __cplusplus
 }

@@ -66,6 +66,28 @@ class FrontEndInfo(ctypes.Structure):
     ]
 
 
+class BatchResult(ctypes.Structure):
+    """w1g_batch_result (include/w1g.h)."""
+
+    _fields_ = [
+        ("pair", _i64),
+        ("i", _i32),
+        ("j", _i32),
+        ("status", _i32),
+        ("pad", _i32),
+        ("info", FrontEndInfo),
+        ("supplies", _vp),
+        ("tails", _vp),
+        ("heads", _vp),
+        ("row_offsets", _vp),
+        ("costs", _vp),
+        ("block", _vp),
+        ("message", ctypes.c_char * 256),
+    ]
+
+
+W1G_DONE = 1
+
 STAGES = ("zero_condense", "rwmd", "delta_condense", "split_tree", "wspd", "emit_arcs", "assemble", "total")
 
 # (name, restype, argtypes)
@@ -92,6 +114,7 @@ _PROTOS = [
     ("w1g_set_rwmd_culling", ctypes.c_int, [_vp, ctypes.c_int]),
     ("w1g_rwmd_range", ctypes.c_int, [_vp, ctypes.c_int, _i64, _i64, _F64P, _I64P]),
     ("w1g_delta_condense", ctypes.c_int, [_vp, _f64, _f64, _f64, _u64, _I64P]),
+    ("w1g_snap_points", ctypes.c_int, [_vp, _F64P, _i64, _f64, _F64P, _I64P]),
     ("w1g_split_tree", ctypes.c_int, [_vp, ctypes.c_int, _I64P, _I32P]),
     ("w1g_fetch_tree", ctypes.c_int, [_vp, _I64P, _I64P, _F64P, _I64P, _I64P]),
     ("w1g_load_tree", ctypes.c_int, [_vp, _F64P, _i64, _I64P, _I64P, _F64P, _I64P, _i64]),
@@ -112,6 +135,17 @@ _PROTOS = [
     ("w1g_front_end_device", ctypes.c_int,
      [_vp, _vp, _i64, _vp, _i64, _f64, ctypes.c_int, ctypes.c_int, _f64, _f64, _u64,
       ctypes.POINTER(FrontEndInfo)]),
+    ("w1g_front_end_batch", ctypes.c_int,
+     [_vp, _vp, _i64, _f64, ctypes.c_int, ctypes.c_int, _f64, _f64, _u64, ctypes.c_int, ctypes.POINTER(FrontEndInfo)]),
+    ("w1g_batch_begin", ctypes.c_int,
+     [_vp, _vp, _i64, _f64, ctypes.c_int, ctypes.c_int, _f64, _f64, _u64, ctypes.c_int, _i64]),
+    ("w1g_batch_next", ctypes.c_int, [_vp, ctypes.POINTER(BatchResult)]),
+    ("w1g_batch_release", ctypes.c_int, [_vp]),
+    ("w1g_batch_end", ctypes.c_int, [_vp]),
+    ("w1g_corpus_load", ctypes.c_int, [_vp, _F64P, _I64P, _i64]),
+    ("w1g_wcd_corpus", ctypes.c_int, [_vp, _F64P, _i64, _I64P, _i64, _F64P]),
+    ("w1g_rwmd_corpus", ctypes.c_int, [_vp, _F64P, _i64, _I64P, _i64, _F64P]),
+    ("w1g_dense_network", ctypes.c_int, [_vp, _I64P, _I64P]),
 ]
 
 EXPORTED = tuple(name for name, _, _ in _PROTOS)
@@ -144,7 +178,11 @@ class NetworkError(ValueError):
 
 
 def _raise(code: int):
-    msg = load().w1g_last_error().decode(errors="replace")
+    raise_code(code, load().w1g_last_error().decode(errors="replace"))
+
+
+def raise_code(code: int, msg: str):
+    """The reference's exception type for a library error code."""
     if code in (W1G_EINVAL, W1G_EOVERFLOW, W1G_EDUPLICATE):
         raise ValueError(msg)
     if code == W1G_ENETWORK:
@@ -305,3 +343,37 @@ def addr(a: np.ndarray) -> int:
 
 def launch_count() -> int:
     return int(load().w1g_launch_count())
+
+
+class _BlockHolder:
+    """Owner of one batch result block (w1g_batch_result.block): the numpy arrays
+    viewing it keep it alive; when the last one dies the block goes back to the
+    library's pool (w1g_batch_release)."""
+
+    __slots__ = ("block", "__array_interface__")
+
+    def __init__(self, block: int, nbytes: int):
+        self.block = block
+        self.__array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (block, False), "version": 3}
+
+    def __del__(self):
+        try:
+            load().w1g_batch_release(ctypes.c_void_p(self.block))
+        except Exception:
+            pass
+
+
+def result_arrays(r: "BatchResult"):
+    """(supplies, tails, heads, costs, row_offsets) numpy views of a delivered
+    network, zero-copy over its page-locked block."""
+    n, m = int(r.info.node_count), int(r.info.n_arcs)
+    lo = r.block
+    hi = max(r.supplies + 8 * n, r.tails + 8 * m, r.heads + 8 * m, r.costs + 8 * m, r.row_offsets + 8 * (n + 1))
+    base = np.asarray(_BlockHolder(lo, hi - lo))
+
+    def view(addr_, count, dtype):
+        off = addr_ - lo
+        return base[off:off + count * 8].view(dtype)
+
+    return (view(r.supplies, n, np.int64), view(r.tails, m, np.int64), view(r.heads, m, np.int64),
+            view(r.costs, m, np.float64), view(r.row_offsets, n + 1, np.int64))

@@ -13,6 +13,8 @@ import ctypes
 import math
 from dataclasses import dataclass
 
+import numpy as np
+
 from . import _lib
 from .diagram import SuppliedNodes, fetch_nodes, load_nodes
 
@@ -46,6 +48,28 @@ def compute_delta(epsilon: float, lower_bound: float, n_points: int) -> float:
     if lower_bound < 0:
         raise ValueError("lower bound must be nonnegative")
     return 2.0 * epsilon * lower_bound / (_SQRT2 * n_points)
+
+
+def snap_points(points, delta: float, k: float, device: int | None = None) -> tuple[np.ndarray, np.ndarray]:
+    """Snap points to the k*delta lattice, round half away from zero
+    (condensation.py:66-77), on device: cells = sign(t) floor(|t| + 0.5) with
+    t = p / pitch, snapped = cells * pitch.  Returns (snapped, int64 cells)."""
+    if delta <= 0:
+        raise ValueError("delta must be positive")
+    pitch = k * delta
+    pts = _lib.as_points(points)
+    n = pts.shape[0]
+    snapped = np.empty((n, 2), dtype=np.float64)
+    cells = np.empty((n, 2), dtype=np.int64)
+    ctx = _lib.context(device)
+    ctx.call("w1g_snap_points", _lib.f64p(pts), n, float(pitch), _lib.f64p(snapped), _lib.i64p(cells))
+    return snapped, cells
+
+
+def snap_point(p, delta: float, k: float = 0.99) -> tuple[float, float]:
+    """condensation.py:80-82."""
+    snapped, _ = snap_points(np.asarray(p, dtype=np.float64).reshape(1, 2), delta, k)
+    return (float(snapped[0, 0]), float(snapped[0, 1]))
 
 
 def delta_condense(nodes: SuppliedNodes, params: CondensationParams,

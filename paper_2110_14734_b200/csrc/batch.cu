@@ -1,0 +1,382 @@
+// batch.cu -- the native batch executor: the sparsify front end of many
+// diagram pairs per library call (the pairwise W1 matrix of cfg4, and any
+// pair list), with no Python in the per-pair loop.
+//
+// The reference's CPU baseline for this workload is a loop of approx_w1 over
+// the i < j pairs; the drop-in's pairwise_w1 / sparsify_batch
+// run it as:
+//   * the diagrams are uploaded once per device (w1g_corpus_load);
+//   * `streams` worker threads, each driving its own child context (own CUDA
+//     stream, scratch and RWMD side context), pull pair indices from a shared
+//     atomic counter -- latency-bound front ends of small diagrams overlap on
+//     one GPU;
+//   * each network is copied out inside its front end call into a page-locked
+//     block from a process-wide pool, and queued for the consumer
+//     (w1g_batch_next), which hands it to the host solver and releases the
+//     block when the arrays die (w1g_batch_release).  The pool bounds the bytes
+//     in flight, so a fast front end cannot pin host memory without limit while
+//     the solver drains the queue (workers wait for a block instead).
+//   * w1g_front_end_batch is the synchronous variant that leaves every network
+//     in device memory (front-end throughput, and the per-pair diagnostics).
+#include <atomic>
+#include <cstring>
+#include <deque>
+#include <map>
+#include <unordered_map>
+#include <vector>
+
+#include "common.cuh"
+
+namespace w1g {
+
+// ---------------------------------------------------------------- page-locked result blocks
+
+namespace {
+
+struct HostPool {
+    std::mutex mu;
+    std::condition_variable cv;
+    std::map<size_t, std::vector<void *>> free_blocks;  // by size class
+    std::unordered_map<void *, size_t> cls_of;
+    size_t in_flight = 0;
+    size_t limit = (size_t)8 << 30;
+
+    static size_t size_class(size_t b) {
+        size_t c = (size_t)1 << 20;
+        while (c < b) c <<= 1;
+        return c;
+    }
+    // a block of at least `bytes`; waits while the bytes in flight exceed the limit
+    // (unless nothing is in flight: one oversized network must still go through)
+    int get(size_t bytes, void **out, const std::atomic<bool> *cancel) {
+        const size_t cls = size_class(bytes);
+        std::unique_lock<std::mutex> lk(mu);
+        cv.wait(lk, [&] { return in_flight == 0 || in_flight + cls <= limit || (cancel && cancel->load()); });
+        if (cancel && cancel->load()) {
+            set_error("batch cancelled");
+            return W1G_ESTATE;
+        }
+        in_flight += cls;
+        auto &fl = free_blocks[cls];
+        if (!fl.empty()) {
+            *out = fl.back();
+            fl.pop_back();
+            return W1G_OK;
+        }
+        lk.unlock();
+        void *p = nullptr;
+        const cudaError_t e = cudaHostAlloc(&p, cls, cudaHostAllocPortable);
+        lk.lock();
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            in_flight -= cls;
+            cv.notify_all();
+            set_error("cudaHostAlloc of %zu bytes failed", cls);
+            return W1G_ENOMEM;
+        }
+        cls_of[p] = cls;
+        *out = p;
+        return W1G_OK;
+    }
+    void put(void *p) {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = cls_of.find(p);
+        if (it == cls_of.end()) return;
+        in_flight -= it->second;
+        auto &fl = free_blocks[it->second];
+        if (fl.size() < 16) {
+            fl.push_back(p);
+        } else {
+            cls_of.erase(it);
+            cudaFreeHost(p);
+        }
+        cv.notify_all();
+    }
+    void wake() { cv.notify_all(); }
+};
+
+HostPool &host_pool() {
+    static HostPool *pool = new HostPool();  // process lifetime: blocks may outlive contexts
+    return *pool;
+}
+
+// carve the five network arrays out of a block laid out for (ncap nodes, mcap arcs)
+struct NetCarve {
+    int64_t *sup, *t, *h, *ro;
+    double *c;
+};
+inline size_t al64(size_t x) { return (x + 63) & ~(size_t)63; }
+inline size_t carve_bytes(int64_t ncap, int64_t mcap) {
+    return al64(8 * (size_t)ncap) + 3 * al64(8 * (size_t)mcap) + al64(8 * (size_t)(ncap + 1));
+}
+NetCarve carve(void *blk, int64_t ncap, int64_t mcap) {
+    char *p = static_cast<char *>(blk);
+    NetCarve r;
+    r.sup = reinterpret_cast<int64_t *>(p);
+    p += al64(8 * (size_t)ncap);
+    r.t = reinterpret_cast<int64_t *>(p);
+    p += al64(8 * (size_t)mcap);
+    r.h = reinterpret_cast<int64_t *>(p);
+    p += al64(8 * (size_t)mcap);
+    r.c = reinterpret_cast<double *>(p);
+    p += al64(8 * (size_t)mcap);
+    r.ro = reinterpret_cast<int64_t *>(p);
+    return r;
+}
+
+}  // namespace
+
+struct BatchParams {
+    double s, delta, k;
+    int use_condensation, delta_mode;
+    uint64_t seed;
+};
+
+struct BatchState {
+    std::vector<w1g_ctx *> kids;
+    std::vector<int64_t> hint_n, hint_m;  // per child: the last network's size (output block sizing)
+    std::vector<std::thread> threads;
+    std::vector<int32_t> pairs;
+    int64_t n_pairs = 0;
+    BatchParams prm{};
+    bool deliver = false;
+    w1g_front_end_info *infos = nullptr;  // synchronous variant
+    std::atomic<int64_t> next{0};
+    std::atomic<bool> cancel{false};
+    std::mutex mu;
+    std::condition_variable cv;
+    std::deque<w1g_batch_result> ready;
+    int64_t delivered = 0;  // results handed to the consumer
+    int64_t produced = 0;   // results queued (or recorded) by the workers
+    int first_rc = W1G_OK;
+    std::string first_err;
+    bool active = false;
+};
+
+static void batch_join(BatchState &b) {
+    for (auto &t : b.threads)
+        if (t.joinable()) t.join();
+    b.threads.clear();
+}
+
+static int ensure_kids(Ctx &c, BatchState &b, int streams) {
+    while ((int)b.kids.size() < streams) {
+        w1g_ctx *x = nullptr;
+        W1G_TRY(w1g_ctx_create(c.device, &x));
+        b.kids.push_back(x);
+        b.hint_n.push_back(0);
+        b.hint_m.push_back(0);
+    }
+    return W1G_OK;
+}
+
+// one worker: pairs from the shared counter, front end on its own child context
+static void batch_worker(Ctx *parent, BatchState *b, int w) {
+    w1g_ctx *x = b->kids[w];
+    const double2 *corpus = ptr<double2>(parent->corpus_pts);
+    const int64_t *off = parent->h_corpus_off;
+    cudaSetDevice(x->device);
+    for (;;) {
+        if (b->cancel.load()) break;
+        const int64_t p = b->next.fetch_add(1);
+        if (p >= b->n_pairs) break;
+        const int32_t i = b->pairs[2 * p], j = b->pairs[2 * p + 1];
+        w1g_batch_result r;
+        memset(&r, 0, sizeof r);
+        r.pair = p;
+        r.i = i;
+        r.j = j;
+        void *blk = nullptr;
+        int64_t ncap = 0, mcap = 0;
+        int rc = W1G_OK;
+        if (b->deliver && b->hint_m[w] > 0) {
+            ncap = b->hint_n[w] + b->hint_n[w] / 8 + 64;
+            mcap = b->hint_m[w] + b->hint_m[w] / 8 + 1024;
+            rc = host_pool().get(carve_bytes(ncap, mcap), &blk, &b->cancel);
+            if (rc == W1G_OK) {
+                NetCarve cv = carve(blk, ncap, mcap);
+                rc = w1g_set_network_out(x, cv.sup, cv.t, cv.h, cv.c, cv.ro, ncap, mcap);
+            }
+        }
+        const double *pa = reinterpret_cast<const double *>(corpus + off[i]);
+        const double *pb = reinterpret_cast<const double *>(corpus + off[j]);
+        if (rc == W1G_OK)
+            rc = w1g_front_end_device(x, pa, off[i + 1] - off[i], pb, off[j + 1] - off[j], b->prm.s,
+                                      b->prm.use_condensation, b->prm.delta_mode, b->prm.delta, b->prm.k,
+                                      b->prm.seed, &r.info);
+        if (rc == W1G_OK && b->deliver && !r.info.short_circuit) {
+            const int64_t n = r.info.node_count, m = r.info.n_arcs;
+            b->hint_n[w] = n;
+            b->hint_m[w] = m;
+            if (!r.info.network_copied) {  // no block yet, or it was too small: exact size, fetched
+                if (blk) host_pool().put(blk);
+                blk = nullptr;
+                ncap = n;
+                mcap = m;
+                rc = host_pool().get(carve_bytes(ncap, mcap), &blk, &b->cancel);
+                if (rc == W1G_OK) {
+                    NetCarve cv = carve(blk, ncap, mcap);
+                    rc = w1g_fetch_network(x, cv.sup, cv.t, cv.h, cv.c, cv.ro);
+                }
+            }
+            if (rc == W1G_OK) {
+                NetCarve cv = carve(blk, ncap, mcap);
+                r.supplies = cv.sup;
+                r.tails = cv.t;
+                r.heads = cv.h;
+                r.costs = cv.c;
+                r.row_offsets = cv.ro;
+                r.block = blk;
+                blk = nullptr;
+            }
+        }
+        if (blk) host_pool().put(blk);  // short circuit or error: nothing to hand over
+        r.status = rc;
+        if (rc != W1G_OK) snprintf(r.message, sizeof r.message, "%s", w1g_last_error());
+        {
+            std::lock_guard<std::mutex> lk(b->mu);
+            if (rc != W1G_OK && b->first_rc == W1G_OK) {
+                b->first_rc = rc;
+                b->first_err = r.message;
+            }
+            if (b->infos) b->infos[p] = r.info;
+            if (b->deliver) b->ready.push_back(r);
+            b->produced++;
+        }
+        b->cv.notify_all();
+        if (rc != W1G_OK) {
+            b->cancel.store(true);  // like the reference's loop: the first error ends the batch
+            host_pool().wake();
+        }
+    }
+}
+
+static int batch_start(Ctx &c, const int32_t *pairs, int64_t n_pairs, const BatchParams &prm, int streams,
+                       bool deliver, w1g_front_end_info *infos) {
+    if (c.corpus_n < 0) {
+        set_error("batch: no diagrams loaded (w1g_corpus_load)");
+        return W1G_ESTATE;
+    }
+    if (n_pairs < 0 || (n_pairs && !pairs) || streams < 1 || streams > 64) {
+        set_error("batch: bad arguments");
+        return W1G_EINVAL;
+    }
+    for (int64_t p = 0; p < 2 * n_pairs; p++)
+        if (pairs[p] < 0 || pairs[p] >= c.corpus_n) {
+            set_error("batch: diagram index %d out of range [0, %lld)", pairs[p], (long long)c.corpus_n);
+            return W1G_EINVAL;
+        }
+    if (!c.batch) c.batch = new BatchState();
+    BatchState &b = *c.batch;
+    if (b.active) {
+        set_error("batch: a batch is already running on this context");
+        return W1G_ESTATE;
+    }
+    W1G_TRY(ensure_kids(c, b, streams));
+    W1G_CUDA(cudaStreamSynchronize(c.stream));  // the corpus upload is complete
+    b.pairs.assign(pairs, pairs + 2 * n_pairs);
+    b.n_pairs = n_pairs;
+    b.prm = prm;
+    b.deliver = deliver;
+    b.infos = infos;
+    b.next.store(0);
+    b.cancel.store(false);
+    b.ready.clear();
+    b.delivered = b.produced = 0;
+    b.first_rc = W1G_OK;
+    b.first_err.clear();
+    b.active = true;
+    const int nt = (int)(n_pairs < streams ? (n_pairs > 0 ? n_pairs : 1) : streams);
+    for (int w = 0; w < nt; w++) b.threads.emplace_back(batch_worker, &c, &b, w);
+    return W1G_OK;
+}
+
+void batch_destroy(Ctx &c) {
+    if (!c.batch) return;
+    BatchState &b = *c.batch;
+    b.cancel.store(true);
+    host_pool().wake();
+    batch_join(b);
+    for (auto &r : b.ready)
+        if (r.block) host_pool().put(r.block);
+    for (w1g_ctx *x : b.kids) w1g_ctx_destroy(x);
+    delete c.batch;
+    c.batch = nullptr;
+}
+
+}  // namespace w1g
+
+using namespace w1g;
+
+extern "C" {
+
+int w1g_front_end_batch(w1g_ctx *c, const int32_t *pairs, int64_t n_pairs, double s, int use_condensation,
+                        int delta_mode, double delta, double k, uint64_t seed, int streams,
+                        w1g_front_end_info *infos) {
+    if (!c) return W1G_EINVAL;
+    cudaSetDevice(c->device);
+    BatchParams prm{s, delta, k, use_condensation, delta_mode, seed};
+    W1G_TRY(batch_start(*c, pairs, n_pairs, prm, streams, false, infos));
+    BatchState &b = *c->batch;
+    batch_join(b);
+    b.active = false;
+    for (w1g_ctx *x : b.kids) W1G_CUDA(cudaStreamSynchronize(x->stream));
+    if (b.first_rc != W1G_OK) {
+        set_error("%s", b.first_err.c_str());
+        return b.first_rc;
+    }
+    return W1G_OK;
+}
+
+int w1g_batch_begin(w1g_ctx *c, const int32_t *pairs, int64_t n_pairs, double s, int use_condensation,
+                    int delta_mode, double delta, double k, uint64_t seed, int streams,
+                    int64_t max_inflight_bytes) {
+    if (!c) return W1G_EINVAL;
+    cudaSetDevice(c->device);
+    if (max_inflight_bytes > 0) {
+        std::lock_guard<std::mutex> lk(host_pool().mu);
+        host_pool().limit = (size_t)max_inflight_bytes;
+    }
+    BatchParams prm{s, delta, k, use_condensation, delta_mode, seed};
+    return batch_start(*c, pairs, n_pairs, prm, streams, true, nullptr);
+}
+
+int w1g_batch_next(w1g_ctx *c, w1g_batch_result *out) {
+    if (!c || !out || !c->batch || !c->batch->active) {
+        set_error("batch_next: no batch running");
+        return W1G_ESTATE;
+    }
+    BatchState &b = *c->batch;
+    std::unique_lock<std::mutex> lk(b.mu);
+    b.cv.wait(lk, [&] {
+        return !b.ready.empty() || b.produced >= b.n_pairs || (b.cancel.load() && b.first_rc != W1G_OK);
+    });
+    if (!b.ready.empty()) {
+        *out = b.ready.front();
+        b.ready.pop_front();
+        b.delivered++;
+        return W1G_OK;
+    }
+    return W1G_DONE;
+}
+
+int w1g_batch_release(void *block) {
+    if (block) host_pool().put(block);
+    return W1G_OK;
+}
+
+int w1g_batch_end(w1g_ctx *c) {
+    if (!c || !c->batch) return W1G_OK;
+    BatchState &b = *c->batch;
+    b.cancel.store(true);
+    host_pool().wake();
+    batch_join(b);
+    for (auto &r : b.ready)
+        if (r.block) host_pool().put(r.block);
+    b.ready.clear();
+    b.active = false;
+    for (w1g_ctx *x : b.kids) cudaStreamSynchronize(x->stream);
+    return W1G_OK;
+}
+
+}  // extern "C"

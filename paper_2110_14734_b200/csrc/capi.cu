@@ -263,6 +263,7 @@ int w1g_ctx_destroy(w1g_ctx *c) {
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
     if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
+    batch_destroy(*c);
     if (c->aux_worker) {
         c->aux_worker->stop();
         delete c->aux_worker;
@@ -290,6 +291,10 @@ int w1g_ctx_destroy(w1g_ctx *c) {
         free_buf(ns.exb);
     }
     for (auto &b : c->scr) free_buf(b);
+    free_buf(c->corpus_pts);
+    free_buf(c->query_pts);
+    for (auto &b : c->dense_scr) free_buf(b);
+    delete[] c->h_corpus_off;
     for (int s2 = 0; s2 < 2; s2++) {
         free_buf(c->pw_nodes[s2]);
         free_buf(c->pw_lev[s2]);
@@ -447,6 +452,16 @@ int w1g_delta_condense(w1g_ctx *c, double delta, double pitch, double half_width
     }
     invalidate_from_nodes(*c);
     return dc_run(*c, delta, pitch, half_width, seed, k);
+}
+
+int w1g_snap_points(w1g_ctx *c, const double *points, int64_t n, double pitch, double *snapped,
+                    int64_t *cells) {
+    CTX_CHECK(c);
+    if (n < 0 || !(pitch > 0.0)) {
+        set_error("delta must be positive");
+        return W1G_EINVAL;
+    }
+    return snap_run(*c, points, n, pitch, snapped, cells);
 }
 
 // ---------------------------------------------------------------- split tree
@@ -695,6 +710,38 @@ static int copy_network_out(Ctx &c, int *copied) {
     }
     *copied = 1;
     return W1G_OK;
+}
+
+// ---------------------------------------------------------------- corpus / retrieval / dense oracle
+
+int w1g_corpus_load(w1g_ctx *c, const double *points, const int64_t *offsets, int64_t n_diagrams) {
+    CTX_CHECK(c);
+    return corpus_load(*c, points, offsets, n_diagrams);
+}
+
+int w1g_wcd_corpus(w1g_ctx *c, const double *query, int64_t nq, const int64_t *candidates, int64_t n_candidates,
+                   double *scores) {
+    CTX_CHECK(c);
+    if (nq < 0 || n_candidates < 0 || (n_candidates && (!candidates || !scores))) return W1G_EINVAL;
+    return wcd_corpus(*c, query, nq, candidates, n_candidates, scores);
+}
+
+int w1g_rwmd_corpus(w1g_ctx *c, const double *query, int64_t nq, const int64_t *candidates, int64_t n_candidates,
+                    double *scores) {
+    CTX_CHECK(c);
+    if (nq < 0 || n_candidates < 0 || (n_candidates && (!candidates || !scores))) return W1G_EINVAL;
+    c->nodes[1].valid = false;
+    return rwmd_corpus(*c, query, nq, candidates, n_candidates, scores);
+}
+
+int w1g_dense_network(w1g_ctx *c, int64_t *node_count, int64_t *n_arcs) {
+    CTX_CHECK(c);
+    if (!c->nodes[0].valid) {
+        set_error("dense_network: no nodes0 (zero_condense or load_nodes first)");
+        return W1G_ESTATE;
+    }
+    if (!node_count || !n_arcs) return W1G_EINVAL;
+    return dense_network_run(*c, node_count, n_arcs);
 }
 
 // ---------------------------------------------------------------- fused front end

@@ -141,6 +141,8 @@ struct AuxWorker {
     }
 };
 
+struct BatchState;  // batch.cu
+
 struct Ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -233,6 +235,13 @@ struct Ctx {
     int split_gate = 0, split_gate_e2e = 1;
     Ctx *aux = nullptr;
     AuxWorker *aux_worker = nullptr;  // the host thread that drives `aux` (owned by this context)
+    BatchState *batch = nullptr;      // batch executor: child contexts + workers (batch.cu)
+
+    // a diagram corpus resident on the device (w1g_corpus_load): points of all
+    // diagrams back to back, diagram i = [corpus_off[i], corpus_off[i+1])
+    DevBuf corpus_pts, query_pts, dense_scr[4];
+    int64_t corpus_n = -1;
+    int64_t *h_corpus_off = nullptr;  // host copy of the offsets (n + 1)
 
     // one-shot host target for the next fused front end's network (w1g_set_network_out)
     struct NetOut {
@@ -513,6 +522,8 @@ int rwmd_range_run(Ctx &c, int side, int64_t begin, int64_t end, double *partial
 // src: the node set to condense (default nodes[0]); the result goes to nodes[1]
 int dc_run(Ctx &c, double delta, double pitch, double half_width, uint64_t seed, int64_t *k,
            NodeSet *src = nullptr);
+// standalone snap_points (host arrays in and out)
+int snap_run(Ctx &c, const double *h_pts, int64_t k, double pitch, double *h_snapped, int64_t *h_cells);
 // the raw diagrams as a node set (unit masses, duplicates kept) into c.raw:
 // delta_condense of it equals delta_condense of zero_condense's output
 int raw_nodes(Ctx &c, const double2 *d_a, int64_t na, const double2 *d_b, int64_t nb);
@@ -529,6 +540,13 @@ int wspd_pair_idx(Ctx &c);  // pair_idx from pair_uv and the tree's reps, unless
 int emit_run(Ctx &c, int64_t *n_arcs);
 int net_run(Ctx &c, const int64_t *d_supplies, int64_t n, int64_t *n_arcs);
 int assemble_supplies(Ctx &c, int64_t **d_sup, int64_t *n);
+// corpus.cu: a resident diagram corpus, WCD / RWMD scores of a query against it
+// (pipeline.py:191-243 nn_search stages), the dense exact-oracle network (oracle.py:66-93)
+int corpus_load(Ctx &c, const double *pts, const int64_t *offsets, int64_t n);
+int wcd_corpus(Ctx &c, const double *query, int64_t nq, const int64_t *cand, int64_t ncand, double *scores);
+int rwmd_corpus(Ctx &c, const double *query, int64_t nq, const int64_t *cand, int64_t ncand, double *scores);
+int dense_network_run(Ctx &c, int64_t *node_count, int64_t *n_arcs);
+void batch_destroy(Ctx &c);  // joins a batch's workers, destroys its child contexts
 // fused front end: emit_arcs + assemble straight from the WSPD pairs (the arc
 // list is not materialised); falls back to emit_run + net_run when needed
 // its validation flags are read by spanner_net_check once the stream has drained

@@ -96,7 +96,8 @@ __global__ void k_zc_stats(const int64_t *am, const int64_t *bm, const double2 *
 
 __device__ __forceinline__ double round_half_away(double t) {
     // condensation.py:62-63: np.sign(t) * np.floor(np.abs(t) + 0.5)
-    double sg = t > 0.0 ? 1.0 : (t < 0.0 ? -1.0 : t);
+    // np.sign: +0.0 for either zero, NaN for NaN
+    double sg = t > 0.0 ? 1.0 : (t < 0.0 ? -1.0 : (t == 0.0 ? 0.0 : t));
     return dmul(sg, floor(dadd(fabs(t), 0.5)));
 }
 
@@ -150,6 +151,23 @@ __global__ void k_dc_snap(const double2 *pts, int64_t k, double pitch, longlong2
         atomicMin((long long *)&f[F_CELL_MIN + 2], (long long)mny);
         atomicMax((long long *)&f[F_CELL_MIN + 3], (long long)mxy);
     }
+}
+
+// standalone snap_points (condensation.py:66-77): the snapped coordinates
+// fl(cell * pitch) and the int64 cells, with the overflow guard
+__global__ void k_snap_points(const double2 *pts, int64_t k, double pitch, double2 *snapped, longlong2 *cells,
+                              int64_t *f) {
+    int ovf = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < k;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double2 p = pts[i];
+        const double cx = round_half_away(ddiv(p.x, pitch));
+        const double cy = round_half_away(ddiv(p.y, pitch));
+        if (!(fabs(cx) < 4611686018427387904.0) || !(fabs(cy) < 4611686018427387904.0)) ovf = 1;
+        snapped[i] = make_double2(dmul(cx, pitch), dmul(cy, pitch));
+        cells[i] = make_longlong2(__double2ll_rz(cx), __double2ll_rz(cy));
+    }
+    if (ovf) atomicOr((unsigned long long *)&f[F_OVERFLOW], 1ull);
 }
 
 __global__ void k_dc_keys(const longlong2 *cells, int64_t k, int packed, int64_t mnx, int64_t mny,
@@ -638,6 +656,33 @@ int dc_run(Ctx &c, double delta, double pitch, double half_width, uint64_t seed,
     dst.valid = true;
     if (lists && !c.h_pinned[F_LISTS]) c.pre_n = dst.k;
     *kout = dst.k;
+    return W1G_OK;
+}
+
+int snap_run(Ctx &c, const double *h_pts, int64_t k, double pitch, double *h_snapped, int64_t *h_cells) {
+    double2 *pts, *snapped;
+    longlong2 *cells;
+    W1G_TRY(ensure(c.scr[0], (size_t)k + 1, &pts));
+    W1G_TRY(ensure(c.scr[1], (size_t)k + 1, &snapped));
+    W1G_TRY(ensure(c.scr[2], (size_t)k + 1, &cells));
+    W1G_TRY(flags_reset(c));
+    if (k) {
+        W1G_CUDA(cudaMemcpyAsync(pts, h_pts, sizeof(double2) * k, cudaMemcpyHostToDevice, c.stream));
+        k_snap_points<<<grid_for(k, 256, 8u * c.sm_count), 256, 0, c.stream>>>(pts, k, pitch, snapped, cells,
+                                                                              dflags(c));
+        W1G_CHECK_LAUNCH();
+    }
+    W1G_TRY(flags_fetch(c, F_OVERFLOW, 1));
+    if (c.h_pinned[F_OVERFLOW]) {
+        set_error("lattice pitch too small for the coordinate range");
+        return W1G_EOVERFLOW;
+    }
+    if (k) {
+        if (h_snapped)
+            W1G_CUDA(cudaMemcpyAsync(h_snapped, snapped, sizeof(double2) * k, cudaMemcpyDeviceToHost, c.stream));
+        if (h_cells) W1G_CUDA(cudaMemcpyAsync(h_cells, cells, sizeof(longlong2) * k, cudaMemcpyDeviceToHost, c.stream));
+        W1G_TRY(stream_sync(c));
+    }
     return W1G_OK;
 }
 

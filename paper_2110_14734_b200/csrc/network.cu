@@ -10,49 +10,13 @@
 //       (tail, head) groups reduced to their min cost, row offsets by a
 //       histogram + scan.
 #include "common.cuh"
+#include "hypot.cuh"
 
 namespace w1g {
 
 static const double SQRT2 = 1.4142135623730951;
 
 namespace {
-
-// glibc sysdeps/ieee754/dbl-64/e_hypot.c (2.35+), the non-FMA kernel that
-// x86-64 numpy calls; verified bit-exact against libm in tests/.
-__device__ __forceinline__ double hypot_kernel(double ax, double ay) {
-    double t1, t2;
-    double h = dsqrt(dadd(dmul(ax, ax), dmul(ay, ay)));
-    if (h <= dmul(2.0, ay)) {
-        const double delta = dsub(h, ay);
-        t1 = dmul(ax, dsub(dmul(2.0, delta), ax));
-        t2 = dmul(dsub(delta, dmul(2.0, dsub(ax, ay))), delta);
-    } else {
-        const double delta = dsub(h, ax);
-        t1 = dmul(dmul(2.0, delta), dsub(ax, dmul(2.0, ay)));
-        t2 = dadd(dmul(dsub(dmul(4.0, delta), ay), ay), dmul(delta, delta));
-    }
-    return dsub(h, ddiv(dadd(t1, t2), dmul(2.0, h)));
-}
-
-__device__ double glibc_hypot(double x, double y) {
-    if (!isfinite(x) || !isfinite(y)) {
-        if (isinf(x) || isinf(y)) return INFINITY;
-        return dadd(x, y);
-    }
-    x = fabs(x);
-    y = fabs(y);
-    double ax = x < y ? y : x, ay = x < y ? x : y;
-    if (ax > 0x1p+511) {
-        if (ay <= dmul(ax, 0x1p-54)) return dadd(ax, ay);
-        return ddiv(hypot_kernel(dmul(ax, 0x1p-600), dmul(ay, 0x1p-600)), 0x1p-600);
-    }
-    if (ay < 0x1p-511) {
-        if (ax >= ddiv(ay, 0x1p-54)) return dadd(ax, ay);
-        return dmul(hypot_kernel(ddiv(ax, 0x1p-600), ddiv(ay, 0x1p-600)), 0x1p-600);
-    }
-    if (ay <= dmul(ax, 0x1p-54)) return dadd(ax, ay);
-    return hypot_kernel(ax, ay);
-}
 
 __global__ void k_emit_spanner(const int64_t *idx, int64_t P, const double2 *pts, int64_t *tails,
                                int64_t *heads, double *costs) {

@@ -39,6 +39,21 @@ def diagonal_projection(p: PDPoint) -> tuple[float, float]:
     return (m, m)
 
 
+def diagonal_distances(points) -> np.ndarray:
+    """|y - x| / sqrt(2) per row of an (n, 2) array (diagram.py:40-47).  The
+    device kernels evaluate the same two IEEE operations inline (rwmd.cu,
+    network.cu); this is the host helper of the public API."""
+    pts = np.asarray(points, dtype=np.float64).reshape(-1, 2)
+    return np.abs(pts[:, 1] - pts[:, 0]) / SQRT2
+
+
+def diagonal_projections(points) -> np.ndarray:
+    """((x+y)/2, (x+y)/2) per row of an (n, 2) array (diagram.py:50-54)."""
+    pts = np.asarray(points, dtype=np.float64).reshape(-1, 2)
+    m = 0.5 * (pts[:, 0] + pts[:, 1])
+    return np.stack([m, m], axis=1)
+
+
 class PersistenceDiagram:
     """Finite multiset of (birth, death) points with death > birth (diagram.py:57-95)."""
 
@@ -74,6 +89,54 @@ class PersistenceDiagram:
 
     def __repr__(self) -> str:
         return f"PersistenceDiagram({len(self)} points)"
+
+
+def _parse_pair(lineno: int, tokens: list[str]) -> tuple[float, float]:
+    """One data line of the diagram text format -> (birth, death), validated."""
+    if len(tokens) != 2:
+        raise DiagramFormatError(f"line {lineno}: expected two numbers, got {len(tokens)} tokens")
+    try:
+        pair = (float(tokens[0]), float(tokens[1]))
+    except ValueError:
+        raise DiagramFormatError(f"line {lineno}: non-numeric token") from None
+    if not all(map(math.isfinite, pair)):
+        raise DiagramFormatError(f"line {lineno}: non-finite coordinate")
+    if pair[1] < pair[0]:
+        raise DiagramFormatError(f"line {lineno}: death < birth")
+    return pair
+
+
+def parse_diagram(text: str) -> tuple[PersistenceDiagram, int]:
+    """Diagram text, one "birth death" pair per line (diagram.py:98-131).
+
+    Blank lines and lines starting with '#' are skipped; repeated lines are
+    multiplicity; zero-persistence points (death == birth) are dropped and
+    counted; any malformed line rejects the input with its line number."""
+    rows = []
+    for lineno, raw in enumerate(text.splitlines(), start=1):
+        body = raw.strip()
+        if body and body[0] != "#":
+            rows.append(_parse_pair(lineno, body.split()))
+    pts = np.array(rows, dtype=np.float64).reshape(-1, 2)
+    keep = pts[:, 1] != pts[:, 0]
+    return PersistenceDiagram(pts[keep]), int(pts.shape[0] - np.count_nonzero(keep))
+
+
+def serialize_diagram(diagram: PersistenceDiagram) -> str:
+    """Inverse of parse_diagram up to point order (diagram.py:134-137): repr()
+    of each coordinate, so a round trip is exact."""
+    lines = [f"{float(b)!r} {float(d)!r}" for b, d in points_of(diagram)]
+    return "\n".join(lines) + ("\n" if lines else "")
+
+
+def load_diagram(path) -> tuple[PersistenceDiagram, int]:
+    """parse_diagram of a file; errors carry the path (diagram.py:140-147)."""
+    with open(path, "r", encoding="utf-8") as fh:
+        text = fh.read()
+    try:
+        return parse_diagram(text)
+    except DiagramFormatError as exc:
+        raise DiagramFormatError(f"{path}: {exc}") from None
 
 
 def points_of(d) -> np.ndarray:

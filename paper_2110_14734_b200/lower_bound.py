@@ -49,3 +49,46 @@ def rwmd_best(nodes: SuppliedNodes, side: str = "a", device: int | None = None) 
     if out.size:
         ctx.call("w1g_fetch_rwmd_best", s, _lib.f64p(out), ctypes.byref(n))
     return out
+
+
+def _corpus_arrays(diagrams) -> tuple[np.ndarray, np.ndarray]:
+    """Points of a list of diagrams back to back plus row offsets (n + 1)."""
+    from .diagram import points_of
+
+    pts = [points_of(d) for d in diagrams]
+    off = np.zeros(len(pts) + 1, dtype=np.int64)
+    if pts:
+        off[1:] = np.cumsum([p.shape[0] for p in pts])
+    flat = np.ascontiguousarray(np.concatenate(pts, axis=0)) if pts else np.empty((0, 2))
+    return flat.reshape(-1, 2), off
+
+
+def load_corpus(diagrams, device: int | None = None):
+    """Upload a diagram corpus to the device once (w1g_corpus_load); returns the context."""
+    ctx = _lib.context(device)
+    flat, off = _corpus_arrays(diagrams)
+    ctx.call("w1g_corpus_load", _lib.f64p(flat), _lib.i64p(off), len(off) - 1)
+    return ctx
+
+
+def corpus_scores(ctx, kind: str, query, candidates) -> np.ndarray:
+    """Scores of `query` against the loaded corpus' `candidates`: kind "wcd" (one
+    launch for all of them, lower_bound.py:78-92) or "rwmd" (rwmd(zero_condense(
+    query, candidate)), pipeline.py:202-203)."""
+    from .diagram import points_of
+
+    q = points_of(query)
+    cand = np.ascontiguousarray(candidates, dtype=np.int64)
+    out = np.empty(cand.shape[0], dtype=np.float64)
+    if cand.shape[0]:
+        ctx.call("w1g_wcd_corpus" if kind == "wcd" else "w1g_rwmd_corpus", _lib.f64p(q), q.shape[0],
+                 _lib.i64p(cand), cand.shape[0], _lib.f64p(out))
+    return out
+
+
+def wcd(a, b, device: int | None = None) -> float:
+    """Centroid-difference lower bound on W1 (lower_bound.py:78-92), on device:
+    N * |mean(A u proj(B)) - mean(B u proj(A))| / 2 with numpy's summation order
+    and glibc's hypot, bit for bit."""
+    ctx = load_corpus([b], device)
+    return float(corpus_scores(ctx, "wcd", a, [0])[0])

@@ -114,10 +114,12 @@ def s_from_error(eps_target: float) -> int:
 
 def _front_end(ctx, ap: np.ndarray, bp: np.ndarray, params: ApproxParams) -> _lib.FrontEndInfo:
     info = _lib.FrontEndInfo()
-    fixed = params.delta is not None
+    # the reference's own ApproxParams (no delta / k fields) works too
+    delta = getattr(params, "delta", None)
+    fixed = delta is not None
     ctx.call("w1g_front_end", _lib.f64p(ap), ap.shape[0], _lib.f64p(bp), bp.shape[0], float(params.s),
              1 if params.use_condensation else 0, 1 if fixed else 0,
-             float(params.delta) if fixed else 0.0, float(params.k),
+             float(delta) if fixed else 0.0, float(getattr(params, "k", 0.99)),
              ctypes.c_uint64(int(params.seed) & 0xFFFFFFFFFFFFFFFF), ctypes.byref(info))
     return info
 
@@ -198,21 +200,57 @@ def pair_shard(n_diagrams: int, rank: int, world: int) -> list[tuple[int, int]]:
     return pairs[rank::world]
 
 
+def _device_pairs(pts, share, params, dev: int, streams: int, on_network) -> None:
+    """One device's share of a pair list through the native batch executor
+    (batch.cu): the diagrams are uploaded once, `streams` library worker threads
+    run the front ends on child contexts, and this thread receives each network
+    (zero-copy, page-locked) as it completes -- no Python in the per-pair loop
+    on the device side."""
+    from .lower_bound import load_corpus
+    from .network import TransshipmentNetwork
+
+    if not share:
+        return
+    ctx = load_corpus(pts, dev)
+    pairs = np.ascontiguousarray(np.asarray(share, dtype=np.int32).reshape(-1, 2))
+    delta = getattr(params, "delta", None)
+    ctx.call("w1g_batch_begin", pairs.ctypes.data, pairs.shape[0], float(params.s),
+             1 if params.use_condensation else 0, 0 if delta is None else 1,
+             0.0 if delta is None else float(delta), float(getattr(params, "k", 0.99)),
+             ctypes.c_uint64(int(params.seed) & 0xFFFFFFFFFFFFFFFF), int(streams), 0)
+    lib = ctx.lib
+    try:
+        r = _lib.BatchResult()
+        while True:
+            rc = lib.w1g_batch_next(ctx.handle, ctypes.byref(r))
+            if rc == _lib.W1G_DONE:
+                break
+            _lib.check(rc)
+            if r.status != _lib.W1G_OK:
+                _lib.raise_code(r.status, r.message.decode(errors="replace"))
+            diag = _diagnostics(r.info)
+            net = None
+            if not r.info.short_circuit:
+                net = TransshipmentNetwork(int(r.info.node_count), *_lib.result_arrays(r))
+            on_network(int(r.i), int(r.j), net, diag)
+    finally:
+        lib.w1g_batch_end(ctx.handle)
+
+
 def _run_pairs(pts, todo, params: ApproxParams, devs, streams_per_device: int, on_network) -> None:
-    """Front ends of `todo` pairs, round-robin over devices x streams: every
-    (device, stream) worker is one host thread with its own context -- own CUDA
-    stream, buffers and RWMD side stream -- so several latency-bound front ends
-    of small diagrams share a GPU.  on_network(i, j, net, diag) runs in the worker."""
-    workers = [(d, k) for k in range(max(1, streams_per_device)) for d in devs]
-
-    def worker(w: int):
-        dev = workers[w][0]
-        for i, j in todo[w::len(workers)]:
-            net, diag = sparsify(pts[i], pts[j], params, device=dev)
-            on_network(i, j, net, diag)
-
-    with ThreadPoolExecutor(max_workers=len(workers)) as wp:
-        list(wp.map(worker, range(len(workers))))
+    """Front ends of `todo` pairs: round-robin over devices (one consumer thread
+    and one context each, no collective), each device's share run by the native
+    batch executor with `streams_per_device` concurrent child contexts.
+    on_network(i, j, net, diag) runs in the device's consumer thread."""
+    shards = [todo[d::len(devs)] for d in range(len(devs))]
+    streams = max(1, streams_per_device)
+    if len(devs) == 1:
+        _device_pairs(pts, shards[0], params, devs[0], streams, on_network)
+        return
+    with ThreadPoolExecutor(max_workers=len(devs)) as wp:
+        futs = [wp.submit(_device_pairs, pts, sh, params, d, streams, on_network) for d, sh in zip(devs, shards)]
+        for f in futs:
+            f.result()
 
 
 def sparsify_batch(diagrams, params: ApproxParams, pairs: list[tuple[int, int]] | None = None, devices=None,
@@ -276,3 +314,101 @@ def pairwise_w1(diagrams, params: ApproxParams, devices=None, solver_threads: in
         out[i, j] = out[j, i] = f.result()
     pool.shutdown()
     return out
+
+
+# ---------------------------------------------------------------- staged nearest-neighbour search
+
+WCD_STAGE = "wcd"
+RWMD_STAGE = "rwmd"
+PDFLOW_STAGE = "pdflow"
+EXACT_STAGE = "exact"
+_STAGE_NAMES = (WCD_STAGE, RWMD_STAGE, PDFLOW_STAGE, EXACT_STAGE)
+
+
+@dataclass(frozen=True)
+class PipelineStage:
+    """One filtering stage: a distance algorithm and its survivor count (pipeline.py:153-169)."""
+
+    algorithm: str
+    keep: int
+    s: float | None = None
+
+    def __post_init__(self):
+        if self.algorithm not in _STAGE_NAMES:
+            raise ValueError(f"unknown stage algorithm {self.algorithm!r}")
+        if self.keep < 1:
+            raise ValueError("stage must keep at least one candidate")
+        if self.algorithm == PDFLOW_STAGE and (self.s is None or self.s <= 0):
+            raise ValueError("pdflow stages need a positive sparsity parameter")
+
+
+@dataclass(frozen=True)
+class PipelineSpec:
+    """Staged filtering plan with strictly decreasing survivor counts (pipeline.py:172-185)."""
+
+    stages: tuple[PipelineStage, ...]
+
+    def __post_init__(self):
+        if not self.stages:
+            raise ValueError("pipeline needs at least one stage")
+        keeps = [st.keep for st in self.stages]
+        if keeps[-1] != 1:
+            raise ValueError("the final stage must keep exactly one candidate")
+        if any(x <= y for x, y in zip(keeps, keeps[1:])):
+            raise ValueError("survivor counts must be strictly decreasing")
+
+
+@dataclass
+class NNDiagnostics:
+    stage_survivors: list[list[int]] = field(default_factory=list)
+    stage_scores: list[dict[int, float]] = field(default_factory=list)
+
+
+def _stage_scores(stage, ctx, query, corpus, survivors, seed: int, threads: int, device) -> list[float]:
+    """One stage's scores for the surviving candidates (pipeline.py:191-207).
+
+    wcd and rwmd score every survivor against the device-resident corpus in one
+    library call; pdflow runs the GPU front end per candidate (pairs of the
+    batch path, several streams) and the reference solver; exact builds the
+    dense network on the GPU and solves it on the host."""
+    from .exact import exact_w1_dense
+    from .lower_bound import corpus_scores
+
+    if stage.algorithm in (WCD_STAGE, RWMD_STAGE):
+        return [float(v) for v in corpus_scores(ctx, stage.algorithm, query, survivors)]
+    if stage.algorithm == EXACT_STAGE:
+        def one(i):
+            return exact_w1_dense(query, corpus[i], device=device)
+    else:
+        # an explicit s in the spec acknowledges best-effort values s <= 2
+        params = ApproxParams(s=stage.s, seed=seed, best_effort=True, threads=1)
+
+        def one(i):
+            return approx_w1(query, corpus[i], params, device=device)[0]
+    if threads > 1 and len(survivors) > 1:
+        with ThreadPoolExecutor(max_workers=threads) as pool:
+            return list(pool.map(one, survivors))
+    return [one(i) for i in survivors]
+
+
+def nn_search(query, corpus, spec: PipelineSpec, seed: int = 0, threads: int = 1,
+              device: int | None = None) -> tuple[int, NNDiagnostics]:
+    """Index of the corpus diagram the staged pipeline ranks nearest (pipeline.py:210-243).
+
+    Each stage rescores the surviving candidates and keeps its `keep` best;
+    ties break toward the lower corpus index.  The corpus is uploaded to the
+    device once for all stages."""
+    from .lower_bound import load_corpus
+
+    if not corpus:
+        raise ValueError("corpus must be nonempty")
+    ctx = load_corpus(corpus, device)
+    diag = NNDiagnostics()
+    survivors = list(range(len(corpus)))
+    for stage in spec.stages:
+        scores = _stage_scores(stage, ctx, query, corpus, survivors, seed, threads, device)
+        ranked = sorted(zip(scores, survivors), key=lambda t: (t[0], t[1]))
+        diag.stage_scores.append({i: sc for sc, i in ranked})
+        survivors = [i for _, i in ranked[: stage.keep]]
+        diag.stage_survivors.append(list(survivors))
+    return survivors[0], diag

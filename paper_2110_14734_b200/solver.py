@@ -39,9 +39,29 @@ def reference_simplex():
     return _simplex
 
 
-def solve(network, block_size=None, stop_c: float = 4.0, stop_b: float = 1e5):
-    """simplex.solve(network, ...) of the reference (simplex.py:339-395)."""
-    return reference_simplex().solve(network, block_size=block_size, stop_c=stop_c, stop_b=stop_b)
+# names of the reference package that are outside the accelerated path and are
+# re-exported unchanged (host solver types, the brute-force oracle, cKDTree index)
+REFERENCE_EXPORTS = {
+    "FlowResult": "simplex",
+    "InfeasibleNetworkError": "simplex",
+    "find_entering_arc": "simplex",
+    "OracleSizeError": "oracle",
+    "exact_w1_bruteforce": "oracle",
+    "PlanarIndex": "lower_bound",
+}
+
+
+def reference_attr(name: str):
+    """`name` from the reference module REFERENCE_EXPORTS assigns it to."""
+    import importlib
+
+    reference_simplex()  # puts the reference on sys.path if it comes from baseline/_ref
+    return getattr(importlib.import_module("w1flow." + REFERENCE_EXPORTS[name]), name)
+
+
+def solve(network, *args, **kwargs):
+    """simplex.solve(network, ...) of the reference (simplex.py:339-395), every argument forwarded."""
+    return reference_simplex().solve(network, *args, **kwargs)
 
 
 OPTIMAL = "optimal"

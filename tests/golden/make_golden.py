@@ -100,8 +100,56 @@ def deep_cases():
     save("deep_pm2i_s8", deep, P([(0.25, 2.5), (0.0, 1.0)]), 8.0, delta=0.0)
 
 
+def retrieval_cases():
+    """nn_search stages (pipeline.py:191-243), WCD (lower_bound.py:78-92) and the dense
+    exact oracle (oracle.py:66-108) on a mixed corpus, from the live reference."""
+    from w1flow import oracle
+
+    rng = np.random.default_rng(77)
+    P = PersistenceDiagram
+    corpus = [random_diagram(rng, max_points=30, min_points=1) for _ in range(14)]
+    corpus += list(synth.gaussian_cluster_pair(400, 300, seed=11))
+    corpus += [synth.gaussian_cluster_diagram(250 + 50 * i, seed=20 + i) for i in range(6)]
+    corpus.append(P())  # an empty diagram
+    corpus.append(P(np.array([[-3.5, -0.0], [-0.0, 2.0], [1.0, 2.5]])))  # signed zeros, negatives
+    query = synth.gaussian_cluster_diagram(300, seed=20)
+    out = {"query": query.points, "n_corpus": np.array(len(corpus))}
+    for i, d in enumerate(corpus):
+        out[f"c{i}"] = d.points
+    out["wcd"] = np.array([lower_bound.wcd(query, d) for d in corpus])
+    out["wcd_rev"] = np.array([lower_bound.wcd(d, query) for d in corpus])
+    out["rwmd"] = np.array([lower_bound.rwmd(diagram.zero_condense(query, d)) for d in corpus])
+    specs = {
+        "spec_wcd_rwmd_pdflow": (("wcd", 12, None), ("rwmd", 5, None), ("pdflow", 1, 12.0)),
+        "spec_rwmd_exact": (("rwmd", 4, None), ("exact", 1, None)),
+        "spec_wcd_only": (("wcd", 1, None),),
+    }
+    for name, stages in specs.items():
+        spec = pipeline.PipelineSpec(tuple(pipeline.PipelineStage(a, k, s) for a, k, s in stages))
+        best, nd = pipeline.nn_search(query, corpus, spec, seed=3)
+        out[name + "_best"] = np.array(best)
+        for si, (surv, sc) in enumerate(zip(nd.stage_survivors, nd.stage_scores)):
+            out[f"{name}_s{si}_survivors"] = np.array(surv, dtype=np.int64)
+            keys = np.array(sorted(sc), dtype=np.int64)
+            out[f"{name}_s{si}_ids"] = keys
+            out[f"{name}_s{si}_scores"] = np.array([sc[k] for k in keys])
+    # dense oracle networks and exact W1
+    for i, (x, y) in enumerate([(query, corpus[15]), (corpus[0], corpus[1]), (corpus[22], corpus[14]),
+                                (corpus[23], query)]):
+        nodes = diagram.zero_condense(x, y)
+        net = oracle.dense_network(nodes)
+        out.update({f"dense{i}_a": x.points, f"dense{i}_b": y.points,
+                    f"dense{i}_supplies": net.supplies, f"dense{i}_tails": net.tails,
+                    f"dense{i}_heads": net.heads, f"dense{i}_costs": net.costs,
+                    f"dense{i}_row_offsets": net.row_offsets,
+                    f"dense{i}_w1": np.array(oracle.exact_w1_dense(x, y))})
+    np.savez_compressed(os.path.join(HERE, "retrieval.npz"), **out)
+    print("retrieval", len(out), "arrays")
+
+
 def main():
     deep_cases()
+    retrieval_cases()
     # cfg1: BASELINE.json configs[0] -- 1k points each, s=1, delta=0.01
     a, b = synth.gaussian_cluster_pair(1000, 1000, seed=0)
     save("cfg1_s1_d001", a, b, 1.0, delta=0.01)
@@ -185,5 +233,7 @@ def main():
 if __name__ == "__main__":
     if sys.argv[1:] == ["deep"]:
         deep_cases()
+    elif sys.argv[1:] == ["retrieval"]:
+        retrieval_cases()
     else:
         main()
