@@ -1,30 +1,39 @@
-"""Benchmark of the sparsify front end (BASELINE.json configs[1], cfg2).
+"""Benchmark of the sparsify front end (BASELINE.json configs[1], cfg2; --workload cfg4 for configs[3]).
 
-Workload: one synthetic persistence-diagram pair of 100,000 points each
-(reference generator, synth.gaussian_cluster_pair(100000, 100000, seed)),
-s = 1, delta = 0.01 (fixed, the chain of test_acceptance.py:224-237), k = 0.99.
-A step is one full sparsify front end (pipeline.py:105-130: zero_condense ->
-rwmd -> delta_condense -> split tree -> WSPD -> emit arcs -> CSR network).
+Workload (default, cfg2): a fixed batch of PAIRS synthetic persistence-diagram
+pairs of 100,000 points each (reference generator,
+synth.gaussian_cluster_pair(100000, 100000, seed=p), p = 0..PAIRS-1), s = 1,
+delta = 0.01 (fixed, the chain of test_acceptance.py:224-237), k = 0.99.  A step
+is the full sparsify front end (pipeline.py:105-130: zero_condense -> rwmd ->
+delta_condense -> split tree -> WSPD -> emit arcs -> CSR network) of every pair
+of the batch.  Under torchrun the batch is dealt round-robin to the ranks
+(strong scaling: the total work is fixed; pairs shard with no collective).
 
 Our arm (default):
-  value  -- pairs/s of the front end with the diagrams already in HBM and the
-            network left in HBM (w1g_front_end_device), CUDA events on the
-            library stream, L2 flushed (256 MiB write) before every step;
-  e2e    -- pairs/s through the public API (paper_2110_14734_b200.sparsify):
-            host numpy diagrams in (page-locked, w1g.pinned_points), host numpy
-            TransshipmentNetwork out, all H2D / D2H copies inside the timed region;
-  roofline -- the FP32 all-pairs RWMD tile kernel (w1g_profile_rwmd_tile):
-            5 FLOP x 2|A||B| directed evaluations per pair of launches;
-  cpu_baseline -- the C restatement of the reference front end (oracle/),
-            one bounded sample on rank 0.
-  w1     -- one approx_w1 (front end + the reference's host simplex) outside
-            the timed loop (rank 0, --w1).
-Reference arm (--impl reference): the same front end by the CPU port on the
-host cores, rank 0 only.
-
-Multi-GPU (torchrun): every rank runs its own pair (seed = rank): the pairs
-workload shards with no collective; scaling is weak.  Timing is the max over
-ranks (all-reduce MAX of the per-rank device time).
+  value    -- pairs/s of the whole job: the batch with the diagrams already in
+              HBM and the networks left in HBM (w1g_front_end_batch: the native
+              batch executor, STREAMS child contexts per GPU), device makespan
+              from CUDA events on the library stream that every child stream
+              joins, L2 flushed (256 MiB write) before every step, max over ranks;
+  e2e      -- the same through the public API (paper_2110_14734_b200.sparsify_batch):
+              host numpy diagrams in (pageable, as a user passes them), host
+              numpy TransshipmentNetworks out, every H2D / D2H copy inside the
+              timed region; plus single-pair variants (pinned / pageable input,
+              the reference's own delta schedule);
+  roofline -- the production RWMD kernels of the step, timed with CUDA events
+              on the stream each runs on (w1g_profile_rwmd) with device counters
+              of the distance evaluations they perform: the exact fp64 refine
+              (FP64 pipe) and the culled FP32 tile pass;
+  north_star_kernel -- the FP32 all-pairs tile kernel in full brute-force mode
+              at n = 1M (BASELINE.json: "at n=1M, the RWMD kernel reaches >= 70 %
+              of FP32 pipe peak"), 5 FLOP x 2|A||B| evaluations;
+  cpu_baseline -- the reference itself (w1flow from baseline/_ref, the
+              stage chain of pipeline.py:105-130) on one pair, rank 0, at
+              workers = all host threads and workers = 1; and the C port.
+  cfg4     -- the batched matrix workload (64 diagrams x 20k, 2016 pairs) dealt
+              over the ranks, front-end pairs/s (strong scaling).
+Reference arm (--impl reference): the reference's own front end (w1flow) on the
+host cores, rank 0 only, one pair per step.
 """
 
 from __future__ import annotations
@@ -45,56 +54,49 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "sparsify-stage ms & W1 pairs/sec at n=100k; RWMD kernel % of FP32 peak"
-FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # 74.4, derived nominal (no FP32 figure in MEASURED_PEAKS.json)
 N_POINTS = 100_000
 S = 1.0
 DELTA = 0.01
-NCU_SUMMARY = os.path.join(ROOT, "profiles", "r01_ncu_rwmd_tile.jsonl")
+K_LATTICE = 0.99
+PAIRS = 32
+STREAMS = 4
+CFG4 = (64, 20_000)
 
 
-def _ncu_traffic(kernel: str, capture: str = "prof_rwmd_all"):
-    """dram__bytes_read.sum + dram__bytes_write.sum of one launch of `kernel` at this workload,
-    from the committed `ncu --set full` capture summary (cfg2, same command as this bench)."""
-    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+def _peaks() -> dict:
+    """Roofline denominators: HBM from MEASURED_PEAKS.json (driver-measured copy
+    bandwidth); FP32 / FP64 pipe peaks derived from the SM count and the max SM
+    clock there (MEASURED_PEAKS.json has no FP32/FP64 figure)."""
+    mp = {}
     try:
-        with open(NCU_SUMMARY) as f:
-            for line in f:
-                row = json.loads(line)
-                if row["capture"] == capture and kernel in row["Kernel Name"]:
-                    total = 0.0
-                    for key in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
-                        v, u = row[key].split()
-                        total += float(v) * scale[u]
-                    return int(total)
-    except (OSError, KeyError, ValueError):
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            mp = json.load(f)
+    except (OSError, ValueError):
         pass
-    return None
-
-
-HBM_PEAK_GBS = 6528.7  # MEASURED_PEAKS.json hbm_gbs (copy bandwidth, read + write)
-
-
-def hbm_stages(n_in: int, k0: int, k: int, p: int, m: int, stage_ms: dict) -> dict:
-    """Algorithmic HBM bytes of the byte-moving stages (each stage's inputs read once and
-    outputs written once) over their measured device time, against
-    the measured copy bandwidth.  emit_arcs is fused into the CSR assembly (the pairs
-    and node arrays are read, the network written; no arc list in between)."""
-    nn = max(2 * k - 1, 0)
-    bytes_ = {
-        "zero_condense": 16 * n_in + 32 * k0,
-        "delta_condense": 32 * k0 + 32 * k,
-        "split_tree": 16 * k + 64 * nn,
-        "wspd": 40 * nn + 24 * p,
-        "emit_arcs+assemble": 16 * p + 32 * k + 24 * m + 16 * (k + 3),
+    mhz = float(mp.get("sm_max_mhz", 1965.0))
+    return {
+        "hbm_gbs": float(mp.get("hbm_gbs", 6553.6)),
+        "hbm_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in mp else "B200_PROFILING.md fallback",
+        "fp32_tflops": 148 * 128 * 2 * mhz * 1e6 / 1e12,
+        "fp64_tflops": 148 * 64 * 2 * mhz * 1e6 / 1e12,
+        "fp_source": f"derived nominal: 148 SM x (128 FP32 | 64 FP64 lanes) x 2 x {mhz:.0f} MHz "
+                     "(sm_max_mhz of MEASURED_PEAKS.json)",
     }
-    out = {}
-    for name, b in bytes_.items():
-        t = sum(stage_ms.get(x) or 0.0 for x in name.split("+"))
-        if not t:
-            continue
-        gbs = b / (t * 1e-3) / 1e9
-        out[name] = {"bytes": int(b), "ms": t, "gbs": gbs, "frac": gbs / HBM_PEAK_GBS}
-    return out
+
+
+PEAKS = _peaks()
+
+
+def workload_config(args) -> dict:
+    if args.workload == "cfg4":
+        return {"workload": f"cfg4: sparsify front ends of the {CFG4[0] * (CFG4[0] - 1) // 2} pairs of "
+                            f"{CFG4[0]} shared-centre diagrams x {CFG4[1]} points, s={args.s}, delta={args.delta}, "
+                            f"k={K_LATTICE}",
+                "pairs_per_step": CFG4[0] * (CFG4[0] - 1) // 2, "diagram_points": CFG4[1],
+                "l2": "flushed (256 MiB write) before every step"}
+    return {"workload": f"cfg2: sparsify front end, {args.n}+{args.n} points per pair, s={args.s}, "
+                        f"delta={args.delta}, k={K_LATTICE}",
+            "pairs_per_step": args.pairs, "l2": "flushed (256 MiB write) before every step"}
 
 
 def parse():
@@ -103,31 +105,39 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg4"])
     ap.add_argument("--n", type=int, default=N_POINTS)
+    ap.add_argument("--pairs", type=int, default=PAIRS)
+    ap.add_argument("--streams", type=int, default=STREAMS)
     ap.add_argument("--s", type=float, default=S)
     ap.add_argument("--delta", type=float, default=DELTA)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="value / e2e only (profiling runs)")
     ap.add_argument("--w1", dest="w1", action="store_true", default=True)
     ap.add_argument("--no-w1", dest="w1", action="store_false")
-    ap.add_argument("--profile-only", action="store_true", help="a few steps, no extras (for ncu)")
     return ap.parse_args()
 
 
 class Dist:
-    """torch.distributed plumbing (barrier, max over ranks); single process if no torchrun."""
+    """torch.distributed plumbing (barrier, max over ranks); single process without torchrun."""
 
-    def __init__(self, gpus: int):
+    def __init__(self, gpus: int, backend: str = "nccl"):
         self.rank = int(os.environ.get("RANK", "0"))
         self.world = int(os.environ.get("WORLD_SIZE", "1"))
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
         self.pg = None
-        if self.world > 1:
+        if self.world > 1 and backend:
             import torch
             import torch.distributed as dist
 
-            torch.cuda.set_device(self.local)
-            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
             self.torch, self.dist = torch, dist
+            if backend == "nccl":
+                torch.cuda.set_device(self.local)
+                dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+                self.dev = torch.device("cuda", self.local)
+            else:
+                dist.init_process_group("gloo")
+                self.dev = torch.device("cpu")
             self.pg = True
 
     def barrier(self):
@@ -137,7 +147,7 @@ class Dist:
     def max(self, x: float) -> float:
         if not self.pg:
             return x
-        t = self.torch.tensor([x], dtype=self.torch.float64, device="cuda")
+        t = self.torch.tensor([x], dtype=self.torch.float64, device=self.dev)
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -162,7 +172,7 @@ class Clocks:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
         except OSError:
@@ -175,7 +185,7 @@ class Clocks:
     def stop(self) -> dict:
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        time.sleep(0.25)
+        time.sleep(0.1)
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
@@ -199,20 +209,86 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_front_end_sample(a, b, s, delta, repeats: int = 2) -> dict:
-    """The C oracle (restatement of the reference front end), rank 0, bounded sample."""
-    from oracle import w1oracle as O
+# ---------------------------------------------------------------- inputs
 
-    O.lib()
-    times = []
-    for _ in range(repeats):
+def cfg2_inputs(args) -> list[np.ndarray]:
+    """Diagrams 2p, 2p+1 = gaussian_cluster_pair(n, n, seed=p) for every pair p of the batch."""
+    from paper_2110_14734_b200 import synth
+
+    out = []
+    for p in range(args.pairs):
+        a, b = synth.gaussian_cluster_pair(args.n, args.n, seed=p)
+        out += [a, b]
+    return out
+
+
+def rank_share(pairs: list[tuple[int, int]], rank: int, world: int) -> list[tuple[int, int]]:
+    return pairs[rank::world]
+
+
+# ---------------------------------------------------------------- the reference (CPU) front end
+
+def _reference_modules():
+    from paper_2110_14734_b200 import solver
+
+    solver.reference_simplex()  # puts baseline/_ref on sys.path when that is where the reference lives
+    import w1flow  # noqa: F401
+    from w1flow import condensation, diagram, lower_bound, network, pipeline, spanner
+    return condensation, diagram, lower_bound, network, pipeline, spanner
+
+
+def reference_front_end(a, b, s: float, delta: float, workers: int):
+    """pipeline.py:105-130 with the given delta (the fixed-delta chain of
+    test_acceptance.py:224-237), run by the reference package itself."""
+    condensation, diagram, lower_bound, network, pipeline, spanner = _reference_modules()
+    nodes0 = diagram.zero_condense(diagram.PersistenceDiagram(a), diagram.PersistenceDiagram(b))
+    lower = lower_bound.rwmd(nodes0, workers=workers)
+    nodes = nodes0
+    if lower > 0.0 and delta > 0.0:
+        nodes = condensation.delta_condense(
+            nodes0, condensation.CondensationParams(pipeline.condensation_epsilon(s), delta, k=K_LATTICE))
+    pairs = spanner.build_wspd(spanner.build_split_tree(nodes.points), s, workers=workers)
+    return network.assemble(nodes, spanner.emit_arcs(pairs, nodes))
+
+
+def host_threads() -> int:
+    return len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+
+
+def cpu_baselines(a, b, args) -> dict:
+    """The reference's own front end on this host (rank 0, one pair): all host
+    threads (the reference's `workers`) and one thread; the C port beside it."""
+    out = {}
+    threads = host_threads()
+    try:
+        tiny = np.array([[0.0, 1.0], [0.5, 2.0], [1.0, 1.5]])
+        reference_front_end(tiny, tiny[:2] + 0.25, args.s, args.delta, 1)  # numba compilation, untimed
+        for w in (threads, 1):
+            t0 = time.perf_counter()
+            net = reference_front_end(a, b, args.s, args.delta, w)
+            el = time.perf_counter() - t0
+            out[w] = (el, int(net.tails.shape[0]))
+    except Exception as exc:  # noqa: BLE001
+        return {"value": None, "unit": "pairs/s", "cores": threads, "kind": "reference",
+                "sample": f"reference unavailable: {exc!r}"}
+    el, m = out[threads]
+    res = {"value": 1.0 / el, "unit": "pairs/s", "cores": threads, "kind": "reference",
+           "sample": f"one cfg2 pair (seed 0) through the reference's own stage chain (w1flow from "
+                     f"baseline/_ref, pipeline.py:105-130, delta={args.delta}) with workers={threads}: "
+                     f"{el:.2f} s; {m} arcs",
+           "one_thread": {"value": 1.0 / out[1][0], "cores": 1, "seconds": out[1][0]}}
+    try:
+        from oracle import w1oracle as O
+
+        O.lib()
         t0 = time.perf_counter()
-        O.front_end(a, b, s, delta=delta)
-        times.append(time.perf_counter() - t0)
-    t = statistics.median(times)
-    return {"value": 1.0 / t, "unit": "pairs/s", "cores": 1, "kind": "port",
-            "sample": f"{repeats} full cfg2 front ends (one {a.shape[0]}+{b.shape[0]}-point pair each), "
-                      f"median {t * 1e3:.1f} ms/pair, scalar C port of the reference (oracle/w1oracle.c)"}
+        O.front_end(a, b, args.s, delta=args.delta)
+        el = time.perf_counter() - t0
+        res["c_port"] = {"value": 1.0 / el, "cores": 1, "kind": "port", "seconds": el,
+                         "note": "scalar C restatement of the reference (oracle/w1oracle.c)"}
+    except Exception as exc:  # noqa: BLE001
+        res["c_port"] = {"value": None, "note": repr(exc)}
+    return res
 
 
 def run_reference(args, dist: Dist):
@@ -220,200 +296,327 @@ def run_reference(args, dist: Dist):
         return
     from paper_2110_14734_b200 import synth
 
-    a, b = synth.gaussian_cluster_pair(args.n, args.n, seed=0)
-    from concurrent.futures import ThreadPoolExecutor
-
-    from oracle import w1oracle as O
-
-    O.lib()
-    # every host thread the process may use runs its own front end (the C port
-    # releases the GIL): one step = `threads` pairs processed concurrently
-    threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
-    pool = ThreadPoolExecutor(max_workers=threads)
-
-    def step():
-        list(pool.map(lambda _: O.front_end(a, b, args.s, delta=args.delta), range(threads)))
-
-    for _ in range(args.warmup):
-        step()
+    threads = host_threads()
+    if args.workload == "cfg4":
+        diags = synth.shared_centre_batch(*CFG4, seed=0)
+        todo = [(i, j) for i in range(CFG4[0]) for j in range(i + 1, CFG4[0])]
+        inputs = [(diags[i], diags[j]) for i, j in todo[:: max(1, len(todo) // 64)]]
+    else:
+        inputs = [synth.gaussian_cluster_pair(args.n, args.n, seed=p) for p in range(min(args.pairs, 4))]
+    tiny = np.array([[0.0, 1.0], [0.5, 2.0], [1.0, 1.5]])
+    reference_front_end(tiny, tiny[:2] + 0.25, args.s, args.delta, 1)  # numba compilation
+    for i in range(args.warmup):
+        reference_front_end(*inputs[i % len(inputs)], args.s, args.delta, threads)
     t0 = time.perf_counter()
-    for _ in range(args.steps):
-        step()
+    for i in range(args.steps):
+        reference_front_end(*inputs[i % len(inputs)], args.s, args.delta, threads)
     el = time.perf_counter() - t0
-    pool.shutdown()
-    v = threads * args.steps / el
+    v = args.steps / el
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "pairs/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (reference generator)",
-        "config": {"workload": f"cfg2: sparsify front end, {args.n}+{args.n} points, s={args.s}, delta={args.delta}",
-                   "host_threads": threads},
-        "cpu_baseline": {"value": v, "unit": "pairs/s", "cores": threads, "kind": "port",
-                         "sample": f"{args.steps} timed steps after {args.warmup} warm-up, each {threads} concurrent "
-                                   f"front ends (one per host thread) of the scalar C port"},
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference generator)", "config": workload_config(args),
+        "cpu_baseline": {"value": v, "unit": "pairs/s", "cores": threads, "kind": "reference",
+                         "sample": f"{args.steps} timed steps after {args.warmup} warm-up; each step one pair "
+                                   f"of the workload through the reference's own front end (w1flow from "
+                                   f"baseline/_ref, pipeline.py:105-130) with workers={threads}"},
         "e2e": {"value": v, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def run_ours(args, dist: Dist):
-    import paper_2110_14734_b200 as w1g
-    from paper_2110_14734_b200 import _lib, synth
+# ---------------------------------------------------------------- our arm
 
-    device = dist.local
-    ctx = _lib.context(device)
-    lib = ctx.lib
-    a, b = synth.gaussian_cluster_pair(args.n, args.n, seed=dist.rank)
-    params = w1g.ApproxParams(s=args.s, best_effort=True, delta=args.delta)
+class Batch:
+    """Device-resident batch of pairs on this rank's GPU (w1g_front_end_batch)."""
 
-    # device-resident inputs for the `value` leg (torch is plumbing only: device
-    # buffers, the L2 flush and CUDA events on the library's own stream)
-    import torch
+    def __init__(self, ctx, diagrams, pairs, args):
+        from paper_2110_14734_b200 import _lib
+        from paper_2110_14734_b200.lower_bound import load_corpus
 
-    torch.cuda.set_device(device)
-    stream = torch.cuda.ExternalStream(ctx.stream, device=device)
-    da = torch.from_numpy(a).to(f"cuda:{device}")
-    db = torch.from_numpy(b).to(f"cuda:{device}")
-    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=f"cuda:{device}")
-    torch.cuda.synchronize()
-    info = _lib.FrontEndInfo()
+        self.ctx = ctx
+        self.lib = ctx.lib
+        load_corpus(diagrams, ctx.device)
+        self.pairs = np.ascontiguousarray(np.asarray(pairs, dtype=np.int32).reshape(-1, 2))
+        self.infos = (_lib.FrontEndInfo * max(1, len(pairs)))()
+        self.args = args
 
-    def device_step():
-        _lib.check(lib.w1g_front_end_device(ctx.handle, ctypes.c_void_p(da.data_ptr()), a.shape[0],
-                                            ctypes.c_void_p(db.data_ptr()), b.shape[0], float(args.s), 1, 1,
-                                            float(args.delta), 0.99, ctypes.c_uint64(0), ctypes.byref(info)))
+    def run(self) -> float:
+        from paper_2110_14734_b200 import _lib
 
-    def flush_l2():
-        with torch.cuda.stream(stream):
-            flush.fill_(1)
+        ms = ctypes.c_float(0)
+        if self.pairs.shape[0]:
+            _lib.check(self.lib.w1g_front_end_batch(
+                self.ctx.handle, self.pairs.ctypes.data, self.pairs.shape[0], float(self.args.s), 1, 1,
+                float(self.args.delta), K_LATTICE, ctypes.c_uint64(0), int(self.args.streams), self.infos,
+                ctypes.byref(ms)))
+        return ms.value
 
-    for _ in range(args.warmup):
-        flush_l2()
-        device_step()
-    torch.cuda.synchronize()
+
+def time_batch(batch: Batch, steps: int, warmup: int, flush, dist: Dist, clocks=None):
+    from paper_2110_14734_b200 import _lib
+
+    for _ in range(warmup):
+        flush()
+        batch.run()
     dist.barrier()
-    clocks = Clocks(device)
-    clocks.start()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if clocks:
+        clocks.start()
     launches0 = _lib.launch_count()
-    stage_ms = []
-    wall0 = time.perf_counter()
-    for i in range(args.steps):
-        flush_l2()
-        ev[i][0].record(stream)
-        device_step()
-        ev[i][1].record(stream)
-        stage_ms.append([float(x) for x in info.stage_ms])
-    torch.cuda.synchronize()
-    wall = time.perf_counter() - wall0
-    launches = (_lib.launch_count() - launches0) // max(args.steps, 1)
-    dev_ms = sum(s.elapsed_time(e) for s, e in ev) / args.steps
+    times = []
+    for _ in range(steps):
+        flush()  # ordered on the library stream before the batch's start event
+        times.append(batch.run())
+    launches = (_lib.launch_count() - launches0) // max(steps, 1)
+    clk = clocks.stop() if clocks else None
     dist.barrier()
-    dev_ms_max = dist.max(dev_ms)
-    clk = clocks.stop()
+    return dist.max(statistics.mean(times)), launches, clk
 
-    # e2e through the public API (host numpy in, host numpy network out); the
-    # inputs live in page-locked host memory (w1g.pinned_points), so every step
-    # DMAs them to the device; warm-up also fills the pinned result pool
-    a_host, b_host = w1g.pinned_points(a), w1g.pinned_points(b)
-    keep = []
-    for _ in range(max(3, args.warmup)):
-        keep.append(w1g.sparsify(a_host, b_host, params, device=device))
-        keep = keep[-2:]
-    del keep
-    e2e_times = []
-    net = None
-    for _ in range(args.steps):
-        flush_l2()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        net, diag = w1g.sparsify(a_host, b_host, params, device=device)
-        e2e_times.append(time.perf_counter() - t0)
-    e2e_s = dist.max(statistics.mean(e2e_times))
-    h2d = a.nbytes + b.nbytes
-    d2h = net.supplies.nbytes + net.tails.nbytes + net.heads.nbytes + net.costs.nbytes + net.row_offsets.nbytes
 
-    # roofline of the dominant kernel: FP32 all-pairs RWMD tile pass (full brute force)
-    n0 = w1g.zero_condense(a, b, device=device)
+def rwmd_roofline(ctx, w1g, a, b) -> dict:
+    """The production RWMD kernels (culled FP32 tile + exact fp64 refine, both
+    sides) on one cfg2 pair: per-launch device time from CUDA events on the stream
+    each kernel runs on, work = the (source, target) distance evaluations each
+    performs x 5 FLOP (2 sub, 2 mul, 1 add), against the FP64 / FP32 pipe peaks."""
+    from paper_2110_14734_b200 import _lib
     from paper_2110_14734_b200.diagram import load_nodes
 
+    n0 = w1g.zero_condense(a, b, device=ctx.device)
+    load_nodes(ctx, _lib.NODES0, n0)
+    ms = (ctypes.c_float * 4)()
+    ev = (ctypes.c_int64 * 4)()
+    directed = ctypes.c_int64(0)
+    ctx.call("w1g_profile_rwmd", 1, ms, ev, ctypes.byref(directed))  # warm
+    ctx.call("w1g_profile_rwmd", 5, ms, ev, ctypes.byref(directed))
+    names = ["tile_a", "refine_a", "tile_b", "refine_b"]
+    per = {nm: {"ms": float(ms[i]), "evals": int(ev[i])} for i, nm in enumerate(names)}
+    ref_ms = (ms[1] + ms[3]) / 2
+    ref_ev = (ev[1] + ev[3]) / 2
+    tile_ms = (ms[0] + ms[2]) / 2
+    tile_ev = (ev[0] + ev[2]) / 2
+    f64 = 5.0 * ref_ev / (ref_ms * 1e-3) / 1e12 if ref_ms else 0.0
+    f32 = 5.0 * tile_ev / (tile_ms * 1e-3) / 1e12 if tile_ms else 0.0
+    total = sum(ms[i] for i in range(4))
+    return {
+        "bound": "fp64", "kernel": "k_refine (rwmd.cu): exact fp64 nearest-neighbour refine, the production RWMD",
+        "achieved": f64, "peak": PEAKS["fp64_tflops"], "unit": "TFLOP/s", "frac": f64 / PEAKS["fp64_tflops"],
+        "traffic": None,
+        "ms_per_launch": ref_ms, "flop_per_launch": 5.0 * ref_ev, "evals_per_launch": ref_ev,
+        "note": "achieved = 5 FLOP x the distance evaluations the launch performs (device counter) / its "
+                "event-timed duration; peak " + PEAKS["fp_source"],
+        "tile": {"bound": "fp32", "kernel": "k_rwmd_f32<2,1,256> (rwmd_tile.cu): culled FP32 seed pass",
+                 "achieved": f32, "peak": PEAKS["fp32_tflops"], "unit": "TFLOP/s",
+                 "frac": f32 / PEAKS["fp32_tflops"], "ms_per_launch": tile_ms, "evals_per_launch": tile_ev},
+        "per_kernel": per,
+        "rwmd_algorithmic": {
+            "directed_evals": int(directed.value),
+            "kernel_ms_both_sides": total,
+            "brute_force_equivalent_tflops": 5.0 * directed.value / (total * 1e-3) / 1e12 if total else None,
+            "evals_performed_frac": (sum(ev[i] for i in range(4)) / directed.value) if directed.value else None,
+            "note": "W = 2|A||B| directed evaluations (SURVEY 8d); culling performs the fraction above"},
+    }
+
+
+def north_star_kernel(ctx, w1g, n: int) -> dict:
+    """FP32 all-pairs tile kernel, full brute force, at n points per side."""
+    from paper_2110_14734_b200 import _lib, synth
+    from paper_2110_14734_b200.diagram import load_nodes
+
+    a, b = synth.gaussian_cluster_pair(n, n, seed=0)
+    n0 = w1g.zero_condense(a, b, device=ctx.device)
     load_nodes(ctx, _lib.NODES0, n0)
     ctx.call("w1g_set_rwmd_culling", 0)
     ms = ctypes.c_float(0)
     evals = ctypes.c_int64(0)
-    ctx.call("w1g_profile_rwmd_tile", 3, ctypes.byref(ms), ctypes.byref(evals))
-    ctx.call("w1g_set_rwmd_culling", 1)
+    try:
+        ctx.call("w1g_profile_rwmd_tile", 1, ctypes.byref(ms), ctypes.byref(evals))
+        ctx.call("w1g_profile_rwmd_tile", 2, ctypes.byref(ms), ctypes.byref(evals))
+    finally:
+        ctx.call("w1g_set_rwmd_culling", 1)
     tflops = 5.0 * evals.value / (ms.value * 1e-3) / 1e12
-    roofline = {"bound": "fp32", "achieved": tflops, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
-                "frac": tflops / FP32_PEAK_TFLOPS, "traffic": _ncu_traffic("k_rwmd_f32<8, 0, 1024>"),
-                "traffic_unit": "bytes/launch (dram read+write, ncu --set full, profiles/r01_ncu_rwmd_tile.jsonl)",
-                "kernel": "k_rwmd_f32 (rwmd_tile.cu)",
-                "ms_per_launch": ms.value, "evals_per_launch": evals.value,
-                "note": "5 FLOP per directed (source,target) evaluation, full brute force (culling off); "
-                        "peak = derived nominal 148 SM x 128 lanes x 2 x 1.965 GHz"}
-    stage_names = list(_lib.STAGES)
-    stage_avg = {nm: statistics.mean(s[i] for s in stage_ms) for i, nm in enumerate(stage_names)}
+    return {"bound": "fp32", "kernel": "k_rwmd_f32<8,0,1024> (rwmd_tile.cu), culling off",
+            "config": f"{n}+{n} points (gaussian_cluster_pair seed 0)", "achieved": tflops,
+            "peak": PEAKS["fp32_tflops"], "unit": "TFLOP/s", "frac": tflops / PEAKS["fp32_tflops"],
+            "ms_per_launch": ms.value, "evals_per_launch": evals.value,
+            "note": "5 FLOP per directed (source, target) evaluation; ncu sm__pipe_fma_cycles_active in profiles/"}
+
+
+def e2e_batch(w1g, diagrams, pairs, args, dist: Dist, reps: int) -> dict:
+    """sparsify_batch with host numpy in and host networks out, max over ranks."""
+    params = w1g.ApproxParams(s=args.s, best_effort=True, delta=args.delta, k=K_LATTICE)
+    nbytes = {"d2h": 0}
+    lock = threading.Lock()
+
+    def keep(i, j, net, d):
+        with lock:
+            nbytes["d2h"] += sum(getattr(net, f).nbytes for f in ("supplies", "tails", "heads", "costs",
+                                                                  "row_offsets"))
+
+    used = sorted({i for p in pairs for i in p})
+    h2d = sum(diagrams[i].nbytes for i in used)
+    w1g.sparsify_batch(diagrams, params, pairs=pairs, devices=[dist.local], streams_per_device=args.streams,
+                       on_network=keep)  # warm (pool blocks, child contexts)
+    dist.barrier()
+    times = []
+    for _ in range(reps):
+        nbytes["d2h"] = 0
+        t0 = time.perf_counter()
+        w1g.sparsify_batch(diagrams, params, pairs=pairs, devices=[dist.local], streams_per_device=args.streams,
+                           on_network=keep)
+        times.append(time.perf_counter() - t0)
+    dist.barrier()
+    t = dist.max(statistics.mean(times))
+    return {"seconds": t, "h2d": int(h2d), "d2h": int(nbytes["d2h"])}
+
+
+def e2e_single(w1g, a, b, args, device: int, flush, reps: int) -> dict:
+    """One pair through sparsify(): pinned input, pageable input, and the reference's
+    own delta schedule (delta derived from L with a host read of L)."""
+    import torch
+
+    out = {}
+    cases = {
+        "pinned_input": (w1g.pinned_points(a), w1g.pinned_points(b),
+                         w1g.ApproxParams(s=args.s, best_effort=True, delta=args.delta)),
+        "pageable_input": (a, b, w1g.ApproxParams(s=args.s, best_effort=True, delta=args.delta)),
+        "auto_delta": (a, b, w1g.ApproxParams(s=args.s, best_effort=True)),
+    }
+    for name, (x, y, params) in cases.items():
+        keep = []
+        for _ in range(3):
+            keep.append(w1g.sparsify(x, y, params, device=device))
+            keep = keep[-2:]
+        del keep
+        ts = []
+        net = diag = None
+        for _ in range(reps):
+            flush()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            net, diag = w1g.sparsify(x, y, params, device=device)
+            ts.append(time.perf_counter() - t0)
+        t = statistics.median(ts)
+        d2h = sum(getattr(net, f).nbytes for f in ("supplies", "tails", "heads", "costs", "row_offsets"))
+        out[name] = {"value": 1.0 / t, "unit": "pairs/s", "ms_per_pair": 1e3 * t,
+                     "h2d_bytes_per_step": int(a.nbytes + b.nbytes), "d2h_bytes_per_step": int(d2h),
+                     "delta": diag.delta, "device_ms": diag.stage_ms.get("total")}
+    return out
+
+
+def run_ours(args, dist: Dist):
+    import torch
+
+    import paper_2110_14734_b200 as w1g
+    from paper_2110_14734_b200 import _lib, synth
+
+    device = dist.local
+    torch.cuda.set_device(device)
+    ctx = _lib.context(device)
+    stream = torch.cuda.ExternalStream(ctx.stream, device=device)
+    flush_buf = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=f"cuda:{device}")
+
+    def flush():
+        with torch.cuda.stream(stream):
+            flush_buf.fill_(1)
+
+    if args.workload == "cfg4":
+        diagrams = synth.shared_centre_batch(*CFG4, seed=0)
+        all_pairs = [(i, j) for i in range(CFG4[0]) for j in range(i + 1, CFG4[0])]
+    else:
+        diagrams = cfg2_inputs(args)
+        all_pairs = [(2 * p, 2 * p + 1) for p in range(args.pairs)]
+    mine = rank_share(all_pairs, dist.rank, dist.world)
+    batch = Batch(ctx, diagrams, mine, args)
+    clocks = Clocks(device)
+    step_ms, launches, clk = time_batch(batch, args.steps, max(3, args.warmup), flush, dist, clocks)
+    infos = [batch.infos[i] for i in range(len(mine))]
+    e2e = e2e_batch(w1g, diagrams, mine, args, dist, reps=max(2, min(5, args.steps // 4)))
 
     extra = {}
-    if dist.rank == 0 and not args.profile_only:
-        if not args.no_cpu_baseline:
-            extra["cpu_baseline"] = cpu_front_end_sample(a, b, args.s, args.delta)
-        if args.w1:
+    if not args.no_extras:
+        a, b = diagrams[0], diagrams[1]
+        # single-pair latency on the device (the stage split of one front end)
+        single = Batch(ctx, [a, b], [(0, 1)], args)
+        single.args = argparse.Namespace(**{**vars(args), "streams": 1})
+        one_ms, _, _ = time_batch(single, max(5, args.steps), 3, flush, _NoDist())
+        extra["single_pair"] = {"device_ms": one_ms, "stage_ms": {nm: float(single.infos[0].stage_ms[i])
+                                                                 for i, nm in enumerate(_lib.STAGES)},
+                                "nodes": int(single.infos[0].n_points), "pairs": int(single.infos[0].n_pairs),
+                                "arcs": int(single.infos[0].n_arcs)}
+        extra["e2e_single_pair"] = e2e_single(w1g, a, b, args, device, flush, reps=max(5, args.steps))
+        if args.workload == "cfg2":
+            extra["roofline"] = rwmd_roofline(ctx, w1g, a, b)
+            if dist.rank == 0:
+                extra["north_star_kernel"] = north_star_kernel(ctx, w1g, 1_000_000)
+            # the cfg4 matrix over the same ranks (strong scaling of the batched workload)
+            c4 = synth.shared_centre_batch(*CFG4, seed=0)
+            p4 = [(i, j) for i in range(CFG4[0]) for j in range(i + 1, CFG4[0])]
+            b4 = Batch(ctx, c4, rank_share(p4, dist.rank, dist.world), args)
+            ms4, _, _ = time_batch(b4, 2, 1, flush, dist)
+            extra["cfg4"] = {"workload": f"{len(p4)} pairs of {CFG4[0]} shared-centre diagrams x {CFG4[1]} points, "
+                                         f"s={args.s}, delta={args.delta}, dealt round-robin over {dist.world} GPU(s)",
+                             "value": len(p4) / (ms4 * 1e-3), "unit": "pairs/s", "ms_per_step": ms4,
+                             "scaling": "strong"}
+        if dist.rank == 0 and not args.no_cpu_baseline:
+            extra["cpu_baseline"] = cpu_baselines(a, b, args)
+        if dist.rank == 0 and args.w1 and args.workload == "cfg2":
+            params = w1g.ApproxParams(s=args.s, best_effort=True, delta=args.delta)
             t0 = time.perf_counter()
             value, d = w1g.approx_w1(a, b, params, device=device)
             t_w1 = time.perf_counter() - t0
             extra["w1"] = {"value": value, "status": d.status, "pivots": d.pivots, "seconds": t_w1,
-                           "pairs_per_s": 1.0 / t_w1, "solver": "reference w1flow.simplex (host, 1 thread)"}
-    if dist.rank == 0:
-        n = dist.world
-        hs = hbm_stages(2 * args.n, int(info.n_points0), int(info.n_points), int(info.n_pairs), int(info.n_arcs),
-                        stage_avg)
-        if hs:
-            # the timed step's longest byte-moving stage against HBM (the RWMD tile above is
-            # the north star's named kernel; this says where the step's own time goes)
-            nm, st = max(hs.items(), key=lambda kv: kv[1]["ms"])
-            roofline["step_longest_stage"] = {
-                "stage": nm, "bound": "hbm", "achieved": st["gbs"], "peak": HBM_PEAK_GBS, "unit": "GB/s",
-                "frac": st["frac"], "ms": st["ms"], "algorithmic_bytes": st["bytes"],
-                "note": "latency-bound: dependent grid-wide phases (levels, sorts, round trips), "
-                        "not bandwidth; see DESIGN.md section 4"}
-        line = {
-            "metric": METRIC,
-            "value": n / (dev_ms_max * 1e-3),
-            "unit": "pairs/s",
-            "n_gpus": n,
-            "steps": args.steps,
-            "warmup": args.warmup,
-            "ms_per_step": dev_ms_max,
-            "higher_is_better": True,
-            "scaling": "weak",
-            "vs_baseline": None,
-            "dtype": "f64",
-            "data": "synthetic (reference generator gaussian_cluster_pair, seed = rank)",
-            "config": {"workload": f"cfg2: sparsify front end, {args.n}+{args.n} points, s={args.s}, "
-                                   f"delta={args.delta}, k=0.99",
-                       "pairs_per_gpu_per_step": 1, "l2": "flushed (256 MiB write) before every step",
-                       "nodes": int(info.n_points), "pairs": int(info.n_pairs), "arcs": int(info.n_arcs)},
-            "sparsify_ms": dev_ms_max,
-            "stage_ms": stage_avg,
-            "wall_s": wall,
-            "e2e": {"value": n / e2e_s, "unit": "pairs/s", "ms_per_pair": e2e_s * 1e3,
-                    "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
-            "roofline": roofline,
-            "hbm_stages": {"peak_gbs": HBM_PEAK_GBS, "note": "algorithmic bytes / stage device time; "
-                           "latency-bound at this size (few-microsecond dependent phases), see DESIGN.md",
-                           "stages": hs},
-            "gpu_launches": int(launches),
-            "clocks": clk,
-        }
-        line.update(extra)
-        print(json.dumps(line), flush=True)
+                           "solver": "reference w1flow.simplex (host, 1 thread)"}
+    if dist.rank != 0:
+        return
+    total_pairs = len(all_pairs)
+    cfg = workload_config(args)  # identical to the reference arm's
+    batch_info = {"streams_per_gpu": args.streams, "pairs_per_gpu": len(mine),
+                  "nodes_pair0": int(infos[0].n_points) if infos else 0,
+                  "tree_pairs_pair0": int(infos[0].n_pairs) if infos else 0,
+                  "arcs_pair0": int(infos[0].n_arcs) if infos else 0}
+    line = {
+        "metric": METRIC,
+        "value": total_pairs / (step_ms * 1e-3),
+        "unit": "pairs/s",
+        "n_gpus": dist.world,
+        "steps": args.steps,
+        "warmup": max(3, args.warmup),
+        "ms_per_step": step_ms,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (the reference generator, restated draw for draw in synth.py)",
+        "config": cfg,
+        "batch": batch_info,
+        "e2e": {"value": total_pairs / e2e["seconds"], "unit": "pairs/s", "ms_per_step": 1e3 * e2e["seconds"],
+                "h2d_bytes_per_step": e2e["h2d"], "d2h_bytes_per_step": e2e["d2h"],
+                "api": "paper_2110_14734_b200.sparsify_batch (host numpy diagrams -> host TransshipmentNetworks)"},
+        "gpu_launches": int(launches),
+        "clocks": clk,
+        "peaks": PEAKS,
+    }
+    if "roofline" not in extra:
+        line["roofline"] = None
+    line.update(extra)
+    print(json.dumps(line), flush=True)
+
+
+class _NoDist:
+    """Single-rank stand-in (per-rank measurements that need no barrier)."""
+
+    def barrier(self):
+        pass
+
+    def max(self, x):
+        return x
 
 
 def main():
     args = parse()
-    dist = Dist(args.gpus)
+    # the reference arm runs on rank 0 alone: no process group (other ranks exit at once)
+    dist = Dist(args.gpus, None if args.impl == "reference" else "nccl")
     try:
         if args.impl == "reference":
             run_reference(args, dist)

@@ -75,6 +75,12 @@ uint64_t w1g_launch_count(void);
  * CUDA events on the context stream; returns the mean device time per launch
  * and the directed (source, target) evaluations one launch covers */
 int w1g_profile_rwmd_tile(w1g_ctx *ctx, int reps, float *ms_per_launch, int64_t *evals_per_launch);
+/* measurement hook: the production RWMD (lower_bound.py:43-75 as w1g_rwmd runs it:
+ * culled FP32 tile pass + exact fp64 refine per side) `reps` times on nodes0, with
+ * CUDA events around each kernel on the stream it runs on and device counters of
+ * the (source, target) distance evaluations each performs.  ms[4], evals[4]: mean
+ * per launch for {A tile, A refine, B tile, B refine}; directed = 2 |A| |B| */
+int w1g_profile_rwmd(w1g_ctx *ctx, int reps, float *ms, int64_t *evals, int64_t *directed);
 /* test hook: stable device radix sort of host keys (`words` arrays of n
  * uint64, word 0 least significant); writes the sorting permutation */
 int w1g_debug_radix_sort(w1g_ctx *ctx, const uint64_t *keys, int words, int64_t n, uint32_t *perm);
@@ -179,10 +185,12 @@ int w1g_front_end_device(w1g_ctx *ctx, const double *d_a, int64_t na, const doub
  * a shared counter.  pairs = n_pairs (i, j) int32 index pairs. */
 
 /* synchronous: every front end runs, networks stay in device memory; infos
- * (n_pairs entries, may be null) receives each pair's diagnostics */
+ * (n_pairs entries, may be null) receives each pair's diagnostics; device_ms (may
+ * be null) the device makespan: CUDA events on the context stream that every
+ * child stream waits on at the start and that waits on every child at the end */
 int w1g_front_end_batch(w1g_ctx *ctx, const int32_t *pairs, int64_t n_pairs, double s, int use_condensation,
                         int delta_mode, double delta, double k, uint64_t seed, int streams,
-                        w1g_front_end_info *infos);
+                        w1g_front_end_info *infos, float *device_ms);
 
 /* one delivered network: host arrays inside a page-locked block owned by the
  * library until w1g_batch_release(block); status != W1G_OK carries the pair's error */

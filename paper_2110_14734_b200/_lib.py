@@ -97,6 +97,7 @@ _PROTOS = [
     ("w1g_host_free", ctypes.c_int, [_vp]),
     ("w1g_launch_count", ctypes.c_uint64, []),
     ("w1g_profile_rwmd_tile", ctypes.c_int, [_vp, ctypes.c_int, ctypes.POINTER(ctypes.c_float), _I64P]),
+    ("w1g_profile_rwmd", ctypes.c_int, [_vp, ctypes.c_int, ctypes.POINTER(ctypes.c_float), _I64P, _I64P]),
     ("w1g_debug_radix_sort", ctypes.c_int, [_vp, _vp, ctypes.c_int, _i64, _vp]),
     ("w1g_device_count", ctypes.c_int, [_I32P]),
     ("w1g_last_error", ctypes.c_char_p, []),
@@ -136,7 +137,8 @@ _PROTOS = [
      [_vp, _vp, _i64, _vp, _i64, _f64, ctypes.c_int, ctypes.c_int, _f64, _f64, _u64,
       ctypes.POINTER(FrontEndInfo)]),
     ("w1g_front_end_batch", ctypes.c_int,
-     [_vp, _vp, _i64, _f64, ctypes.c_int, ctypes.c_int, _f64, _f64, _u64, ctypes.c_int, ctypes.POINTER(FrontEndInfo)]),
+     [_vp, _vp, _i64, _f64, ctypes.c_int, ctypes.c_int, _f64, _f64, _u64, ctypes.c_int, ctypes.POINTER(FrontEndInfo),
+      ctypes.POINTER(ctypes.c_float)]),
     ("w1g_batch_begin", ctypes.c_int,
      [_vp, _vp, _i64, _f64, ctypes.c_int, ctypes.c_int, _f64, _f64, _u64, ctypes.c_int, _i64]),
     ("w1g_batch_next", ctypes.c_int, [_vp, ctypes.POINTER(BatchResult)]),

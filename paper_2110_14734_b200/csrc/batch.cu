@@ -151,6 +151,8 @@ struct BatchState {
     int first_rc = W1G_OK;
     std::string first_err;
     bool active = false;
+    cudaEvent_t ev_start = nullptr, ev_end = nullptr;  // device makespan of a synchronous batch
+    std::vector<cudaEvent_t> kid_ev;
 };
 
 static void batch_join(BatchState &b) {
@@ -300,6 +302,9 @@ void batch_destroy(Ctx &c) {
     for (auto &r : b.ready)
         if (r.block) host_pool().put(r.block);
     for (w1g_ctx *x : b.kids) w1g_ctx_destroy(x);
+    for (cudaEvent_t e : b.kid_ev) cudaEventDestroy(e);
+    if (b.ev_start) cudaEventDestroy(b.ev_start);
+    if (b.ev_end) cudaEventDestroy(b.ev_end);
     delete c.batch;
     c.batch = nullptr;
 }
@@ -312,15 +317,36 @@ extern "C" {
 
 int w1g_front_end_batch(w1g_ctx *c, const int32_t *pairs, int64_t n_pairs, double s, int use_condensation,
                         int delta_mode, double delta, double k, uint64_t seed, int streams,
-                        w1g_front_end_info *infos) {
+                        w1g_front_end_info *infos, float *device_ms) {
     if (!c) return W1G_EINVAL;
     cudaSetDevice(c->device);
     BatchParams prm{s, delta, k, use_condensation, delta_mode, seed};
-    W1G_TRY(batch_start(*c, pairs, n_pairs, prm, streams, false, infos));
+    if (!c->batch) c->batch = new BatchState();
     BatchState &b = *c->batch;
+    W1G_TRY(ensure_kids(*c, b, streams));
+    // device makespan: every child stream starts after an event on the parent
+    // stream, and the parent stream's end event waits for every child
+    if (!b.ev_start) {
+        W1G_CUDA(cudaEventCreate(&b.ev_start));
+        W1G_CUDA(cudaEventCreate(&b.ev_end));
+    }
+    while (b.kid_ev.size() < b.kids.size()) {
+        cudaEvent_t e;
+        W1G_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        b.kid_ev.push_back(e);
+    }
+    W1G_CUDA(cudaEventRecord(b.ev_start, c->stream));
+    for (w1g_ctx *x : b.kids) W1G_CUDA(cudaStreamWaitEvent(x->stream, b.ev_start, 0));
+    W1G_TRY(batch_start(*c, pairs, n_pairs, prm, streams, false, infos));
     batch_join(b);
     b.active = false;
-    for (w1g_ctx *x : b.kids) W1G_CUDA(cudaStreamSynchronize(x->stream));
+    for (size_t w = 0; w < b.kids.size(); w++) {
+        W1G_CUDA(cudaEventRecord(b.kid_ev[w], b.kids[w]->stream));
+        W1G_CUDA(cudaStreamWaitEvent(c->stream, b.kid_ev[w], 0));
+    }
+    W1G_CUDA(cudaEventRecord(b.ev_end, c->stream));
+    W1G_CUDA(cudaEventSynchronize(b.ev_end));
+    if (device_ms) W1G_CUDA(cudaEventElapsedTime(device_ms, b.ev_start, b.ev_end));
     if (b.first_rc != W1G_OK) {
         set_error("%s", b.first_err.c_str());
         return b.first_rc;

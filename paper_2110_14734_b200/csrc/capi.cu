@@ -196,6 +196,16 @@ int w1g_profile_rwmd_tile(w1g_ctx *c, int reps, float *ms_per_launch, int64_t *e
     return rwmd_tile_profile(*c, reps, ms_per_launch, evals_per_launch);
 }
 
+int w1g_profile_rwmd(w1g_ctx *c, int reps, float *ms, int64_t *evals, int64_t *directed) {
+    CTX_CHECK(c);
+    if (!ms || !evals || !directed) return W1G_EINVAL;
+    if (!c->nodes[0].valid) {
+        set_error("profile_rwmd: no nodes0");
+        return W1G_ESTATE;
+    }
+    return rwmd_profile(*c, reps, ms, evals, directed);
+}
+
 const char *w1g_last_error(void) { return g_err; }
 
 int w1g_device_count(int *count) {
@@ -291,6 +301,11 @@ int w1g_ctx_destroy(w1g_ctx *c) {
         free_buf(ns.exb);
     }
     for (auto &b : c->scr) free_buf(b);
+    free_buf(c->prof_cnt);
+    for (auto &side : c->prof_ev)
+        for (auto &kind : side)
+            for (auto &e : kind)
+                if (e) cudaEventDestroy(e);
     free_buf(c->corpus_pts);
     free_buf(c->query_pts);
     for (auto &b : c->dense_scr) free_buf(b);

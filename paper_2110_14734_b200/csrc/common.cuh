@@ -158,6 +158,12 @@ struct Ctx {
     int culling = 1;
     int cull_steps = 0;  // 0 = by size; W1G_CULL_STEPS overrides (tuning)
     int debug_radius = 0;  // W1G_DEBUG_RADIUS=1: rwmd "best" reports the exact-pass radius
+    // RWMD kernel profiling (w1g_profile_rwmd): events around the FP32 tile and the
+    // exact refine kernels of each side, and device counters of the (source,
+    // target) evaluations they perform: [side][0 = tile, 1 = refine]
+    int prof = 0, prof_side = 0;
+    cudaEvent_t prof_ev[2][2][2] = {};
+    DevBuf prof_cnt;  // 4 x unsigned long long
     int heavy_ratio = 16;  // exact pass: disc / median disc beyond which a source is searched alone (W1G_HEAVY, 0 off)
     DevBuf best[2];
     int64_t n_best[2] = {0, 0};
@@ -518,6 +524,7 @@ int zc_run(Ctx &c, const double2 *d_a, int64_t na, const double2 *d_b, int64_t n
            int32_t *balanced, bool speculative = true);
 int rwmd_run(Ctx &c, double *L, double *LA, double *LB);
 int rwmd_tile_profile(Ctx &c, int reps, float *ms, int64_t *evals);
+int rwmd_profile(Ctx &c, int reps, float *ms, int64_t *evals, int64_t *directed);
 int rwmd_range_run(Ctx &c, int side, int64_t begin, int64_t end, double *partial, int64_t *n_members);
 // src: the node set to condense (default nodes[0]); the result goes to nodes[1]
 int dc_run(Ctx &c, double delta, double pitch, double half_width, uint64_t seed, int64_t *k,

@@ -212,10 +212,11 @@ __device__ __forceinline__ double gap2(double4 b, double4 a) {  // squared box g
 // is exact.  All lanes return the same m2.
 __device__ double solo_nn(double2 pj, double rad, const double2 *__restrict__ t, int64_t nt,
                           const double4 *__restrict__ tbox, const double4 *__restrict__ sbox, int64_t ntile,
-                          int64_t nsup, int lane) {
+                          int64_t nsup, int lane, unsigned long long *evals) {
     const double4 pb = make_double4(pj.x, pj.y, pj.x, pj.y);
     double m2 = INFINITY, R = rad;
     auto eval_tile = [&](int64_t k) {
+        if (evals && lane == 0) atomicAdd(evals, (unsigned long long)RT);
         double ma = INFINITY;
         for (int64_t jt = k * RT + lane; jt < min(nt, (k + 1) * RT); jt += 32) {
             const double2 ta = t[jt];
@@ -317,7 +318,7 @@ __global__ void __launch_bounds__(RF_BLOCK) k_refine(const double2 *__restrict__
                                                      const double4 *__restrict__ tbox,
                                                      const double4 *__restrict__ sbox,
                                                      double *__restrict__ best_out, double *__restrict__ terms,
-                                                     int direct) {
+                                                     int direct, unsigned long long *evals) {
     __shared__ int32_t s_cand[RF_CAND];
     __shared__ int32_t s_sup[RF_SUPCAP];
     __shared__ double2 s_t[RF_STAGE * RT];
@@ -456,6 +457,7 @@ __global__ void __launch_bounds__(RF_BLOCK) k_refine(const double2 *__restrict__
                 for (int c = 0; c < ns; c++) {
                     const bool need = valid && r >= 0.0 && within(s_tb[c], pb, r * (1.0 + 1e-9));
                     if (!__any_sync(0xffffffffu, need)) continue;
+                    if (evals && lane == 0) atomicAdd(evals, (unsigned long long)(32 / RF_TPQ) * RT);
                     const double2 *st = s_t + c * RT + sub;
 #pragma unroll
                     for (int j = 0; j < RT / RF_TPQ; j += 2) {
@@ -485,7 +487,7 @@ __global__ void __launch_bounds__(RF_BLOCK) k_refine(const double2 *__restrict__
             unsigned m = s_hmask[w2];
             for (int q = 0; q < kk; q++) m &= m - 1;
             const int j = w2 * (32 / RF_TPQ) + (__ffs(m) - 1) / RF_TPQ;
-            const double ms = solo_nn(s_p[j], s_solo_r[j], t, nt, tbox, sbox, ntile, nsup, lane);
+            const double ms = solo_nn(s_p[j], s_solo_r[j], t, nt, tbox, sbox, ntile, nsup, lane, evals);
             if (lane == 0) s_solo_m2[j] = ms;
         }
         if (H) __syncthreads();  // H is block-uniform
@@ -514,9 +516,12 @@ static int launch_refine(Ctx &c, const double2 *q, const int32_t *qpos, const in
                          double *terms) {
     // bit 0 culled (direct-form bound), bit 1 debug, bits 8+ heavy ratio (0: off)
     const int flags = c.culling | (c.debug_radius << 1) | (c.heavy_ratio << 8);
+    unsigned long long *evals = c.prof ? ptr<unsigned long long>(c.prof_cnt) + 2 * c.prof_side + 1 : nullptr;
+    if (c.prof) W1G_CUDA(cudaEventRecord(c.prof_ev[c.prof_side][1][0], c.stream));
     k_refine<<<(unsigned)((nq + RF_QPB - 1) / RF_QPB), RF_BLOCK, 0, c.stream>>>(
-        q, qpos, members, mass, nq, mf, qn, unscale, t, nt, tbox, sbox, best, terms, flags);
+        q, qpos, members, mass, nq, mf, qn, unscale, t, nt, tbox, sbox, best, terms, flags, evals);
     W1G_CHECK_LAUNCH();
+    if (c.prof) W1G_CUDA(cudaEventRecord(c.prof_ev[c.prof_side][1][1], c.stream));
     return W1G_OK;
 }
 
@@ -650,6 +655,7 @@ int rwmd_run(Ctx &c, double *L, double *LA, double *LB) {
     const bool conc = side && F.nm[0] > 0 && F.nm[1] > 0 && c.pw_n[1] == F.nm[1];
     auto run_side = [&](int s) -> int {
         const int o = 1 - s;
+        c.prof_side = s;
         const int64_t n_src = F.nm[s], n_dst = F.nm[o];
         c.n_best[s] = n_src;
         double *best = best_s[s];
@@ -785,6 +791,53 @@ int rwmd_tile_profile(Ctx &c, int reps, float *ms, int64_t *evals) {
     float t = 0.f;
     W1G_CUDA(cudaEventElapsedTime(&t, c.ev[8], c.ev[9]));
     *ms = t / (2.0f * reps);
+    return W1G_OK;
+}
+
+// measurement hook (w1g_profile_rwmd): the production RWMD (culled FP32 tile +
+// exact fp64 refine per side, both sides as rwmd_run schedules them) `reps`
+// times, with events around each side's tile and refine kernels (on the stream
+// each runs on) and device counters of the evaluations they perform.
+// ms[4] / evals[4]: mean per launch for [A tile, A refine, B tile, B refine];
+// directed = 2 |A| |B| (the algorithmic all-pairs work).
+int rwmd_profile(Ctx &c, int reps, float *ms, int64_t *evals, int64_t *directed) {
+    for (int i = 0; i < 4; i++) {
+        ms[i] = 0.f;
+        evals[i] = 0;
+    }
+    *directed = 0;
+    if (c.nodes[0].k == 0 || reps < 1) return W1G_OK;
+    for (auto &side : c.prof_ev)
+        for (auto &kind : side)
+            for (auto &e : kind)
+                if (!e) W1G_CUDA(cudaEventCreate(&e));
+    unsigned long long *cnt;
+    W1G_TRY(ensure(c.prof_cnt, 4, &cnt));
+    W1G_CUDA(cudaMemsetAsync(cnt, 0, 4 * sizeof(unsigned long long), c.stream));
+    double acc[4] = {0, 0, 0, 0};
+    struct Off {
+        Ctx &c;
+        ~Off() { c.prof = 0; }
+    } off{c};
+    for (int r = 0; r < reps; r++) {
+        c.prof = 1;
+        double L, la, lb;
+        W1G_TRY(rwmd_run(c, &L, &la, &lb));  // ends with a host synchronisation
+        c.prof = 0;
+        for (int s = 0; s < 2; s++)
+            for (int k = 0; k < 2; k++) {
+                float t = 0.f;
+                if (cudaEventElapsedTime(&t, c.prof_ev[s][k][0], c.prof_ev[s][k][1]) == cudaSuccess) acc[2 * s + k] += t;
+                cudaGetLastError();
+            }
+    }
+    unsigned long long h[4];
+    W1G_CUDA(cudaMemcpy(h, cnt, sizeof h, cudaMemcpyDeviceToHost));
+    for (int i = 0; i < 4; i++) {
+        ms[i] = (float)(acc[i] / reps);
+        evals[i] = (int64_t)(h[i] / (unsigned long long)reps);
+    }
+    *directed = 2 * c.rw_members[0] * c.rw_members[1];
     return W1G_OK;
 }
 

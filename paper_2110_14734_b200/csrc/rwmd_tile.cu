@@ -58,6 +58,7 @@ struct TileArgs {
     float *qn_out;          // |q'| per source
     int chunk;              // targets per grid.y chunk (full mode)
     int cull_steps;         // culled mode: tiles walked outward from the Morton position
+    unsigned long long *evals;  // profiling: evaluations performed (null: not counted)
 };
 
 template <int R, bool CULL, int T_TS>
@@ -200,6 +201,7 @@ __global__ void __launch_bounds__(T_BLOCK) k_rwmd_f32(TileArgs A) {
         }
         __syncthreads();
         const int pairs = (cnt + 1) >> 1;
+        if (A.evals && tid == 0) atomicAdd(A.evals, (unsigned long long)(T_BLOCK * R) * (unsigned long long)(2 * pairs));
 #pragma unroll 4
         for (int j = 0; j < pairs; j++) {
             const float4 v = s_xy[j];
@@ -291,6 +293,7 @@ int rwmd_f32_min(Ctx &c, const double2 *q, const uint64_t *qkey, int64_t nq, con
     A.scale = scale;
     A.mout = mout;
     A.qn_out = qn_out;
+    A.evals = c.prof ? ptr<unsigned long long>(c.prof_cnt) + 2 * c.prof_side : nullptr;
     // tiles walked per CTA in culled mode: the centre tile and its two Morton
     // neighbours (measured: 3 seeds cfg2 and 1M points as tightly as 5 -- same
     // exact-pass time -- while 1-2 do not; the few sources a short walk leaves
@@ -303,8 +306,10 @@ int rwmd_f32_min(Ctx &c, const double2 *q, const uint64_t *qkey, int64_t nq, con
         constexpr int R = 2;
         const int gx = (int)((nq + T_BLOCK * R - 1) / (T_BLOCK * R));
         A.chunk = (int)nt;
+        if (c.prof) W1G_CUDA(cudaEventRecord(c.prof_ev[c.prof_side][0][0], c.stream));
         k_rwmd_f32<R, true, TS_CULL><<<gx, T_BLOCK, 0, c.stream>>>(A);
         W1G_CHECK_LAUNCH();
+        if (c.prof) W1G_CUDA(cudaEventRecord(c.prof_ev[c.prof_side][0][1], c.stream));
         return W1G_OK;
     }
     constexpr int R = 8;
@@ -321,8 +326,10 @@ int rwmd_f32_min(Ctx &c, const double2 *q, const uint64_t *qkey, int64_t nq, con
     chunk = (chunk + 1) & ~1;
     gy = (int)((nt + chunk - 1) / chunk);
     A.chunk = chunk;
+    if (c.prof) W1G_CUDA(cudaEventRecord(c.prof_ev[c.prof_side][0][0], c.stream));
     k_rwmd_f32<R, false, TS_FULL><<<dim3(gx, gy), T_BLOCK, 0, c.stream>>>(A);
     W1G_CHECK_LAUNCH();
+    if (c.prof) W1G_CUDA(cudaEventRecord(c.prof_ev[c.prof_side][0][1], c.stream));
     return W1G_OK;
 }
 
