@@ -224,6 +224,11 @@ int w1g_batch_end(w1g_ctx *ctx);
 /* upload a diagram corpus once: points of all diagrams back to back ((total,2)
  * float64), diagram i = rows [offsets[i], offsets[i+1]) (n_diagrams + 1 offsets) */
 int w1g_corpus_load(w1g_ctx *ctx, const double *points, const int64_t *offsets, int64_t n_diagrams);
+/* a host-resident corpus for the batch executor: the caller's (n_i, 2) float64
+ * arrays (kept alive and unchanged until the batch ends); each worker copies its
+ * pair's two diagrams to the device inside its own front end, so uploads overlap
+ * the other workers' compute (page-locked arrays are DMA'd directly) */
+int w1g_corpus_set_host(w1g_ctx *ctx, const double *const *points, const int64_t *sizes, int64_t n_diagrams);
 /* replaces lower_bound.wcd (lower_bound.py:78-92) for query vs corpus[candidates[i]],
  * all candidates in one launch: scores[i] = wcd(query, corpus[candidates[i]]) bit for bit */
 int w1g_wcd_corpus(w1g_ctx *ctx, const double *query, int64_t nq, const int64_t *candidates,

@@ -145,6 +145,7 @@ _PROTOS = [
     ("w1g_batch_release", ctypes.c_int, [_vp]),
     ("w1g_batch_end", ctypes.c_int, [_vp]),
     ("w1g_corpus_load", ctypes.c_int, [_vp, _F64P, _I64P, _i64]),
+    ("w1g_corpus_set_host", ctypes.c_int, [_vp, _vp, _I64P, _i64]),
     ("w1g_wcd_corpus", ctypes.c_int, [_vp, _F64P, _i64, _I64P, _i64, _F64P]),
     ("w1g_rwmd_corpus", ctypes.c_int, [_vp, _F64P, _i64, _I64P, _i64, _F64P]),
     ("w1g_dense_network", ctypes.c_int, [_vp, _I64P, _I64P]),

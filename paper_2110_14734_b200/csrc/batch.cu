@@ -200,12 +200,20 @@ static void batch_worker(Ctx *parent, BatchState *b, int w) {
                 rc = w1g_set_network_out(x, cv.sup, cv.t, cv.h, cv.c, cv.ro, ncap, mcap);
             }
         }
-        const double *pa = reinterpret_cast<const double *>(corpus + off[i]);
-        const double *pb = reinterpret_cast<const double *>(corpus + off[j]);
-        if (rc == W1G_OK)
-            rc = w1g_front_end_device(x, pa, off[i + 1] - off[i], pb, off[j + 1] - off[j], b->prm.s,
-                                      b->prm.use_condensation, b->prm.delta_mode, b->prm.delta, b->prm.k,
-                                      b->prm.seed, &r.info);
+        if (rc == W1G_OK) {
+            if (parent->h_corpus_ptr) {
+                // host-resident diagrams: this worker's H2D overlaps the other workers' front ends
+                rc = w1g_front_end(x, parent->h_corpus_ptr[i], off[i + 1] - off[i], parent->h_corpus_ptr[j],
+                                   off[j + 1] - off[j], b->prm.s, b->prm.use_condensation, b->prm.delta_mode,
+                                   b->prm.delta, b->prm.k, b->prm.seed, &r.info);
+            } else {
+                const double *pa = reinterpret_cast<const double *>(corpus + off[i]);
+                const double *pb = reinterpret_cast<const double *>(corpus + off[j]);
+                rc = w1g_front_end_device(x, pa, off[i + 1] - off[i], pb, off[j + 1] - off[j], b->prm.s,
+                                          b->prm.use_condensation, b->prm.delta_mode, b->prm.delta, b->prm.k,
+                                          b->prm.seed, &r.info);
+            }
+        }
         if (rc == W1G_OK && b->deliver && !r.info.short_circuit) {
             const int64_t n = r.info.node_count, m = r.info.n_arcs;
             b->hint_n[w] = n;
@@ -275,7 +283,7 @@ static int batch_start(Ctx &c, const int32_t *pairs, int64_t n_pairs, const Batc
         return W1G_ESTATE;
     }
     W1G_TRY(ensure_kids(c, b, streams));
-    W1G_CUDA(cudaStreamSynchronize(c.stream));  // the corpus upload is complete
+    if (!c.h_corpus_ptr) W1G_CUDA(cudaStreamSynchronize(c.stream));  // the corpus upload is complete
     b.pairs.assign(pairs, pairs + 2 * n_pairs);
     b.n_pairs = n_pairs;
     b.prm = prm;

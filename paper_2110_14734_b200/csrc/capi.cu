@@ -310,6 +310,7 @@ int w1g_ctx_destroy(w1g_ctx *c) {
     free_buf(c->query_pts);
     for (auto &b : c->dense_scr) free_buf(b);
     delete[] c->h_corpus_off;
+    delete[] c->h_corpus_ptr;
     for (int s2 = 0; s2 < 2; s2++) {
         free_buf(c->pw_nodes[s2]);
         free_buf(c->pw_lev[s2]);
@@ -732,6 +733,11 @@ static int copy_network_out(Ctx &c, int *copied) {
 int w1g_corpus_load(w1g_ctx *c, const double *points, const int64_t *offsets, int64_t n_diagrams) {
     CTX_CHECK(c);
     return corpus_load(*c, points, offsets, n_diagrams);
+}
+
+int w1g_corpus_set_host(w1g_ctx *c, const double *const *points, const int64_t *sizes, int64_t n_diagrams) {
+    CTX_CHECK(c);
+    return corpus_set_host(*c, points, sizes, n_diagrams);
 }
 
 int w1g_wcd_corpus(w1g_ctx *c, const double *query, int64_t nq, const int64_t *candidates, int64_t n_candidates,

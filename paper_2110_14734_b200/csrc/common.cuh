@@ -248,6 +248,9 @@ struct Ctx {
     DevBuf corpus_pts, query_pts, dense_scr[4];
     int64_t corpus_n = -1;
     int64_t *h_corpus_off = nullptr;  // host copy of the offsets (n + 1)
+    // host-resident corpus (w1g_corpus_set_host): the caller's arrays, copied to the
+    // device per pair inside each batch worker's front end (overlapping other pairs)
+    const double **h_corpus_ptr = nullptr;
 
     // one-shot host target for the next fused front end's network (w1g_set_network_out)
     struct NetOut {
@@ -550,6 +553,7 @@ int assemble_supplies(Ctx &c, int64_t **d_sup, int64_t *n);
 // corpus.cu: a resident diagram corpus, WCD / RWMD scores of a query against it
 // (pipeline.py:191-243 nn_search stages), the dense exact-oracle network (oracle.py:66-93)
 int corpus_load(Ctx &c, const double *pts, const int64_t *offsets, int64_t n);
+int corpus_set_host(Ctx &c, const double *const *pts, const int64_t *sizes, int64_t n);
 int wcd_corpus(Ctx &c, const double *query, int64_t nq, const int64_t *cand, int64_t ncand, double *scores);
 int rwmd_corpus(Ctx &c, const double *query, int64_t nq, const int64_t *cand, int64_t ncand, double *scores);
 int dense_network_run(Ctx &c, int64_t *node_count, int64_t *n_arcs);

@@ -172,6 +172,8 @@ int corpus_load(Ctx &c, const double *pts, const int64_t *offsets, int64_t n) {
     if (total) W1G_CUDA(cudaMemcpyAsync(d, pts, sizeof(double2) * total, cudaMemcpyHostToDevice, c.stream));
     W1G_CUDA(cudaMemcpyAsync(doff, offsets, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, c.stream));
     delete[] c.h_corpus_off;
+    delete[] c.h_corpus_ptr;
+    c.h_corpus_ptr = nullptr;
     c.h_corpus_off = new int64_t[n + 1];
     memcpy(c.h_corpus_off, offsets, sizeof(int64_t) * (n + 1));
     c.corpus_n = n;
@@ -179,7 +181,34 @@ int corpus_load(Ctx &c, const double *pts, const int64_t *offsets, int64_t n) {
     return W1G_OK;
 }
 
+int corpus_set_host(Ctx &c, const double *const *pts, const int64_t *sizes, int64_t n) {
+    if (n < 0 || (n && (!pts || !sizes))) {
+        set_error("corpus: bad arguments");
+        return W1G_EINVAL;
+    }
+    delete[] c.h_corpus_off;
+    delete[] c.h_corpus_ptr;
+    c.h_corpus_off = new int64_t[n + 1];
+    c.h_corpus_ptr = new const double *[n + 1];
+    c.h_corpus_off[0] = 0;
+    for (int64_t i = 0; i < n; i++) {
+        if (sizes[i] < 0) {
+            set_error("corpus: negative diagram size");
+            c.corpus_n = -1;
+            return W1G_EINVAL;
+        }
+        c.h_corpus_ptr[i] = pts[i];
+        c.h_corpus_off[i + 1] = c.h_corpus_off[i] + sizes[i];
+    }
+    c.corpus_n = n;
+    return W1G_OK;
+}
+
 static int check_candidates(Ctx &c, const int64_t *cand, int64_t ncand) {
+    if (c.corpus_n >= 0 && c.h_corpus_ptr) {
+        set_error("the corpus is host-resident (w1g_corpus_set_host); scoring needs w1g_corpus_load");
+        return W1G_ESTATE;
+    }
     if (c.corpus_n < 0) {
         set_error("no corpus loaded (w1g_corpus_load)");
         return W1G_ESTATE;

@@ -206,12 +206,16 @@ def _device_pairs(pts, share, params, dev: int, streams: int, on_network) -> Non
     run the front ends on child contexts, and this thread receives each network
     (zero-copy, page-locked) as it completes -- no Python in the per-pair loop
     on the device side."""
-    from .lower_bound import load_corpus
     from .network import TransshipmentNetwork
 
     if not share:
         return
-    ctx = load_corpus(pts, dev)
+    # the diagrams stay in host memory: each library worker uploads its own pair
+    # inside its front end, overlapping the others (no up-front bulk copy)
+    ctx = _lib.context(dev)
+    ptrs = (ctypes.c_void_p * max(1, len(pts)))(*[_lib.addr(p) for p in pts])
+    sizes = np.array([p.shape[0] for p in pts], dtype=np.int64)
+    ctx.call("w1g_corpus_set_host", ptrs, _lib.i64p(sizes), len(pts))
     pairs = np.ascontiguousarray(np.asarray(share, dtype=np.int32).reshape(-1, 2))
     delta = getattr(params, "delta", None)
     ctx.call("w1g_batch_begin", pairs.ctypes.data, pairs.shape[0], float(params.s),
