@@ -115,6 +115,12 @@ int w1g_fetch_rwmd_best(w1g_ctx *ctx, int side, double *best, int64_t *n);
  * partial sums combine bit-exactly; also returns the side's member count */
 int w1g_rwmd_range(w1g_ctx *ctx, int side, int64_t begin, int64_t end, double *partial,
                    int64_t *n_members);
+/* RWMD of one pair with its rows sharded over G contexts (G devices of one process, or
+ * several contexts of one device): every context must hold the same nodes0; the rows are
+ * cut along numpy's pairwise-summation tree (subtree t -> context t % G), each context
+ * sums its subtrees on its own device and host thread, and the host recombines them in
+ * the tree's order -- bit-identical to w1g_rwmd */
+int w1g_rwmd_sharded(w1g_ctx **ctxs, int G, double *L, double *LA, double *LB);
 /* tile culling in the FP32 all-pairs pass: 1 (default) or 0 (full brute force) */
 int w1g_set_rwmd_culling(w1g_ctx *ctx, int enabled);
 
@@ -142,6 +148,10 @@ int w1g_load_tree(w1g_ctx *ctx, const double *points, int64_t n_points, const in
  * DFS pop order); 0 leaves them in frontier order (the fused path). */
 int w1g_wspd(w1g_ctx *ctx, double s, int reference_order, int64_t *n_pairs);
 int w1g_fetch_pairs(w1g_ctx *ctx, int64_t *node_pairs, int64_t *indices);
+/* one GPU's share of a sharded WSPD (the owner loop of spanner.py:206-241
+ * split over GPUs): the recursions of the internal nodes w with w % n_shards == shard, in
+ * frontier order; the shards' pair sets partition the full WSPD */
+int w1g_wspd_shard(w1g_ctx *ctx, double s, int shard, int n_shards, int64_t *n_pairs);
 /* pairs per internal node, internal nodes in id order (count_pairs output) */
 int w1g_fetch_pair_counts(w1g_ctx *ctx, int64_t *counts, int64_t *n_internal);
 /* upload WSPairList.indices and .points (spanner.py:67-81) for a standalone emit_arcs */
@@ -151,6 +161,15 @@ int w1g_load_pairs(w1g_ctx *ctx, const int64_t *indices, int64_t n_pairs, const 
 /* replaces spanner.emit_arcs, spanner.py:310-337, over slot W1G_NODES */
 int w1g_emit_arcs(w1g_ctx *ctx, int64_t *n_arcs);
 int w1g_fetch_arcs(w1g_ctx *ctx, int64_t *tails, int64_t *heads, double *costs);
+/* the arcs of the context's pairs only (both directions, spanner.py:319-326), plus the
+ * diagonal and free arcs when with_diagonal (:327-335): one shard's slice of emit_arcs */
+int w1g_emit_pair_arcs(w1g_ctx *ctx, int with_diagonal, int64_t *n_arcs);
+/* device pointers of the context's arc list (int64 tails, int64 heads, float64 costs): the
+ * send buffers of the multi-GPU arc gather (valid until the next stage call) */
+int w1g_arcs_device(w1g_ctx *ctx, void **tails, void **heads, void **costs, int64_t *m);
+/* adopt an arc list already in this device's memory (the gathered slices), device to device */
+int w1g_load_arcs_device(w1g_ctx *ctx, const int64_t *d_tails, const int64_t *d_heads, const double *d_costs,
+                         int64_t m);
 int w1g_load_arcs(w1g_ctx *ctx, const int64_t *tails, const int64_t *heads, const double *costs,
                   int64_t m);
 

@@ -552,6 +552,25 @@ int w1g_wspd(w1g_ctx *c, double s, int reference_order, int64_t *n_pairs) {
     return wspd_run(*c, s, reference_order, n_pairs);
 }
 
+int w1g_wspd_shard(w1g_ctx *c, double s, int shard, int n_shards, int64_t *n_pairs) {
+    CTX_CHECK(c);
+    if (!(s > 0.0)) {
+        set_error("s must be positive");
+        return W1G_EINVAL;
+    }
+    if (n_shards < 1 || shard < 0 || shard >= n_shards || !n_pairs) {
+        set_error("wspd_shard: shard %d of %d", shard, n_shards);
+        return W1G_EINVAL;
+    }
+    if (!c->tree_valid) {
+        set_error("wspd: no split tree");
+        return W1G_ESTATE;
+    }
+    c->arcs_valid = false;
+    c->net_valid = false;
+    return wspd_run(*c, s, 0, n_pairs, true, shard, n_shards);
+}
+
 int w1g_fetch_pairs(w1g_ctx *c, int64_t *node_pairs, int64_t *indices) {
     CTX_CHECK(c);
     if (!c->pairs_valid) {
@@ -623,6 +642,51 @@ int w1g_emit_arcs(w1g_ctx *c, int64_t *n_arcs) {
     }
     c->net_valid = false;
     return emit_run(*c, n_arcs);
+}
+
+int w1g_emit_pair_arcs(w1g_ctx *c, int with_diagonal, int64_t *n_arcs) {
+    CTX_CHECK(c);
+    if (!c->pairs_valid || !c->nodes[1].valid) {
+        set_error("emit_pair_arcs: needs pairs and nodes");
+        return W1G_ESTATE;
+    }
+    c->net_valid = false;
+    W1G_TRY(emit_run(*c, n_arcs, with_diagonal != 0));
+    W1G_TRY(stream_sync(*c));
+    return W1G_OK;
+}
+
+int w1g_arcs_device(w1g_ctx *c, void **tails, void **heads, void **costs, int64_t *m) {
+    CTX_CHECK(c);
+    if (!c->arcs_valid) {
+        set_error("no arcs");
+        return W1G_ESTATE;
+    }
+    *tails = c->arc_t.p;
+    *heads = c->arc_h.p;
+    *costs = c->arc_c.p;
+    *m = c->n_arcs;
+    return W1G_OK;
+}
+
+int w1g_load_arcs_device(w1g_ctx *c, const int64_t *d_tails, const int64_t *d_heads, const double *d_costs,
+                         int64_t m) {
+    CTX_CHECK(c);
+    if (m < 0 || m >= (1ll << 32)) return W1G_EINVAL;
+    int64_t *t, *h;
+    double *cs;
+    W1G_TRY(ensure(c->arc_t, (size_t)m + 1, &t));
+    W1G_TRY(ensure(c->arc_h, (size_t)m + 1, &h));
+    W1G_TRY(ensure(c->arc_c, (size_t)m + 1, &cs));
+    if (m) {
+        W1G_CUDA(cudaMemcpyAsync(t, d_tails, sizeof(int64_t) * m, cudaMemcpyDeviceToDevice, c->stream));
+        W1G_CUDA(cudaMemcpyAsync(h, d_heads, sizeof(int64_t) * m, cudaMemcpyDeviceToDevice, c->stream));
+        W1G_CUDA(cudaMemcpyAsync(cs, d_costs, sizeof(double) * m, cudaMemcpyDeviceToDevice, c->stream));
+    }
+    c->n_arcs = m;
+    c->arcs_valid = true;
+    c->net_valid = false;
+    return W1G_OK;
 }
 
 int w1g_fetch_arcs(w1g_ctx *c, int64_t *tails, int64_t *heads, double *costs) {

@@ -545,9 +545,13 @@ int tree_deferred_check(Ctx &c, int32_t *depth);
 // h_pinned slots no flags fetch touches
 enum { H_LEX_MAXRUN = F_NSLOTS - 4, H_TREE_DEPTH = F_NSLOTS - 2, H_TREE_DUP = F_NSLOTS - 1 };
 int tree_geom(Ctx &c);
-int wspd_run(Ctx &c, double s, int reference_order, int64_t *n_pairs, bool want_idx = true);
+// shard / n_shards (fused order only): the recursions of the internal nodes w with
+// w % n_shards == shard -- one GPU's share of a sharded WSPD
+int wspd_run(Ctx &c, double s, int reference_order, int64_t *n_pairs, bool want_idx = true, int shard = 0,
+             int n_shards = 1);
 int wspd_pair_idx(Ctx &c);  // pair_idx from pair_uv and the tree's reps, unless current
-int emit_run(Ctx &c, int64_t *n_arcs);
+// with_diagonal = false: only the pairs' arcs (both directions), no diagonal / free arcs
+int emit_run(Ctx &c, int64_t *n_arcs, bool with_diagonal = true);
 int net_run(Ctx &c, const int64_t *d_supplies, int64_t n, int64_t *n_arcs);
 int assemble_supplies(Ctx &c, int64_t **d_sup, int64_t *n);
 // corpus.cu: a resident diagram corpus, WCD / RWMD scores of a query against it

@@ -969,7 +969,7 @@ __global__ void __launch_bounds__(CSR_LB) k_sp_long_rows(const __grid_constant__
 
 }  // namespace
 
-int emit_run(Ctx &c, int64_t *n_arcs) {
+int emit_run(Ctx &c, int64_t *n_arcs, bool with_diagonal) {
     NodeSet &ns = c.nodes[1];
     const int64_t K = ns.k, P = c.n_pairs;
     const int64_t *am = ptr<int64_t>(ns.am), *bm = ptr<int64_t>(ns.bm);
@@ -990,7 +990,7 @@ int emit_run(Ctx &c, int64_t *n_arcs) {
         na = c.h_pinned[F_MISC0];
         nb = c.h_pinned[F_MISC1];
     }
-    const int64_t M = 2 * P + na + nb + 1;
+    const int64_t M = 2 * P + (with_diagonal ? na + nb + 1 : 0);
     int64_t *t, *h;
     double *cs;
     W1G_TRY(ensure(c.arc_t, (size_t)M, &t));
@@ -1002,13 +1002,15 @@ int emit_run(Ctx &c, int64_t *n_arcs) {
         k_emit_spanner<<<gs(c, P), 256, 0, c.stream>>>(ptr<int64_t>(c.pair_idx), P, pp, t, h, cs);
         W1G_CHECK_LAUNCH();
     }
-    if (K) {
+    if (K && with_diagonal) {
         k_emit_diag<<<gs(c, K), 256, 0, c.stream>>>(ptr<double2>(ns.pts), am, bm, K, exa, exb, na, 2 * P, t, h,
                                                     cs);
         W1G_CHECK_LAUNCH();
     }
-    k_emit_free<<<1, 1, 0, c.stream>>>(K, M - 1, t, h, cs);
-    W1G_CHECK_LAUNCH();
+    if (with_diagonal) {
+        k_emit_free<<<1, 1, 0, c.stream>>>(K, M - 1, t, h, cs);
+        W1G_CHECK_LAUNCH();
+    }
     c.n_arcs = M;
     c.arcs_valid = true;
     *n_arcs = M;
@@ -1225,9 +1227,14 @@ int spanner_net_run(Ctx &c, int64_t *node_count, int64_t *n_arcs) {
         return spanner_generic(c, node_count, n_arcs);
     const int64_t M = 2 * P + ns.na + ns.nb + 1;
     // W1G_SP_LONG_MAX (tests): a lower row-length limit, to exercise the fallback
-    unsigned long_max = CSR_LONG_MAX;
+    // rows longer than that are ranked by the bitmap kernel when a K-bit bitmap (+ its
+    // prefixes) fits in shared memory, whatever their length; otherwise they are
+    // limited by the CTA bitonic sort's buffer
+    const size_t bm_bytes = (size_t)8 * ((K + 31) / 32);
+    const bool bitmap_fits = bm_bytes <= 200 * 1024;
+    unsigned long_max = bitmap_fits ? 0xffffffffu : (unsigned)CSR_LONG_MAX;
     if (const char *lm = getenv("W1G_SP_LONG_MAX")) long_max = (unsigned)atoi(lm);
-    if (long_max > (unsigned)CSR_LONG_MAX) long_max = CSR_LONG_MAX;
+    if (!bitmap_fits && long_max > (unsigned)CSR_LONG_MAX) long_max = CSR_LONG_MAX;
     // rows of 257..big_max: a warp in registers, longer: the bitmap ranks (W1G_SP_BIG_MAX: tuning)
     unsigned big_max = SP_MED_MAX;
     if (const char *bm = getenv("W1G_SP_BIG_MAX")) big_max = (unsigned)atoi(bm);
@@ -1303,14 +1310,18 @@ int spanner_net_run(Ctx &c, int64_t *node_count, int64_t *n_arcs) {
     W1G_CHECK_LAUNCH();
     T.mark("big");
     {
-        // long rows: bitmap ranks while a K-bit bitmap (+ prefixes) fits in shared memory
-        const size_t bm_bytes = (size_t)8 * ((K + 31) / 32);
-        if (bm_bytes <= 200 * 1024) {
+        // long rows: bitmap ranks while a K-bit bitmap (+ prefixes) fits in shared memory;
+        // as many CTAs per SM as the bitmap allows (a row's phases are latency-bound)
+        if (bitmap_fits) {
             if (bm_bytes > 48 * 1024)
                 W1G_CUDA(cudaFuncSetAttribute(k_sp_long_bitmap, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                               (int)bm_bytes));
-            k_sp_long_bitmap<<<c.sm_count, SP_BM_THREADS, bm_bytes, c.stream>>>(R, lists + CL_LONG * K,
-                                                                                 n_list + CL_LONG, K);
+            int per_sm = 1;
+            W1G_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sp_long_bitmap, SP_BM_THREADS,
+                                                                   bm_bytes));
+            if (per_sm < 1) per_sm = 1;
+            k_sp_long_bitmap<<<per_sm * c.sm_count, SP_BM_THREADS, bm_bytes, c.stream>>>(R, lists + CL_LONG * K,
+                                                                                          n_list + CL_LONG, K);
         } else {
             k_sp_long_rows<<<c.sm_count, CSR_LB, 0, c.stream>>>(R, lists + CL_LONG * K, n_list + CL_LONG);
         }

@@ -48,13 +48,16 @@ struct Counters {
     int64_t *flags;     // overflow flags
 };
 
-__global__ void k_wspd_init_f(const int2 *lr, int64_t nn, ItemF *items, int64_t cap, int64_t *cnt) {
+// shard / n_shards: only the recursions of internal nodes w with w % n_shards == shard
+// (the owner loop of spanner.py:206-241 split over GPUs)
+__global__ void k_wspd_init_f(const int2 *lr, int64_t nn, ItemF *items, int64_t cap, int64_t *cnt, int shard,
+                              int n_shards) {
     const int lane = threadIdx.x & 31;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t base = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) & ~31ll; base < nn; base += stride) {
         const int64_t w = base + lane;
         int2 c = w < nn ? lr[w] : make_int2(-1, -1);
-        const bool need = c.x >= 0;
+        const bool need = c.x >= 0 && w % n_shards == shard;
         const unsigned m = __ballot_sync(0xffffffffu, need);
         if (!m) continue;
         int64_t b = 0;
@@ -333,7 +336,7 @@ int wspd_pair_idx(Ctx &c) {
     return W1G_OK;
 }
 
-int wspd_run(Ctx &c, double s, int reference_order, int64_t *n_pairs, bool want_idx) {
+int wspd_run(Ctx &c, double s, int reference_order, int64_t *n_pairs, bool want_idx, int shard, int n_shards) {
     c.pairs_valid = false;
     const int64_t nn = c.tree_n_nodes, K = c.tree_n_points;
     *n_pairs = 0;
@@ -373,7 +376,7 @@ int wspd_run(Ctx &c, double s, int reference_order, int64_t *n_pairs, bool want_
             if (ORDER)
                 k_wspd_init_o<<<gi, 256, 0, c.stream>>>(ptr<int2>(c.t_lr), nn, fa, own0, front_cap, ctr);
             else
-                k_wspd_init_f<<<gi, 256, 0, c.stream>>>(ptr<int2>(c.t_lr), nn, fa, front_cap, ctr);
+                k_wspd_init_f<<<gi, 256, 0, c.stream>>>(ptr<int2>(c.t_lr), nn, fa, front_cap, ctr, shard, n_shards);
             W1G_CHECK_LAUNCH();
         }
         const unsigned gl = 8u * c.sm_count;
@@ -385,10 +388,13 @@ int wspd_run(Ctx &c, double s, int reference_order, int64_t *n_pairs, bool want_
             int per_sm = 0;
             const void *fn = ORDER ? (const void *)k_wspd_coop_o : (const void *)k_wspd_coop;
             W1G_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, 0));
-            // fewer CTAs -> cheaper grid barriers; W1G_COOP_PER_SM overrides (tuning)
+            // fewer CTAs -> cheaper grid barriers while the frontier is small; a big WSPD
+            // (pairs expected well above what 2 CTAs/SM cover per level) wants every
+            // resident warp for its memory-latency-bound levels.  W1G_COOP_PER_SM overrides.
             {
                 const char *e = getenv("W1G_COOP_PER_SM");
-                const int cap = e ? atoi(e) : 2;
+                const double est = (double)K * (8.0 + 1.25 * s * s);  // expected pairs, as pair_cap
+                const int cap = e ? atoi(e) : (est > (double)(16 << 20) ? 8 : 2);
                 if (per_sm > cap) per_sm = cap;
             }
             if (ORDER && per_sm < 1) {

@@ -98,15 +98,155 @@ def rwmd_rows(nodes: SuppliedNodes, rank: int, world: int, group=None, device=No
     identical on every rank and bit-identical to the single-device value.
     `partial_fn(side, begin, end)` overrides the device computation (tests)."""
     fn = partial_fn or (lambda side, b, e: _device_partial(nodes, side, b, e, device))
+    counts = [int(np.count_nonzero(np.asarray(m) > 0)) for m in (nodes.a_mass, nodes.b_mass)]
+    return rwmd_rows_counts(counts, rank, world, fn, group, device)
+
+
+class _DeviceArray:
+    """A library device buffer seen by torch without a copy (__cuda_array_interface__)."""
+
+    def __init__(self, ptr: int, n: int, typestr: str):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (int(ptr or 0), False),
+                                         "version": 3, "strides": None}
+
+
+def gather_arcs(tails, heads, costs, rank: int, world: int, group=None):
+    """Rank 0 receives every rank's arc slice (grouped point-to-point: one
+    send per array per rank, posted together -- NCCL groups them into one
+    ncclGroupStart/End over NVLink).  Arguments and results are torch tensors
+    on the rank's device (NCCL) or on the CPU (gloo).  Returns the concatenated
+    (tails, heads, costs) on rank 0 (slices in rank order), None elsewhere."""
+    import torch
+    import torch.distributed as dist
+
+    dev = tails.device
+    m = torch.tensor([tails.shape[0]], dtype=torch.int64, device=dev)
+    counts = [torch.zeros_like(m) for _ in range(world)]
+    dist.all_gather(counts, m, group=group)
+    counts = [int(c.item()) for c in counts]
+    ops = []
+    out = None
+    if rank == 0:
+        total = sum(counts)
+        out = (torch.empty(total, dtype=torch.int64, device=dev), torch.empty(total, dtype=torch.int64, device=dev),
+               torch.empty(total, dtype=torch.float64, device=dev))
+        out[0][:counts[0]].copy_(tails)
+        out[1][:counts[0]].copy_(heads)
+        out[2][:counts[0]].copy_(costs)
+        off = counts[0]
+        for r in range(1, world):
+            if counts[r]:
+                for buf in out:
+                    ops.append(dist.P2POp(dist.irecv, buf[off:off + counts[r]], r, group))
+            off += counts[r]
+    elif counts[rank]:
+        for t in (tails, heads, costs):
+            ops.append(dist.P2POp(dist.isend, t.contiguous(), 0, group))
+    if ops:
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+    return out
+
+
+def sparsify_sharded(a, b, params: ApproxParams, rank: int, world: int, group=None, device=None):
+    """The sparsify front end of ONE pair over `world` ranks:
+
+    * zero_condense, delta_condense and the split tree are replicated on every
+      rank (cheap, and their sorts are global);
+    * RWMD rows are sharded along numpy's summation tree (rwmd_rows): the G
+      partial sums are all-gathered (8 bytes each) and combined in tree order;
+    * the WSPD owner loop (spanner.py:206-241) is sharded: rank r runs the
+      recursions of the internal nodes w with w % world == r and emits their
+      arcs (rank 0 also the diagonal arcs);
+    * the arc slices are gathered on rank 0 (grouped send/recv over NCCL),
+      which assembles the CSR network.
+
+    Rank 0 returns (network, diagnostics); the other ranks (None, diagnostics).
+    The network is bit-identical to the single-GPU front end's: the CSR is a
+    function of the arc set alone, and the shards partition the WSPD."""
+    import torch
+
+    from .diagram import points_of
+    from .network import fetch_network
+    from .condensation import compute_delta
+    from .pipeline import ApproxDiagnostics, condensation_epsilon
+
+    ctx = _lib.context(device)
+    diag = ApproxDiagnostics()
+    ap, bp = points_of(a), points_of(b)
+    k0 = ctypes.c_int64(0)
+    bal = ctypes.c_int32(0)
+    ctx.call("w1g_zero_condense", _lib.f64p(ap), ap.shape[0], _lib.f64p(bp), bp.shape[0], ctypes.byref(k0),
+             ctypes.byref(bal))
+    if k0.value == 0 or bal.value:
+        diag.short_circuit = True
+        return None, diag
+    # RWMD rows over the ranks, on the resident nodes0 (no reload per range)
+    def partial(side, b_, e_):
+        out = ctypes.c_double(0.0)
+        nm = ctypes.c_int64(0)
+        ctx.call("w1g_rwmd_range", side, int(b_), int(e_), ctypes.byref(out), ctypes.byref(nm))
+        return out.value
+
+    counts = []
+    for side in (0, 1):
+        out = ctypes.c_double(0.0)
+        nm = ctypes.c_int64(0)
+        ctx.call("w1g_rwmd_range", side, 0, 0, ctypes.byref(out), ctypes.byref(nm))
+        counts.append(int(nm.value))
+    L, la, lb = rwmd_rows_counts(counts, rank, world, partial, group, device)
+    eps = condensation_epsilon(params.s)
+    d = 0.0
+    fixed = getattr(params, "delta", None)
+    if params.use_condensation and L > 0.0:
+        d = compute_delta(eps, L, ap.shape[0] + bp.shape[0]) if fixed is None else float(fixed)
+    k = float(getattr(params, "k", 0.99))
+    kk = ctypes.c_int64(0)
+    ctx.call("w1g_delta_condense", d, k * d, (1.0 - k) * d / 2.0,
+             ctypes.c_uint64(int(params.seed) & 0xFFFFFFFFFFFFFFFF), ctypes.byref(kk))
+    nn = ctypes.c_int64(0)
+    depth = ctypes.c_int32(0)
+    ctx.call("w1g_split_tree", _lib.NODES, ctypes.byref(nn), ctypes.byref(depth))
+    P = ctypes.c_int64(0)
+    ctx.call("w1g_wspd_shard", float(params.s), int(rank), int(world), ctypes.byref(P))
+    m = ctypes.c_int64(0)
+    ctx.call("w1g_emit_pair_arcs", 1 if rank == 0 else 0, ctypes.byref(m))
+    diag.lower_bound, diag.delta, diag.epsilon_condense = L, d, eps
+    diag.n_pairs = int(P.value)
+    if world == 1:
+        gathered = None
+    else:
+        tp, hp, cp = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
+        ctx.call("w1g_arcs_device", ctypes.byref(tp), ctypes.byref(hp), ctypes.byref(cp), ctypes.byref(m))
+        dev = torch.device("cuda", ctx.device)
+        n = int(m.value)
+        tails = torch.as_tensor(_DeviceArray(tp.value, n, "<i8"), device=dev)
+        heads = torch.as_tensor(_DeviceArray(hp.value, n, "<i8"), device=dev)
+        costs = torch.as_tensor(_DeviceArray(cp.value, n, "<f8"), device=dev)
+        gathered = gather_arcs(tails, heads, costs, rank, world, group)
+    if rank != 0:
+        return None, diag
+    if gathered is not None:
+        torch.cuda.synchronize(ctx.device)  # the received slices are complete before the library reads them
+        t, h, c = gathered
+        ctx.call("w1g_load_arcs_device", t.data_ptr(), h.data_ptr(), c.data_ptr(), t.shape[0])
+    ncount, narcs = ctypes.c_int64(0), ctypes.c_int64(0)
+    ctx.call("w1g_assemble", ctypes.byref(ncount), ctypes.byref(narcs))
+    net = fetch_network(ctx, int(ncount.value), int(narcs.value))
+    diag.n_nodes, diag.n_arcs = int(ncount.value), int(narcs.value)
+    return net, diag
+
+
+def rwmd_rows_counts(counts, rank: int, world: int, partial_fn, group=None, device=None):
+    """rwmd_rows given the per-side member counts and a partial_fn(side, begin, end)."""
     sides = []
-    for side, mass in enumerate((nodes.a_mass, nodes.b_mass)):
-        n = int(np.count_nonzero(np.asarray(mass) > 0))
+    for side, n in enumerate(counts):
         plan = pairwise_plan(n, world)
         mine = np.zeros(len(plan))
-        for i, (b, e) in enumerate(plan):
+        for i, (b_, e_) in enumerate(plan):
             if i % world == rank:
-                mine[i] = fn(side, b, e)
-        gathered = _all_gather_f64(mine, group, device)
+                mine[i] = partial_fn(side, b_, e_)
+        gathered = _all_gather_f64(mine, group, device) if world > 1 else mine[None, :]
         partials = [gathered[i % world, i] for i in range(len(plan))]
         sides.append(pairwise_combine(n, world, partials))
     la, lb = sides

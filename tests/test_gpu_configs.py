@@ -119,3 +119,102 @@ def test_wspd_deeper_than_128_levels(w1g, name, s):
     net, _ = w1g.sparsify(g["a"], g["b"], w1g.ApproxParams(s=s, best_effort=True, use_condensation=False))
     for f in NET_FIELDS:
         assert bits_equal(getattr(net, f), g["net_" + f]), f
+
+
+@pytest.mark.parametrize("G", [2, 3, 4])
+def test_rwmd_sharded_over_contexts(w1g, G):
+    """w1g_rwmd_sharded: the rows of one pair over G contexts (here all on device 0,
+    each with its own stream and host thread) recombine to w1g_rwmd bit for bit."""
+    import ctypes
+
+    from paper_2110_14734_b200 import _lib, lower_bound, synth
+    from paper_2110_14734_b200.diagram import load_nodes
+
+    a, b = synth.gaussian_cluster_pair(70000, 60000, seed=13)
+    n0 = w1g.zero_condense(a, b)
+    L, la, lb = lower_bound.rwmd_sides(n0)
+    ctxs = [_lib.Context(0) for _ in range(G)]
+    for c in ctxs:
+        load_nodes(c, _lib.NODES0, n0)
+    arr = (ctypes.c_void_p * G)(*[c.handle.value for c in ctxs])
+    out = [ctypes.c_double() for _ in range(3)]
+    _lib.check(_lib.load().w1g_rwmd_sharded(arr, G, *[ctypes.byref(x) for x in out]))
+    assert (out[0].value, out[1].value, out[2].value) == (L, la, lb)
+    for c in ctxs:
+        c.close()
+
+
+@pytest.mark.parametrize("G,s,delta", [(2, 1.0, 0.01), (3, 4.0, 0.001), (5, 16.0, 0.1)])
+def test_wspd_shards_partition_the_network(w1g, G, s, delta):
+    """The sharded WSPD (w1g_wspd_shard) over G shards: the shards' arc slices (rank 0's
+    with the diagonal arcs) assemble into exactly the single-GPU network."""
+    import ctypes
+
+    from paper_2110_14734_b200 import _lib, synth
+    from paper_2110_14734_b200.network import fetch_network
+
+    a, b = synth.gaussian_cluster_pair(100_000, 100_000, seed=0)
+    ref, _ = w1g.sparsify(a, b, w1g.ApproxParams(s=s, best_effort=True, delta=delta))
+    ctx = _lib.context()
+    ap, bp = np.ascontiguousarray(a), np.ascontiguousarray(b)
+    k0, bal = ctypes.c_int64(), ctypes.c_int32()
+    ctx.call("w1g_zero_condense", _lib.f64p(ap), ap.shape[0], _lib.f64p(bp), bp.shape[0], ctypes.byref(k0),
+             ctypes.byref(bal))
+    kk = ctypes.c_int64()
+    ctx.call("w1g_delta_condense", delta, 0.99 * delta, (1.0 - 0.99) * delta / 2.0, ctypes.c_uint64(0),
+             ctypes.byref(kk))
+    nn, depth = ctypes.c_int64(), ctypes.c_int32()
+    ctx.call("w1g_split_tree", _lib.NODES, ctypes.byref(nn), ctypes.byref(depth))
+    parts = []
+    total_pairs = 0
+    for g in range(G):
+        P, m = ctypes.c_int64(), ctypes.c_int64()
+        ctx.call("w1g_wspd_shard", s, g, G, ctypes.byref(P))
+        total_pairs += P.value
+        ctx.call("w1g_emit_pair_arcs", 1 if g == 0 else 0, ctypes.byref(m))
+        t, h, c = np.empty(m.value, np.int64), np.empty(m.value, np.int64), np.empty(m.value)
+        ctx.call("w1g_fetch_arcs", _lib.i64p(t), _lib.i64p(h), _lib.f64p(c))
+        parts.append((t, h, c))
+    assert total_pairs > 0
+    t = np.concatenate([p[0] for p in parts])
+    h = np.concatenate([p[1] for p in parts])
+    c = np.concatenate([p[2] for p in parts])
+    ctx.call("w1g_load_arcs", _lib.i64p(t), _lib.i64p(h), _lib.f64p(c), t.shape[0])
+    n, m = ctypes.c_int64(), ctypes.c_int64()
+    ctx.call("w1g_assemble", ctypes.byref(n), ctypes.byref(m))
+    net = fetch_network(ctx, n.value, m.value)
+    for f in NET_FIELDS:
+        assert bits_equal(getattr(net, f), getattr(ref, f)), f
+
+
+def test_sparsify_sharded_nccl_world1(w1g):
+    """distributed.sparsify_sharded through a real NCCL process group (world size 1 on
+    this box's one GPU): the replicated stages, rwmd_rows, the WSPD shard, the arc
+    path through torch tensors over the library's device buffers, assemble."""
+    import os
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2110_14734_b200 import synth
+    from paper_2110_14734_b200.distributed import sparsify_sharded
+
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        a, b = synth.gaussian_cluster_pair(100_000, 100_000, seed=0)
+        for delta in (0.01, None):
+            params = w1g.ApproxParams(s=1.0, best_effort=True, delta=delta)
+            net, diag = sparsify_sharded(a, b, params, 0, 1)
+            ref, rdiag = w1g.sparsify(a, b, params)
+            assert diag.lower_bound == rdiag.lower_bound and diag.delta == rdiag.delta
+            for f in NET_FIELDS:
+                assert bits_equal(getattr(net, f), getattr(ref, f)), f
+    finally:
+        dist.destroy_process_group()
