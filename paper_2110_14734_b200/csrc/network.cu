@@ -384,8 +384,8 @@ __device__ void dedup_sorted(const uint64_t *sk, int len, int part, int nparts, 
 // one warp sorts 32*E keys (head << 32 | arc) held E per lane in registers
 // (element i = lane * E + q): bitonic stages with partner distance >= E are
 // shuffles, shorter ones swaps inside the lane; the sorted row goes to sk
-template <int E>
-__device__ __forceinline__ void warp_bitonic(uint64_t (&v)[E], int lane) {
+template <int E, class Key = uint64_t>
+__device__ __forceinline__ void warp_bitonic(Key (&v)[E], int lane) {
 #pragma unroll
     for (int k = 2; k <= 32 * E; k <<= 1)
 #pragma unroll
@@ -393,7 +393,7 @@ __device__ __forceinline__ void warp_bitonic(uint64_t (&v)[E], int lane) {
             if (j >= E) {
 #pragma unroll
                 for (int q = 0; q < E; q++) {
-                    const uint64_t o = __shfl_xor_sync(0xffffffffu, v[q], j / E);
+                    const Key o = __shfl_xor_sync(0xffffffffu, v[q], j / E);
                     const int i = lane * E + q;
                     const bool keep_min = ((i & k) == 0) == ((i & j) == 0);
                     v[q] = keep_min ? (v[q] < o ? v[q] : o) : (v[q] > o ? v[q] : o);
@@ -404,7 +404,7 @@ __device__ __forceinline__ void warp_bitonic(uint64_t (&v)[E], int lane) {
                     if (q & j) continue;
                     const int p = q | j;
                     const bool up = ((lane * E + q) & k) == 0;
-                    const uint64_t a = v[q], b = v[p];
+                    const Key a = v[q], b = v[p];
                     if ((a > b) == up) {
                         v[q] = b;
                         v[p] = a;
@@ -612,16 +612,23 @@ __global__ void k_csr_emit_long(const int64_t *__restrict__ start, const int64_t
 // A repeated head (impossible for a WSPD) or a row longer than CSR_LONG_MAX
 // is flagged, and the host redoes the network on the generic path.
 constexpr long long SP_DUP_BIT = 1ll << 16;  // in F_NET_ERR
-constexpr int SP_MED_MAX = 512;              // longest row a warp sorts in registers
-constexpr int SP_CL_BIG = CL_HUGE;           // list of rows of 257..SP_MED_MAX (no huge class here)
+// longest row a warp sorts in registers.  With 32-bit keys a warp could sort 1024
+// (E = 32, 128 registers), but measured at cfg5 (s = 16, delta = 0.001) the rows of
+// 513..1024 took 0.76 ms that way against ~0.5 ms in the bitmap kernel
+constexpr int SP_MED_MAX = 512;
+constexpr int SP_CL_BIG = CL_HUGE;           // list of rows of 257..512 (no huge class here)
+constexpr int SP_CL_BIG2 = 4;                // list of rows of 513..SP_MED_MAX
 
 // the bucketed pair arcs: per CSR slot the head and the cost; rows are sorted
 // by (head << 32 | position in the row), the position then fetches the cost
+// (the cost of arc t -> h is np.hypot of p[t] - p[h]; np.hypot's |dx|, |dy| make it the
+// same value for both arcs of a pair (spanner.py:322-325), so it is computed where the
+// arc is written, from (row, head), and the scatter moves 4-byte heads only)
 struct SpRows {
     const int64_t *ro;     // row offsets (final CSR positions)
     const unsigned *cnt;   // pair arcs per row
     const uint32_t *sh;    // slot heads
-    const double *sc;      // slot costs
+    const double2 *pts;    // node points (arc costs)
     int64_t *ot, *oh;
     double *oc;
     int64_t *f;
@@ -659,11 +666,9 @@ struct SpRowLen {
 // both arcs of every pair into their tail rows (warp-aggregated slots) with
 // the pair's cost, np.hypot of the representatives (spanner.py:322-325)
 __global__ void k_sp_scatter(const int2 *__restrict__ uv, const int32_t *__restrict__ rep, int64_t P,
-                             const double2 *__restrict__ pts, const int64_t *__restrict__ ro, unsigned *cursor,
-                             uint32_t *sh, double *sc, int64_t *f) {
+                             const int64_t *__restrict__ ro, unsigned *cursor, uint32_t *sh) {
     const int lane = threadIdx.x & 31;
     const unsigned lt = lanemask_lt();
-    unsigned bad = 0;
     const int64_t pr = (P + 31) & ~31ll;
     for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < pr; p += (int64_t)gridDim.x * blockDim.x) {
         int e[2] = {-1, -1};
@@ -672,7 +677,6 @@ __global__ void k_sp_scatter(const int2 *__restrict__ uv, const int32_t *__restr
             e[0] = rep[q.x];
             e[1] = rep[q.y];
         }
-        // the slot atomics first; the cost's point loads overlap them
         int64_t slot[2];
 #pragma unroll
         for (int d = 0; d < 2; d++) {
@@ -685,16 +689,10 @@ __global__ void k_sp_scatter(const int2 *__restrict__ uv, const int32_t *__restr
             slot[d] = t >= 0 ? ro[t] + base + __popc(peers & lt) : 0;
         }
         if (p < P) {
-            const double2 a = pts[e[0]], b = pts[e[1]];
-            const double cc = glibc_hypot(dsub(a.x, b.x), dsub(a.y, b.y));
-            if (!isfinite(cc)) bad = 1;
             sh[slot[0]] = (uint32_t)e[1];
-            sc[slot[0]] = cc;
             sh[slot[1]] = (uint32_t)e[0];
-            sc[slot[1]] = cc;
         }
     }
-    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr((unsigned long long *)&f[F_NET_ERR], 4ull);
 }
 
 // the tails column of the CSR: a function of the row offsets alone (a warp per
@@ -713,10 +711,19 @@ __global__ void k_sp_tails(const int64_t *__restrict__ ro, int64_t K, int64_t *o
 }
 
 // sorted element i of row r: key = head << 32 | original position in the row
-__device__ __forceinline__ void sp_put(const SpRows &R, int64_t r, int64_t s0, int64_t i, uint64_t key) {
-    (void)r;  // the tails are written by k_sp_tails
-    R.oh[s0 + i] = (int64_t)(key >> 32);
-    R.oc[s0 + i] = R.sc[s0 + (uint32_t)key];
+__device__ __forceinline__ void sp_put_head(const SpRows &R, int64_t r, int64_t q, uint32_t h) {
+    // the tails are written by k_sp_tails
+    const double2 a = R.pts[r], b = R.pts[h];
+    const double cc = glibc_hypot(dsub(a.x, b.x), dsub(a.y, b.y));  // spanner.py:324
+    if (!isfinite(cc)) atomicOr((unsigned long long *)&R.f[F_NET_ERR], 4ull);
+    R.oh[q] = (int64_t)h;
+    R.oc[q] = cc;
+}
+// the fused path's rows are keyed by the head alone: heads are distinct within a
+// row (a WSPD never repeats a (tail, head); a repeat is flagged), so no arc
+// position is needed to break ties or to find the cost
+__device__ __forceinline__ void sp_put(const SpRows &R, int64_t r, int64_t s0, int64_t i, uint32_t head) {
+    sp_put_head(R, r, s0 + i, head);
 }
 
 // rows of <= W pair arcs on W-lane groups: bitonic sort of the keys in
@@ -724,19 +731,18 @@ __device__ __forceinline__ void sp_put(const SpRows &R, int64_t r, int64_t s0, i
 template <int W>
 __device__ __forceinline__ void sp_row_reg(const SpRows &R, int64_t r, int64_t s0, int len, unsigned &dup) {
     const int lane = threadIdx.x & 31, gl = lane & (W - 1);
-    uint64_t key = gl < len ? (((uint64_t)R.sh[s0 + gl] << 32) | (uint32_t)gl) : ~0ull;
+    uint32_t key = gl < len ? R.sh[s0 + gl] : 0xffffffffu;
 #pragma unroll
     for (int k = 2; k <= W; k <<= 1)
 #pragma unroll
         for (int j = k >> 1; j; j >>= 1) {
-            const uint64_t o = __shfl_xor_sync(0xffffffffu, key, j);
+            const uint32_t o = __shfl_xor_sync(0xffffffffu, key, j);
             const bool up = ((gl & k) == 0) == ((gl & j) == 0);
             key = up ? (key < o ? key : o) : (key > o ? key : o);
         }
-    const uint32_t head = (uint32_t)(key >> 32);
-    const uint32_t prev = __shfl_up_sync(0xffffffffu, head, 1);
+    const uint32_t prev = __shfl_up_sync(0xffffffffu, key, 1);
     if (gl < len) {
-        if (gl > 0 && prev == head) dup = 1;
+        if (gl > 0 && prev == key) dup = 1;
         sp_put(R, r, s0, gl, key);
     }
 }
@@ -793,7 +799,8 @@ __global__ void k_sp_short_rows(const __grid_constant__ SpRows R, int64_t K, int
                     if (l > long_max) {
                         atomicOr((unsigned long long *)&R.f[F_OVERFLOW], 1ull);
                     } else {
-                        const int cl = l <= 32 ? CL_W32 : l <= 256 ? CL_MED : l <= big_max ? SP_CL_BIG : CL_LONG;
+                        const int cl = l <= 32 ? CL_W32 : l <= 256 ? CL_MED : l > big_max ? CL_LONG
+                                                                            : l <= 512 ? SP_CL_BIG : SP_CL_BIG2;
                         lists[(int64_t)cl * K + atomicAdd(&n_list[cl], 1)] = (int32_t)r;
                     }
                 }
@@ -821,43 +828,45 @@ __global__ void k_sp_w32_rows(const __grid_constant__ SpRows R, const int32_t *r
 // rows of 33..SP_MED_MAX pair arcs: a warp each; keys staged through shared
 // memory (coalesced loads and stores), 32*E of them sorted in registers
 template <int E>
-__device__ __forceinline__ void sp_warp_row(const SpRows &R, int64_t r, int64_t s0, int len, uint64_t *sk,
+__device__ __forceinline__ void sp_warp_row(const SpRows &R, int64_t r, int64_t s0, int len, uint32_t *sk,
                                             unsigned &dup, int lane) {
-    for (int i = lane; i < 32 * E; i += 32) sk[i] = i < len ? (((uint64_t)R.sh[s0 + i] << 32) | (uint32_t)i) : ~0ull;
+    for (int i = lane; i < 32 * E; i += 32) sk[i] = i < len ? R.sh[s0 + i] : 0xffffffffu;
     __syncwarp();
-    uint64_t v[E];
+    uint32_t v[E];
 #pragma unroll
     for (int q = 0; q < E; q++) v[q] = sk[lane * E + q];
-    warp_bitonic<E>(v, lane);
+    warp_bitonic<E, uint32_t>(v, lane);
     __syncwarp();
 #pragma unroll
     for (int q = 0; q < E; q++) sk[lane * E + q] = v[q];
     __syncwarp();
     for (int i = lane; i < len; i += 32) {
-        const uint64_t key = sk[i];
-        if (i > 0 && (key >> 32) == (sk[i - 1] >> 32)) dup = 1;
+        const uint32_t key = sk[i];
+        if (i > 0 && key == sk[i - 1]) dup = 1;
         sp_put(R, r, s0, i, key);
     }
     __syncwarp();
 }
 
-// BIG: rows of 257..SP_MED_MAX (more registers: a kernel of their own so the
-// common classes keep their occupancy)
-template <bool BIG>
+// CLS 0: rows of 33..256; 1: 257..512; 2: 513..SP_MED_MAX (more registers per
+// class: kernels of their own so the common classes keep their occupancy)
+template <int CLS>
 __global__ void __launch_bounds__(CSR_MB) k_sp_med_rows(const __grid_constant__ SpRows R, const int32_t *rows,
                                                         const int32_t *n_rows) {
-    constexpr int SK = BIG ? SP_MED_MAX : 256;
-    __shared__ uint64_t sk_all[CSR_MB / 32][SK];
+    constexpr int SK = CLS == 2 ? SP_MED_MAX : CLS == 1 ? 512 : 256;
+    __shared__ uint32_t sk_all[CSR_MB / 32][SK];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    uint64_t *sk = sk_all[wid];
+    uint32_t *sk = sk_all[wid];
     const int nr = *n_rows;
     unsigned dup = 0;
     for (int ri = blockIdx.x * (CSR_MB / 32) + wid; ri < nr; ri += gridDim.x * (CSR_MB / 32)) {
         const int64_t r = rows[ri];
         const int64_t s0 = R.ro[r];
         const int len = (int)R.cnt[r];
-        if (BIG) {
+        if (CLS == 2) {
             sp_warp_row<SP_MED_MAX / 32>(R, r, s0, len, sk, dup, lane);
+        } else if (CLS == 1) {
+            sp_warp_row<16>(R, r, s0, len, sk, dup, lane);
         } else {
             if (len <= 64) sp_warp_row<2>(R, r, s0, len, sk, dup, lane);
             else if (len <= 128) sp_warp_row<4>(R, r, s0, len, sk, dup, lane);
@@ -918,8 +927,7 @@ __global__ void __launch_bounds__(SP_BM_THREADS) k_sp_long_bitmap(const __grid_c
         for (int i = tid; i < len; i += SP_BM_THREADS) {
             const uint32_t h = R.sh[s0 + i];
             const uint32_t rank = pre[h >> 5] + __popc(sbm[h >> 5] & ((1u << (h & 31)) - 1u));
-            R.oh[s0 + rank] = h;
-            R.oc[s0 + rank] = R.sc[s0 + i];
+            sp_put_head(R, r, s0 + rank, h);
         }
         __syncthreads();
         for (int i = tid; i < len; i += SP_BM_THREADS) sbm[R.sh[s0 + i] >> 5] = 0;
@@ -931,7 +939,7 @@ __global__ void __launch_bounds__(SP_BM_THREADS) k_sp_long_bitmap(const __grid_c
 // bitonic sort in shared memory
 __global__ void __launch_bounds__(CSR_LB) k_sp_long_rows(const __grid_constant__ SpRows R, const int32_t *rows,
                                                          const int32_t *n_rows) {
-    __shared__ uint64_t sk[CSR_LONG_MAX];
+    __shared__ uint32_t sk[CSR_LONG_MAX];
     const int tid = threadIdx.x;
     const int nr = *n_rows;
     unsigned dup = 0;
@@ -942,14 +950,14 @@ __global__ void __launch_bounds__(CSR_LB) k_sp_long_rows(const __grid_constant__
         int np2 = 64;
         while (np2 < len) np2 <<= 1;
         __syncthreads();
-        for (int i = tid; i < np2; i += CSR_LB) sk[i] = i < len ? (((uint64_t)R.sh[s0 + i] << 32) | (uint32_t)i) : ~0ull;
+        for (int i = tid; i < np2; i += CSR_LB) sk[i] = i < len ? R.sh[s0 + i] : 0xffffffffu;
         __syncthreads();
         for (int k = 2; k <= np2; k <<= 1)
             for (int j = k >> 1; j; j >>= 1) {
                 for (int i = tid; i < np2; i += CSR_LB) {
                     const int p = i ^ j;
                     if (p > i) {
-                        const uint64_t a = sk[i], b = sk[p];
+                        const uint32_t a = sk[i], b = sk[p];
                         if ((a > b) == ((i & k) == 0)) {
                             sk[i] = b;
                             sk[p] = a;
@@ -959,8 +967,8 @@ __global__ void __launch_bounds__(CSR_LB) k_sp_long_rows(const __grid_constant__
                 __syncthreads();
             }
         for (int i = tid; i < len; i += CSR_LB) {
-            const uint64_t key = sk[i];
-            if (i > 0 && (key >> 32) == (sk[i - 1] >> 32)) dup = 1;
+            const uint32_t key = sk[i];
+            if (i > 0 && key == sk[i - 1]) dup = 1;
             sp_put(R, r, s0, i, key);
         }
     }
@@ -1116,7 +1124,7 @@ int net_run(Ctx &c, const int64_t *d_sup, int64_t n, int64_t *n_arcs) {
     W1G_TRY(ensure(c.net_t, (size_t)m + 1, &ot));
     W1G_TRY(ensure(c.net_h, (size_t)m + 1, &oh));
     W1G_TRY(ensure(c.net_c, (size_t)m + 1, &oc));
-    W1G_TRY(ensure(c.scr[13], (size_t)2 * (n + 2), &cnt));
+    W1G_TRY(ensure(c.scr[13], (size_t)2 * (n + 2) + 8, &cnt));
     cursor = cnt + n + 2;
     W1G_TRY(ensure(c.scr[3], (size_t)n + 2, &start));
     W1G_TRY(ensure(c.scr[5], (size_t)n + 1, &dcnt));
@@ -1241,7 +1249,7 @@ int spanner_net_run(Ctx &c, int64_t *node_count, int64_t *n_arcs) {
     if (big_max > (unsigned)SP_MED_MAX) big_max = SP_MED_MAX;
     SubTimer T(c, "spcsr");
     int64_t *sup, *ro, *ot, *oh;
-    double *oc, *sc;
+    double *oc;
     unsigned *cnt;
     uint32_t *sh;
     int32_t *lists;
@@ -1250,15 +1258,14 @@ int spanner_net_run(Ctx &c, int64_t *node_count, int64_t *n_arcs) {
     W1G_TRY(ensure(c.net_t, (size_t)M + 1, &ot));
     W1G_TRY(ensure(c.net_h, (size_t)M + 1, &oh));
     W1G_TRY(ensure(c.net_c, (size_t)M + 1, &oc));
-    W1G_TRY(ensure(c.scr[13], (size_t)2 * (n + 2), &cnt));
+    W1G_TRY(ensure(c.scr[13], (size_t)2 * (n + 2) + 8, &cnt));
     unsigned *cursor = cnt + n + 2;
     // slots sit at their final CSR positions (the diagonal ones stay unused)
     W1G_TRY(ensure(c.scr[0], (size_t)M + 1, &sh));
-    W1G_TRY(ensure(c.scr[4], (size_t)M + 1, &sc));
-    W1G_TRY(ensure(c.scr[6], (size_t)4 * (K + 1), &lists));
-    int32_t *n_list = reinterpret_cast<int32_t *>(dflags(c) + F_MISC2);  // 4 int32 counters (F_MISC2, F_MISC3)
+    W1G_TRY(ensure(c.scr[6], (size_t)5 * (K + 1), &lists));
+    int32_t *n_list = reinterpret_cast<int32_t *>(cnt + 2 * (n + 2));  // 5 int32 class counters
     W1G_TRY(flags_reset(c));
-    W1G_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned) * 2 * (n + 2), c.stream));
+    W1G_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned) * (2 * (n + 2) + 8), c.stream));
     const int2 *uv = ptr<int2>(c.pair_uv);
     const int32_t *rep = ptr<int32_t>(c.t_rep32);
     const double2 *pp = c.pair_pts ? c.pair_pts : ptr<double2>(ns.pts);
@@ -1291,11 +1298,11 @@ int spanner_net_run(Ctx &c, int64_t *node_count, int64_t *n_arcs) {
     }
     if (side != c.stream) W1G_CUDA(cudaEventRecord(c.ev[13], side));
     if (P) {
-        k_sp_scatter<<<gs(c, P), 256, 0, c.stream>>>(uv, rep, P, pp, ro, cursor, sh, sc, dflags(c));
+        k_sp_scatter<<<gs(c, P), 256, 0, c.stream>>>(uv, rep, P, ro, cursor, sh);
         W1G_CHECK_LAUNCH();
     }
     T.mark("bucket");
-    const SpRows R{ro, cnt, sh, sc, ot, oh, oc, dflags(c)};
+    const SpRows R{ro, cnt, sh, pp, ot, oh, oc, dflags(c)};
     const DiagArgs D{ptr<double2>(ns.pts), ptr<int64_t>(ns.am), ptr<int64_t>(ns.bm), ptr<int64_t>(ns.exb),
                      ns.abar, ns.bbar, sup};
     k_sp_short_rows<<<grid_for(K * 16, 256, 16u * c.sm_count), 256, 0, c.stream>>>(R, K, lists, n_list, long_max,
@@ -1303,11 +1310,15 @@ int spanner_net_run(Ctx &c, int64_t *node_count, int64_t *n_arcs) {
     W1G_CHECK_LAUNCH();
     k_sp_w32_rows<<<4 * c.sm_count, 256, 0, c.stream>>>(R, lists + CL_W32 * K, n_list + CL_W32);
     W1G_CHECK_LAUNCH();
-    k_sp_med_rows<false><<<8 * c.sm_count, CSR_MB, 0, c.stream>>>(R, lists + CL_MED * K, n_list + CL_MED);
+    k_sp_med_rows<0><<<8 * c.sm_count, CSR_MB, 0, c.stream>>>(R, lists + CL_MED * K, n_list + CL_MED);
     W1G_CHECK_LAUNCH();
     T.mark("short_med");
-    k_sp_med_rows<true><<<4 * c.sm_count, CSR_MB, 0, c.stream>>>(R, lists + SP_CL_BIG * K, n_list + SP_CL_BIG);
+    k_sp_med_rows<1><<<4 * c.sm_count, CSR_MB, 0, c.stream>>>(R, lists + SP_CL_BIG * K, n_list + SP_CL_BIG);
     W1G_CHECK_LAUNCH();
+    if (big_max > 512) {
+        k_sp_med_rows<2><<<2 * c.sm_count, CSR_MB, 0, c.stream>>>(R, lists + SP_CL_BIG2 * K, n_list + SP_CL_BIG2);
+        W1G_CHECK_LAUNCH();
+    }
     T.mark("big");
     {
         // long rows: bitmap ranks while a K-bit bitmap (+ prefixes) fits in shared memory;

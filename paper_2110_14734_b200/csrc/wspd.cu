@@ -95,8 +95,11 @@ __global__ void k_wspd_init_o(const int2 *lr, int64_t nn, ItemF *items, int32_t 
 
 // one frontier level.  ORDER: cur / next are consecutive levels of the one
 // item array (global indices base_cur + i / base_next + slot) and every item
-// records its link: ~pair slot, or the index of its first child
-template <bool ORDER>
+// records its link: ~pair slot, or the index of its first child.  IPT items
+// per thread and round: their loads are all in flight together (the level is
+// bound by the latency of the dependent item -> geometry loads), and the
+// round's appends are aggregated per CTA (two global atomics per CTA).
+template <bool ORDER, int IPT = 1>
 __device__ __forceinline__ void wspd_level(const ItemF *__restrict__ cur, ItemF *__restrict__ next,
                                            int64_t cap, int level, Counters k,
                                            int2 *__restrict__ out_uv, int64_t *__restrict__ links,
@@ -109,38 +112,58 @@ __device__ __forceinline__ void wspd_level(const ItemF *__restrict__ cur, ItemF 
     if (blockIdx.x == 0 && threadIdx.x == 0) k.cnt[(level + 2) % 3] = 0;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const unsigned lt = lanemask_lt();
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x * IPT;
     __shared__ int s_np[8], s_ns[8];
     __shared__ int64_t s_bp, s_bs;
-    // block-uniform trip count: appends are aggregated per CTA (two global
-    // atomics per CTA and round instead of two per warp)
-    for (int64_t bbase = (int64_t)blockIdx.x * blockDim.x; bbase < n; bbase += stride) {
-        const int64_t i = bbase + threadIdx.x;
-        const bool valid = i < n;
-        Item it;
-        bool ws = false;
-        int2 c0 = make_int2(0, 0), c1 = make_int2(0, 0);
-        if (valid) {
-            it = cur[i];
-            // every load the item may need, issued together
-            const NodeGeom gu = geom[it.u], gv = geom[it.v];
-            const int2 lu = lr[it.u], lv = lr[it.v];
-            ws = ws_predicate(gu, gv, s);
-            if (!ws) {
-                if (gu.dsq > gv.dsq) {  // spanner.py:226-230
-                    c0 = make_int2(lu.x, it.v);
-                    c1 = make_int2(lu.y, it.v);
-                } else {                // spanner.py:231-235
-                    c0 = make_int2(it.u, lv.x);
-                    c1 = make_int2(it.u, lv.y);
-                }
+    // block-uniform trip count
+    for (int64_t bbase = (int64_t)blockIdx.x * blockDim.x * IPT; bbase < n; bbase += stride) {
+        Item it[IPT];
+        bool valid[IPT], ws[IPT];
+        int2 c0[IPT], c1[IPT];
+        NodeGeom gu[IPT], gv[IPT];
+        int2 lu[IPT], lv[IPT];
+#pragma unroll
+        for (int q = 0; q < IPT; q++) {
+            const int64_t i = bbase + q * blockDim.x + threadIdx.x;
+            valid[q] = i < n;
+            it[q] = valid[q] ? cur[i] : ItemF{0, 0};
+        }
+#pragma unroll
+        for (int q = 0; q < IPT; q++) {
+            // every load the items may need, issued together
+            if (valid[q]) {
+                gu[q] = geom[it[q].u];
+                gv[q] = geom[it[q].v];
+                lu[q] = lr[it[q].u];
+                lv[q] = lr[it[q].v];
             }
         }
-        const unsigned mp = __ballot_sync(0xffffffffu, valid && ws);
-        const unsigned ms = __ballot_sync(0xffffffffu, valid && !ws);
+        unsigned mp[IPT], ms[IPT];
+        int np = 0, ns = 0;
+#pragma unroll
+        for (int q = 0; q < IPT; q++) {
+            ws[q] = false;
+            c0[q] = c1[q] = make_int2(0, 0);
+            if (valid[q]) {
+                ws[q] = ws_predicate(gu[q], gv[q], s);
+                if (!ws[q]) {
+                    if (gu[q].dsq > gv[q].dsq) {  // spanner.py:226-230
+                        c0[q] = make_int2(lu[q].x, it[q].v);
+                        c1[q] = make_int2(lu[q].y, it[q].v);
+                    } else {                      // spanner.py:231-235
+                        c0[q] = make_int2(it[q].u, lv[q].x);
+                        c1[q] = make_int2(it[q].u, lv[q].y);
+                    }
+                }
+            }
+            mp[q] = __ballot_sync(0xffffffffu, valid[q] && ws[q]);
+            ms[q] = __ballot_sync(0xffffffffu, valid[q] && !ws[q]);
+            np += __popc(mp[q]);
+            ns += 2 * __popc(ms[q]);
+        }
         if (lane == 0) {
-            s_np[wid] = __popc(mp);
-            s_ns[wid] = 2 * __popc(ms);
+            s_np[wid] = np;
+            s_ns[wid] = ns;
         }
         __syncthreads();
         if (threadIdx.x == 0) {
@@ -156,26 +179,32 @@ __device__ __forceinline__ void wspd_level(const ItemF *__restrict__ cur, ItemF 
             s_bs = ts ? (int64_t)atomicAdd((unsigned long long *)&k.cnt[(level + 1) % 3], (unsigned long long)ts) : 0;
         }
         __syncthreads();
-        const int64_t bp = s_bp + s_np[wid], bs = s_bs + s_ns[wid];
+        int64_t bp = s_bp + s_np[wid], bs = s_bs + s_ns[wid];
         __syncthreads();  // s_* are rewritten by the next round
-        if (valid && ws) {
-            const int64_t slot = bp + __popc(mp & lt);
-            if constexpr (ORDER) links[base_cur + i] = ~slot;
-            if (slot < pair_cap) {
-                out_uv[slot] = make_int2(it.u, it.v);
-            } else if (slot == pair_cap) {
-                atomicOr((unsigned long long *)&k.flags[F_PAIR_OVF], 1ull);
+#pragma unroll
+        for (int q = 0; q < IPT; q++) {
+            const int64_t i = bbase + q * blockDim.x + threadIdx.x;
+            if (valid[q] && ws[q]) {
+                const int64_t slot = bp + __popc(mp[q] & lt);
+                if constexpr (ORDER) links[base_cur + i] = ~slot;
+                if (slot < pair_cap) {
+                    out_uv[slot] = make_int2(it[q].u, it[q].v);
+                } else if (slot == pair_cap) {
+                    atomicOr((unsigned long long *)&k.flags[F_PAIR_OVF], 1ull);
+                }
             }
-        }
-        if (valid && !ws) {
-            const int64_t slot = bs + 2 * __popc(ms & lt);
-            if constexpr (ORDER) links[base_cur + i] = base_next + slot;
-            if (slot + 1 < cap) {
-                next[slot] = ItemF{c0.x, c0.y};      // left child
-                next[slot + 1] = ItemF{c1.x, c1.y};  // right child
-            } else {
-                atomicOr((unsigned long long *)&k.flags[F_FRONT_OVF], 1ull);
+            if (valid[q] && !ws[q]) {
+                const int64_t slot = bs + 2 * __popc(ms[q] & lt);
+                if constexpr (ORDER) links[base_cur + i] = base_next + slot;
+                if (slot + 1 < cap) {
+                    next[slot] = ItemF{c0[q].x, c0[q].y};      // left child
+                    next[slot + 1] = ItemF{c1[q].x, c1[q].y};  // right child
+                } else {
+                    atomicOr((unsigned long long *)&k.flags[F_FRONT_OVF], 1ull);
+                }
             }
+            bp += __popc(mp[q]);
+            bs += 2 * __popc(ms[q]);
         }
     }
 }
@@ -190,6 +219,7 @@ __global__ void __launch_bounds__(256) k_wspd_level(const ItemF *__restrict__ cu
 
 // all frontier levels in ONE persistent cooperative launch: a grid barrier
 // per level instead of a launch per level and a host poll per batch
+template <int IPT>
 __global__ void __launch_bounds__(256) k_wspd_coop(ItemF *fa, ItemF *fb, int64_t cap, Counters k,
                                                    int2 *__restrict__ out_uv, int64_t pair_cap, double s,
                                                    const NodeGeom *__restrict__ geom, const int2 *__restrict__ lr,
@@ -199,8 +229,8 @@ __global__ void __launch_bounds__(256) k_wspd_coop(ItemF *fa, ItemF *fb, int64_t
     while (true) {
         const int64_t n = *((volatile int64_t *)&k.cnt[level % 3]);
         if (n == 0 || n > cap) break;  // done, or the last level overflowed (flag set)
-        wspd_level<false>((level & 1) ? fb : fa, (level & 1) ? fa : fb, cap, level, k, out_uv, nullptr, 0, 0,
-                          pair_cap, s, geom, lr, n);
+        wspd_level<false, IPT>((level & 1) ? fb : fa, (level & 1) ? fa : fb, cap, level, k, out_uv, nullptr, 0, 0,
+                               pair_cap, s, geom, lr, n);
         grid.sync();
         level++;
     }
@@ -386,15 +416,20 @@ int wspd_run(Ctx &c, double s, int reference_order, int64_t *n_pairs, bool want_
         if (nn > 1) {
             // persistent cooperative launch: every level, one grid barrier each
             int per_sm = 0;
-            const void *fn = ORDER ? (const void *)k_wspd_coop_o : (const void *)k_wspd_coop;
+            // big frontiers (many expected pairs) use every resident warp.  (wspd_level can
+            // take several items per thread and round, but 4 items need 156 registers
+            // against 64, which cuts the resident CTAs by the same factor: the loads in
+            // flight per SM would not grow, so one item per thread is used.)
+            const double est_pairs = (double)K * (8.0 + 1.25 * s * s);  // as pair_cap
+            const bool big = est_pairs > (double)(16 << 20);
+            const void *fn = ORDER ? (const void *)k_wspd_coop_o : (const void *)k_wspd_coop<1>;
             W1G_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, 0));
             // fewer CTAs -> cheaper grid barriers while the frontier is small; a big WSPD
             // (pairs expected well above what 2 CTAs/SM cover per level) wants every
             // resident warp for its memory-latency-bound levels.  W1G_COOP_PER_SM overrides.
             {
                 const char *e = getenv("W1G_COOP_PER_SM");
-                const double est = (double)K * (8.0 + 1.25 * s * s);  // expected pairs, as pair_cap
-                const int cap = e ? atoi(e) : (est > (double)(16 << 20) ? 8 : 2);
+                const int cap = e ? atoi(e) : (big ? 8 : 2);
                 if (per_sm > cap) per_sm = cap;
             }
             if (ORDER && per_sm < 1) {
