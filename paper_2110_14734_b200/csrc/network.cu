@@ -617,7 +617,6 @@ constexpr long long SP_DUP_BIT = 1ll << 16;  // in F_NET_ERR
 // 513..1024 took 0.76 ms that way against ~0.5 ms in the bitmap kernel
 constexpr int SP_MED_MAX = 512;
 constexpr int SP_CL_BIG = CL_HUGE;           // list of rows of 257..512 (no huge class here)
-constexpr int SP_CL_BIG2 = 4;                // list of rows of 513..SP_MED_MAX
 
 // the bucketed pair arcs: per CSR slot the head and the cost; rows are sorted
 // by (head << 32 | position in the row), the position then fetches the cost
@@ -799,8 +798,7 @@ __global__ void k_sp_short_rows(const __grid_constant__ SpRows R, int64_t K, int
                     if (l > long_max) {
                         atomicOr((unsigned long long *)&R.f[F_OVERFLOW], 1ull);
                     } else {
-                        const int cl = l <= 32 ? CL_W32 : l <= 256 ? CL_MED : l > big_max ? CL_LONG
-                                                                            : l <= 512 ? SP_CL_BIG : SP_CL_BIG2;
+                        const int cl = l <= 32 ? CL_W32 : l <= 256 ? CL_MED : l <= big_max ? SP_CL_BIG : CL_LONG;
                         lists[(int64_t)cl * K + atomicAdd(&n_list[cl], 1)] = (int32_t)r;
                     }
                 }
@@ -848,12 +846,12 @@ __device__ __forceinline__ void sp_warp_row(const SpRows &R, int64_t r, int64_t 
     __syncwarp();
 }
 
-// CLS 0: rows of 33..256; 1: 257..512; 2: 513..SP_MED_MAX (more registers per
-// class: kernels of their own so the common classes keep their occupancy)
+// CLS 0: rows of 33..256; 1: 257..SP_MED_MAX (more registers: a kernel of its own
+// so the common class keeps its occupancy)
 template <int CLS>
 __global__ void __launch_bounds__(CSR_MB) k_sp_med_rows(const __grid_constant__ SpRows R, const int32_t *rows,
                                                         const int32_t *n_rows) {
-    constexpr int SK = CLS == 2 ? SP_MED_MAX : CLS == 1 ? 512 : 256;
+    constexpr int SK = CLS == 1 ? SP_MED_MAX : 256;
     __shared__ uint32_t sk_all[CSR_MB / 32][SK];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     uint32_t *sk = sk_all[wid];
@@ -863,10 +861,8 @@ __global__ void __launch_bounds__(CSR_MB) k_sp_med_rows(const __grid_constant__ 
         const int64_t r = rows[ri];
         const int64_t s0 = R.ro[r];
         const int len = (int)R.cnt[r];
-        if (CLS == 2) {
+        if (CLS == 1) {
             sp_warp_row<SP_MED_MAX / 32>(R, r, s0, len, sk, dup, lane);
-        } else if (CLS == 1) {
-            sp_warp_row<16>(R, r, s0, len, sk, dup, lane);
         } else {
             if (len <= 64) sp_warp_row<2>(R, r, s0, len, sk, dup, lane);
             else if (len <= 128) sp_warp_row<4>(R, r, s0, len, sk, dup, lane);
@@ -1262,8 +1258,8 @@ int spanner_net_run(Ctx &c, int64_t *node_count, int64_t *n_arcs) {
     unsigned *cursor = cnt + n + 2;
     // slots sit at their final CSR positions (the diagonal ones stay unused)
     W1G_TRY(ensure(c.scr[0], (size_t)M + 1, &sh));
-    W1G_TRY(ensure(c.scr[6], (size_t)5 * (K + 1), &lists));
-    int32_t *n_list = reinterpret_cast<int32_t *>(cnt + 2 * (n + 2));  // 5 int32 class counters
+    W1G_TRY(ensure(c.scr[6], (size_t)4 * (K + 1), &lists));
+    int32_t *n_list = reinterpret_cast<int32_t *>(cnt + 2 * (n + 2));  // 4 int32 class counters
     W1G_TRY(flags_reset(c));
     W1G_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned) * (2 * (n + 2) + 8), c.stream));
     const int2 *uv = ptr<int2>(c.pair_uv);
@@ -1315,10 +1311,6 @@ int spanner_net_run(Ctx &c, int64_t *node_count, int64_t *n_arcs) {
     T.mark("short_med");
     k_sp_med_rows<1><<<4 * c.sm_count, CSR_MB, 0, c.stream>>>(R, lists + SP_CL_BIG * K, n_list + SP_CL_BIG);
     W1G_CHECK_LAUNCH();
-    if (big_max > 512) {
-        k_sp_med_rows<2><<<2 * c.sm_count, CSR_MB, 0, c.stream>>>(R, lists + SP_CL_BIG2 * K, n_list + SP_CL_BIG2);
-        W1G_CHECK_LAUNCH();
-    }
     T.mark("big");
     {
         // long rows: bitmap ranks while a K-bit bitmap (+ prefixes) fits in shared memory;
