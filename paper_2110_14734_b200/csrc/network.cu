@@ -872,29 +872,21 @@ __global__ void __launch_bounds__(CSR_MB) k_sp_med_rows(const __grid_constant__ 
     if (__any_sync(0xffffffffu, dup) && lane == 0) atomicOr((unsigned long long *)&R.f[F_NET_ERR], SP_DUP_BIT);
 }
 
-// long rows by enumeration instead of comparison: heads are distinct within a
-// row and below K, so a row's heads mark a K-bit bitmap in shared memory, and
-// reading the bitmap back in word order lists them sorted.  Each warp owns a
-// contiguous range of words: a popcount pass gives the warps' bases (a block
-// scan of 16 totals), then every warp walks its range 32 words at a time
-// (coalesced, conflict-free), places each lane's bits after a warp scan of the
-// word popcounts and clears the words it read.  The sorted heads land in a
-// shared buffer (rows <= SP_BM_BUF) and leave with coalesced stores; longer
-// rows are listed straight into the output.  O(len + K/32) per row, a CTA
-// per row.  A head already marked is a repeated (tail, head).
+// long rows by rank instead of comparison: heads are distinct within a row
+// and below K, so a row's heads mark a K-bit bitmap in shared memory; a block
+// scan of the per-word popcounts then gives every head its rank (its place in
+// the sorted row) directly.  O(len + K/32) per row, a CTA per row.  A head
+// already marked is a repeated (tail, head).
 constexpr int SP_BM_THREADS = 512;
-constexpr int SP_BM_BUF = 4096;
 __global__ void __launch_bounds__(SP_BM_THREADS) k_sp_long_bitmap(const __grid_constant__ SpRows R,
                                                                   const int32_t *rows, const int32_t *n_rows,
                                                                   int64_t K) {
-    extern __shared__ uint32_t sbm[];  // W bitmap words, then SP_BM_BUF sorted heads
-    constexpr int NW = SP_BM_THREADS / 32;
+    extern __shared__ uint32_t sbm[];  // W bitmap words, then W exclusive popcount prefixes
     const int W = (int)((K + 31) >> 5);
-    uint32_t *buf = sbm + W;
-    __shared__ uint32_t s_warp[NW];
+    uint32_t *pre = sbm + W;
+    __shared__ uint32_t s_warp[SP_BM_THREADS / 32];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const int wpw = (W + NW - 1) / NW;  // words per warp
-    const int w_lo = min(W, wid * wpw), w_hi = min(W, w_lo + wpw);
+    const int per = (W + SP_BM_THREADS - 1) / SP_BM_THREADS;  // words per thread in the scan
     for (int i = tid; i < W; i += SP_BM_THREADS) sbm[i] = 0;
     const int nr = *n_rows;
     unsigned dup = 0;
@@ -902,46 +894,39 @@ __global__ void __launch_bounds__(SP_BM_THREADS) k_sp_long_bitmap(const __grid_c
         const int64_t r = rows[ri];
         const int64_t s0 = R.ro[r];
         const int len = (int)R.cnt[r];
-        __syncthreads();  // the previous row has left buf and cleared its words
+        __syncthreads();  // bitmap clear (previous row)
         for (int i = tid; i < len; i += SP_BM_THREADS) {
             const uint32_t h = R.sh[s0 + i];
             const uint32_t bit = 1u << (h & 31);
             if (atomicOr(&sbm[h >> 5], bit) & bit) dup = 1;
         }
         __syncthreads();
-        uint32_t cnt = 0;
-        for (int w = w_lo + lane; w < w_hi; w += 32) cnt += __popc(sbm[w]);
+        // exclusive prefix of the word popcounts: a contiguous run of words per thread
+        const int w0 = tid * per, w1 = min(W, w0 + per);
+        uint32_t mine = 0;
+        for (int w = w0; w < w1; w++) mine += __popc(sbm[w]);
+        uint32_t x = mine;
 #pragma unroll
-        for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-        if (lane == 0) s_warp[wid] = cnt;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) s_warp[wid] = x;
         __syncthreads();
-        uint32_t base = 0;
+        uint32_t base = x - mine;
         for (int w = 0; w < wid; w++) base += s_warp[w];
-        const bool in_buf = len <= SP_BM_BUF;
-        for (int w0 = w_lo; w0 < w_hi; w0 += 32) {
-            const int w = w0 + lane;
-            uint32_t x = w < w_hi ? sbm[w] : 0u;
-            const uint32_t c = __popc(x);
-            uint32_t inc = c;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
-                if (lane >= o) inc += y;
-            }
-            uint32_t k = base + inc - c;
-            if (x) sbm[w] = 0u;
-            while (x) {
-                const uint32_t h = ((uint32_t)w << 5) + (uint32_t)(__ffs(x) - 1);
-                if (in_buf) buf[k] = h;
-                else R.oh[s0 + k] = (int64_t)h;
-                k++;
-                x &= x - 1;
-            }
-            base += __shfl_sync(0xffffffffu, inc, 31);
+        for (int w = w0; w < w1; w++) {
+            pre[w] = base;
+            base += __popc(sbm[w]);
         }
         __syncthreads();
-        for (int i = tid; i < len; i += SP_BM_THREADS)
-            sp_put_head(R, r, s0 + i, in_buf ? buf[i] : (uint32_t)R.oh[s0 + i]);
+        for (int i = tid; i < len; i += SP_BM_THREADS) {
+            const uint32_t h = R.sh[s0 + i];
+            const uint32_t rank = pre[h >> 5] + __popc(sbm[h >> 5] & ((1u << (h & 31)) - 1u));
+            sp_put_head(R, r, s0 + rank, h);
+        }
+        __syncthreads();
+        for (int i = tid; i < len; i += SP_BM_THREADS) sbm[R.sh[s0 + i] >> 5] = 0;
     }
     if (__any_sync(0xffffffffu, dup) && lane == 0) atomicOr((unsigned long long *)&R.f[F_NET_ERR], SP_DUP_BIT);
 }
@@ -1249,7 +1234,7 @@ int spanner_net_run(Ctx &c, int64_t *node_count, int64_t *n_arcs) {
     // rows longer than that are ranked by the bitmap kernel when a K-bit bitmap (+ its
     // prefixes) fits in shared memory, whatever their length; otherwise they are
     // limited by the CTA bitonic sort's buffer
-    const size_t bm_bytes = (size_t)4 * ((K + 31) / 32) + 4 * SP_BM_BUF;  // bitmap + sorted-head buffer
+    const size_t bm_bytes = (size_t)8 * ((K + 31) / 32);
     const bool bitmap_fits = bm_bytes <= 200 * 1024;
     unsigned long_max = bitmap_fits ? 0xffffffffu : (unsigned)CSR_LONG_MAX;
     if (const char *lm = getenv("W1G_SP_LONG_MAX")) long_max = (unsigned)atoi(lm);
