@@ -87,6 +87,35 @@ def _peaks() -> dict:
 PEAKS = _peaks()
 
 
+def _ncu_capture(fname: str, kernel: str) -> dict | None:
+    """The committed `ncu --set full` summary of `kernel` for this workload (profiles/,
+    tools/ncu_summary.py): DRAM bytes per launch and pipe utilisation.  ncu cannot run
+    inside the timed bench, so the capture of the same configuration is read here."""
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    try:
+        with open(os.path.join(ROOT, "profiles", fname)) as f:
+            for line in f:
+                row = json.loads(line)
+                if kernel not in row["kernel"]:
+                    continue
+                out = {"capture": "profiles/" + fname}
+                tr = 0.0
+                for key in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                    v, u = row[key].split()
+                    tr += float(v) * scale[u]
+                out["dram_bytes_per_launch"] = int(tr)
+                for key, name in (("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "fp64_pipe_pct"),
+                                  ("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", "fma_pipe_pct"),
+                                  ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue_pct"),
+                                  ("sm__warps_active.avg.pct_of_peak_sustained_active", "warps_active_pct")):
+                    if key in row:
+                        out[name] = float(row[key].split()[0])
+                return out
+    except (OSError, KeyError, ValueError, IndexError):
+        pass
+    return None
+
+
 def workload_config(args) -> dict:
     if args.workload == "cfg4":
         return {"workload": f"cfg4: sparsify front ends of the {CFG4[0] * (CFG4[0] - 1) // 2} pairs of "
@@ -398,16 +427,20 @@ def rwmd_roofline(ctx, w1g, a, b) -> dict:
     f64 = 5.0 * ref_ev / (ref_ms * 1e-3) / 1e12 if ref_ms else 0.0
     f32 = 5.0 * tile_ev / (tile_ms * 1e-3) / 1e12 if tile_ms else 0.0
     total = sum(ms[i] for i in range(4))
+    ncu_ref = _ncu_capture("r02_ncu_cfg2_rwmd.jsonl", "k_refine")
+    ncu_tile = _ncu_capture("r02_ncu_cfg2_rwmd.jsonl", "k_rwmd_f32")
     return {
         "bound": "fp64", "kernel": "k_refine (rwmd.cu): exact fp64 nearest-neighbour refine, the production RWMD",
         "achieved": f64, "peak": PEAKS["fp64_tflops"], "unit": "TFLOP/s", "frac": f64 / PEAKS["fp64_tflops"],
-        "traffic": None,
+        "traffic": ncu_ref["dram_bytes_per_launch"] if ncu_ref else None,
+        "ncu": ncu_ref,
         "ms_per_launch": ref_ms, "flop_per_launch": 5.0 * ref_ev, "evals_per_launch": ref_ev,
         "note": "achieved = 5 FLOP x the distance evaluations the launch performs (device counter) / its "
                 "event-timed duration; peak " + PEAKS["fp_source"],
         "tile": {"bound": "fp32", "kernel": "k_rwmd_f32<2,1,256> (rwmd_tile.cu): culled FP32 seed pass",
                  "achieved": f32, "peak": PEAKS["fp32_tflops"], "unit": "TFLOP/s",
-                 "frac": f32 / PEAKS["fp32_tflops"], "ms_per_launch": tile_ms, "evals_per_launch": tile_ev},
+                 "frac": f32 / PEAKS["fp32_tflops"], "ms_per_launch": tile_ms, "evals_per_launch": tile_ev,
+                 "ncu": ncu_tile},
         "per_kernel": per,
         "rwmd_algorithmic": {
             "directed_evals": int(directed.value),
@@ -439,7 +472,9 @@ def north_star_kernel(ctx, w1g, n: int) -> dict:
             "config": f"{n}+{n} points (gaussian_cluster_pair seed 0)", "achieved": tflops,
             "peak": PEAKS["fp32_tflops"], "unit": "TFLOP/s", "frac": tflops / PEAKS["fp32_tflops"],
             "ms_per_launch": ms.value, "evals_per_launch": evals.value,
-            "note": "5 FLOP per directed (source, target) evaluation; ncu sm__pipe_fma_cycles_active in profiles/"}
+            "traffic": (_ncu_capture("r02_ncu_brute_1m.jsonl", "k_rwmd_f32") or {}).get("dram_bytes_per_launch"),
+            "ncu": _ncu_capture("r02_ncu_brute_1m.jsonl", "k_rwmd_f32"),
+            "note": "5 FLOP per directed (source, target) evaluation (4 FMA FLOP executed: 2 FFMA per evaluation)"}
 
 
 def e2e_batch(w1g, diagrams, pairs, args, dist: Dist, reps: int) -> dict:

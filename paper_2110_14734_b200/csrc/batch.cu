@@ -19,6 +19,7 @@
 //   * w1g_front_end_batch is the synchronous variant that leaves every network
 //     in device memory (front-end throughput, and the per-pair diagnostics).
 #include <atomic>
+#include <chrono>
 #include <cstring>
 #include <deque>
 #include <map>
@@ -153,6 +154,9 @@ struct BatchState {
     bool active = false;
     cudaEvent_t ev_start = nullptr, ev_end = nullptr;  // device makespan of a synchronous batch
     std::vector<cudaEvent_t> kid_ev;
+    // W1G_BATCH_TRACE=1: per-worker host time in each phase (us), printed at the batch's end
+    bool trace = false;
+    std::vector<double> tr_block, tr_fe, tr_fetch, tr_pairs;
 };
 
 static void batch_join(BatchState &b) {
@@ -178,6 +182,10 @@ static void batch_worker(Ctx *parent, BatchState *b, int w) {
     const double2 *corpus = ptr<double2>(parent->corpus_pts);
     const int64_t *off = parent->h_corpus_off;
     cudaSetDevice(x->device);
+    using clk = std::chrono::steady_clock;
+    auto us = [](clk::time_point a, clk::time_point b) {
+        return 1e-3 * (double)std::chrono::duration_cast<std::chrono::nanoseconds>(b - a).count();
+    };
     for (;;) {
         if (b->cancel.load()) break;
         const int64_t p = b->next.fetch_add(1);
@@ -191,15 +199,18 @@ static void batch_worker(Ctx *parent, BatchState *b, int w) {
         void *blk = nullptr;
         int64_t ncap = 0, mcap = 0;
         int rc = W1G_OK;
+        const clk::time_point t0 = clk::now();
         if (b->deliver && b->hint_m[w] > 0) {
-            ncap = b->hint_n[w] + b->hint_n[w] / 8 + 64;
-            mcap = b->hint_m[w] + b->hint_m[w] / 8 + 1024;
+            // sized from this worker's previous network (+25 %: the pairs of a batch differ)
+            ncap = b->hint_n[w] + b->hint_n[w] / 4 + 64;
+            mcap = b->hint_m[w] + b->hint_m[w] / 4 + 1024;
             rc = host_pool().get(carve_bytes(ncap, mcap), &blk, &b->cancel);
             if (rc == W1G_OK) {
                 NetCarve cv = carve(blk, ncap, mcap);
                 rc = w1g_set_network_out(x, cv.sup, cv.t, cv.h, cv.c, cv.ro, ncap, mcap);
             }
         }
+        const clk::time_point t1 = clk::now();
         if (rc == W1G_OK) {
             if (parent->h_corpus_ptr) {
                 // host-resident diagrams: this worker's H2D overlaps the other workers' front ends
@@ -214,6 +225,7 @@ static void batch_worker(Ctx *parent, BatchState *b, int w) {
                                           b->prm.seed, &r.info);
             }
         }
+        const clk::time_point t2 = clk::now();
         if (rc == W1G_OK && b->deliver && !r.info.short_circuit) {
             const int64_t n = r.info.node_count, m = r.info.n_arcs;
             b->hint_n[w] = n;
@@ -241,6 +253,13 @@ static void batch_worker(Ctx *parent, BatchState *b, int w) {
             }
         }
         if (blk) host_pool().put(blk);  // short circuit or error: nothing to hand over
+        if (b->trace) {
+            const clk::time_point t3 = clk::now();
+            b->tr_block[w] += us(t0, t1);
+            b->tr_fe[w] += us(t1, t2);
+            b->tr_fetch[w] += us(t2, t3);
+            b->tr_pairs[w] += 1;
+        }
         r.status = rc;
         if (rc != W1G_OK) snprintf(r.message, sizeof r.message, "%s", w1g_last_error());
         {
@@ -296,6 +315,14 @@ static int batch_start(Ctx &c, const int32_t *pairs, int64_t n_pairs, const Batc
     b.first_rc = W1G_OK;
     b.first_err.clear();
     b.active = true;
+    {
+        const char *e = getenv("W1G_BATCH_TRACE");
+        b.trace = e && *e == '1';
+        b.tr_block.assign(b.kids.size(), 0.0);
+        b.tr_fe.assign(b.kids.size(), 0.0);
+        b.tr_fetch.assign(b.kids.size(), 0.0);
+        b.tr_pairs.assign(b.kids.size(), 0.0);
+    }
     const int nt = (int)(n_pairs < streams ? (n_pairs > 0 ? n_pairs : 1) : streams);
     for (int w = 0; w < nt; w++) b.threads.emplace_back(batch_worker, &c, &b, w);
     return W1G_OK;
@@ -399,12 +426,21 @@ int w1g_batch_release(void *block) {
     return W1G_OK;
 }
 
+static void batch_trace_print(BatchState &b) {
+    if (!b.trace) return;
+    for (size_t w = 0; w < b.tr_fe.size(); w++)
+        if (b.tr_pairs[w] > 0)
+            fprintf(stderr, "[w1g batch] worker %zu: %.0f pairs, block wait %.0f us, front end %.0f us, fetch %.0f us\n",
+                    w, b.tr_pairs[w], b.tr_block[w], b.tr_fe[w], b.tr_fetch[w]);
+}
+
 int w1g_batch_end(w1g_ctx *c) {
     if (!c || !c->batch) return W1G_OK;
     BatchState &b = *c->batch;
     b.cancel.store(true);
     host_pool().wake();
     batch_join(b);
+    batch_trace_print(b);
     for (auto &r : b.ready)
         if (r.block) host_pool().put(r.block);
     b.ready.clear();

@@ -303,11 +303,21 @@ int rwmd_f32_min(Ctx &c, const double2 *q, const uint64_t *qkey, int64_t nq, con
         const int ntile = (int)((nt + TS_CULL - 1) / TS_CULL);
         k_tile_boxes<<<grid_for((int64_t)ntile * 32, 256, 8u * c.sm_count), 256, 0, c.stream>>>(t, (int)nt, TS_CULL, tbox);
         W1G_CHECK_LAUNCH();
-        constexpr int R = 2;
+        // sources per thread: 1 below ~300k sources (twice the CTAs of R = 2 for a short,
+        // latency-bound kernel), 2 above; W1G_TILE_R overrides (tuning).  Any R is exact:
+        // the seed only sizes the exact pass's search (rwmd.cu)
+        static const int r_env = [] {
+            const char *e = getenv("W1G_TILE_R");
+            return e ? atoi(e) : 0;
+        }();
+        const int R = r_env == 1 || r_env == 2 ? r_env : (nq <= 300000 ? 1 : 2);
         const int gx = (int)((nq + T_BLOCK * R - 1) / (T_BLOCK * R));
         A.chunk = (int)nt;
         if (c.prof) W1G_CUDA(cudaEventRecord(c.prof_ev[c.prof_side][0][0], c.stream));
-        k_rwmd_f32<R, true, TS_CULL><<<gx, T_BLOCK, 0, c.stream>>>(A);
+        if (R == 1)
+            k_rwmd_f32<1, true, TS_CULL><<<gx, T_BLOCK, 0, c.stream>>>(A);
+        else
+            k_rwmd_f32<2, true, TS_CULL><<<gx, T_BLOCK, 0, c.stream>>>(A);
         W1G_CHECK_LAUNCH();
         if (c.prof) W1G_CUDA(cudaEventRecord(c.prof_ev[c.prof_side][0][1], c.stream));
         return W1G_OK;

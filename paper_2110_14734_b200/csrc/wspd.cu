@@ -237,6 +237,143 @@ __global__ void __launch_bounds__(256) k_wspd_coop(ItemF *fa, ItemF *fb, int64_t
     if (blockIdx.x == 0 && threadIdx.x == 0) *levels_out = level;
 }
 
+// Fused order, first phase: the recursions run CTA-locally, with no grid barrier.
+// The owners' recursions are independent (spanner.py:206-241 runs one DFS per
+// internal node), so each CTA grabs a batch of owners from a global counter and
+// advances their items as a CTA-local breadth-first frontier in shared memory,
+// one __syncthreads-separated level at a time; pairs leave through one global
+// atomic per CTA and round.  Frontier items that do not fit in shared memory
+// spill to the global level-0 frontier (fa, counter cnt[0]) and are finished by
+// the grid-wide cooperative kernel that runs next (usually on nothing).
+constexpr int OW_T = 256;
+constexpr int OW_CAP = 2048;    // items per shared-memory frontier buffer
+constexpr int OW_BATCH = 64;    // owners grabbed per CTA at a time
+__global__ void __launch_bounds__(OW_T) k_wspd_owners(const int2 *__restrict__ lr, int64_t nn, int shard,
+                                                      int n_shards, const NodeGeom *__restrict__ geom, double s,
+                                                      Counters k, int64_t *owner_next, int32_t *max_depth,
+                                                      int2 *__restrict__ out_uv, int64_t pair_cap,
+                                                      ItemF *__restrict__ spill, int64_t spill_cap) {
+    __shared__ ItemF f[2][OW_CAP];
+    __shared__ int s_n[2];
+    __shared__ int s_np[OW_T / 32], s_ns[OW_T / 32];
+    __shared__ int64_t s_bp, s_w0;
+    __shared__ int s_next_base;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const unsigned lt = lanemask_lt();
+    int depth_max = 0;
+    for (;;) {
+        if (tid == 0) s_w0 = (int64_t)atomicAdd((unsigned long long *)owner_next, (unsigned long long)OW_BATCH);
+        if (tid == 0) s_n[0] = 0;
+        __syncthreads();
+        const int64_t w0 = s_w0;
+        if (w0 >= nn) break;
+        // seed: (left[w], right[w]) of the batch's internal nodes (this shard's)
+        int2 c = make_int2(-1, -1);
+        bool need = false;
+        unsigned m = 0;
+        if (tid < OW_BATCH) {
+            const int64_t w = w0 + tid;
+            c = w < nn ? lr[w] : make_int2(-1, -1);
+            need = c.x >= 0 && w % n_shards == shard;
+            m = __ballot_sync(0xffffffffu, need);
+            if (lane == 0) s_np[wid] = __popc(m);
+        }
+        __syncthreads();
+        if (tid < OW_BATCH) {
+            int off = 0;
+            for (int q = 0; q < wid; q++) off += s_np[q];
+            if (need) f[0][off + __popc(m & lt)] = ItemF{c.x, c.y};
+        }
+        if (tid == 0) {
+            int tot = 0;
+            for (int q = 0; q < OW_BATCH / 32; q++) tot += s_np[q];
+            s_n[0] = tot;
+        }
+        __syncthreads();
+        int cur = 0, depth = 0;
+        while (true) {
+            const int n = s_n[cur];
+            if (n == 0) break;
+            depth++;
+            if (tid == 0) s_n[cur ^ 1] = 0;
+            __syncthreads();
+            for (int base = 0; base < n; base += OW_T) {
+                const int i = base + tid;
+                const bool valid = i < n;
+                ItemF it{0, 0};
+                bool ws = false;
+                int2 c0 = make_int2(0, 0), c1 = make_int2(0, 0);
+                if (valid) {
+                    it = f[cur][i];
+                    const NodeGeom gu = geom[it.u], gv = geom[it.v];
+                    const int2 lu = lr[it.u], lv = lr[it.v];
+                    ws = ws_predicate(gu, gv, s);
+                    if (!ws) {
+                        if (gu.dsq > gv.dsq) {  // spanner.py:226-230
+                            c0 = make_int2(lu.x, it.v);
+                            c1 = make_int2(lu.y, it.v);
+                        } else {                // spanner.py:231-235
+                            c0 = make_int2(it.u, lv.x);
+                            c1 = make_int2(it.u, lv.y);
+                        }
+                    }
+                }
+                const unsigned mp = __ballot_sync(0xffffffffu, valid && ws);
+                const unsigned ms = __ballot_sync(0xffffffffu, valid && !ws);
+                if (lane == 0) {
+                    s_np[wid] = __popc(mp);
+                    s_ns[wid] = 2 * __popc(ms);
+                }
+                __syncthreads();
+                if (tid == 0) {
+                    int tp = 0, ts = 0;
+                    for (int w = 0; w < OW_T / 32; w++) {
+                        const int a = s_np[w], b = s_ns[w];
+                        s_np[w] = tp;
+                        s_ns[w] = ts;
+                        tp += a;
+                        ts += b;
+                    }
+                    s_bp = tp ? (int64_t)atomicAdd((unsigned long long *)k.pairs, (unsigned long long)tp) : 0;
+                    s_next_base = s_n[cur ^ 1];
+                    s_n[cur ^ 1] += ts;
+                }
+                __syncthreads();
+                const int64_t bp = s_bp + s_np[wid];
+                const int bs = s_next_base + s_ns[wid];
+                if (valid && ws) {
+                    const int64_t slot = bp + __popc(mp & lt);
+                    if (slot < pair_cap) out_uv[slot] = make_int2(it.u, it.v);
+                    else if (slot == pair_cap) atomicOr((unsigned long long *)&k.flags[F_PAIR_OVF], 1ull);
+                }
+                if (valid && !ws) {
+                    const int pos = bs + 2 * __popc(ms & lt);
+                    if (pos + 1 < OW_CAP) {
+                        f[cur ^ 1][pos] = ItemF{c0.x, c0.y};
+                        f[cur ^ 1][pos + 1] = ItemF{c1.x, c1.y};
+                    } else {
+                        // the CTA's frontier is full: these two continue in the grid-wide pass
+                        const int64_t g = (int64_t)atomicAdd((unsigned long long *)&k.cnt[0], 2ull);
+                        if (g + 1 < spill_cap) {
+                            spill[g] = ItemF{c0.x, c0.y};
+                            spill[g + 1] = ItemF{c1.x, c1.y};
+                        } else {
+                            atomicOr((unsigned long long *)&k.flags[F_FRONT_OVF], 1ull);
+                        }
+                    }
+                }
+                __syncthreads();  // s_np / s_ns are rewritten by the next round
+            }
+            if (tid == 0 && s_n[cur ^ 1] > OW_CAP) s_n[cur ^ 1] = OW_CAP;  // the rest spilled
+            __syncthreads();
+            cur ^= 1;
+        }
+        depth_max = depth > depth_max ? depth : depth_max;
+        __syncthreads();
+    }
+    if (tid == 0) atomicMax(max_depth, depth_max);
+}
+
 // reference order: the levels are appended to one array (level l occupies
 // [starts[l], starts[l+1])), so the whole recursion forest stays for the
 // ordering passes; `cap` is the array's capacity, max_levels starts' capacity
@@ -402,11 +539,26 @@ int wspd_run(Ctx &c, double s, int reference_order, int64_t *n_pairs, bool want_
         W1G_CUDA(cudaMemsetAsync(ctr, 0, sizeof(int64_t) * 8, c.stream));
         Counters k{ctr, ctr + 4, dflags(c)};
         const unsigned gi = grid_for(nn, 256, 8u * c.sm_count);
+        // fused order: the owners' recursions CTA-locally first (no grid barriers), the
+        // spilled remainder by the cooperative frontier below (W1G_WSPD_OWNERS=0: the
+        // frontier alone, every recursion seeded at level 0)
+        static const bool owners_env = [] {
+            const char *e = getenv("W1G_WSPD_OWNERS");
+            return !(e && *e == '0');
+        }();
         if (nn > 1) {
-            if (ORDER)
+            if (ORDER) {
                 k_wspd_init_o<<<gi, 256, 0, c.stream>>>(ptr<int2>(c.t_lr), nn, fa, own0, front_cap, ctr);
-            else
+            } else if (owners_env) {
+                int per = 0;
+                W1G_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_wspd_owners, OW_T, 0));
+                if (per < 1) per = 1;
+                k_wspd_owners<<<per * c.sm_count, OW_T, 0, c.stream>>>(
+                    ptr<int2>(c.t_lr), nn, shard, n_shards, ptr<NodeGeom>(c.t_geom), s, Counters{ctr, ctr + 4, dflags(c)},
+                    ctr + 5, reinterpret_cast<int32_t *>(ctr + 7), uv, pair_cap, fa, front_cap);
+            } else {
                 k_wspd_init_f<<<gi, 256, 0, c.stream>>>(ptr<int2>(c.t_lr), nn, fa, front_cap, ctr, shard, n_shards);
+            }
             W1G_CHECK_LAUNCH();
         }
         const unsigned gl = 8u * c.sm_count;
@@ -459,11 +611,14 @@ int wspd_run(Ctx &c, double s, int reference_order, int64_t *n_pairs, bool want_
                 W1G_TRY(stream_sync(c));
                 level = (int)(c.h_pinned[F_MISC0 + 6] & 0x7fffffff);
                 const int64_t live = c.h_pinned[F_MISC0 + level % 3];
+                // levels (diagnostics): the CTA-local owners' deepest recursion + the grid-wide rest
+                const int owner_depth = ORDER ? 0 : (int)(c.h_pinned[F_MISC0 + 7] & 0x7fffffff);
                 if (c.h_pinned[F_FRONT_OVF] || (!ORDER && live > front_cap)) {
                     ovf = true;
                     front_cap = front_cap * 2 + (live > front_cap ? live : 0);
                 }
                 nn_done = true;
+                if (!ORDER && !ovf) level += owner_depth;  // read after the overflow check
             }
         }
         while (nn > 1 && !nn_done) {

@@ -42,6 +42,7 @@ def run(ds, streams, reps=3):
             "d2h_gbs_if_link_bound": nbytes[0] / t / 1e9}
 
 
+streams = [int(x) for x in sys.argv[2].split(",")] if len(sys.argv) > 2 else [2, 4, 6, 8]
 for inputs, ds in (("pageable", diags), ("pinned", pinned)):
-    for st in (2, 4, 6, 8):
+    for st in streams:
         print(json.dumps({"inputs": inputs, **run(ds, st)}), flush=True)
