@@ -5,6 +5,9 @@
 //   V1 direct packed : FADD2 FADD2 FMUL2 FFMA2 + FMNMX3   per 2 evaluations
 //   V2 expand scalar : FFMA FFMA FMNMX                    per evaluation
 //   V3 expand packed : FFMA2 FFMA2 + FMNMX3               per 2 evaluations
+//   V4 expand packed, source pairs: the target broadcast as the scalar operand,
+//      two sources per FFMA2 (FFMA2 FFMA2 per 2 evaluations, FMNMX3 per 2 targets)
+//   V5 = V3 with 16 sources per thread
 // (expand: min_t |t|^2 - 2 q.t, |q|^2 added after the min).
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/rwmd_micro tools/rwmd_micro.cu
 #include <cstdio>
@@ -12,8 +15,11 @@
 #include <vector>
 
 constexpr int BLOCK = 256;
-constexpr int R = 8;
 constexpr int TILE = 2048;
+template <int V>
+struct RofV {
+    static constexpr int R = V == 5 ? 16 : 8;
+};
 
 __device__ __forceinline__ float min3(float a, float b, float c) {
     float d;
@@ -28,6 +34,7 @@ __global__ void __launch_bounds__(BLOCK) k(const float2 *q, int nq, const float2
     // V1/V3 layout: x pair, y pair, (V3) t2 pair
     __shared__ float4 s4[TILE / 2];
     __shared__ float2 s2[TILE / 2];
+    constexpr int R = RofV<V>::R;
     const int q0 = blockIdx.x * (BLOCK * R) + threadIdx.x;
     float qx[R], qy[R], m[R];
 #pragma unroll
@@ -56,6 +63,9 @@ __global__ void __launch_bounds__(BLOCK) k(const float2 *q, int nq, const float2
                 s4[j] = make_float4(a.x, b.x, a.y, b.y);
             else if (V == 2)
                 s4[j] = make_float4(a.x, a.y, a.x * a.x + a.y * a.y, 0.f), s2[j] = make_float2(b.x, b.y);
+            else if (V == 4)
+                s4[j] = make_float4(a.x, a.y, b.x, b.y),
+                s2[j] = make_float2(a.x * a.x + a.y * a.y, b.x * b.x + b.y * b.y);
             else {
                 s4[j] = make_float4(a.x, b.x, a.y, b.y);
                 s2[j] = make_float2(a.x * a.x + a.y * a.y, b.x * b.x + b.y * b.y);
@@ -93,6 +103,18 @@ __global__ void __launch_bounds__(BLOCK) k(const float2 *q, int nq, const float2
                     float e = fmaf(qy[r], w.y, fmaf(qx[r], w.x, w2));
                     m[r] = min3(m[r], d, e);
                 }
+            } else if (V == 4) {
+                const float2 tt = s2[j];
+#pragma unroll
+                for (int r = 0; r < R; r += 2) {
+                    const float2 qx2 = make_float2(qx[r], qx[r + 1]), qy2 = make_float2(qy[r], qy[r + 1]);
+                    float2 d0 = __ffma2_rn(make_float2(v.y, v.y), qy2,
+                                           __ffma2_rn(make_float2(v.x, v.x), qx2, make_float2(tt.x, tt.x)));
+                    float2 d1 = __ffma2_rn(make_float2(v.w, v.w), qy2,
+                                           __ffma2_rn(make_float2(v.z, v.z), qx2, make_float2(tt.y, tt.y)));
+                    m[r] = min3(m[r], d0.x, d1.x);
+                    m[r + 1] = min3(m[r + 1], d0.y, d1.y);
+                }
             } else {
                 const float2 tx = make_float2(v.x, v.y), ty = make_float2(v.z, v.w), tt = s2[j];
 #pragma unroll
@@ -113,6 +135,7 @@ __global__ void __launch_bounds__(BLOCK) k(const float2 *q, int nq, const float2
 
 template <int V>
 float run(const float2 *q, int nq, const float2 *t, int nt, unsigned *out, int sms) {
+    constexpr int R = RofV<V>::R;
     const int gx = (nq + BLOCK * R - 1) / (BLOCK * R);
     int gy = (16 * sms + gx - 1) / gx;
     int chunk = (nt + gy - 1) / gy;
@@ -148,11 +171,13 @@ int main(int argc, char **argv) {
     cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
     const double evals = (double)n * n;
     const double peak = sms * 128.0 * 2 * clk * 1e3;  // FP32 FLOP/s at the max clock
-    const char *names[] = {"V0 direct scalar", "V1 direct packed", "V2 expand scalar", "V3 expand packed"};
-    float ms[4] = {run<0>(d, n, d + n, n, o, sms), run<1>(d, n, d + n, n, o, sms),
-                   run<2>(d, n, d + n, n, o, sms), run<3>(d, n, d + n, n, o, sms)};
+    const char *names[] = {"V0 direct scalar", "V1 direct packed", "V2 expand scalar", "V3 expand packed",
+                           "V4 expand packed, source pairs", "V5 expand packed, R=16"};
+    float ms[6] = {run<0>(d, n, d + n, n, o, sms), run<1>(d, n, d + n, n, o, sms),
+                   run<2>(d, n, d + n, n, o, sms), run<3>(d, n, d + n, n, o, sms),
+                   run<4>(d, n, d + n, n, o, sms), run<5>(d, n, d + n, n, o, sms)};
     printf("{\"n\": %d, \"sms\": %d, \"clock_khz\": %d, \"variants\": [", n, sms, clk);
-    for (int v = 0; v < 4; v++)
+    for (int v = 0; v < 6; v++)
         printf("%s{\"name\": \"%s\", \"ms\": %.4f, \"Geval_per_s\": %.1f, \"tflops_5flop\": %.2f, "
                "\"frac_nominal_fp32\": %.3f}",
                v ? ", " : "", names[v], ms[v], evals / ms[v] / 1e6, 5 * evals / ms[v] / 1e9,
