@@ -602,6 +602,19 @@ def run_ours(args, dist: Dist):
             t_w1 = time.perf_counter() - t0
             extra["w1"] = {"value": value, "status": d.status, "pivots": d.pivots, "seconds": t_w1,
                            "solver": "reference w1flow.simplex (host, 1 thread)"}
+            # W1 pairs/s end to end on the batched matrix: front ends on the GPU, the networks
+            # handed (page-locked, zero-copy) to a pool of host solver threads
+            c4 = synth.shared_centre_batch(*CFG4, seed=0)
+            sub = [(i, j) for i in range(CFG4[0]) for j in range(i + 1, CFG4[0])][:48]
+            threads = max(1, host_threads() - 2)
+            t0 = time.perf_counter()
+            m = w1g.pairwise_w1(c4, params, devices=[device], pairs=sub, solver_threads=threads)
+            t_m = time.perf_counter() - t0
+            extra["w1_pairs"] = {"value": len(sub) / t_m, "unit": "W1 pairs/s", "pairs": len(sub),
+                                 "seconds": t_m, "solver_threads": threads,
+                                 "workload": f"{len(sub)} pairs of the cfg4 batch (64 x {CFG4[1]} points), "
+                                             "approx_w1 end to end (GPU front end + reference host simplex)",
+                                 "finite": bool(np.isfinite([m[i, j] for i, j in sub]).all())}
     if dist.rank != 0:
         return
     total_pairs = len(all_pairs)

@@ -135,7 +135,6 @@ struct BatchParams {
 
 struct BatchState {
     std::vector<w1g_ctx *> kids;
-    std::vector<int64_t> hint_n, hint_m;  // per child: the last network's size (output block sizing)
     std::vector<std::thread> threads;
     std::vector<int32_t> pairs;
     int64_t n_pairs = 0;
@@ -170,10 +169,95 @@ static int ensure_kids(Ctx &c, BatchState &b, int streams) {
         w1g_ctx *x = nullptr;
         W1G_TRY(w1g_ctx_create(c.device, &x));
         b.kids.push_back(x);
-        b.hint_n.push_back(0);
-        b.hint_m.push_back(0);
     }
     return W1G_OK;
+}
+
+// A delivered network leaves the worker asynchronously: when its front end has
+// finished, the five network arrays are copied device-to-device into one of the
+// worker's two staging slots (~15 us at cfg2), and their D2H into a page-locked
+// block is queued on the child's copy stream; the worker goes straight on to its
+// next pair, whose kernels run while the previous network crosses the host link.
+// A result is handed to the consumer once its copy has landed (checked after the
+// next front end, or before its staging slot is reused).
+struct PendingNet {
+    w1g_batch_result r;
+    int slot = -1;
+};
+
+// device-to-device copy of the network into a staging slot with SM loads/stores:
+// a cudaMemcpyAsync D2D would queue on the copy engines behind the link-bound D2H
+// transfers of earlier networks, and the next front end would wait for it
+struct CopyJob {
+    const int4 *src[5];
+    int4 *dst[5];
+    int64_t n16[5];  // 16-byte words
+};
+
+__global__ void k_stage_copy(CopyJob J) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int a = 0; a < 5; a++)
+        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < J.n16[a]; i += stride)
+            J.dst[a][i] = J.src[a][i];
+}
+
+struct StageSlot {
+    DevBuf sup, t, h, c, ro;
+    cudaEvent_t d2d = nullptr, done = nullptr;
+};
+
+static int stage_copy(w1g_ctx *x, cudaStream_t cs, StageSlot &st, int64_t n, int64_t m, const NetCarve &cv) {
+    int64_t *sup, *t, *h, *ro;
+    double *c;
+    W1G_TRY(ensure(st.sup, (size_t)n + 1, &sup));
+    W1G_TRY(ensure(st.t, (size_t)m + 1, &t));
+    W1G_TRY(ensure(st.h, (size_t)m + 1, &h));
+    W1G_TRY(ensure(st.c, (size_t)m + 1, &c));
+    W1G_TRY(ensure(st.ro, (size_t)n + 2, &ro));
+    if (!st.d2d) {
+        W1G_CUDA(cudaEventCreateWithFlags(&st.d2d, cudaEventDisableTiming));
+        W1G_CUDA(cudaEventCreateWithFlags(&st.done, cudaEventDisableTiming));
+    }
+    const cudaStream_t ms = x->stream;
+    // every buffer holds whole 16-byte words (ensure() pads by 16 bytes)
+    CopyJob J;
+    const void *src[5] = {x->net_sup.p, x->net_t.p, x->net_h.p, x->net_c.p, x->net_ro.p};
+    void *dst[5] = {sup, t, h, c, ro};
+    const int64_t cnt[5] = {n, m, m, m, n + 1};
+    for (int a = 0; a < 5; a++) {
+        J.src[a] = static_cast<const int4 *>(src[a]);
+        J.dst[a] = static_cast<int4 *>(dst[a]);
+        J.n16[a] = (cnt[a] + 1) / 2;
+    }
+    k_stage_copy<<<4 * x->sm_count, 256, 0, ms>>>(J);
+    W1G_CHECK_LAUNCH();
+    W1G_CUDA(cudaEventRecord(st.d2d, ms));
+    W1G_CUDA(cudaStreamWaitEvent(cs, st.d2d, 0));
+    W1G_CUDA(cudaMemcpyAsync(cv.sup, sup, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, cs));
+    W1G_CUDA(cudaMemcpyAsync(cv.t, t, sizeof(int64_t) * m, cudaMemcpyDeviceToHost, cs));
+    W1G_CUDA(cudaMemcpyAsync(cv.h, h, sizeof(int64_t) * m, cudaMemcpyDeviceToHost, cs));
+    W1G_CUDA(cudaMemcpyAsync(cv.c, c, sizeof(double) * m, cudaMemcpyDeviceToHost, cs));
+    W1G_CUDA(cudaMemcpyAsync(cv.ro, ro, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost, cs));
+    W1G_CUDA(cudaEventRecord(st.done, cs));
+    return W1G_OK;
+}
+
+static void batch_publish(BatchState *b, w1g_batch_result &r) {
+    {
+        std::lock_guard<std::mutex> lk(b->mu);
+        if (r.status != W1G_OK && b->first_rc == W1G_OK) {
+            b->first_rc = r.status;
+            b->first_err = r.message;
+        }
+        if (b->infos) b->infos[r.pair] = r.info;
+        if (b->deliver) b->ready.push_back(r);
+        b->produced++;
+    }
+    b->cv.notify_all();
+    if (r.status != W1G_OK) {
+        b->cancel.store(true);  // like the reference's loop: the first error ends the batch
+        host_pool().wake();
+    }
 }
 
 // one worker: pairs from the shared counter, front end on its own child context
@@ -182,9 +266,35 @@ static void batch_worker(Ctx *parent, BatchState *b, int w) {
     const double2 *corpus = ptr<double2>(parent->corpus_pts);
     const int64_t *off = parent->h_corpus_off;
     cudaSetDevice(x->device);
+    set_thread_stream(x->stream);
     using clk = std::chrono::steady_clock;
     auto us = [](clk::time_point a, clk::time_point b) {
         return 1e-3 * (double)std::chrono::duration_cast<std::chrono::nanoseconds>(b - a).count();
+    };
+    StageSlot slots[2];
+    // the D2H of delivered networks has a stream of its own: the context's copy stream
+    // carries work of the front end itself (the CSR's tails, RWMD's second side)
+    cudaStream_t d2h = nullptr;
+    if (b->deliver) cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking);
+    std::deque<PendingNet> pending;  // oldest first, at most 2 (one per slot)
+    int next_slot = 0;
+    // hand over the oldest pending network once its copy has landed (wait: block for it)
+    auto drain = [&](bool wait) {
+        while (!pending.empty()) {
+            PendingNet &pn = pending.front();
+            cudaEvent_t e = slots[pn.slot].done;
+            if (!wait && cudaEventQuery(e) == cudaErrorNotReady) return;
+            const cudaError_t err = cudaEventSynchronize(e);
+            if (err != cudaSuccess) {
+                pn.r.status = W1G_ECUDA;
+                snprintf(pn.r.message, sizeof pn.r.message, "network copy failed: %s", cudaGetErrorString(err));
+                if (pn.r.block) host_pool().put(pn.r.block);
+                pn.r.block = nullptr;
+            }
+            batch_publish(b, pn.r);
+            pending.pop_front();
+            wait = false;
+        }
     };
     for (;;) {
         if (b->cancel.load()) break;
@@ -196,87 +306,77 @@ static void batch_worker(Ctx *parent, BatchState *b, int w) {
         r.pair = p;
         r.i = i;
         r.j = j;
-        void *blk = nullptr;
-        int64_t ncap = 0, mcap = 0;
         int rc = W1G_OK;
-        const clk::time_point t0 = clk::now();
-        if (b->deliver && b->hint_m[w] > 0) {
-            // sized from this worker's previous network (+25 %: the pairs of a batch differ)
-            ncap = b->hint_n[w] + b->hint_n[w] / 4 + 64;
-            mcap = b->hint_m[w] + b->hint_m[w] / 4 + 1024;
-            rc = host_pool().get(carve_bytes(ncap, mcap), &blk, &b->cancel);
-            if (rc == W1G_OK) {
-                NetCarve cv = carve(blk, ncap, mcap);
-                rc = w1g_set_network_out(x, cv.sup, cv.t, cv.h, cv.c, cv.ro, ncap, mcap);
-            }
-        }
         const clk::time_point t1 = clk::now();
-        if (rc == W1G_OK) {
-            if (parent->h_corpus_ptr) {
-                // host-resident diagrams: this worker's H2D overlaps the other workers' front ends
-                rc = w1g_front_end(x, parent->h_corpus_ptr[i], off[i + 1] - off[i], parent->h_corpus_ptr[j],
-                                   off[j + 1] - off[j], b->prm.s, b->prm.use_condensation, b->prm.delta_mode,
-                                   b->prm.delta, b->prm.k, b->prm.seed, &r.info);
-            } else {
-                const double *pa = reinterpret_cast<const double *>(corpus + off[i]);
-                const double *pb = reinterpret_cast<const double *>(corpus + off[j]);
-                rc = w1g_front_end_device(x, pa, off[i + 1] - off[i], pb, off[j + 1] - off[j], b->prm.s,
-                                          b->prm.use_condensation, b->prm.delta_mode, b->prm.delta, b->prm.k,
-                                          b->prm.seed, &r.info);
-            }
+        if (parent->h_corpus_ptr) {
+            // host-resident diagrams: this worker's H2D overlaps the other workers' front ends
+            rc = w1g_front_end(x, parent->h_corpus_ptr[i], off[i + 1] - off[i], parent->h_corpus_ptr[j],
+                               off[j + 1] - off[j], b->prm.s, b->prm.use_condensation, b->prm.delta_mode,
+                               b->prm.delta, b->prm.k, b->prm.seed, &r.info);
+        } else {
+            const double *pa = reinterpret_cast<const double *>(corpus + off[i]);
+            const double *pb = reinterpret_cast<const double *>(corpus + off[j]);
+            rc = w1g_front_end_device(x, pa, off[i + 1] - off[i], pb, off[j + 1] - off[j], b->prm.s,
+                                      b->prm.use_condensation, b->prm.delta_mode, b->prm.delta, b->prm.k,
+                                      b->prm.seed, &r.info);
         }
         const clk::time_point t2 = clk::now();
+        drain(false);  // the previous network's copy ran under this front end
+        double t_block = 0.0;
+        bool queued = false;
         if (rc == W1G_OK && b->deliver && !r.info.short_circuit) {
             const int64_t n = r.info.node_count, m = r.info.n_arcs;
-            b->hint_n[w] = n;
-            b->hint_m[w] = m;
-            if (!r.info.network_copied) {  // no block yet, or it was too small: exact size, fetched
-                if (blk) host_pool().put(blk);
-                blk = nullptr;
-                ncap = n;
-                mcap = m;
-                rc = host_pool().get(carve_bytes(ncap, mcap), &blk, &b->cancel);
+            const int sl = next_slot;
+            // the slot's previous network must have left before the slot is rewritten
+            while (!pending.empty() && pending.front().slot == sl) drain(true);
+            void *blk = nullptr;
+            const clk::time_point tb = clk::now();
+            rc = host_pool().get(carve_bytes(n, m), &blk, &b->cancel);
+            t_block = us(tb, clk::now());
+            if (rc == W1G_OK) {
+                const NetCarve cv = carve(blk, n, m);
+                rc = d2h ? stage_copy(x, d2h, slots[sl], n, m, cv) : W1G_ECUDA;
                 if (rc == W1G_OK) {
-                    NetCarve cv = carve(blk, ncap, mcap);
-                    rc = w1g_fetch_network(x, cv.sup, cv.t, cv.h, cv.c, cv.ro);
+                    r.supplies = cv.sup;
+                    r.tails = cv.t;
+                    r.heads = cv.h;
+                    r.costs = cv.c;
+                    r.row_offsets = cv.ro;
+                    r.block = blk;
+                    pending.push_back(PendingNet{r, sl});
+                    next_slot ^= 1;
+                    queued = true;
+                } else {
+                    host_pool().put(blk);
                 }
             }
-            if (rc == W1G_OK) {
-                NetCarve cv = carve(blk, ncap, mcap);
-                r.supplies = cv.sup;
-                r.tails = cv.t;
-                r.heads = cv.h;
-                r.costs = cv.c;
-                r.row_offsets = cv.ro;
-                r.block = blk;
-                blk = nullptr;
-            }
         }
-        if (blk) host_pool().put(blk);  // short circuit or error: nothing to hand over
         if (b->trace) {
-            const clk::time_point t3 = clk::now();
-            b->tr_block[w] += us(t0, t1);
+            b->tr_block[w] += t_block;
             b->tr_fe[w] += us(t1, t2);
-            b->tr_fetch[w] += us(t2, t3);
+            b->tr_fetch[w] += us(t2, clk::now()) - t_block;
             b->tr_pairs[w] += 1;
         }
-        r.status = rc;
-        if (rc != W1G_OK) snprintf(r.message, sizeof r.message, "%s", w1g_last_error());
-        {
-            std::lock_guard<std::mutex> lk(b->mu);
-            if (rc != W1G_OK && b->first_rc == W1G_OK) {
-                b->first_rc = rc;
-                b->first_err = r.message;
-            }
-            if (b->infos) b->infos[p] = r.info;
-            if (b->deliver) b->ready.push_back(r);
-            b->produced++;
+        if (!queued) {
+            r.status = rc;
+            if (rc != W1G_OK) snprintf(r.message, sizeof r.message, "%s", w1g_last_error());
+            drain(true);  // keep completion order per worker
+            batch_publish(b, r);
         }
-        b->cv.notify_all();
-        if (rc != W1G_OK) {
-            b->cancel.store(true);  // like the reference's loop: the first error ends the batch
-            host_pool().wake();
-        }
+    }
+    drain(true);
+    if (d2h) {
+        cudaStreamSynchronize(d2h);
+        cudaStreamDestroy(d2h);
+    }
+    for (StageSlot &st : slots) {
+        free_buf(st.sup);
+        free_buf(st.t);
+        free_buf(st.h);
+        free_buf(st.c);
+        free_buf(st.ro);
+        if (st.d2d) cudaEventDestroy(st.d2d);
+        if (st.done) cudaEventDestroy(st.done);
     }
 }
 
@@ -302,6 +402,13 @@ static int batch_start(Ctx &c, const int32_t *pairs, int64_t n_pairs, const Batc
         return W1G_ESTATE;
     }
     W1G_TRY(ensure_kids(c, b, streams));
+    // several concurrent front ends: the level loops instead of the cooperative kernels
+    // (measured at cfg2 with 4 child contexts: 1546 vs 1411 pairs/s; W1G_BATCH_COOP=1 keeps them)
+    static const bool batch_coop = [] {
+        const char *e = getenv("W1G_BATCH_COOP");
+        return e && *e == '1';
+    }();
+    for (w1g_ctx *x : b.kids) x->no_coop = (streams > 1 && !batch_coop) ? 1 : 0;
     if (!c.h_corpus_ptr) W1G_CUDA(cudaStreamSynchronize(c.stream));  // the corpus upload is complete
     b.pairs.assign(pairs, pairs + 2 * n_pairs);
     b.n_pairs = n_pairs;

@@ -87,9 +87,23 @@ int stream_sync(Ctx &c) {
     return W1G_OK;
 }
 
+namespace {
+__global__ void k_to_host(const uint32_t *__restrict__ src, volatile uint32_t *dst, int n) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+}
+}  // namespace
+
+int to_host_small(Ctx &c, void *h_dst, const void *d_src, size_t bytes, cudaStream_t s) {
+    const int n = (int)(bytes / 4);
+    if (n <= 0) return W1G_OK;
+    k_to_host<<<1, n < 256 ? ((n + 31) & ~31) : 256, 0, s ? s : c.stream>>>(
+        static_cast<const uint32_t *>(d_src), static_cast<volatile uint32_t *>(h_dst), n);
+    W1G_CHECK_LAUNCH();
+    return W1G_OK;
+}
+
 int flags_fetch(Ctx &c, int first, int count) {
-    W1G_CUDA(cudaMemcpyAsync(c.h_pinned + first, dflags(c) + first, sizeof(int64_t) * count,
-                             cudaMemcpyDeviceToHost, c.stream));
+    W1G_TRY(to_host_small(c, c.h_pinned + first, dflags(c) + first, sizeof(int64_t) * count));
     W1G_TRY(stream_sync(c));
     return W1G_OK;
 }

@@ -162,6 +162,10 @@ struct Ctx {
     // exact refine kernels of each side, and device counters of the (source,
     // target) evaluations they perform: [side][0 = tile, 1 = refine]
     int prof = 0, prof_side = 0;
+    // prefer the multi-kernel level loops to the cooperative (grid-barrier) kernels of the
+    // split tree and the WSPD: set on the batch executor's child contexts when several run
+    // concurrently (a cooperative grid must be co-resident, which throttles the others)
+    int no_coop = 0;
     cudaEvent_t prof_ev[2][2][2] = {};
     DevBuf prof_cnt;  // 4 x unsigned long long
     int heavy_ratio = 16;  // exact pass: disc / median disc beyond which a source is searched alone (W1G_HEAVY, 0 off)
@@ -292,6 +296,15 @@ enum FlagSlot {
     F_NSLOTS = 64
 };
 
+// Small device -> host transfers (flags, counters, scalars) are written by a one-CTA
+// kernel straight into page-locked host memory (device-accessible under UVA) instead
+// of a cudaMemcpyAsync: copies go through the copy engines, where a few bytes would
+// queue behind the large network transfers of other contexts on the same GPU (the
+// batch executor's workers), stalling this context's host round trip.  h_dst must be
+// page-locked (h_pinned slots, pool blocks); bytes a multiple of 4.
+int to_host_small(Ctx &c, void *h_dst, const void *d_src, size_t bytes, cudaStream_t s = nullptr);
+// h_pinned slots for scalar results read back by the stages (RWMD sums)
+enum { H_SCALAR = 48 };  // 8 slots: 48..55
 int flags_reset(Ctx &c);
 // host wait for the context stream.  Every host round trip leaves the GPU
 // idle (D2H + wake-up + next launch); with W1G_TIMING=1 the idle time is

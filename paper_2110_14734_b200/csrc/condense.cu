@@ -438,8 +438,7 @@ int zc_run(Ctx &c, const double2 *d_a, int64_t na, const double2 *d_b, int64_t n
     W1G_CHECK_LAUNCH();
     k_zc_stats<<<grid_for(n, 256, 2u * c.sm_count), 256, 0, c.stream>>>(am, bm, pts, dflags(c) + F_K0, dflags(c));
     W1G_CHECK_LAUNCH();
-    W1G_CUDA(cudaMemcpyAsync(c.h_pinned + F_ZSTAT, dflags(c) + F_ZSTAT, sizeof(int64_t) * 6, cudaMemcpyDeviceToHost,
-                             c.stream));
+    W1G_TRY(to_host_small(c, c.h_pinned + F_ZSTAT, dflags(c) + F_ZSTAT, sizeof(int64_t) * 6));
     W1G_TRY(flags_fetch(c, F_K0, 2));
     if (speculative && lex2_speculation_failed(c, 1)) return zc_run(c, d_a, na, d_b, nb, k0, balanced, false);
     ns.k = c.h_pinned[F_K0];
@@ -643,8 +642,7 @@ int dc_run(Ctx &c, double delta, double pitch, double half_width, uint64_t seed,
         k_cl_check<<<grid_for(k, 256, 2u * c.sm_count), 256, 0, c.stream>>>(pts, dK, xl, yl, dflags(c));
         W1G_CHECK_LAUNCH();
         T.mark("check");
-        W1G_CUDA(cudaMemcpyAsync(c.h_pinned + F_LISTS, dflags(c) + F_LISTS, sizeof(int64_t), cudaMemcpyDeviceToHost,
-                                 c.stream));
+        W1G_TRY(to_host_small(c, c.h_pinned + F_LISTS, dflags(c) + F_LISTS, sizeof(int64_t)));
     }
     // node positions per side for emit_arcs, over k >= K (the masses past K are 0),
     // so their totals come back with K in the same round trip

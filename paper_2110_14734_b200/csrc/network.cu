@@ -1333,8 +1333,8 @@ int spanner_net_run(Ctx &c, int64_t *node_count, int64_t *n_arcs) {
     T.mark("long");
     if (side != c.stream) W1G_CUDA(cudaStreamWaitEvent(c.stream, c.ev[13], 0));  // the tails (and their copy)
     // the flags ride on the caller's final wait (no round trip here)
-    W1G_CUDA(cudaMemcpyAsync(c.h_pinned + F_OVERFLOW, dflags(c) + F_OVERFLOW, sizeof(int64_t) * (F_NET_ERR - F_OVERFLOW + 1),
-                             cudaMemcpyDeviceToHost, c.stream));
+    W1G_TRY(to_host_small(c, c.h_pinned + F_OVERFLOW, dflags(c) + F_OVERFLOW,
+                          sizeof(int64_t) * (F_NET_ERR - F_OVERFLOW + 1)));
     c.net_check_pending = true;
     c.arcs_valid = false;  // never materialised on this path
     c.net_n = n;

@@ -702,9 +702,10 @@ int rwmd_run(Ctx &c, double *L, double *LA, double *LB) {
         W1G_TRY(run_side(0));
         W1G_TRY(run_side(1));
     }
-    double h[2];
-    W1G_CUDA(cudaMemcpyAsync(h, dres, sizeof(double) * 2, cudaMemcpyDeviceToHost, c.stream));
+    W1G_TRY(to_host_small(c, c.h_pinned + H_SCALAR, dres, sizeof(double) * 2));
     W1G_TRY(stream_sync(c));
+    double h[2];
+    memcpy(h, c.h_pinned + H_SCALAR, sizeof h);
     *LA = h[0];
     *LB = h[1];
     *L = h[1] > h[0] ? h[1] : h[0];  // python max(l_a, l_b)
@@ -760,8 +761,9 @@ int rwmd_range_run(Ctx &c, int side, int64_t begin, int64_t end, double *partial
     W1G_TRY(launch_refine(c, F.mpts[s], F.mpos[s], F.members[s], mass[s], n_src, mf, qn, F.unscale, F.mpts[o], n_dst,
                           box64, sbox, best, terms));
     W1G_TRY(pairwise_sum(c, terms + begin, n_src, dres, c.scr[17], c.scr[18], c.scr[19]));
-    W1G_CUDA(cudaMemcpyAsync(partial, dres, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+    W1G_TRY(to_host_small(c, c.h_pinned + H_SCALAR, dres, sizeof(double)));
     W1G_TRY(stream_sync(c));
+    memcpy(partial, c.h_pinned + H_SCALAR, sizeof(double));
     return W1G_OK;
 }
 

@@ -473,6 +473,10 @@ __global__ void k_tie_put(const uint32_t *tpos, const uint32_t *tmp, int64_t t, 
 // preserves the primary's order weakly (k_key_compress) and elements whose
 // compressed keys tie (true primary ties and compression collisions alike)
 // are ordered afterwards by the full (primary, secondary, input position).
+__global__ void k_mm_init(unsigned long long *mm, int n) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) mm[i] = (i % 4) == 0 ? ~0ull : 0ull;
+}
+
 __global__ void k_key_range(const uint64_t *k, int64_t n, unsigned long long *mm) {
     unsigned long long lo = ~0ull, hi = 0ull;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -586,10 +590,10 @@ int sort_lex2_multi(Ctx &c, const Lex2Job *jobs, int njobs, bool speculative) {
     unsigned long long *mm;  // per job: key min, key max, longest tie run, tie count
     SortJob sj[RS_JOBS];
     W1G_TRY(ensure(c.sort_scr[1][3], (size_t)4 * RS_JOBS, &mm));
-    {
-        const unsigned long long init[4 * RS_JOBS] = {~0ull, 0ull, 0ull, 0ull, ~0ull, 0ull, 0ull, 0ull};
-        W1G_CUDA(cudaMemcpyAsync(mm, init, sizeof init, cudaMemcpyHostToDevice, c.stream));
-    }
+    // per job {key min = ~0, max = 0, longest run = 0, ties = 0}, set by a kernel: a
+    // host-to-device copy of a (pageable) stack array would go through the copy engines
+    k_mm_init<<<1, 32, 0, c.stream>>>(mm, 4 * RS_JOBS);
+    W1G_CHECK_LAUNCH();
     for (int j = 0; j < njobs; j++) {
         const int64_t n = jobs[j].n;
         W1G_TRY(ensure(c.lex_scr[j][0], (size_t)n + 1, &pk[j]));
@@ -618,13 +622,12 @@ int sort_lex2_multi(Ctx &c, const Lex2Job *jobs, int njobs, bool speculative) {
             k_tie_small<<<grid_for(jobs[j].n, 256, 8u * c.sm_count), 256, 0, c.stream>>>(
                 pk[j], jobs[j].n, jobs[j].primary, jobs[j].secondary, jobs[j].vals);
             W1G_CHECK_LAUNCH();
-            W1G_CUDA(cudaMemcpyAsync(c.h_pinned + H_LEX_MAXRUN + j, mm + 4 * j + 2, sizeof(unsigned long long),
-                                     cudaMemcpyDeviceToHost, c.stream));
+            W1G_TRY(to_host_small(c, c.h_pinned + H_LEX_MAXRUN + j, mm + 4 * j + 2, sizeof(unsigned long long)));
         }
         return W1G_OK;
     }
     unsigned long long *hm = reinterpret_cast<unsigned long long *>(c.h_pinned + F_SCAL);
-    W1G_CUDA(cudaMemcpyAsync(hm, mm, sizeof(unsigned long long) * 4 * njobs, cudaMemcpyDeviceToHost, c.stream));
+    W1G_TRY(to_host_small(c, hm, mm, sizeof(unsigned long long) * 4 * njobs));
     W1G_TRY(stream_sync(c));
     // elements of tie runs: short runs in place by one thread each; jobs with a
     // long run (e.g. an H0 diagram whose births are all 0) by a two-word radix
@@ -644,7 +647,7 @@ int sort_lex2_multi(Ctx &c, const Lex2Job *jobs, int njobs, bool speculative) {
         }
     }
     if (!any_long) return W1G_OK;
-    W1G_CUDA(cudaMemcpyAsync(&c.h_pinned[F_MISC2], dt, sizeof(int64_t) * njobs, cudaMemcpyDeviceToHost, c.stream));
+    W1G_TRY(to_host_small(c, &c.h_pinned[F_MISC2], dt, sizeof(int64_t) * njobs));
     W1G_TRY(stream_sync(c));
     SortJob tj[RS_JOBS];
     uint32_t *tpos[RS_JOBS], *pl[RS_JOBS];

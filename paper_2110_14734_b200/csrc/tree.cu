@@ -905,7 +905,11 @@ int tree_run(Ctx &c, const double2 *pts, int64_t n, int64_t *n_nodes, int32_t *d
     W1G_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * 16, c.stream));
     int levels = 0;
     const int64_t ntiles = (n + TP_TILE - 1) / TP_TILE;
-    const bool coop = n > LOCAL_MAX && ntiles <= COOP_MAX_TILES;
+    static const bool no_coop = [] {  // W1G_NO_COOP=1: the multi-kernel level loop (measurement)
+        const char *e = getenv("W1G_NO_COOP");
+        return e && *e == '1';
+    }();
+    const bool coop = n > LOCAL_MAX && ntiles <= COOP_MAX_TILES && !no_coop && !c.no_coop;
     double2 *xc[2] = {nullptr, nullptr}, *yc[2] = {nullptr, nullptr};
     if (coop) {
         W1G_TRY(ensure(c.scr[2], (size_t)n, &xc[0]));
@@ -960,7 +964,7 @@ int tree_run(Ctx &c, const double2 *pts, int64_t n, int64_t *n_nodes, int32_t *d
         W1G_CUDA(cudaLaunchCooperativeKernel((void *)k_tree_coop, G, 256, args, smem, c.stream));
         W1G_CHECK_LAUNCH();
         // the depth is read after the stage's (or, deferred, the caller's) next round trip
-        W1G_CUDA(cudaMemcpyAsync(c.h_pinned + H_TREE_DEPTH, lv, sizeof(int32_t), cudaMemcpyDeviceToHost, c.stream));
+        W1G_TRY(to_host_small(c, c.h_pinned + H_TREE_DEPTH, lv, sizeof(int32_t)));
         levels = -1;
     } else if (n > LOCAL_MAX) {
         // fallback for very large inputs: one launch per phase, host polls per batch
@@ -983,8 +987,7 @@ int tree_run(Ctx &c, const double2 *pts, int64_t n, int64_t *n_nodes, int32_t *d
                 W1G_CHECK_LAUNCH();
                 cur ^= 1;
             }
-            W1G_CUDA(cudaMemcpyAsync(c.h_pinned + F_ACTIVE, cnt + level % 3, sizeof(int32_t),
-                                     cudaMemcpyDeviceToHost, c.stream));
+            W1G_TRY(to_host_small(c, c.h_pinned + F_ACTIVE, cnt + level % 3, sizeof(int32_t)));
             W1G_TRY(stream_sync(c));
             const int32_t live = *reinterpret_cast<int32_t *>(c.h_pinned + F_ACTIVE);
             if (live == 0 || level > max_levels) break;
@@ -1003,8 +1006,7 @@ int tree_run(Ctx &c, const double2 *pts, int64_t n, int64_t *n_nodes, int32_t *d
     }
     T.mark("local");
     if (levels >= 0) c.h_pinned[H_TREE_DEPTH] = levels;  // host-known (multi-kernel path / no global levels)
-    W1G_CUDA(cudaMemcpyAsync(c.h_pinned + H_TREE_DUP, dflags(c) + F_DUP, sizeof(int64_t), cudaMemcpyDeviceToHost,
-                             c.stream));
+    W1G_TRY(to_host_small(c, c.h_pinned + H_TREE_DUP, dflags(c) + F_DUP, sizeof(int64_t)));
     W1G_CUDA(cudaEventRecord(c.ev[10], c.stream));  // the two copies above have landed once this has
     c.tree_valid = true;
     if (defer) {

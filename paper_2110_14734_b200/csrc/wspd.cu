@@ -588,7 +588,11 @@ int wspd_run(Ctx &c, double s, int reference_order, int64_t *n_pairs, bool want_
                 set_error("WSPD (reference order): cooperative launch unavailable");
                 return W1G_ECUDA;
             }
-            if (per_sm >= 1) {
+            static const bool no_coop = [] {  // W1G_NO_COOP=1: one launch per level (measurement)
+                const char *e = getenv("W1G_NO_COOP");
+                return e && *e == '1';
+            }();
+            if (per_sm >= 1 && !((no_coop || c.no_coop) && !ORDER)) {
                 const int G = per_sm * c.sm_count;
                 int32_t *lv = reinterpret_cast<int32_t *>(ctr + 6);
                 NodeGeom *geom = ptr<NodeGeom>(c.t_geom);
@@ -605,9 +609,8 @@ int wspd_run(Ctx &c, double s, int reference_order, int64_t *n_pairs, bool want_
                     W1G_CUDA(cudaLaunchCooperativeKernel(fn, G, 256, args, 0, c.stream));
                 }
                 W1G_CHECK_LAUNCH();
-                W1G_CUDA(cudaMemcpyAsync(c.h_pinned + F_MISC0, ctr, sizeof(int64_t) * 8, cudaMemcpyDeviceToHost, c.stream));
-                W1G_CUDA(cudaMemcpyAsync(c.h_pinned + F_PAIR_OVF, dflags(c) + F_PAIR_OVF, sizeof(int64_t) * 5,
-                                         cudaMemcpyDeviceToHost, c.stream));
+                W1G_TRY(to_host_small(c, c.h_pinned + F_MISC0, ctr, sizeof(int64_t) * 8));
+                W1G_TRY(to_host_small(c, c.h_pinned + F_PAIR_OVF, dflags(c) + F_PAIR_OVF, sizeof(int64_t) * 5));
                 W1G_TRY(stream_sync(c));
                 level = (int)(c.h_pinned[F_MISC0 + 6] & 0x7fffffff);
                 const int64_t live = c.h_pinned[F_MISC0 + level % 3];
@@ -628,9 +631,8 @@ int wspd_run(Ctx &c, double s, int reference_order, int64_t *n_pairs, bool want_
                                                        ptr<NodeGeom>(c.t_geom), ptr<int2>(c.t_lr));
                 W1G_CHECK_LAUNCH();
             }
-            W1G_CUDA(cudaMemcpyAsync(c.h_pinned + F_MISC0, ctr, sizeof(int64_t) * 8, cudaMemcpyDeviceToHost, c.stream));
-            W1G_CUDA(cudaMemcpyAsync(c.h_pinned + F_PAIR_OVF, dflags(c) + F_PAIR_OVF, sizeof(int64_t) * 5,
-                                     cudaMemcpyDeviceToHost, c.stream));
+            W1G_TRY(to_host_small(c, c.h_pinned + F_MISC0, ctr, sizeof(int64_t) * 8));
+            W1G_TRY(to_host_small(c, c.h_pinned + F_PAIR_OVF, dflags(c) + F_PAIR_OVF, sizeof(int64_t) * 5));
             W1G_TRY(stream_sync(c));
             const int64_t live = c.h_pinned[F_MISC0 + level % 3];
             if (c.h_pinned[F_FRONT_OVF] || live > front_cap) {
