@@ -574,7 +574,15 @@ int wspd_run(Ctx &c, double s, int reference_order, int64_t *n_pairs, bool want_
             // flight per SM would not grow, so one item per thread is used.)
             const double est_pairs = (double)K * (8.0 + 1.25 * s * s);  // as pair_cap
             const bool big = est_pairs > (double)(16 << 20);
-            const void *fn = ORDER ? (const void *)k_wspd_coop_o : (const void *)k_wspd_coop<1>;
+            // W1G_WSPD_IPT (tuning): items per thread and round of the grid-wide frontier
+            static const int ipt_env = [] {
+                const char *e = getenv("W1G_WSPD_IPT");
+                return e ? atoi(e) : 1;
+            }();
+            const void *fn = ORDER ? (const void *)k_wspd_coop_o
+                           : ipt_env == 2 ? (const void *)k_wspd_coop<2>
+                           : ipt_env == 4 ? (const void *)k_wspd_coop<4>
+                                          : (const void *)k_wspd_coop<1>;
             W1G_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, 0));
             // fewer CTAs -> cheaper grid barriers while the frontier is small; a big WSPD
             // (pairs expected well above what 2 CTAs/SM cover per level) wants every

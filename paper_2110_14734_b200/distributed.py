@@ -238,16 +238,20 @@ def sparsify_sharded(a, b, params: ApproxParams, rank: int, world: int, group=No
 
 
 def rwmd_rows_counts(counts, rank: int, world: int, partial_fn, group=None, device=None):
-    """rwmd_rows given the per-side member counts and a partial_fn(side, begin, end)."""
-    sides = []
-    for side, n in enumerate(counts):
-        plan = pairwise_plan(n, world)
-        mine = np.zeros(len(plan))
+    """rwmd_rows given the per-side member counts and a partial_fn(side, begin, end):
+    both sides' subtree sums of this rank travel in ONE all-gather."""
+    plans = [pairwise_plan(n, world) for n in counts]
+    mine = np.zeros(len(plans[0]) + len(plans[1]))
+    for side, plan in enumerate(plans):
+        base = 0 if side == 0 else len(plans[0])
         for i, (b_, e_) in enumerate(plan):
             if i % world == rank:
-                mine[i] = partial_fn(side, b_, e_)
-        gathered = _all_gather_f64(mine, group, device) if world > 1 else mine[None, :]
-        partials = [gathered[i % world, i] for i in range(len(plan))]
+                mine[base + i] = partial_fn(side, b_, e_)
+    gathered = _all_gather_f64(mine, group, device) if world > 1 else mine[None, :]
+    sides = []
+    for side, (n, plan) in enumerate(zip(counts, plans)):
+        base = 0 if side == 0 else len(plans[0])
+        partials = [gathered[i % world, base + i] for i in range(len(plan))]
         sides.append(pairwise_combine(n, world, partials))
     la, lb = sides
     return (lb if lb > la else la), la, lb
