@@ -58,7 +58,7 @@ N_POINTS = 100_000
 S = 1.0
 DELTA = 0.01
 K_LATTICE = 0.99
-PAIRS = 32
+PAIRS = 64
 STREAMS = 4
 CFG4 = (64, 20_000)
 
@@ -201,7 +201,7 @@ class Clocks:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
         except OSError:
@@ -209,9 +209,20 @@ class Clocks:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.monotonic(), line.strip()))
 
-    def stop(self) -> dict:
+    def wait_first(self, timeout: float = 3.0):
+        """Block until the sampler produces output (nvidia-smi takes a moment to start),
+        so the samples cover the timed region that follows."""
+        t0 = time.monotonic()
+        while self.proc and not self.lines and time.monotonic() - t0 < timeout:
+            time.sleep(0.01)
+
+    def mark(self):
+        return time.monotonic()
+
+    def stop(self, window=None) -> dict:
+        """Summary of the samples taken inside `window` = (t_start, t_end) (monotonic)."""
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         time.sleep(0.1)
@@ -222,7 +233,9 @@ class Clocks:
             self.proc.kill()
         sm, smax, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        for t, ln in self.lines:
+            if window and not (window[0] <= t <= window[1] + 0.06):
+                continue
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 9:
                 continue
@@ -235,7 +248,8 @@ class Clocks:
                 if v.lower() == "active":
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "sample_period_ms": 20,
+                "window_s": (window[1] - window[0]) if window else None}
 
 
 # ---------------------------------------------------------------- inputs
@@ -389,16 +403,18 @@ def time_batch(batch: Batch, steps: int, warmup: int, flush, dist: Dist, clocks=
     for _ in range(warmup):
         flush()
         batch.run()
-    dist.barrier()
     if clocks:
         clocks.start()
+        clocks.wait_first()
+    dist.barrier()
+    t_start = time.monotonic()
     launches0 = _lib.launch_count()
     times = []
     for _ in range(steps):
         flush()  # ordered on the library stream before the batch's start event
         times.append(batch.run())
     launches = (_lib.launch_count() - launches0) // max(steps, 1)
-    clk = clocks.stop() if clocks else None
+    clk = clocks.stop((t_start, time.monotonic())) if clocks else None
     dist.barrier()
     return dist.max(statistics.mean(times)), launches, clk
 

@@ -102,6 +102,16 @@ def rwmd_rows(nodes: SuppliedNodes, rank: int, world: int, group=None, device=No
     return rwmd_rows_counts(counts, rank, world, fn, group, device)
 
 
+def _dist_on() -> bool:
+    """A torch.distributed process group is up (even of one rank: its collectives run)."""
+    try:
+        import torch.distributed as dist
+
+        return dist.is_available() and dist.is_initialized()
+    except ImportError:
+        return False
+
+
 class _DeviceArray:
     """A library device buffer seen by torch without a copy (__cuda_array_interface__)."""
 
@@ -213,7 +223,7 @@ def sparsify_sharded(a, b, params: ApproxParams, rank: int, world: int, group=No
     ctx.call("w1g_emit_pair_arcs", 1 if rank == 0 else 0, ctypes.byref(m))
     diag.lower_bound, diag.delta, diag.epsilon_condense = L, d, eps
     diag.n_pairs = int(P.value)
-    if world == 1:
+    if not _dist_on():
         gathered = None
     else:
         tp, hp, cp = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
@@ -247,7 +257,7 @@ def rwmd_rows_counts(counts, rank: int, world: int, partial_fn, group=None, devi
         for i, (b_, e_) in enumerate(plan):
             if i % world == rank:
                 mine[base + i] = partial_fn(side, b_, e_)
-    gathered = _all_gather_f64(mine, group, device) if world > 1 else mine[None, :]
+    gathered = _all_gather_f64(mine, group, device) if _dist_on() else mine[None, :]
     sides = []
     for side, (n, plan) in enumerate(zip(counts, plans)):
         base = 0 if side == 0 else len(plans[0])

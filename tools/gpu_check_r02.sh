@@ -1,4 +1,3 @@
 mkdir -p gpurun_out
-W1G_TIMING=1 python tools/fe_once.py 1000000 1.0 0.01 2 > gpurun_out/timing_1m.log 2>&1
-ncu --set full --clock-control none --import-source on -k 'regex:k_sp_long_bitmap|k_sp_scatter|k_wspd_coop' -s 3 -c 3 -o gpurun_out/r02_cfg5w_csr \
-  python tools/fe_once.py 100000 16.0 0.001 > gpurun_out/ncu_cfg5w_csr.log 2>&1; echo rc=$?
+python -m pytest tests/test_gpu_retrieval.py tests/test_distributed.py -q -x > gpurun_out/t17.log 2>&1; echo rc=$? >> gpurun_out/t17.log
+python bench.py --steps 20 --warmup 5 > gpurun_out/bench5.json 2> gpurun_out/bench5.err; echo bench_rc=$?
