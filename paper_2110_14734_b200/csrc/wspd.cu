@@ -113,8 +113,9 @@ __device__ __forceinline__ void wspd_level(const ItemF *__restrict__ cur, ItemF 
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const unsigned lt = lanemask_lt();
     const int64_t stride = (int64_t)gridDim.x * blockDim.x * IPT;
-    __shared__ int s_np[8], s_ns[8];
+    __shared__ int s_np[32], s_ns[32];
     __shared__ int64_t s_bp, s_bs;
+    const int nw = blockDim.x >> 5;
     // block-uniform trip count
     for (int64_t bbase = (int64_t)blockIdx.x * blockDim.x * IPT; bbase < n; bbase += stride) {
         Item it[IPT];
@@ -166,17 +167,28 @@ __device__ __forceinline__ void wspd_level(const ItemF *__restrict__ cur, ItemF 
             s_ns[wid] = ns;
         }
         __syncthreads();
-        if (threadIdx.x == 0) {
-            int tp = 0, ts = 0;
-            for (int w = 0; w < 8; w++) {
-                const int a = s_np[w], b = s_ns[w];
-                s_np[w] = tp;
-                s_ns[w] = ts;
-                tp += a;
-                ts += b;
+        if (wid == 0) {
+            // exclusive scan of the warps' counts by warp 0, then one atomic per counter
+            int a = lane < nw ? s_np[lane] : 0, b = lane < nw ? s_ns[lane] : 0;
+            int ia = a, ib = b;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int ya = __shfl_up_sync(0xffffffffu, ia, o), yb = __shfl_up_sync(0xffffffffu, ib, o);
+                if (lane >= o) {
+                    ia += ya;
+                    ib += yb;
+                }
             }
-            s_bp = tp ? (int64_t)atomicAdd((unsigned long long *)k.pairs, (unsigned long long)tp) : 0;
-            s_bs = ts ? (int64_t)atomicAdd((unsigned long long *)&k.cnt[(level + 1) % 3], (unsigned long long)ts) : 0;
+            const int tp = __shfl_sync(0xffffffffu, ia, 31), ts = __shfl_sync(0xffffffffu, ib, 31);
+            if (lane < nw) {
+                s_np[lane] = ia - a;
+                s_ns[lane] = ib - b;
+            }
+            if (lane == 0) {
+                s_bp = tp ? (int64_t)atomicAdd((unsigned long long *)k.pairs, (unsigned long long)tp) : 0;
+                s_bs = ts ? (int64_t)atomicAdd((unsigned long long *)&k.cnt[(level + 1) % 3], (unsigned long long)ts)
+                          : 0;
+            }
         }
         __syncthreads();
         int64_t bp = s_bp + s_np[wid], bs = s_bs + s_ns[wid];
@@ -219,8 +231,8 @@ __global__ void __launch_bounds__(256) k_wspd_level(const ItemF *__restrict__ cu
 
 // all frontier levels in ONE persistent cooperative launch: a grid barrier
 // per level instead of a launch per level and a host poll per batch
-template <int IPT>
-__global__ void __launch_bounds__(256) k_wspd_coop(ItemF *fa, ItemF *fb, int64_t cap, Counters k,
+template <int IPT, int BT = 256>
+__global__ void __launch_bounds__(BT) k_wspd_coop(ItemF *fa, ItemF *fb, int64_t cap, Counters k,
                                                    int2 *__restrict__ out_uv, int64_t pair_cap, double s,
                                                    const NodeGeom *__restrict__ geom, const int2 *__restrict__ lr,
                                                    int32_t *levels_out) {
@@ -549,7 +561,9 @@ int wspd_run(Ctx &c, double s, int reference_order, int64_t *n_pairs, bool want_
         if (nn > 1) {
             if (ORDER) {
                 k_wspd_init_o<<<gi, 256, 0, c.stream>>>(ptr<int2>(c.t_lr), nn, fa, own0, front_cap, ctr);
-            } else if (owners_env) {
+            } else if (owners_env && K * (8.0 + 1.25 * s * s) <= (double)(16 << 20)) {
+                // (big WSPDs skip it: their recursions overflow the CTA-local frontier almost at
+                // once -- measured at cfg5 s = 16: owners 0.43 ms + grid 1.31 ms vs grid 1.26-1.6 ms)
                 int per = 0;
                 W1G_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_wspd_owners, OW_T, 0));
                 if (per < 1) per = 1;
@@ -579,11 +593,20 @@ int wspd_run(Ctx &c, double s, int reference_order, int64_t *n_pairs, bool want_
                 const char *e = getenv("W1G_WSPD_IPT");
                 return e ? atoi(e) : 1;
             }();
+            // W1G_WSPD_BT=1024 (tuning): 1024-thread CTAs -- a quarter of the CTAs, so a quarter
+            // of the per-round counter atomics and grid-barrier arrivals; measured slower at
+            // cfg5 s = 16 (5.48 vs 5.26 ms), so 256 by default
+            static const int bt_env = [] {
+                const char *e = getenv("W1G_WSPD_BT");
+                return e ? atoi(e) : 256;
+            }();
+            const int BT = ORDER ? 256 : (bt_env == 1024 ? 1024 : 256);
             const void *fn = ORDER ? (const void *)k_wspd_coop_o
+                           : BT == 1024 ? (const void *)k_wspd_coop<1, 1024>
                            : ipt_env == 2 ? (const void *)k_wspd_coop<2>
                            : ipt_env == 4 ? (const void *)k_wspd_coop<4>
                                           : (const void *)k_wspd_coop<1>;
-            W1G_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, 0));
+            W1G_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, BT, 0));
             // fewer CTAs -> cheaper grid barriers while the frontier is small; a big WSPD
             // (pairs expected well above what 2 CTAs/SM cover per level) wants every
             // resident warp for its memory-latency-bound levels.  W1G_COOP_PER_SM overrides.
@@ -614,7 +637,7 @@ int wspd_run(Ctx &c, double s, int reference_order, int64_t *n_pairs, bool want_
                     W1G_CUDA(cudaLaunchCooperativeKernel(fn, G, 256, args, 0, c.stream));
                 } else {
                     void *args[] = {&fap, &fbp, &fc, &k, &uvp, &pc, &sv, &geom, &lr, &lv};
-                    W1G_CUDA(cudaLaunchCooperativeKernel(fn, G, 256, args, 0, c.stream));
+                    W1G_CUDA(cudaLaunchCooperativeKernel(fn, G, BT, args, 0, c.stream));
                 }
                 W1G_CHECK_LAUNCH();
                 W1G_TRY(to_host_small(c, c.h_pinned + F_MISC0, ctr, sizeof(int64_t) * 8));
