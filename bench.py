@@ -134,7 +134,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg4"])
+    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg4", "cfg3"])
     ap.add_argument("--n", type=int, default=N_POINTS)
     ap.add_argument("--pairs", type=int, default=PAIRS)
     ap.add_argument("--streams", type=int, default=STREAMS)
@@ -453,7 +453,8 @@ def rwmd_roofline(ctx, w1g, a, b) -> dict:
         "ms_per_launch": ref_ms, "flop_per_launch": 5.0 * ref_ev, "evals_per_launch": ref_ev,
         "note": "achieved = 5 FLOP x the distance evaluations the launch performs (device counter) / its "
                 "event-timed duration; peak " + PEAKS["fp_source"],
-        "tile": {"bound": "fp32", "kernel": "k_rwmd_f32<2,1,256> (rwmd_tile.cu): culled FP32 seed pass",
+        "tile": {"bound": "fp32", "kernel": "k_rwmd_f32<R,1,256> (rwmd_tile.cu): culled FP32 seed pass, R = 1 source per thread below "
+                           "300k sources",
                  "achieved": f32, "peak": PEAKS["fp32_tflops"], "unit": "TFLOP/s",
                  "frac": f32 / PEAKS["fp32_tflops"], "ms_per_launch": tile_ms, "evals_per_launch": tile_ev,
                  "ncu": ncu_tile},
@@ -553,6 +554,51 @@ def e2e_single(w1g, a, b, args, device: int, flush, reps: int) -> dict:
                      "h2d_bytes_per_step": int(a.nbytes + b.nbytes), "d2h_bytes_per_step": int(d2h),
                      "delta": diag.delta, "device_ms": diag.stage_ms.get("total")}
     return out
+
+
+def run_sharded(args, dist: Dist):
+    """--workload cfg3: ONE 1M+1M pair, its front end sharded over the ranks
+    (distributed.sparsify_sharded: replicated condensing and tree, RWMD rows along
+    numpy's summation tree with one all-gather, WSPD owners by rank, arc slices
+    gathered on rank 0 with grouped NCCL send/recv).  Wall time of each step with a
+    device synchronisation on both sides and a barrier, max over ranks (the step has
+    host round trips and collectives; no single stream brackets it)."""
+    import torch
+
+    from paper_2110_14734_b200 import ApproxParams, synth
+    from paper_2110_14734_b200.distributed import sparsify_sharded
+
+    device = dist.local
+    torch.cuda.set_device(device)
+    n = args.n if args.n != N_POINTS else 1_000_000
+    a, b = synth.gaussian_cluster_pair(n, n, seed=0)
+    params = ApproxParams(s=args.s, best_effort=True, delta=args.delta)
+    for _ in range(max(3, args.warmup)):
+        sparsify_sharded(a, b, params, dist.rank, dist.world, device=device)
+    ts = []
+    net = None
+    for _ in range(args.steps):
+        torch.cuda.synchronize()
+        dist.barrier()
+        t0 = time.perf_counter()
+        net, diag = sparsify_sharded(a, b, params, dist.rank, dist.world, device=device)
+        torch.cuda.synchronize()
+        ts.append(time.perf_counter() - t0)
+    t = dist.max(statistics.mean(ts))
+    if dist.rank != 0:
+        return
+    d2h = sum(getattr(net, f).nbytes for f in ("supplies", "tails", "heads", "costs", "row_offsets"))
+    print(json.dumps({
+        "metric": METRIC, "value": 1.0 / t, "unit": "pairs/s", "n_gpus": dist.world, "steps": args.steps,
+        "warmup": max(3, args.warmup), "ms_per_step": 1e3 * t, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (the reference generator)",
+        "config": {"workload": f"cfg3: one {n}+{n}-point pair, front end sharded over {dist.world} rank(s), "
+                               f"s={args.s}, delta={args.delta}", "pairs_per_step": 1},
+        "e2e": {"value": 1.0 / t, "unit": "pairs/s", "h2d_bytes_per_step": int(a.nbytes + b.nbytes),
+                "d2h_bytes_per_step": int(d2h), "api": "paper_2110_14734_b200.distributed.sparsify_sharded"},
+        "timing": "wall clock per step between device synchronisations and a barrier, max over ranks",
+        "lower_bound": diag.lower_bound, "arcs": int(net.tails.shape[0]), "gpu_launches": None,
+        "roofline": None}), flush=True)
 
 
 def run_ours(args, dist: Dist):
@@ -684,6 +730,8 @@ def main():
     try:
         if args.impl == "reference":
             run_reference(args, dist)
+        elif args.workload == "cfg3":
+            run_sharded(args, dist)
         else:
             run_ours(args, dist)
     finally:
