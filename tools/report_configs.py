@@ -68,7 +68,14 @@ def cfg1():
     from w1flow.diagram import PersistenceDiagram
 
     a, b = synth.gaussian_cluster_pair(1000, 1000, seed=0)
-    exact = ref_oracle.exact_w1_dense(PersistenceDiagram(a), PersistenceDiagram(b))
+    t0 = time.perf_counter()
+    exact = w1g.exact_w1_dense(a, b)  # the dense network built on the B200, the reference simplex
+    t_gpu = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    exact_ref = ref_oracle.exact_w1_dense(PersistenceDiagram(a), PersistenceDiagram(b))
+    t_ref = time.perf_counter() - t0
+    emit({"config": "cfg1", "exact_w1_dense": exact, "reference_exact_w1_dense": exact_ref,
+          "rel_diff": abs(exact - exact_ref) / exact_ref, "seconds_dropin": t_gpu, "seconds_reference": t_ref})
     for s, delta in ((1.0, 0.01), (1.0, None), (12.0, None), (40.0, None)):
         params = w1g.ApproxParams(s=s, best_effort=True, delta=delta)
         w1g.sparsify(a, b, params)  # warm: device buffers sized for this s (first-use allocations)
