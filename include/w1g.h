@@ -121,6 +121,9 @@ int w1g_rwmd_range(w1g_ctx *ctx, int side, int64_t begin, int64_t end, double *p
  * sums its subtrees on its own device and host thread, and the host recombines them in
  * the tree's order -- bit-identical to w1g_rwmd */
 int w1g_rwmd_sharded(w1g_ctx **ctxs, int G, double *L, double *LA, double *LB);
+/* the A- and B-member counts of nodes0 (the row counts w1g_rwmd_range splits); free when
+ * nodes0 came from zero_condense */
+int w1g_member_counts(w1g_ctx *ctx, int64_t *n_a, int64_t *n_b);
 /* tile culling in the FP32 all-pairs pass: 1 (default) or 0 (full brute force) */
 int w1g_set_rwmd_culling(w1g_ctx *ctx, int enabled);
 
@@ -167,6 +170,14 @@ int w1g_emit_pair_arcs(w1g_ctx *ctx, int with_diagonal, int64_t *n_arcs);
 /* device pointers of the context's arc list (int64 tails, int64 heads, float64 costs): the
  * send buffers of the multi-GPU arc gather (valid until the next stage call) */
 int w1g_arcs_device(w1g_ctx *ctx, void **tails, void **heads, void **costs, int64_t *m);
+/* the WSPD node pairs (int2 (u, v) tree node ids) in device memory: the compact send
+ * buffer of the multi-GPU gather (8 bytes per pair instead of two 24-byte arcs) */
+int w1g_pairs_device(w1g_ctx *ctx, void **uv, int64_t *n_pairs);
+/* adopt gathered node pairs (device memory) over this context's own split tree */
+int w1g_load_pairs_device(w1g_ctx *ctx, const void *d_uv, int64_t n_pairs);
+/* emit_arcs + assemble fused (the front end's network builder) from the context's
+ * nodes, split tree and node pairs: the network of a sharded front end on rank 0 */
+int w1g_network_from_pairs(w1g_ctx *ctx, int64_t *node_count, int64_t *n_arcs);
 /* adopt an arc list already in this device's memory (the gathered slices), device to device */
 int w1g_load_arcs_device(w1g_ctx *ctx, const int64_t *d_tails, const int64_t *d_heads, const double *d_costs,
                          int64_t m);

@@ -113,6 +113,7 @@ _PROTOS = [
     ("w1g_rwmd", ctypes.c_int, [_vp, _F64P, _F64P, _F64P]),
     ("w1g_fetch_rwmd_best", ctypes.c_int, [_vp, ctypes.c_int, _F64P, _I64P]),
     ("w1g_set_rwmd_culling", ctypes.c_int, [_vp, ctypes.c_int]),
+    ("w1g_member_counts", ctypes.c_int, [_vp, _I64P, _I64P]),
     ("w1g_rwmd_sharded", ctypes.c_int, [ctypes.POINTER(_vp), ctypes.c_int, _F64P, _F64P, _F64P]),
     ("w1g_rwmd_range", ctypes.c_int, [_vp, ctypes.c_int, _i64, _i64, _F64P, _I64P]),
     ("w1g_delta_condense", ctypes.c_int, [_vp, _f64, _f64, _f64, _u64, _I64P]),
@@ -126,6 +127,9 @@ _PROTOS = [
     ("w1g_emit_pair_arcs", ctypes.c_int, [_vp, ctypes.c_int, _I64P]),
     ("w1g_arcs_device", ctypes.c_int, [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(_vp), _I64P]),
     ("w1g_load_arcs_device", ctypes.c_int, [_vp, _vp, _vp, _vp, _i64]),
+    ("w1g_pairs_device", ctypes.c_int, [_vp, ctypes.POINTER(_vp), _I64P]),
+    ("w1g_load_pairs_device", ctypes.c_int, [_vp, _vp, _i64]),
+    ("w1g_network_from_pairs", ctypes.c_int, [_vp, _I64P, _I64P]),
     ("w1g_fetch_pair_counts", ctypes.c_int, [_vp, _I64P, _I64P]),
     ("w1g_load_pairs", ctypes.c_int, [_vp, _I64P, _i64, _F64P, _i64]),
     ("w1g_emit_arcs", ctypes.c_int, [_vp, _I64P]),

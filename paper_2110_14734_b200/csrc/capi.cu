@@ -461,6 +461,24 @@ int w1g_rwmd_range(w1g_ctx *c, int side, int64_t begin, int64_t end, double *par
     return rwmd_range_run(*c, side, begin, end, partial, n_members);
 }
 
+int w1g_member_counts(w1g_ctx *c, int64_t *n_a, int64_t *n_b) {
+    CTX_CHECK(c);
+    NodeSet &ns = c->nodes[0];
+    if (!ns.valid) {
+        set_error("member_counts: no nodes0");
+        return W1G_ESTATE;
+    }
+    if (ns.stats) {  // zero_condense delivered them
+        *n_a = ns.nmem[0];
+        *n_b = ns.nmem[1];
+        return W1G_OK;
+    }
+    double dummy;
+    W1G_TRY(rwmd_range_run(*c, 0, 0, 0, &dummy, n_a));
+    W1G_TRY(rwmd_range_run(*c, 1, 0, 0, &dummy, n_b));
+    return W1G_OK;
+}
+
 int w1g_set_rwmd_culling(w1g_ctx *c, int enabled) {
     if (!c) return W1G_EINVAL;
     c->culling = enabled ? 1 : 0;
@@ -680,6 +698,49 @@ int w1g_arcs_device(w1g_ctx *c, void **tails, void **heads, void **costs, int64_
     *heads = c->arc_h.p;
     *costs = c->arc_c.p;
     *m = c->n_arcs;
+    return W1G_OK;
+}
+
+int w1g_pairs_device(w1g_ctx *c, void **uv, int64_t *n_pairs) {
+    CTX_CHECK(c);
+    if (!c->pairs_valid || !c->pairs_have_nodes) {
+        set_error("no WSPD node pairs");
+        return W1G_ESTATE;
+    }
+    *uv = c->pair_uv.p;
+    *n_pairs = c->n_pairs;
+    return W1G_OK;
+}
+
+int w1g_load_pairs_device(w1g_ctx *c, const void *d_uv, int64_t n_pairs) {
+    CTX_CHECK(c);
+    if (n_pairs < 0 || n_pairs >= (1ll << 31)) return W1G_EINVAL;
+    if (!c->tree_valid) {
+        set_error("load_pairs_device: the pairs index this context's split tree (build it first)");
+        return W1G_ESTATE;
+    }
+    int2 *uv;
+    W1G_TRY(ensure(c->pair_uv, (size_t)n_pairs + 1, &uv));
+    if (n_pairs) W1G_CUDA(cudaMemcpyAsync(uv, d_uv, sizeof(int2) * n_pairs, cudaMemcpyDeviceToDevice, c->stream));
+    c->n_pairs = n_pairs;
+    c->pairs_valid = true;
+    c->pairs_have_nodes = true;
+    c->pair_idx_valid = false;
+    c->arcs_valid = false;
+    c->net_valid = false;
+    return W1G_OK;
+}
+
+int w1g_network_from_pairs(w1g_ctx *c, int64_t *node_count, int64_t *n_arcs) {
+    CTX_CHECK(c);
+    if (!c->pairs_valid || !c->pairs_have_nodes || !c->nodes[1].valid || !c->tree_valid) {
+        set_error("network_from_pairs: needs the condensed nodes, their split tree and WSPD node pairs");
+        return W1G_ESTATE;
+    }
+    W1G_TRY(spanner_net_run(*c, node_count, n_arcs));
+    W1G_TRY(stream_sync(*c));
+    bool redone = false;
+    W1G_TRY(spanner_net_check(*c, node_count, n_arcs, &redone));
     return W1G_OK;
 }
 

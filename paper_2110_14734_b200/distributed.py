@@ -121,14 +121,20 @@ class _DeviceArray:
 
 
 def gather_arcs(tails, heads, costs, rank: int, world: int, group=None):
-    """Rank 0 receives every rank's arc slice (grouped point-to-point: one
-    send per array per rank, posted together -- NCCL groups them into one
-    ncclGroupStart/End over NVLink).  Arguments and results are torch tensors
-    on the rank's device (NCCL) or on the CPU (gloo).  Returns the concatenated
-    (tails, heads, costs) on rank 0 (slices in rank order), None elsewhere."""
+    """Rank 0 receives every rank's arc slice: gather_slices of (tails, heads, costs)."""
+    return gather_slices((tails, heads, costs), rank, world, group)
+
+
+def gather_slices(arrays, rank: int, world: int, group=None):
+    """Rank 0 receives every rank's slices of the equally long 1-D `arrays`
+    (grouped point-to-point: one send per array per rank, posted together --
+    NCCL groups them into one ncclGroupStart/End over NVLink).  Arguments and
+    results are torch tensors on the rank's device (NCCL) or on the CPU (gloo).
+    Returns the concatenations on rank 0 (slices in rank order), None elsewhere."""
     import torch
     import torch.distributed as dist
 
+    tails = arrays[0]
     dev = tails.device
     m = torch.tensor([tails.shape[0]], dtype=torch.int64, device=dev)
     counts = [torch.zeros_like(m) for _ in range(world)]
@@ -138,11 +144,9 @@ def gather_arcs(tails, heads, costs, rank: int, world: int, group=None):
     out = None
     if rank == 0:
         total = sum(counts)
-        out = (torch.empty(total, dtype=torch.int64, device=dev), torch.empty(total, dtype=torch.int64, device=dev),
-               torch.empty(total, dtype=torch.float64, device=dev))
-        out[0][:counts[0]].copy_(tails)
-        out[1][:counts[0]].copy_(heads)
-        out[2][:counts[0]].copy_(costs)
+        out = tuple(torch.empty(total, dtype=x.dtype, device=dev) for x in arrays)
+        for o, x in zip(out, arrays):
+            o[:counts[0]].copy_(x)
         off = counts[0]
         for r in range(1, world):
             if counts[r]:
@@ -150,7 +154,7 @@ def gather_arcs(tails, heads, costs, rank: int, world: int, group=None):
                     ops.append(dist.P2POp(dist.irecv, buf[off:off + counts[r]], r, group))
             off += counts[r]
     elif counts[rank]:
-        for t in (tails, heads, costs):
+        for t in arrays:
             ops.append(dist.P2POp(dist.isend, t.contiguous(), 0, group))
     if ops:
         for w in dist.batch_isend_irecv(ops):
@@ -166,10 +170,11 @@ def sparsify_sharded(a, b, params: ApproxParams, rank: int, world: int, group=No
     * RWMD rows are sharded along numpy's summation tree (rwmd_rows): the G
       partial sums are all-gathered (8 bytes each) and combined in tree order;
     * the WSPD owner loop (spanner.py:206-241) is sharded: rank r runs the
-      recursions of the internal nodes w with w % world == r and emits their
-      arcs (rank 0 also the diagonal arcs);
-    * the arc slices are gathered on rank 0 (grouped send/recv over NCCL),
-      which assembles the CSR network.
+      recursions of the internal nodes w with w % world == r;
+    * the arc list is gathered on rank 0 in its compact form -- the shards' node
+      pairs, 8 bytes per pair instead of two 24-byte arcs (grouped send/recv over
+      NCCL) -- and rank 0, which holds the same nodes and tree, emits the arcs
+      fused into its CSR build (the front end's network builder).
 
     Rank 0 returns (network, diagnostics); the other ranks (None, diagnostics).
     The network is bit-identical to the single-GPU front end's: the CSR is a
@@ -198,12 +203,9 @@ def sparsify_sharded(a, b, params: ApproxParams, rank: int, world: int, group=No
         ctx.call("w1g_rwmd_range", side, int(b_), int(e_), ctypes.byref(out), ctypes.byref(nm))
         return out.value
 
-    counts = []
-    for side in (0, 1):
-        out = ctypes.c_double(0.0)
-        nm = ctypes.c_int64(0)
-        ctx.call("w1g_rwmd_range", side, 0, 0, ctypes.byref(out), ctypes.byref(nm))
-        counts.append(int(nm.value))
+    na_, nb_ = ctypes.c_int64(0), ctypes.c_int64(0)
+    ctx.call("w1g_member_counts", ctypes.byref(na_), ctypes.byref(nb_))
+    counts = [int(na_.value), int(nb_.value)]
     L, la, lb = rwmd_rows_counts(counts, rank, world, partial, group, device)
     eps = condensation_epsilon(params.s)
     d = 0.0
@@ -219,31 +221,28 @@ def sparsify_sharded(a, b, params: ApproxParams, rank: int, world: int, group=No
     ctx.call("w1g_split_tree", _lib.NODES, ctypes.byref(nn), ctypes.byref(depth))
     P = ctypes.c_int64(0)
     ctx.call("w1g_wspd_shard", float(params.s), int(rank), int(world), ctypes.byref(P))
-    m = ctypes.c_int64(0)
-    ctx.call("w1g_emit_pair_arcs", 1 if rank == 0 else 0, ctypes.byref(m))
     diag.lower_bound, diag.delta, diag.epsilon_condense = L, d, eps
     diag.n_pairs = int(P.value)
-    if not _dist_on():
-        gathered = None
-    else:
-        tp, hp, cp = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
-        ctx.call("w1g_arcs_device", ctypes.byref(tp), ctypes.byref(hp), ctypes.byref(cp), ctypes.byref(m))
-        dev = torch.device("cuda", ctx.device)
-        n = int(m.value)
-        tails = torch.as_tensor(_DeviceArray(tp.value, n, "<i8"), device=dev)
-        heads = torch.as_tensor(_DeviceArray(hp.value, n, "<i8"), device=dev)
-        costs = torch.as_tensor(_DeviceArray(cp.value, n, "<f8"), device=dev)
-        gathered = gather_arcs(tails, heads, costs, rank, world, group)
+    gathered = None
+    if _dist_on():
+        # the shard's node pairs (int2, 8 bytes each) travel, not its arcs (two 24-byte arcs
+        # per pair): every rank holds the same tree, so rank 0 emits the arcs itself, fused
+        # into its CSR build
+        up = ctypes.c_void_p()
+        ctx.call("w1g_pairs_device", ctypes.byref(up), ctypes.byref(P))
+        uv = torch.as_tensor(_DeviceArray(up.value, 2 * int(P.value), "<i4"), device=torch.device("cuda", ctx.device))
+        gathered = gather_slices((uv,), rank, world, group)
     if rank != 0:
         return None, diag
     if gathered is not None:
         torch.cuda.synchronize(ctx.device)  # the received slices are complete before the library reads them
-        t, h, c = gathered
-        ctx.call("w1g_load_arcs_device", t.data_ptr(), h.data_ptr(), c.data_ptr(), t.shape[0])
+        (guv,) = gathered
+        ctx.call("w1g_load_pairs_device", guv.data_ptr(), guv.shape[0] // 2)
     ncount, narcs = ctypes.c_int64(0), ctypes.c_int64(0)
-    ctx.call("w1g_assemble", ctypes.byref(ncount), ctypes.byref(narcs))
+    ctx.call("w1g_network_from_pairs", ctypes.byref(ncount), ctypes.byref(narcs))
     net = fetch_network(ctx, int(ncount.value), int(narcs.value))
     diag.n_nodes, diag.n_arcs = int(ncount.value), int(narcs.value)
+    diag.n_pairs = int(guv.shape[0] // 2) if gathered is not None else diag.n_pairs
     return net, diag
 
 

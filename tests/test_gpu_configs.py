@@ -218,3 +218,50 @@ def test_sparsify_sharded_nccl_world1(w1g):
                 assert bits_equal(getattr(net, f), getattr(ref, f)), f
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("G", [2, 4])
+def test_gathered_shard_pairs_build_the_network(w1g, G):
+    """The sharded front end's gather: each shard's node pairs (w1g_pairs_device), concatenated
+    on "rank 0" (w1g_load_pairs_device) and turned into the network by the fused builder
+    (w1g_network_from_pairs) -- bit-identical to the single-GPU front end."""
+    import ctypes
+
+    import torch
+
+    from paper_2110_14734_b200 import _lib, synth
+    from paper_2110_14734_b200.network import fetch_network
+
+    a, b = synth.gaussian_cluster_pair(100_000, 100_000, seed=3)
+    ref, _ = w1g.sparsify(a, b, w1g.ApproxParams(s=2.0, best_effort=True, delta=0.01))
+    ctx = _lib.context()
+    k0, bal = ctypes.c_int64(), ctypes.c_int32()
+    ap, bp = np.ascontiguousarray(a), np.ascontiguousarray(b)
+    ctx.call("w1g_zero_condense", _lib.f64p(ap), ap.shape[0], _lib.f64p(bp), bp.shape[0], ctypes.byref(k0),
+             ctypes.byref(bal))
+    kk = ctypes.c_int64()
+    ctx.call("w1g_delta_condense", 0.01, 0.99 * 0.01, (1.0 - 0.99) * 0.01 / 2.0, ctypes.c_uint64(0), ctypes.byref(kk))
+    nn, depth = ctypes.c_int64(), ctypes.c_int32()
+    ctx.call("w1g_split_tree", _lib.NODES, ctypes.byref(nn), ctypes.byref(depth))
+    parts = []
+    for g in range(G):
+        P = ctypes.c_int64()
+        ctx.call("w1g_wspd_shard", 2.0, g, G, ctypes.byref(P))
+        up = ctypes.c_void_p()
+        ctx.call("w1g_pairs_device", ctypes.byref(up), ctypes.byref(P))
+        ctx.call("w1g_synchronize")
+        n = 2 * P.value
+        buf = torch.empty(n, dtype=torch.int32, device="cuda")
+        src = torch.as_tensor(type("A", (), {"__cuda_array_interface__": {
+            "shape": (n,), "typestr": "<i4", "data": (up.value, False), "version": 3, "strides": None}})(),
+            device="cuda")
+        buf.copy_(src)
+        parts.append(buf)
+    allp = torch.cat(parts)
+    torch.cuda.synchronize()
+    ctx.call("w1g_load_pairs_device", allp.data_ptr(), allp.shape[0] // 2)
+    n_, m_ = ctypes.c_int64(), ctypes.c_int64()
+    ctx.call("w1g_network_from_pairs", ctypes.byref(n_), ctypes.byref(m_))
+    net = fetch_network(ctx, n_.value, m_.value)
+    for f in NET_FIELDS:
+        assert bits_equal(getattr(net, f), getattr(ref, f)), f
