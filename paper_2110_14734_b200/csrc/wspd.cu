@@ -231,8 +231,8 @@ __global__ void __launch_bounds__(256) k_wspd_level(const ItemF *__restrict__ cu
 
 // all frontier levels in ONE persistent cooperative launch: a grid barrier
 // per level instead of a launch per level and a host poll per batch
-template <int IPT, int BT = 256>
-__global__ void __launch_bounds__(BT) k_wspd_coop(ItemF *fa, ItemF *fb, int64_t cap, Counters k,
+template <int IPT, int BT = 256, int MINB = 1>
+__global__ void __launch_bounds__(BT, MINB) k_wspd_coop(ItemF *fa, ItemF *fb, int64_t cap, Counters k,
                                                    int2 *__restrict__ out_uv, int64_t pair_cap, double s,
                                                    const NodeGeom *__restrict__ geom, const int2 *__restrict__ lr,
                                                    int32_t *levels_out) {
@@ -561,9 +561,8 @@ int wspd_run(Ctx &c, double s, int reference_order, int64_t *n_pairs, bool want_
         if (nn > 1) {
             if (ORDER) {
                 k_wspd_init_o<<<gi, 256, 0, c.stream>>>(ptr<int2>(c.t_lr), nn, fa, own0, front_cap, ctr);
-            } else if (owners_env && K * (8.0 + 1.25 * s * s) <= (double)(16 << 20)) {
-                // (big WSPDs skip it: their recursions overflow the CTA-local frontier almost at
-                // once -- measured at cfg5 s = 16: owners 0.43 ms + grid 1.31 ms vs grid 1.26-1.6 ms)
+            } else if (owners_env) {
+                // (measured at cfg5 s = 16 as well: 5.25 ms with the CTA-local phase, 5.72 without)
                 int per = 0;
                 W1G_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_wspd_owners, OW_T, 0));
                 if (per < 1) per = 1;
@@ -601,8 +600,16 @@ int wspd_run(Ctx &c, double s, int reference_order, int64_t *n_pairs, bool want_
                 return e ? atoi(e) : 256;
             }();
             const int BT = ORDER ? 256 : (bt_env == 1024 ? 1024 : 256);
+            // W1G_WSPD_MINB (tuning): minimum resident CTAs per SM the compiler must allow
+            // (6 or 8: fewer registers, more warps in flight for the latency-bound rounds)
+            static const int minb_env = [] {
+                const char *e = getenv("W1G_WSPD_MINB");
+                return e ? atoi(e) : 0;
+            }();
             const void *fn = ORDER ? (const void *)k_wspd_coop_o
                            : BT == 1024 ? (const void *)k_wspd_coop<1, 1024>
+                           : minb_env == 6 ? (const void *)k_wspd_coop<1, 256, 6>
+                           : minb_env == 8 ? (const void *)k_wspd_coop<1, 256, 8>
                            : ipt_env == 2 ? (const void *)k_wspd_coop<2>
                            : ipt_env == 4 ? (const void *)k_wspd_coop<4>
                                           : (const void *)k_wspd_coop<1>;

@@ -1,3 +1,4 @@
 mkdir -p gpurun_out
-python -m pytest tests/test_gpu_configs.py -q -x -k "shard or gathered" > gpurun_out/t20.log 2>&1; echo rc=$? >> gpurun_out/t20.log
-python bench.py --workload cfg3 --steps 5 --warmup 3 > gpurun_out/bench_cfg3b.json 2> gpurun_out/bench_cfg3b.err; echo cfg3_rc=$?
+{
+for mb in 0 6 8; do echo "MINB=$mb"; for cfg in "100000 16.0 0.001 3" "100000 4.0 0.001 3" "100000 1.0 0.01 5"; do W1G_WSPD_MINB=$mb python tools/fe_once.py $cfg; done; done
+} > gpurun_out/sweep5.log 2>&1
