@@ -402,13 +402,21 @@ static int batch_start(Ctx &c, const int32_t *pairs, int64_t n_pairs, const Batc
         return W1G_ESTATE;
     }
     W1G_TRY(ensure_kids(c, b, streams));
-    // several concurrent front ends: the level loops instead of the cooperative kernels
-    // (measured at cfg2 with 4 child contexts: 1546 vs 1411 pairs/s; W1G_BATCH_COOP=1 keeps them)
-    static const bool batch_coop = [] {
+    // several concurrent front ends: the cooperative kernels of the split tree and the WSPD
+    // on a 1/streams share of the device each, so the children's grids are co-resident
+    // (measured, 4 child contexts: cfg2 1706 pairs/s with shares, 1624 with the multi-kernel
+    // level loops, 1496 with full grids; 20k points 3265 / 2508 / 2748).
+    // W1G_BATCH_COOP=full: full grids; =off: the level loops.
+    static const int batch_coop = [] {
         const char *e = getenv("W1G_BATCH_COOP");
-        return e && *e == '1';
+        if (!e) return 0;
+        return !strcmp(e, "full") ? 1 : !strcmp(e, "off") ? 2 : 0;
     }();
-    for (w1g_ctx *x : b.kids) x->no_coop = (streams > 1 && !batch_coop) ? 1 : 0;
+    for (w1g_ctx *x : b.kids) {
+        const bool several = streams > 1;
+        x->no_coop = (several && batch_coop == 2) ? 1 : 0;
+        x->coop_share = (several && batch_coop == 0) ? streams : 1;
+    }
     if (!c.h_corpus_ptr) W1G_CUDA(cudaStreamSynchronize(c.stream));  // the corpus upload is complete
     b.pairs.assign(pairs, pairs + 2 * n_pairs);
     b.n_pairs = n_pairs;

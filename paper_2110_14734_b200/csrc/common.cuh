@@ -166,6 +166,9 @@ struct Ctx {
     // split tree and the WSPD: set on the batch executor's child contexts when several run
     // concurrently (a cooperative grid must be co-resident, which throttles the others)
     int no_coop = 0;
+    // the cooperative kernels' grid as a share of the device's resident CTAs (1 = all):
+    // concurrent child contexts each take 1/share, so their grids stay co-resident
+    int coop_share = 1;
     cudaEvent_t prof_ev[2][2][2] = {};
     DevBuf prof_cnt;  // 4 x unsigned long long
     int heavy_ratio = 16;  // exact pass: disc / median disc beyond which a source is searched alone (W1G_HEAVY, 0 off)
@@ -196,6 +199,10 @@ struct Ctx {
     int64_t n_pairs = 0;
     int32_t wspd_levels = 0;
     DevBuf pair_uv;    // int2 (u, v) tree node ids
+    // depth-first WSPD: the work pool's per-chunk ready flags (all zero between runs)
+    // and its counters, one 128-byte line each
+    DevBuf wspd_ready, wspd_ctr;
+    int32_t wspd_epoch = 0;
     DevBuf pair_w;     // int32 owner internal node of each level-0 recursion item (reference order)
     DevBuf pair_idx;   // int64 (P,2) representative point indices
     DevBuf pair_counts;

@@ -959,7 +959,7 @@ int tree_run(Ctx &c, const double2 *pts, int64_t n, int64_t *n_nodes, int32_t *d
             const int cap = e ? atoi(e) : 2;
             if (per_sm > cap) per_sm = cap;
         }
-        const int G = per_sm * c.sm_count;
+        const int G = max(1, per_sm * c.sm_count / max(1, c.coop_share));
         void *args[] = {&A};
         W1G_CUDA(cudaLaunchCooperativeKernel((void *)k_tree_coop, G, 256, args, smem, c.stream));
         W1G_CHECK_LAUNCH();

@@ -51,7 +51,7 @@ struct Counters {
 // shard / n_shards: only the recursions of internal nodes w with w % n_shards == shard
 // (the owner loop of spanner.py:206-241 split over GPUs)
 __global__ void k_wspd_init_f(const int2 *lr, int64_t nn, ItemF *items, int64_t cap, int64_t *cnt, int shard,
-                              int n_shards) {
+                              int n_shards, int64_t *cnt2 = nullptr) {
     const int lane = threadIdx.x & 31;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t base = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) & ~31ll; base < nn; base += stride) {
@@ -61,7 +61,10 @@ __global__ void k_wspd_init_f(const int2 *lr, int64_t nn, ItemF *items, int64_t 
         const unsigned m = __ballot_sync(0xffffffffu, need);
         if (!m) continue;
         int64_t b = 0;
-        if (lane == 0) b = (int64_t)atomicAdd((unsigned long long *)cnt, (unsigned long long)__popc(m));
+        if (lane == 0) {
+            b = (int64_t)atomicAdd((unsigned long long *)cnt, (unsigned long long)__popc(m));
+            if (cnt2) atomicAdd((unsigned long long *)cnt2, (unsigned long long)__popc(m));
+        }
         b = __shfl_sync(0xffffffffu, b, 0);
         if (need) {
             int64_t slot = b + __popc(m & lanemask_lt());
@@ -386,6 +389,246 @@ __global__ void __launch_bounds__(OW_T) k_wspd_owners(const int2 *__restrict__ l
     if (tid == 0) atomicMax(max_depth, depth_max);
 }
 
+// Fused order, depth-first: every warp runs recursions on its own stack in
+// shared memory -- pop the top 32 items, one lane each: one round of geometry
+// loads, the predicate, pairs into a per-warp buffer (flushed with one global
+// atomic per ~DF_PB pairs), the split items' two children pushed back -- with no
+// CTA or grid barrier, so a step costs one dependent load instead of a level's
+// barrier, load chain and counter atomic.
+// Work moves between warps through a global queue of 32-item chunks: the owners'
+// root items (left[w], right[w]) are its first chunks; a warp whose stack would
+// overflow, or that sees waiting warps, appends the BOTTOM of its stack (the
+// oldest, biggest sub-recursions).  A warp out of work takes a ticket (one
+// atomicAdd, no retry storm) and waits on that chunk's own ready flag (set after
+// its items, cleared by its consumer, so all flags are zero between runs).
+// Termination: `pending` = busy warps + appended-but-unconsumed chunks; it only
+// reaches 0 once nothing is left anywhere, and then stays 0, so a waiting warp
+// leaves when it reads 0.  Warps that start late or never start do not matter
+// (no co-residency needed).  The emitted pair SET is the reference's (the
+// recursions are independent and each runs exactly); their order is not (the
+// fused front end builds the CSR, a function of the set).
+constexpr int DF_W = 8;        // warps per CTA
+constexpr int DF_S = 512;      // per-warp stack ring, items
+constexpr int DF_PB = 128;     // per-warp pair buffer
+constexpr int DF_POLL = 8;     // steps between donation checks
+// counters, one 128-byte line each
+constexpr int DL_PUSH = 0 * 16;     // chunks appended after the owners'
+constexpr int DL_TICKET = 1 * 16;   // tickets taken
+constexpr int DL_PENDING = 2 * 16;  // pending - owner chunks (signed)
+constexpr int DL_PAIRS = 3 * 16;    // pairs
+constexpr int DL_OWNERS = 5 * 16;   // owner items (the init kernel's count)
+constexpr int DL_N = 6 * 16;
+__device__ __forceinline__ int64_t vld64(const int64_t *p) { return *(volatile const int64_t *)p; }
+__device__ __forceinline__ int32_t ld_relaxed(const int32_t *p) {
+    int32_t v;
+    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed(int32_t *p, int32_t v) {
+    asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+struct DfPool {
+    ItemF *items;      // [0, n0): the owners' items; appended chunk k at (o_chunks + k) * 32
+    int32_t *ready;    // per appended chunk: 2 epoch = its items are written, 2 epoch + 1 = the end
+    int64_t cap_items; // capacity of items
+    int64_t *ctr;
+    int64_t *flags;
+    int32_t epoch;     // this run's (flags of earlier runs never match: no clearing)
+};
+
+// append stack ring positions [b, b + m) (m a multiple of 32) to the queue
+__device__ __forceinline__ void df_push(const ItemF *st, int b, int m, const DfPool &P, int64_t o_chunks) {
+    const int lane = threadIdx.x & 31;
+    const int nch = m >> 5;
+    int64_t k0 = 0;
+    if (lane == 0) {
+        atomicAdd((unsigned long long *)&P.ctr[DL_PENDING], (unsigned long long)nch);  // before any is ready
+        k0 = (int64_t)atomicAdd((unsigned long long *)&P.ctr[DL_PUSH], (unsigned long long)nch);
+    }
+    k0 = __shfl_sync(0xffffffffu, k0, 0);
+    const int64_t cap_chunks = P.cap_items / 32 - o_chunks;
+    for (int j = 0; j < nch; j++) {
+        const int64_t k = k0 + j;
+        if (k < cap_chunks) P.items[(o_chunks + k) * 32 + lane] = st[(b + 32 * j + lane) & (DF_S - 1)];
+    }
+    __threadfence();
+    __syncwarp();
+    for (int j = lane; j < nch; j += 32) {
+        const int64_t k = k0 + j;
+        if (k < cap_chunks) st_relaxed(&P.ready[k], 2 * P.epoch);
+        else atomicOr((unsigned long long *)&P.flags[F_FRONT_OVF], 1ull);
+    }
+    __syncwarp();
+}
+
+__device__ __forceinline__ void df_flush(int2 *pb, int &pbn, const DfPool &P, int2 *__restrict__ out_uv,
+                                         int64_t pair_cap) {
+    const int lane = threadIdx.x & 31;
+    if (pbn == 0) return;
+    int64_t base = 0;
+    if (lane == 0) base = (int64_t)atomicAdd((unsigned long long *)&P.ctr[DL_PAIRS], (unsigned long long)pbn);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    for (int i = lane; i < pbn; i += 32) {
+        const int64_t slot = base + i;
+        if (slot < pair_cap) out_uv[slot] = pb[i];
+        else if (slot == pair_cap) atomicOr((unsigned long long *)&P.flags[F_PAIR_OVF], 1ull);
+    }
+    pbn = 0;
+    __syncwarp();
+}
+
+__global__ void __launch_bounds__(DF_W * 32) k_wspd_dfs(const int2 *__restrict__ lr, const NodeGeom *__restrict__ geom,
+                                                        double s, const __grid_constant__ DfPool P,
+                                                        int2 *__restrict__ out_uv, int64_t pair_cap) {
+    __shared__ ItemF stk[DF_W][DF_S];
+    __shared__ int2 pbs[DF_W][DF_PB];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const unsigned lt = lanemask_lt();
+    ItemF *st = stk[wid];
+    int2 *pb = pbs[wid];
+    const int64_t n0 = P.ctr[DL_OWNERS];
+    const int64_t o_chunks = (n0 + 31) >> 5;
+    const int64_t cap_chunks = P.cap_items / 32 - o_chunks;
+    int top = 0, bot = 0, pbn = 0, step = 0;
+    while (true) {
+        if (top == bot) {
+            // out of work: take a ticket and wait for that chunk (or for the end)
+            top = bot = 0;
+            int64_t t = 0;
+            if (lane == 0) t = (int64_t)atomicAdd((unsigned long long *)&P.ctr[DL_TICKET], 1ull);
+            t = __shfl_sync(0xffffffffu, t, 0);
+            ItemF it{-1, -1};
+            bool got = true;
+            if (t < o_chunks) {
+                const int64_t g = t * 32 + lane;
+                if (g < n0) it = P.items[g];  // written by the init kernel
+            } else {
+                const int64_t k = t - o_chunks;
+                int state = 0;  // 1: ready, 2: dropped (overflow), 3: the end
+                if (lane == 0) {
+                    unsigned backoff = 32;
+                    for (int poll = 0;; poll++) {
+                        if (k < cap_chunks) {
+                            const int32_t v = ld_relaxed(&P.ready[k]);
+                            if (v == 2 * P.epoch) {
+                                state = 1;
+                                break;
+                            }
+                            if (v == 2 * P.epoch + 1) {  // the finishing warp's broadcast
+                                state = 3;
+                                break;
+                            }
+                        } else if (vld64(&P.ctr[DL_PUSH]) > k) {
+                            state = 2;
+                            break;
+                        }
+                        // (tickets taken after the broadcast see the end here)
+                        if ((poll & 7) == 7 && o_chunks + vld64(&P.ctr[DL_PENDING]) == 0) {
+                            state = 3;
+                            break;
+                        }
+                        __nanosleep(backoff);
+                        backoff = backoff < 1024 ? backoff * 2 : 1024;
+                    }
+                }
+                state = __shfl_sync(0xffffffffu, state, 0);
+                if (state == 3) {
+                    got = false;
+                } else if (state == 1) {
+                    __threadfence();
+                    const ItemF *src = &P.items[(o_chunks + k) * 32 + lane];
+                    it = ItemF{__ldcg(&src->u), __ldcg(&src->v)};  // through L2: never a stale L1 line
+                }
+            }
+            if (!got) break;
+            st[lane] = it;
+            top = 32;
+            __syncwarp();
+            continue;
+        }
+        // one step: the top min(32, size) items, one lane each
+        const int size = top - bot;
+        const int n = size < 32 ? size : 32;
+        const bool valid = lane < n;
+        ItemF it{-1, -1};
+        if (valid) it = st[(top - 1 - lane) & (DF_S - 1)];
+        __syncwarp();
+        top -= n;
+        const bool live = valid && it.u >= 0;
+        bool ws = false;
+        int2 c0 = make_int2(0, 0), c1 = make_int2(0, 0);
+        if (live) {
+            // every field of both nodes in one round of loads (the split side's dsq
+            // would otherwise be fetched only after the predicate: a second round trip)
+            const double2 *gp = reinterpret_cast<const double2 *>(geom);
+            const double2 u0 = __ldg(gp + 2 * (int64_t)it.u), u1 = __ldg(gp + 2 * (int64_t)it.u + 1);
+            const double2 v0 = __ldg(gp + 2 * (int64_t)it.v), v1 = __ldg(gp + 2 * (int64_t)it.v + 1);
+            const int2 lu = __ldg(lr + it.u), lv = __ldg(lr + it.v);
+            const NodeGeom gu{u0.x, u0.y, u1.x, u1.y}, gv{v0.x, v0.y, v1.x, v1.y};
+            const bool split_u = gu.dsq > gv.dsq;  // spanner.py:226-235
+            ws = ws_predicate(gu, gv, s);
+            c0 = split_u ? make_int2(lu.x, it.v) : make_int2(it.u, lv.x);
+            c1 = split_u ? make_int2(lu.y, it.v) : make_int2(it.u, lv.y);
+        }
+        const unsigned mp = __ballot_sync(0xffffffffu, live && ws);
+        const unsigned ms = __ballot_sync(0xffffffffu, live && !ws);
+        // pairs into the warp's buffer (flushed first if it could overflow)
+        if (pbn + 32 > DF_PB) df_flush(pb, pbn, P, out_uv, pair_cap);
+        if (live && ws) pb[pbn + __popc(mp & lt)] = make_int2(it.u, it.v);
+        pbn += __popc(mp);
+        // children: make room at the bottom first (the oldest items go to the queue)
+        const int nc = 2 * __popc(ms);
+        if (top - bot + nc > DF_S) {
+            const int m = ((top - bot + nc - DF_S + 31) & ~31);
+            df_push(st, bot, m, P, o_chunks);
+            bot += m;
+        }
+        if (live && !ws) {
+            const int pos = top + 2 * __popc(ms & lt);
+            st[pos & (DF_S - 1)] = ItemF{c0.x, c0.y};
+            st[(pos + 1) & (DF_S - 1)] = ItemF{c1.x, c1.y};
+        }
+        top += nc;
+        __syncwarp();
+        if (top == bot) {
+            // this warp's work is done: its pairs leave, then its busy unit
+            df_flush(pb, pbn, P, out_uv, pair_cap);
+            __threadfence();
+            int64_t left = 1;
+            if (lane == 0)
+                left = o_chunks - 1 +
+                       (int64_t)atomicAdd((unsigned long long *)&P.ctr[DL_PENDING], (unsigned long long)-1ll);
+            left = __shfl_sync(0xffffffffu, left, 0);
+            if (left == 0) {
+                // the last work anywhere: wake every waiting ticket with the end mark
+                const int64_t k0 = vld64(&P.ctr[DL_PUSH]);
+                int64_t k1 = vld64(&P.ctr[DL_TICKET]) - o_chunks;
+                if (k1 > cap_chunks) k1 = cap_chunks;
+                for (int64_t k = k0 + lane; k < k1; k += 32) st_relaxed(&P.ready[k], 2 * P.epoch + 1);
+            }
+            continue;
+        }
+        // share with waiting warps: up to half of the stack's bottom
+        if (++step % DF_POLL == 0 && top - bot >= 64) {
+            int give = 0;
+            if (lane == 0) {
+                const int64_t waiting = vld64(&P.ctr[DL_TICKET]) - (o_chunks + vld64(&P.ctr[DL_PUSH]));
+                if (waiting > 0) {
+                    const int64_t most = 32 * waiting;
+                    give = ((top - bot) / 2) & ~31;
+                    if (give > most) give = (int)most;
+                }
+            }
+            give = __shfl_sync(0xffffffffu, give, 0);
+            if (give) {
+                df_push(st, bot, give, P, o_chunks);
+                bot += give;
+            }
+        }
+    }
+}
+
 // reference order: the levels are appended to one array (level l occupies
 // [starts[l], starts[l+1])), so the whole recursion forest stays for the
 // ordering passes; `cap` is the array's capacity, max_levels starts' capacity
@@ -551,6 +794,65 @@ int wspd_run(Ctx &c, double s, int reference_order, int64_t *n_pairs, bool want_
         W1G_CUDA(cudaMemsetAsync(ctr, 0, sizeof(int64_t) * 8, c.stream));
         Counters k{ctr, ctr + 4, dflags(c)};
         const unsigned gi = grid_for(nn, 256, 8u * c.sm_count);
+        // fused order: the depth-first warp kernel (W1G_WSPD_DFS=0: the level-synchronous
+        // phases below)
+        static const bool dfs_env = [] {
+            const char *e = getenv("W1G_WSPD_DFS");
+            return !(e && *e == '0');
+        }();
+        if (!ORDER && dfs_env) {
+            int64_t P = 0;
+            bool ovf = false;
+            if (nn > 1) {
+                DfPool pool;
+                pool.items = fa;
+                pool.cap_items = front_cap;
+                pool.flags = dflags(c);
+                const size_t ready_n = (size_t)(front_cap / 32 + 2);
+                const void *was = c.wspd_ready.p;
+                const size_t was_cap = c.wspd_ready.cap;
+                W1G_TRY(ensure(c.wspd_ready, ready_n, &pool.ready));
+                // the flags carry the run's epoch: cleared only when the buffer is new or the
+                // epochs wrap
+                if (c.wspd_ready.p != was || c.wspd_ready.cap != was_cap || c.wspd_epoch >= (1 << 29)) {
+                    W1G_CUDA(cudaMemsetAsync(pool.ready, 0, c.wspd_ready.cap, c.stream));
+                    c.wspd_epoch = 0;
+                }
+                pool.epoch = ++c.wspd_epoch;
+                W1G_TRY(ensure(c.wspd_ctr, DL_N, &pool.ctr));
+                W1G_CUDA(cudaMemsetAsync(pool.ctr, 0, sizeof(int64_t) * DL_N, c.stream));
+                k_wspd_init_f<<<gi, 256, 0, c.stream>>>(ptr<int2>(c.t_lr), nn, fa, front_cap, pool.ctr + DL_OWNERS,
+                                                        shard, n_shards);
+                W1G_CHECK_LAUNCH();
+                int per = 0;
+                W1G_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_wspd_dfs, DF_W * 32, 0));
+                if (per < 1) per = 1;
+                const int G = max(1, per * c.sm_count / max(1, c.coop_share));
+                k_wspd_dfs<<<G, DF_W * 32, 0, c.stream>>>(ptr<int2>(c.t_lr), ptr<NodeGeom>(c.t_geom), s, pool, uv,
+                                                          pair_cap);
+                W1G_CHECK_LAUNCH();
+                W1G_TRY(to_host_small(c, c.h_pinned + F_MISC0, pool.ctr + DL_PAIRS, sizeof(int64_t)));
+                W1G_TRY(to_host_small(c, c.h_pinned + F_PAIR_OVF, dflags(c) + F_PAIR_OVF, sizeof(int64_t) * 5));
+                W1G_TRY(stream_sync(c));
+                P = c.h_pinned[F_MISC0];
+                if (c.h_pinned[F_FRONT_OVF]) {
+                    ovf = true;
+                    front_cap *= 2;
+                }
+            }
+            if (P > pair_cap) {
+                ovf = true;
+                pair_cap = P + P / 8 + 1024;
+            }
+            if (ovf) continue;
+            c.wspd_levels = 0;  // no levels: depth-first
+            c.n_pairs = P;
+            *n_pairs = P;
+            c.pairs_valid = true;
+            c.pairs_have_nodes = true;
+            c.pair_idx_valid = false;
+            return want_idx ? wspd_pair_idx(c) : W1G_OK;
+        }
         // fused order: the owners' recursions CTA-locally first (no grid barriers), the
         // spilled remainder by the cooperative frontier below (W1G_WSPD_OWNERS=0: the
         // frontier alone, every recursion seeded at level 0)
@@ -631,7 +933,7 @@ int wspd_run(Ctx &c, double s, int reference_order, int64_t *n_pairs, bool want_
                 return e && *e == '1';
             }();
             if (per_sm >= 1 && !((no_coop || c.no_coop) && !ORDER)) {
-                const int G = per_sm * c.sm_count;
+                const int G = max(1, per_sm * c.sm_count / max(1, c.coop_share));
                 int32_t *lv = reinterpret_cast<int32_t *>(ctr + 6);
                 NodeGeom *geom = ptr<NodeGeom>(c.t_geom);
                 int2 *lr = ptr<int2>(c.t_lr);
