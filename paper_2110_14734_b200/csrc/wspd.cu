@@ -424,6 +424,9 @@ __device__ __forceinline__ int32_t ld_relaxed(const int32_t *p) {
     asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+__device__ __forceinline__ void st_release(int32_t *p, int32_t v) {
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ void st_relaxed(int32_t *p, int32_t v) {
     asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -452,11 +455,10 @@ __device__ __forceinline__ void df_push(const ItemF *st, int b, int m, const DfP
         const int64_t k = k0 + j;
         if (k < cap_chunks) P.items[(o_chunks + k) * 32 + lane] = st[(b + 32 * j + lane) & (DF_S - 1)];
     }
-    __threadfence();
-    __syncwarp();
+    __syncwarp();  // orders the warp's item writes before the release stores below
     for (int j = lane; j < nch; j += 32) {
         const int64_t k = k0 + j;
-        if (k < cap_chunks) st_relaxed(&P.ready[k], 2 * P.epoch);
+        if (k < cap_chunks) st_release(&P.ready[k], 2 * P.epoch);
         else atomicOr((unsigned long long *)&P.flags[F_FRONT_OVF], 1ull);
     }
     __syncwarp();
@@ -506,6 +508,7 @@ __global__ void __launch_bounds__(DF_W * 32) k_wspd_dfs(const int2 *__restrict__
             } else {
                 const int64_t k = t - o_chunks;
                 int state = 0;  // 1: ready, 2: dropped (overflow), 3: the end
+                int zero_dep = 0;  // 0, computed from the ready flag's value
                 if (lane == 0) {
                     unsigned backoff = 32;
                     for (int poll = 0;; poll++) {
@@ -513,6 +516,7 @@ __global__ void __launch_bounds__(DF_W * 32) k_wspd_dfs(const int2 *__restrict__
                             const int32_t v = ld_relaxed(&P.ready[k]);
                             if (v == 2 * P.epoch) {
                                 state = 1;
+                                zero_dep = v - 2 * P.epoch;
                                 break;
                             }
                             if (v == 2 * P.epoch + 1) {  // the finishing warp's broadcast
@@ -533,12 +537,15 @@ __global__ void __launch_bounds__(DF_W * 32) k_wspd_dfs(const int2 *__restrict__
                     }
                 }
                 state = __shfl_sync(0xffffffffu, state, 0);
+                zero_dep = __shfl_sync(0xffffffffu, zero_dep, 0);
                 if (state == 3) {
                     got = false;
                 } else if (state == 1) {
-                    __threadfence();
-                    const ItemF *src = &P.items[(o_chunks + k) * 32 + lane];
-                    it = ItemF{__ldcg(&src->u), __ldcg(&src->v)};  // through L2: never a stale L1 line
+                    // the items' addresses depend on the flag value lane 0 read (an
+                    // acquire load would invalidate the SM's L1 -- the geometry cache --
+                    // on every poll); read through L2: never a stale L1 line
+                    const ItemF *src = &P.items[(o_chunks + k) * 32 + lane + zero_dep];
+                    it = ItemF{__ldcg(&src->u), __ldcg(&src->v)};
                 }
             }
             if (!got) break;
@@ -547,35 +554,30 @@ __global__ void __launch_bounds__(DF_W * 32) k_wspd_dfs(const int2 *__restrict__
             __syncwarp();
             continue;
         }
-        // one step: the top min(32, size) items, one lane each
+        // one step: the top min(32, size) items, one lane each; uniform control flow
+        // (lanes without an item evaluate node 0 against itself and are masked out)
         const int size = top - bot;
         const int n = size < 32 ? size : 32;
         const bool valid = lane < n;
-        ItemF it{-1, -1};
-        if (valid) it = st[(top - 1 - lane) & (DF_S - 1)];
+        const ItemF it = st[(top - 1 - (valid ? lane : 0)) & (DF_S - 1)];
         __syncwarp();
         top -= n;
         const bool live = valid && it.u >= 0;
-        bool ws = false;
-        int2 c0 = make_int2(0, 0), c1 = make_int2(0, 0);
-        if (live) {
-            // every field of both nodes in one round of loads (the split side's dsq
-            // would otherwise be fetched only after the predicate: a second round trip)
-            const double2 *gp = reinterpret_cast<const double2 *>(geom);
-            const double2 u0 = __ldg(gp + 2 * (int64_t)it.u), u1 = __ldg(gp + 2 * (int64_t)it.u + 1);
-            const double2 v0 = __ldg(gp + 2 * (int64_t)it.v), v1 = __ldg(gp + 2 * (int64_t)it.v + 1);
-            const int2 lu = __ldg(lr + it.u), lv = __ldg(lr + it.v);
-            const NodeGeom gu{u0.x, u0.y, u1.x, u1.y}, gv{v0.x, v0.y, v1.x, v1.y};
-            const bool split_u = gu.dsq > gv.dsq;  // spanner.py:226-235
-            ws = ws_predicate(gu, gv, s);
-            c0 = split_u ? make_int2(lu.x, it.v) : make_int2(it.u, lv.x);
-            c1 = split_u ? make_int2(lu.y, it.v) : make_int2(it.u, lv.y);
-        }
-        const unsigned mp = __ballot_sync(0xffffffffu, live && ws);
-        const unsigned ms = __ballot_sync(0xffffffffu, live && !ws);
+        const int u = live ? it.u : 0, v = live ? it.v : 0;
+        // every field of both nodes in one round of loads (the split side's dsq would
+        // otherwise be fetched only after the predicate: a second round trip)
+        const double2 *gp = reinterpret_cast<const double2 *>(geom);
+        const double2 u0 = __ldg(gp + 2 * u), u1 = __ldg(gp + 2 * u + 1);
+        const double2 v0 = __ldg(gp + 2 * v), v1 = __ldg(gp + 2 * v + 1);
+        const int2 lu = __ldg(lr + u), lv = __ldg(lr + v);
+        const bool ok = ws_predicate(NodeGeom{u0.x, u0.y, u1.x, u1.y}, NodeGeom{v0.x, v0.y, v1.x, v1.y}, s);
+        const bool split_u = u1.y > v1.y;  // dsq: spanner.py:226-235
+        const bool ws = live && ok, sp = live && !ok;
+        const unsigned mp = __ballot_sync(0xffffffffu, ws);
+        const unsigned ms = __ballot_sync(0xffffffffu, sp);
         // pairs into the warp's buffer (flushed first if it could overflow)
         if (pbn + 32 > DF_PB) df_flush(pb, pbn, P, out_uv, pair_cap);
-        if (live && ws) pb[pbn + __popc(mp & lt)] = make_int2(it.u, it.v);
+        if (ws) pb[pbn + __popc(mp & lt)] = make_int2(u, v);
         pbn += __popc(mp);
         // children: make room at the bottom first (the oldest items go to the queue)
         const int nc = 2 * __popc(ms);
@@ -584,17 +586,16 @@ __global__ void __launch_bounds__(DF_W * 32) k_wspd_dfs(const int2 *__restrict__
             df_push(st, bot, m, P, o_chunks);
             bot += m;
         }
-        if (live && !ws) {
+        if (sp) {
             const int pos = top + 2 * __popc(ms & lt);
-            st[pos & (DF_S - 1)] = ItemF{c0.x, c0.y};
-            st[(pos + 1) & (DF_S - 1)] = ItemF{c1.x, c1.y};
+            st[pos & (DF_S - 1)] = split_u ? ItemF{lu.x, v} : ItemF{u, lv.x};
+            st[(pos + 1) & (DF_S - 1)] = split_u ? ItemF{lu.y, v} : ItemF{u, lv.y};
         }
         top += nc;
         __syncwarp();
         if (top == bot) {
             // this warp's work is done: its pairs leave, then its busy unit
             df_flush(pb, pbn, P, out_uv, pair_cap);
-            __threadfence();
             int64_t left = 1;
             if (lane == 0)
                 left = o_chunks - 1 +

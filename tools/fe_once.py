@@ -18,9 +18,13 @@ p = w1g.ApproxParams(s=s, best_effort=True, delta=delta)
 ctx = _lib.context()
 _front_end(ctx, a, b, p)  # warm
 c0 = _lib.launch_count()
+tot = []
 for _ in range(reps):
     info = _front_end(ctx, a, b, p)
+    tot.append(float(info.stage_ms[7]))
 c1 = _lib.launch_count()
-print(f"n={n} s={s} delta={delta}: launches per front end {(c1 - c0) // reps}, device ms {info.stage_ms[7]:.3f}, "
+tot.sort()
+print(f"n={n} s={s} delta={delta}: launches per front end {(c1 - c0) // reps}, device ms {info.stage_ms[7]:.3f} "
+      f"(min {tot[0]:.3f}, median {tot[len(tot) // 2]:.3f} of {reps}), "
       f"K={info.n_points} P={info.n_pairs} M={info.n_arcs} wspd_levels={info.n_levels_wspd}")
 print({nm: round(float(info.stage_ms[i]), 4) for i, nm in enumerate(_lib.STAGES)})
