@@ -22,7 +22,10 @@ __device__ __forceinline__ double hypot_kernel(double ax, double ay) {
         t1 = dmul(dmul(2.0, delta), dsub(ax, dmul(2.0, ay)));
         t2 = dadd(dmul(dsub(dmul(4.0, delta), ay), ay), dmul(delta, delta));
     }
-    return dsub(h, ddiv(dadd(t1, t2), dmul(2.0, h)));
+    // an exact h (t1 + t2 == +-0: h - (+-0) / 2h is h) skips the division -- and its slow
+    // path, which a zero quotient takes (lattice points give exact distances often)
+    const double num = dadd(t1, t2);
+    return num == 0.0 ? h : dsub(h, ddiv(num, dmul(2.0, h)));
 }
 
 __device__ __forceinline__ double glibc_hypot(double x, double y) {

@@ -710,6 +710,14 @@ __global__ void k_sp_tails(const int64_t *__restrict__ ro, int64_t K, int64_t *o
 }
 
 // sorted element i of row r: key = head << 32 | original position in the row
+__device__ __forceinline__ void sp_put_head_a(const SpRows &R, const double2 a, int64_t q, uint32_t h) {
+    // the tails are written by k_sp_tails; a = the row's own point
+    const double2 b = R.pts[h];
+    const double cc = glibc_hypot(dsub(a.x, b.x), dsub(a.y, b.y));  // spanner.py:324
+    if (!isfinite(cc)) atomicOr((unsigned long long *)&R.f[F_NET_ERR], 4ull);
+    R.oh[q] = (int64_t)h;
+    R.oc[q] = cc;
+}
 __device__ __forceinline__ void sp_put_head(const SpRows &R, int64_t r, int64_t q, uint32_t h) {
     // the tails are written by k_sp_tails
     const double2 a = R.pts[r], b = R.pts[h];
@@ -758,7 +766,8 @@ struct DiagArgs {
 // arcs (network.py:88-93, spanner.py:326-335): i -> abar last in an A-member
 // row, bbar -> i at the member's place in the bbar row
 __global__ void k_sp_short_rows(const __grid_constant__ SpRows R, int64_t K, int32_t *lists, int32_t *n_list,
-                                unsigned long_max, unsigned big_max, const __grid_constant__ DiagArgs D) {
+                                unsigned long_max, unsigned med_max, unsigned big_max,
+                                const __grid_constant__ DiagArgs D) {
     const int lane = threadIdx.x & 31, gl = lane & 15;
     const int64_t groups = ((int64_t)gridDim.x * blockDim.x) >> 4;
     const int64_t nr = (K + 1) & ~1ll;  // both halves of a warp iterate together
@@ -798,7 +807,7 @@ __global__ void k_sp_short_rows(const __grid_constant__ SpRows R, int64_t K, int
                     if (l > long_max) {
                         atomicOr((unsigned long long *)&R.f[F_OVERFLOW], 1ull);
                     } else {
-                        const int cl = l <= 32 ? CL_W32 : l <= 256 ? CL_MED : l <= big_max ? SP_CL_BIG : CL_LONG;
+                        const int cl = l <= 32 ? CL_W32 : l <= med_max ? CL_MED : l <= big_max ? SP_CL_BIG : CL_LONG;
                         lists[(int64_t)cl * K + atomicAdd(&n_list[cl], 1)] = (int32_t)r;
                     }
                 }
@@ -872,10 +881,116 @@ __global__ void __launch_bounds__(CSR_MB) k_sp_med_rows(const __grid_constant__ 
     if (__any_sync(0xffffffffu, dup) && lane == 0) atomicOr((unsigned long long *)&R.f[F_NET_ERR], SP_DUP_BIT);
 }
 
+// long rows, windowed: a CTA per row, ranks from a bitmap of the row's head span
+// only (its heads are the representatives of the WSPD partners of its point's
+// nodes -- spatially near it, so in the lexicographic point order their span is
+// small: cfg5 s = 16, rows of 513..1024 arcs span ~460 32-bit words, of 1025+ arcs
+// ~1070, of K/32 = 6200).  The row's span (a block min / max), its bits, a block
+// scan of the span's word popcounts, then each head's rank = the popcounts before
+// its word + the bits below it in its word.  The window is small, so many CTAs fit
+// per SM.  A repeated head is flagged; rows whose span exceeds the window go to
+// `ovf` (the full-K kernel below).
+constexpr int WB_T = 256;       // threads per row
+constexpr int WB_WORDS = 2048;  // window, 32-bit words (65536 head values)
+constexpr int WB_SORTED = 4096; // rows up to this length are written coalesced from shared memory
+__global__ void __launch_bounds__(WB_T) k_sp_win_bitmap(const __grid_constant__ SpRows R, const int32_t *rows,
+                                                        const int32_t *n_rows, int32_t *ovf, int32_t *n_ovf) {
+    __shared__ uint32_t bm[WB_WORDS], pre[WB_WORDS];
+    __shared__ uint32_t sorted[WB_SORTED];
+    __shared__ uint32_t s_warp[WB_T / 32];
+    __shared__ unsigned s_lo[2], s_hi[2];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    for (int w = tid; w < WB_WORDS; w += WB_T) bm[w] = 0;
+    const int nr = *n_rows;
+    unsigned dup = 0;
+    int it = 0;
+    for (int ri = blockIdx.x; ri < nr; ri += gridDim.x, it ^= 1) {
+        const int64_t r = rows[ri];
+        const int64_t s0 = R.ro[r];
+        const int len = (int)R.cnt[r];
+        const uint32_t *hs = R.sh + s0;
+        const double2 a = R.pts[r];
+        if (tid == 0) {
+            s_lo[it] = 0xffffffffu;
+            s_hi[it] = 0;
+        }
+        __syncthreads();  // the previous row's clear and writes; this row's range reset
+        unsigned lo = 0xffffffffu, hi = 0;
+        for (int i = tid; i < len; i += WB_T) {
+            const uint32_t h = hs[i];
+            lo = min(lo, h);
+            hi = max(hi, h);
+        }
+        lo = __reduce_min_sync(0xffffffffu, lo);
+        hi = __reduce_max_sync(0xffffffffu, hi);
+        if (lane == 0) {
+            atomicMin(&s_lo[it], lo);
+            atomicMax(&s_hi[it], hi);
+        }
+        __syncthreads();
+        const int wlo = (int)(s_lo[it] >> 5), span = (int)(s_hi[it] >> 5) - wlo + 1;
+        if (span > WB_WORDS) {  // (uniform) the full-K kernel takes it
+            if (tid == 0) ovf[atomicAdd(n_ovf, 1)] = (int32_t)r;
+            continue;
+        }
+        for (int i = tid; i < len; i += WB_T) {
+            const uint32_t h = hs[i];
+            const uint32_t bit = 1u << (h & 31);
+            if (atomicOr(&bm[(h >> 5) - wlo], bit) & bit) dup = 1;
+        }
+        __syncthreads();
+        const int per = (span + WB_T - 1) / WB_T;
+        const int w0 = tid * per, w1 = min(span, w0 + per);
+        uint32_t mine = 0;
+        for (int w = w0; w < w1; w++) mine += __popc(bm[w]);
+        uint32_t x = mine;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) s_warp[wid] = x;
+        __syncthreads();
+        uint32_t base = x - mine;
+#pragma unroll
+        for (int w = 0; w < WB_T / 32; w++)
+            if (w < wid) base += s_warp[w];
+        for (int w = w0; w < w1; w++) {
+            pre[w] = base;
+            base += __popc(bm[w]);
+        }
+        __syncthreads();
+        if (len <= WB_SORTED) {
+            // heads into their sorted places in shared memory, then the row is written
+            // in order: coalesced stores instead of one 32-byte sector per arc
+            for (int i = tid; i < len; i += WB_T) {
+                const uint32_t h = hs[i];
+                const int w = (int)(h >> 5) - wlo;
+                sorted[pre[w] + __popc(bm[w] & ((1u << (h & 31)) - 1u))] = h;
+            }
+            __syncthreads();
+            for (int i = tid; i < len; i += WB_T) sp_put_head_a(R, a, s0 + i, sorted[i]);
+        } else {
+            for (int i = tid; i < len; i += WB_T) {
+                const uint32_t h = hs[i];
+                const int w = (int)(h >> 5) - wlo;
+                sp_put_head_a(R, a, s0 + pre[w] + __popc(bm[w] & ((1u << (h & 31)) - 1u)), h);
+            }
+        }
+        __syncthreads();
+        for (int w = w0; w < w1; w++) bm[w] = 0;
+    }
+    if (__any_sync(0xffffffffu, dup) && lane == 0) atomicOr((unsigned long long *)&R.f[F_NET_ERR], SP_DUP_BIT);
+}
+
 // long rows by rank instead of comparison: heads are distinct within a row
 // and below K, so a row's heads mark a K-bit bitmap in shared memory; a block
 // scan of the per-word popcounts then gives every head its rank (its place in
-// the sorted row) directly.  O(len + K/32) per row, a CTA per row.  A head
+// the sorted row) directly.  Only the words between the row's smallest and
+// largest head are scanned and cleared: a row's heads are the representatives of
+// the WSPD partners of its point's nodes, spatially near it, so in the lexicographic
+// point order their span is a small part of K (cfg5 s = 16: rows of 513..1024
+// arcs span ~460 words of 6200).  O(len + span/32) per row, a CTA per row.  A head
 // already marked is a repeated (tail, head).
 constexpr int SP_BM_THREADS = 512;
 __global__ void __launch_bounds__(SP_BM_THREADS) k_sp_long_bitmap(const __grid_constant__ SpRows R,
@@ -885,8 +1000,8 @@ __global__ void __launch_bounds__(SP_BM_THREADS) k_sp_long_bitmap(const __grid_c
     const int W = (int)((K + 31) >> 5);
     uint32_t *pre = sbm + W;
     __shared__ uint32_t s_warp[SP_BM_THREADS / 32];
+    __shared__ unsigned s_lo, s_hi;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const int per = (W + SP_BM_THREADS - 1) / SP_BM_THREADS;  // words per thread in the scan
     for (int i = tid; i < W; i += SP_BM_THREADS) sbm[i] = 0;
     const int nr = *n_rows;
     unsigned dup = 0;
@@ -894,15 +1009,32 @@ __global__ void __launch_bounds__(SP_BM_THREADS) k_sp_long_bitmap(const __grid_c
         const int64_t r = rows[ri];
         const int64_t s0 = R.ro[r];
         const int len = (int)R.cnt[r];
-        __syncthreads();  // bitmap clear (previous row)
+        if (tid == 0) {
+            s_lo = 0xffffffffu;
+            s_hi = 0;
+        }
+        __syncthreads();  // bitmap clear (previous row), range reset
+        unsigned lo = 0xffffffffu, hi = 0;
         for (int i = tid; i < len; i += SP_BM_THREADS) {
             const uint32_t h = R.sh[s0 + i];
             const uint32_t bit = 1u << (h & 31);
             if (atomicOr(&sbm[h >> 5], bit) & bit) dup = 1;
+            lo = min(lo, h);
+            hi = max(hi, h);
+        }
+        lo = __reduce_min_sync(0xffffffffu, lo);
+        hi = __reduce_max_sync(0xffffffffu, hi);
+        if (lane == 0) {
+            atomicMin(&s_lo, lo);
+            atomicMax(&s_hi, hi);
         }
         __syncthreads();
-        // exclusive prefix of the word popcounts: a contiguous run of words per thread
-        const int w0 = tid * per, w1 = min(W, w0 + per);
+        // exclusive prefix of the word popcounts over the row's span: a contiguous
+        // run of words per thread
+        const int wlo = (int)(s_lo >> 5), whi = (int)(s_hi >> 5);
+        const int span = whi - wlo + 1;
+        const int per = (span + SP_BM_THREADS - 1) / SP_BM_THREADS;
+        const int w0 = wlo + tid * per, w1 = min(whi + 1, w0 + per);
         uint32_t mine = 0;
         for (int w = w0; w < w1; w++) mine += __popc(sbm[w]);
         uint32_t x = mine;
@@ -926,7 +1058,7 @@ __global__ void __launch_bounds__(SP_BM_THREADS) k_sp_long_bitmap(const __grid_c
             sp_put_head(R, r, s0 + rank, h);
         }
         __syncthreads();
-        for (int i = tid; i < len; i += SP_BM_THREADS) sbm[R.sh[s0 + i] >> 5] = 0;
+        for (int w = w0; w < w1; w++) sbm[w] = 0;
     }
     if (__any_sync(0xffffffffu, dup) && lane == 0) atomicOr((unsigned long long *)&R.f[F_NET_ERR], SP_DUP_BIT);
 }
@@ -1239,10 +1371,17 @@ int spanner_net_run(Ctx &c, int64_t *node_count, int64_t *n_arcs) {
     unsigned long_max = bitmap_fits ? 0xffffffffu : (unsigned)CSR_LONG_MAX;
     if (const char *lm = getenv("W1G_SP_LONG_MAX")) long_max = (unsigned)atoi(lm);
     if (!bitmap_fits && long_max > (unsigned)CSR_LONG_MAX) long_max = CSR_LONG_MAX;
-    // rows of 257..big_max: a warp in registers, longer: the bitmap ranks (W1G_SP_BIG_MAX: tuning)
-    unsigned big_max = SP_MED_MAX;
+    // rows of 257..big_max: a warp in registers, longer: the bitmap ranks (W1G_SP_BIG_MAX: tuning;
+    // since the windowed bitmap kernel the ranks are faster from 257 arcs: cfg5 s = 16
+    // delta = 0.001, 3.98 ms vs 4.29 with the register sorts up to 512)
+    unsigned big_max = 256;
     if (const char *bm = getenv("W1G_SP_BIG_MAX")) big_max = (unsigned)atoi(bm);
     if (big_max > (unsigned)SP_MED_MAX) big_max = SP_MED_MAX;
+    // rows of 33..med_max: a warp's register sort (W1G_SP_MED_MAX: tuning, <= 256)
+    unsigned med_max = 256;
+    if (const char *mm = getenv("W1G_SP_MED_MAX")) med_max = (unsigned)atoi(mm);
+    if (med_max > 256u) med_max = 256u;
+    if (med_max < 32u) med_max = 32u;
     SubTimer T(c, "spcsr");
     int64_t *sup, *ro, *ot, *oh;
     double *oc;
@@ -1258,8 +1397,8 @@ int spanner_net_run(Ctx &c, int64_t *node_count, int64_t *n_arcs) {
     unsigned *cursor = cnt + n + 2;
     // slots sit at their final CSR positions (the diagonal ones stay unused)
     W1G_TRY(ensure(c.scr[0], (size_t)M + 1, &sh));
-    W1G_TRY(ensure(c.scr[6], (size_t)4 * (K + 1), &lists));
-    int32_t *n_list = reinterpret_cast<int32_t *>(cnt + 2 * (n + 2));  // 4 int32 class counters
+    W1G_TRY(ensure(c.scr[6], (size_t)5 * (K + 1), &lists));
+    int32_t *n_list = reinterpret_cast<int32_t *>(cnt + 2 * (n + 2));  // 5 int32 class counters
     W1G_TRY(flags_reset(c));
     W1G_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned) * (2 * (n + 2) + 8), c.stream));
     const int2 *uv = ptr<int2>(c.pair_uv);
@@ -1302,7 +1441,7 @@ int spanner_net_run(Ctx &c, int64_t *node_count, int64_t *n_arcs) {
     const DiagArgs D{ptr<double2>(ns.pts), ptr<int64_t>(ns.am), ptr<int64_t>(ns.bm), ptr<int64_t>(ns.exb),
                      ns.abar, ns.bbar, sup};
     k_sp_short_rows<<<grid_for(K * 16, 256, 16u * c.sm_count), 256, 0, c.stream>>>(R, K, lists, n_list, long_max,
-                                                                                   big_max, D);
+                                                                                   med_max, big_max, D);
     W1G_CHECK_LAUNCH();
     k_sp_w32_rows<<<4 * c.sm_count, 256, 0, c.stream>>>(R, lists + CL_W32 * K, n_list + CL_W32);
     W1G_CHECK_LAUNCH();
@@ -1316,6 +1455,22 @@ int spanner_net_run(Ctx &c, int64_t *node_count, int64_t *n_arcs) {
         // long rows: bitmap ranks while a K-bit bitmap (+ prefixes) fits in shared memory;
         // as many CTAs per SM as the bitmap allows (a row's phases are latency-bound)
         if (bitmap_fits) {
+            const int32_t *cta_rows = lists + CL_LONG * K, *cta_n = n_list + CL_LONG;
+            static const bool win_bm = [] {  // W1G_SP_WIN_BITMAP=0: the full-K kernel for every long row
+                const char *e = getenv("W1G_SP_WIN_BITMAP");
+                return !(e && *e == '0');
+            }();
+            if (win_bm) {
+                // a CTA per row over its head span; rows with wider spans to the full-K kernel
+                int32_t *ovf = lists + 4 * K, *n_ovf = n_list + 4;
+                int per = 1;
+                W1G_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_sp_win_bitmap, WB_T, 0));
+                if (per < 1) per = 1;
+                k_sp_win_bitmap<<<per * c.sm_count, WB_T, 0, c.stream>>>(R, cta_rows, cta_n, ovf, n_ovf);
+                W1G_CHECK_LAUNCH();
+                cta_rows = ovf;
+                cta_n = n_ovf;
+            }
             if (bm_bytes > 48 * 1024)
                 W1G_CUDA(cudaFuncSetAttribute(k_sp_long_bitmap, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                               (int)bm_bytes));
@@ -1323,8 +1478,7 @@ int spanner_net_run(Ctx &c, int64_t *node_count, int64_t *n_arcs) {
             W1G_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sp_long_bitmap, SP_BM_THREADS,
                                                                    bm_bytes));
             if (per_sm < 1) per_sm = 1;
-            k_sp_long_bitmap<<<per_sm * c.sm_count, SP_BM_THREADS, bm_bytes, c.stream>>>(R, lists + CL_LONG * K,
-                                                                                          n_list + CL_LONG, K);
+            k_sp_long_bitmap<<<per_sm * c.sm_count, SP_BM_THREADS, bm_bytes, c.stream>>>(R, cta_rows, cta_n, K);
         } else {
             k_sp_long_rows<<<c.sm_count, CSR_LB, 0, c.stream>>>(R, lists + CL_LONG * K, n_list + CL_LONG);
         }
