@@ -80,18 +80,24 @@ struct HostPool {
         return W1G_OK;
     }
     void put(void *p) {
-        std::lock_guard<std::mutex> lk(mu);
-        auto it = cls_of.find(p);
-        if (it == cls_of.end()) return;
-        in_flight -= it->second;
-        auto &fl = free_blocks[it->second];
-        if (fl.size() < 16) {
-            fl.push_back(p);
-        } else {
-            cls_of.erase(it);
-            cudaFreeHost(p);
+        bool release = false;
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            auto it = cls_of.find(p);
+            if (it == cls_of.end()) return;
+            in_flight -= it->second;
+            auto &fl = free_blocks[it->second];
+            if (fl.size() < 64) {
+                fl.push_back(p);
+            } else {
+                cls_of.erase(it);
+                release = true;
+            }
         }
         cv.notify_all();
+        // outside the lock: cudaFreeHost waits for the device, which must not stall the
+        // workers' block requests
+        if (release) cudaFreeHost(p);
     }
     void wake() { cv.notify_all(); }
 };
@@ -155,6 +161,7 @@ struct BatchState {
     std::vector<cudaEvent_t> kid_ev;
     // W1G_BATCH_TRACE=1: per-worker host time in each phase (us), printed at the batch's end
     bool trace = false;
+    bool trace_steps = false;  // W1G_BATCH_TRACE=2: every worker step to stderr (debugging)
     std::vector<double> tr_block, tr_fe, tr_fetch, tr_pairs;
 };
 
@@ -308,6 +315,7 @@ static void batch_worker(Ctx *parent, BatchState *b, int w) {
         r.j = j;
         int rc = W1G_OK;
         const clk::time_point t1 = clk::now();
+        if (b->trace_steps) fprintf(stderr, "[w1g batch] w%d pair %lld: front end\n", w, (long long)p);
         if (parent->h_corpus_ptr) {
             // host-resident diagrams: this worker's H2D overlaps the other workers' front ends
             rc = w1g_front_end(x, parent->h_corpus_ptr[i], off[i + 1] - off[i], parent->h_corpus_ptr[j],
@@ -328,13 +336,16 @@ static void batch_worker(Ctx *parent, BatchState *b, int w) {
             const int64_t n = r.info.node_count, m = r.info.n_arcs;
             const int sl = next_slot;
             // the slot's previous network must have left before the slot is rewritten
+            if (b->trace_steps) fprintf(stderr, "[w1g batch] w%d pair %lld: slot %d\n", w, (long long)p, sl);
             while (!pending.empty() && pending.front().slot == sl) drain(true);
             void *blk = nullptr;
+            if (b->trace_steps) fprintf(stderr, "[w1g batch] w%d pair %lld: block\n", w, (long long)p);
             const clk::time_point tb = clk::now();
             rc = host_pool().get(carve_bytes(n, m), &blk, &b->cancel);
             t_block = us(tb, clk::now());
             if (rc == W1G_OK) {
                 const NetCarve cv = carve(blk, n, m);
+                if (b->trace_steps) fprintf(stderr, "[w1g batch] w%d pair %lld: copy\n", w, (long long)p);
                 rc = d2h ? stage_copy(x, d2h, slots[sl], n, m, cv) : W1G_ECUDA;
                 if (rc == W1G_OK) {
                     r.supplies = cv.sup;
@@ -432,7 +443,8 @@ static int batch_start(Ctx &c, const int32_t *pairs, int64_t n_pairs, const Batc
     b.active = true;
     {
         const char *e = getenv("W1G_BATCH_TRACE");
-        b.trace = e && *e == '1';
+        b.trace = e && (*e == '1' || *e == '2');
+        b.trace_steps = e && *e == '2';
         b.tr_block.assign(b.kids.size(), 0.0);
         b.tr_fe.assign(b.kids.size(), 0.0);
         b.tr_fetch.assign(b.kids.size(), 0.0);

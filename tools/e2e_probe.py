@@ -2,7 +2,7 @@
 pageable vs page-locked inputs, several stream counts, with and without keeping
 the networks, against the device-only batch and the host link's D2H bound.
 
-    python tools/e2e_probe.py [PAIRS]
+    python tools/e2e_probe.py [PAIRS] [STREAMS,..] [DISTINCT]
 """
 import json
 import sys
@@ -15,12 +15,13 @@ import paper_2110_14734_b200 as w1g  # noqa: E402
 from paper_2110_14734_b200 import synth  # noqa: E402
 
 P = int(sys.argv[1]) if len(sys.argv) > 1 else 32
+D = int(sys.argv[3]) if len(sys.argv) > 3 else P  # distinct pairs (generating them dominates the run)
 diags = []
-for p in range(P):
+for p in range(D):
     a, b = synth.gaussian_cluster_pair(100_000, 100_000, seed=p)
     diags += [a, b]
 pinned = [w1g.pinned_points(d) for d in diags]
-pairs = [(2 * p, 2 * p + 1) for p in range(P)]
+pairs = [(2 * (p % D), 2 * (p % D) + 1) for p in range(P)]
 params = w1g.ApproxParams(s=1.0, best_effort=True, delta=0.01)
 
 
