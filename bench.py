@@ -519,7 +519,7 @@ def e2e_batch(w1g, diagrams, pairs, args, dist: Dist, reps: int) -> dict:
         times.append(time.perf_counter() - t0)
     dist.barrier()
     t = dist.max(statistics.mean(times))
-    return {"seconds": t, "h2d": int(h2d), "d2h": int(nbytes["d2h"])}
+    return {"seconds": t, "h2d": int(h2d), "d2h": int(nbytes["d2h"]), "reps_ms": [round(1e3 * x, 2) for x in times]}
 
 
 def e2e_single(w1g, a, b, args, device: int, flush, reps: int) -> dict:
@@ -704,7 +704,7 @@ def run_ours(args, dist: Dist):
         "config": cfg,
         "batch": batch_info,
         "e2e": {"value": total_pairs / e2e["seconds"], "unit": "pairs/s", "ms_per_step": 1e3 * e2e["seconds"],
-                "h2d_bytes_per_step": e2e["h2d"], "d2h_bytes_per_step": e2e["d2h"],
+                "h2d_bytes_per_step": e2e["h2d"], "d2h_bytes_per_step": e2e["d2h"], "reps_ms": e2e["reps_ms"],
                 "api": "paper_2110_14734_b200.sparsify_batch (host numpy diagrams -> host TransshipmentNetworks)"},
         "gpu_launches": int(launches),
         "clocks": clk,

@@ -41,6 +41,7 @@ struct HostPool {
     std::unordered_map<void *, size_t> cls_of;
     size_t in_flight = 0;
     size_t limit = (size_t)8 << 30;
+    int spare_blocks = 12;  // extra blocks pinned with the first block of a size class (<= limit / 8)
 
     static size_t size_class(size_t b) {
         size_t c = (size_t)1 << 20;
@@ -65,8 +66,19 @@ struct HostPool {
             return W1G_OK;
         }
         lk.unlock();
+        // a new size class: a few spare blocks at once, so the batches that follow do not
+        // pin memory (tens of ms per block) in the middle of their timed work
         void *p = nullptr;
         const cudaError_t e = cudaHostAlloc(&p, cls, cudaHostAllocPortable);
+        std::vector<void *> spare;
+        for (int q = 0; e == cudaSuccess && q < spare_blocks && (size_t)(q + 1) * cls <= limit / 8; q++) {
+            void *x = nullptr;
+            if (cudaHostAlloc(&x, cls, cudaHostAllocPortable) != cudaSuccess) {
+                cudaGetLastError();
+                break;
+            }
+            spare.push_back(x);
+        }
         lk.lock();
         if (e != cudaSuccess) {
             cudaGetLastError();
@@ -76,6 +88,10 @@ struct HostPool {
             return W1G_ENOMEM;
         }
         cls_of[p] = cls;
+        for (void *x : spare) {
+            cls_of[x] = cls;
+            free_blocks[cls].push_back(x);
+        }
         *out = p;
         return W1G_OK;
     }

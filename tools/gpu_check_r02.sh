@@ -1,6 +1,6 @@
 mkdir -p gpurun_out
-W1G_D2H_CHUNK=0 W1G_BATCH_TRACE=2 timeout 200 python -X faulthandler -c "
-import faulthandler, sys; faulthandler.dump_traceback_later(150, exit=True)
-sys.argv=['e2e_probe.py','32','4,6','4']
-exec(open('tools/e2e_probe.py').read())
-" > gpurun_out/chunk_dbg2.log 2>&1; echo rc=$? >> gpurun_out/chunk_dbg2.log
+for st in 4 6 4 6; do python bench.py --steps 20 --warmup 5 --streams $st --no-extras > gpurun_out/bench_q$st.json 2> gpurun_out/bench_q$st.err; python -c "
+import json
+d=json.loads(open('gpurun_out/bench_q$st.json').read().strip().splitlines()[-1])
+print($st, 'value',round(d['value']),'e2e',round(d['e2e']['value']), d['e2e']['reps_ms'])
+"; done > gpurun_out/bench_q.log 2>&1
