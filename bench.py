@@ -497,13 +497,18 @@ def north_star_kernel(ctx, w1g, n: int) -> dict:
 def e2e_batch(w1g, diagrams, pairs, args, dist: Dist, reps: int) -> dict:
     """sparsify_batch with host numpy in and host networks out, max over ranks."""
     params = w1g.ApproxParams(s=args.s, best_effort=True, delta=args.delta, k=K_LATTICE)
-    nbytes = {"d2h": 0}
+    nbytes = {"d2h": 0, "net": 0}
     lock = threading.Lock()
+    # the batch executor's compact transfer (batch.cu) does not copy the tails (rebuilt on the
+    # host from the row offsets) and copies the heads as int32: the bytes that cross the link
+    compact = os.environ.get("W1G_BATCH_COMPACT", "1") != "0"
 
     def keep(i, j, net, d):
         with lock:
-            nbytes["d2h"] += sum(getattr(net, f).nbytes for f in ("supplies", "tails", "heads", "costs",
+            nbytes["net"] += sum(getattr(net, f).nbytes for f in ("supplies", "tails", "heads", "costs",
                                                                   "row_offsets"))
+            nbytes["d2h"] += sum(getattr(net, f).nbytes for f in ("supplies", "costs", "row_offsets")) + (
+                net.heads.nbytes // 2 if compact else net.heads.nbytes + net.tails.nbytes)
 
     used = sorted({i for p in pairs for i in p})
     h2d = sum(diagrams[i].nbytes for i in used)
@@ -512,14 +517,15 @@ def e2e_batch(w1g, diagrams, pairs, args, dist: Dist, reps: int) -> dict:
     dist.barrier()
     times = []
     for _ in range(reps):
-        nbytes["d2h"] = 0
+        nbytes["d2h"] = nbytes["net"] = 0
         t0 = time.perf_counter()
         w1g.sparsify_batch(diagrams, params, pairs=pairs, devices=[dist.local], streams_per_device=args.streams,
                            on_network=keep)
         times.append(time.perf_counter() - t0)
     dist.barrier()
     t = dist.max(statistics.mean(times))
-    return {"seconds": t, "h2d": int(h2d), "d2h": int(nbytes["d2h"]), "reps_ms": [round(1e3 * x, 2) for x in times]}
+    return {"seconds": t, "h2d": int(h2d), "d2h": int(nbytes["d2h"]), "net_bytes": int(nbytes["net"]),
+            "compact": compact, "reps_ms": [round(1e3 * x, 2) for x in times]}
 
 
 def e2e_single(w1g, a, b, args, device: int, flush, reps: int) -> dict:
@@ -705,6 +711,9 @@ def run_ours(args, dist: Dist):
         "batch": batch_info,
         "e2e": {"value": total_pairs / e2e["seconds"], "unit": "pairs/s", "ms_per_step": 1e3 * e2e["seconds"],
                 "h2d_bytes_per_step": e2e["h2d"], "d2h_bytes_per_step": e2e["d2h"], "reps_ms": e2e["reps_ms"],
+                "network_bytes_per_step": e2e["net_bytes"],
+                "transfer": ("compact: tails rebuilt on the host from the row offsets, heads as int32 widened on the "
+                             "host (batch.cu expanders)") if e2e["compact"] else "every network array copied",
                 "api": "paper_2110_14734_b200.sparsify_batch (host numpy diagrams -> host TransshipmentNetworks)"},
         "gpu_launches": int(launches),
         "clocks": clk,
