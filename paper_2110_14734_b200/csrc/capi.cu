@@ -102,6 +102,26 @@ int to_host_small(Ctx &c, void *h_dst, const void *d_src, size_t bytes, cudaStre
     return W1G_OK;
 }
 
+namespace {
+__global__ void k_to_host2(const uint32_t *__restrict__ s0, volatile uint32_t *d0, int n0,
+                           const uint32_t *__restrict__ s1, volatile uint32_t *d1, int n1) {
+    for (int i = threadIdx.x; i < n0; i += blockDim.x) d0[i] = s0[i];
+    for (int i = threadIdx.x; i < n1; i += blockDim.x) d1[i] = s1[i];
+}
+}  // namespace
+
+// two small reads in one launch
+int to_host_small2(Ctx &c, void *h0, const void *d0, size_t b0, void *h1, const void *d1, size_t b1) {
+    const int n0 = (int)(b0 / 4), n1 = (int)(b1 / 4);
+    const int n = n0 > n1 ? n0 : n1;
+    if (n <= 0) return W1G_OK;
+    k_to_host2<<<1, n < 256 ? ((n + 31) & ~31) : 256, 0, c.stream>>>(
+        static_cast<const uint32_t *>(d0), static_cast<volatile uint32_t *>(h0), n0,
+        static_cast<const uint32_t *>(d1), static_cast<volatile uint32_t *>(h1), n1);
+    W1G_CHECK_LAUNCH();
+    return W1G_OK;
+}
+
 int flags_fetch(Ctx &c, int first, int count) {
     W1G_TRY(to_host_small(c, c.h_pinned + first, dflags(c) + first, sizeof(int64_t) * count));
     W1G_TRY(stream_sync(c));

@@ -310,6 +310,7 @@ enum FlagSlot {
 // batch executor's workers), stalling this context's host round trip.  h_dst must be
 // page-locked (h_pinned slots, pool blocks); bytes a multiple of 4.
 int to_host_small(Ctx &c, void *h_dst, const void *d_src, size_t bytes, cudaStream_t s = nullptr);
+int to_host_small2(Ctx &c, void *h0, const void *d0, size_t b0, void *h1, const void *d1, size_t b1);
 // h_pinned slots for scalar results read back by the stages (RWMD sums)
 enum { H_SCALAR = 48 };  // 8 slots: 48..55
 int flags_reset(Ctx &c);

@@ -438,8 +438,9 @@ int zc_run(Ctx &c, const double2 *d_a, int64_t na, const double2 *d_b, int64_t n
     W1G_CHECK_LAUNCH();
     k_zc_stats<<<grid_for(n, 256, 2u * c.sm_count), 256, 0, c.stream>>>(am, bm, pts, dflags(c) + F_K0, dflags(c));
     W1G_CHECK_LAUNCH();
-    W1G_TRY(to_host_small(c, c.h_pinned + F_ZSTAT, dflags(c) + F_ZSTAT, sizeof(int64_t) * 6));
-    W1G_TRY(flags_fetch(c, F_K0, 2));
+    W1G_TRY(to_host_small2(c, c.h_pinned + F_ZSTAT, dflags(c) + F_ZSTAT, sizeof(int64_t) * 6, c.h_pinned + F_K0,
+                           dflags(c) + F_K0, sizeof(int64_t) * 2));
+    W1G_TRY(stream_sync(c));
     if (speculative && lex2_speculation_failed(c, 1)) return zc_run(c, d_a, na, d_b, nb, k0, balanced, false);
     ns.k = c.h_pinned[F_K0];
     *k0 = ns.k;
@@ -642,12 +643,17 @@ int dc_run(Ctx &c, double delta, double pitch, double half_width, uint64_t seed,
         k_cl_check<<<grid_for(k, 256, 2u * c.sm_count), 256, 0, c.stream>>>(pts, dK, xl, yl, dflags(c));
         W1G_CHECK_LAUNCH();
         T.mark("check");
-        W1G_TRY(to_host_small(c, c.h_pinned + F_LISTS, dflags(c) + F_LISTS, sizeof(int64_t)));
     }
     // node positions per side for emit_arcs, over k >= K (the masses past K are 0),
     // so their totals come back with K in the same round trip
     if (!members_done) W1G_TRY(member_scans(c, dst, k));
-    W1G_TRY(flags_fetch(c, F_TOTAL, F_MISC1 - F_TOTAL + 1));
+    if (lists) {
+        W1G_TRY(to_host_small2(c, c.h_pinned + F_LISTS, dflags(c) + F_LISTS, sizeof(int64_t), c.h_pinned + F_TOTAL,
+                               dflags(c) + F_TOTAL, sizeof(int64_t) * (F_MISC1 - F_TOTAL + 1)));
+        W1G_TRY(stream_sync(c));
+    } else {
+        W1G_TRY(flags_fetch(c, F_TOTAL, F_MISC1 - F_TOTAL + 1));
+    }
     dst.k = c.h_pinned[F_TOTAL];
     dst.na = c.h_pinned[F_MISC0];
     dst.nb = c.h_pinned[F_MISC1];

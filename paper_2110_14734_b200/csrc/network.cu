@@ -1448,8 +1448,10 @@ int spanner_net_run(Ctx &c, int64_t *node_count, int64_t *n_arcs) {
     k_sp_med_rows<0><<<8 * c.sm_count, CSR_MB, 0, c.stream>>>(R, lists + CL_MED * K, n_list + CL_MED);
     W1G_CHECK_LAUNCH();
     T.mark("short_med");
-    k_sp_med_rows<1><<<4 * c.sm_count, CSR_MB, 0, c.stream>>>(R, lists + SP_CL_BIG * K, n_list + SP_CL_BIG);
-    W1G_CHECK_LAUNCH();
+    if (big_max > med_max) {  // (rows of med_max+1..big_max; none by default)
+        k_sp_med_rows<1><<<4 * c.sm_count, CSR_MB, 0, c.stream>>>(R, lists + SP_CL_BIG * K, n_list + SP_CL_BIG);
+        W1G_CHECK_LAUNCH();
+    }
     T.mark("big");
     {
         // long rows: bitmap ranks while a K-bit bitmap (+ prefixes) fits in shared memory;

@@ -904,6 +904,7 @@ int tree_run(Ctx &c, const double2 *pts, int64_t n, int64_t *n_nodes, int32_t *d
     W1G_TRY(flags_reset(c));
     W1G_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * 16, c.stream));
     int levels = 0;
+    const int32_t *depth_src = nullptr;  // the cooperative kernel's level count (device)
     const int64_t ntiles = (n + TP_TILE - 1) / TP_TILE;
     static const bool no_coop = [] {  // W1G_NO_COOP=1: the multi-kernel level loop (measurement)
         const char *e = getenv("W1G_NO_COOP");
@@ -964,7 +965,7 @@ int tree_run(Ctx &c, const double2 *pts, int64_t n, int64_t *n_nodes, int32_t *d
         W1G_CUDA(cudaLaunchCooperativeKernel((void *)k_tree_coop, G, 256, args, smem, c.stream));
         W1G_CHECK_LAUNCH();
         // the depth is read after the stage's (or, deferred, the caller's) next round trip
-        W1G_TRY(to_host_small(c, c.h_pinned + H_TREE_DEPTH, lv, sizeof(int32_t)));
+        depth_src = lv;
         levels = -1;
     } else if (n > LOCAL_MAX) {
         // fallback for very large inputs: one launch per phase, host polls per batch
@@ -1006,7 +1007,12 @@ int tree_run(Ctx &c, const double2 *pts, int64_t n, int64_t *n_nodes, int32_t *d
     }
     T.mark("local");
     if (levels >= 0) c.h_pinned[H_TREE_DEPTH] = levels;  // host-known (multi-kernel path / no global levels)
-    W1G_TRY(to_host_small(c, c.h_pinned + H_TREE_DUP, dflags(c) + F_DUP, sizeof(int64_t)));
+    if (depth_src) {
+        W1G_TRY(to_host_small2(c, c.h_pinned + H_TREE_DEPTH, depth_src, sizeof(int32_t), c.h_pinned + H_TREE_DUP,
+                               dflags(c) + F_DUP, sizeof(int64_t)));
+    } else {
+        W1G_TRY(to_host_small(c, c.h_pinned + H_TREE_DUP, dflags(c) + F_DUP, sizeof(int64_t)));
+    }
     W1G_CUDA(cudaEventRecord(c.ev[10], c.stream));  // the two copies above have landed once this has
     c.tree_valid = true;
     if (defer) {

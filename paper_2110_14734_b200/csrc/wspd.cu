@@ -832,8 +832,8 @@ int wspd_run(Ctx &c, double s, int reference_order, int64_t *n_pairs, bool want_
                 k_wspd_dfs<<<G, DF_W * 32, 0, c.stream>>>(ptr<int2>(c.t_lr), ptr<NodeGeom>(c.t_geom), s, pool, uv,
                                                           pair_cap);
                 W1G_CHECK_LAUNCH();
-                W1G_TRY(to_host_small(c, c.h_pinned + F_MISC0, pool.ctr + DL_PAIRS, sizeof(int64_t)));
-                W1G_TRY(to_host_small(c, c.h_pinned + F_PAIR_OVF, dflags(c) + F_PAIR_OVF, sizeof(int64_t) * 5));
+                W1G_TRY(to_host_small2(c, c.h_pinned + F_MISC0, pool.ctr + DL_PAIRS, sizeof(int64_t),
+                                       c.h_pinned + F_PAIR_OVF, dflags(c) + F_PAIR_OVF, sizeof(int64_t) * 5));
                 W1G_TRY(stream_sync(c));
                 P = c.h_pinned[F_MISC0];
                 if (c.h_pinned[F_FRONT_OVF]) {
