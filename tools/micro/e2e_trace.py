@@ -18,17 +18,21 @@ for p in range(D):
     diags += [a, b]
 pairs = [(2 * (p % D), 2 * (p % D) + 1) for p in range(P)]
 params = w1g.ApproxParams(s=1.0, best_effort=True, delta=0.01)
+import numpy as np  # noqa: E402
+
 for name, ds in (("pageable", diags), ("pinned", [w1g.pinned_points(d) for d in diags])):
     for rep in range(3):
+        st = []
         t = time.perf_counter()
-        w1g.sparsify_batch(ds, params, pairs=pairs, streams_per_device=4, on_network=lambda i, j, n, d: None)
+        w1g.sparsify_batch(ds, params, pairs=pairs, streams_per_device=4,
+                           on_network=lambda i, j, n, d: st.append(d.stage_ms))
         print(name, rep, round(1e3 * (time.perf_counter() - t), 2), "ms", file=sys.stderr, flush=True)
+    # per-stage device time (events on the front end's stream), median over the last batch
+    print(name, "stage ms", {k: round(float(np.median([x[k] for x in st])), 3) for k in st[0]}, file=sys.stderr)
 
 # the same front ends without delivering the networks: host inputs (each worker uploads
 # its pair), networks left on the device -- the input side alone
 import ctypes  # noqa: E402
-
-import numpy as np  # noqa: E402
 
 from paper_2110_14734_b200 import _lib  # noqa: E402
 
@@ -46,3 +50,5 @@ for name, ds in (("pageable", diags), ("pinned", [w1g.pinned_points(d) for d in 
                                                ctypes.c_uint64(0), 4, infos, ctypes.byref(ms)))
         print("no-delivery", name, rep, round(1e3 * (time.perf_counter() - t), 2), "ms wall,", round(ms.value, 2),
               "ms device", file=sys.stderr, flush=True)
+    print("no-delivery", name, "stage ms", {nm: round(float(np.median([infos[q].stage_ms[i] for q in range(P)])), 3)
+                                            for i, nm in enumerate(_lib.STAGES)}, file=sys.stderr)
