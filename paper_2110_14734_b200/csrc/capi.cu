@@ -35,10 +35,12 @@ int cuda_fail(cudaError_t e, const char *what, const char *file, int line) {
 // device's memory pool, so a first call at a new size does not stall the device
 // on cudaFree's implicit synchronisation
 static thread_local cudaStream_t g_tl_stream = nullptr;
+static thread_local bool g_tl_capturing = false;
 void set_thread_stream(cudaStream_t s) { g_tl_stream = s; }
 
 int ensure_bytes(DevBuf &b, size_t bytes) {
     if (bytes <= b.cap) return W1G_OK;
+    if (g_tl_capturing) return W1G_ERECAPTURE;  // graph_segment re-runs the body eagerly
     size_t want = bytes + bytes / 4 + 4096;
     cudaStream_t st = g_tl_stream;
     if (b.p) {
@@ -119,6 +121,55 @@ int to_host_small2(Ctx &c, void *h0, const void *d0, size_t b0, void *h1, const 
         static_cast<const uint32_t *>(d0), static_cast<volatile uint32_t *>(h0), n0,
         static_cast<const uint32_t *>(d1), static_cast<volatile uint32_t *>(h1), n1);
     W1G_CHECK_LAUNCH();
+    return W1G_OK;
+}
+
+int graph_segment(Ctx &c, int slot, const std::function<int()> &body) {
+    static const bool on = [] {  // opt-in: measured no better (measured and rejected)
+        const char *e = getenv("W1G_GRAPHS");
+        return e && *e == '1';
+    }();
+    if (!on || c.timing || c.gseg_off[slot] || g_tl_capturing) return body();
+    if (cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+        cudaGetLastError();
+        c.gseg_off[slot] = 1;
+        return body();
+    }
+    g_tl_capturing = true;
+    const int rc = body();
+    g_tl_capturing = false;
+    cudaGraph_t g = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(c.stream, &g);
+    if (rc != W1G_OK || e != cudaSuccess || !g) {
+        if (g) cudaGraphDestroy(g);
+        cudaGetLastError();
+        // a buffer had to grow (next time it will not), or capture rejected an operation
+        if (rc != W1G_ERECAPTURE) c.gseg_off[slot] = 1;
+        return body();
+    }
+    cudaGraphExec_t &x = c.gseg[slot];
+    bool ok = false;
+    if (x) {
+        cudaGraphExecUpdateResultInfo info;
+        ok = cudaGraphExecUpdate(x, g, &info) == cudaSuccess;
+        if (!ok) {
+            cudaGetLastError();
+            cudaGraphExecDestroy(x);
+            x = nullptr;
+        }
+    }
+    if (!ok) {
+        const cudaError_t ei = cudaGraphInstantiate(&x, g, 0);
+        if (ei != cudaSuccess) {
+            cudaGetLastError();
+            x = nullptr;
+            cudaGraphDestroy(g);
+            c.gseg_off[slot] = 1;
+            return body();
+        }
+    }
+    cudaGraphDestroy(g);
+    W1G_CUDA(cudaGraphLaunch(x, c.stream));
     return W1G_OK;
 }
 
@@ -326,6 +377,13 @@ int w1g_ctx_destroy(w1g_ctx *c) {
                       &c->net_c, &c->net_ro, &c->scan_state, &c->scan_state2, &c->flags, &c->pre_xl, &c->pre_yl,
                       &c->pre_cells, &c->pre_rows, &c->pre_rcnt};
     for (DevBuf *b : bufs) free_buf(*b);
+    free_buf(c->wspd_ready);
+    free_buf(c->wspd_ctr);
+    for (auto &x : c->gseg)
+        if (x) {
+            cudaGraphExecDestroy(x);
+            x = nullptr;
+        }
     for (NodeSet *ns_p : {&c->nodes[0], &c->nodes[1], &c->raw}) {
         NodeSet &ns = *ns_p;
         free_buf(ns.pts);

@@ -272,6 +272,10 @@ struct Ctx {
 
     // host round-trip accounting (stream_sync)
     int timing = 0;
+    // launch sequences between host round trips replayed as CUDA graphs (graph_segment):
+    // one executable graph per segment, updated in place for each call's parameters
+    cudaGraphExec_t gseg[8] = {};
+    int gseg_off[8] = {};  // the segment could not be captured: eager launches
     int64_t n_syncs = 0;
     double sync_gap_us = 0.0;
     cudaEvent_t sync_ev[2] = {};
@@ -311,6 +315,16 @@ enum FlagSlot {
 // page-locked (h_pinned slots, pool blocks); bytes a multiple of 4.
 int to_host_small(Ctx &c, void *h_dst, const void *d_src, size_t bytes, cudaStream_t s = nullptr);
 int to_host_small2(Ctx &c, void *h0, const void *d0, size_t b0, void *h1, const void *d1, size_t b1);
+// Run `body` (launches on c.stream, no host synchronisation) captured as a CUDA graph and
+// replayed with one graph launch: the device fetches one command instead of one per
+// kernel (launches are slow to submit while the host link is busy with network copies:
+// 87 small kernels 375 -> 862 us, as one graph 84 -> 107 us).  Buffers that must grow,
+// or an operation capture rejects, fall back to running `body` eagerly.  Opt-in
+// (W1G_GRAPHS=1): capturing and updating cost the host as much as the launches, and the
+// end-to-end batch did not gain (measured and rejected).
+enum { GSEG_ZC = 0, GSEG_DC = 1, GSEG_TREE_WSPD = 2, GSEG_CSR = 3 };
+constexpr int W1G_ERECAPTURE = -100;  // internal: ensure() would allocate during a capture
+int graph_segment(Ctx &c, int slot, const std::function<int()> &body);
 // h_pinned slots for scalar results read back by the stages (RWMD sums)
 enum { H_SCALAR = 48 };  // 8 slots: 48..55
 int flags_reset(Ctx &c);

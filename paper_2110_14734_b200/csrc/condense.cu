@@ -559,101 +559,106 @@ int dc_run(Ctx &c, double delta, double pitch, double half_width, uint64_t seed,
     const uint64_t sx = (uint64_t)(mxx - mnx), sy = (uint64_t)(mxy - mny);
     const int bx = sx ? 64 - __builtin_clzll(sx) : 0, by = sy ? 64 - __builtin_clzll(sy) : 0;
     const int packed = (bx + by) <= 64;
-    k_dc_keys<<<gs(c, k), 256, 0, c.stream>>>(cells, k, packed, mnx, mny, by, k0, k1, vals);
-    W1G_CHECK_LAUNCH();
-    uint64_t *keys[2] = {k0, k1};
-    W1G_TRY(radix_sort(c, keys, packed ? 1 : 2, vals, k, packed ? (bx + by > 0 ? bx + by : 1) : 64));
-    DcFlag f{cells, vals};
-    W1G_TRY(scan_i64(c, f, k, excl, dflags(c) + F_TOTAL));
-    double2 *pts;
-    int64_t *am, *bm;
-    W1G_TRY(ensure(dst.pts, k, &pts));
-    W1G_TRY(ensure(dst.am, k, &am));
-    W1G_TRY(ensure(dst.bm, k, &bm));
-    W1G_CUDA(cudaMemsetAsync(am, 0, sizeof(int64_t) * k, c.stream));
-    W1G_CUDA(cudaMemsetAsync(bm, 0, sizeof(int64_t) * k, c.stream));
-    // base = splitmix64(seed & 0xFFFF_FFFF_FFFF_FFFF), condensation.py:96 (host, same arithmetic)
-    uint64_t x = seed + 0x9E3779B97F4A7C15ull;
-    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
-    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
-    const uint64_t base = x ^ (x >> 31);
-    // the split tree's X- / Y-lists from the cell order (k_cl_columns), while the
-    // row range allows a counting sort (W1G_DC_LISTS=0: the tree sorts itself)
-    const bool lists_env = [] {  // read per call (tests toggle it)
-        const char *e = getenv("W1G_DC_LISTS");
-        return !(e && *e == '0');
-    }();
-    const int64_t R = (int64_t)(mxy - mny) + 1;
-    const bool lists = lists_env && k >= 2 && R > 0 && R <= 4 * k + 1024;
-    longlong2 *ncell = nullptr;
-    unsigned *rcnt = nullptr;
-    bool members_done = false;
-    if (lists) {
-        W1G_TRY(ensure(c.pre_cells, (size_t)k, &ncell));
-        W1G_TRY(ensure(c.pre_rcnt, (size_t)2 * (R + 2), &rcnt));
-        W1G_CUDA(cudaMemsetAsync(rcnt, 0, sizeof(unsigned) * 2 * (R + 2), c.stream));
-    }
-    k_dc_emit<<<gs(c, k), 256, 0, c.stream>>>(f, k, excl, ptr<int64_t>(src.am), ptr<int64_t>(src.bm),
-                                              pitch, half_width, base, pts, am, bm, ncell, mny, rcnt);
-    W1G_CHECK_LAUNCH();
-    if (lists) {
-        SubTimer T(c, "dc_lists");
-        uint32_t *xl, *yl, *rows;
-        int64_t *rstart;
-        W1G_TRY(ensure(c.pre_xl, (size_t)k, &xl));
-        W1G_TRY(ensure(c.pre_yl, (size_t)k, &yl));
-        W1G_TRY(ensure(c.pre_rows, (size_t)k, &rows));
-        W1G_TRY(ensure(c.scr[1], (size_t)R + 2, &rstart));  // the sort keys are dead by now
-        const int64_t *dK = dflags(c) + F_TOTAL;
-        const unsigned gk = grid_for(k, 256, 8u * c.sm_count);
-        // the columns (X-list) and the member scans on the side stream, concurrently with the
-        // rows' bucketing and sort; everything they use is allocated (on the main stream) first
-        cudaStream_t side = c.copy_stream ? c.copy_stream : c.stream;
-        int64_t *exa_, *exb_;
-        unsigned long long *st2;
-        W1G_TRY(ensure(dst.exa, (size_t)k + 1, &exa_));
-        W1G_TRY(ensure(dst.exb, (size_t)k + 1, &exb_));
-        W1G_TRY(ensure(c.scan_state2, (size_t)((k + SCAN_TILE - 1) / SCAN_TILE) + 16, &st2));
-        if (side != c.stream) {
-            W1G_CUDA(cudaEventRecord(c.ev[14], c.stream));
-            W1G_CUDA(cudaStreamWaitEvent(side, c.ev[14], 0));
+    // keys, sort, emit and the tree's lists: one graph (graph_segment) up to the round trip
+    bool lists = false;
+    W1G_TRY(graph_segment(c, GSEG_DC, [&]() -> int {
+        k_dc_keys<<<gs(c, k), 256, 0, c.stream>>>(cells, k, packed, mnx, mny, by, k0, k1, vals);
+        W1G_CHECK_LAUNCH();
+        uint64_t *keys[2] = {k0, k1};
+        W1G_TRY(radix_sort(c, keys, packed ? 1 : 2, vals, k, packed ? (bx + by > 0 ? bx + by : 1) : 64));
+        DcFlag f{cells, vals};
+        W1G_TRY(scan_i64(c, f, k, excl, dflags(c) + F_TOTAL));
+        double2 *pts;
+        int64_t *am, *bm;
+        W1G_TRY(ensure(dst.pts, k, &pts));
+        W1G_TRY(ensure(dst.am, k, &am));
+        W1G_TRY(ensure(dst.bm, k, &bm));
+        W1G_CUDA(cudaMemsetAsync(am, 0, sizeof(int64_t) * k, c.stream));
+        W1G_CUDA(cudaMemsetAsync(bm, 0, sizeof(int64_t) * k, c.stream));
+        // base = splitmix64(seed & 0xFFFF_FFFF_FFFF_FFFF), condensation.py:96 (host, same arithmetic)
+        uint64_t x = seed + 0x9E3779B97F4A7C15ull;
+        x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+        x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+        const uint64_t base = x ^ (x >> 31);
+        // the split tree's X- / Y-lists from the cell order (k_cl_columns), while the
+        // row range allows a counting sort (W1G_DC_LISTS=0: the tree sorts itself)
+        const bool lists_env = [] {  // read per call (tests toggle it)
+            const char *e = getenv("W1G_DC_LISTS");
+            return !(e && *e == '0');
+        }();
+        const int64_t R = (int64_t)(mxy - mny) + 1;
+        lists = lists_env && k >= 2 && R > 0 && R <= 4 * k + 1024;
+        longlong2 *ncell = nullptr;
+        unsigned *rcnt = nullptr;
+        bool members_done = false;
+        if (lists) {
+            W1G_TRY(ensure(c.pre_cells, (size_t)k, &ncell));
+            W1G_TRY(ensure(c.pre_rcnt, (size_t)2 * (R + 2), &rcnt));
+            W1G_CUDA(cudaMemsetAsync(rcnt, 0, sizeof(unsigned) * 2 * (R + 2), c.stream));
         }
-        k_cl_columns<<<gk, 256, 0, side>>>(ncell, pts, dK, xl, dflags(c));
+        k_dc_emit<<<gs(c, k), 256, 0, c.stream>>>(f, k, excl, ptr<int64_t>(src.am), ptr<int64_t>(src.bm),
+                                                  pitch, half_width, base, pts, am, bm, ncell, mny, rcnt);
         W1G_CHECK_LAUNCH();
-        if (side != c.stream) {
-            // member_scans on the side stream with its own scan state
-            std::swap(c.stream, side);
-            std::swap(c.scan_state, c.scan_state2);
-            const int rc = member_scans(c, dst, k);
-            std::swap(c.scan_state, c.scan_state2);
-            std::swap(c.stream, side);
-            W1G_TRY(rc);
-            members_done = true;
-            W1G_CUDA(cudaEventRecord(c.ev[15], side));
+        if (lists) {
+            SubTimer T(c, "dc_lists");
+            uint32_t *xl, *yl, *rows;
+            int64_t *rstart;
+            W1G_TRY(ensure(c.pre_xl, (size_t)k, &xl));
+            W1G_TRY(ensure(c.pre_yl, (size_t)k, &yl));
+            W1G_TRY(ensure(c.pre_rows, (size_t)k, &rows));
+            W1G_TRY(ensure(c.scr[1], (size_t)R + 2, &rstart));  // the sort keys are dead by now
+            const int64_t *dK = dflags(c) + F_TOTAL;
+            const unsigned gk = grid_for(k, 256, 8u * c.sm_count);
+            // the columns (X-list) and the member scans on the side stream, concurrently with the
+            // rows' bucketing and sort; everything they use is allocated (on the main stream) first
+            cudaStream_t side = c.copy_stream ? c.copy_stream : c.stream;
+            int64_t *exa_, *exb_;
+            unsigned long long *st2;
+            W1G_TRY(ensure(dst.exa, (size_t)k + 1, &exa_));
+            W1G_TRY(ensure(dst.exb, (size_t)k + 1, &exb_));
+            W1G_TRY(ensure(c.scan_state2, (size_t)((k + SCAN_TILE - 1) / SCAN_TILE) + 16, &st2));
+            if (side != c.stream) {
+                W1G_CUDA(cudaEventRecord(c.ev[14], c.stream));
+                W1G_CUDA(cudaStreamWaitEvent(side, c.ev[14], 0));
+            }
+            k_cl_columns<<<gk, 256, 0, side>>>(ncell, pts, dK, xl, dflags(c));
+            W1G_CHECK_LAUNCH();
+            if (side != c.stream) {
+                // member_scans on the side stream with its own scan state
+                std::swap(c.stream, side);
+                std::swap(c.scan_state, c.scan_state2);
+                const int rc = member_scans(c, dst, k);
+                std::swap(c.scan_state, c.scan_state2);
+                std::swap(c.stream, side);
+                W1G_TRY(rc);
+                members_done = true;
+                W1G_CUDA(cudaEventRecord(c.ev[15], side));
+            }
+            T.mark("columns");
+            W1G_TRY(scan_i64(c, RowCnt{rcnt, R}, R + 1, rstart, nullptr));
+            k_cl_rowscatter<<<gk, 256, 0, c.stream>>>(ncell, dK, mny, rstart, rcnt + R + 2, rows);
+            W1G_CHECK_LAUNCH();
+            T.mark("row_bucket");
+            k_cl_rows<<<grid_for(R * 32, 256, 8u * c.sm_count), 256, 0, c.stream>>>(pts, rows, rstart, R, yl, dflags(c));
+            W1G_CHECK_LAUNCH();
+            T.mark("rows");
+            if (side != c.stream) W1G_CUDA(cudaStreamWaitEvent(c.stream, c.ev[15], 0));
+            k_cl_check<<<grid_for(k, 256, 2u * c.sm_count), 256, 0, c.stream>>>(pts, dK, xl, yl, dflags(c));
+            W1G_CHECK_LAUNCH();
+            T.mark("check");
         }
-        T.mark("columns");
-        W1G_TRY(scan_i64(c, RowCnt{rcnt, R}, R + 1, rstart, nullptr));
-        k_cl_rowscatter<<<gk, 256, 0, c.stream>>>(ncell, dK, mny, rstart, rcnt + R + 2, rows);
-        W1G_CHECK_LAUNCH();
-        T.mark("row_bucket");
-        k_cl_rows<<<grid_for(R * 32, 256, 8u * c.sm_count), 256, 0, c.stream>>>(pts, rows, rstart, R, yl, dflags(c));
-        W1G_CHECK_LAUNCH();
-        T.mark("rows");
-        if (side != c.stream) W1G_CUDA(cudaStreamWaitEvent(c.stream, c.ev[15], 0));
-        k_cl_check<<<grid_for(k, 256, 2u * c.sm_count), 256, 0, c.stream>>>(pts, dK, xl, yl, dflags(c));
-        W1G_CHECK_LAUNCH();
-        T.mark("check");
-    }
-    // node positions per side for emit_arcs, over k >= K (the masses past K are 0),
-    // so their totals come back with K in the same round trip
-    if (!members_done) W1G_TRY(member_scans(c, dst, k));
-    if (lists) {
-        W1G_TRY(to_host_small2(c, c.h_pinned + F_LISTS, dflags(c) + F_LISTS, sizeof(int64_t), c.h_pinned + F_TOTAL,
-                               dflags(c) + F_TOTAL, sizeof(int64_t) * (F_MISC1 - F_TOTAL + 1)));
-        W1G_TRY(stream_sync(c));
-    } else {
-        W1G_TRY(flags_fetch(c, F_TOTAL, F_MISC1 - F_TOTAL + 1));
-    }
+        // node positions per side for emit_arcs, over k >= K (the masses past K are 0),
+        // so their totals come back with K in the same round trip
+        if (!members_done) W1G_TRY(member_scans(c, dst, k));
+        if (lists) {
+            W1G_TRY(to_host_small2(c, c.h_pinned + F_LISTS, dflags(c) + F_LISTS, sizeof(int64_t), c.h_pinned + F_TOTAL,
+                                   dflags(c) + F_TOTAL, sizeof(int64_t) * (F_MISC1 - F_TOTAL + 1)));
+        } else {
+            W1G_TRY(to_host_small(c, c.h_pinned + F_TOTAL, dflags(c) + F_TOTAL, sizeof(int64_t) * (F_MISC1 - F_TOTAL + 1)));
+        }
+        return W1G_OK;
+    }));
+    W1G_TRY(stream_sync(c));
     dst.k = c.h_pinned[F_TOTAL];
     dst.na = c.h_pinned[F_MISC0];
     dst.nb = c.h_pinned[F_MISC1];

@@ -1382,115 +1382,125 @@ int spanner_net_run(Ctx &c, int64_t *node_count, int64_t *n_arcs) {
     if (const char *mm = getenv("W1G_SP_MED_MAX")) med_max = (unsigned)atoi(mm);
     if (med_max > 256u) med_max = 256u;
     if (med_max < 32u) med_max = 32u;
-    SubTimer T(c, "spcsr");
-    int64_t *sup, *ro, *ot, *oh;
-    double *oc;
-    unsigned *cnt;
-    uint32_t *sh;
-    int32_t *lists;
-    W1G_TRY(ensure(c.net_sup, (size_t)n, &sup));
-    W1G_TRY(ensure(c.net_ro, (size_t)n + 2, &ro));
-    W1G_TRY(ensure(c.net_t, (size_t)M + 1, &ot));
-    W1G_TRY(ensure(c.net_h, (size_t)M + 1, &oh));
-    W1G_TRY(ensure(c.net_c, (size_t)M + 1, &oc));
-    W1G_TRY(ensure(c.scr[13], (size_t)2 * (n + 2) + 8, &cnt));
-    unsigned *cursor = cnt + n + 2;
-    // slots sit at their final CSR positions (the diagonal ones stay unused)
-    W1G_TRY(ensure(c.scr[0], (size_t)M + 1, &sh));
-    W1G_TRY(ensure(c.scr[6], (size_t)5 * (K + 1), &lists));
-    int32_t *n_list = reinterpret_cast<int32_t *>(cnt + 2 * (n + 2));  // 5 int32 class counters
-    W1G_TRY(flags_reset(c));
-    W1G_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned) * (2 * (n + 2) + 8), c.stream));
-    const int2 *uv = ptr<int2>(c.pair_uv);
-    const int32_t *rep = ptr<int32_t>(c.t_rep32);
-    const double2 *pp = c.pair_pts ? c.pair_pts : ptr<double2>(ns.pts);
-    if (P) {
-        k_sp_count<<<gs(c, P), 256, 0, c.stream>>>(uv, rep, P, cnt);
-        W1G_CHECK_LAUNCH();
-    }
-    W1G_TRY(scan_i64(c, SpRowLen{cnt, ptr<int64_t>(ns.am), K, ns.nb}, n + 1, ro, nullptr));
-    // the tails depend on the row offsets alone: on the side stream, concurrently with the
-    // scatter and the row sorts, followed there by their early D2H copy (when armed)
-    cudaStream_t side = c.copy_stream ? c.copy_stream : c.stream;
-    if (side != c.stream) {
-        W1G_CUDA(cudaEventRecord(c.ev[12], c.stream));
-        W1G_CUDA(cudaStreamWaitEvent(side, c.ev[12], 0));
-    }
-    k_sp_tails<<<gs(c, M), 256, 0, side>>>(ro, K, ot);
-    W1G_CHECK_LAUNCH();
-    c.net_early_copy = false;
-    {
-        const Ctx::NetOut &o = c.net_out;
-        const bool early_env = [] {  // W1G_EARLY_COPY=0: copy everything after the rows (read per call)
-            const char *e = getenv("W1G_EARLY_COPY");
-            return !(e && *e == '0');
-        }();
-        if (early_env && o.sup && n <= o.node_cap && M <= o.arc_cap && side != c.stream) {
-            W1G_CUDA(cudaMemcpyAsync(o.t, ot, sizeof(int64_t) * M, cudaMemcpyDeviceToHost, side));
-            W1G_CUDA(cudaMemcpyAsync(o.ro, ro, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost, side));
-            c.net_early_copy = true;
+    // the whole CSR build, one graph (graph_segment); the flags ride on the caller's final wait
+    W1G_TRY(graph_segment(c, GSEG_CSR, [&]() -> int {
+        SubTimer T(c, "spcsr");
+        int64_t *sup, *ro, *ot, *oh;
+        double *oc;
+        unsigned *cnt;
+        uint32_t *sh;
+        int32_t *lists;
+        W1G_TRY(ensure(c.net_sup, (size_t)n, &sup));
+        W1G_TRY(ensure(c.net_ro, (size_t)n + 2, &ro));
+        W1G_TRY(ensure(c.net_t, (size_t)M + 1, &ot));
+        W1G_TRY(ensure(c.net_h, (size_t)M + 1, &oh));
+        W1G_TRY(ensure(c.net_c, (size_t)M + 1, &oc));
+        W1G_TRY(ensure(c.scr[13], (size_t)2 * (n + 2) + 8, &cnt));
+        unsigned *cursor = cnt + n + 2;
+        // slots sit at their final CSR positions (the diagonal ones stay unused)
+        W1G_TRY(ensure(c.scr[0], (size_t)M + 1, &sh));
+        W1G_TRY(ensure(c.scr[6], (size_t)5 * (K + 1), &lists));
+        int32_t *n_list = reinterpret_cast<int32_t *>(cnt + 2 * (n + 2));  // 5 int32 class counters
+        W1G_TRY(flags_reset(c));
+        W1G_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned) * (2 * (n + 2) + 8), c.stream));
+        const int2 *uv = ptr<int2>(c.pair_uv);
+        const int32_t *rep = ptr<int32_t>(c.t_rep32);
+        const double2 *pp = c.pair_pts ? c.pair_pts : ptr<double2>(ns.pts);
+        if (P) {
+            k_sp_count<<<gs(c, P), 256, 0, c.stream>>>(uv, rep, P, cnt);
+            W1G_CHECK_LAUNCH();
         }
-    }
-    if (side != c.stream) W1G_CUDA(cudaEventRecord(c.ev[13], side));
-    if (P) {
-        k_sp_scatter<<<gs(c, P), 256, 0, c.stream>>>(uv, rep, P, ro, cursor, sh);
+        W1G_TRY(scan_i64(c, SpRowLen{cnt, ptr<int64_t>(ns.am), K, ns.nb}, n + 1, ro, nullptr));
+        // the tails depend on the row offsets alone: on the side stream, concurrently with the
+        // scatter and the row sorts, followed there by their early D2H copy (when armed)
+        cudaStream_t side = c.copy_stream ? c.copy_stream : c.stream;
+        if (side != c.stream) {
+            W1G_CUDA(cudaEventRecord(c.ev[12], c.stream));
+            W1G_CUDA(cudaStreamWaitEvent(side, c.ev[12], 0));
+        }
+        k_sp_tails<<<gs(c, M), 256, 0, side>>>(ro, K, ot);
         W1G_CHECK_LAUNCH();
-    }
-    T.mark("bucket");
-    const SpRows R{ro, cnt, sh, pp, ot, oh, oc, dflags(c)};
-    const DiagArgs D{ptr<double2>(ns.pts), ptr<int64_t>(ns.am), ptr<int64_t>(ns.bm), ptr<int64_t>(ns.exb),
-                     ns.abar, ns.bbar, sup};
-    k_sp_short_rows<<<grid_for(K * 16, 256, 16u * c.sm_count), 256, 0, c.stream>>>(R, K, lists, n_list, long_max,
-                                                                                   med_max, big_max, D);
-    W1G_CHECK_LAUNCH();
-    k_sp_w32_rows<<<4 * c.sm_count, 256, 0, c.stream>>>(R, lists + CL_W32 * K, n_list + CL_W32);
-    W1G_CHECK_LAUNCH();
-    k_sp_med_rows<0><<<8 * c.sm_count, CSR_MB, 0, c.stream>>>(R, lists + CL_MED * K, n_list + CL_MED);
-    W1G_CHECK_LAUNCH();
-    T.mark("short_med");
-    if (big_max > med_max) {  // (rows of med_max+1..big_max; none by default)
-        k_sp_med_rows<1><<<4 * c.sm_count, CSR_MB, 0, c.stream>>>(R, lists + SP_CL_BIG * K, n_list + SP_CL_BIG);
-        W1G_CHECK_LAUNCH();
-    }
-    T.mark("big");
-    {
-        // long rows: bitmap ranks while a K-bit bitmap (+ prefixes) fits in shared memory;
-        // as many CTAs per SM as the bitmap allows (a row's phases are latency-bound)
-        if (bitmap_fits) {
-            const int32_t *cta_rows = lists + CL_LONG * K, *cta_n = n_list + CL_LONG;
-            static const bool win_bm = [] {  // W1G_SP_WIN_BITMAP=0: the full-K kernel for every long row
-                const char *e = getenv("W1G_SP_WIN_BITMAP");
+        c.net_early_copy = false;
+        {
+            const Ctx::NetOut &o = c.net_out;
+            const bool early_env = [] {  // W1G_EARLY_COPY=0: copy everything after the rows (read per call)
+                const char *e = getenv("W1G_EARLY_COPY");
                 return !(e && *e == '0');
             }();
-            if (win_bm) {
-                // a CTA per row over its head span; rows with wider spans to the full-K kernel
-                int32_t *ovf = lists + 4 * K, *n_ovf = n_list + 4;
-                int per = 1;
-                W1G_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_sp_win_bitmap, WB_T, 0));
-                if (per < 1) per = 1;
-                k_sp_win_bitmap<<<per * c.sm_count, WB_T, 0, c.stream>>>(R, cta_rows, cta_n, ovf, n_ovf);
-                W1G_CHECK_LAUNCH();
-                cta_rows = ovf;
-                cta_n = n_ovf;
+            if (early_env && o.sup && n <= o.node_cap && M <= o.arc_cap && side != c.stream) {
+                W1G_CUDA(cudaMemcpyAsync(o.t, ot, sizeof(int64_t) * M, cudaMemcpyDeviceToHost, side));
+                W1G_CUDA(cudaMemcpyAsync(o.ro, ro, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost, side));
+                c.net_early_copy = true;
             }
-            if (bm_bytes > 48 * 1024)
-                W1G_CUDA(cudaFuncSetAttribute(k_sp_long_bitmap, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              (int)bm_bytes));
-            int per_sm = 1;
-            W1G_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sp_long_bitmap, SP_BM_THREADS,
-                                                                   bm_bytes));
-            if (per_sm < 1) per_sm = 1;
-            k_sp_long_bitmap<<<per_sm * c.sm_count, SP_BM_THREADS, bm_bytes, c.stream>>>(R, cta_rows, cta_n, K);
-        } else {
-            k_sp_long_rows<<<c.sm_count, CSR_LB, 0, c.stream>>>(R, lists + CL_LONG * K, n_list + CL_LONG);
         }
-        W1G_CHECK_LAUNCH();
+        // (also waited for after this stage: a graph-external record when captured)
+    if (side != c.stream) {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        W1G_CUDA(cudaStreamIsCapturing(side, &cs));
+        W1G_CUDA(cudaEventRecordWithFlags(c.ev[13], side,
+                                          cs == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : 0));
     }
-    T.mark("long");
-    if (side != c.stream) W1G_CUDA(cudaStreamWaitEvent(c.stream, c.ev[13], 0));  // the tails (and their copy)
-    // the flags ride on the caller's final wait (no round trip here)
-    W1G_TRY(to_host_small(c, c.h_pinned + F_OVERFLOW, dflags(c) + F_OVERFLOW,
-                          sizeof(int64_t) * (F_NET_ERR - F_OVERFLOW + 1)));
+        if (P) {
+            k_sp_scatter<<<gs(c, P), 256, 0, c.stream>>>(uv, rep, P, ro, cursor, sh);
+            W1G_CHECK_LAUNCH();
+        }
+        T.mark("bucket");
+        const SpRows R{ro, cnt, sh, pp, ot, oh, oc, dflags(c)};
+        const DiagArgs D{ptr<double2>(ns.pts), ptr<int64_t>(ns.am), ptr<int64_t>(ns.bm), ptr<int64_t>(ns.exb),
+                         ns.abar, ns.bbar, sup};
+        k_sp_short_rows<<<grid_for(K * 16, 256, 16u * c.sm_count), 256, 0, c.stream>>>(R, K, lists, n_list, long_max,
+                                                                                       med_max, big_max, D);
+        W1G_CHECK_LAUNCH();
+        k_sp_w32_rows<<<4 * c.sm_count, 256, 0, c.stream>>>(R, lists + CL_W32 * K, n_list + CL_W32);
+        W1G_CHECK_LAUNCH();
+        k_sp_med_rows<0><<<8 * c.sm_count, CSR_MB, 0, c.stream>>>(R, lists + CL_MED * K, n_list + CL_MED);
+        W1G_CHECK_LAUNCH();
+        T.mark("short_med");
+        if (big_max > med_max) {  // (rows of med_max+1..big_max; none by default)
+            k_sp_med_rows<1><<<4 * c.sm_count, CSR_MB, 0, c.stream>>>(R, lists + SP_CL_BIG * K, n_list + SP_CL_BIG);
+            W1G_CHECK_LAUNCH();
+        }
+        T.mark("big");
+        {
+            // long rows: bitmap ranks while a K-bit bitmap (+ prefixes) fits in shared memory;
+            // as many CTAs per SM as the bitmap allows (a row's phases are latency-bound)
+            if (bitmap_fits) {
+                const int32_t *cta_rows = lists + CL_LONG * K, *cta_n = n_list + CL_LONG;
+                static const bool win_bm = [] {  // W1G_SP_WIN_BITMAP=0: the full-K kernel for every long row
+                    const char *e = getenv("W1G_SP_WIN_BITMAP");
+                    return !(e && *e == '0');
+                }();
+                if (win_bm) {
+                    // a CTA per row over its head span; rows with wider spans to the full-K kernel
+                    int32_t *ovf = lists + 4 * K, *n_ovf = n_list + 4;
+                    int per = 1;
+                    W1G_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_sp_win_bitmap, WB_T, 0));
+                    if (per < 1) per = 1;
+                    k_sp_win_bitmap<<<per * c.sm_count, WB_T, 0, c.stream>>>(R, cta_rows, cta_n, ovf, n_ovf);
+                    W1G_CHECK_LAUNCH();
+                    cta_rows = ovf;
+                    cta_n = n_ovf;
+                }
+                if (bm_bytes > 48 * 1024)
+                    W1G_CUDA(cudaFuncSetAttribute(k_sp_long_bitmap, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  (int)bm_bytes));
+                int per_sm = 1;
+                W1G_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sp_long_bitmap, SP_BM_THREADS,
+                                                                       bm_bytes));
+                if (per_sm < 1) per_sm = 1;
+                k_sp_long_bitmap<<<per_sm * c.sm_count, SP_BM_THREADS, bm_bytes, c.stream>>>(R, cta_rows, cta_n, K);
+            } else {
+                k_sp_long_rows<<<c.sm_count, CSR_LB, 0, c.stream>>>(R, lists + CL_LONG * K, n_list + CL_LONG);
+            }
+            W1G_CHECK_LAUNCH();
+        }
+        T.mark("long");
+        if (side != c.stream) W1G_CUDA(cudaStreamWaitEvent(c.stream, c.ev[13], 0));  // the tails (and their copy)
+        // the flags ride on the caller's final wait (no round trip here)
+        W1G_TRY(to_host_small(c, c.h_pinned + F_OVERFLOW, dflags(c) + F_OVERFLOW,
+                              sizeof(int64_t) * (F_NET_ERR - F_OVERFLOW + 1)));
+        return W1G_OK;
+    }));
     c.net_check_pending = true;
     c.arcs_valid = false;  // never materialised on this path
     c.net_n = n;
