@@ -155,6 +155,12 @@ class Dist:
         self.world = int(os.environ.get("WORLD_SIZE", "1"))
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
         self.pg = None
+        # W1G_BENCH_SHARE_GPU=1 (checks only, never a bench number): every rank on GPU 0 with a
+        # gloo group, to exercise the multi-rank code path where one GPU is available (the
+        # ranks' kernels never wait on one another; only host barriers join them)
+        if os.environ.get("W1G_BENCH_SHARE_GPU") == "1" and backend:
+            self.local = 0
+            backend = "gloo"
         if self.world > 1 and backend:
             import torch
             import torch.distributed as dist
