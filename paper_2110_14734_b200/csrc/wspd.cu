@@ -775,6 +775,16 @@ int wspd_run(Ctx &c, double s, int reference_order, int64_t *n_pairs, bool want_
     // fused: two ping-pong frontiers; reference order: one array holding every
     // level (the recursion forest has ~2P items)
     int64_t front_cap = ORDER ? 2 * pair_cap + K + 4096 : pair_cap / 2 + 2 * K + 4096;
+    {
+        // W1G_WSPD_TINY_CAPS=1 (tests, read per call): capacities far below the need, so the
+        // overflow flags and the regrow-and-retry path run (the depth-first kernel's pool
+        // still holds every owner's root item: front_cap >= 2K)
+        const char *e = getenv("W1G_WSPD_TINY_CAPS");
+        if (e && *e == '1') {
+            pair_cap = K / 4 + 64;
+            front_cap = ORDER ? pair_cap + K + 64 : 2 * K + 64;
+        }
+    }
     // the recursion depth is at most depth(u) + depth(v) <= 2 nn
     const int64_t max_levels = 2 * nn + 8;
     for (int attempt = 0; attempt < 8; attempt++) {
@@ -828,7 +838,13 @@ int wspd_run(Ctx &c, double s, int reference_order, int64_t *n_pairs, bool want_
                 int per = 0;
                 W1G_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_wspd_dfs, DF_W * 32, 0));
                 if (per < 1) per = 1;
-                const int G = max(1, per * c.sm_count / max(1, c.coop_share));
+                // W1G_WSPD_DFS_DIV (tuning): a further divisor of the grid (fewer resident warps
+                // left waiting in the kernel's tail next to other contexts' kernels)
+                static const int dfs_div = [] {
+                    const char *e = getenv("W1G_WSPD_DFS_DIV");
+                    return e ? max(1, atoi(e)) : 1;
+                }();
+                const int G = max(1, per * c.sm_count / max(1, c.coop_share) / dfs_div);
                 k_wspd_dfs<<<G, DF_W * 32, 0, c.stream>>>(ptr<int2>(c.t_lr), ptr<NodeGeom>(c.t_geom), s, pool, uv,
                                                           pair_cap);
                 W1G_CHECK_LAUNCH();

@@ -265,3 +265,25 @@ def test_gathered_shard_pairs_build_the_network(w1g, G):
     net = fetch_network(ctx, n_.value, m_.value)
     for f in NET_FIELDS:
         assert bits_equal(getattr(net, f), getattr(ref, f)), f
+
+
+def test_wspd_capacity_regrow(w1g, monkeypatch):
+    """The WSPD's pair and frontier / pool capacities start far too small
+    (W1G_WSPD_TINY_CAPS=1): the overflow flags and the regrow-and-retry path give the
+    same network (depth-first kernel) and the same reference-order pairs (standalone
+    build_wspd) as the normal capacities."""
+    from paper_2110_14734_b200 import synth
+
+    a, b = synth.gaussian_cluster_pair(20_000, 20_000, seed=3)
+    params = w1g.ApproxParams(s=4.0, best_effort=True, delta=0.001)
+    ref, _ = w1g.sparsify(a, b, params)
+    nodes = w1g.zero_condense(a, b)
+    tree = w1g.build_split_tree(nodes.points)
+    ref_pairs = w1g.build_wspd(tree, 4.0)
+    monkeypatch.setenv("W1G_WSPD_TINY_CAPS", "1")
+    got, _ = w1g.sparsify(a, b, params)
+    for f in NET_FIELDS:
+        assert bits_equal(getattr(got, f), getattr(ref, f)), f
+    got_pairs = w1g.build_wspd(tree, 4.0)
+    for f in ("node_pairs", "indices"):
+        assert bits_equal(getattr(got_pairs, f), getattr(ref_pairs, f)), f
