@@ -408,7 +408,8 @@ __global__ void __launch_bounds__(OW_T) k_wspd_owners(const int2 *__restrict__ l
 // recursions are independent and each runs exactly); their order is not (the
 // fused front end builds the CSR, a function of the set).
 constexpr int DF_W = 8;        // warps per CTA
-constexpr int DF_S = 512;      // per-warp stack ring, items
+constexpr int DF_S = 256;      // per-warp stack ring, items (512: the L1 left beside the stacks
+                               // caches less node geometry: cfg5 s = 16 kernel 0.92 vs 0.74-0.77 ms)
 constexpr int DF_PB = 128;     // per-warp pair buffer
 constexpr int DF_POLL = 8;     // steps between donation checks
 // counters, one 128-byte line each
@@ -835,6 +836,14 @@ int wspd_run(Ctx &c, double s, int reference_order, int64_t *n_pairs, bool want_
                 k_wspd_init_f<<<gi, 256, 0, c.stream>>>(ptr<int2>(c.t_lr), nn, fa, front_cap, pool.ctr + DL_OWNERS,
                                                         shard, n_shards);
                 W1G_CHECK_LAUNCH();
+                // W1G_WSPD_DFS_CARVEOUT (tuning): the shared-memory carveout in percent (the rest
+                // is L1, which caches the node geometry the steps load)
+                static const int carve = [] {
+                    const char *e = getenv("W1G_WSPD_DFS_CARVEOUT");
+                    return e ? atoi(e) : -1;
+                }();
+                if (carve >= 0)
+                    W1G_CUDA(cudaFuncSetAttribute(k_wspd_dfs, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
                 int per = 0;
                 W1G_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_wspd_dfs, DF_W * 32, 0));
                 if (per < 1) per = 1;

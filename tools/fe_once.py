@@ -27,4 +27,6 @@ tot.sort()
 print(f"n={n} s={s} delta={delta}: launches per front end {(c1 - c0) // reps}, device ms {info.stage_ms[7]:.3f} "
       f"(min {tot[0]:.3f}, median {tot[len(tot) // 2]:.3f} of {reps}), "
       f"K={info.n_points} P={info.n_pairs} M={info.n_arcs} wspd_levels={info.n_levels_wspd}")
+if reps > 1:
+    print("device ms, sorted:", [round(x, 3) for x in tot])
 print({nm: round(float(info.stage_ms[i]), 4) for i, nm in enumerate(_lib.STAGES)})
