@@ -316,7 +316,10 @@ int w1g_ctx_create(int device, w1g_ctx **out) {
     if (const char *e = getenv("W1G_HEAVY")) c->heavy_ratio = atoi(e) > 0 ? atoi(e) : 0;
     if (const char *e = getenv("W1G_OVERLAP")) c->overlap = atoi(e) > 0 ? atoi(e) : 0;
     if (const char *e = getenv("W1G_OVERLAP_E2E")) c->overlap_e2e = atoi(e) > 0 ? atoi(e) : 0;
-    if (const char *e = getenv("W1G_SPLIT_GATE")) c->split_gate = atoi(e) > 0 ? atoi(e) : 0;
+    if (const char *e = getenv("W1G_SPLIT_GATE")) {
+        c->split_gate = atoi(e) > 0 ? atoi(e) : 0;
+        c->split_gate_set = 1;
+    }
     if (const char *e = getenv("W1G_SPLIT_GATE_E2E")) c->split_gate_e2e = atoi(e) > 0 ? atoi(e) : 0;
     {
         // contexts launch at the highest stream priority; the auxiliary RWMD
@@ -1032,7 +1035,14 @@ static int front_end_impl(w1g_ctx *c, const double *d_a, int64_t na, const doubl
     // (gate) only once the main stream has reached the point `gate` names (the
     // spawn points below); with an armed output target it waits for the WSPD so
     // it runs under the CSR and the network's D2H copy
-    const int gate = split ? (c->net_out.sup ? c->split_gate_e2e : c->split_gate) : 0;
+    // when the spanner dominates (s >= 8 at >= 100k points) RWMD waits for the first gate:
+    // started at once, its kernels land in the WSPD / CSR phase about half the time
+    // (cfg5 s = 16, delta = 0.001: bimodal 3.8 / 4.3 ms; gated 3.82-3.88 ms; s = 8: 2.18 vs
+    // 2.25 ms); below that it starts at once (cfg2: 0.835 vs 0.996 ms gated)
+    const bool spanner_heavy = s >= 8.0 && na + nb >= 100000;
+    const int gate = split ? (c->net_out.sup ? c->split_gate_e2e
+                                             : (spanner_heavy && !c->split_gate_set ? 1 : c->split_gate))
+                           : 0;
     std::mutex gate_mu;
     std::condition_variable gate_cv;
     bool gate_open = gate == 0;

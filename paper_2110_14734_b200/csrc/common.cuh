@@ -250,6 +250,7 @@ struct Ctx {
     // split front end: the main-stream point RWMD waits for (0 = none, else a
     // spawn point as above), without / with an armed output target
     int split_gate = 0, split_gate_e2e = 1;
+    int split_gate_set = 0;  // W1G_SPLIT_GATE given: no size-based choice
     Ctx *aux = nullptr;
     AuxWorker *aux_worker = nullptr;  // the host thread that drives `aux` (owned by this context)
     BatchState *batch = nullptr;      // batch executor: child contexts + workers (batch.cu)
