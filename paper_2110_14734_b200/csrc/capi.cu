@@ -1035,8 +1035,9 @@ static int front_end_impl(w1g_ctx *c, const double *d_a, int64_t na, const doubl
     // (gate) only once the main stream has reached the point `gate` names (the
     // spawn points below); with an armed output target it waits for the WSPD so
     // it runs under the CSR and the network's D2H copy
-    // when the spanner dominates (s >= 8 at >= 100k points) RWMD waits for the first gate:
-    // started at once, its kernels land in the WSPD / CSR phase about half the time
+    // when the spanner dominates (s >= 8 at >= 100k points) RWMD waits for the WSPD (gate 1)
+    // and runs under the CSR: started at once, its kernels collide with the WSPD about half
+    // the time
     // (cfg5 s = 16, delta = 0.001: bimodal 3.8 / 4.3 ms; gated 3.82-3.88 ms; s = 8: 2.18 vs
     // 2.25 ms); below that it starts at once (cfg2: 0.835 vs 0.996 ms gated)
     const bool spanner_heavy = s >= 8.0 && na + nb >= 100000;
