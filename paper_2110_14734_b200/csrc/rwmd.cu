@@ -197,6 +197,24 @@ __device__ __forceinline__ double upper_bound(float est, float qn, int direct) {
 }
 
 
+// FP32 twin of within() for the refine's filters: true whenever within(b, a, R) is (it
+// never drops a tile the fp64 test keeps -- extra exact distances cannot change a min):
+// boxes rounded outward, gaps and squares rounded down, the radius (carrying 2^-40 of
+// relative slack over fp64's own rounding) rounded up.  Overflow and NaN only widen it
+// (fmaxf drops a NaN gap to 0; an infinite radius keeps everything).
+__device__ __forceinline__ float4 box_out32(double4 b) {
+    return make_float4(__double2float_rd(b.x), __double2float_rd(b.y), __double2float_ru(b.z),
+                       __double2float_ru(b.w));
+}
+__device__ __forceinline__ float rad_up32(double R) {
+    return R >= 0.0 ? __double2float_ru(R * (1.0 + 0x1p-40)) : -1.0f;
+}
+__device__ __forceinline__ bool within32(float4 b, float4 a, float R) {
+    const float gx = fmaxf(0.0f, fmaxf(__fsub_rd(b.x, a.z), __fsub_rd(a.x, b.z)));
+    const float gy = fmaxf(0.0f, fmaxf(__fsub_rd(b.y, a.w), __fsub_rd(a.y, b.w)));
+    return R >= 0.0f && __fadd_rd(__fmul_rd(gx, gx), __fmul_rd(gy, gy)) <= __fmul_ru(R, R);
+}
+
 __device__ __forceinline__ double gap2(double4 b, double4 a) {  // squared box gap, as within()
     const double gx = fmax(0.0, fmax(b.x - a.z, a.x - b.z));
     const double gy = fmax(0.0, fmax(b.y - a.w, a.y - b.w));
@@ -322,14 +340,19 @@ __global__ void __launch_bounds__(RF_BLOCK) k_refine(const double2 *__restrict__
     __shared__ int32_t s_cand[RF_CAND];
     __shared__ int32_t s_sup[RF_SUPCAP];
     __shared__ double2 s_t[RF_STAGE * RT];
-    __shared__ double4 s_tb[RF_STAGE];
+    __shared__ float4 s_tb32[RF_STAGE];
     __shared__ int s_nc, s_nsup;
     __shared__ double s_r[RF_BLOCK / 32];
     __shared__ double4 s_box[RF_BLOCK / 32];
     __shared__ double4 s_qb;
     __shared__ double s_rmax;
-    __shared__ double2 s_p[RF_QPB];  // per-source point and search radius, for the
-    __shared__ double s_rad[RF_QPB]; // per-source candidate filter
+    __shared__ double2 s_p[RF_QPB];  // per-source point (solo searches)
+    __shared__ float4 s_p32[RF_QPB]; // per-source point box and radius for the candidate
+    __shared__ float s_rad32[RF_QPB];  // filter (FP32, conservative: within32)
+    __shared__ float4 s_box32[RF_BLOCK / 32];
+    __shared__ float s_r32[RF_BLOCK / 32];
+    __shared__ float4 s_qb32;
+    __shared__ float s_rmax32;
     __shared__ double s_solo_r[RF_QPB], s_solo_m2[RF_QPB];  // heavy sources: radius (-1: none), result
     __shared__ unsigned s_hmask[RF_BLOCK / 32];  // heavy sources per warp (lanes with sub == 0)
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, sub = tid & (RF_TPQ - 1);
@@ -360,11 +383,15 @@ __global__ void __launch_bounds__(RF_BLOCK) k_refine(const double2 *__restrict__
     const bool heavy = (direct >> 8) > 0 && valid && r >= 0.0 && r > (double)(direct >> 8) * wmed;
     const double rh = r;
     if (heavy) r = -1.0;  // block-search radius
+    const float4 p32 = box_out32(make_double4(p.x, p.y, p.x, p.y));
     if (sub == 0) {
         s_p[tid / RF_TPQ] = p;
-        s_rad[tid / RF_TPQ] = (valid && r >= 0.0) ? r * (1.0 + 1e-9) : -1.0;
+        s_p32[tid / RF_TPQ] = p32;
+        s_rad32[tid / RF_TPQ] = rad_up32((valid && r >= 0.0) ? r * (1.0 + 1e-9) : -1.0);
         s_solo_r[tid / RF_TPQ] = heavy ? rh * (1.0 + 1e-9) : -1.0;
     }
+    // this thread's own evaluation filter (the same radius as the fp64 test had)
+    const float r_eval32 = rad_up32((valid && r >= 0.0) ? r * (1.0 + 1e-9) : -1.0);
     {
         const unsigned hm = __ballot_sync(0xffffffffu, heavy && sub == 0);
         if (lane == 0) s_hmask[wid] = hm;
@@ -386,6 +413,8 @@ __global__ void __launch_bounds__(RF_BLOCK) k_refine(const double2 *__restrict__
         if (lane == 0) {
             s_box[wid] = b;
             s_r[wid] = rm;
+            s_box32[wid] = box_out32(b);
+            s_r32[wid] = rad_up32(rm * (1.0 + 1e-9));
         }
         __syncthreads();
         if (tid == 0) {
@@ -400,10 +429,14 @@ __global__ void __launch_bounds__(RF_BLOCK) k_refine(const double2 *__restrict__
             }
             s_qb = bb;
             s_rmax = rr * (1.0 + 1e-9);
+            s_qb32 = box_out32(bb);
+            s_rmax32 = rad_up32(rr * (1.0 + 1e-9));
         }
         __syncthreads();
         const double4 qb = s_qb;
         const double rmax = s_rmax;
+        const float4 qb32 = s_qb32;
+        const float rmax32 = s_rmax32;
         const double4 pb = make_double4(p.x, p.y, p.x, p.y);
         const int64_t ntile = (nt + RT - 1) / RT;
         const int64_t nsup = (ntile + SUP - 1) / SUP;
@@ -425,14 +458,13 @@ __global__ void __launch_bounds__(RF_BLOCK) k_refine(const double2 *__restrict__
             for (int e = tid; e < nsr * SUP; e += RF_BLOCK) {
                 const int64_t k = (int64_t)s_sup[u0 + e / SUP] * SUP + (e % SUP);
                 if (k >= ntile) continue;
-                const double4 tb = tbox[k];
-                if (!within(tb, qb, rmax)) continue;
+                const float4 tb = box_out32(tbox[k]);
+                if (!within32(tb, qb32, rmax32)) continue;
                 bool need = false;
                 for (int w = 0; w < RF_BLOCK / 32 && !need; w++) {
-                    if (!within(tb, s_box[w], s_r[w] * (1.0 + 1e-9))) continue;
+                    if (!within32(tb, s_box32[w], s_r32[w])) continue;
                     for (int j = w * (32 / RF_TPQ); j < (w + 1) * (32 / RF_TPQ); j++) {
-                        const double2 pj = s_p[j];
-                        if (within(tb, make_double4(pj.x, pj.y, pj.x, pj.y), s_rad[j])) {
+                        if (within32(tb, s_p32[j], s_rad32[j])) {
                             need = true;
                             break;
                         }
@@ -452,10 +484,10 @@ __global__ void __launch_bounds__(RF_BLOCK) k_refine(const double2 *__restrict__
                     const int64_t j = k * RT + (e % RT);
                     s_t[e] = j < nt ? t[j] : make_double2(INFINITY, INFINITY);
                 }
-                if (tid < ns) s_tb[tid] = tbox[s_cand[c0 + tid]];
+                if (tid < ns) s_tb32[tid] = box_out32(tbox[s_cand[c0 + tid]]);
                 __syncthreads();
                 for (int c = 0; c < ns; c++) {
-                    const bool need = valid && r >= 0.0 && within(s_tb[c], pb, r * (1.0 + 1e-9));
+                    const bool need = within32(s_tb32[c], p32, r_eval32);
                     if (!__any_sync(0xffffffffu, need)) continue;
                     if (evals && lane == 0) atomicAdd(evals, (unsigned long long)(32 / RF_TPQ) * RT);
                     const double2 *st = s_t + c * RT + sub;
