@@ -18,6 +18,8 @@
 //     the solver drains the queue (workers wait for a block instead).
 //   * w1g_front_end_batch is the synchronous variant that leaves every network
 //     in device memory (front-end throughput, and the per-pair diagnostics).
+#include <emmintrin.h>
+
 #include <atomic>
 #include <chrono>
 #include <cstring>
@@ -249,16 +251,20 @@ __global__ void k_stage_copy(CopyJob J) {
 // upper half of their int64 array, widened in place front to back (element i's
 // 8 bytes never overlap an int32 not yet read)
 static void expand_network(const w1g_batch_result &r) {
+    // non-temporal 8-byte stores (MOVNTI): the arrays are written once and read later by
+    // the consumer, so no read-for-ownership of their cache lines (the expansion is bound
+    // by host memory traffic: 22.5 MB written per cfg2 network)
     const int64_t n = r.info.node_count, m = r.info.n_arcs;
     const int64_t *ro = r.row_offsets;
-    int64_t *t = r.tails;
+    long long *t = reinterpret_cast<long long *>(r.tails);
     for (int64_t q = 0; q < n; q++) {
         const int64_t e = ro[q + 1];
-        for (int64_t a = ro[q]; a < e; a++) t[a] = q;
+        for (int64_t a = ro[q]; a < e; a++) _mm_stream_si64(t + a, (long long)q);
     }
     const int32_t *h32 = reinterpret_cast<const int32_t *>(reinterpret_cast<const char *>(r.heads) + 4 * m);
-    int64_t *h = r.heads;
-    for (int64_t i = 0; i < m; i++) h[i] = h32[i];
+    long long *h = reinterpret_cast<long long *>(r.heads);
+    for (int64_t i = 0; i < m; i++) _mm_stream_si64(h + i, (long long)h32[i]);
+    _mm_sfence();
 }
 
 struct StageSlot {

@@ -111,7 +111,12 @@ __device__ __forceinline__ void wspd_level(const ItemF *__restrict__ cur, ItemF 
                                            const int2 *__restrict__ lr, int64_t n_known = -1) {
     using Item = ItemF;
     int64_t n = n_known >= 0 ? n_known : *((volatile int64_t *)&k.cnt[level % 3]);
-    if (n > cap) n = cap;  // previous level overflowed: its flag is already set
+    // (level-loop launches: a previous level that overflowed left more items than the
+    // buffer holds; its flag is already set.  With n_known the caller checked the level
+    // fits -- and `cap` is the NEXT level's room, which in reference order is the rest of
+    // the one array: clamping the current level by it would leave items unprocessed,
+    // their links unwritten, without any flag)
+    if (n_known < 0 && n > cap) n = cap;
     if (blockIdx.x == 0 && threadIdx.x == 0) k.cnt[(level + 2) % 3] = 0;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const unsigned lt = lanemask_lt();
@@ -783,7 +788,7 @@ int wspd_run(Ctx &c, double s, int reference_order, int64_t *n_pairs, bool want_
         const char *e = getenv("W1G_WSPD_TINY_CAPS");
         if (e && *e == '1') {
             pair_cap = K / 4 + 64;
-            front_cap = ORDER ? pair_cap + K + 64 : 2 * K + 64;
+            front_cap = ORDER ? 4 * pair_cap + K + 64 : 2 * K + 64;
         }
     }
     // the recursion depth is at most depth(u) + depth(v) <= 2 nn

@@ -1,2 +1,2 @@
 mkdir -p gpurun_out
-timeout 1200 python tools/stress_r02.py 60 > gpurun_out/stress.log 2>&1; echo rc=$? >> gpurun_out/stress.log
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1; echo "tests rc=$?" >> gpurun_out/gpu_tests.log
