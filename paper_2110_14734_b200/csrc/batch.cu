@@ -180,7 +180,7 @@ struct BatchState {
     // compact transfer (W1G_BATCH_COMPACT=0: off): the tails are not copied and the heads
     // cross as int32; expander threads rebuild both on the host before a result is
     // handed over (cfg2: 25.5 instead of 47.3 MB per network over the link)
-    bool compact = true;
+    int compact = 1;  // 0: off, 1: tails rebuilt + int32 heads widened, 2: tails rebuilt only
     std::vector<std::thread> expanders;
     std::deque<w1g_batch_result> expand_q;
     std::mutex emu;
@@ -250,7 +250,7 @@ __global__ void k_stage_copy(CopyJob J) {
 // offsets (row r's arcs are [ro[r], ro[r+1])) and the heads arrive as int32 in the
 // upper half of their int64 array, widened in place front to back (element i's
 // 8 bytes never overlap an int32 not yet read)
-static void expand_network(const w1g_batch_result &r) {
+static void expand_network(const w1g_batch_result &r, int mode) {
     // non-temporal 8-byte stores (MOVNTI): the arrays are written once and read later by
     // the consumer, so no read-for-ownership of their cache lines (the expansion is bound
     // by host memory traffic: 22.5 MB written per cfg2 network)
@@ -261,9 +261,11 @@ static void expand_network(const w1g_batch_result &r) {
         const int64_t e = ro[q + 1];
         for (int64_t a = ro[q]; a < e; a++) _mm_stream_si64(t + a, (long long)q);
     }
-    const int32_t *h32 = reinterpret_cast<const int32_t *>(reinterpret_cast<const char *>(r.heads) + 4 * m);
-    long long *h = reinterpret_cast<long long *>(r.heads);
-    for (int64_t i = 0; i < m; i++) _mm_stream_si64(h + i, (long long)h32[i]);
+    if (mode == 1) {
+        const int32_t *h32 = reinterpret_cast<const int32_t *>(reinterpret_cast<const char *>(r.heads) + 4 * m);
+        long long *h = reinterpret_cast<long long *>(r.heads);
+        for (int64_t i = 0; i < m; i++) _mm_stream_si64(h + i, (long long)h32[i]);
+    }
     _mm_sfence();
 }
 
@@ -273,7 +275,7 @@ struct StageSlot {
 };
 
 static int stage_copy(w1g_ctx *x, cudaStream_t cs, StageSlot &st, int64_t n, int64_t m, const NetCarve &cv,
-                      bool compact) {
+                      int compact) {
     int64_t *sup, *t = nullptr, *h, *ro;
     double *c;
     W1G_TRY(ensure(st.sup, (size_t)n + 1, &sup));
@@ -299,8 +301,8 @@ static int stage_copy(w1g_ctx *x, cudaStream_t cs, StageSlot &st, int64_t n, int
     J.h64 = nullptr;
     J.h32 = nullptr;
     J.n_h2 = 0;
-    if (compact) {
-        J.n16[1] = 0;  // no tails
+    if (compact) J.n16[1] = 0;  // no tails
+    if (compact == 1) {
         J.n16[2] = 0;  // heads narrowed instead (the int64 buffers hold whole 16-byte words)
         J.h64 = static_cast<const longlong2 *>(x->net_h.p);
         J.h32 = reinterpret_cast<int2 *>(h);
@@ -311,9 +313,11 @@ static int stage_copy(w1g_ctx *x, cudaStream_t cs, StageSlot &st, int64_t n, int
     W1G_CUDA(cudaEventRecord(st.d2d, ms));
     W1G_CUDA(cudaStreamWaitEvent(cs, st.d2d, 0));
     W1G_CUDA(cudaMemcpyAsync(cv.sup, sup, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, cs));
-    if (compact) {
+    if (compact == 1) {
         W1G_CUDA(cudaMemcpyAsync(reinterpret_cast<char *>(cv.h) + 4 * m, h, sizeof(int32_t) * m,
                                  cudaMemcpyDeviceToHost, cs));
+    } else if (compact == 2) {
+        W1G_CUDA(cudaMemcpyAsync(cv.h, h, sizeof(int64_t) * m, cudaMemcpyDeviceToHost, cs));
     } else {
         W1G_CUDA(cudaMemcpyAsync(cv.t, t, sizeof(int64_t) * m, cudaMemcpyDeviceToHost, cs));
         W1G_CUDA(cudaMemcpyAsync(cv.h, h, sizeof(int64_t) * m, cudaMemcpyDeviceToHost, cs));
@@ -354,7 +358,7 @@ static void batch_expander(BatchState *b) {
             r = b->expand_q.front();
             b->expand_q.pop_front();
         }
-        expand_network(r);
+        expand_network(r, b->compact);
         batch_publish(b, r);
     }
 }
@@ -563,7 +567,7 @@ static int batch_start(Ctx &c, const int32_t *pairs, int64_t n_pairs, const Batc
     const int nt = (int)(n_pairs < streams ? (n_pairs > 0 ? n_pairs : 1) : streams);
     {
         const char *e = getenv("W1G_BATCH_COMPACT");
-        b.compact = deliver && !(e && *e == '0');
+        b.compact = !deliver ? 0 : (e && *e == '0') ? 0 : (e && *e == '2') ? 2 : 1;
     }
     b.expand_q.clear();
     b.workers_left = nt;
