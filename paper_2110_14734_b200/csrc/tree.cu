@@ -313,7 +313,7 @@ struct LocalSmem {
     LocalInfo info[LOCAL_MAX / 2 + 1];
     int16_t big[LOCAL_MAX / 2 + 1];
     int32_t warp_tot[LT / 32];
-    int32_t nsub_next, nbig;
+    int32_t nsub_ring[3], nbig_ring[2];  // per-level counters, rings (no reset barrier)
 };
 
 __device__ __forceinline__ double lcoord(const LocalSmem &S, int id, int axis) {
@@ -363,7 +363,8 @@ __device__ __forceinline__ int scalar_prefix_count(const LocalSmem &S, const uin
 // split one sub-segment (spanner.py:124-148); WARP = true: the calling warp
 // cooperates on the search and lane 0 writes, false: the calling thread alone
 template <bool WARP>
-__device__ __forceinline__ void local_split(LocalSmem &S, int s, int cur, const TreeOut &o, int64_t *flags) {
+__device__ __forceinline__ void local_split(LocalSmem &S, int s, int cur, const TreeOut &o, int64_t *flags,
+                                            int32_t *nsub_next) {
     const int lane = threadIdx.x & 31;
     const bool writer = WARP ? lane == 0 : true;
     const LocalSub sg = S.sub[cur][s];
@@ -407,7 +408,7 @@ __device__ __forceinline__ void local_split(LocalSmem &S, int s, int cur, const 
     in.thr = thr;
     const int nr = n - nl;
     const int want = (nl > 1) + (nr > 1);
-    int slot = want ? atomicAdd(&S.nsub_next, want) : 0;
+    int slot = want ? atomicAdd(nsub_next, want) : 0;
     if (nl == 1) {
         const int li = al[lo];
         write_node(o, lid, S.px[li], S.py[li], S.px[li], S.py[li], S.gid[li], 1, -1, -1);
@@ -453,21 +454,31 @@ __global__ void __launch_bounds__(LT) k_tree_local(const double2 *__restrict__ p
         for (int i = tid; i < m; i += LT) S.yl[0][i] = (uint16_t)inv[gy[L.lo + i]];
         if (tid == 0) {
             S.sub[0][0] = LocalSub{0, (int16_t)m, L.nid};
-            S.nsub_next = 0;
-            S.nbig = 0;
+            S.nsub_ring[1] = 0;
+            S.nbig_ring[0] = 0;
         }
         __syncthreads();
-        int cur = 0, nsub = 1;
+        int cur = 0, nsub = 1, lv = 0;
         while (nsub > 0) {
+            // level lv appends to nsub_ring[(lv+1)%3] and counts its big sub-segments in
+            // nbig_ring[lv&1]; the slots the NEXT level uses are zeroed during this one
+            // (after the first barrier: every thread has read them by then), so no
+            // barrier-separated reset is needed
+            int32_t *nnext = &S.nsub_ring[(lv + 1) % 3];
+            int32_t *nbig = &S.nbig_ring[lv & 1];
             // (A) small sub-segments: one thread each; large ones: one warp each
             for (int s = tid; s < nsub; s += LT) {
                 if (S.sub[cur][s].hi - S.sub[cur][s].lo > 64)
-                    S.big[atomicAdd(&S.nbig, 1)] = (int16_t)s;
+                    S.big[atomicAdd(nbig, 1)] = (int16_t)s;
                 else
-                    local_split<false>(S, s, cur, o, flags);
+                    local_split<false>(S, s, cur, o, flags, nnext);
             }
             __syncthreads();
-            for (int k = wid; k < S.nbig; k += LT / 32) local_split<true>(S, S.big[k], cur, o, flags);
+            if (tid == 0) {
+                S.nsub_ring[(lv + 2) % 3] = 0;
+                S.nbig_ring[(lv + 1) & 1] = 0;
+            }
+            for (int k = wid; k < *nbig; k += LT / 32) local_split<true>(S, S.big[k], cur, o, flags, nnext);
             __syncthreads();
             // (B) flags of the other list + block exclusive scan (8 positions per thread)
             int f[LPT], sum = 0;
@@ -531,14 +542,9 @@ __global__ void __launch_bounds__(LT) k_tree_local(const double2 *__restrict__ p
                 S.ps[cur ^ 1][p] = (p < in.lo + in.nl) ? in.cl : in.cr;
             }
             __syncthreads();
-            nsub = S.nsub_next;
-            __syncthreads();
-            if (tid == 0) {
-                S.nsub_next = 0;
-                S.nbig = 0;
-            }
-            __syncthreads();  // the resets must land before the next level's atomics
+            nsub = *nnext;
             cur ^= 1;
+            lv++;
         }
         __syncthreads();
     }
