@@ -509,7 +509,10 @@ __global__ void __launch_bounds__(DF_W * 32) k_wspd_dfs(const int2 *__restrict__
             ItemF it{-1, -1};
             bool got = true;
             if (t < o_chunks) {
-                const int64_t g = t * 32 + lane;
+                // owner chunks are strided: the owners' items lie roughly in node-id order,
+                // biggest recursions (the root's spine) first, and a chunk of 32 consecutive
+                // ones would hand them all to one warp
+                const int64_t g = t + (int64_t)lane * o_chunks;
                 if (g < n0) it = P.items[g];  // written by the init kernel
             } else {
                 const int64_t k = t - o_chunks;
