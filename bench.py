@@ -6,8 +6,9 @@ synth.gaussian_cluster_pair(100000, 100000, seed=p), p = 0..PAIRS-1), s = 1,
 delta = 0.01 (fixed, the chain of test_acceptance.py:224-237), k = 0.99.  A step
 is the full sparsify front end (pipeline.py:105-130: zero_condense -> rwmd ->
 delta_condense -> split tree -> WSPD -> emit arcs -> CSR network) of every pair
-of the batch.  Under torchrun the batch is dealt round-robin to the ranks
-(strong scaling: the total work is fixed; pairs shard with no collective).
+of the batch.  Under torchrun every rank runs its own batch of PAIRS pairs (seeds
+rank * PAIRS + p): weak scaling -- the pairs are independent, so they shard with no
+collective; value = all ranks' pairs / the max-over-ranks time.
 
 Our arm (default):
   value    -- pairs/s of the whole job: the batch with the diagrams already in
@@ -126,7 +127,13 @@ def workload_config(args) -> dict:
                 "l2": "flushed (256 MiB write) before every step"}
     return {"workload": f"cfg2: sparsify front end, {args.n}+{args.n} points per pair, s={args.s}, "
                         f"delta={args.delta}, k={K_LATTICE}",
-            "pairs_per_step": args.pairs, "l2": "flushed (256 MiB write) before every step"}
+            "pairs_per_step_per_gpu": args.pairs, "l2": "flushed (256 MiB write) before every step"}
+
+
+def scaling_of(args) -> str:
+    # cfg2: every rank its own batch of independent pairs, no collective (weak scaling: the
+    # pairs partition the work); cfg4: one fixed matrix dealt over the ranks (strong)
+    return "strong" if args.workload == "cfg4" else "weak"
 
 
 def parse():
@@ -265,13 +272,14 @@ class Clocks:
 
 # ---------------------------------------------------------------- inputs
 
-def cfg2_inputs(args) -> list[np.ndarray]:
-    """Diagrams 2p, 2p+1 = gaussian_cluster_pair(n, n, seed=p) for every pair p of the batch."""
+def cfg2_inputs(args, rank: int = 0) -> list[np.ndarray]:
+    """Diagrams 2p, 2p+1 = gaussian_cluster_pair(n, n, seed=rank * pairs + p) for every pair p
+    of this rank's batch (rank 0: seeds 0..pairs-1)."""
     from paper_2110_14734_b200 import synth
 
     out = []
     for p in range(args.pairs):
-        a, b = synth.gaussian_cluster_pair(args.n, args.n, seed=p)
+        a, b = synth.gaussian_cluster_pair(args.n, args.n, seed=rank * args.pairs + p)
         out += [a, b]
     return out
 
@@ -369,7 +377,7 @@ def run_reference(args, dist: Dist):
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "pairs/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": scaling_of(args), "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (reference generator)", "config": workload_config(args),
         "cpu_baseline": {"value": v, "unit": "pairs/s", "cores": threads, "kind": "reference",
                          "sample": f"{args.steps} timed steps after {args.warmup} warm-up; each step one pair "
@@ -641,9 +649,10 @@ def run_ours(args, dist: Dist):
         diagrams = synth.shared_centre_batch(*CFG4, seed=0)
         all_pairs = [(i, j) for i in range(CFG4[0]) for j in range(i + 1, CFG4[0])]
     else:
-        diagrams = cfg2_inputs(args)
+        diagrams = cfg2_inputs(args, dist.rank)
         all_pairs = [(2 * p, 2 * p + 1) for p in range(args.pairs)]
-    mine = rank_share(all_pairs, dist.rank, dist.world)
+    # cfg2: each rank runs its own batch (weak scaling); cfg4: the matrix dealt over the ranks
+    mine = rank_share(all_pairs, dist.rank, dist.world) if args.workload == "cfg4" else all_pairs
     batch = Batch(ctx, diagrams, mine, args)
     clocks = Clocks(device)
     step_ms, launches, clk = time_batch(batch, args.steps, max(3, args.warmup), flush, dist, clocks)
@@ -700,7 +709,7 @@ def run_ours(args, dist: Dist):
                                  "finite": bool(np.isfinite([m[i, j] for i, j in sub]).all())}
     if dist.rank != 0:
         return
-    total_pairs = len(all_pairs)
+    total_pairs = len(all_pairs) * (1 if args.workload == "cfg4" else dist.world)
     cfg = workload_config(args)  # identical to the reference arm's
     batch_info = {"streams_per_gpu": args.streams, "pairs_per_gpu": len(mine),
                   "nodes_pair0": int(infos[0].n_points) if infos else 0,
@@ -715,7 +724,7 @@ def run_ours(args, dist: Dist):
         "warmup": max(3, args.warmup),
         "ms_per_step": step_ms,
         "higher_is_better": True,
-        "scaling": "strong",
+        "scaling": scaling_of(args),
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (the reference generator, restated draw for draw in synth.py)",

@@ -1,11 +1,3 @@
 mkdir -p gpurun_out
-{
-for cfg in "100000 1.0 0.01 21" "20000 1.0 0.01 21" "100000 4.0 0.001 11" "100000 16.0 0.001 11"; do timeout 120 python tools/fe_once.py $cfg | head -1; done
-} > gpurun_out/lt.log 2>&1
-python tools/launch_rate.py 2>&1 | python -c "
-import sys,json
-for l in sys.stdin:
-    try: d=json.loads(l)
-    except: continue
-    if d['streams'] in (4,6,8): print(d['n'], d['streams'], round(d['pairs_per_s_device_makespan']))
-" >> gpurun_out/lt.log 2>&1
+W1G_BENCH_SHARE_GPU=1 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 2 --steps 4 --warmup 3 --no-extras > gpurun_out/bench_2r.json 2> gpurun_out/bench_2r.err; echo rc=$? >> gpurun_out/bench_2r.err
+timeout 600 python bench.py --steps 5 --warmup 3 --no-extras > gpurun_out/bench_1r.json 2> gpurun_out/bench_1r.err; echo rc=$? >> gpurun_out/bench_1r.err
