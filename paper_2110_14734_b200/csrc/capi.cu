@@ -126,6 +126,29 @@ int to_host_small2(Ctx &c, void *h0, const void *d0, size_t b0, void *h1, const 
     return W1G_OK;
 }
 
+// copy into page-locked staging with non-temporal 16-byte stores (no read-for-ownership of
+// the destination lines: the copy is bound by host memory traffic, and in the batch it
+// runs on every worker next to the network expansion)
+void host_copy_nt(void *dst, const void *src, size_t bytes) {
+    char *d = static_cast<char *>(dst);
+    const char *s = static_cast<const char *>(src);
+    size_t i = 0;
+    if ((reinterpret_cast<uintptr_t>(d) & 15) == 0) {
+        for (; i + 64 <= bytes; i += 64) {
+            const __m128i x0 = _mm_loadu_si128(reinterpret_cast<const __m128i *>(s + i));
+            const __m128i x1 = _mm_loadu_si128(reinterpret_cast<const __m128i *>(s + i + 16));
+            const __m128i x2 = _mm_loadu_si128(reinterpret_cast<const __m128i *>(s + i + 32));
+            const __m128i x3 = _mm_loadu_si128(reinterpret_cast<const __m128i *>(s + i + 48));
+            _mm_stream_si128(reinterpret_cast<__m128i *>(d + i), x0);
+            _mm_stream_si128(reinterpret_cast<__m128i *>(d + i + 16), x1);
+            _mm_stream_si128(reinterpret_cast<__m128i *>(d + i + 32), x2);
+            _mm_stream_si128(reinterpret_cast<__m128i *>(d + i + 48), x3);
+        }
+        _mm_sfence();
+    }
+    if (i < bytes) memcpy(d + i, s + i, bytes - i);
+}
+
 int graph_segment(Ctx &c, int slot, const std::function<int()> &body) {
     static const bool on = [] {  // opt-in: measured no better (measured and rejected)
         const char *e = getenv("W1G_GRAPHS");
@@ -1329,29 +1352,6 @@ int w1g_front_end_device(w1g_ctx *c, const double *d_a, int64_t na, const double
     return rc;
 }
 
-// copy into page-locked staging with non-temporal 16-byte stores (no read-for-ownership of
-// the destination lines: the copy is bound by host memory traffic, and in the batch it
-// runs on every worker next to the network expansion)
-static void copy_nt(void *dst, const void *src, size_t bytes) {
-    char *d = static_cast<char *>(dst);
-    const char *s = static_cast<const char *>(src);
-    size_t i = 0;
-    if ((reinterpret_cast<uintptr_t>(d) & 15) == 0) {
-        for (; i + 64 <= bytes; i += 64) {
-            const __m128i x0 = _mm_loadu_si128(reinterpret_cast<const __m128i *>(s + i));
-            const __m128i x1 = _mm_loadu_si128(reinterpret_cast<const __m128i *>(s + i + 16));
-            const __m128i x2 = _mm_loadu_si128(reinterpret_cast<const __m128i *>(s + i + 32));
-            const __m128i x3 = _mm_loadu_si128(reinterpret_cast<const __m128i *>(s + i + 48));
-            _mm_stream_si128(reinterpret_cast<__m128i *>(d + i), x0);
-            _mm_stream_si128(reinterpret_cast<__m128i *>(d + i + 16), x1);
-            _mm_stream_si128(reinterpret_cast<__m128i *>(d + i + 32), x2);
-            _mm_stream_si128(reinterpret_cast<__m128i *>(d + i + 48), x3);
-        }
-        _mm_sfence();
-    }
-    if (i < bytes) memcpy(d + i, s + i, bytes - i);
-}
-
 int w1g_front_end(w1g_ctx *c, const double *a, int64_t na, const double *b, int64_t nb, double s,
                   int use_condensation, int delta_mode, double delta, double k, uint64_t seed,
                   w1g_front_end_info *info) {
@@ -1368,8 +1368,8 @@ int w1g_front_end(w1g_ctx *c, const double *a, int64_t na, const double *b, int6
         // pageable inputs: stage both diagrams through pinned memory, one full-speed H2D
         W1G_TRY(stage_ensure(*c, bytes));
         W1G_TRY(stream_sync(*c));
-        if (na) copy_nt(c->h_stage, a, sizeof(double2) * na);
-        if (nb) copy_nt(static_cast<char *>(c->h_stage) + sizeof(double2) * na, b, sizeof(double2) * nb);
+        if (na) host_copy_nt(c->h_stage, a, sizeof(double2) * na);
+        if (nb) host_copy_nt(static_cast<char *>(c->h_stage) + sizeof(double2) * na, b, sizeof(double2) * nb);
         if (bytes) W1G_CUDA(cudaMemcpyAsync(d, c->h_stage, bytes, cudaMemcpyHostToDevice, c->stream));
     }
     return w1g_front_end_device(c, reinterpret_cast<double *>(d), na,

@@ -316,6 +316,7 @@ enum FlagSlot {
 // page-locked (h_pinned slots, pool blocks); bytes a multiple of 4.
 int to_host_small(Ctx &c, void *h_dst, const void *d_src, size_t bytes, cudaStream_t s = nullptr);
 int to_host_small2(Ctx &c, void *h0, const void *d0, size_t b0, void *h1, const void *d1, size_t b1);
+void host_copy_nt(void *dst, const void *src, size_t bytes);  // host copy, non-temporal stores
 // Run `body` (launches on c.stream, no host synchronisation) captured as a CUDA graph and
 // replayed with one graph launch: the device fetches one command instead of one per
 // kernel (launches are slow to submit while the host link is busy with network copies:
