@@ -404,12 +404,15 @@ __global__ void __launch_bounds__(OW_T) k_wspd_owners(const int2 *__restrict__ l
 // root items (left[w], right[w]) are its first chunks; a warp whose stack would
 // overflow, or that sees waiting warps, appends the BOTTOM of its stack (the
 // oldest, biggest sub-recursions).  A warp out of work takes a ticket (one
-// atomicAdd, no retry storm) and waits on that chunk's own ready flag (set after
-// its items, cleared by its consumer, so all flags are zero between runs).
-// Termination: `pending` = busy warps + appended-but-unconsumed chunks; it only
-// reaches 0 once nothing is left anywhere, and then stays 0, so a waiting warp
-// leaves when it reads 0.  Warps that start late or never start do not matter
-// (no co-residency needed).  The emitted pair SET is the reference's (the
+// atomicAdd, no retry storm) and waits on that chunk's own ready flag, which carries
+// the run's epoch (set with release semantics after the chunk's items; flags of
+// earlier runs never match, so nothing is cleared between runs).  The owner chunks
+// are strided over the owners (their items lie roughly in node-id order, the
+// biggest recursions first).  Termination: `pending` = busy warps +
+// appended-but-unconsumed chunks; it only reaches 0 once nothing is left anywhere,
+// and then stays 0: the warp that takes it to 0 marks every waiting ticket's flag
+// with the end, and a waiting warp also checks `pending` now and then.  Warps that
+// start late or never start do not matter (no co-residency needed).  The emitted pair SET is the reference's (the
 // recursions are independent and each runs exactly); their order is not (the
 // fused front end builds the CSR, a function of the set).
 constexpr int DF_W = 8;        // warps per CTA
