@@ -3,13 +3,17 @@
 // The reference runs one DFS per internal node w from (left[w], right[w]):
 // a pair (u, v) is emitted when _ws_predicate holds, otherwise the side with
 // the larger bbox diagonal (_diag_sq) is replaced by its two children.  The
-// emitted SET is a function of the tree and s only, so on device all
-// recursions advance together as one breadth-first frontier of (u, v) items,
-// one level per launch: every item evaluates the predicate with the
-// reference's exact fp64 operation order (per-node centres/radii precomputed
-// in tree.cu with the same operations), and warp-aggregated atomics append
-// either a pair or two children.  Levels run in batches; the host polls the
-// frontier size between batches and regrows buffers on overflow.
+// emitted SET is a function of the tree and s only.  Every item evaluates the
+// predicate with the reference's exact fp64 operation order (per-node
+// centres/radii precomputed in tree.cu with the same operations).
+//
+// Fused order (the front end): k_wspd_dfs -- every warp runs recursions depth
+// first on a stack in shared memory, work shared through a ticketed chunk queue
+// (see there).  The level-synchronous alternative (W1G_WSPD_DFS=0): CTA-local
+// owner recursions, then all remaining recursions advance together as one
+// breadth-first frontier of (u, v) items in a cooperative kernel (a grid
+// barrier per level) or level launches.  Buffers regrow and the pass reruns on
+// overflow.
 //
 // reference_order = 1 additionally keeps every level of the frontier (the
 // whole recursion forest, one item per (u, v) the reference's stacks ever
