@@ -5,17 +5,22 @@
 // The reference's CPU baseline for this workload is a loop of approx_w1 over
 // the i < j pairs; the drop-in's pairwise_w1 / sparsify_batch
 // run it as:
-//   * the diagrams are uploaded once per device (w1g_corpus_load);
+//   * the diagrams stay in host memory (w1g_corpus_set_host; each worker uploads
+//     its pair inside its front end) or are uploaded once (w1g_corpus_load);
 //   * `streams` worker threads, each driving its own child context (own CUDA
 //     stream, scratch and RWMD side context), pull pair indices from a shared
 //     atomic counter -- latency-bound front ends of small diagrams overlap on
-//     one GPU;
-//   * each network is copied out inside its front end call into a page-locked
-//     block from a process-wide pool, and queued for the consumer
-//     (w1g_batch_next), which hands it to the host solver and releases the
-//     block when the arrays die (w1g_batch_release).  The pool bounds the bytes
-//     in flight, so a fast front end cannot pin host memory without limit while
-//     the solver drains the queue (workers wait for a block instead).
+//     one GPU; their cooperative kernels run on a 1/streams share of the device;
+//   * a finished network is copied device-to-device into one of the worker's two
+//     staging slots and its D2H into a page-locked block from a process-wide pool
+//     is queued on the worker's own stream, while the worker goes on to its next
+//     pair.  The compact transfer leaves the tails behind and narrows the heads
+//     to int32; expander threads rebuild both on the host (non-temporal stores)
+//     before the result is queued for the consumer (w1g_batch_next), which hands
+//     it to the host solver and releases the block when the arrays die
+//     (w1g_batch_release).  The pool bounds the bytes in flight, so a fast front
+//     end cannot pin host memory without limit while the solver drains the queue
+//     (workers wait for a block instead).
 //   * w1g_front_end_batch is the synchronous variant that leaves every network
 //     in device memory (front-end throughput, and the per-pair diagnostics).
 #include <emmintrin.h>
