@@ -407,6 +407,8 @@ int w1g_ctx_destroy(w1g_ctx *c) {
     for (DevBuf *b : bufs) free_buf(*b);
     free_buf(c->wspd_ready);
     free_buf(c->wspd_ctr);
+    delete c->fill_pool;
+    c->fill_pool = nullptr;
     for (auto &x : c->gseg)
         if (x) {
             cudaGraphExecDestroy(x);
@@ -955,6 +957,32 @@ int w1g_set_network_out(w1g_ctx *c, int64_t *supplies, int64_t *tails, int64_t *
 // the network into the armed output target (asynchronously, on the context
 // stream); the tails and row offsets may already be on their way (spanner_net_run
 // starts them on the copy stream as soon as the row offsets are known)
+// the tails column rebuilt on the host from the row offsets (row r's arcs are
+// [ro[r], ro[r+1])), in parallel, with non-temporal stores, while the rest of the
+// network is still crossing the link
+static void fill_tails(Ctx &c, int64_t *t, const int64_t *ro, int64_t n, int64_t m) {
+    if (!c.fill_pool) {
+        c.fill_pool = new FillPool();
+        c.fill_pool->start(3);
+    }
+    const int parts = 4;
+    c.fill_pool->run(parts, [&](int p) {
+        const int64_t a0 = m * p / parts, a1 = m * (p + 1) / parts;
+        // the row holding arc a0: the last r with ro[r] <= a0
+        int64_t lo = 0, hi = n;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi + 1) / 2;
+            if (ro[mid] <= a0) lo = mid; else hi = mid - 1;
+        }
+        long long *tt = reinterpret_cast<long long *>(t);
+        for (int64_t r = lo; r < n && ro[r] < a1; r++) {
+            const int64_t e = ro[r + 1] < a1 ? ro[r + 1] : a1;
+            for (int64_t q = ro[r] > a0 ? ro[r] : a0; q < e; q++) _mm_stream_si64(tt + q, (long long)r);
+        }
+        _mm_sfence();
+    });
+}
+
 static int copy_network_out(Ctx &c, int *copied) {
     *copied = 0;
     const Ctx::NetOut &o = c.net_out;
@@ -965,6 +993,10 @@ static int copy_network_out(Ctx &c, int *copied) {
     W1G_TRY(download(c, o.c, c.net_c.p, sizeof(double) * m));
     if (c.net_early_copy) {
         W1G_CUDA(cudaStreamWaitEvent(c.stream, c.ev[13], 0));  // the early copies are part of this one
+        if (c.net_tails_host) {
+            W1G_CUDA(cudaEventSynchronize(c.ev[16]));  // the row offsets have landed
+            fill_tails(c, o.t, o.ro, (int64_t)n, (int64_t)m);
+        }
     } else {
         W1G_TRY(download(c, o.t, c.net_t.p, sizeof(int64_t) * m));
         W1G_TRY(download(c, o.ro, c.net_ro.p, sizeof(int64_t) * (n + 1)));

@@ -15,6 +15,7 @@
 #include <mutex>
 #include <string>
 #include <thread>
+#include <vector>
 
 #include "../../include/w1g.h"
 
@@ -98,6 +99,63 @@ enum { SCR_N = 24 };
 // submit() hands a job over; wait() blocks until it has finished.  The job
 // may reference the submitter's stack: every submitter waits before returning
 // (the front end's scope guard does so on every exit path).
+// A few persistent host threads for a parallel host loop inside one API call
+// (run(parts, f): f(0..parts-1), the caller takes a share; returns when all are done).
+struct FillPool {
+    std::vector<std::thread> th;
+    std::mutex mu;
+    std::condition_variable cv, done_cv;
+    std::function<void(int)> job;
+    int parts = 0, next = 0, left = 0;
+    uint64_t gen = 0;
+    bool quit = false;
+    void start(int n) {
+        for (int q = 0; q < n; q++)
+            th.emplace_back([this] {
+                uint64_t seen = 0;
+                std::unique_lock<std::mutex> lk(mu);
+                for (;;) {
+                    cv.wait(lk, [&] { return quit || gen != seen; });
+                    if (quit) return;
+                    seen = gen;
+                    while (next < parts) {
+                        const int p = next++;
+                        lk.unlock();
+                        job(p);
+                        lk.lock();
+                        if (--left == 0) done_cv.notify_all();
+                    }
+                }
+            });
+    }
+    void run(int n, std::function<void(int)> f) {
+        std::unique_lock<std::mutex> lk(mu);
+        job = std::move(f);
+        parts = n;
+        next = 0;
+        left = n;
+        gen++;
+        cv.notify_all();
+        while (next < parts) {
+            const int p = next++;
+            lk.unlock();
+            job(p);
+            lk.lock();
+            --left;
+        }
+        done_cv.wait(lk, [&] { return left == 0; });
+        job = nullptr;
+    }
+    ~FillPool() {
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            quit = true;
+        }
+        cv.notify_all();
+        for (auto &t : th) t.join();
+    }
+};
+
 struct AuxWorker {
     std::thread th;
     std::mutex mu;
@@ -218,6 +276,8 @@ struct Ctx {
     bool net_valid = false;
     bool net_check_pending = false;  // spanner_net_run's flags not yet read
     bool net_early_copy = false;     // tails + row offsets already copied out (copy_stream, ev[13])
+    bool net_tails_host = false;     // ...row offsets only: the tails are rebuilt on the host (ev[16])
+    struct FillPool *fill_pool = nullptr;  // host threads rebuilding the tails (lazily started)
     int64_t net_n = 0, net_m = 0;
     DevBuf net_sup, net_t, net_h, net_c, net_ro;
 
@@ -233,7 +293,7 @@ struct Ctx {
     void *h_stage = nullptr;      // pinned staging buffer for H2D / D2H
     size_t h_stage_cap = 0;
 
-    cudaEvent_t ev[16] = {};
+    cudaEvent_t ev[18] = {};
 
     // fixed-delta front end: RWMD (which then only feeds diagnostics and the
     // L > 0 test) runs on a second context -- own stream, scratch and host

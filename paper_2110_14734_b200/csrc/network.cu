@@ -1421,15 +1421,31 @@ int spanner_net_run(Ctx &c, int64_t *node_count, int64_t *n_arcs) {
         k_sp_tails<<<gs(c, M), 256, 0, side>>>(ro, K, ot);
         W1G_CHECK_LAUNCH();
         c.net_early_copy = false;
+        c.net_tails_host = false;
         {
             const Ctx::NetOut &o = c.net_out;
             const bool early_env = [] {  // W1G_EARLY_COPY=0: copy everything after the rows (read per call)
                 const char *e = getenv("W1G_EARLY_COPY");
                 return !(e && *e == '0');
             }();
+            // W1G_HOST_TAILS=0: copy the tails too (by default the host rebuilds them from the
+            // row offsets while the rest of the network crosses the link: 15 of 47 MB at cfg2)
+            const bool host_tails = [] {
+                const char *e = getenv("W1G_HOST_TAILS");
+                return !(e && *e == '0');
+            }();
             if (early_env && o.sup && n <= o.node_cap && M <= o.arc_cap && side != c.stream) {
-                W1G_CUDA(cudaMemcpyAsync(o.t, ot, sizeof(int64_t) * M, cudaMemcpyDeviceToHost, side));
                 W1G_CUDA(cudaMemcpyAsync(o.ro, ro, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost, side));
+                if (host_tails) {
+                    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+                    W1G_CUDA(cudaStreamIsCapturing(side, &cs));
+                    W1G_CUDA(cudaEventRecordWithFlags(c.ev[16], side,
+                                                      cs == cudaStreamCaptureStatusActive ? cudaEventRecordExternal
+                                                                                           : 0));
+                    c.net_tails_host = true;
+                } else {
+                    W1G_CUDA(cudaMemcpyAsync(o.t, ot, sizeof(int64_t) * M, cudaMemcpyDeviceToHost, side));
+                }
                 c.net_early_copy = true;
             }
         }
