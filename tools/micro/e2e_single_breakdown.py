@@ -36,11 +36,12 @@ import timeit  # noqa: E402
 from paper_2110_14734_b200.pipeline import _diagnostics  # noqa: E402
 
 ncap, mcap = ctx.net_hint
+_info = _front_end(ctx, a, b, p)
 specs = [((ncap,), np.int64), ((mcap,), np.int64), ((mcap,), np.int64), ((mcap,), np.float64), ((ncap + 1,), np.int64)]
 pieces = {
     "points_of x2": lambda: (w1g.diagram.points_of(a), w1g.diagram.points_of(b)),
     "pinned_arrays": lambda: _lib.pinned_arrays(specs),
-    "diagnostics": lambda: _diagnostics(_front_end.__globals__["_lib"].FrontEndInfo()),
+    "diagnostics": lambda: _diagnostics(_info),
     "context()": lambda: _lib.context(),
 }
 out = _lib.pinned_arrays(specs)
