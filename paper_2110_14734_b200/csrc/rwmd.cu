@@ -318,8 +318,6 @@ __device__ double solo_nn(double2 pj, double rad, const double2 *__restrict__ t,
 }
 
 constexpr int RF_BLOCK = 128;
-constexpr int RF_TPQ = 2;                     // threads per source
-constexpr int RF_QPB = RF_BLOCK / RF_TPQ;     // sources per block
 constexpr int RF_CAND = 2048;
 constexpr int RF_STAGE = 16;  // candidate tiles staged per round (16 x 64 targets, 16 KB)
 constexpr int RF_SUPCAP = 1024;  // super-tiles listed per outer round (4M targets)
@@ -327,6 +325,7 @@ constexpr int RF_SUPCAP = 1024;  // super-tiles listed per outer round (4M targe
 // exact fp64 refinement + mass * best (lower_bound.py:51-58).  Two threads per
 // source (each takes every other target of a staged tile, then a shuffle
 // min), sources in Morton order, 64-target Morton tiles kept by a box test
+template <int RF_TPQ>  // threads per source
 __global__ void __launch_bounds__(RF_BLOCK) k_refine(const double2 *__restrict__ q, const int32_t *__restrict__ qpos,
                                                      const int32_t *__restrict__ members,
                                                      const int64_t *__restrict__ mass, int64_t nq,
@@ -337,6 +336,7 @@ __global__ void __launch_bounds__(RF_BLOCK) k_refine(const double2 *__restrict__
                                                      const double4 *__restrict__ sbox,
                                                      double *__restrict__ best_out, double *__restrict__ terms,
                                                      int direct, unsigned long long *evals) {
+    constexpr int RF_QPB = RF_BLOCK / RF_TPQ;  // sources per block
     __shared__ int32_t s_cand[RF_CAND];
     __shared__ int32_t s_sup[RF_SUPCAP];
     __shared__ double2 s_t[RF_STAGE * RT];
@@ -526,8 +526,11 @@ __global__ void __launch_bounds__(RF_BLOCK) k_refine(const double2 *__restrict__
         if (heavy) m2 = fmin(m2, s_solo_m2[tid / RF_TPQ]);
     }
     m2 = m2b < m2 ? m2b : m2;
-    const double other = __shfl_xor_sync(0xffffffffu, m2, 1);
-    m2 = other < m2 ? other : m2;
+#pragma unroll
+    for (int o = 1; o < RF_TPQ; o <<= 1) {
+        const double other = __shfl_xor_sync(0xffffffffu, m2, o);
+        m2 = other < m2 ? other : m2;
+    }
     if (valid && sub == 0) {
         double best = diag;
         if (nt > 0) {
@@ -550,8 +553,27 @@ static int launch_refine(Ctx &c, const double2 *q, const int32_t *qpos, const in
     const int flags = c.culling | (c.debug_radius << 1) | (c.heavy_ratio << 8);
     unsigned long long *evals = c.prof ? ptr<unsigned long long>(c.prof_cnt) + 2 * c.prof_side + 1 : nullptr;
     if (c.prof) W1G_CUDA(cudaEventRecord(c.prof_ev[c.prof_side][1][0], c.stream));
-    k_refine<<<(unsigned)((nq + RF_QPB - 1) / RF_QPB), RF_BLOCK, 0, c.stream>>>(
-        q, qpos, members, mass, nq, mf, qn, unscale, t, nt, tbox, sbox, best, terms, flags, evals);
+    // threads per source (W1G_RF_TPQ = 1, 2, 4 or 8): a warp evaluates a staged tile for all of
+    // its 32 / TPQ sources as soon as one of them needs it
+    static const int tpq = [] {
+        const char *e = getenv("W1G_RF_TPQ");
+        const int v = e ? atoi(e) : 2;
+        return (v == 1 || v == 4 || v == 8) ? v : 2;
+    }();
+    const unsigned qpb = RF_BLOCK / tpq;
+    const unsigned grid = (unsigned)((nq + qpb - 1) / qpb);
+    if (tpq == 8)
+        k_refine<8><<<grid, RF_BLOCK, 0, c.stream>>>(q, qpos, members, mass, nq, mf, qn, unscale, t, nt, tbox,
+                                                     sbox, best, terms, flags, evals);
+    else if (tpq == 1)
+        k_refine<1><<<grid, RF_BLOCK, 0, c.stream>>>(q, qpos, members, mass, nq, mf, qn, unscale, t, nt, tbox,
+                                                     sbox, best, terms, flags, evals);
+    else if (tpq == 4)
+        k_refine<4><<<grid, RF_BLOCK, 0, c.stream>>>(q, qpos, members, mass, nq, mf, qn, unscale, t, nt, tbox,
+                                                     sbox, best, terms, flags, evals);
+    else
+        k_refine<2><<<grid, RF_BLOCK, 0, c.stream>>>(q, qpos, members, mass, nq, mf, qn, unscale, t, nt, tbox,
+                                                     sbox, best, terms, flags, evals);
     W1G_CHECK_LAUNCH();
     if (c.prof) W1G_CUDA(cudaEventRecord(c.prof_ev[c.prof_side][1][1], c.stream));
     return W1G_OK;
