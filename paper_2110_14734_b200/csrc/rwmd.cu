@@ -372,14 +372,18 @@ __global__ void __launch_bounds__(RF_BLOCK) k_refine(const double2 *__restrict__
     // a disc far wider than the warp's median (a poor FP32 seed or an isolated
     // point) would flood the block's shared search: such a source is searched
     // alone afterwards (solo_nn) and takes no part in the block search
-    double v = (valid && r >= 0.0) ? r : INFINITY;  // warp median by a 32-wide bitonic sort
+    // warp median by a 32-wide bitonic sort, in FP32 (a heuristic split only: both the
+    // block search and the solo search are exact, so the rounding cannot change a result)
+    float v = (valid && r >= 0.0) ? (float)r : INFINITY;
+#pragma unroll
     for (int k = 2; k <= 32; k <<= 1)
+#pragma unroll
         for (int jb = k >> 1; jb; jb >>= 1) {
-            const double o = __shfl_xor_sync(0xffffffffu, v, jb);
+            const float o = __shfl_xor_sync(0xffffffffu, v, jb);
             const bool up = ((lane & k) == 0) == ((lane & jb) == 0);
-            v = up ? fmin(v, o) : fmax(v, o);
+            v = up ? fminf(v, o) : fmaxf(v, o);
         }
-    const double wmed = __shfl_sync(0xffffffffu, v, 16);
+    const double wmed = (double)__shfl_sync(0xffffffffu, v, 16);
     const bool heavy = (direct >> 8) > 0 && valid && r >= 0.0 && r > (double)(direct >> 8) * wmed;
     const double rh = r;
     if (heavy) r = -1.0;  // block-search radius
