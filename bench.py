@@ -462,8 +462,8 @@ def rwmd_roofline(ctx, w1g, a, b) -> dict:
     f64 = 5.0 * ref_ev / (ref_ms * 1e-3) / 1e12 if ref_ms else 0.0
     f32 = 5.0 * tile_ev / (tile_ms * 1e-3) / 1e12 if tile_ms else 0.0
     total = sum(ms[i] for i in range(4))
-    ncu_ref = _ncu_capture("r02_ncu_cfg2_rwmd.jsonl", "k_refine")
-    ncu_tile = _ncu_capture("r02_ncu_cfg2_rwmd.jsonl", "k_rwmd_f32")
+    ncu_ref = _ncu_capture("r02c_ncu_cfg2_rwmd.jsonl", "k_refine")
+    ncu_tile = _ncu_capture("r02c_ncu_cfg2_rwmd.jsonl", "k_rwmd_f32")
     return {
         "bound": "fp64", "kernel": "k_refine (rwmd.cu): exact fp64 nearest-neighbour refine, the production RWMD",
         "achieved": f64, "peak": PEAKS["fp64_tflops"], "unit": "TFLOP/s", "frac": f64 / PEAKS["fp64_tflops"],
@@ -504,12 +504,12 @@ def north_star_kernel(ctx, w1g, n: int) -> dict:
     finally:
         ctx.call("w1g_set_rwmd_culling", 1)
     tflops = 5.0 * evals.value / (ms.value * 1e-3) / 1e12
-    return {"bound": "fp32", "kernel": "k_rwmd_f32<8,0,1024> (rwmd_tile.cu), culling off",
+    return {"bound": "fp32", "kernel": "k_rwmd_f32<8,0,1024,1> (rwmd_tile.cu), culling off, two sources packed per FP32x2 lane pair",
             "config": f"{n}+{n} points (gaussian_cluster_pair seed 0)", "achieved": tflops,
             "peak": PEAKS["fp32_tflops"], "unit": "TFLOP/s", "frac": tflops / PEAKS["fp32_tflops"],
             "ms_per_launch": ms.value, "evals_per_launch": evals.value,
-            "traffic": (_ncu_capture("r02_ncu_brute_1m.jsonl", "k_rwmd_f32") or {}).get("dram_bytes_per_launch"),
-            "ncu": _ncu_capture("r02_ncu_brute_1m.jsonl", "k_rwmd_f32"),
+            "traffic": (_ncu_capture("r02c_ncu_brute_1m.jsonl", "k_rwmd_f32") or {}).get("dram_bytes_per_launch"),
+            "ncu": _ncu_capture("r02c_ncu_brute_1m.jsonl", "k_rwmd_f32"),
             "note": "5 FLOP per directed (source, target) evaluation (4 FMA FLOP executed: 2 FFMA per evaluation)"}
 
 

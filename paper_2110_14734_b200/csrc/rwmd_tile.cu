@@ -6,11 +6,13 @@
 //
 //  * R sources per thread in registers, targets staged through shared
 //    memory in tiles and broadcast to the warp;
-//  * expanded form with packed FP32x2 math: per two targets
-//        s = fma2(-2qy, ty, fma2(-2qx, tx, |t|^2))   (2 x FFMA2)
-//        m = min3(m, s.x, s.y)                        (1 x FMNMX3)
-//    i.e. one FFMA2 and half an FMNMX3 per evaluation; |q|^2 is added
-//    after the min;
+//  * expanded form with packed FP32x2 math, two SOURCES per lane pair and
+//    the target broadcast (full mode; PACKQ):
+//        s = fma2((-2y_r, -2y_r+1), ty, fma2((-2x_r, -2x_r+1), tx, |t|^2))
+//        m_r = min3(m_r, s_a.x, s_b.x)   over a target pair (a, b)
+//    i.e. one FFMA2 and half an FMNMX3 per evaluation, the target's operands
+//    shared by every source pair of the thread (operand reuse); |q|^2 is
+//    added after the min (PACKQ = false: two targets per lane pair);
 //  * the expansion cancels, so every CTA works in a LOCAL frame: origin =
 //    its first source (sources are Morton-ordered, so a CTA's sources are
 //    spatially compact) and targets are shifted into that frame as they are
@@ -30,6 +32,8 @@
 //
 // The result only sizes the exact fp64 search in rwmd.cu.  This translation
 // unit is compiled with FMA contraction allowed.
+#include <cmath>
+
 #include "common.cuh"
 
 namespace w1g {
@@ -61,7 +65,7 @@ struct TileArgs {
     unsigned long long *evals;  // profiling: evaluations performed (null: not counted)
 };
 
-template <int R, bool CULL, int T_TS>
+template <int R, bool CULL, int T_TS, bool PACKQ = false>
 __global__ void __launch_bounds__(T_BLOCK) k_rwmd_f32(TileArgs A) {
     __shared__ float4 s_xy[T_TS / 2];
     __shared__ float2 s_tt[T_TS / 2];
@@ -86,8 +90,10 @@ __global__ void __launch_bounds__(T_BLOCK) k_rwmd_f32(TileArgs A) {
         const float fx = CULL ? x : -2.f * x, fy = CULL ? y : -2.f * y;
         ax[r] = make_float2(fx, fx);
         ay[r] = make_float2(fy, fy);
-        qq[r] = fmaf(x, x, y * y);
-        qn[r] = sqrtf(qq[r]);
+        if (CULL) {  // full mode recomputes them after the loop (fewer live registers)
+            qq[r] = fmaf(x, x, y * y);
+            qn[r] = sqrtf(qq[r]);
+        }
         m[r] = INFINITY;
         if (CULL && v) {
             bx0 = fmin(bx0, p.x);
@@ -213,6 +219,21 @@ __global__ void __launch_bounds__(T_BLOCK) k_rwmd_f32(TileArgs A) {
                     const float2 d = __ffma2_rn(dy, dy, __fmul2_rn(dx, dx));
                     m[r] = min3(m[r], d.x, d.y);
                 }
+            } else if (PACKQ) {
+                // two SOURCES per packed lane pair, each target broadcast: the target's
+                // operands are shared by every source pair (register reuse), the sources'
+                // pairs are (-2x_r, -2x_r+1)
+                const float2 tt = s_tt[j];
+#pragma unroll
+                for (int r = 0; r < R; r += 2) {
+                    const float2 qx = make_float2(ax[r].x, ax[r + 1].x), qy = make_float2(ay[r].x, ay[r + 1].x);
+                    const float2 sa = __ffma2_rn(qy, make_float2(v.z, v.z),
+                                                 __ffma2_rn(qx, make_float2(v.x, v.x), make_float2(tt.x, tt.x)));
+                    const float2 sb = __ffma2_rn(qy, make_float2(v.w, v.w),
+                                                 __ffma2_rn(qx, make_float2(v.y, v.y), make_float2(tt.y, tt.y)));
+                    m[r] = min3(m[r], sa.x, sb.x);
+                    m[r + 1] = min3(m[r + 1], sa.y, sb.y);
+                }
             } else {
                 const float2 tt = s_tt[j];
 #pragma unroll
@@ -241,6 +262,11 @@ __global__ void __launch_bounds__(T_BLOCK) k_rwmd_f32(TileArgs A) {
 #pragma unroll
     for (int r = 0; r < R; r++) {
         const int i = q0 + r * T_BLOCK + tid;
+        if (!CULL) {  // -2x and -2y are exact: x and y come back bit for bit
+            const float x = -0.5f * ax[r].x, y = -0.5f * ay[r].x;
+            qq[r] = fmaf(x, x, y * y);
+            qn[r] = sqrtf(qq[r]);
+        }
         if (i < A.nq) {
             const float est = CULL ? m[r] : fmaxf(m[r] + qq[r], 0.f);
             atomicMin(&A.mout[i], __float_as_uint(est));
@@ -278,6 +304,9 @@ __global__ void k_tile_boxes(const double2 *t, int nt, int T_TS, double4 *box) {
 // FP32 pass for one direction: sources q (nq, Morton order) against targets t
 // (nt, Morton order).  mout (float bits, pre-set to +huge) receives the
 // scaled squared-distance estimate, qn_out the local radius |q'|.
+template <int R>
+static int launch_full(Ctx &c, TileArgs &A, int64_t nq, int64_t nt);
+
 int rwmd_f32_min(Ctx &c, const double2 *q, const uint64_t *qkey, int64_t nq, const double2 *t,
                  const uint64_t *tkey, int64_t nt, double scale, unsigned *mout, float *qn_out, double4 *tbox,
                  int culling) {
@@ -322,22 +351,59 @@ int rwmd_f32_min(Ctx &c, const double2 *q, const uint64_t *qkey, int64_t nq, con
         if (c.prof) W1G_CUDA(cudaEventRecord(c.prof_ev[c.prof_side][0][1], c.stream));
         return W1G_OK;
     }
-    constexpr int R = 8;
+    static const int rfull = [] {  // W1G_TILE_RFULL=16: 16 sources per thread (tuning)
+        const char *e = getenv("W1G_TILE_RFULL");
+        return e && atoi(e) == 16 ? 16 : 8;
+    }();
+    if (rfull == 16) return launch_full<16>(c, A, nq, nt);
+    return launch_full<8>(c, A, nq, nt);
+}
+
+template <int R>
+static int launch_full(Ctx &c, TileArgs &A, int64_t nq, int64_t nt) {
     const int per_block = T_BLOCK * R;
     const int gx = (int)((nq + per_block - 1) / per_block);
-    // enough CTAs for several waves of the resident CTAs on every SM
-    const int want = 16 * c.sm_count;
-    int gy = (want + gx - 1) / gx;
-    const int64_t max_gy = (nt + TS_FULL - 1) / TS_FULL;
-    if (gy > max_gy) gy = (int)max_gy;
-    if (gy < 1) gy = 1;
-    if (gy > 65535) gy = 65535;
+    // the target range is split over grid.y so that the CTAs fill whole waves of the
+    // resident slots (occupancy x SMs): the smallest split giving at least two waves at
+    // >= 97 % wave efficiency (waves / ceil(waves)), else the most efficient split up to
+    // 64 chunks (round 2: a fixed 16 x SMs target gave 4.13 waves at 1M, 17 % idle tail)
+    static const bool packq = [] {  // W1G_TILE_PACKQ: sources packed in the FP32x2 lanes (1) or targets (0)
+        const char *e = getenv("W1G_TILE_PACKQ");
+        return !(e && atoi(e) == 0);
+    }();
+    void (*kern)(TileArgs) = packq ? k_rwmd_f32<R, false, TS_FULL, true> : k_rwmd_f32<R, false, TS_FULL, false>;
+    static const int occ = [kern] {
+        int o = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, T_BLOCK, 0) != cudaSuccess || o < 1) {
+            cudaGetLastError();
+            o = 1;
+        }
+        return o;
+    }();
+    const int64_t slots = (int64_t)occ * c.sm_count;
+    int64_t max_gy = (nt + TS_FULL - 1) / TS_FULL;
+    if (max_gy > 65535) max_gy = 65535;
+    if (max_gy < 1) max_gy = 1;
+    int gy = 1;
+    double best_eff = -1.0;
+    for (int y = 1; y <= max_gy && y <= 64; y++) {
+        const double waves = (double)gx * y / (double)slots;
+        const double eff = waves / std::ceil(waves);
+        if (waves >= 2.0 && eff >= 0.97) {
+            gy = y;
+            break;
+        }
+        if (eff > best_eff + 1e-9) {
+            best_eff = eff;
+            gy = y;
+        }
+    }
     int chunk = (int)((nt + gy - 1) / gy);
     chunk = (chunk + 1) & ~1;
     gy = (int)((nt + chunk - 1) / chunk);
     A.chunk = chunk;
     if (c.prof) W1G_CUDA(cudaEventRecord(c.prof_ev[c.prof_side][0][0], c.stream));
-    k_rwmd_f32<R, false, TS_FULL><<<dim3(gx, gy), T_BLOCK, 0, c.stream>>>(A);
+    kern<<<dim3(gx, gy), T_BLOCK, 0, c.stream>>>(A);
     W1G_CHECK_LAUNCH();
     if (c.prof) W1G_CUDA(cudaEventRecord(c.prof_ev[c.prof_side][0][1], c.stream));
     return W1G_OK;
