@@ -342,10 +342,6 @@ __global__ void __launch_bounds__(RF_BLOCK) k_refine(const double2 *__restrict__
     __shared__ double2 s_t[RF_STAGE * RT];
     __shared__ float4 s_tb32[RF_STAGE];
     __shared__ int s_nc, s_nsup;
-    __shared__ double s_r[RF_BLOCK / 32];
-    __shared__ double4 s_box[RF_BLOCK / 32];
-    __shared__ double4 s_qb;
-    __shared__ double s_rmax;
     __shared__ double2 s_p[RF_QPB];  // per-source point (solo searches)
     __shared__ float4 s_p32[RF_QPB]; // per-source point box and radius for the candidate
     __shared__ float s_rad32[RF_QPB];  // filter (FP32, conservative: within32)
@@ -403,54 +399,48 @@ __global__ void __launch_bounds__(RF_BLOCK) k_refine(const double2 *__restrict__
     if (tid == 0) s_nsup = s_nc = 0;
     double m2 = INFINITY, m2b = INFINITY;
     if (nt > 0) {
-        // block bbox and radius
-        double4 b = (valid && !heavy) ? make_double4(p.x, p.y, p.x, p.y)
-                                      : make_double4(INFINITY, INFINITY, -INFINITY, -INFINITY);
-        double rm = r;
+        // warp and block boxes and radii, in FP32 rounded outward: box_out32 and rad_up32
+        // are monotonic, so reducing the rounded per-source values gives exactly the
+        // rounding of the fp64 reduction (min of rounded-down = rounded-down min)
+        float4 b = (valid && !heavy) ? p32 : make_float4(INFINITY, INFINITY, -INFINITY, -INFINITY);
+        float rm = r_eval32;
         for (int o = 16; o; o >>= 1) {
-            b.x = fmin(b.x, __shfl_xor_sync(0xffffffffu, b.x, o));
-            b.y = fmin(b.y, __shfl_xor_sync(0xffffffffu, b.y, o));
-            b.z = fmax(b.z, __shfl_xor_sync(0xffffffffu, b.z, o));
-            b.w = fmax(b.w, __shfl_xor_sync(0xffffffffu, b.w, o));
-            rm = fmax(rm, __shfl_xor_sync(0xffffffffu, rm, o));
+            b.x = fminf(b.x, __shfl_xor_sync(0xffffffffu, b.x, o));
+            b.y = fminf(b.y, __shfl_xor_sync(0xffffffffu, b.y, o));
+            b.z = fmaxf(b.z, __shfl_xor_sync(0xffffffffu, b.z, o));
+            b.w = fmaxf(b.w, __shfl_xor_sync(0xffffffffu, b.w, o));
+            rm = fmaxf(rm, __shfl_xor_sync(0xffffffffu, rm, o));
         }
         if (lane == 0) {
-            s_box[wid] = b;
-            s_r[wid] = rm;
-            s_box32[wid] = box_out32(b);
-            s_r32[wid] = rad_up32(rm * (1.0 + 1e-9));
+            s_box32[wid] = b;
+            s_r32[wid] = rm;
         }
         __syncthreads();
         if (tid == 0) {
-            double4 bb = s_box[0];
-            double rr = s_r[0];
+            float4 bb = s_box32[0];
+            float rr = s_r32[0];
             for (int w = 1; w < RF_BLOCK / 32; w++) {
-                bb.x = fmin(bb.x, s_box[w].x);
-                bb.y = fmin(bb.y, s_box[w].y);
-                bb.z = fmax(bb.z, s_box[w].z);
-                bb.w = fmax(bb.w, s_box[w].w);
-                rr = fmax(rr, s_r[w]);
+                bb.x = fminf(bb.x, s_box32[w].x);
+                bb.y = fminf(bb.y, s_box32[w].y);
+                bb.z = fmaxf(bb.z, s_box32[w].z);
+                bb.w = fmaxf(bb.w, s_box32[w].w);
+                rr = fmaxf(rr, s_r32[w]);
             }
-            s_qb = bb;
-            s_rmax = rr * (1.0 + 1e-9);
-            s_qb32 = box_out32(bb);
-            s_rmax32 = rad_up32(rr * (1.0 + 1e-9));
+            s_qb32 = bb;
+            s_rmax32 = rr;
         }
         __syncthreads();
-        const double4 qb = s_qb;
-        const double rmax = s_rmax;
         const float4 qb32 = s_qb32;
         const float rmax32 = s_rmax32;
-        const double4 pb = make_double4(p.x, p.y, p.x, p.y);
         const int64_t ntile = (nt + RT - 1) / RT;
         const int64_t nsup = (ntile + SUP - 1) / SUP;
         constexpr int SUP_ROUND = RF_CAND / SUP;  // super-tiles per round: <= RF_CAND child tiles
         // two-level candidate search: the super-tiles meeting the block are
         // listed once, then their child tiles are tested SUP_ROUND super-tiles
-        // at a time (box tests in fp64 with slack)
+        // at a time (conservative FP32 box tests)
         for (int64_t sb = 0; sb < nsup; sb += RF_SUPCAP) {
           for (int64_t sp = sb + tid; sp < min(nsup, sb + RF_SUPCAP); sp += RF_BLOCK)
-            if (within(sbox[sp], qb, rmax)) s_sup[atomicAdd(&s_nsup, 1)] = (int32_t)sp;
+            if (within32(box_out32(sbox[sp]), qb32, rmax32)) s_sup[atomicAdd(&s_nsup, 1)] = (int32_t)sp;
           __syncthreads();
           const int n_sup = s_nsup;
           for (int u0 = 0; u0 < n_sup; u0 += SUP_ROUND) {
