@@ -179,9 +179,12 @@ __device__ __forceinline__ bool within(double4 b, double4 a, double R) {
 //   |est - D~^2| <= 5u (2|x| + D~)^2          (expanded form, FFMA/FFMA2)
 //   |D - D~|     <= u (2|x| + D~)              (one rounding per coordinate)
 // so with c = 2^-20 >= 5u:  D~ <= (sqrt(est) + 2 sqrt(c) |x|) / (1 - sqrt(c)).
+// (sqrt taken in FP32 rounded up -- >= the exact root of est -- and the division by
+// 1 - 2^-10 replaced by a multiplication by 1 + 2^-9 > 1 / (1 - 2^-10): both only raise
+// the bound, and no fp64 square root or division runs per source)
 __device__ __forceinline__ double upper_bound_expanded(float est, float qn) {
     const double x = (double)qn * (1.0 + 0x1p-20) + 0x1p-60;
-    const double dt = (sqrt(fmax((double)est, 0.0)) + 0x1p-9 * x) / (1.0 - 0x1p-10);
+    const double dt = ((double)__fsqrt_ru(fmaxf(est, 0.0f)) + 0x1p-9 * x) * (1.0 + 0x1p-9);
     return dt * (1.0 + 0x1p-20) + 0x1p-20 * x + 0x1p-40;
 }
 // The direct form (culled mode: dx = x - y, est = fl(dy^2 + fl(dx^2))) does
@@ -190,7 +193,7 @@ __device__ __forceinline__ double upper_bound_expanded(float est, float qn) {
 //   D <= (sqrt(est)(1 + 1.01u)/(1 - u) + 2u|x|(1 + 3u)) / (1 - u);
 // 2^-20 = 16u covers every factor.
 __device__ __forceinline__ double upper_bound_direct(float est, float qn) {
-    return (sqrt(fmax((double)est, 0.0)) * (1.0 + 0x1p-20) + 0x1p-20 * (double)qn) * (1.0 + 0x1p-20) + 0x1p-60;
+    return ((double)__fsqrt_ru(fmaxf(est, 0.0f)) * (1.0 + 0x1p-20) + 0x1p-20 * (double)qn) * (1.0 + 0x1p-20) + 0x1p-60;
 }
 __device__ __forceinline__ double upper_bound(float est, float qn, int direct) {
     return direct ? upper_bound_direct(est, qn) : upper_bound_expanded(est, qn);
