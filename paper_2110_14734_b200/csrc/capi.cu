@@ -983,6 +983,31 @@ static void fill_tails(Ctx &c, int64_t *t, const int64_t *ro, int64_t n, int64_t
     });
 }
 
+// pageable inputs into the page-locked staging buffer: the byte range [a | b] split over
+// the fill threads (non-temporal stores), for inputs of a megabyte and more outside a batch
+// (whose workers already run one per core)
+static void stage_inputs(Ctx &c, char *dst, const char *a, size_t abytes, const char *b, size_t bbytes) {
+    const size_t bytes = abytes + bbytes;
+    if (bytes < ((size_t)1 << 20) || c.coop_share > 1) {
+        if (abytes) host_copy_nt(dst, a, abytes);
+        if (bbytes) host_copy_nt(dst + abytes, b, bbytes);
+        return;
+    }
+    if (!c.fill_pool) {
+        c.fill_pool = new FillPool();
+        c.fill_pool->start(3);
+    }
+    const int parts = 4;
+    c.fill_pool->run(parts, [&](int p) {
+        const size_t lo = (bytes * p / parts) & ~(size_t)63, hi = p + 1 == parts ? bytes : (bytes * (p + 1) / parts) & ~(size_t)63;
+        if (lo < abytes) host_copy_nt(dst + lo, a + lo, (hi < abytes ? hi : abytes) - lo);
+        if (hi > abytes) {
+            const size_t b0 = lo > abytes ? lo - abytes : 0, b1 = hi - abytes;
+            host_copy_nt(dst + abytes + b0, b + b0, b1 - b0);
+        }
+    });
+}
+
 static int copy_network_out(Ctx &c, int *copied) {
     *copied = 0;
     const Ctx::NetOut &o = c.net_out;
@@ -1400,8 +1425,8 @@ int w1g_front_end(w1g_ctx *c, const double *a, int64_t na, const double *b, int6
         // pageable inputs: stage both diagrams through pinned memory, one full-speed H2D
         W1G_TRY(stage_ensure(*c, bytes));
         W1G_TRY(stream_sync(*c));
-        if (na) host_copy_nt(c->h_stage, a, sizeof(double2) * na);
-        if (nb) host_copy_nt(static_cast<char *>(c->h_stage) + sizeof(double2) * na, b, sizeof(double2) * nb);
+        stage_inputs(*c, static_cast<char *>(c->h_stage), reinterpret_cast<const char *>(a), sizeof(double2) * na,
+                     reinterpret_cast<const char *>(b), sizeof(double2) * nb);
         if (bytes) W1G_CUDA(cudaMemcpyAsync(d, c->h_stage, bytes, cudaMemcpyHostToDevice, c->stream));
     }
     return w1g_front_end_device(c, reinterpret_cast<double *>(d), na,

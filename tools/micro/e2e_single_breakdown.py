@@ -1,5 +1,8 @@
 """Where the single-pair end-to-end time goes: sparsify() wall time vs the device
-makespan of its front end, and the cost of the Python wrapper around the C call."""
+makespan of its front end, and the cost of the Python wrapper around the C call.
+
+    python tools/micro/e2e_single_breakdown.py [pageable]
+"""
 import sys
 import time
 
@@ -11,7 +14,8 @@ from paper_2110_14734_b200 import _lib, synth  # noqa: E402
 from paper_2110_14734_b200.pipeline import _front_end  # noqa: E402
 
 a, b = synth.gaussian_cluster_pair(100_000, 100_000, seed=0)
-a, b = w1g.pinned_points(a), w1g.pinned_points(b)
+if "pageable" not in sys.argv:
+    a, b = w1g.pinned_points(a), w1g.pinned_points(b)
 p = w1g.ApproxParams(s=1.0, best_effort=True, delta=0.01)
 for _ in range(5):
     w1g.sparsify(a, b, p)
