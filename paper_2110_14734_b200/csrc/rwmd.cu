@@ -24,7 +24,7 @@ namespace w1g {
 
 int rwmd_f32_min(Ctx &c, const double2 *q, const uint64_t *qkey, int64_t nq, const double2 *t,
                  const uint64_t *tkey, int64_t nt, double scale,
-                 unsigned *mout, float *qn_out, double4 *tbox, int culling);
+                 unsigned *mout, float *qn_out, double4 *tbox, int culling, int tbox_ready = 0);
 int pairwise_sum(Ctx &c, const double *d_v, int64_t n, double *d_out, DevBuf &nodes_buf,
                  DevBuf &val_buf, DevBuf &lev_buf, int64_t *cached_n = nullptr);
 
@@ -39,10 +39,15 @@ struct MemberFlag {
     __device__ int64_t operator()(int64_t i) const { return mass[i] > 0 ? 1 : 0; }
 };
 
-__global__ void k_compact(const int64_t *mass, int64_t k, const int64_t *excl, int32_t *out) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < k;
-         i += (int64_t)gridDim.x * blockDim.x)
-        if (mass[i] > 0) out[excl[i]] = (int32_t)i;
+// both sides' member lists in one launch (after both sides' scans)
+__global__ void k_compact2(const int64_t *mass0, const int64_t *mass1, int64_t k, const int64_t *excl0,
+                           const int64_t *excl1, int32_t *out0, int32_t *out1) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < 2 * k;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const bool b = i >= k;
+        const int64_t j = b ? i - k : i;
+        if ((b ? mass1 : mass0)[j] > 0) (b ? out1 : out0)[(b ? excl1 : excl0)[j]] = (int32_t)j;
+    }
 }
 
 __global__ void k_bbox_init(int64_t *f) {
@@ -92,26 +97,45 @@ __device__ __forceinline__ uint32_t spread16(uint32_t v) {
 // radix passes; a finer grid buys nothing at 64-target tiles); payload = member position
 constexpr double MORTON_MAX = 4095.0;
 constexpr int MORTON_BITS = 24;
-__global__ void k_morton(const double2 *pts, const int32_t *members, int64_t n, double x0, double y0,
-                         double inv, uint64_t *key, uint32_t *val) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const double2 p = pts[members[i]];
+// Morton keys of both sides in one launch
+struct Morton2 {
+    const int32_t *members[2];
+    int64_t n[2];
+    uint64_t *key[2];
+    uint32_t *val[2];
+};
+__global__ void k_morton2(const double2 *pts, Morton2 M, double x0, double y0, double inv) {
+    const int64_t tot = M.n[0] + M.n[1];
+    for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < tot;
+         g += (int64_t)gridDim.x * blockDim.x) {
+        const int s = g >= M.n[0];
+        const int64_t i = s ? g - M.n[0] : g;
+        const double2 p = pts[M.members[s][i]];
         double fx = (p.x - x0) * inv, fy = (p.y - y0) * inv;
         fx = fx < 0 ? 0 : (fx > MORTON_MAX ? MORTON_MAX : fx);
         fy = fy < 0 ? 0 : (fy > MORTON_MAX ? MORTON_MAX : fy);
-        key[i] = (uint64_t)(spread16((uint32_t)fx) | (spread16((uint32_t)fy) << 1));
-        val[i] = (uint32_t)i;
+        M.key[s][i] = (uint64_t)(spread16((uint32_t)fx) | (spread16((uint32_t)fy) << 1));
+        M.val[s][i] = (uint32_t)i;
     }
 }
 
-__global__ void k_gather_members(const double2 *pts, const int32_t *members, const uint32_t *perm,
-                                  int64_t n, int64_t offset, double2 *out, int32_t *pos) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const uint32_t m = perm[i];
-        out[i] = pts[members[m]];
-        pos[i] = (int32_t)(m + offset);
+// both sides' Morton-ordered member points in one launch
+struct Gather2 {
+    const int32_t *members[2];
+    const uint32_t *perm[2];
+    int64_t n[2], offset[2];
+    double2 *out[2];
+    int32_t *pos[2];
+};
+__global__ void k_gather2(const double2 *pts, Gather2 G) {
+    const int64_t tot = G.n[0] + G.n[1];
+    for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < tot;
+         g += (int64_t)gridDim.x * blockDim.x) {
+        const int s = g >= G.n[0];
+        const int64_t i = s ? g - G.n[0] : g;
+        const uint32_t m = G.perm[s][i];
+        G.out[s][i] = pts[G.members[s][m]];
+        G.pos[s][i] = (int32_t)(m + G.offset[s]);
     }
 }
 
@@ -161,6 +185,85 @@ __global__ void k_superboxes(const double4 *box, int64_t ntile, double4 *sbox) {
             y1 = fmax(y1, __shfl_xor_sync(0xffffffffu, y1, o));
         }
         if (lane == 0) sbox[sp] = make_double4(x0, y0, x1, y1);
+    }
+}
+
+
+// the targets' boxes for both sides in one launch: a 128-thread block per 256-target tile (the
+// culled FP32 pass's tile, TS_CULL in rwmd_tile.cu), one warp per 64-target refine tile inside it;
+// min / max are order-independent, so the boxes equal k_tile_boxes' and k_boxes64's
+struct SideBoxes {
+    const double2 *t[2];  // side s's targets
+    int64_t n[2];
+    int64_t nblk0;        // 256-target tiles of side 0
+    double4 *tbox[2], *box64[2], *sbox[2];
+};
+__global__ void __launch_bounds__(128) k_side_boxes(SideBoxes A) {
+    __shared__ double4 s_b[4];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int s = (int64_t)blockIdx.x >= A.nblk0;
+    const int64_t ct = s ? (int64_t)blockIdx.x - A.nblk0 : (int64_t)blockIdx.x;
+    const int64_t nt = A.n[s];
+    const int64_t k = ct * 4 + w, j0 = k * RT, je = min(nt, j0 + RT);
+    double x0 = INFINITY, y0 = INFINITY, x1 = -INFINITY, y1 = -INFINITY;
+    for (int64_t j = j0 + lane; j < je; j += 32) {
+        const double2 p = A.t[s][j];
+        x0 = fmin(x0, p.x);
+        y0 = fmin(y0, p.y);
+        x1 = fmax(x1, p.x);
+        y1 = fmax(y1, p.y);
+    }
+    for (int o = 16; o; o >>= 1) {
+        x0 = fmin(x0, __shfl_xor_sync(0xffffffffu, x0, o));
+        y0 = fmin(y0, __shfl_xor_sync(0xffffffffu, y0, o));
+        x1 = fmax(x1, __shfl_xor_sync(0xffffffffu, x1, o));
+        y1 = fmax(y1, __shfl_xor_sync(0xffffffffu, y1, o));
+    }
+    if (lane == 0) {
+        s_b[w] = make_double4(x0, y0, x1, y1);
+        if (j0 < nt) A.box64[s][k] = s_b[w];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double4 b = s_b[0];
+        for (int q = 1; q < 4; q++) {
+            b.x = fmin(b.x, s_b[q].x);
+            b.y = fmin(b.y, s_b[q].y);
+            b.z = fmax(b.z, s_b[q].z);
+            b.w = fmax(b.w, s_b[q].w);
+        }
+        A.tbox[s][ct] = b;
+    }
+}
+
+// both sides' super-tile boxes in one launch (a warp per super-tile, as k_superboxes)
+__global__ void k_side_superboxes(SideBoxes A) {
+    const int lane = threadIdx.x & 31;
+    int64_t ntile[2], nsup[2];
+    for (int q = 0; q < 2; q++) {
+        ntile[q] = (A.n[q] + RT - 1) / RT;
+        nsup[q] = (ntile[q] + SUP - 1) / SUP;
+    }
+    for (int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; g < nsup[0] + nsup[1];
+         g += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int s = g >= nsup[0];
+        const int64_t sp = s ? g - nsup[0] : g;
+        const double4 *box = A.box64[s];
+        double x0 = INFINITY, y0 = INFINITY, x1 = -INFINITY, y1 = -INFINITY;
+        for (int64_t k = sp * SUP + lane; k < min(ntile[s], (sp + 1) * SUP); k += 32) {
+            const double4 b = box[k];
+            x0 = fmin(x0, b.x);
+            y0 = fmin(y0, b.y);
+            x1 = fmax(x1, b.z);
+            y1 = fmax(y1, b.w);
+        }
+        for (int o = 16; o; o >>= 1) {
+            x0 = fmin(x0, __shfl_xor_sync(0xffffffffu, x0, o));
+            y0 = fmin(y0, __shfl_xor_sync(0xffffffffu, y0, o));
+            x1 = fmax(x1, __shfl_xor_sync(0xffffffffu, x1, o));
+            y1 = fmax(y1, __shfl_xor_sync(0xffffffffu, y1, o));
+        }
+        if (lane == 0) A.sbox[s][sp] = make_double4(x0, y0, x1, y1);
     }
 }
 
@@ -601,16 +704,14 @@ static int rwmd_prepare(Ctx &c, RwmdFrame &F, int range_side = -1, int64_t begin
     const double2 *pts = ptr<double2>(ns.pts);
     const int64_t *mass[2] = {ptr<int64_t>(ns.am), ptr<int64_t>(ns.bm)};
     int64_t *excl;
-    W1G_TRY(ensure(c.scr[3], k, &excl));
+    W1G_TRY(ensure(c.scr[3], 2 * (size_t)k, &excl));
     W1G_TRY(ensure(c.scr[5], k, &F.members[0]));
     W1G_TRY(ensure(c.scr[6], k, &F.members[1]));
     W1G_TRY(flags_reset(c));
-    const unsigned g = grid_for(k, 256, 8u * c.sm_count);
-    for (int s = 0; s < 2; s++) {
-        W1G_TRY(scan_i64(c, MemberFlag{mass[s]}, k, excl, dflags(c) + F_MISC0 + s));
-        k_compact<<<g, 256, 0, c.stream>>>(mass[s], k, excl, F.members[s]);
-        W1G_CHECK_LAUNCH();
-    }
+    for (int s = 0; s < 2; s++) W1G_TRY(scan_i64(c, MemberFlag{mass[s]}, k, excl + s * k, dflags(c) + F_MISC0 + s));
+    k_compact2<<<grid_for(2 * k, 256, 8u * c.sm_count), 256, 0, c.stream>>>(mass[0], mass[1], k, excl, excl + k,
+                                                                            F.members[0], F.members[1]);
+    W1G_CHECK_LAUNCH();
     uint64_t bk[4];
     if (ns.stats && range_side < 0) {
         // zero_condense delivered the member counts and the bbox: no round trip here
@@ -642,6 +743,7 @@ static int rwmd_prepare(Ctx &c, RwmdFrame &F, int range_side = -1, int64_t begin
     const double inv = MORTON_MAX / ext;
     SortJob jobs[2];
     int64_t off[2];
+    Morton2 M;
     for (int s = 0; s < 2; s++) {
         off[s] = s == range_side ? begin : 0;
         const int64_t n = s == range_side ? end - begin : F.nm[s];
@@ -653,17 +755,28 @@ static int rwmd_prepare(Ctx &c, RwmdFrame &F, int range_side = -1, int64_t begin
         W1G_TRY(ensure(c.scr[8 + 2 * s], (size_t)n + 1, &F.mpos[s]));
         F.mkey[s] = key;
         jobs[s] = SortJob{{key, nullptr, nullptr}, perm, n};
-        if (n == 0) continue;
-        k_morton<<<grid_for(n, 256, 8u * c.sm_count), 256, 0, c.stream>>>(pts, F.members[s] + off[s], n, xmin, ymin,
-                                                                          inv, key, perm);
+        M.members[s] = F.members[s] + off[s];
+        M.n[s] = n;
+        M.key[s] = key;
+        M.val[s] = perm;
+    }
+    // both sides' keys, sorts and gathers in the same launches
+    if (M.n[0] + M.n[1] > 0) {
+        k_morton2<<<grid_for(M.n[0] + M.n[1], 256, 8u * c.sm_count), 256, 0, c.stream>>>(pts, M, xmin, ymin, inv);
         W1G_CHECK_LAUNCH();
     }
-    W1G_TRY(radix_sort_multi(c, jobs, 2, 1, MORTON_BITS));  // both sides in the same launches
+    W1G_TRY(radix_sort_multi(c, jobs, 2, 1, MORTON_BITS));
+    Gather2 G;
     for (int s = 0; s < 2; s++) {
-        const int64_t n = jobs[s].n;
-        if (n == 0) continue;
-        k_gather_members<<<grid_for(n, 256, 8u * c.sm_count), 256, 0, c.stream>>>(
-            pts, F.members[s] + off[s], jobs[s].vals, n, off[s], F.mpts[s], F.mpos[s]);
+        G.members[s] = M.members[s];
+        G.perm[s] = jobs[s].vals;
+        G.n[s] = jobs[s].n;
+        G.offset[s] = off[s];
+        G.out[s] = F.mpts[s];
+        G.pos[s] = F.mpos[s];
+    }
+    if (G.n[0] + G.n[1] > 0) {
+        k_gather2<<<grid_for(G.n[0] + G.n[1], 256, 8u * c.sm_count), 256, 0, c.stream>>>(pts, G);
         W1G_CHECK_LAUNCH();
     }
     return W1G_OK;
@@ -721,15 +834,8 @@ int rwmd_run(Ctx &c, double *L, double *LA, double *LB) {
         if (n_dst > 0) {
             W1G_CUDA(cudaMemsetAsync(mf_s, 0x7f, sizeof(unsigned) * n_src, c.stream));
             W1G_TRY(rwmd_f32_min(c, F.mpts[s], F.mkey[s], n_src, F.mpts[o], F.mkey[o], n_dst, F.scale, mf_s, qn_s,
-                                 tbox_s, c.culling));
+                                 tbox_s, c.culling, c.culling ? 1 : 0));
             T.mark(s ? "f32_b" : "f32_a");
-            k_boxes64<<<grid_for((n_dst / RT + 1) * 32, 256, 8u * c.sm_count), 256, 0, c.stream>>>(F.mpts[o], n_dst,
-                                                                                                    box64_s);
-            W1G_CHECK_LAUNCH();
-            k_superboxes<<<grid_for((n_dst / RT / SUP + 1) * 32, 256, 8u * c.sm_count), 256, 0, c.stream>>>(
-                box64_s, (n_dst + RT - 1) / RT, sbox_s);
-            W1G_CHECK_LAUNCH();
-            T.mark("boxes");
         }
         W1G_TRY(launch_refine(c, F.mpts[s], F.mpos[s], F.members[s], mass[s], n_src, mf_s, qn_s, F.unscale,
                               F.mpts[o], n_dst, box64_s, sbox_s, best, terms_s));
@@ -739,6 +845,29 @@ int rwmd_run(Ctx &c, double *L, double *LA, double *LB) {
         T.mark("sum");
         return W1G_OK;
     };
+    // every tile / refine-tile / super-tile box of both sides' targets, before the sides fork
+    {
+        SideBoxes B;
+        for (int s = 0; s < 2; s++) {
+            const int o = 1 - s;
+            const bool on = F.nm[s] > 0 && F.nm[o] > 0;
+            B.t[s] = F.mpts[o];
+            B.n[s] = on ? F.nm[o] : 0;
+            B.tbox[s] = tbox + s * mtb;
+            B.box64[s] = box64 + s * mtb;
+            B.sbox[s] = sbox + s * msb;
+        }
+        B.nblk0 = (B.n[0] + 4 * RT - 1) / (4 * RT);
+        const int64_t nblk = B.nblk0 + (B.n[1] + 4 * RT - 1) / (4 * RT);
+        if (nblk > 0) {
+            k_side_boxes<<<(unsigned)nblk, 128, 0, c.stream>>>(B);
+            W1G_CHECK_LAUNCH();
+            const int64_t nsup = (B.n[0] + RT * SUP - 1) / (RT * SUP) + (B.n[1] + RT * SUP - 1) / (RT * SUP);
+            k_side_superboxes<<<grid_for(nsup * 32, 256, 8u * c.sm_count), 256, 0, c.stream>>>(B);
+            W1G_CHECK_LAUNCH();
+        }
+        T.mark("boxes");
+    }
     if (conc) {
         W1G_CUDA(cudaEventRecord(c.ev[14], c.stream));
         W1G_CUDA(cudaStreamWaitEvent(side, c.ev[14], 0));

@@ -309,7 +309,7 @@ static int launch_full(Ctx &c, TileArgs &A, int64_t nq, int64_t nt);
 
 int rwmd_f32_min(Ctx &c, const double2 *q, const uint64_t *qkey, int64_t nq, const double2 *t,
                  const uint64_t *tkey, int64_t nt, double scale, unsigned *mout, float *qn_out, double4 *tbox,
-                 int culling) {
+                 int culling, int tbox_ready) {
     if (nq == 0 || nt == 0) return W1G_OK;
     TileArgs A;
     A.q = q;
@@ -329,9 +329,14 @@ int rwmd_f32_min(Ctx &c, const double2 *q, const uint64_t *qkey, int64_t nq, con
     // with a poor seed are caught by the exact pass's heavy-source path)
     A.cull_steps = c.cull_steps > 0 ? c.cull_steps : 3;
     if (culling) {
-        const int ntile = (int)((nt + TS_CULL - 1) / TS_CULL);
-        k_tile_boxes<<<grid_for((int64_t)ntile * 32, 256, 8u * c.sm_count), 256, 0, c.stream>>>(t, (int)nt, TS_CULL, tbox);
-        W1G_CHECK_LAUNCH();
+        // (the caller may have computed the tile boxes already: rwmd.cu k_side_boxes, 4 x 64 = TS_CULL)
+        static_assert(TS_CULL == 256, "k_side_boxes builds 256-target tile boxes");
+        if (!tbox_ready) {
+            const int ntile = (int)((nt + TS_CULL - 1) / TS_CULL);
+            k_tile_boxes<<<grid_for((int64_t)ntile * 32, 256, 8u * c.sm_count), 256, 0, c.stream>>>(t, (int)nt, TS_CULL,
+                                                                                                   tbox);
+            W1G_CHECK_LAUNCH();
+        }
         // sources per thread: 1 below ~300k sources (twice the CTAs of R = 2 for a short,
         // latency-bound kernel), 2 above; W1G_TILE_R overrides (tuning).  Any R is exact:
         // the seed only sizes the exact pass's search (rwmd.cu)
