@@ -816,7 +816,9 @@ int rwmd_run(Ctx &c, double *L, double *LA, double *LB) {
     // side B on the side stream, concurrently with side A, once its summation tree is cached
     // (nothing left to allocate inside)
     cudaStream_t side = c.copy_stream;
-    const bool conc = side && F.nm[0] > 0 && F.nm[1] > 0 && c.pw_n[1] == F.nm[1];
+    // (per-kernel profiling, w1g_profile_rwmd, runs the sides one after the other so each
+    // kernel's event time is its own)
+    const bool conc = side && !c.prof && F.nm[0] > 0 && F.nm[1] > 0 && c.pw_n[1] == F.nm[1];
     auto run_side = [&](int s) -> int {
         const int o = 1 - s;
         c.prof_side = s;
