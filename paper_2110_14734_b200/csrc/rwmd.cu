@@ -267,13 +267,6 @@ __global__ void k_side_superboxes(SideBoxes A) {
     }
 }
 
-// is box b within distance R of box a?  (squared compare: no sqrt on the hot path;
-// R carries the caller's relative slack, a negative R matches nothing)
-__device__ __forceinline__ bool within(double4 b, double4 a, double R) {
-    const double gx = fmax(0.0, fmax(b.x - a.z, a.x - b.z));
-    const double gy = fmax(0.0, fmax(b.y - a.w, a.y - b.w));
-    return R >= 0.0 && gx * gx + gy * gy <= R * R;
-}
 
 // Rigorous upper bound (scaled units) on the distance from a source to the
 // target that produced its FP32 estimate `est` in the local frame of
@@ -303,8 +296,9 @@ __device__ __forceinline__ double upper_bound(float est, float qn, int direct) {
 }
 
 
-// FP32 twin of within() for the refine's filters: true whenever within(b, a, R) is (it
-// never drops a tile the fp64 test keeps -- extra exact distances cannot change a min):
+// Is box b within distance R of box a, conservatively in FP32 (the refine's filters): true
+// whenever the exact fp64 test gx^2 + gy^2 <= R^2 is (it never drops a tile that test keeps --
+// extra exact distances cannot change a min):
 // boxes rounded outward, gaps and squares rounded down, the radius (carrying 2^-40 of
 // relative slack over fp64's own rounding) rounded up.  Overflow and NaN only widen it
 // (fmaxf drops a NaN gap to 0; an infinite radius keeps everything).
