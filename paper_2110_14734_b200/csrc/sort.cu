@@ -32,9 +32,17 @@ struct KeyPtrs {
     uint64_t *k[4];
 };
 
-__global__ void __launch_bounds__(512) k_rs_hist_all(KeyPtrs kp, int words, int64_t n,
-                                                     uint32_t *hist) {
+// digit histograms of every word of up to two jobs (blockIdx.y = job) in one launch
+struct HistArgs {
+    KeyPtrs kp[2];
+    int64_t n[2];
+    uint32_t *hist[2];
+};
+__global__ void __launch_bounds__(512) k_rs_hist_all(HistArgs H, int words) {
     extern __shared__ uint32_t sh[];  // words*8*256
+    const KeyPtrs kp = H.kp[blockIdx.y];
+    const int64_t n = H.n[blockIdx.y];
+    uint32_t *hist = H.hist[blockIdx.y];
     const int nb = words * 8 * 256;
     for (int i = threadIdx.x; i < nb; i += blockDim.x) sh[i] = 0;
     __syncthreads();
@@ -267,9 +275,24 @@ __global__ void __launch_bounds__(1024) k_rs_plan(const __grid_constant__ PlanAr
 }
 
 // result in the b buffers (odd number of passes): copy payload and top key word back
-__global__ void k_rs_fixup(const int8_t *final_par, const uint32_t *vb, uint32_t *va, const uint64_t *kb,
-                           uint64_t *ka, int64_t n) {
-    if (*final_par == 0) return;
+// the sorted data back into the caller's buffers when the last pass left it in the scratch
+// ones, for up to two jobs (blockIdx.y = job) in one launch
+struct FixupArgs {
+    const int8_t *final_par[2];
+    const uint32_t *vb[2];
+    uint32_t *va[2];
+    const uint64_t *kb[2];
+    uint64_t *ka[2];
+    int64_t n[2];
+};
+__global__ void k_rs_fixup(FixupArgs F) {
+    const int q = blockIdx.y;
+    if (*F.final_par[q] == 0) return;
+    const uint32_t *vb = F.vb[q];
+    uint32_t *va = F.va[q];
+    const uint64_t *kb = F.kb[q];
+    uint64_t *ka = F.ka[q];
+    const int64_t n = F.n[q];
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         va[i] = vb[i];
@@ -357,16 +380,23 @@ int radix_sort_multi(Ctx &c, const SortJob *jobs, int njobs, int words, int top_
     P.words = words;
     P.top_bits = top_bits;
     P.plan = plan;
+    HistArgs H;
+    int64_t nmax = 0;
     for (int j = 0; j < nj; j++) {
         W1G_CUDA(cudaMemsetAsync(hist[j], 0, sizeof(uint32_t) * nh, c.stream));
-        unsigned g = grid_for(J[j]->n, 512, 2u * c.sm_count);
-        size_t sm = sizeof(uint32_t) * nh;
-        if (sm > 48 * 1024)
-            W1G_CUDA(cudaFuncSetAttribute(k_rs_hist_all, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-        k_rs_hist_all<<<g, 512, sm, c.stream>>>(a[j], words, J[j]->n, hist[j]);
-        W1G_CHECK_LAUNCH();
+        H.kp[j] = a[j];
+        H.n[j] = J[j]->n;
+        H.hist[j] = hist[j];
+        nmax = J[j]->n > nmax ? J[j]->n : nmax;
         P.hist[j] = hist[j];
         P.n[j] = J[j]->n;
+    }
+    {
+        const size_t sm = sizeof(uint32_t) * nh;
+        if (sm > 48 * 1024)
+            W1G_CUDA(cudaFuncSetAttribute(k_rs_hist_all, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        k_rs_hist_all<<<dim3(grid_for(nmax, 512, 2u * c.sm_count), nj), 512, sm, c.stream>>>(H, words);
+        W1G_CHECK_LAUNCH();
     }
     k_rs_plan<<<1, 1024, 0, c.stream>>>(P);
     W1G_CHECK_LAUNCH();
@@ -408,11 +438,17 @@ int radix_sort_multi(Ctx &c, const SortJob *jobs, int njobs, int words, int top_
         // large inputs: 8192-key tiles when the staged words fit in shared memory
         W1G_TRY(dispatch_pass(words, words - w, c, A, large && words - w <= 2));
     }
+    FixupArgs X;
     for (int j = 0; j < nj; j++) {
-        k_rs_fixup<<<grid_for(J[j]->n, 256, 8u * c.sm_count), 256, 0, c.stream>>>(
-            plan + j * RS_PLAN + 32, vb[j], J[j]->vals, b[j].k[words - 1], J[j]->keys[words - 1], J[j]->n);
-        W1G_CHECK_LAUNCH();
+        X.final_par[j] = plan + j * RS_PLAN + 32;
+        X.vb[j] = vb[j];
+        X.va[j] = J[j]->vals;
+        X.kb[j] = b[j].k[words - 1];
+        X.ka[j] = J[j]->keys[words - 1];
+        X.n[j] = J[j]->n;
     }
+    k_rs_fixup<<<dim3(grid_for(nmax, 256, 8u * c.sm_count), nj), 256, 0, c.stream>>>(X);
+    W1G_CHECK_LAUNCH();
     return W1G_OK;
 }
 
