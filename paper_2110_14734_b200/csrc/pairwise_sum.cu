@@ -83,12 +83,17 @@ __global__ void __launch_bounds__(1024) k_pw_build(int64_t n, PwNode *nodes, int
         if (threadIdx.x == 0) levels[L + 1] = hi;
         __syncthreads();
     }
-    if (threadIdx.x == 0) *n_levels = L;
+    if (threadIdx.x == 0) {
+        *n_levels = L;
+        n_levels[1] = 0;  // the leaves kernel's block ticket (k_pw_sum)
+    }
 }
 
-// one warp per leaf: numpy's 8-accumulator block (n <= 128) or sequential (n < 8)
-__global__ void k_pw_leaves(const double *v, const PwNode *nodes, const int32_t *levels,
-                            const int32_t *n_levels, double *val) {
+// one warp per leaf: numpy's 8-accumulator block (n <= 128) or sequential (n < 8); the
+// last block to finish then combines the internal nodes level by level (bottom-up, the
+// tree order numpy's recursion adds in) and writes the sum: one launch
+__global__ void __launch_bounds__(256) k_pw_sum(const double *v, const PwNode *nodes, const int32_t *levels,
+                                                int32_t *n_levels, double *val, double *out) {
     const int total = levels[*n_levels];
     const int lane = threadIdx.x & 31;
     for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < total;
@@ -120,20 +125,30 @@ __global__ void k_pw_leaves(const double *v, const PwNode *nodes, const int32_t 
             val[i] = res;
         }
     }
-}
-
-__global__ void __launch_bounds__(1024) k_pw_combine(const PwNode *nodes, const int32_t *levels,
-                                                     const int32_t *n_levels, double *val,
-                                                     double *out) {
+    // the last block to arrive combines (the other blocks' leaf sums read from L2)
+    __shared__ bool s_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const int t = atomicAdd(&n_levels[1], 1);
+        s_last = t == (int)gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
     const int L = *n_levels;
     for (int l = L - 1; l >= 0; l--) {
         for (int i = levels[l] + threadIdx.x; i < levels[l + 1]; i += blockDim.x) {
             const int ch = nodes[i].child;
-            if (ch >= 0) val[i] = dadd(val[ch], val[ch + 1]);
+            if (ch >= 0) val[i] = dadd(__ldcg(&val[ch]), __ldcg(&val[ch + 1]));
         }
+        __threadfence();
         __syncthreads();
     }
-    if (threadIdx.x == 0) *out = val[0];
+    if (threadIdx.x == 0) {
+        *out = __ldcg(&val[0]);
+        n_levels[1] = 0;  // ready for the next sum over this tree
+    }
 }
 
 }  // namespace
@@ -151,7 +166,7 @@ int pairwise_sum(Ctx &c, const double *d_v, int64_t n, double *d_out, DevBuf &no
     int32_t *lev;
     W1G_TRY(ensure(nodes_buf, (size_t)cap, &nodes));
     W1G_TRY(ensure(val_buf, (size_t)cap, &val));
-    W1G_TRY(ensure(lev_buf, PW_MAX_LEVELS + 2, &lev));
+    W1G_TRY(ensure(lev_buf, PW_MAX_LEVELS + 2, &lev));  // levels, their count, the block ticket
     // the tree is a function of n alone: kept across calls when the caller owns the buffers
     if (!cached_n || *cached_n != n) {
         k_pw_build<<<1, 1024, 0, c.stream>>>(n, nodes, lev, lev + PW_MAX_LEVELS);
@@ -159,9 +174,8 @@ int pairwise_sum(Ctx &c, const double *d_v, int64_t n, double *d_out, DevBuf &no
         if (cached_n) *cached_n = n;
     }
     const unsigned warps = (unsigned)(n / 64 + 2);
-    k_pw_leaves<<<grid_for(warps * 32, 256, 4u * c.sm_count), 256, 0, c.stream>>>(d_v, nodes, lev, lev + PW_MAX_LEVELS, val);
-    W1G_CHECK_LAUNCH();
-    k_pw_combine<<<1, 1024, 0, c.stream>>>(nodes, lev, lev + PW_MAX_LEVELS, val, d_out);
+    k_pw_sum<<<grid_for(warps * 32, 256, 4u * c.sm_count), 256, 0, c.stream>>>(d_v, nodes, lev, lev + PW_MAX_LEVELS,
+                                                                               val, d_out);
     W1G_CHECK_LAUNCH();
     return W1G_OK;
 }
