@@ -93,7 +93,8 @@ __global__ void __launch_bounds__(1024) k_pw_build(int64_t n, PwNode *nodes, int
 // last block to finish then combines the internal nodes level by level (bottom-up, the
 // tree order numpy's recursion adds in) and writes the sum: one launch
 __global__ void __launch_bounds__(256) k_pw_sum(const double *v, const PwNode *nodes, const int32_t *levels,
-                                                int32_t *n_levels, double *val, double *out) {
+                                                int32_t *n_levels, double *val, double *out,
+                                                volatile double *h_out) {
     const int total = levels[*n_levels];
     const int lane = threadIdx.x & 31;
     for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < total;
@@ -146,7 +147,9 @@ __global__ void __launch_bounds__(256) k_pw_sum(const double *v, const PwNode *n
         __syncthreads();
     }
     if (threadIdx.x == 0) {
-        *out = __ldcg(&val[0]);
+        const double r = __ldcg(&val[0]);
+        *out = r;
+        if (h_out) *h_out = r;
         n_levels[1] = 0;  // ready for the next sum over this tree
     }
 }
@@ -154,9 +157,11 @@ __global__ void __launch_bounds__(256) k_pw_sum(const double *v, const PwNode *n
 }  // namespace
 
 // np.sum of a contiguous float64 vector on device -> *d_out (device)
+// (h_out, optional: page-locked host memory the sum is also written to, by the same kernel)
 int pairwise_sum(Ctx &c, const double *d_v, int64_t n, double *d_out, DevBuf &nodes_buf,
-                 DevBuf &val_buf, DevBuf &lev_buf, int64_t *cached_n) {
+                 DevBuf &val_buf, DevBuf &lev_buf, int64_t *cached_n, double *h_out) {
     if (n == 0) {
+        if (h_out) *h_out = 0.0;
         W1G_CUDA(cudaMemsetAsync(d_out, 0, sizeof(double), c.stream));
         return W1G_OK;
     }
@@ -175,7 +180,7 @@ int pairwise_sum(Ctx &c, const double *d_v, int64_t n, double *d_out, DevBuf &no
     }
     const unsigned warps = (unsigned)(n / 64 + 2);
     k_pw_sum<<<grid_for(warps * 32, 256, 4u * c.sm_count), 256, 0, c.stream>>>(d_v, nodes, lev, lev + PW_MAX_LEVELS,
-                                                                               val, d_out);
+                                                                               val, d_out, h_out);
     W1G_CHECK_LAUNCH();
     return W1G_OK;
 }

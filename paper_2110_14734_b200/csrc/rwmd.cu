@@ -26,7 +26,7 @@ int rwmd_f32_min(Ctx &c, const double2 *q, const uint64_t *qkey, int64_t nq, con
                  const uint64_t *tkey, int64_t nt, double scale,
                  unsigned *mout, float *qn_out, double4 *tbox, int culling, int tbox_ready = 0);
 int pairwise_sum(Ctx &c, const double *d_v, int64_t n, double *d_out, DevBuf &nodes_buf,
-                 DevBuf &val_buf, DevBuf &lev_buf, int64_t *cached_n = nullptr);
+                 DevBuf &val_buf, DevBuf &lev_buf, int64_t *cached_n = nullptr, double *h_out = nullptr);
 
 static const double SQRT2 = 1.4142135623730951;  // math.sqrt(2.0), diagram.py:17
 
@@ -825,6 +825,7 @@ int rwmd_run(Ctx &c, double *L, double *LA, double *LB) {
         double4 *tbox_s = tbox + s * mtb, *box64_s = box64 + s * mtb, *sbox_s = sbox + s * msb;
         if (n_src == 0) {
             W1G_CUDA(cudaMemsetAsync(dres + s, 0, sizeof(double), c.stream));
+            reinterpret_cast<double *>(c.h_pinned + H_SCALAR)[s] = 0.0;
             return W1G_OK;
         }
         if (n_dst > 0) {
@@ -836,8 +837,9 @@ int rwmd_run(Ctx &c, double *L, double *LA, double *LB) {
         W1G_TRY(launch_refine(c, F.mpts[s], F.mpos[s], F.members[s], mass[s], n_src, mf_s, qn_s, F.unscale,
                               F.mpts[o], n_dst, box64_s, sbox_s, best, terms_s));
         T.mark("refine");
+        // the sum also lands in the page-locked scalar slot the host reads (no extra small read)
         W1G_TRY(pairwise_sum(c, terms_s, n_src, dres + s, c.pw_nodes[s], s ? c.scr[17] : c.scr[18], c.pw_lev[s],
-                             &c.pw_n[s]));
+                             &c.pw_n[s], reinterpret_cast<double *>(c.h_pinned + H_SCALAR) + s));
         T.mark("sum");
         return W1G_OK;
     };
@@ -878,7 +880,6 @@ int rwmd_run(Ctx &c, double *L, double *LA, double *LB) {
         W1G_TRY(run_side(0));
         W1G_TRY(run_side(1));
     }
-    W1G_TRY(to_host_small(c, c.h_pinned + H_SCALAR, dres, sizeof(double) * 2));
     W1G_TRY(stream_sync(c));
     double h[2];
     memcpy(h, c.h_pinned + H_SCALAR, sizeof h);
