@@ -355,7 +355,7 @@ enum FlagSlot {
     F_FRONT_OVF = 8,
     F_NET_ERR = 9,
     F_TOTAL = 10,
-    F_RESERVED11 = 11,
+    F_ZC_TICKET = 11,  // k_zc_stats: blocks done (the last one publishes to the host mirror)
     F_MISC0 = 12,
     F_MISC1 = 13,
     F_MISC2 = 14,

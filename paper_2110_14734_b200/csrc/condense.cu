@@ -56,7 +56,10 @@ __global__ void k_zc_emit(ZcFlag f, int64_t n, const int64_t *excl, double2 *pts
 
 // identical multisets (pipeline.py:106-109), plus what RWMD's frame needs
 // (lower_bound.py:61-75): the member count of each side and the bbox
-__global__ void k_zc_stats(const int64_t *am, const int64_t *bm, const double2 *pts, const int64_t *kp, int64_t *f) {
+// (h: the page-locked mirror of the flag block; the last block to finish copies K0, the
+// imbalance flag and the six statistics there -- the stage's round trip needs no small read)
+__global__ void k_zc_stats(const int64_t *am, const int64_t *bm, const double2 *pts, const int64_t *kp, int64_t *f,
+                           int64_t *h) {
     const int64_t k = *kp;
     int any = 0;
     unsigned long long na = 0, nb = 0, nx = 0, xx = 0, ny = 0, xy = 0;  // nx/ny: max of ~key = ~min key
@@ -89,6 +92,17 @@ __global__ void k_zc_stats(const int64_t *am, const int64_t *bm, const double2 *
         atomicMax(&u[3], xx);
         atomicMax(&u[4], ny);
         atomicMax(&u[5], xy);
+    }
+    __shared__ bool s_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0)
+        s_last = atomicAdd(reinterpret_cast<unsigned long long *>(&f[F_ZC_TICKET]), 1ull) == gridDim.x - 1;
+    __syncthreads();
+    if (s_last && threadIdx.x < 8) {
+        __threadfence();
+        const int slot = threadIdx.x < 2 ? F_K0 + threadIdx.x : F_ZSTAT + threadIdx.x - 2;
+        reinterpret_cast<volatile int64_t *>(h)[slot] = reinterpret_cast<volatile int64_t *>(f)[slot];
     }
 }
 
@@ -436,10 +450,9 @@ int zc_run(Ctx &c, const double2 *d_a, int64_t na, const double2 *d_b, int64_t n
     W1G_CUDA(cudaMemsetAsync(bm, 0, sizeof(int64_t) * n, c.stream));
     k_zc_emit<<<gs(c, n), 256, 0, c.stream>>>(f, n, excl, pts, am, bm);
     W1G_CHECK_LAUNCH();
-    k_zc_stats<<<grid_for(n, 256, 2u * c.sm_count), 256, 0, c.stream>>>(am, bm, pts, dflags(c) + F_K0, dflags(c));
+    k_zc_stats<<<grid_for(n, 256, 2u * c.sm_count), 256, 0, c.stream>>>(am, bm, pts, dflags(c) + F_K0, dflags(c),
+                                                                        c.h_pinned);
     W1G_CHECK_LAUNCH();
-    W1G_TRY(to_host_small2(c, c.h_pinned + F_ZSTAT, dflags(c) + F_ZSTAT, sizeof(int64_t) * 6, c.h_pinned + F_K0,
-                           dflags(c) + F_K0, sizeof(int64_t) * 2));
     W1G_TRY(stream_sync(c));
     if (speculative && lex2_speculation_failed(c, 1)) return zc_run(c, d_a, na, d_b, nb, k0, balanced, false);
     ns.k = c.h_pinned[F_K0];

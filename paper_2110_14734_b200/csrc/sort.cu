@@ -587,8 +587,11 @@ __global__ void k_tie_runs(const uint64_t *pk, int64_t n, unsigned long long *ma
     }
 }
 
+// (mr / hmr, optional: the speculative path's longest tie run, counted by k_tie_runs before
+// this launch, copied to its page-locked host slot -- no small-read launch of its own)
 __global__ void k_tie_small(const uint64_t *pk, int64_t n, const uint64_t *primary, const uint64_t *secondary,
-                            uint32_t *vals) {
+                            uint32_t *vals, const unsigned long long *mr, volatile unsigned long long *hmr) {
+    if (hmr && blockIdx.x == 0 && threadIdx.x == 0) *hmr = *mr;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         const uint64_t v = pk[i];
@@ -656,9 +659,9 @@ int sort_lex2_multi(Ctx &c, const Lex2Job *jobs, int njobs, bool speculative) {
         for (int j = 0; j < njobs; j++) {
             if (jobs[j].n <= 1) continue;
             k_tie_small<<<grid_for(jobs[j].n, 256, 8u * c.sm_count), 256, 0, c.stream>>>(
-                pk[j], jobs[j].n, jobs[j].primary, jobs[j].secondary, jobs[j].vals);
+                pk[j], jobs[j].n, jobs[j].primary, jobs[j].secondary, jobs[j].vals, mm + 4 * j + 2,
+                reinterpret_cast<volatile unsigned long long *>(c.h_pinned + H_LEX_MAXRUN + j));
             W1G_CHECK_LAUNCH();
-            W1G_TRY(to_host_small(c, c.h_pinned + H_LEX_MAXRUN + j, mm + 4 * j + 2, sizeof(unsigned long long)));
         }
         return W1G_OK;
     }
@@ -675,7 +678,7 @@ int sort_lex2_multi(Ctx &c, const Lex2Job *jobs, int njobs, bool speculative) {
         if (hm[4 * j + 3] == 0) continue;
         if (hm[4 * j + 2] <= (unsigned long long)TIE_SMALL) {
             k_tie_small<<<grid_for(jobs[j].n, 256, 8u * c.sm_count), 256, 0, c.stream>>>(
-                pk[j], jobs[j].n, jobs[j].primary, jobs[j].secondary, jobs[j].vals);
+                pk[j], jobs[j].n, jobs[j].primary, jobs[j].secondary, jobs[j].vals, nullptr, nullptr);
             W1G_CHECK_LAUNCH();
         } else {
             is_long[j] = any_long = true;
