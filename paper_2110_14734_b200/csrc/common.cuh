@@ -361,6 +361,7 @@ enum FlagSlot {
     F_MISC2 = 14,
     F_MISC3 = 15,
     F_CELL_MIN = 16,  // 4 slots: min cx, max cx, min cy, max cy
+    F_TREE_TICKET = 20,  // k_tree_local: CTAs done (the last one publishes depth / duplicates; reset by it)
     F_BBOX = 24,      // 4 doubles (as bits)
     F_SCAL = 32,      // 8 doubles of scalar results
     F_LISTS = 40,     // delta_condense's presorted tree lists failed a check (tree sorts itself)

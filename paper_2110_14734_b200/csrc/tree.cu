@@ -430,7 +430,7 @@ __global__ void __launch_bounds__(LT) k_tree_local(const double2 *__restrict__ p
                                                     const uint32_t *xl1, const uint32_t *yl0,
                                                     const uint32_t *yl1, const Seg *__restrict__ local,
                                                     const int32_t *local_cnt, int32_t *inv, TreeOut o,
-                                                    int64_t *flags) {
+                                                    int64_t *flags, const int32_t *depth_src, int64_t *h) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     LocalSmem &S = *reinterpret_cast<LocalSmem *>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -547,6 +547,20 @@ __global__ void __launch_bounds__(LT) k_tree_local(const double2 *__restrict__ p
             lv++;
         }
         __syncthreads();
+    }
+    // the last CTA to finish copies the depth of the cooperative levels and the duplicate
+    // flag to the page-locked host mirror (the stage needs no small-read launch)
+    __shared__ bool s_last;
+    __threadfence();
+    __syncthreads();
+    unsigned long long *ticket = reinterpret_cast<unsigned long long *>(flags + F_TREE_TICKET);
+    if (tid == 0) s_last = atomicAdd(ticket, 1ull) == gridDim.x - 1;
+    __syncthreads();
+    if (s_last && tid == 0) {
+        __threadfence();
+        if (depth_src) *reinterpret_cast<volatile int32_t *>(h + H_TREE_DEPTH) = *(const volatile int32_t *)depth_src;
+        reinterpret_cast<volatile int64_t *>(h)[H_TREE_DUP] = reinterpret_cast<volatile int64_t *>(flags)[F_DUP];
+        *ticket = 0;
     }
 }
 
@@ -1007,19 +1021,13 @@ int tree_run(Ctx &c, const double2 *pts, int64_t n, int64_t *n_nodes, int32_t *d
         const size_t smem = sizeof(LocalSmem);
         W1G_CUDA(cudaFuncSetAttribute(k_tree_local, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         const unsigned gl = (unsigned)(2 * c.sm_count);
+        if (levels >= 0) c.h_pinned[H_TREE_DEPTH] = levels;  // host-known (multi-kernel path / no global levels)
         k_tree_local<<<gl, LT, smem, c.stream>>>(pts, xl[0], xl[1], yl[0], yl[1], local, local_cnt, fl, o,
-                                                  dflags(c));
+                                                  dflags(c), depth_src, c.h_pinned);
         W1G_CHECK_LAUNCH();
     }
     T.mark("local");
-    if (levels >= 0) c.h_pinned[H_TREE_DEPTH] = levels;  // host-known (multi-kernel path / no global levels)
-    if (depth_src) {
-        W1G_TRY(to_host_small2(c, c.h_pinned + H_TREE_DEPTH, depth_src, sizeof(int32_t), c.h_pinned + H_TREE_DUP,
-                               dflags(c) + F_DUP, sizeof(int64_t)));
-    } else {
-        W1G_TRY(to_host_small(c, c.h_pinned + H_TREE_DUP, dflags(c) + F_DUP, sizeof(int64_t)));
-    }
-    W1G_CUDA(cudaEventRecord(c.ev[10], c.stream));  // the two copies above have landed once this has
+    W1G_CUDA(cudaEventRecord(c.ev[10], c.stream));  // depth and duplicate flag have landed once this has
     c.tree_valid = true;
     if (defer) {
         *depth = 0;
